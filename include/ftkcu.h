@@ -1,0 +1,154 @@
+/*
+ * ftkcu.h — the C-ABI of the B200-native FastTuckerPlus engine.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (/root/reference/proj) has no FFI: its boundary is the C++ header API
+ * the proj/include/ftk headers, linked statically as ftkcore.  The engine keeps
+ * that C++ API (the include/ftk headers, implemented in
+ * paper_2404_10087_b200/host/ on top of this header) and moves the device
+ * boundary *inside* ftk::epoch_plus / ftk::train / ftk::loss /
+ * ftk::evaluate.  Every entry point below names the reference interface it
+ * replaces.
+ *
+ * Conventions (mirroring the reference's):
+ *   - Every call returns FTKCU_OK (0) or a non-zero status; the message is
+ *     ftkcu_last_error(session).  The C++ shim turns non-zero into
+ *     ftk::Error(message), which is how the reference reports every failure
+ *     (common.hpp:23-32).
+ *   - Host buffers are caller-owned and only read/written during the call.
+ *     Device buffers are owned by the session.
+ *   - A session is bound to one CUDA device and must be driven by one host
+ *     thread at a time (the reference's Model& is likewise not to be touched
+ *     concurrently, decomposition.hpp Hogwild contract).
+ *   - Plain pointers and sizes only; no torch or CUDA types cross the ABI.
+ */
+#ifndef FTKCU_H_
+#define FTKCU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTKCU_ABI_VERSION 1
+
+/* status codes */
+#define FTKCU_OK 0
+#define FTKCU_ERR_ARG 1      /* invalid argument (ftk::require failure)     */
+#define FTKCU_ERR_CUDA 2     /* CUDA runtime / driver error                 */
+#define FTKCU_ERR_STATE 3    /* call out of order (no tensor / no model)    */
+#define FTKCU_ERR_NCCL 4     /* collective failure                          */
+#define FTKCU_ERR_EMPTY 5    /* apply_core_update: empty tensor             */
+
+/* execution modes for the two SGD sweeps */
+#define FTKCU_MODE_DETERMINISTIC 0 /* single stream, reference fp32 order,
+                                      bit-identical to workers == 1        */
+#define FTKCU_MODE_HOGWILD 1       /* all SMs, lock-free row updates        */
+
+/* contraction precision for FTKCU_MODE_HOGWILD (ftkcu_set_option) */
+#define FTKCU_PREC_FP32 0   /* FFMA, no tensor cores                        */
+#define FTKCU_PREC_TF32 1   /* tcgen05 kind::tf32, fp32 accumulate          */
+#define FTKCU_PREC_3XTF32 2 /* tcgen05 split-tf32 (hi*hi + hi*lo + lo*hi)   */
+
+/* evaluation reduction order */
+#define FTKCU_EVAL_EXACT 0 /* reference slab order, bit-identical fp64     */
+#define FTKCU_EVAL_FAST 1  /* tree reduction, fp64                          */
+
+typedef struct ftkcu_session ftkcu_session;
+
+/* ---- session --------------------------------------------------------- */
+
+/* Creates a session on CUDA device `device`.  No reference counterpart
+ * (the reference's "session" is the calling thread). */
+int ftkcu_session_create(int device, ftkcu_session** out);
+void ftkcu_session_destroy(ftkcu_session* s);
+/* Last error message of `s`, or of the calling thread's last failed
+ * ftkcu_session_create when s == NULL.  Never NULL. */
+const char* ftkcu_last_error(const ftkcu_session* s);
+int ftkcu_abi_version(void);
+
+/* Tunables: "precision" (FTKCU_PREC_*), "eval" (FTKCU_EVAL_*),
+ * "hog_blocks_per_sm", "verbose".  Unknown keys are FTKCU_ERR_ARG. */
+int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value);
+int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value);
+
+/* ---- data ------------------------------------------------------------ */
+
+/* Uploads a COO tensor into slot `slot` (0 = train, 1 = test, ...).
+ * idx_rowmajor is nnz x order int32, 0-based; values fp32.  Replaces the
+ * device-side role of ftk::SparseTensor (sparse_tensor.hpp:14-33); the host
+ * loader ftk::load_coo (sparse_tensor.hpp:38) stays on the host.  The engine
+ * keeps the entries in storage order (SoA, one int32 column per mode) for
+ * the deterministic sweeps and builds a shuffled, tiled copy lazily for the
+ * Hogwild sweeps. */
+int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order,
+                        const int32_t* dims, int64_t nnz,
+                        const int32_t* idx_rowmajor, const float* values);
+int ftkcu_tensor_release(ftkcu_session* s, int slot);
+int64_t ftkcu_tensor_nnz(ftkcu_session* s, int slot);
+
+/* Uploads / downloads the model: A[n] is dims[n] x ranks[n], B[n] is
+ * ranks[n] x R, fp32 row-major (ftk::Model, model.hpp:31-48). */
+int ftkcu_model_upload(ftkcu_session* s, int order, const int32_t* dims,
+                       const int32_t* ranks, int32_t R,
+                       const float* const* A, const float* const* B);
+int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B);
+
+/* ---- the hot path ------------------------------------------------------ */
+
+/* Factor phase of ftk::epoch_plus (decomposition.cpp:637-661, Eq. 14,
+ * Alg. 4).  perm: the EpochPlan::global permutation (nnz int64 entry
+ * positions, batches of M in order) or NULL in Hogwild mode to use the
+ * engine's device tile order keyed by `seed`.  In deterministic mode perm is
+ * required and the result is bit-identical to the reference with
+ * workers == 1.  ms (optional) receives the device time of the sweep. */
+int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm,
+                       int32_t M, float lr_a, float reg_a, int mode,
+                       uint64_t seed, double* ms);
+
+/* Core phase of ftk::epoch_plus (decomposition.cpp:663-703, Eq. 15,
+ * Alg. 5): accumulate Grad(B) = sum (x - xhat) A_psi^T D over the tensor,
+ * then B += lr_b (Grad/|Omega| - reg_b B) (apply_core_update,
+ * decomposition.cpp:576-589).  Same perm / mode / seed rules as above.
+ * grad_out (optional, sum_n J_n*R floats) receives the merged gradient. */
+int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm,
+                     int32_t M, float lr_b, float reg_b, int mode,
+                     uint64_t seed, float* grad_out, double* ms);
+
+/* fp64 metrics of the resident model on tensor `slot`
+ * (ftk::loss / ftk::evaluate, evaluation.cpp:36-72, predict_element
+ * model.cpp:70-92).  out[0] = sum (x - xhat)^2, out[1] = sum |x - xhat|,
+ * out[2] = reg_a sum_n |A_n|^2 + reg_b sum_n |B_n|^2, each reduced in the
+ * reference's slab order for `workers` when the "eval" option is EXACT. */
+int ftkcu_eval(ftkcu_session* s, int slot, int workers, double reg_a,
+               double reg_b, double* out3);
+
+/* One batch through the device pipeline (parity probe for the reference's
+ * per-batch API decomposition.hpp:86-124).  rows: m_eff entry positions,
+ * batch capacity cap.  Outputs (all optional): C, D [order][cap][R];
+ * U, A_new [order][cap][Jmax]; xhat/resid factor side and C side [cap];
+ * G [order][Jmax][R].  Mutates the resident A exactly like
+ * update_factors_plus. */
+int ftkcu_batch_probe(ftkcu_session* s, int slot, const int64_t* rows,
+                      int m_eff, int cap, float lr_a, float reg_a, float* C,
+                      float* D, float* U, float* xhat_f, float* resid_f,
+                      float* xhat_c, float* resid_c, float* A_new, float* G);
+
+/* ---- multi-GPU (DSGD) --------------------------------------------------- */
+
+/* 128-byte NCCL unique id for rank 0 to broadcast out of band. */
+int ftkcu_comm_unique_id(uint8_t* id128);
+/* Joins an NCCL communicator (one rank per session / GPU). */
+int ftkcu_comm_init(ftkcu_session* s, const uint8_t* id128, int rank,
+                    int world);
+/* In-place sum all-reduce of a device-resident core gradient, exposed for
+ * tests; the DSGD epoch calls it internally once per core phase. */
+int ftkcu_comm_allreduce_grad(ftkcu_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FTKCU_H_ */

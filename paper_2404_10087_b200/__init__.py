@@ -1,0 +1,242 @@
+"""B200-native FastTuckerPlus engine (arXiv 2404.10087) -- Python binding.
+
+The product is native code: ``libftkcu.so`` (sm_100a kernels + the C-ABI in
+``include/ftkcu.h``) and ``libftk.so`` (the drop-in ``ftk::`` C++ API in
+``include/ftk/*.hpp``).  This module is a thin ctypes layer over the C-ABI so
+tests and ``bench.py`` can drive the engine from Python with numpy buffers.
+There is no Python or CPU fallback: if the shared library is missing or no
+sm_100 device is present, calls raise ``FtkError``.
+
+Reference counterparts (``/root/reference/proj``): ``ftk::epoch_plus``
+(decomposition.cpp:623-705) = :meth:`Session.factor_phase` +
+:meth:`Session.core_phase`; ``ftk::loss`` / ``ftk::evaluate``
+(evaluation.cpp:36-72) = :meth:`Session.eval`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import host  # noqa: F401  (seed derivation, sampler, counters)
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libftkcu.so")
+CXX_LIB_PATH = os.path.join(PKG, "libftk.so")
+
+MODE_DETERMINISTIC = 0
+MODE_HOGWILD = 1
+PREC_FP32, PREC_TF32, PREC_3XTF32 = 0, 1, 2
+EVAL_EXACT, EVAL_FAST = 0, 1
+
+# Every entry point declared in include/ftkcu.h (checked by tests/test_abi.py).
+EXPORTS = (
+    "ftkcu_abi_version", "ftkcu_session_create", "ftkcu_session_destroy",
+    "ftkcu_last_error", "ftkcu_set_option", "ftkcu_get_option", "ftkcu_tensor_upload",
+    "ftkcu_tensor_release", "ftkcu_tensor_nnz", "ftkcu_model_upload",
+    "ftkcu_model_download", "ftkcu_factor_phase", "ftkcu_core_phase", "ftkcu_eval",
+    "ftkcu_batch_probe", "ftkcu_comm_unique_id", "ftkcu_comm_init",
+    "ftkcu_comm_allreduce_grad",
+)
+
+
+class FtkError(RuntimeError):
+    """Mirror of ftk::Error (common.hpp:23-32): every failure raises."""
+
+
+_f32p = C.POINTER(C.c_float)
+_f64p = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_fpp = C.POINTER(_f32p)
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libftkcu.so once; raises FtkError if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FtkError(f"{path} not built -- run __graft_entry__.build() or make -C {PKG}")
+    L = C.CDLL(path)
+    L.ftkcu_abi_version.restype = C.c_int
+    L.ftkcu_last_error.restype = C.c_char_p
+    L.ftkcu_last_error.argtypes = [C.c_void_p]
+    L.ftkcu_session_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    L.ftkcu_session_destroy.argtypes = [C.c_void_p]
+    L.ftkcu_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    L.ftkcu_get_option.argtypes = [C.c_void_p, C.c_char_p, _i64p]
+    L.ftkcu_tensor_upload.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, C.c_int64, _i32p,
+                                      _f32p]
+    L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
+    L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
+    L.ftkcu_tensor_nnz.restype = C.c_int64
+    L.ftkcu_model_upload.argtypes = [C.c_void_p, C.c_int, _i32p, _i32p, C.c_int32, _fpp, _fpp]
+    L.ftkcu_model_download.argtypes = [C.c_void_p, _fpp, _fpp]
+    L.ftkcu_factor_phase.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int32, C.c_float,
+                                     C.c_float, C.c_int, C.c_uint64, _f64p]
+    L.ftkcu_core_phase.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int32, C.c_float,
+                                   C.c_float, C.c_int, C.c_uint64, _f32p, _f64p]
+    L.ftkcu_eval.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, _f64p]
+    L.ftkcu_batch_probe.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int, C.c_int, C.c_float,
+                                    C.c_float] + [_f32p] * 9
+    L.ftkcu_comm_unique_id.argtypes = [C.c_char_p]
+    L.ftkcu_comm_init.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
+    L.ftkcu_comm_allreduce_grad.argtypes = [C.c_void_p]
+    _lib = L
+    return L
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _ptrs(arrs):
+    out = (_f32p * len(arrs))()
+    for i, a in enumerate(arrs):
+        if a.dtype != np.float32 or not a.flags.c_contiguous:
+            raise FtkError("model matrices must be C-contiguous float32")
+        out[i] = a.ctypes.data_as(_f32p)
+    return out
+
+
+class Session:
+    """One engine session on one CUDA device (``ftkcu_session``)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.ftkcu_session_create(device, C.byref(h))
+        if rc != 0:
+            raise FtkError(self.lib.ftkcu_last_error(None).decode())
+        self.h = h
+        self.order = 0
+        self.ranks = None
+        self.r = 0
+        self.dims = None
+
+    # -- plumbing
+    def _ck(self, rc):
+        if rc != 0:
+            raise FtkError(self.lib.ftkcu_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ftkcu_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_option(self, key: str, value: int):
+        self._ck(self.lib.ftkcu_set_option(self.h, key.encode(), int(value)))
+
+    def get_option(self, key: str) -> int:
+        v = C.c_int64()
+        self._ck(self.lib.ftkcu_get_option(self.h, key.encode(), C.byref(v)))
+        return v.value
+
+    @property
+    def stream_handle(self) -> int:
+        """cudaStream_t of the session (for torch.cuda.ExternalStream timing)."""
+        return self.get_option("stream")
+
+    # -- data
+    def upload_tensor(self, slot, dims, idx, vals):
+        dims = np.ascontiguousarray(dims, np.int32)
+        idx = np.ascontiguousarray(idx, np.int32)
+        vals = np.ascontiguousarray(vals, np.float32)
+        nnz = vals.shape[0]
+        if idx.shape != (nnz, dims.shape[0]):
+            raise FtkError("index array must be nnz x order")
+        self._ck(self.lib.ftkcu_tensor_upload(self.h, slot, dims.shape[0], _p(dims, _i32p), nnz,
+                                              _p(idx, _i32p), _p(vals, _f32p)))
+
+    def upload_tensor_ptr(self, slot, dims, nnz, idx_ptr: int, vals_ptr: int):
+        """Upload from raw (e.g. pinned) host pointers."""
+        dims = np.ascontiguousarray(dims, np.int32)
+        self._ck(self.lib.ftkcu_tensor_upload(self.h, slot, dims.shape[0], _p(dims, _i32p), nnz,
+                                              C.cast(idx_ptr, _i32p), C.cast(vals_ptr, _f32p)))
+
+    def release_tensor(self, slot):
+        self._ck(self.lib.ftkcu_tensor_release(self.h, slot))
+
+    def upload_model(self, dims, ranks, r, a, b):
+        dims = np.ascontiguousarray(dims, np.int32)
+        ranks = np.ascontiguousarray(ranks, np.int32)
+        self._ck(self.lib.ftkcu_model_upload(self.h, dims.shape[0], _p(dims, _i32p),
+                                             _p(ranks, _i32p), int(r), _ptrs(a), _ptrs(b)))
+        self.order, self.dims, self.ranks, self.r = dims.shape[0], dims.copy(), ranks.copy(), int(r)
+
+    def download_model(self, a=None, b=None):
+        if a is None:
+            a = [np.empty((int(d), int(j)), np.float32) for d, j in zip(self.dims, self.ranks)]
+        if b is None:
+            b = [np.empty((int(j), self.r), np.float32) for j in self.ranks]
+        self._ck(self.lib.ftkcu_model_download(self.h, _ptrs(a), _ptrs(b)))
+        return a, b
+
+    # -- hot path
+    def factor_phase(self, slot=0, perm=None, M=16, lr_a=1e-3, reg_a=1e-4,
+                     mode=MODE_DETERMINISTIC, seed=0, timed=True):
+        pa = None if perm is None else np.ascontiguousarray(perm, np.int64)
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_factor_phase(self.h, slot, _p(pa, _i64p), M, lr_a, reg_a, mode,
+                                             C.c_uint64(seed & (2**64 - 1)),
+                                             C.byref(ms) if timed else None))
+        return ms.value
+
+    def core_phase(self, slot=0, perm=None, M=16, lr_b=1e-3, reg_b=1e-4,
+                   mode=MODE_DETERMINISTIC, seed=0, want_grad=False, timed=True):
+        pa = None if perm is None else np.ascontiguousarray(perm, np.int64)
+        g = np.zeros(int(np.sum(self.ranks)) * self.r, np.float32) if want_grad else None
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_core_phase(self.h, slot, _p(pa, _i64p), M, lr_b, reg_b, mode,
+                                           C.c_uint64(seed & (2**64 - 1)), _p(g, _f32p),
+                                           C.byref(ms) if timed else None))
+        return (ms.value, g) if want_grad else ms.value
+
+    def eval(self, slot=1, workers=1, reg_a=0.0, reg_b=0.0):
+        out = np.zeros(3, np.float64)
+        self._ck(self.lib.ftkcu_eval(self.h, slot, workers, reg_a, reg_b, _p(out, _f64p)))
+        return out
+
+    def batch_probe(self, slot, rows, cap, lr_a, reg_a):
+        rows = np.ascontiguousarray(rows, np.int64)
+        order, r, jmax = self.order, self.r, int(np.max(self.ranks))
+        out = dict(
+            c=np.zeros((order, cap, r), np.float32), d=np.zeros((order, cap, r), np.float32),
+            u=np.zeros((order, cap, jmax), np.float32), xhat_f=np.zeros(cap, np.float32),
+            resid_f=np.zeros(cap, np.float32), xhat_c=np.zeros(cap, np.float32),
+            resid_c=np.zeros(cap, np.float32), a_new=np.zeros((order, cap, jmax), np.float32),
+            g=np.zeros((order, jmax, r), np.float32))
+        self._ck(self.lib.ftkcu_batch_probe(
+            self.h, slot, _p(rows, _i64p), rows.size, cap, lr_a, reg_a,
+            *[_p(out[k], _f32p) for k in ("c", "d", "u", "xhat_f", "resid_f", "xhat_c",
+                                           "resid_c", "a_new", "g")]))
+        return out
+
+    # -- multi-GPU
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        L = load_library()
+        buf = C.create_string_buffer(128)
+        rc = L.ftkcu_comm_unique_id(buf)
+        if rc != 0:
+            raise FtkError(L.ftkcu_last_error(None).decode())
+        return buf.raw
+
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        self._ck(self.lib.ftkcu_comm_init(self.h, uid, rank, world))

@@ -1,0 +1,127 @@
+// Internal declarations shared by the engine's translation units.
+//
+// Device data layout:
+//   * COO tensor, storage order: SoA, one int32 column per mode + fp32 values
+//     (the reference's AoS `indices[nnz*N]`, sparse_tensor.hpp:14-33, is
+//     transposed once at upload so a warp reads 128 B per mode per 32 nnz).
+//   * COO tensor, Hogwild order: the same SoA shuffled once per session
+//     (cub radix sort on hashed keys) and visited tile by tile in a per-epoch
+//     affine tile permutation.
+//   * Model: A_n (I_n x J_n) and B_n (J_n x R) fp32 row-major, one cudaMalloc
+//     each (256-B aligned rows when J_n % 64 == 0).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/ftkcu.h"
+
+namespace ftkcu {
+
+constexpr int kMaxOrder = 8;
+constexpr int kTile = 16;  // reference tile edge (tiles.hpp:12-14)
+
+inline int pad16(int x) { return (x + kTile - 1) / kTile * kTile; }
+
+struct DevTensor {
+  int order = 0;
+  int32_t dims[kMaxOrder] = {};
+  int64_t nnz = 0;
+  int32_t* idx[kMaxOrder] = {};  // storage order SoA
+  float* vals = nullptr;
+  // Hogwild (shuffled) copy, built lazily by the tiler.
+  bool shuffled = false;
+  int32_t* sidx[kMaxOrder] = {};
+  float* svals = nullptr;
+};
+
+struct DevModel {
+  int order = 0;
+  int32_t dims[kMaxOrder] = {};
+  int32_t ranks[kMaxOrder] = {};
+  int32_t r = 0;
+  float* a[kMaxOrder] = {};
+  float* b[kMaxOrder] = {};
+  int sum_j() const {
+    int s = 0;
+    for (int n = 0; n < order; ++n) s += ranks[n];
+    return s;
+  }
+  int max_j() const {
+    int s = 0;
+    for (int n = 0; n < order; ++n) s = ranks[n] > s ? ranks[n] : s;
+    return s;
+  }
+};
+
+// Kernel-side view of model + tensor, passed by value.
+struct KView {
+  int order;
+  int r;
+  int32_t j[kMaxOrder];
+  float* a[kMaxOrder];
+  const float* b[kMaxOrder];
+  const int32_t* idx[kMaxOrder];
+  const float* vals;
+  int64_t nnz;
+};
+
+// Optional per-batch debug outputs of the deterministic kernels (device
+// pointers, any may be null).  Layouts match ftkcu_batch_probe.
+struct DetDebug {
+  float* c = nullptr;       // [order][cap][R]
+  float* d = nullptr;       // [order][cap][R]
+  float* u = nullptr;       // [order][cap][Jmax]
+  float* xhat = nullptr;    // [cap]
+  float* resid = nullptr;   // [cap]
+  int jmax = 0;
+};
+
+// ---- deterministic sweeps (det_kernels.cu) ---------------------------------
+cudaError_t launch_det_factor(const KView& v, const int64_t* perm, int cap,
+                              float lr_a, float reg_a, const DetDebug& dbg,
+                              cudaStream_t st);
+// Accumulates the ordered core gradient into grad (sum_n J_n*R floats,
+// zeroed by the caller).
+cudaError_t launch_det_core(const KView& v, const int64_t* perm, int cap,
+                            float* grad, const DetDebug& dbg, cudaStream_t st);
+// total = 0 + grad; B += lr_b (total * (1/nnz) - reg_b B)
+cudaError_t launch_apply_core(const KView& v, float* grad, float lr_b,
+                              float reg_b, cudaStream_t st);
+
+// ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
+cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
+                              float lr_a, float reg_a, int blocks_per_sm,
+                              cudaStream_t st);
+cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
+                            float* grad, int blocks_per_sm, float* scratch,
+                            size_t scratch_bytes, cudaStream_t st);
+// Builds the shuffled SoA copy (the tiler).  perm == nullptr: random order
+// from `seed`; otherwise entries are laid out in perm order.
+cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
+                           void* scratch, size_t scratch_bytes,
+                           cudaStream_t st);
+size_t shuffle_scratch_bytes(int64_t nnz);
+constexpr int kHogTile = 128;  // nonzeros per Hogwild tile
+
+// ---- tensor-core sweeps (tc_kernels.cu) -------------------------------------
+bool tc_supported(const KView& v);
+cudaError_t launch_tc_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
+                             float lr_a, float reg_a, int precision,
+                             cudaStream_t st);
+cudaError_t launch_tc_core(const KView& v, int64_t tile_mul, int64_t tile_add,
+                           float* grad, int precision, float* scratch,
+                           size_t scratch_bytes, cudaStream_t st);
+
+// ---- evaluation (eval_kernels.cu) ---------------------------------------------
+// out3 = {sum sq, sum abs, reg}; exact = reference slab order.
+cudaError_t run_eval(const DevModel& m, const DevTensor& t, int workers,
+                     double reg_a, double reg_b, bool exact, double* out3,
+                     void* scratch, size_t scratch_bytes, cudaStream_t st);
+size_t eval_scratch_bytes(const DevModel& m, const DevTensor& t, int workers);
+
+int num_sms();
+
+}  // namespace ftkcu

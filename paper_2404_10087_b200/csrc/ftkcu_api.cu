@@ -1,0 +1,668 @@
+// The C-ABI (include/ftkcu.h): session, data movement and dispatch of the
+// device sweeps.  Host-side C++ only; kernels live in *_kernels.cu.
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+
+using namespace ftkcu;
+
+struct ftkcu_session {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  DevTensor slots[8];
+  DevModel model;
+  bool have_model = false;
+  float* grad = nullptr;
+  size_t grad_len = 0;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int64_t* d_perm = nullptr;
+  size_t perm_cap = 0;
+  int64_t opt_precision = FTKCU_PREC_FP32;
+  int64_t opt_eval = FTKCU_EVAL_EXACT;
+  int64_t opt_hog_bps = 2;
+  int64_t opt_verbose = 0;
+  int64_t opt_shuffle_seed = 0x5eed5eedLL;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  int64_t launches = 0;  // kernels launched by this session (for benches)
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int fail(ftkcu_session* s, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (s)
+    s->err = buf;
+  else
+    g_create_err = buf;
+  return code;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(s, FTKCU_ERR_CUDA, "%s: %s (%s:%d)", #call,                 \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                \
+  } while (0)
+
+#define NK(call)                                                              \
+  do {                                                                        \
+    ncclResult_t r_ = (call);                                                 \
+    if (r_ != ncclSuccess)                                                    \
+      return fail(s, FTKCU_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+int bind(ftkcu_session* s) {
+  if (!s) return fail(nullptr, FTKCU_ERR_ARG, "null session");
+  CK(cudaSetDevice(s->device));
+  return FTKCU_OK;
+}
+
+int ensure_scratch(ftkcu_session* s, size_t bytes) {
+  if (bytes <= s->scratch_bytes) return FTKCU_OK;
+  if (s->scratch) CK(cudaFree(s->scratch));
+  s->scratch = nullptr;
+  s->scratch_bytes = 0;
+  CK(cudaMalloc(&s->scratch, bytes));
+  s->scratch_bytes = bytes;
+  return FTKCU_OK;
+}
+
+int upload_perm(ftkcu_session* s, const int64_t* perm, int64_t n) {
+  if ((size_t)n > s->perm_cap) {
+    if (s->d_perm) CK(cudaFree(s->d_perm));
+    s->d_perm = nullptr;
+    CK(cudaMalloc(&s->d_perm, sizeof(int64_t) * (n > 0 ? n : 1)));
+    s->perm_cap = n;
+  }
+  if (n > 0)
+    CK(cudaMemcpyAsync(s->d_perm, perm, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                       s->stream));
+  return FTKCU_OK;
+}
+
+void free_tensor(DevTensor& t) {
+  for (int n = 0; n < kMaxOrder; ++n) {
+    if (t.idx[n]) cudaFree(t.idx[n]);
+    if (t.sidx[n]) cudaFree(t.sidx[n]);
+  }
+  if (t.vals) cudaFree(t.vals);
+  if (t.svals) cudaFree(t.svals);
+  t = DevTensor{};
+}
+
+void free_model(DevModel& m) {
+  for (int n = 0; n < kMaxOrder; ++n) {
+    if (m.a[n]) cudaFree(m.a[n]);
+    if (m.b[n]) cudaFree(m.b[n]);
+  }
+  m = DevModel{};
+}
+
+// AoS -> SoA transpose with range check (SparseTensor::validate's index
+// check, sparse_tensor.cpp:40-50; the O(nnz log nnz) duplicate check stays
+// with the host loader).
+struct SoAView {
+  int order;
+  int32_t dims[kMaxOrder];
+  int32_t* col[kMaxOrder];
+};
+__global__ void aos_to_soa_kernel(const int32_t* __restrict__ aos, int64_t nnz, SoAView v,
+                                  int* __restrict__ bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    for (int n = 0; n < v.order; ++n) {
+      const int32_t x = aos[e * v.order + n];
+      if (x < 0 || x >= v.dims[n]) atomicExch(bad, 1);
+      v.col[n][e] = x;
+    }
+  }
+}
+
+// A rows of the probe batch after the update (ftkcu_batch_probe A_new).
+__global__ void gather_rows_kernel(KView v, const int64_t* __restrict__ rows, int m_eff,
+                                   int cap, int jmax, float* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < v.order * m_eff * jmax;
+       e += gridDim.x * blockDim.x) {
+    const int n = e / (m_eff * jmax), rem = e - n * m_eff * jmax;
+    const int m = rem / jmax, j = rem - m * jmax;
+    if (j >= v.j[n]) continue;
+    const int32_t i = v.idx[n][rows[m]];
+    out[((size_t)n * cap + m) * jmax + j] = v.a[n][(size_t)i * v.j[n] + j];
+  }
+}
+
+KView make_view(const ftkcu_session* s, const DevTensor& t, bool shuffled) {
+  KView v{};
+  const DevModel& m = s->model;
+  v.order = m.order;
+  v.r = m.r;
+  for (int n = 0; n < m.order; ++n) {
+    v.j[n] = m.ranks[n];
+    v.a[n] = m.a[n];
+    v.b[n] = m.b[n];
+    v.idx[n] = shuffled ? t.sidx[n] : t.idx[n];
+  }
+  v.vals = shuffled ? t.svals : t.vals;
+  v.nnz = t.nnz;
+  return v;
+}
+
+int check_ready(ftkcu_session* s, int slot) {
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  const DevTensor& t = s->slots[slot];
+  if (!t.vals && t.nnz == 0 && t.order == 0)
+    return fail(s, FTKCU_ERR_STATE, "no tensor in slot %d", slot);
+  if (t.order != s->model.order)
+    return fail(s, FTKCU_ERR_ARG, "model/tensor order mismatch");
+  for (int n = 0; n < t.order; ++n)
+    if (s->model.dims[n] < t.dims[n])
+      return fail(s, FTKCU_ERR_ARG, "model dims too small for tensor");
+  return FTKCU_OK;
+}
+
+uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Per-epoch affine tile permutation t -> (t * mul + add) mod T.
+void tile_perm(uint64_t seed, int64_t ntiles, int64_t* mul, int64_t* add) {
+  if (ntiles <= 1) {
+    *mul = 1;
+    *add = 0;
+    return;
+  }
+  uint64_t h = splitmix(seed ^ 0x7469ull);
+  int64_t m = (int64_t)(h % (uint64_t)ntiles);
+  if (m == 0) m = 1;
+  while (gcd64(m, ntiles) != 1) m = (m + 1) % ntiles == 0 ? 1 : m + 1;
+  *mul = m;
+  *add = (int64_t)(splitmix(h) % (uint64_t)ntiles);
+}
+
+// Ensures the Hogwild stream exists.  perm != null lays it out in perm
+// order (one gather pass, plan-generation cost, outside the sweep timing).
+int prepare_stream(ftkcu_session* s, DevTensor& t, const int64_t* perm) {
+  if (perm) {
+    int rc = upload_perm(s, perm, t.nnz);
+    if (rc) return rc;
+    CK(build_shuffled(t, s->d_perm, 0, nullptr, 0, s->stream));
+    t.shuffled = false;  // stream is in a caller order, not the session shuffle
+    return FTKCU_OK;
+  }
+  if (!t.shuffled) CK(build_shuffled(t, nullptr, (uint64_t)s->opt_shuffle_seed, nullptr, 0,
+                                     s->stream));
+  return FTKCU_OK;
+}
+
+int finish_timing(ftkcu_session* s, double* ms) {
+  CK(cudaEventRecord(s->ev1, s->stream));
+  if (ms) {
+    CK(cudaEventSynchronize(s->ev1));
+    float f = 0.0f;
+    CK(cudaEventElapsedTime(&f, s->ev0, s->ev1));
+    *ms = f;
+  }
+  return FTKCU_OK;
+}
+
+}  // namespace
+
+namespace ftkcu {
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+}  // namespace ftkcu
+
+extern "C" {
+
+int ftkcu_abi_version(void) { return FTKCU_ABI_VERSION; }
+
+const char* ftkcu_last_error(const ftkcu_session* s) {
+  return s ? s->err.c_str() : g_create_err.c_str();
+}
+
+int ftkcu_session_create(int device, ftkcu_session** out) {
+  ftkcu_session* s = nullptr;
+  if (!out) return fail(nullptr, FTKCU_ERR_ARG, "null out pointer");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(nullptr, FTKCU_ERR_CUDA, "no CUDA device available: %s",
+                cudaGetErrorString(e));
+  if (device < 0 || device >= count)
+    return fail(nullptr, FTKCU_ERR_ARG, "device %d out of range (%d devices)", device, count);
+  s = new ftkcu_session;
+  s->device = device;
+  int major = 0;
+  cudaSetDevice(device);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) {
+    delete s;
+    return fail(nullptr, FTKCU_ERR_CUDA, "device %d is sm_%d0, engine is built for sm_100a",
+                device, major);
+  }
+  if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
+    delete s;
+    return fail(nullptr, FTKCU_ERR_CUDA, "stream/event creation failed");
+  }
+  *out = s;
+  return FTKCU_OK;
+}
+
+void ftkcu_session_destroy(ftkcu_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  for (auto& t : s->slots) free_tensor(t);
+  free_model(s->model);
+  if (s->grad) cudaFree(s->grad);
+  if (s->scratch) cudaFree(s->scratch);
+  if (s->d_perm) cudaFree(s->d_perm);
+  if (s->comm) ncclCommDestroy(s->comm);
+  cudaEventDestroy(s->ev0);
+  cudaEventDestroy(s->ev1);
+  cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
+  if (!s || !key) return fail(s, FTKCU_ERR_ARG, "null argument");
+  std::string k(key);
+  if (k == "precision") {
+    if (value < FTKCU_PREC_FP32 || value > FTKCU_PREC_3XTF32)
+      return fail(s, FTKCU_ERR_ARG, "bad precision %lld", (long long)value);
+    s->opt_precision = value;
+  } else if (k == "eval") {
+    if (value != FTKCU_EVAL_EXACT && value != FTKCU_EVAL_FAST)
+      return fail(s, FTKCU_ERR_ARG, "bad eval mode %lld", (long long)value);
+    s->opt_eval = value;
+  } else if (k == "hog_blocks_per_sm") {
+    if (value < 1 || value > 16) return fail(s, FTKCU_ERR_ARG, "bad hog_blocks_per_sm");
+    s->opt_hog_bps = value;
+  } else if (k == "verbose") {
+    s->opt_verbose = value;
+  } else if (k == "shuffle_seed") {
+    s->opt_shuffle_seed = value;
+    for (auto& t : s->slots) t.shuffled = false;
+  } else {
+    return fail(s, FTKCU_ERR_ARG, "unknown option '%s'", key);
+  }
+  return FTKCU_OK;
+}
+
+int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
+  if (!s || !key || !value) return fail(s, FTKCU_ERR_ARG, "null argument");
+  std::string k(key);
+  if (k == "precision") *value = s->opt_precision;
+  else if (k == "eval") *value = s->opt_eval;
+  else if (k == "hog_blocks_per_sm") *value = s->opt_hog_bps;
+  else if (k == "verbose") *value = s->opt_verbose;
+  else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
+  else if (k == "launches") *value = s->launches;
+  else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
+  else if (k == "num_sms") *value = num_sms();
+  else return fail(s, FTKCU_ERR_ARG, "unknown option '%s'", key);
+  return FTKCU_OK;
+}
+
+int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                        int64_t nnz, const int32_t* idx_rowmajor, const float* values) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (order < 1 || order > kMaxOrder)
+    return fail(s, FTKCU_ERR_ARG, "order %d unsupported (1..%d)", order, kMaxOrder);
+  if (nnz < 0) return fail(s, FTKCU_ERR_ARG, "negative nnz");
+  if (nnz > 0 && (!idx_rowmajor || !values)) return fail(s, FTKCU_ERR_ARG, "null data");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
+  DevTensor& t = s->slots[slot];
+  free_tensor(t);
+  t.order = order;
+  t.nnz = nnz;
+  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
+  const size_t cnt = nnz > 0 ? (size_t)nnz : 1;
+  for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * cnt));
+  CK(cudaMalloc(&t.vals, sizeof(float) * cnt));
+  if (nnz > 0) {
+    int rc2 = ensure_scratch(s, sizeof(int32_t) * (size_t)nnz * order + 256);
+    if (rc2) return rc2;
+    int32_t* aos = static_cast<int32_t*>(s->scratch);
+    int* bad = reinterpret_cast<int*>(static_cast<char*>(s->scratch) +
+                                      sizeof(int32_t) * (size_t)nnz * order);
+    CK(cudaMemcpyAsync(aos, idx_rowmajor, sizeof(int32_t) * (size_t)nnz * order,
+                       cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(t.vals, values, sizeof(float) * nnz, cudaMemcpyHostToDevice,
+                       s->stream));
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), s->stream));
+    SoAView v{};
+    v.order = order;
+    for (int n = 0; n < order; ++n) {
+      v.dims[n] = dims[n];
+      v.col[n] = t.idx[n];
+    }
+    aos_to_soa_kernel<<<num_sms() * 8, 256, 0, s->stream>>>(aos, nnz, v, bad);
+    CK(cudaGetLastError());
+    int h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (h_bad) {
+      free_tensor(t);
+      return fail(s, FTKCU_ERR_ARG, "index out of range in tensor upload");
+    }
+  }
+  return FTKCU_OK;
+}
+
+int ftkcu_tensor_release(ftkcu_session* s, int slot) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  CK(cudaStreamSynchronize(s->stream));
+  free_tensor(s->slots[slot]);
+  return FTKCU_OK;
+}
+
+int64_t ftkcu_tensor_nnz(ftkcu_session* s, int slot) {
+  if (!s || slot < 0 || slot >= 8) return -1;
+  return s->slots[slot].nnz;
+}
+
+int ftkcu_model_upload(ftkcu_session* s, int order, const int32_t* dims, const int32_t* ranks,
+                       int32_t R, const float* const* A, const float* const* B) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (order < 1 || order > kMaxOrder)
+    return fail(s, FTKCU_ERR_ARG, "order %d unsupported (1..%d)", order, kMaxOrder);
+  if (R < 1) return fail(s, FTKCU_ERR_ARG, "low rank must be positive");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1 || ranks[n] < 1) return fail(s, FTKCU_ERR_ARG, "zero dim or rank");
+  DevModel& m = s->model;
+  bool same = s->have_model && m.order == order && m.r == R;
+  for (int n = 0; same && n < order; ++n)
+    same = m.dims[n] == dims[n] && m.ranks[n] == ranks[n];
+  if (!same) {
+    CK(cudaStreamSynchronize(s->stream));
+    free_model(m);
+    s->have_model = false;
+    m.order = order;
+    m.r = R;
+    for (int n = 0; n < order; ++n) {
+      m.dims[n] = dims[n];
+      m.ranks[n] = ranks[n];
+      CK(cudaMalloc(&m.a[n], sizeof(float) * (size_t)dims[n] * ranks[n]));
+      CK(cudaMalloc(&m.b[n], sizeof(float) * (size_t)ranks[n] * R));
+    }
+    const size_t glen = (size_t)m.sum_j() * R;
+    if (glen > s->grad_len) {
+      if (s->grad) CK(cudaFree(s->grad));
+      CK(cudaMalloc(&s->grad, sizeof(float) * glen));
+      s->grad_len = glen;
+    }
+  }
+  for (int n = 0; n < order; ++n) {
+    CK(cudaMemcpyAsync(m.a[n], A[n], sizeof(float) * (size_t)dims[n] * ranks[n],
+                       cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(m.b[n], B[n], sizeof(float) * (size_t)ranks[n] * R,
+                       cudaMemcpyHostToDevice, s->stream));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  s->have_model = true;
+  return FTKCU_OK;
+}
+
+int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  const DevModel& m = s->model;
+  for (int n = 0; n < m.order; ++n) {
+    if (A && A[n])
+      CK(cudaMemcpyAsync(A[n], m.a[n], sizeof(float) * (size_t)m.dims[n] * m.ranks[n],
+                         cudaMemcpyDeviceToHost, s->stream));
+    if (B && B[n])
+      CK(cudaMemcpyAsync(B[n], m.b[n], sizeof(float) * (size_t)m.ranks[n] * m.r,
+                         cudaMemcpyDeviceToHost, s->stream));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  return FTKCU_OK;
+}
+
+int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_a,
+                       float reg_a, int mode, uint64_t seed, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  if (M < 1) return fail(s, FTKCU_ERR_ARG, "batch size must be positive");
+  DevTensor& t = s->slots[slot];
+  if (mode == FTKCU_MODE_DETERMINISTIC) {
+    if (!perm && t.nnz > 0) return fail(s, FTKCU_ERR_ARG, "deterministic mode needs a permutation");
+    if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+    KView v = make_view(s, t, false);
+    DetDebug dbg{};
+    CK(cudaEventRecord(s->ev0, s->stream));
+    if (t.nnz > 0) {
+      CK(launch_det_factor(v, s->d_perm, M, lr_a, reg_a, dbg, s->stream));
+      s->launches += 1;
+    }
+    return finish_timing(s, ms);
+  }
+  if (mode != FTKCU_MODE_HOGWILD) return fail(s, FTKCU_ERR_ARG, "unknown mode %d", mode);
+  if ((rc = prepare_stream(s, t, perm))) return rc;
+  KView v = make_view(s, t, true);
+  int64_t ntiles = (t.nnz + kHogTile - 1) / kHogTile, mul = 1, add = 0;
+  if (!perm) tile_perm(seed, ntiles, &mul, &add);
+  CK(cudaEventRecord(s->ev0, s->stream));
+  if (t.nnz > 0) {
+    if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+      CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision, s->stream));
+    } else {
+      CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps, s->stream));
+    }
+    s->launches += 1;
+  }
+  return finish_timing(s, ms);
+}
+
+int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_b,
+                     float reg_b, int mode, uint64_t seed, float* grad_out, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  if (M < 1) return fail(s, FTKCU_ERR_ARG, "batch size must be positive");
+  DevTensor& t = s->slots[slot];
+  if (t.nnz <= 0) return fail(s, FTKCU_ERR_EMPTY, "apply_core_update: empty tensor");
+  const size_t glen = (size_t)s->model.sum_j() * s->model.r;
+  KView v;
+  if (mode == FTKCU_MODE_DETERMINISTIC) {
+    if (!perm) return fail(s, FTKCU_ERR_ARG, "deterministic mode needs a permutation");
+    if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+    v = make_view(s, t, false);
+    CK(cudaEventRecord(s->ev0, s->stream));
+    CK(cudaMemsetAsync(s->grad, 0, sizeof(float) * glen, s->stream));
+    CK(launch_det_core(v, s->d_perm, M, s->grad, DetDebug{}, s->stream));
+    s->launches += 1;
+  } else if (mode == FTKCU_MODE_HOGWILD) {
+    if ((rc = prepare_stream(s, t, perm))) return rc;
+    v = make_view(s, t, true);
+    int64_t ntiles = (t.nnz + kHogTile - 1) / kHogTile, mul = 1, add = 0;
+    if (!perm) tile_perm(seed ^ 0xc0e5ull, ntiles, &mul, &add);
+    const size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
+    if ((rc = ensure_scratch(s, need))) return rc;
+    CK(cudaEventRecord(s->ev0, s->stream));
+    if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+      CK(launch_tc_core(v, mul, add, s->grad, (int)s->opt_precision,
+                        static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+    } else {
+      CK(launch_hog_core(v, mul, add, s->grad, (int)s->opt_hog_bps,
+                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+    }
+    s->launches += 2;
+  } else {
+    return fail(s, FTKCU_ERR_ARG, "unknown mode %d", mode);
+  }
+  if (s->comm && s->world > 1) {
+    NK(ncclAllReduce(s->grad, s->grad, glen, ncclFloat, ncclSum, s->comm, s->stream));
+  }
+  CK(launch_apply_core(v, s->grad, lr_b, reg_b, s->stream));
+  s->launches += 1;
+  if ((rc = finish_timing(s, ms))) return rc;
+  if (grad_out) {
+    CK(cudaMemcpyAsync(grad_out, s->grad, sizeof(float) * glen, cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  return FTKCU_OK;
+}
+
+int ftkcu_eval(ftkcu_session* s, int slot, int workers, double reg_a, double reg_b,
+               double* out3) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  if (!out3) return fail(s, FTKCU_ERR_ARG, "null output");
+  const DevTensor& t = s->slots[slot];
+  if ((rc = ensure_scratch(s, eval_scratch_bytes(s->model, t, workers)))) return rc;
+  CK(run_eval(s->model, t, workers, reg_a, reg_b, s->opt_eval == FTKCU_EVAL_EXACT, out3,
+              s->scratch, s->scratch_bytes, s->stream));
+  s->launches += 2 + s->model.order;
+  return FTKCU_OK;
+}
+
+int ftkcu_batch_probe(ftkcu_session* s, int slot, const int64_t* rows, int m_eff, int cap,
+                      float lr_a, float reg_a, float* C, float* D, float* U, float* xhat_f,
+                      float* resid_f, float* xhat_c, float* resid_c, float* A_new, float* G) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  if (cap < 1 || m_eff < 0 || m_eff > cap) return fail(s, FTKCU_ERR_ARG, "batch overflow");
+  if ((rc = upload_perm(s, rows, m_eff))) return rc;
+  const DevModel& m = s->model;
+  const int order = m.order, r = m.r, jmax = m.max_j();
+  const size_t n_cr = (size_t)order * cap * r, n_cj = (size_t)order * cap * jmax;
+  const size_t n_g = (size_t)order * jmax * r;
+  const size_t glen = (size_t)m.sum_j() * r;
+  const size_t floats = 2 * n_cr + 2 * n_cj + 4 * (size_t)cap + glen;
+  if ((rc = ensure_scratch(s, floats * sizeof(float)))) return rc;
+  float* base = static_cast<float*>(s->scratch);
+  float *dc = base, *dd = dc + n_cr, *du = dd + n_cr, *da = du + n_cj;
+  float *dxf = da + n_cj, *drf = dxf + cap, *dxc = drf + cap, *drc = dxc + cap;
+  float* dg = drc + cap;
+  CK(cudaMemsetAsync(base, 0, floats * sizeof(float), s->stream));
+  KView v = make_view(s, s->slots[slot], false);
+  v.nnz = m_eff;  // the probe batch is the whole "epoch"
+  DetDebug dbg_core{};
+  dbg_core.xhat = dxc;
+  dbg_core.resid = drc;
+  dbg_core.jmax = jmax;
+  if (m_eff > 0) CK(launch_det_core(v, s->d_perm, cap, dg, dbg_core, s->stream));
+  DetDebug dbg{};
+  dbg.c = dc;
+  dbg.d = dd;
+  dbg.u = du;
+  dbg.xhat = dxf;
+  dbg.resid = drf;
+  dbg.jmax = jmax;
+  if (m_eff > 0) CK(launch_det_factor(v, s->d_perm, cap, lr_a, reg_a, dbg, s->stream));
+  if (m_eff > 0)
+    gather_rows_kernel<<<32, 256, 0, s->stream>>>(v, s->d_perm, m_eff, cap, jmax, da);
+  CK(cudaGetLastError());
+  auto d2h = [&](float* dst, const float* src, size_t n) -> int {
+    if (dst) CK(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+    return FTKCU_OK;
+  };
+  if ((rc = d2h(C, dc, n_cr)) || (rc = d2h(D, dd, n_cr)) || (rc = d2h(U, du, n_cj)) ||
+      (rc = d2h(A_new, da, n_cj)) || (rc = d2h(xhat_f, dxf, cap)) || (rc = d2h(resid_f, drf, cap)) ||
+      (rc = d2h(xhat_c, dxc, cap)) || (rc = d2h(resid_c, drc, cap)))
+    return rc;
+  std::vector<float> hg(glen);
+  CK(cudaMemcpyAsync(hg.data(), dg, glen * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (G) {
+    std::memset(G, 0, n_g * sizeof(float));
+    size_t off = 0;
+    for (int n = 0; n < order; ++n) {
+      for (int j = 0; j < m.ranks[n]; ++j)
+        for (int c = 0; c < r; ++c) G[((size_t)n * jmax + j) * r + c] = hg[off + (size_t)j * r + c];
+      off += (size_t)m.ranks[n] * r;
+    }
+  }
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_unique_id(uint8_t* id128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, FTKCU_ERR_NCCL, "ncclGetUniqueId: %s",
+                                    ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "nccl unique id size");
+  std::memcpy(id128, &id, 128);
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_init(ftkcu_session* s, const uint8_t* id128, int rank, int world) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world) return fail(s, FTKCU_ERR_ARG, "bad rank/world");
+  if (s->comm) {
+    ncclCommDestroy(s->comm);
+    s->comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  NK(ncclCommInitRank(&s->comm, world, id, rank));
+  s->rank = rank;
+  s->world = world;
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_allreduce_grad(ftkcu_session* s) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->comm) return fail(s, FTKCU_ERR_STATE, "no communicator");
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  const size_t glen = (size_t)s->model.sum_j() * s->model.r;
+  NK(ncclAllReduce(s->grad, s->grad, glen, ncclFloat, ncclSum, s->comm, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return FTKCU_OK;
+}
+
+}  // extern "C"

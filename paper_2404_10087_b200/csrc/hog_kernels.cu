@@ -1,0 +1,395 @@
+// Hogwild FastTuckerPlus sweeps on CUDA cores (FTKCU_PREC_FP32), plus the
+// tiler that lays the COO stream out for them.
+//
+// Reference semantics: ftk::epoch_plus with workers > 1 -- batches are
+// processed concurrently and factor rows are written without locks
+// (Hogwild contract, model.hpp:27-30; decomposition.cpp:644-658).  Here every
+// warp is a "worker": it walks whole tiles of kHogTile nonzeros of the
+// shuffled stream, G nonzeros at a time, with
+//   stage a rows -> C = a B -> D = hadamard -> xhat, r -> U = D B^T ->
+//   a += lr (r u - reg a)      (Eq. 14 / Alg. 4)
+// and, in the core sweep, grad += r a^T D accumulated per warp in shared
+// memory, reduced per CTA and then across CTAs in a fixed order (Eq. 15 /
+// Alg. 5) -- so the core sweep is deterministic run to run.
+//
+// Tile order: tile t of the epoch is physical tile (t * mul + add) mod T with
+// gcd(mul, T) = 1, keyed per epoch by the host.  The shuffled stream itself is
+// built once per session by a Feistel bijection (no scratch, no sort).
+#include "engine.cuh"
+
+namespace ftkcu {
+namespace {
+
+constexpr int kHogThreads = 256;
+constexpr int kG = 4;  // nonzeros per warp step (share every B load)
+
+// ---- tiler -------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t k) {
+  x ^= k;
+  x *= 0x9e3779b1u;
+  x ^= x >> 15;
+  x *= 0x85ebca77u;
+  x ^= x >> 13;
+  return x;
+}
+
+// Bijection on [0, 2^bits) (balanced Feistel, 4 rounds), cycle-walked to
+// [0, n).
+__device__ int64_t feistel_perm(int64_t i, int64_t n, int bits, uint64_t seed) {
+  const int hb = bits / 2;
+  const uint64_t mask = (1ull << hb) - 1;
+  uint64_t x = (uint64_t)i;
+  do {
+    uint64_t lo = x & mask, hi = x >> hb;
+    for (int r = 0; r < 4; ++r) {
+      uint64_t f = mix32((uint32_t)lo, (uint32_t)(seed >> (r * 8)) ^ (uint32_t)(seed >> 32) * (r + 1)) & mask;
+      uint64_t nl = hi ^ f;
+      hi = lo;
+      lo = nl;
+    }
+    x = (hi << hb) | lo;
+  } while ((int64_t)x >= n);
+  return (int64_t)x;
+}
+
+struct ShuffleView {
+  int order;
+  const int32_t* src_idx[kMaxOrder];
+  int32_t* dst_idx[kMaxOrder];
+  const float* src_vals;
+  float* dst_vals;
+  int64_t nnz;
+};
+
+__global__ void shuffle_kernel(ShuffleView v, const int64_t* __restrict__ perm,
+                               int bits, uint64_t seed) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < v.nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = perm ? perm[k] : feistel_perm(k, v.nnz, bits, seed);
+    for (int n = 0; n < v.order; ++n) v.dst_idx[n][k] = v.src_idx[n][p];
+    v.dst_vals[k] = v.src_vals[p];
+  }
+}
+
+// ---- shared-memory layout of the sweep kernels --------------------------------
+
+struct HogLayout {
+  int sum_j, b_in_smem;
+  int aoff[kMaxOrder];  // offsets of mode blocks inside one G-row of a
+  size_t o_b[kMaxOrder], o_bt[kMaxOrder];
+  size_t o_warp, warp_floats, o_acc, acc_floats, end;  // floats
+};
+
+__host__ __device__ inline HogLayout hog_layout(const KView& v, bool core, int warps) {
+  HogLayout L{};
+  int s = 0;
+  for (int n = 0; n < v.order; ++n) {
+    L.aoff[n] = s;
+    s += v.j[n];
+  }
+  L.sum_j = s;
+  size_t o = 0;
+  size_t bfloats = 0;
+  for (int n = 0; n < v.order; ++n) bfloats += 2 * (size_t)v.j[n] * v.r;
+  L.b_in_smem = bfloats * 4 <= 96 * 1024;
+  if (L.b_in_smem) {
+    for (int n = 0; n < v.order; ++n) {
+      L.o_b[n] = o; o += (size_t)v.j[n] * v.r;
+      L.o_bt[n] = o; o += (size_t)v.j[n] * v.r;
+    }
+  }
+  // per warp: a[G][sum_j], c[G][N*R], d[G][N*R], x/res[G]
+  L.o_warp = o;
+  L.warp_floats = (size_t)kG * (s + 2 * v.order * v.r) + 2 * kG;
+  o += L.warp_floats * warps;
+  L.o_acc = o;
+  L.acc_floats = core ? (size_t)s * v.r : 0;
+  o += L.acc_floats * warps;
+  L.end = o;
+  return L;
+}
+
+__device__ void load_b(const KView& v, const HogLayout& L, float* sm) {
+  if (!L.b_in_smem) return;
+  for (int n = 0; n < v.order; ++n) {
+    const int jn = v.j[n], r = v.r;
+    for (int e = threadIdx.x; e < jn * r; e += blockDim.x) {
+      const int j = e / r, c = e - j * r;
+      const float x = v.b[n][e];
+      sm[L.o_b[n] + e] = x;
+      sm[L.o_bt[n] + (size_t)c * jn + j] = x;
+    }
+  }
+}
+
+__device__ __forceinline__ float bval(const KView& v, const HogLayout& L, const float* sm,
+                                      int n, int j, int c) {  // B_n[j][c]
+  return L.b_in_smem ? sm[L.o_b[n] + (size_t)j * v.r + c] : __ldg(v.b[n] + (size_t)j * v.r + c);
+}
+__device__ __forceinline__ float btval(const KView& v, const HogLayout& L, const float* sm,
+                                       int n, int c, int j) {  // B_n[j][c] via B^T
+  return L.b_in_smem ? sm[L.o_bt[n] + (size_t)c * v.j[n] + j] : __ldg(v.b[n] + (size_t)j * v.r + c);
+}
+
+// Shared front half of both sweeps for G nonzeros starting at stream
+// position e0: stage a rows, C, D, xhat and residual.  Returns through the
+// per-warp scratch `w`: a rows at w[g*sum_j + aoff[n] + j], C at wc, D at wd,
+// residuals at wres.
+__device__ void front(const KView& v, const HogLayout& L, const float* sm, float* w,
+                      int64_t e0, int32_t (&rows)[kG][kMaxOrder]) {
+  const int lane = threadIdx.x & 31;
+  const int N = v.order, r = v.r, sj = L.sum_j;
+  float* wa = w;
+  float* wc = w + kG * sj;
+  float* wd = wc + kG * N * r;
+  float* wx = wd + kG * N * r;
+  float* wres = wx + kG;
+  // indices + values: lane g*N+n loads idx[n][e0+g]
+  {
+    int32_t my = 0;
+    float xv = 0.0f;
+    const int g = lane / N, n = lane - g * N;
+    if (g < kG && e0 + g < v.nnz) my = v.idx[n][e0 + g];
+    if (lane < kG && e0 + lane < v.nnz) xv = v.vals[e0 + lane];
+#pragma unroll
+    for (int gg = 0; gg < kG; ++gg)
+#pragma unroll
+      for (int nn = 0; nn < kMaxOrder; ++nn)
+        if (nn < N) rows[gg][nn] = __shfl_sync(0xffffffffu, my, gg * N + nn);
+    if (lane < kG) wx[lane] = xv;
+  }
+  // stage a rows (coalesced: one warp reads whole rows)
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    const bool ok = e0 + g < v.nnz;
+    for (int n = 0; n < N; ++n) {
+      const int jn = v.j[n];
+      const float* src = v.a[n] + (size_t)rows[g][n] * jn;
+      for (int j = lane; j < jn; j += 32) wa[g * sj + L.aoff[n] + j] = ok ? src[j] : 0.0f;
+    }
+  }
+  __syncwarp();
+  // C^(n)[g][c] = sum_j a[g][n][j] B_n[j][c]
+  for (int n = 0; n < N; ++n) {
+    const int jn = v.j[n];
+    for (int c = lane; c < r; c += 32) {
+      float acc[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) acc[g] = 0.0f;
+      for (int j = 0; j < jn; ++j) {
+        const float b = bval(v, L, sm, n, j, c);
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[g] = fmaf(wa[g * sj + L.aoff[n] + j], b, acc[g]);
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) wc[(g * N + n) * r + c] = acc[g];
+    }
+  }
+  __syncwarp();
+  // D and the C-side prediction xhat = sum_c C1 D1 (== A1 . U1, PAPER Eq. 14)
+  float part[kG];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) part[g] = 0.0f;
+  for (int c = lane; c < r; c += 32) {
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+      for (int n = 0; n < N; ++n) {
+        float p = 1.0f;
+        for (int k = 0; k < N; ++k)
+          if (k != n) p *= wc[(g * N + k) * r + c];
+        wd[(g * N + n) * r + c] = p;
+        if (n == 0) part[g] = fmaf(wc[(g * N) * r + c], p, part[g]);
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    float s = part[g];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) wres[g] = (e0 + g < v.nnz) ? wx[g] - s : 0.0f;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kHogThreads)
+hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
+                  float reg) {
+  extern __shared__ float sm[];
+  const int warps = blockDim.x / 32;
+  const HogLayout L = hog_layout(v, false, warps);
+  load_b(v, L, sm);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* w = sm + L.o_warp + L.warp_floats * wid;
+  const int N = v.order, r = v.r, sj = L.sum_j;
+  const float* wa = w;
+  const float* wd = w + kG * sj + kG * N * r;
+  const float* wres = wd + kG * N * r + kG;
+  const int64_t gw = (int64_t)blockIdx.x * warps + wid, nw = (int64_t)gridDim.x * warps;
+  int32_t rows[kG][kMaxOrder];
+  for (int64_t t = gw; t < ntiles; t += nw) {
+    const int64_t tile = (t * tmul + tadd) % ntiles;
+    const int64_t base = tile * kHogTile;
+    for (int g0 = 0; g0 < kHogTile && base + g0 < v.nnz; g0 += kG) {
+      front(v, L, sm, w, base + g0, rows);
+      // U^(n)[g][j] = sum_c D[g][n][c] B_n[j][c]; a += lr (r u - reg a)
+      for (int n = 0; n < N; ++n) {
+        const int jn = v.j[n];
+        for (int j = lane; j < jn; j += 32) {
+          float u[kG];
+#pragma unroll
+          for (int g = 0; g < kG; ++g) u[g] = 0.0f;
+          for (int c = 0; c < r; ++c) {
+            const float b = btval(v, L, sm, n, c, j);
+#pragma unroll
+            for (int g = 0; g < kG; ++g) u[g] = fmaf(wd[(g * N + n) * r + c], b, u[g]);
+          }
+#pragma unroll
+          for (int g = 0; g < kG; ++g) {
+            if (base + g0 + g < v.nnz) {
+              const float a = wa[g * sj + L.aoff[n] + j];
+              v.a[n][(size_t)rows[g][n] * jn + j] = a + lr * (wres[g] * u[g] - reg * a);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kHogThreads)
+hog_core_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd,
+                float* __restrict__ partials) {
+  extern __shared__ float sm[];
+  const int warps = blockDim.x / 32;
+  const HogLayout L = hog_layout(v, true, warps);
+  load_b(v, L, sm);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* acc = sm + L.o_acc + L.acc_floats * wid;
+  for (size_t e = lane; e < L.acc_floats; e += 32) acc[e] = 0.0f;
+  __syncthreads();
+  float* w = sm + L.o_warp + L.warp_floats * wid;
+  const int N = v.order, r = v.r, sj = L.sum_j;
+  const float* wa = w;
+  const float* wd = w + kG * sj + kG * N * r;
+  const float* wres = wd + kG * N * r + kG;
+  const int64_t gw = (int64_t)blockIdx.x * warps + wid, nw = (int64_t)gridDim.x * warps;
+  int32_t rows[kG][kMaxOrder];
+  for (int64_t t = gw; t < ntiles; t += nw) {
+    const int64_t tile = (t * tmul + tadd) % ntiles;
+    const int64_t base = tile * kHogTile;
+    for (int g0 = 0; g0 < kHogTile && base + g0 < v.nnz; g0 += kG) {
+      front(v, L, sm, w, base + g0, rows);
+      // grad_n[j][c] += sum_g r_g a_g[j] D_g[c]
+      int off = 0;
+      for (int n = 0; n < N; ++n) {
+        const int jn = v.j[n];
+        for (int c = lane; c < r; c += 32) {
+          float dd[kG];
+#pragma unroll
+          for (int g = 0; g < kG; ++g) dd[g] = wres[g] * wd[(g * N + n) * r + c];
+          for (int j = 0; j < jn; ++j) {
+            float s = acc[off + j * r + c];
+#pragma unroll
+            for (int g = 0; g < kG; ++g) s = fmaf(wa[g * sj + L.aoff[n] + j], dd[g], s);
+            acc[off + j * r + c] = s;
+          }
+        }
+        off += jn * r;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // CTA reduction in warp order, then one partial per CTA.
+  for (size_t e = threadIdx.x; e < L.acc_floats; e += blockDim.x) {
+    float s = 0.0f;
+    for (int k = 0; k < warps; ++k) s += sm[L.o_acc + L.acc_floats * k + e];
+    partials[(size_t)blockIdx.x * L.acc_floats + e] = s;
+  }
+}
+
+// grad[e] = sum over CTAs in index order (deterministic).
+__global__ void reduce_partials_kernel(const float* __restrict__ partials, int nparts,
+                                       int len, float* __restrict__ grad) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int k = 0; k < nparts; ++k) s += partials[(size_t)k * len + e];
+    grad[e] = s;
+  }
+}
+
+int hog_grid(int blocks_per_sm) { return num_sms() * (blocks_per_sm < 1 ? 1 : blocks_per_sm); }
+
+}  // namespace
+
+size_t shuffle_scratch_bytes(int64_t) { return 0; }
+
+cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
+                           void*, size_t, cudaStream_t st) {
+  cudaError_t e;
+  if (!t.svals) {
+    for (int n = 0; n < t.order; ++n) {
+      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * (t.nnz > 0 ? t.nnz : 1));
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaMalloc(&t.svals, sizeof(float) * (t.nnz > 0 ? t.nnz : 1));
+    if (e != cudaSuccess) return e;
+  }
+  ShuffleView v{};
+  v.order = t.order;
+  for (int n = 0; n < t.order; ++n) {
+    v.src_idx[n] = t.idx[n];
+    v.dst_idx[n] = t.sidx[n];
+  }
+  v.src_vals = t.vals;
+  v.dst_vals = t.svals;
+  v.nnz = t.nnz;
+  int bits = 2;
+  while ((1ll << bits) < t.nnz) bits += 2;
+  if (t.nnz > 0)
+    shuffle_kernel<<<num_sms() * 8, 256, 0, st>>>(v, d_perm, bits, seed);
+  t.shuffled = true;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
+                              float lr_a, float reg_a, int blocks_per_sm,
+                              cudaStream_t st) {
+  const int warps = kHogThreads / 32;
+  const HogLayout L = hog_layout(v, false, warps);
+  const size_t bytes = L.end * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(hog_factor_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (v.nnz + kHogTile - 1) / kHogTile;
+  if (ntiles == 0) return cudaSuccess;
+  hog_factor_kernel<<<hog_grid(blocks_per_sm), kHogThreads, bytes, st>>>(
+      v, ntiles, tile_mul, tile_add, lr_a, reg_a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
+                            float* grad, int blocks_per_sm, float* scratch,
+                            size_t scratch_bytes, cudaStream_t st) {
+  const int warps = kHogThreads / 32;
+  const HogLayout L = hog_layout(v, true, warps);
+  const size_t bytes = L.end * sizeof(float);
+  const int grid = hog_grid(blocks_per_sm);
+  if (scratch_bytes < (size_t)grid * L.acc_floats * sizeof(float)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(hog_core_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (v.nnz + kHogTile - 1) / kHogTile;
+  hog_core_kernel<<<grid, kHogThreads, bytes, st>>>(v, ntiles, tile_mul, tile_add, scratch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int len = (int)L.acc_floats;
+  reduce_partials_kernel<<<(len + 255) / 256, 256, 0, st>>>(scratch, grid, len, grad);
+  return cudaGetLastError();
+}
+
+}  // namespace ftkcu

@@ -1,0 +1,383 @@
+// The device bridge: ftk::epoch_plus, ftk::train, ftk::loss, ftk::evaluate
+// implemented over the C-ABI (include/ftkcu.h), plus history I/O and the
+// analytic cost billing.  Reference: decomposition.cpp:623-705 (epoch_plus),
+// :849-948 (train, history), evaluation.cpp:36-72 (loss, evaluate).
+//
+// Device state: one process-wide ftkcu_session (device from DeviceOptions
+// or $FTK_DEVICE), with up to 8 host tensors cached on the device keyed by
+// their buffers and a content fingerprint (a SparseTensor is read-only after
+// construction, sparse_tensor.hpp:11-13).  epoch_plus syncs the model
+// H2D/D2H around each call; train keeps it resident for all epochs.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <charconv>
+#include <fstream>
+#include <limits>
+#include <mutex>
+#include <sstream>
+
+#include "ftk/decomposition.hpp"
+#include "ftkcu.h"
+
+namespace ftk {
+
+namespace {
+
+struct SlotKey {
+  const void* vals = nullptr;
+  const void* idx = nullptr;
+  size64 nnz = -1;
+  int order = 0;
+  std::uint64_t fp = 0;
+  std::uint64_t used = 0;
+};
+
+struct Engine {
+  ftkcu_session* s = nullptr;
+  SlotKey slots[8];
+  std::uint64_t tick = 0;
+  const Model* model_owner = nullptr;
+};
+
+std::mutex g_mu;
+Engine g_eng;
+DeviceOptions g_opts;
+
+void check(int rc) {
+  if (rc != FTKCU_OK) fail(ftkcu_last_error(g_eng.s));
+}
+
+ftkcu_session* session() {
+  if (g_eng.s) return g_eng.s;
+  int dev = g_opts.device;
+  if (dev < 0) {
+    const char* e = std::getenv("FTK_DEVICE");
+    dev = e ? std::atoi(e) : 0;
+  }
+  ftkcu_session* s = nullptr;
+  if (ftkcu_session_create(dev, &s) != FTKCU_OK) fail(ftkcu_last_error(nullptr));
+  g_eng.s = s;
+  return s;
+}
+
+void apply_options(ftkcu_session* s) {
+  const int prec = g_opts.precision == DevicePrecision::kFp32   ? FTKCU_PREC_FP32
+                   : g_opts.precision == DevicePrecision::kTf32 ? FTKCU_PREC_TF32
+                                                                : FTKCU_PREC_3XTF32;
+  check(ftkcu_set_option(s, "precision", prec));
+  check(ftkcu_set_option(s, "eval", g_opts.exact_eval ? FTKCU_EVAL_EXACT : FTKCU_EVAL_FAST));
+}
+
+std::uint64_t fingerprint(const SparseTensor& t) {
+  std::uint64_t h = mix64(static_cast<std::uint64_t>(t.nnz()) ^ (static_cast<std::uint64_t>(t.order) << 56));
+  for (index_t d : t.dims) h = mix64(h ^ static_cast<std::uint32_t>(d));
+  const size64 n = t.nnz();
+  const size64 step = n > 64 ? n / 64 : 1;
+  for (size64 p = 0; p < n; p += step) {
+    std::uint32_t v;
+    std::memcpy(&v, &t.values[p], 4);
+    h = mix64(h ^ v);
+    for (int k = 0; k < t.order; ++k) h = mix64(h ^ static_cast<std::uint32_t>(t.indices[p * t.order + k]));
+  }
+  return h;
+}
+
+// Returns the device slot holding t, uploading it if needed.
+int ensure_tensor(const SparseTensor& t) {
+  ftkcu_session* s = session();
+  const std::uint64_t fp = fingerprint(t);
+  int victim = 0;
+  for (int i = 0; i < 8; ++i) {
+    SlotKey& k = g_eng.slots[i];
+    if (k.vals == t.values.data() && k.idx == t.indices.data() && k.nnz == t.nnz() &&
+        k.order == t.order && k.fp == fp) {
+      k.used = ++g_eng.tick;
+      return i;
+    }
+    if (k.used < g_eng.slots[victim].used) victim = i;
+  }
+  require(static_cast<size64>(t.indices.size()) == t.nnz() * t.order, "index storage size mismatch");
+  check(ftkcu_tensor_upload(s, victim, t.order, t.dims.data(), t.nnz(), t.indices.data(),
+                            t.values.data()));
+  g_eng.slots[victim] = {t.values.data(), t.indices.data(), t.nnz(), t.order, fp, ++g_eng.tick};
+  return victim;
+}
+
+void upload_model(const Model& m) {
+  std::vector<const float*> a(m.order()), b(m.order());
+  for (int n = 0; n < m.order(); ++n) {
+    a[n] = m.a[n].data();
+    b[n] = m.b[n].data();
+  }
+  check(ftkcu_model_upload(session(), m.order(), m.dims.data(), m.ranks.data(), m.r, a.data(),
+                           b.data()));
+}
+
+void download_model(Model& m) {
+  std::vector<float*> a(m.order()), b(m.order());
+  for (int n = 0; n < m.order(); ++n) {
+    a[n] = m.a[n].data();
+    b[n] = m.b[n].data();
+  }
+  check(ftkcu_model_download(session(), a.data(), b.data()));
+}
+
+int device_mode(int workers) {
+  if (g_opts.mode == DeviceMode::kDeterministic) return FTKCU_MODE_DETERMINISTIC;
+  if (g_opts.mode == DeviceMode::kHogwild) return FTKCU_MODE_HOGWILD;
+  return workers == 1 ? FTKCU_MODE_DETERMINISTIC : FTKCU_MODE_HOGWILD;
+}
+
+// Analytic replay of the reference's per-batch billing for one phase
+// (decomposition.cpp:644-658 factor, :678-703 core).
+void bill_phase(CostCounters& cc, const Model& m, size64 nnz, index_t cap, bool factor,
+                bool store_c) {
+  const int N = m.order();
+  const size64 R = m.r;
+  const size64 combine = N >= 2 ? N - 2 : 0;
+  auto bill = [&](size64 me, size64 k, bool full) {
+    if (k == 0) return;
+    for (int n = 0; n < N; ++n) cc.count_batches(n, full, k);
+    for (int n = 0; n < N; ++n) {
+      const size64 J = m.ranks[n];
+      cc.add(n, kRead, me * J * k, full);  // staged factor rows
+      cc.add(n, kDStage, combine * me * R * k, full);
+      if (factor) {
+        cc.add(n, kRead, J * R * k, full);  // B^(n)
+        cc.add(n, kDStage, me * J * R * k, full);
+        cc.add(n, kBdtStage, me * R * J * k, full);
+        cc.add(n, kUpdate, me * J * k, full);
+      } else {
+        if (store_c) {
+          cc.add(n, kRead, me * R * k, full);  // cached C rows
+        } else {
+          cc.add(n, kRead, J * R * k, full);
+          cc.add(n, kDStage, me * J * R * k, full);
+        }
+        cc.add(n, kOther, me * J * k, full);
+        cc.add(n, kBdtStage, me * J * R * k, full);
+      }
+    }
+    cc.add(0, kOther, me * (factor ? m.ranks[0] : R) * k, full);
+  };
+  bill(cap, nnz / cap, true);
+  bill(nnz % cap, 1, false);
+  if (!factor) {
+    if (store_c)
+      for (int n = 0; n < N; ++n) cc.add_overhead(kOther, static_cast<size64>(m.dims[n]) * m.ranks[n] * R);
+    for (int n = 0; n < N; ++n) cc.add_overhead(kUpdate, static_cast<size64>(m.ranks[n]) * R);
+  }
+}
+
+// One FastTuckerPlus epoch on the resident model.
+EpochStats run_epoch(const SparseTensor& t, int slot, const Model& m, const Hyperparams& h,
+                     const EpochOptions& opts, std::uint64_t seed) {
+  ftkcu_session* s = session();
+  const int workers = resolve_workers(opts.workers);
+  const index_t cap = opts.canonical_order ? 1 : h.batch_size;
+  const int mode = device_mode(workers);
+  EpochStats st;
+  st.factor.reset(m.order());
+  st.core.reset(m.order());
+  const bool need_plan = mode == FTKCU_MODE_DETERMINISTIC || opts.canonical_order;
+  double ms_f = 0.0, ms_c = 0.0;
+  {
+    Rng rng(derive_seed(seed, {1}));
+    const int64_t* perm = nullptr;
+    EpochPlan plan;
+    if (need_plan) {
+      plan = opts.canonical_order ? EpochPlan::canonical(t) : EpochPlan::global(t, cap, rng);
+      perm = plan.positions().data();
+    }
+    check(ftkcu_factor_phase(s, slot, perm, cap, h.lr_a, h.reg_a, mode, derive_seed(seed, {1}),
+                             &ms_f));
+  }
+  {
+    Rng rng(derive_seed(seed, {2}));
+    const int64_t* perm = nullptr;
+    EpochPlan plan;
+    if (need_plan) {
+      plan = opts.canonical_order ? EpochPlan::canonical(t) : EpochPlan::global(t, cap, rng);
+      perm = plan.positions().data();
+    }
+    check(ftkcu_core_phase(s, slot, perm, cap, h.lr_b, h.reg_b, mode, derive_seed(seed, {2}),
+                           nullptr, &ms_c));
+  }
+  st.seconds_factor = ms_f * 1e-3;
+  st.seconds_core = ms_c * 1e-3;
+  bill_phase(st.factor, m, t.nnz(), cap, true, opts.store_c);
+  bill_phase(st.core, m, t.nnz(), cap, false, opts.store_c);
+  return st;
+}
+
+std::string num_json(double v) {
+  if (!std::isfinite(v)) return "null";
+  char buf[64];
+  auto r = std::to_chars(buf, buf + sizeof buf, v);
+  std::string s(buf, r.ptr);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+
+}  // namespace
+
+void set_device_options(const DeviceOptions& o) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_opts = o;
+  if (g_eng.s) apply_options(g_eng.s);
+}
+
+DeviceOptions device_options() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_opts;
+}
+
+EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
+                      const EpochOptions& opts, std::uint64_t seed) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(t);
+  upload_model(m);
+  EpochStats st;
+  try {
+    st = run_epoch(t, slot, m, h, opts, seed);
+  } catch (...) {
+    download_model(m);  // the reference mutates m in place before throwing
+    throw;
+  }
+  download_model(m);
+  return st;
+}
+
+namespace {
+
+// Device loss/metrics of the resident model.
+double device_loss(int slot, double reg_a, double reg_b, int workers) {
+  double out[3];
+  check(ftkcu_eval(session(), slot, workers, reg_a, reg_b, out));
+  return out[0] + out[2];
+}
+
+Metrics device_metrics(int slot, size64 n, int workers) {
+  require(n > 0, "empty evaluation set");
+  double out[3];
+  check(ftkcu_eval(session(), slot, workers, 0.0, 0.0, out));
+  Metrics mt;
+  mt.samples = n;
+  mt.rmse = std::sqrt(out[0] / static_cast<double>(n));
+  mt.mae = out[1] / static_cast<double>(n);
+  return mt;
+}
+
+}  // namespace
+
+double loss(const Model& m, const SparseTensor& t, double reg_a, double reg_b, int workers) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(t);
+  upload_model(m);
+  return device_loss(slot, reg_a, reg_b, std::max(1, workers));
+}
+
+Metrics evaluate(const Model& m, const SparseTensor& testset, int workers) {
+  require(testset.nnz() > 0, "empty evaluation set");
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(testset);
+  upload_model(m);
+  return device_metrics(slot, testset.nnz(), std::max(1, workers));
+}
+
+double rmse(const Model& m, const SparseTensor& testset, int workers) {
+  return evaluate(m, testset, workers).rmse;
+}
+
+double mae(const Model& m, const SparseTensor& testset, int workers) {
+  return evaluate(m, testset, workers).mae;
+}
+
+History train(const SparseTensor& train_set, const SparseTensor* test_set, Model& m,
+              const Hyperparams& h, const TrainOptions& opts) {
+  h.validate();
+  m.validate();
+  require(m.order() == train_set.order, "model/tensor order mismatch");
+  for (int n = 0; n < m.order(); ++n)
+    require(m.dims[n] >= train_set.dims[n], "model dims too small for tensor");
+  require(opts.variant == Variant::kPlus,
+          "the B200 engine implements the plus variant only (fasttucker/fastertucker are "
+          "out of scope)");
+  const int workers = resolve_workers(opts.workers);
+  EpochOptions eo;
+  eo.workers = workers;
+  eo.store_c = opts.store_c;
+  History hist;
+  if (h.epochs == 0) return hist;
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(train_set);
+  int test_slot = -1;
+  if (test_set != nullptr && test_set->nnz() > 0) {
+    test_slot = ensure_tensor(*test_set);
+  }
+  upload_model(m);
+  for (int epoch = 1; epoch <= h.epochs; ++epoch) {
+    const std::uint64_t es = derive_seed(opts.seed, {static_cast<std::uint64_t>(epoch)});
+    EpochRecord rec;
+    rec.epoch = epoch;
+    rec.stats = run_epoch(train_set, slot, m, h, eo, es);
+    rec.seconds = rec.stats.seconds_factor + rec.stats.seconds_core;
+    rec.train_loss = device_loss(slot, h.reg_a, h.reg_b, workers);
+    if (test_slot >= 0) {
+      Metrics mt = device_metrics(test_slot, test_set->nnz(), workers);
+      rec.test_rmse = mt.rmse;
+      rec.test_mae = mt.mae;
+    } else {
+      rec.test_rmse = std::numeric_limits<double>::quiet_NaN();
+      rec.test_mae = std::numeric_limits<double>::quiet_NaN();
+    }
+    const auto& f = rec.stats.factor;
+    const auto& c = rec.stats.core;
+    rec.reads = f.total(kRead) + c.total(kRead);
+    rec.mults = f.total(kDStage) + f.total(kBdtStage) + f.total(kOther) + c.total(kDStage) +
+                c.total(kBdtStage) + c.total(kOther);
+    if (!std::isfinite(rec.train_loss)) {
+      download_model(m);
+      fail("training diverged: non-finite loss at epoch " + std::to_string(epoch));
+    }
+    hist.push_back(std::move(rec));
+  }
+  download_model(m);
+  return hist;
+}
+
+std::string history_line_json(const EpochRecord& r) {
+  // Keys in the order nlohmann::json (std::map) emits them.
+  std::string s = "{\"epoch\":" + std::to_string(r.epoch);
+  s += ",\"mults\":" + std::to_string(r.mults);
+  s += ",\"reads\":" + std::to_string(r.reads);
+  s += ",\"seconds\":" + num_json(r.seconds);
+  s += ",\"test_mae\":" + num_json(r.test_mae);
+  s += ",\"test_rmse\":" + num_json(r.test_rmse);
+  s += ",\"train_loss\":" + num_json(r.train_loss) + "}";
+  return s;
+}
+
+void write_history_jsonl(const History& h, const std::string& path) {
+  std::ofstream out(path);
+  require(out.good(), "cannot write " + path);
+  for (const auto& r : h) out << history_line_json(r) << '\n';
+  require(out.good(), "write failed: " + path);
+}
+
+void write_history_csv(const History& h, const std::string& path) {
+  std::ofstream out(path);
+  require(out.good(), "cannot write " + path);
+  out << "epoch,train_loss,test_rmse,test_mae,seconds,reads,mults\n";
+  for (const auto& r : h)
+    out << r.epoch << ',' << r.train_loss << ',' << r.test_rmse << ',' << r.test_mae << ','
+        << r.seconds << ',' << r.reads << ',' << r.mults << '\n';
+  require(out.good(), "write failed: " + path);
+}
+
+}  // namespace ftk

@@ -1,0 +1,131 @@
+"""Shaped synthetic COO tensors for the benchmark configurations.
+
+The reference's synthgen takes one `dim` for all modes and stores tuples as
+vector<vector<int>> (synthgen.cpp:44-57), so it cannot express the per-mode
+Netflix / Yahoo!Music shapes of BASELINE.json or scale to 1e8 nonzeros.
+This generator keeps its contract -- distinct uniformly random tuples in a
+shuffled storage order, values uniform (synthgen.cpp:85-97) or planted from a
+FastTucker model plus Gaussian noise (synthgen.cpp:99-121) -- with per-mode
+dims:
+
+* tuples: 64-bit mixed-radix keys drawn uniformly, sort-unique, top up until
+  nnz distinct keys exist, then a uniform shuffle;
+* numpy for test-scale tensors (bit-reproducible across machines), torch on
+  the GPU for the 1e8-scale bench tensors (generation only; never timed).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+CONFIGS = {
+    # BASELINE.json configs
+    "c1": dict(dims=(10000, 10000, 1000), nnz=1_000_000, rank=16, lo=1.0, hi=5.0, seed=1),
+    "netflix": dict(dims=(480189, 17770, 2182), nnz=99_072_112, rank=32, lo=1.0, hi=5.0, seed=2),
+    "yahoo": dict(dims=(1000990, 624961, 3075), nnz=250_272_286, rank=32, lo=0.025, hi=5.0,
+                  seed=3),
+    "order6": dict(dims=(16384,) * 6, nnz=100_000_000, rank=16, lo=1.0, hi=5.0, seed=4),
+}
+
+
+@dataclass
+class Coo:
+    dims: np.ndarray  # int32 [order]
+    idx: np.ndarray   # int32 [nnz, order] (numpy) or torch int32 [nnz, order]
+    vals: np.ndarray  # float32 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.shape[0])
+
+    @property
+    def order(self) -> int:
+        return int(self.dims.shape[0])
+
+
+def _decode(keys, dims):
+    out = np.empty((keys.shape[0], len(dims)), np.int32)
+    rem = keys.copy()
+    for n in range(len(dims) - 1, -1, -1):
+        out[:, n] = rem % dims[n]
+        rem //= dims[n]
+    return out
+
+
+def uniform_numpy(dims, nnz, seed, lo=1.0, hi=5.0) -> Coo:
+    dims = [int(d) for d in dims]
+    cells = float(np.prod(np.array(dims, np.float64)))
+    if nnz > cells:
+        raise ValueError("nnz exceeds cell count")
+    rng = np.random.default_rng(seed)
+    keys = np.empty(0, np.int64)
+    while keys.size < nnz:
+        need = nnz - keys.size
+        k = np.zeros(need + need // 64 + 16, np.int64)
+        for d in dims:
+            k = k * d + rng.integers(0, d, size=k.size)
+        keys = np.unique(np.concatenate([keys, k]))
+    keys = keys[rng.permutation(keys.size)[:nnz]]
+    idx = _decode(keys, dims)
+    vals = rng.uniform(lo, hi, size=nnz).astype(np.float32)
+    return Coo(np.array(dims, np.int32), idx, vals)
+
+
+def planted_numpy(dims, nnz, seed, rank_j, rank_r, noise=0.1) -> tuple[Coo, list, list]:
+    """Values = FastTucker(truth) + N(0, noise^2); truth scaled to unit
+    predictions (default_init_scale(1.0, ...), like synthgen.cpp:104-107)."""
+    t = uniform_numpy(dims, nnz, seed)
+    order = len(dims)
+    rng = np.random.default_rng(seed + 1)
+    s = 2.0 / np.sqrt(rank_j) * (1.0 / rank_r) ** (1.0 / (2 * order))
+    a = [rng.uniform(0, s, size=(int(d), rank_j)).astype(np.float32) for d in dims]
+    b = [rng.uniform(0, s, size=(rank_j, rank_r)).astype(np.float32) for _ in dims]
+    prod = np.ones((nnz, rank_r), np.float64)
+    for n in range(order):
+        c = a[n].astype(np.float64) @ b[n].astype(np.float64)
+        prod *= c[t.idx[:, n]]
+    x = prod.sum(axis=1) + noise * rng.standard_normal(nnz)
+    t.vals = x.astype(np.float32)
+    return t, a, b
+
+
+def uniform_torch(dims, nnz, seed, lo=1.0, hi=5.0, device="cuda") -> Coo:
+    """GPU generation for 1e8-scale tensors; returns numpy host arrays."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    dims = [int(d) for d in dims]
+    keys = torch.empty(0, dtype=torch.int64, device=device)
+    while keys.numel() < nnz:
+        need = nnz - keys.numel()
+        m = need + need // 64 + 16
+        k = torch.zeros(m, dtype=torch.int64, device=device)
+        for d in dims:
+            k = k * d + torch.randint(0, d, (m,), generator=g, device=device, dtype=torch.int64)
+        keys = torch.unique(torch.cat([keys, k]))
+    perm = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
+    keys = keys[perm]
+    idx = torch.empty((nnz, len(dims)), dtype=torch.int32, device=device)
+    rem = keys
+    for n in range(len(dims) - 1, -1, -1):
+        idx[:, n] = (rem % dims[n]).to(torch.int32)
+        rem = rem // dims[n]
+    del keys, rem, perm
+    vals = torch.empty(nnz, dtype=torch.float32, device=device).uniform_(lo, hi, generator=g)
+    out = Coo(np.array(dims, np.int32), idx.cpu().numpy(), vals.cpu().numpy())
+    del idx, vals
+    torch.cuda.empty_cache()
+    return out
+
+
+def algorithmic_bytes_per_nnz(order: int, ranks) -> int:
+    """2 (4N + 4) + 12 sum J  (COO record per phase, A rows
+    read + written in the factor phase, read in the core phase)."""
+    return 2 * (4 * order + 4) + 12 * int(sum(ranks))
+
+
+def flops_per_nnz(order: int, ranks, r: int) -> int:
+    """8 R sum J + 2 N (N - 2) R per epoch."""
+    return 8 * r * int(sum(ranks)) + 2 * order * (order - 2) * r

@@ -1,0 +1,74 @@
+"""The C-ABI boundary (include/ftkcu.h): the library loads, exports every
+declared entry point, and fails loudly (never silently on the CPU) when no
+sm_100 device is present."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2404_10087_b200 as eng
+from paper_2404_10087_b200 import host
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ftkcu_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declarations_are_exported():
+    names = declared("ftkcu.h")
+    assert len(names) >= 18
+    lib = eng.load_library()
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(eng.EXPORTS)
+    assert lib.ftkcu_abi_version() == 1
+
+
+def test_exports_are_plain_c_symbols():
+    out = subprocess.run(["nm", "-D", "--defined-only", eng.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    syms = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    for n in declared("ftkcu.h"):
+        assert n in syms, n  # unmangled: callable from C, cgo, ctypes alike
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", eng.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_cxx_api_library_loads():
+    L = host.lib()
+    assert hasattr(L, "ftkh_epoch_plus") and hasattr(L, "ftkh_train")
+
+
+def _has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure path")
+def test_no_gpu_fails_loudly():
+    with pytest.raises(eng.FtkError, match="CUDA|device"):
+        eng.Session(0)
+
+
+def test_null_session_errors_are_reported():
+    lib = eng.load_library()
+    assert lib.ftkcu_set_option(None, b"precision", 0) != 0
+    assert lib.ftkcu_tensor_nnz(None, 0) == -1
+    h = C.c_void_p()
+    rc = lib.ftkcu_session_create(-5, C.byref(h))
+    assert rc != 0 and lib.ftkcu_last_error(None)
