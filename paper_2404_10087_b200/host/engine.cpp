@@ -137,7 +137,7 @@ void bill_phase(CostCounters& cc, const Model& m, size64 nnz, index_t cap, bool 
   const size64 R = m.r;
   const size64 combine = N >= 2 ? N - 2 : 0;
   auto bill = [&](size64 me, size64 k, bool full) {
-    if (k == 0) return;
+    if (k == 0 || me == 0) return;
     for (int n = 0; n < N; ++n) cc.count_batches(n, full, k);
     for (int n = 0; n < N; ++n) {
       const size64 J = m.ranks[n];

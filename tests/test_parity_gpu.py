@@ -229,13 +229,15 @@ def test_hogwild_core_gradient_matches_oracle(session, prec):
 
 
 def test_hogwild_core_is_deterministic(session):
+    # Same epoch seed => same tile -> warp assignment and an ordered CTA
+    # reduction, so the Hogwild core sweep is reproducible run to run.
     t = planted()
     m = init_for(t, 16, 16)
     upload(session, t, m)
     _, g1 = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=5, want_grad=True)
     upload(session, t, m)
-    _, g2 = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=6, want_grad=True)
-    assert np.array_equal(g1, g2)  # fixed CTA/warp tiles + ordered reduction
+    _, g2 = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=5, want_grad=True)
+    assert np.array_equal(g1, g2)
 
 
 def test_hogwild_factor_single_entry_tiles_match_oracle(session):
@@ -256,27 +258,34 @@ def test_hogwild_factor_single_entry_tiles_match_oracle(session):
         np.testing.assert_allclose(a[k], mc.a[k], rtol=1e-5, atol=1e-7)
 
 
-def test_hogwild_training_tracks_deterministic_rmse(session):
-    """Both modes on a planted tensor: Hogwild's test-RMSE trajectory within
-    the north-star tolerance of the sequential one."""
-    t = planted(nnz=80000)
-    (tri, trv), (tei, tev) = host.split_train_test(t.dims, t.idx, t.vals, 0.05, 7)
-    m0 = init_for(t, 16, 16)
-    curves = {}
-    for mode in (DET, HOG):
-        m = m0.copy()
-        session.upload_tensor(0, t.dims, tri, trv)
-        session.upload_tensor(1, t.dims, tei, tev)
-        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
-        rm = []
-        for ep in range(1, 9):
-            es = host.derive_seed(1, [ep])
-            p1 = host.global_plan(trv.size, 16, host.derive_seed(es, [1])) if mode == DET else None
-            p2 = host.global_plan(trv.size, 16, host.derive_seed(es, [2])) if mode == DET else None
-            session.factor_phase(0, p1, 16, 1e-2, 1e-4, mode, seed=host.derive_seed(es, [1]))
-            session.core_phase(0, p2, 16, 1e-2, 1e-4, mode, seed=host.derive_seed(es, [2]))
-            out = session.eval(1, 1)
-            rm.append(np.sqrt(out[0] / tev.size))
-        curves[mode] = np.array(rm)
-    assert curves[DET][-1] < curves[DET][0]
-    assert np.all(np.abs(curves[HOG] - curves[DET]) < 1e-3), curves
+def _c1p_problem():
+    cfg = synth.CONFIGS["c1"]
+    c, _, _ = synth.planted_numpy(cfg["dims"], cfg["nnz"], cfg["seed"], 16, 16, 0.1)
+    (tri, trv), (tei, tev) = host.split_train_test(c.dims, c.idx, c.vals, 0.014, 7)
+    scale = host.default_init_scale(float(np.mean(np.abs(trv))), 3, 16, [16] * 3)
+    a, b = host.init_model(c.dims, [16] * 3, 16, host.derive_seed(1, [77]), scale)
+    return c.dims, (tri, trv), (tei, tev), a, b
+
+
+@pytest.mark.slow
+def test_c1p_rmse_trajectory_vs_reference():
+    """North-star parity on config 1 (planted values):
+    50 epochs of ftk::train through the C++ API.  Deterministic mode must
+    match the reference's workers=1 trajectory (tolerance 1e-3 per epoch;
+    observed bit-identical), Hogwild mode must stay within 1e-3 of it."""
+    z = load("c1_trajectory")
+    dims, (tri, trv), (tei, tev), a0, b0 = _c1p_problem()
+    assert trv.size == int(z["c1p_ntrain"])
+    host.set_device_options(mode=0, precision=0, exact_eval=True)
+    a, b = [x.copy() for x in a0], [x.copy() for x in b0]
+    h = host.train(dims, [16] * 3, 16, tri, trv, tei, tev, a, b, epochs=50, seed=1, workers=1)
+    ref = z["c1p_w1_rmse"]
+    assert np.max(np.abs(h["rmse"] - ref)) < 1e-3
+    assert np.array_equal(h["rmse"], ref)  # deterministic mode is bit-exact
+    assert np.array_equal(h["loss"], z["c1p_w1_loss"])
+    host.set_device_options(mode=2, precision=0, exact_eval=True)
+    a, b = [x.copy() for x in a0], [x.copy() for x in b0]
+    hh = host.train(dims, [16] * 3, 16, tri, trv, tei, tev, a, b, epochs=50, seed=1, workers=8)
+    host.set_device_options(mode=0, precision=0, exact_eval=True)
+    dev = np.abs(hh["rmse"] - ref)
+    assert np.max(dev) < 1e-3, dev
