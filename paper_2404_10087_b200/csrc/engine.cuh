@@ -93,7 +93,7 @@ cudaError_t launch_apply_core(const KView& v, float* grad, float lr_b,
 
 // ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
-                              float lr_a, float reg_a, int blocks_per_sm,
+                              float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
                               cudaStream_t st);
 cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                             float* grad, int blocks_per_sm, float* scratch,
@@ -109,7 +109,7 @@ constexpr int kHogTile = 128;  // nonzeros per Hogwild tile
 // ---- tensor-core sweeps (tc_kernels.cu) -------------------------------------
 bool tc_supported(const KView& v);
 cudaError_t launch_tc_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
-                             float lr_a, float reg_a, int precision,
+                             float lr_a, float reg_a, int precision, int atomic_update,
                              cudaStream_t st);
 cudaError_t launch_tc_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                            float* grad, int precision, float* scratch,

@@ -153,7 +153,7 @@ size_t eval_scratch_bytes(const DevModel& m, const DevTensor& t, int workers) {
   for (int n = 0; n < m.order; ++n) s += align256((size_t)m.dims[n] * m.r * sizeof(double));
   s += 2 * align256((size_t)t.nnz * sizeof(double));  // exact per-entry buffers
   s += align256((size_t)(workers < 1 ? 1 : workers) * 2 * sizeof(double));
-  s += align256((size_t)(num_sms() * 8) * 2 * sizeof(double));
+  s += align256((size_t)(num_sms() * 8) * (2 + 2 * kMaxOrder) * sizeof(double));
   s += align256((size_t)2 * kMaxOrder * sizeof(double));
   return s;
 }
@@ -185,7 +185,7 @@ cudaError_t run_eval(const DevModel& m, const DevTensor& t, int workers,
   double* slabs = reinterpret_cast<double*>(p);
   p += align256((size_t)workers * 2 * sizeof(double));
   double* part = reinterpret_cast<double*>(p);
-  p += align256((size_t)(num_sms() * 8) * 2 * sizeof(double));
+  p += align256((size_t)(num_sms() * 8) * (2 + 2 * kMaxOrder) * sizeof(double));
   double* mats = reinterpret_cast<double*>(p);
 
   std::vector<double> h_mats(2 * m.order, 0.0);
@@ -221,38 +221,35 @@ cudaError_t run_eval(const DevModel& m, const DevTensor& t, int workers,
     for (int w = 0; w < workers; ++w) sum_sq = sum_sq + h_slabs[w];
     for (int w = 0; w < workers; ++w) sum_ab = sum_ab + h_slabs[workers + w];
   } else {
+    // part layout: [2 g] entry partials, then one [g_mat] block per matrix.
     const int g = grid_for(t.nnz);
+    const int gm = num_sms() * 8;
     if (t.nnz > 0) entry_fast_kernel<<<g, kEvalThreads, 0, st>>>(ev, part);
-    std::vector<double> h_part(2 * g, 0.0);
-    cudaError_t e;
-    if (t.nnz > 0) {
-      e = cudaMemcpyAsync(h_part.data(), part, sizeof(double) * 2 * g,
-                          cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) return e;
-    }
-    std::vector<double> h_mp;
     for (int n = 0; n < 2 * m.order; ++n) {
       const bool isa = n < m.order;
       const int k = isa ? n : n - m.order;
       const float* x = isa ? m.a[k] : m.b[k];
       const int64_t len = isa ? (int64_t)m.dims[k] * m.ranks[k] : (int64_t)m.ranks[k] * m.r;
-      const int gg = grid_for(len);
-      sq_fast_kernel<<<gg, kEvalThreads, 0, st>>>(x, len, part + 2 * g);
-      std::vector<double> tmp(gg);
-      e = cudaMemcpyAsync(tmp.data(), part + 2 * g, sizeof(double) * gg,
-                          cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) return e;
-      e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return e;
-      double s = 0.0;
-      for (double v : tmp) s += v;
-      h_mats[n] = s;
+      cudaMemsetAsync(part + 2 * gm + (size_t)n * gm, 0, sizeof(double) * gm, st);
+      sq_fast_kernel<<<grid_for(len), kEvalThreads, 0, st>>>(x, len, part + 2 * gm + (size_t)n * gm);
     }
+    const size_t nparts = 2 * (size_t)gm + 2 * (size_t)m.order * gm;
+    std::vector<double> h_part(nparts, 0.0);
+    cudaError_t e = cudaSuccess;
+    if (t.nnz == 0) e = cudaMemsetAsync(part, 0, sizeof(double) * 2 * gm, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(h_part.data(), part, sizeof(double) * nparts, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     for (int i = 0; i < g; ++i) {
       sum_sq += h_part[2 * i];
       sum_ab += h_part[2 * i + 1];
+    }
+    for (int n = 0; n < 2 * m.order; ++n) {
+      double acc = 0.0;
+      for (int i = 0; i < gm; ++i) acc += h_part[2 * gm + (size_t)n * gm + i];
+      h_mats[n] = acc;
     }
   }
   double reg = 0.0;

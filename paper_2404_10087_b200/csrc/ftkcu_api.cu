@@ -29,6 +29,7 @@ struct ftkcu_session {
   int64_t opt_precision = FTKCU_PREC_FP32;
   int64_t opt_eval = FTKCU_EVAL_EXACT;
   int64_t opt_hog_bps = 2;
+  int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -317,6 +318,9 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "hog_blocks_per_sm") {
     if (value < 1 || value > 16) return fail(s, FTKCU_ERR_ARG, "bad hog_blocks_per_sm");
     s->opt_hog_bps = value;
+  } else if (k == "hog_update") {
+    if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "bad hog_update");
+    s->opt_hog_update = value;
   } else if (k == "verbose") {
     s->opt_verbose = value;
   } else if (k == "shuffle_seed") {
@@ -335,6 +339,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "eval") *value = s->opt_eval;
   else if (k == "hog_blocks_per_sm") *value = s->opt_hog_bps;
   else if (k == "verbose") *value = s->opt_verbose;
+  else if (k == "hog_update") *value = s->opt_hog_update;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "launches") *value = s->launches;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
@@ -493,9 +498,11 @@ int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t 
   CK(cudaEventRecord(s->ev0, s->stream));
   if (t.nnz > 0) {
     if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
-      CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision, s->stream));
+      CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
+                          (int)s->opt_hog_update, s->stream));
     } else {
-      CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps, s->stream));
+      CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps,
+                           (int)s->opt_hog_update, s->stream));
     }
     s->launches += 1;
   }

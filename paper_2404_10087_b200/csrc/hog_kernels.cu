@@ -215,7 +215,7 @@ __device__ void front(const KView& v, const HogLayout& L, const float* sm, float
 
 __global__ void __launch_bounds__(kHogThreads)
 hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
-                  float reg) {
+                  float reg, int atomic_update) {
   extern __shared__ float sm[];
   const int warps = blockDim.x / 32;
   const HogLayout L = hog_layout(v, false, warps);
@@ -250,7 +250,13 @@ hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
           for (int g = 0; g < kG; ++g) {
             if (base + g0 + g < v.nnz) {
               const float a = wa[g * sj + L.aoff[n] + j];
-              v.a[n][(size_t)rows[g][n] * jn + j] = a + lr * (wres[g] * u[g] - reg * a);
+              const float step = lr * (wres[g] * u[g] - reg * a);
+              float* dst = v.a[n] + (size_t)rows[g][n] * jn + j;
+              // Overwrite = the reference's rule (snapshot + step, last writer
+              // wins); accumulate = lock-free RED.ADD, no update is lost when
+              // thousands of warps hit the same short-mode row.
+              if (atomic_update) atomicAdd(dst, step);
+              else *dst = a + step;
             }
           }
         }
@@ -357,7 +363,7 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
 }
 
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
-                              float lr_a, float reg_a, int blocks_per_sm,
+                              float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
                               cudaStream_t st) {
   const int warps = kHogThreads / 32;
   const HogLayout L = hog_layout(v, false, warps);
@@ -368,7 +374,7 @@ cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add
   const int64_t ntiles = (v.nnz + kHogTile - 1) / kHogTile;
   if (ntiles == 0) return cudaSuccess;
   hog_factor_kernel<<<hog_grid(blocks_per_sm), kHogThreads, bytes, st>>>(
-      v, ntiles, tile_mul, tile_add, lr_a, reg_a);
+      v, ntiles, tile_mul, tile_add, lr_a, reg_a, atomic_update);
   return cudaGetLastError();
 }
 
