@@ -115,6 +115,15 @@ cudaError_t launch_tc_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                            float* grad, int precision, float* scratch,
                            size_t scratch_bytes, cudaStream_t st);
 
+// ---- warp-specialized tensor-core sweeps, N = 3, J = R = 32 (tc_ws_kernels.cu)
+bool ws_supported(const KView& v);
+cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                             float lr, float reg, int precision, int atomic_update,
+                             cudaStream_t st);
+cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                           float* grad, int precision, float* scratch, size_t scratch_bytes,
+                           cudaStream_t st);
+
 // ---- evaluation (eval_kernels.cu) ---------------------------------------------
 // out3 = {sum sq, sum abs, reg}; exact = reference slab order.
 cudaError_t run_eval(const DevModel& m, const DevTensor& t, int workers,

@@ -29,7 +29,8 @@ struct ftkcu_session {
   int64_t opt_precision = FTKCU_PREC_FP32;
   int64_t opt_eval = FTKCU_EVAL_EXACT;
   int64_t opt_hog_bps = 2;
-  int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
+  int64_t opt_hog_update = 1;
+  int64_t opt_tc_ws = 1;       // warp-specialized tcgen05 sweeps where supported  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -318,6 +319,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "hog_blocks_per_sm") {
     if (value < 1 || value > 16) return fail(s, FTKCU_ERR_ARG, "bad hog_blocks_per_sm");
     s->opt_hog_bps = value;
+  } else if (k == "tc_ws") {
+    s->opt_tc_ws = value != 0;
   } else if (k == "hog_update") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "bad hog_update");
     s->opt_hog_update = value;
@@ -340,6 +343,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "hog_blocks_per_sm") *value = s->opt_hog_bps;
   else if (k == "verbose") *value = s->opt_verbose;
   else if (k == "hog_update") *value = s->opt_hog_update;
+  else if (k == "tc_ws") *value = s->opt_tc_ws;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "launches") *value = s->launches;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
@@ -497,7 +501,10 @@ int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t 
   if (!perm) tile_perm(seed, ntiles, &mul, &add);
   CK(cudaEventRecord(s->ev0, s->stream));
   if (t.nnz > 0) {
-    if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+    if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
+      CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
+                          (int)s->opt_hog_update, s->stream));
+    } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
       CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
                           (int)s->opt_hog_update, s->stream));
     } else {
@@ -535,7 +542,10 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     const size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
     if ((rc = ensure_scratch(s, need))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
-    if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+    if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
+      CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
+                        static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+    } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
       CK(launch_tc_core(v, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
     } else {

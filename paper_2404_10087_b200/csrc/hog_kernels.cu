@@ -337,12 +337,20 @@ size_t shuffle_scratch_bytes(int64_t) { return 0; }
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void*, size_t, cudaStream_t st) {
   cudaError_t e;
+  // Padded to whole tiles (index 0, value 0) so tile loads never run past
+  // the end; the sweeps mask rows >= nnz.
+  const int64_t padded = ((t.nnz + kHogTile - 1) / kHogTile) * kHogTile;
   if (!t.svals) {
+    const size_t cnt = padded > 0 ? (size_t)padded : 1;
     for (int n = 0; n < t.order; ++n) {
-      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * (t.nnz > 0 ? t.nnz : 1));
+      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * cnt);
+      if (e != cudaSuccess) return e;
+      e = cudaMemsetAsync(t.sidx[n], 0, sizeof(int32_t) * cnt, st);
       if (e != cudaSuccess) return e;
     }
-    e = cudaMalloc(&t.svals, sizeof(float) * (t.nnz > 0 ? t.nnz : 1));
+    e = cudaMalloc(&t.svals, sizeof(float) * cnt);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(t.svals, 0, sizeof(float) * cnt, st);
     if (e != cudaSuccess) return e;
   }
   ShuffleView v{};

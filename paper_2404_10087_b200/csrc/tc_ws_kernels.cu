@@ -1,0 +1,627 @@
+// Warp-specialized tcgen05 sweeps for the headline shape N = 3, J = R = 32
+// (Netflix- / Yahoo!Music-shaped configs).  One persistent CTA per SM:
+//
+//   warp 0      producer: per tile, one 1-D bulk copy per COO column into an
+//               index slot, then TMA tile::gather4 of the factor rows straight
+//               into the UMMA operand layout (K-major SWIZZLE_128B for the
+//               factor sweep, MN-major SWIZZLE_128B_ATOM_32B for the core
+//               sweep's gradient GEMM), 3-slot ring, mbarrier transactions;
+//   warp 1      MMA issuer (one thread): C = A B per tile into a double-
+//               buffered TMEM accumulator, then U = D B^T (factor) or
+//               G += A^T (r D) (core) one tile behind, so tensor-core latency
+//               overlaps the epilogue of the previous tile;
+//   warps 2-9   epilogue: two warps per TMEM lane quarter (128 rows), each
+//               owning half of the R (D) and J (update) columns; x_hat halves
+//               are exchanged through shared memory with a 64-thread named
+//               barrier; Hogwild row updates leave as 128-B-coalesced vector
+//               RED.ADD (or STG).
+//
+// Same algebra as tc_kernels.cu (the synchronous 4-warp sweeps that serve
+// every other shape); reference: decomposition.cpp:644-658 / :678-698,
+// PAPER.md Alg. 4 / Alg. 5.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "engine.cuh"
+#include "tc_common.cuh"
+
+namespace ftkcu {
+namespace {
+using namespace tc;
+
+constexpr int kN = 3;            // modes
+constexpr int kW = 32;           // J = R
+constexpr int kRows = 128;       // nonzeros per tile == TMEM lanes
+constexpr int kS = 3;            // A-slot ring depth
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsWs = (2 + kEpiWarps) * 32;
+constexpr uint32_t kModeTile = kRows * 128;  // 128 rows x 32 fp32 = 16 KB
+
+struct __align__(64) WsParams {
+  CUtensorMap tmap[kN];
+  const int32_t* idx[kN];
+  const float* vals;
+  float* a[kN];
+  const float* b[kN];
+  int64_t nnz, ntiles, tmul, tadd;
+  float lr, reg;
+  int atomic_update, prec3;
+  float* partials;
+};
+
+template <bool kCore>
+struct WsLayout {
+  static constexpr uint32_t kSlot = kN * kModeTile;
+  static constexpr uint32_t o_a = 0;
+  // core: the r-scaled D tile directly after the slots -- the G GEMM's fourth
+  // (garbage) M segment of the last slot then still reads shared memory.
+  static constexpr uint32_t o_d = o_a + kS * kSlot;
+  static constexpr uint32_t d_bytes = kCore ? kN * kModeTile : 0;
+  static constexpr uint32_t o_bt = o_d + d_bytes;       // B^T hi  (C GEMM operand)
+  static constexpr uint32_t o_btlo = o_bt + kN * 4096;  // B^T lo
+  static constexpr uint32_t o_b = o_btlo + kN * 4096;   // B (U GEMM operand, factor)
+  static constexpr uint32_t o_idx = o_b + (kCore ? 0 : kN * 4096);
+  static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
+  static constexpr uint32_t o_xp = o_idx + kS * kIdxSlot;  // x_hat halves [2][2][128]
+  static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
+  static constexpr int kBars = 24;
+  static constexpr uint32_t o_tmem = o_bar + kBars * 8;
+  static constexpr uint32_t bytes = o_tmem + 16 + 1024;
+  static_assert(bytes <= 227 * 1024, "shared-memory budget");
+  static_assert(!kCore || 4 * kModeTile - kSlot <= d_bytes, "G GEMM overrun");
+};
+
+// barrier ids
+enum : int {
+  B_FULL = 0,        // [kS] gathered rows landed (TMA tx)
+  B_IDX = 3,         // [kS] COO columns landed (bulk tx)
+  B_EMPTY = 6,       // [kS] slot free
+  B_CFULL = 9,       // [2]  C accumulator ready
+  B_DFULL = 11,      // factor [2]: D in TMEM; core [1]: D tile in smem
+  B_UFULL = 13,      // factor [2]: U ready
+  B_TEMPTY = 15,     // factor [2]: TMEM buffer free
+  B_LO = 17,         // factor: A_lo in TMEM (split tf32)
+  B_AFULL = 18,      // core: A rows copied to TMEM
+  B_DEMPTY = 19,     // core: G GEMM done with the D tile
+};
+
+__device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
+  const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
+  return (t * p.tmul + p.tadd) % p.ntiles;
+}
+
+template <bool kCore>
+__device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tslot) {
+  using L = WsLayout<kCore>;
+  for (int n = 0; n < kN; ++n) {
+    const float* b = p.b[n];
+    for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
+      const int j = e / kW, r = e - j * kW;
+      const float x = b[e];
+      const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+      *reinterpret_cast<float*>(sm + L::o_bt + n * 4096 + swz(r, j * 4, 128)) = hi;
+      *reinterpret_cast<float*>(sm + L::o_btlo + n * 4096 + swz(r, j * 4, 128)) = lo;
+      if constexpr (!kCore)
+        *reinterpret_cast<float*>(sm + L::o_b + n * 4096 + swz(j, r * 4, 128)) = hi;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&bars[B_FULL + s], 1);
+      mbar_init(&bars[B_IDX + s], 1);
+      mbar_init(&bars[B_EMPTY + s], kCore ? 1 : kEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[B_CFULL + b], 1);
+      mbar_init(&bars[B_DFULL + b], kEpiWarps);
+      mbar_init(&bars[B_UFULL + b], 1);
+      mbar_init(&bars[B_TEMPTY + b], kEpiWarps);
+    }
+    mbar_init(&bars[B_LO], kEpiWarps);
+    mbar_init(&bars[B_AFULL], kEpiWarps);
+    mbar_init(&bars[B_DEMPTY], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0)
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+}
+
+__device__ void ws_teardown(uint32_t tmem) {
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// Warp 0: COO columns, then the N x 32 gather4 of the tile's factor rows.
+template <bool kCore>
+__device__ void ws_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
+  using L = WsLayout<kCore>;
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = 0; k < nk; ++k) {
+    const int s = (int)(k % kS);
+    const uint32_t ph = (uint32_t)((k / kS) & 1);
+    const int64_t tile = ws_tile(p, k);
+    mbar_wait(&bars[B_EMPTY + s], ph ^ 1);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
+    if (lane == 0) {
+      mbar_expect_tx(&bars[B_IDX + s], L::kIdxSlot);
+      for (int n = 0; n < kN; ++n)
+        bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IDX + s]);
+      bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IDX + s]);
+    }
+    mbar_wait(&bars[B_IDX + s], ph);
+    if (lane == 0) mbar_expect_tx(&bars[B_FULL + s], L::kSlot);
+    __syncwarp();
+    uint8_t* slot = sm + L::o_a + s * L::kSlot;
+#pragma unroll
+    for (int n = 0; n < kN; ++n) {
+      const int4 r = *reinterpret_cast<const int4*>(s_idx + n * kRows + lane * 4);
+      tma_gather4(slot + n * kModeTile + lane * 512, &p.tmap[n], 0, r.x, r.y, r.z, r.w,
+                  &bars[B_FULL + s]);
+    }
+  }
+}
+
+// ---- factor sweep --------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_constant__ WsParams p) {
+  using L = WsLayout<false>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  ws_setup<false>(p, sm, bars, tslot);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // TMEM: per buffer b: C/U at 192 b, D at 192 b + 96; A_lo at 384.
+  constexpr uint32_t kLo = 384;
+
+  if (warp == 0) {
+    ws_producer<false>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
+      const uint32_t bt = smem_u32(sm + L::o_bt), btl = smem_u32(sm + L::o_btlo);
+      const uint32_t bb = smem_u32(sm + L::o_b);
+      auto issue_u = [&](int64_t k) {
+        const int b = (int)(k & 1);
+        mbar_wait(&bars[B_DFULL + b], (uint32_t)((k >> 1) & 1));
+        tc_after();
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 8; ++ks)
+            mma_ts(tmem + b * 192 + n * kW, tmem + b * 192 + 96 + n * kW + ks * 8,
+                   sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
+        mma_commit(&bars[B_UFULL + b]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kS), b = (int)(k & 1);
+        mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+        mbar_wait(&bars[B_TEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
+        if (p.prec3) mbar_wait(&bars[B_LO], (uint32_t)(k & 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 8; ++ks) {
+            const uint64_t da = sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128);
+            const uint64_t db = sdesc(bt + n * 4096 + ks * 32, 16, 1024, 128);
+            mma_ss(tmem + b * 192 + n * kW, da, db, id, ks > 0);
+            if (p.prec3) {
+              mma_ss(tmem + b * 192 + n * kW, da, sdesc(btl + n * 4096 + ks * 32, 16, 1024, 128),
+                     id, 1);
+              mma_ts(tmem + b * 192 + n * kW, tmem + kLo + n * kW + ks * 8, db, id, 1);
+            }
+          }
+        mma_commit(&bars[B_CFULL + b]);
+        if (k >= 1) issue_u(k - 1);
+      }
+      if (nk >= 1) issue_u(nk - 1);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* xp = reinterpret_cast<float*>(sm + L::o_xp);
+    // Split-tf32: this row's (half of the) factor rows minus their truncated
+    // tf32 part, into TMEM for the lo x hi MMA.
+    auto stage_lo = [&](int64_t k) {
+      const int s = (int)(k % kS);
+      mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 x =
+              *reinterpret_cast<const float4*>(slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+          v[q4 * 4 + 0] = __float_as_uint(x.x - tf32_trunc(x.x));
+          v[q4 * 4 + 1] = __float_as_uint(x.y - tf32_trunc(x.y));
+          v[q4 * 4 + 2] = __float_as_uint(x.z - tf32_trunc(x.z));
+          v[q4 * 4 + 3] = __float_as_uint(x.w - tf32_trunc(x.w));
+        }
+        tmem_st16(tl + kLo + n * kW + h * 16, v);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_LO]);
+    };
+    if (p.prec3 && nk > 0) stage_lo(0);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kS), b = (int)(k & 1);
+      const int64_t tile = ws_tile(p, k);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
+      const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
+      uint8_t* slot = sm + L::o_a + s * L::kSlot;
+
+      mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
+      tc_after();
+      float c[kN][16];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+        tmem_ld16(tl + b * 192 + n * kW + h * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
+      }
+      if (p.prec3 && k + 1 < nk) stage_lo(k + 1);
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      xp[((k & 1) * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
+      const bool ok = tile * kRows + row < p.nnz;
+      const float resid = ok ? s_val[row] - xhat : 0.0f;
+      // D^(n) halves -> TMEM (A operand of the U GEMM).
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float d = n == 0 ? c[1][i] * c[2][i] : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
+          v[i] = __float_as_uint(d);
+        }
+        tmem_st16(tl + b * 192 + 96 + n * kW + h * 16, v);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
+
+      mbar_wait(&bars[B_UFULL + b], (uint32_t)((k >> 1) & 1));
+      tc_after();
+      const float lr_r = p.lr * resid, lr_reg = p.lr * p.reg;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+        tmem_ld16(tl + b * 192 + n * kW + h * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float4* cell = reinterpret_cast<float4*>(slot + n * kModeTile +
+                                                   swz(row, (h * 16 + q4 * 4) * 4, 128));
+          const float4 a = *cell;
+          float4 st;
+          st.x = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 0]), -lr_reg * a.x);
+          st.y = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 1]), -lr_reg * a.y);
+          st.z = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 2]), -lr_reg * a.z);
+          st.w = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 3]), -lr_reg * a.w);
+          if (!p.atomic_update) {
+            st.x += a.x;
+            st.y += a.y;
+            st.z += a.z;
+            st.w += a.w;
+          }
+          *cell = st;
+        }
+      }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_TEMPTY + b]);
+      // 128-B-coalesced write-back of this warp's rows, column half h:
+      // 4 lanes x 16 B per row, 8 rows per instruction.
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        float* dst = p.a[n];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r2 = q * 32 + i * 8 + (lane >> 2);
+          const int ch = h * 4 + (lane & 3);
+          if (tile * kRows + r2 < p.nnz) {
+            const float4 v =
+                *reinterpret_cast<const float4*>(slot + n * kModeTile + swz(r2, ch * 16, 128));
+            float* gp = dst + (size_t)s_idx[n * kRows + r2] * kW + ch * 4;
+            if (p.atomic_update)
+              red_add_v4(gp, v);
+            else
+              *reinterpret_cast<float4*>(gp) = v;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);
+    }
+  }
+  ws_teardown(tmem);
+}
+
+// ---- core sweep ------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_constant__ WsParams p) {
+  using L = WsLayout<true>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  ws_setup<true>(p, sm, bars, tslot);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // TMEM: C[b] at 96 b; G at 192; A rows hi at 288, lo at 384.
+  constexpr uint32_t kG = 192, kAhi = 288, kAlo = 384;
+
+  if (warp == 0) {
+    ws_producer<true>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idc = idesc_tf32(128, kW, 0, 0);
+      constexpr uint32_t idg = idesc_tf32(128, kW, 1, 1);
+      const uint32_t bt = smem_u32(sm + L::o_bt), btl = smem_u32(sm + L::o_btlo);
+      const uint32_t d0 = smem_u32(sm + L::o_d);
+      auto issue_g = [&](int64_t k) {
+        const int s = (int)(k % kS);
+        mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll 4
+          for (int ks = 0; ks < kRows / 8; ++ks)
+            mma_ss(tmem + kG + n * kW, sdesc_l(a0 + ks * 1024, kModeTile, 512, 1),
+                   sdesc_l(d0 + n * kModeTile + ks * 1024, kModeTile, 512, 1), idg,
+                   (k > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&bars[B_DEMPTY]);
+        mma_commit(&bars[B_EMPTY + s]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        const int b = (int)(k & 1);
+        mbar_wait(&bars[B_AFULL], (uint32_t)(k & 1));
+        tc_after();
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 8; ++ks) {
+            const uint64_t db = sdesc(bt + n * 4096 + ks * 32, 16, 1024, 128);
+            mma_ts(tmem + b * 96 + n * kW, tmem + kAhi + n * kW + ks * 8, db, idc, ks > 0);
+            if (p.prec3) {
+              mma_ts(tmem + b * 96 + n * kW, tmem + kAhi + n * kW + ks * 8,
+                     sdesc(btl + n * 4096 + ks * 32, 16, 1024, 128), idc, 1);
+              mma_ts(tmem + b * 96 + n * kW, tmem + kAlo + n * kW + ks * 8, db, idc, 1);
+            }
+          }
+        mma_commit(&bars[B_CFULL + b]);
+        if (k >= 1) issue_g(k - 1);
+      }
+      if (nk >= 1) issue_g(nk - 1);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* xp = reinterpret_cast<float*>(sm + L::o_xp);
+    // Own row (half h of each mode) -> TMEM: the smem tile is in the MN-major
+    // layout of the G GEMM, which the K-major C GEMM cannot read.
+    auto stage_a = [&](int64_t k) {
+      const int s = (int)(k % kS);
+      mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 x = *reinterpret_cast<const float4*>(slot + n * kModeTile +
+                                                            swz32(row, (h * 16 + q4 * 4) * 4));
+          v[q4 * 4 + 0] = __float_as_uint(x.x);
+          v[q4 * 4 + 1] = __float_as_uint(x.y);
+          v[q4 * 4 + 2] = __float_as_uint(x.z);
+          v[q4 * 4 + 3] = __float_as_uint(x.w);
+        }
+        tmem_st16(tl + kAhi + n * kW + h * 16, v);
+        if (p.prec3) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float x = __uint_as_float(v[i]);
+            v[i] = __float_as_uint(x - tf32_trunc(x));
+          }
+          tmem_st16(tl + kAlo + n * kW + h * 16, v);
+        }
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_AFULL]);
+    };
+    if (nk > 0) stage_a(0);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kS), b = (int)(k & 1);
+      const int64_t tile = ws_tile(p, k);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
+      const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
+      mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
+      tc_after();
+      float c[kN][16];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+        tmem_ld16(tl + b * 96 + n * kW + h * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
+      }
+      if (k + 1 < nk) stage_a(k + 1);  // C(k) is complete: A rows TMEM is free
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      xp[((k & 1) * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
+      const bool ok = tile * kRows + row < p.nnz;
+      const float resid = ok ? s_val[row] - xhat : 0.0f;
+      mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with the D tile
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float4 d;
+          const int i = q4 * 4;
+#define FTK_D(ii) (n == 0 ? c[1][ii] * c[2][ii] : (n == 1 ? c[0][ii] * c[2][ii] : c[0][ii] * c[1][ii]))
+          d.x = tf32_rna(resid * FTK_D(i + 0));
+          d.y = tf32_rna(resid * FTK_D(i + 1));
+          d.z = tf32_rna(resid * FTK_D(i + 2));
+          d.w = tf32_rna(resid * FTK_D(i + 3));
+#undef FTK_D
+          *reinterpret_cast<float4*>(sm + L::o_d + n * kModeTile +
+                                     swz32(row, (h * 16 + i) * 4)) = d;
+        }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DFULL]);
+    }
+    // Publish this CTA's gradient once the last G GEMM has landed: TMEM lane
+    // j' = 32 n + j (quarter q = mode n) holds G_n[j][:], half h = columns.
+    if (nk > 0) mbar_wait(&bars[B_DEMPTY], (uint32_t)((nk - 1) & 1));
+    tc_after();
+    if (q < kN) {
+      uint32_t v[16];
+      tmem_ld16(tl + kG + q * kW + h * 16, v);
+      tmem_wait_ld();
+      float* out = p.partials + (size_t)blockIdx.x * (kN * kW * kW) + ((size_t)q * kW + lane) * kW + h * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = nk > 0 ? __uint_as_float(v[i]) : 0.0f;
+    }
+  }
+  ws_teardown(tmem);
+}
+
+__global__ void ws_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
+                                 float* __restrict__ grad) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int k = 0; k < nparts; ++k) s += partials[(size_t)k * len + e];
+    grad[e] = s;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn),
+                            cudaEnableDefault, &q);
+  }
+  return fn;
+}
+
+// Row-gather tensor map of A_n (I_n x 32 fp32): box of one 128-B row.
+bool make_row_map(CUtensorMap* tm, const float* a, int64_t rows, bool atom32) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)kW, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kW * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kW, 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                 bool core) {
+  for (int n = 0; n < kN; ++n) {
+    if (!make_row_map(&p.tmap[n], v.a[n], dims[n], core)) return false;
+    p.idx[n] = v.idx[n];
+    p.a[n] = v.a[n];
+    p.b[n] = v.b[n];
+  }
+  p.vals = v.vals;
+  p.nnz = v.nnz;
+  p.ntiles = (v.nnz + kRows - 1) / kRows;
+  p.tmul = mul;
+  p.tadd = add;
+  return true;
+}
+
+}  // namespace
+
+bool ws_supported(const KView& v) {
+  return v.order == kN && v.r == kW && v.j[0] == kW && v.j[1] == kW && v.j[2] == kW &&
+         encode_fn() != nullptr;
+}
+
+cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                             float lr, float reg, int precision, int atomic_update,
+                             cudaStream_t st) {
+  WsParams p{};
+  if (!make_params(p, v, dims, mul, add, false)) return cudaErrorNotSupported;
+  p.lr = lr;
+  p.reg = reg;
+  p.atomic_update = atomic_update;
+  p.prec3 = precision == FTKCU_PREC_3XTF32;
+  if (p.ntiles == 0) return cudaSuccess;
+  const int bytes = (int)WsLayout<false>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(ws_factor_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  ws_factor_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                           float* grad, int precision, float* scratch, size_t scratch_bytes,
+                           cudaStream_t st) {
+  WsParams p{};
+  if (!make_params(p, v, dims, mul, add, true)) return cudaErrorNotSupported;
+  p.prec3 = precision == FTKCU_PREC_3XTF32;
+  const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  const int len = kN * kW * kW;
+  if (grid < 1) return cudaErrorInvalidValue;
+  if (scratch_bytes < (size_t)grid * len * sizeof(float)) return cudaErrorInvalidValue;
+  p.partials = scratch;
+  const int bytes = (int)WsLayout<true>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(ws_core_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  ws_core_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ws_reduce_kernel<<<(len + 255) / 256, 256, 0, st>>>(scratch, grid, len, grad);
+  return cudaGetLastError();
+}
+
+}  // namespace ftkcu
