@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", default="netflix", choices=["netflix", "c1", "yahoo", "order6"])
     ap.add_argument("--rank", type=int, default=0, help="override J = R")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "3xtf32"])
+    ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
+    ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
@@ -222,6 +224,8 @@ def run_engine(args):
     prec = {"fp32": eng.PREC_FP32, "tf32": eng.PREC_TF32, "3xtf32": eng.PREC_3XTF32}[args.precision]
     s.set_option("precision", prec)
     s.set_option("eval", eng.EVAL_FAST)
+    s.set_option("hog_update", args.hog_update)
+    s.set_option("tc_ws", args.tc_ws)
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
     s.upload_tensor(0, coo.dims, coo.idx, coo.vals)

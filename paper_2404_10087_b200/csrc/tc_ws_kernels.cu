@@ -19,6 +19,7 @@
 // Same algebra as tc_kernels.cu (the synchronous 4-warp sweeps that serve
 // every other shape); reference: decomposition.cpp:644-658 / :678-698,
 // PAPER.md Alg. 4 / Alg. 5.
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -35,7 +36,9 @@ constexpr int kW = 32;           // J = R
 constexpr int kRows = 128;       // nonzeros per tile == TMEM lanes
 constexpr int kS = 3;            // A-slot ring depth
 constexpr int kEpiWarps = 8;
-constexpr int kThreadsWs = (2 + kEpiWarps) * 32;
+// warp 0 COO-column producer, warp 1 MMA, warps 2-9 epilogue, warp 10 gather producer
+constexpr int kThreadsWs = (3 + kEpiWarps) * 32;
+constexpr int kGatherWarp = 2 + kEpiWarps;
 constexpr uint32_t kModeTile = kRows * 128;  // 128 rows x 32 fp32 = 16 KB
 
 struct __align__(64) WsParams {
@@ -63,11 +66,12 @@ struct WsLayout {
   static constexpr uint32_t o_b = o_btlo + kN * 4096;   // B (U GEMM operand, factor)
   static constexpr uint32_t o_idx = o_b + (kCore ? 0 : kN * 4096);
   static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
-  static constexpr uint32_t o_xp = o_idx + kS * kIdxSlot;  // x_hat halves [2][2][128]
+  static constexpr int kI = kCore ? 4 : 6;  // COO-column ring depth (decoupled from A slots)
+  static constexpr uint32_t o_xp = o_idx + kI * kIdxSlot;  // x_hat halves [2][2][128]
   static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
-  static constexpr int kBars = 24;
+  static constexpr int kBars = 32;
   static constexpr uint32_t o_tmem = o_bar + kBars * 8;
-  static constexpr uint32_t bytes = o_tmem + 16 + 1024;
+  static constexpr uint32_t bytes = o_tmem + 16;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
   static_assert(!kCore || 4 * kModeTile - kSlot <= d_bytes, "G GEMM overrun");
 };
@@ -75,15 +79,16 @@ struct WsLayout {
 // barrier ids
 enum : int {
   B_FULL = 0,        // [kS] gathered rows landed (TMA tx)
-  B_IDX = 3,         // [kS] COO columns landed (bulk tx)
-  B_EMPTY = 6,       // [kS] slot free
-  B_CFULL = 9,       // [2]  C accumulator ready
-  B_DFULL = 11,      // factor [2]: D in TMEM; core [1]: D tile in smem
-  B_UFULL = 13,      // factor [2]: U ready
-  B_TEMPTY = 15,     // factor [2]: TMEM buffer free
-  B_LO = 17,         // factor: A_lo in TMEM (split tf32)
-  B_AFULL = 18,      // core: A rows copied to TMEM
-  B_DEMPTY = 19,     // core: G GEMM done with the D tile
+  B_EMPTY = 3,       // [kS] A slot free
+  B_IFULL = 6,       // [kI <= 6] COO columns landed (bulk tx)
+  B_IEMPTY = 12,     // [kI <= 6] COO slot free
+  B_CFULL = 18,      // [2]  C accumulator ready
+  B_DFULL = 20,      // factor [2]: D in TMEM; core [1]: D tile in smem
+  B_UFULL = 22,      // factor [2]: U ready
+  B_TEMPTY = 24,     // factor [2]: TMEM buffer free
+  B_LO = 26,         // factor: A_lo in TMEM (split tf32)
+  B_AFULL = 27,      // core: A rows copied to TMEM
+  B_DEMPTY = 28,     // core: G GEMM done with the D tile
 };
 
 __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
@@ -109,8 +114,11 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
   if (threadIdx.x == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&bars[B_FULL + s], 1);
-      mbar_init(&bars[B_IDX + s], 1);
       mbar_init(&bars[B_EMPTY + s], kCore ? 1 : kEpiWarps);
+    }
+    for (int i = 0; i < L::kI; ++i) {
+      mbar_init(&bars[B_IFULL + i], 1);
+      mbar_init(&bars[B_IEMPTY + i], kEpiWarps);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[B_CFULL + b], 1);
@@ -145,24 +153,35 @@ __device__ void ws_teardown(uint32_t tmem) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-// Warp 0: COO columns, then the N x 32 gather4 of the tile's factor rows.
+// Warp 0: the tile's COO columns (N index columns + values, 512 B each) by
+// 1-D bulk copies into a kI-deep ring, running ahead of the gathers.
 template <bool kCore>
-__device__ void ws_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
+__device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
+  using L = WsLayout<kCore>;
+  if ((threadIdx.x & 31) != 0) return;
+  for (int64_t k = 0; k < nk; ++k) {
+    const int i = (int)(k % L::kI);
+    const int64_t tile = ws_tile(p, k);
+    mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
+    int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+    mbar_expect_tx(&bars[B_IFULL + i], L::kIdxSlot);
+    for (int n = 0; n < kN; ++n)
+      bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+    bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+  }
+}
+
+// Gather warp: as soon as an A slot is free, TMA gather4 of the tile's factor
+// rows (32 lanes x N modes x 4 rows) into it.
+template <bool kCore>
+__device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsLayout<kCore>;
   const int lane = threadIdx.x & 31;
   for (int64_t k = 0; k < nk; ++k) {
-    const int s = (int)(k % kS);
-    const uint32_t ph = (uint32_t)((k / kS) & 1);
-    const int64_t tile = ws_tile(p, k);
-    mbar_wait(&bars[B_EMPTY + s], ph ^ 1);
-    int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
-    if (lane == 0) {
-      mbar_expect_tx(&bars[B_IDX + s], L::kIdxSlot);
-      for (int n = 0; n < kN; ++n)
-        bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IDX + s]);
-      bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IDX + s]);
-    }
-    mbar_wait(&bars[B_IDX + s], ph);
+    const int s = (int)(k % kS), i = (int)(k % L::kI);
+    mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
+    mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
+    const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
     if (lane == 0) mbar_expect_tx(&bars[B_FULL + s], L::kSlot);
     __syncwarp();
     uint8_t* slot = sm + L::o_a + s * L::kSlot;
@@ -177,11 +196,11 @@ __device__ void ws_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int6
 
 // ---- factor sweep --------------------------------------------------------------
 
+template <bool kAtomic>
 __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_constant__ WsParams p) {
   using L = WsLayout<false>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
   ws_setup<false>(p, sm, bars, tslot);
@@ -192,7 +211,9 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   constexpr uint32_t kLo = 384;
 
   if (warp == 0) {
-    ws_producer<false>(p, sm, bars, nk);
+    ws_idx_producer<false>(p, sm, bars, nk);
+  } else if (warp == kGatherWarp) {
+    ws_gather_producer<false>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
@@ -265,14 +286,27 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_LO]);
     };
-    if (p.prec3 && nk > 0) stage_lo(0);
-    for (int64_t k = 0; k < nk; ++k) {
-      const int s = (int)(k % kS), b = (int)(k & 1);
+    // Software pipeline: epi1(k + 1) runs while U(k) is on the tensor core.
+    // epi1: C -> D (TMEM), residual, and this thread's A snapshot + global
+    // row indices into registers, after which the smem slot is released.
+    // epi2: U -> step -> vector RED (or STG) of the row's column half.
+    // kAtomic: the snapshot only feeds the regulariser lr reg a (~1e-7 a),
+    // so an fp16 copy suffices and the slot is released in epi1.  Overwrite
+    // mode (a' = a + step) keeps the slot until epi2 and reads fp32 there.
+    struct Tile {
+      __half2 a[kAtomic ? kN : 1][8];
+      int32_t g[kN];
+      float resid;
+      bool ok;
+      int slot;
+    };
+    Tile cur, nxt;
+    auto epi1 = [&](int64_t k, Tile& t) {
+      const int s = (int)(k % kS), b = (int)(k & 1), ii = (int)(k % L::kI);
       const int64_t tile = ws_tile(p, k);
-      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
-      uint8_t* slot = sm + L::o_a + s * L::kSlot;
-
+      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
       mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
       float c[kN][16];
@@ -289,11 +323,31 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
 #pragma unroll
       for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
       xp[((k & 1) * 2 + h) * kRows + row] = part;
+      t.slot = s;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        t.g[n] = s_idx[n * kRows + row];
+        if constexpr (kAtomic) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 x = *reinterpret_cast<const float4*>(
+                slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+            t.a[n][q4 * 2 + 0] = __floats2half2_rn(x.x, x.y);
+            t.a[n][q4 * 2 + 1] = __floats2half2_rn(x.z, x.w);
+          }
+        }
+      }
+      const float xv = s_val[row];
       named_bar(1 + q, 64);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);  // COO slot may be refilled
+      if constexpr (kAtomic) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);  // slot k may be refilled
+      }
       const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
-      const bool ok = tile * kRows + row < p.nnz;
-      const float resid = ok ? s_val[row] - xhat : 0.0f;
-      // D^(n) halves -> TMEM (A operand of the U GEMM).
+      t.ok = tile * kRows + row < p.nnz;
+      t.resid = t.ok ? xv - xhat : 0.0f;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
@@ -308,59 +362,62 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
-
+    };
+    auto epi2 = [&](int64_t k, const Tile& t) {
+      const int b = (int)(k & 1);
       mbar_wait(&bars[B_UFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
-      const float lr_r = p.lr * resid, lr_reg = p.lr * p.reg;
+      uint32_t u[kN][16];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 192 + n * kW + h * 16, u[n]);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_TEMPTY + b]);
+      const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
+      const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
-        uint32_t v[16];
-        tmem_ld16(tl + b * 192 + n * kW + h * 16, v);
-        tmem_wait_ld();
+        float* gp = p.a[n] + (size_t)t.g[n] * kW + h * 16;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          float4* cell = reinterpret_cast<float4*>(slot + n * kModeTile +
-                                                   swz(row, (h * 16 + q4 * 4) * 4, 128));
-          const float4 a = *cell;
+          float4 a;
+          if constexpr (kAtomic) {
+            const float2 lo = __half22float2(t.a[n][q4 * 2 + 0]);
+            const float2 hi = __half22float2(t.a[n][q4 * 2 + 1]);
+            a = make_float4(lo.x, lo.y, hi.x, hi.y);
+          } else {
+            a = *reinterpret_cast<const float4*>(slot + n * kModeTile +
+                                                 swz(row, (h * 16 + q4 * 4) * 4, 128));
+          }
           float4 st;
-          st.x = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 0]), -lr_reg * a.x);
-          st.y = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 1]), -lr_reg * a.y);
-          st.z = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 2]), -lr_reg * a.z);
-          st.w = fmaf(lr_r, __uint_as_float(v[q4 * 4 + 3]), -lr_reg * a.w);
-          if (!p.atomic_update) {
+          st.x = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 0]), -lr_reg * a.x);
+          st.y = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 1]), -lr_reg * a.y);
+          st.z = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
+          st.w = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
+          if (!t.ok) continue;
+          if constexpr (kAtomic) {
+            red_add_v4(gp + q4 * 4, st);
+          } else {
             st.x += a.x;
             st.y += a.y;
             st.z += a.z;
             st.w += a.w;
-          }
-          *cell = st;
-        }
-      }
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_TEMPTY + b]);
-      // 128-B-coalesced write-back of this warp's rows, column half h:
-      // 4 lanes x 16 B per row, 8 rows per instruction.
-#pragma unroll
-      for (int n = 0; n < kN; ++n) {
-        float* dst = p.a[n];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r2 = q * 32 + i * 8 + (lane >> 2);
-          const int ch = h * 4 + (lane & 3);
-          if (tile * kRows + r2 < p.nnz) {
-            const float4 v =
-                *reinterpret_cast<const float4*>(slot + n * kModeTile + swz(r2, ch * 16, 128));
-            float* gp = dst + (size_t)s_idx[n * kRows + r2] * kW + ch * 4;
-            if (p.atomic_update)
-              red_add_v4(gp, v);
-            else
-              *reinterpret_cast<float4*>(gp) = v;
+            *reinterpret_cast<float4*>(gp + q4 * 4) = st;
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);
+      if constexpr (!kAtomic) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);
+      }
+    };
+    if (p.prec3 && nk > 0) stage_lo(0);
+    if (nk > 0) epi1(0, cur);
+    for (int64_t k = 0; k < nk; ++k) {
+      if (k + 1 < nk) epi1(k + 1, nxt);
+      epi2(k, cur);
+      cur = nxt;
     }
   }
   ws_teardown(tmem);
@@ -370,9 +427,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
 
 __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_constant__ WsParams p) {
   using L = WsLayout<true>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
   ws_setup<true>(p, sm, bars, tslot);
@@ -383,7 +439,9 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
   constexpr uint32_t kG = 192, kAhi = 288, kAlo = 384;
 
   if (warp == 0) {
-    ws_producer<true>(p, sm, bars, nk);
+    ws_idx_producer<true>(p, sm, bars, nk);
+  } else if (warp == kGatherWarp) {
+    ws_gather_producer<true>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idc = idesc_tf32(128, kW, 0, 0);
@@ -466,9 +524,9 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
     };
     if (nk > 0) stage_a(0);
     for (int64_t k = 0; k < nk; ++k) {
-      const int s = (int)(k % kS), b = (int)(k & 1);
+      const int b = (int)(k & 1), ii = (int)(k % L::kI);
       const int64_t tile = ws_tile(p, k);
-      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + s * L::kIdxSlot);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
       mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
@@ -490,6 +548,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
       const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
       const bool ok = tile * kRows + row < p.nnz;
       const float resid = ok ? s_val[row] - xhat : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);
       mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with the D tile
 #pragma unroll
       for (int n = 0; n < kN; ++n)
@@ -594,11 +654,11 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   p.prec3 = precision == FTKCU_PREC_3XTF32;
   if (p.ntiles == 0) return cudaSuccess;
   const int bytes = (int)WsLayout<false>::bytes;
-  cudaError_t e = cudaFuncSetAttribute(ws_factor_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  auto kern = atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
-  ws_factor_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+  kern<<<grid, kThreadsWs, bytes, st>>>(p);
   return cudaGetLastError();
 }
 
