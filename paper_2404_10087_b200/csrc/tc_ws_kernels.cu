@@ -67,7 +67,9 @@ struct WsLayout {
   static constexpr uint32_t o_idx = o_b + (kCore ? 0 : kN * 4096);
   static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
   static constexpr int kI = kCore ? 4 : 6;  // COO-column ring depth (decoupled from A slots)
-  static constexpr uint32_t o_xp = o_idx + kI * kIdxSlot;  // x_hat halves [2][2][128]
+  static constexpr uint32_t o_stage = o_idx + kI * kIdxSlot;  // factor: per-quarter write-back rows
+  static constexpr uint32_t stage_bytes = kCore ? 0 : 4 * 32 * 128;
+  static constexpr uint32_t o_xp = o_stage + stage_bytes;  // x_hat halves [2][2][128]
   static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
   static constexpr int kBars = 32;
   static constexpr uint32_t o_tmem = o_bar + kBars * 8;
@@ -376,9 +378,13 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_TEMPTY + b]);
       const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
+      // Per mode: both warps of the quarter write their column half of the
+      // step rows into the quarter's 4 KB staging tile, then each warp sends
+      // 16 whole 128-B rows (8 lanes per row) -- one coalesced RED (or STG)
+      // request per row instead of eight 16-B ones.
+      uint8_t* stage = sm + L::o_stage + q * 4096;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
-        float* gp = p.a[n] + (size_t)t.g[n] * kW + h * 16;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           float4 a;
@@ -395,17 +401,31 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
           st.y = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 1]), -lr_reg * a.y);
           st.z = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
           st.w = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
-          if (!t.ok) continue;
-          if constexpr (kAtomic) {
-            red_add_v4(gp + q4 * 4, st);
-          } else {
+          if constexpr (!kAtomic) {
             st.x += a.x;
             st.y += a.y;
             st.z += a.z;
             st.w += a.w;
-            *reinterpret_cast<float4*>(gp + q4 * 4) = st;
+          }
+          *reinterpret_cast<float4*>(stage + swz(lane, (h * 16 + q4 * 4) * 4, 128)) = st;
+        }
+        named_bar(1 + q, 64);
+        float* dst = p.a[n];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
+          const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
+          const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
+          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
+          if (okr) {
+            float* gp = dst + (size_t)g * kW + ch * 4;
+            if constexpr (kAtomic)
+              red_add_v4(gp, v);
+            else
+              *reinterpret_cast<float4*>(gp) = v;
           }
         }
+        named_bar(1 + q, 64);
       }
       if constexpr (!kAtomic) {
         __syncwarp();
