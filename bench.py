@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--config", default="netflix", choices=["netflix", "c1", "yahoo", "order6"])
     ap.add_argument("--rank", type=int, default=0, help="override J = R")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "3xtf32"])
+    ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
     ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
     ap.add_argument("--no-e2e", action="store_true")

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_factor_kernel(TcParams p) {
       for (int h = 0; h < R / 16; ++h) {
         uint32_t v[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = __float_as_uint(tf32_rna(d_of<N, R>(c, n, h * 16 + q)));
+        for (int q = 0; q < 16; ++q) v[q] = __float_as_uint(d_of<N, R>(c, n, h * 16 + q)) + 0x1000u;
         tmem_st16(tlane + L::t_x + n * R + h * 16, v);
       }
     tmem_wait_st();
@@ -476,6 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
             v[q4 * 4 + 2] = __float_as_uint(x.z);
             v[q4 * 4 + 3] = __float_as_uint(x.w);
           }
+          if (!p.prec3)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += 0x1000u;  // round, don't truncate
           tmem_st16(tlane + L::t_a + sg * 32 + h * 16, v);
           if (p.prec3) {
 #pragma unroll
@@ -535,10 +538,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
 #pragma unroll
       for (int q4 = 0; q4 < R / 4; ++q4) {
         float4 d;
-        d.x = tf32_rna(resid * d_of<N, R>(c, n, q4 * 4 + 0));
-        d.y = tf32_rna(resid * d_of<N, R>(c, n, q4 * 4 + 1));
-        d.z = tf32_rna(resid * d_of<N, R>(c, n, q4 * 4 + 2));
-        d.w = tf32_rna(resid * d_of<N, R>(c, n, q4 * 4 + 3));
+        // + half a tf32 ulp: the tensor core's truncation becomes rounding
+        d.x = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 0)) + 0x1000u);
+        d.y = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 1)) + 0x1000u);
+        d.z = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 2)) + 0x1000u);
+        d.w = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 3)) + 0x1000u);
         const uint32_t byte = (n * R + q4 * 4) * 4;
         *reinterpret_cast<float4*>(sm + L::o_d + (byte >> 7) * L::kSeg + swz32(t, byte & 127)) = d;
       }

@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "tc_common.cuh"
@@ -51,6 +52,7 @@ struct __align__(64) WsParams {
   float lr, reg;
   int atomic_update, prec3;
   float* partials;
+  int exp;  // timing experiments (FTKCU_WS_EXP), never set in production
 };
 
 template <bool kCore>
@@ -92,6 +94,28 @@ enum : int {
   B_AFULL = 27,      // core: A rows copied to TMEM
   B_DEMPTY = 28,     // core: G GEMM done with the D tile
 };
+
+// Round-to-nearest for an operand the tensor core will read as tf32: it
+// ignores the low 13 mantissa bits, so adding half an ulp of tf32 to the bit
+// pattern turns its truncation into rounding (ties away from zero).
+__device__ __forceinline__ uint32_t tf32_rn_bits(float x) { return __float_as_uint(x) + 0x1000u; }
+
+// x_hat = sum_r C0 C1 C2 over all 32 columns of this row: the warp's own
+// column half c[][] plus the other half, loaded and consumed here.
+__device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)[kN][16]) {
+  uint32_t o0[16], o1[16], o2[16];
+  tmem_ld16(tcol_other, o0);
+  tmem_ld16(tcol_other + kW, o1);
+  tmem_ld16(tcol_other + 2 * kW, o2);
+  tmem_wait_ld();
+  float x = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    x = fmaf(c[0][i], c[1][i] * c[2][i], x);
+    x = fmaf(__uint_as_float(o0[i]), __uint_as_float(o1[i]) * __uint_as_float(o2[i]), x);
+  }
+  return x;
+}
 
 __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
@@ -184,6 +208,10 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
     mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
     mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
     const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+    if (p.exp & 2) {  // exp: no gathers (timing only)
+      if (lane == 0) mbar_arrive(&bars[B_FULL + s]);
+      continue;
+    }
     if (lane == 0) mbar_expect_tx(&bars[B_FULL + s], L::kSlot);
     __syncwarp();
     uint8_t* slot = sm + L::o_a + s * L::kSlot;
@@ -262,7 +290,6 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
     const int ew = warp - 2, q = warp & 3, h = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    float* xp = reinterpret_cast<float*>(sm + L::o_xp);
     // Split-tf32: this row's (half of the) factor rows minus their truncated
     // tf32 part, into TMEM for the lo x hi MMA.
     auto stage_lo = [&](int64_t k) {
@@ -321,10 +348,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
       }
       if (p.prec3 && k + 1 < nk) stage_lo(k + 1);
-      float part = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
-      xp[((k & 1) * 2 + h) * kRows + row] = part;
+      const float xhat = xhat_full(tl + b * 192 + (h ^ 1) * 16, c);
       t.slot = s;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
@@ -340,14 +364,11 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         }
       }
       const float xv = s_val[row];
-      named_bar(1 + q, 64);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);  // COO slot may be refilled
       if constexpr (kAtomic) {
-        __syncwarp();
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);  // slot k may be refilled
       }
-      const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
       t.ok = tile * kRows + row < p.nnz;
       t.resid = t.ok ? xv - xhat : 0.0f;
 #pragma unroll
@@ -356,7 +377,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float d = n == 0 ? c[1][i] * c[2][i] : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
-          v[i] = __float_as_uint(d);
+          v[i] = tf32_rn_bits(d);
         }
         tmem_st16(tl + b * 192 + 96 + n * kW + h * 16, v);
       }
@@ -465,23 +486,24 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idc = idesc_tf32(128, kW, 0, 0);
-      constexpr uint32_t idg = idesc_tf32(128, kW, 1, 1);
+      constexpr uint32_t idg = idesc_tf32(128, kN * kW, 1, 1);  // all modes' D at once
       const uint32_t bt = smem_u32(sm + L::o_bt), btl = smem_u32(sm + L::o_btlo);
       const uint32_t d0 = smem_u32(sm + L::o_d);
       auto issue_g = [&](int64_t k) {
         const int s = (int)(k % kS);
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
         tc_after();
+        // G[j'][n' R + r] += sum_t A[t][j'] (r D_n')[t][r]: one N = 96 MMA per
+        // 8 nonzeros; only the diagonal blocks n' = mode(j') are read back.
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
-#pragma unroll
-        for (int n = 0; n < kN; ++n)
+        const uint64_t da = sdesc_l(a0, kModeTile, 512, 1);
+        const uint64_t dd = sdesc_l(d0, kModeTile, 512, 1);
 #pragma unroll 4
-          for (int ks = 0; ks < kRows / 8; ++ks)
-            mma_ss(tmem + kG + n * kW, sdesc_l(a0 + ks * 1024, kModeTile, 512, 1),
-                   sdesc_l(d0 + n * kModeTile + ks * 1024, kModeTile, 512, 1), idg,
-                   (k > 0 || ks > 0) ? 1u : 0u);
+        for (int ks = 0; ks < kRows / 8; ++ks)
+          mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
+                 (k > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&bars[B_DEMPTY]);
-        mma_commit(&bars[B_EMPTY + s]);
+        if (!(p.exp & 1)) mma_commit(&bars[B_EMPTY + s]);
       };
       for (int64_t k = 0; k < nk; ++k) {
         const int b = (int)(k & 1);
@@ -500,6 +522,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
             }
           }
         mma_commit(&bars[B_CFULL + b]);
+        if (p.exp & 1) mma_commit(&bars[B_EMPTY + (int)(k % kS)]);  // exp: slot freed after C
         if (k >= 1) issue_g(k - 1);
       }
       if (nk >= 1) issue_g(nk - 1);
@@ -508,7 +531,6 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
     const int ew = warp - 2, q = warp & 3, h = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    float* xp = reinterpret_cast<float*>(sm + L::o_xp);
     // Own row (half h of each mode) -> TMEM: the smem tile is in the MN-major
     // layout of the G GEMM, which the K-major C GEMM cannot read.
     auto stage_a = [&](int64_t k) {
@@ -527,14 +549,18 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
           v[q4 * 4 + 2] = __float_as_uint(x.z);
           v[q4 * 4 + 3] = __float_as_uint(x.w);
         }
-        tmem_st16(tl + kAhi + n * kW + h * 16, v);
-        if (p.prec3) {
+        if (p.prec3) {  // exact split: hi = what the tensor core reads, lo = rest
+          tmem_st16(tl + kAhi + n * kW + h * 16, v);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float x = __uint_as_float(v[i]);
             v[i] = __float_as_uint(x - tf32_trunc(x));
           }
           tmem_st16(tl + kAlo + n * kW + h * 16, v);
+        } else {  // single pass: round to nearest instead of truncating
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += 0x1000u;
+          tmem_st16(tl + kAhi + n * kW + h * 16, v);
         }
       }
       tmem_wait_st();
@@ -559,13 +585,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
 #pragma unroll
         for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
       }
+      const float xhat = xhat_full(tl + b * 96 + (h ^ 1) * 16, c);
       if (k + 1 < nk) stage_a(k + 1);  // C(k) is complete: A rows TMEM is free
-      float part = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
-      xp[((k & 1) * 2 + h) * kRows + row] = part;
-      named_bar(1 + q, 64);
-      const float xhat = xp[((k & 1) * 2 + 0) * kRows + row] + xp[((k & 1) * 2 + 1) * kRows + row];
       const bool ok = tile * kRows + row < p.nnz;
       const float resid = ok ? s_val[row] - xhat : 0.0f;
       __syncwarp();
@@ -578,10 +599,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
           float4 d;
           const int i = q4 * 4;
 #define FTK_D(ii) (n == 0 ? c[1][ii] * c[2][ii] : (n == 1 ? c[0][ii] * c[2][ii] : c[0][ii] * c[1][ii]))
-          d.x = tf32_rna(resid * FTK_D(i + 0));
-          d.y = tf32_rna(resid * FTK_D(i + 1));
-          d.z = tf32_rna(resid * FTK_D(i + 2));
-          d.w = tf32_rna(resid * FTK_D(i + 3));
+          d.x = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 0)));
+          d.y = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 1)));
+          d.z = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 2)));
+          d.w = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 3)));
 #undef FTK_D
           *reinterpret_cast<float4*>(sm + L::o_d + n * kModeTile +
                                      swz32(row, (h * 16 + i) * 4)) = d;
@@ -672,6 +693,7 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   p.reg = reg;
   p.atomic_update = atomic_update;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
+  if (const char* e = std::getenv("FTKCU_WS_EXP")) p.exp = std::atoi(e);
   if (p.ntiles == 0) return cudaSuccess;
   const int bytes = (int)WsLayout<false>::bytes;
   auto kern = atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>;
@@ -688,6 +710,7 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   WsParams p{};
   if (!make_params(p, v, dims, mul, add, true)) return cudaErrorNotSupported;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
+  if (const char* e = std::getenv("FTKCU_WS_EXP")) p.exp = std::atoi(e);
   const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
   const int len = kN * kW * kW;
   if (grid < 1) return cudaErrorInvalidValue;

@@ -212,9 +212,10 @@ def init_for(t, j, r, seed=9):
 
 PRECS = [eng.PREC_FP32, eng.PREC_TF32, eng.PREC_3XTF32]
 # Gradient tolerance per precision: fp32 = reassociation only; 3xtf32 =
-# split-tf32 x_hat (~5e-4 observed); tf32 = truncated A operand biases x_hat
-# and therefore every residual of this heavily cancelling sum (~4e-2).
-GRAD_TOL = {eng.PREC_FP32: 2e-5, eng.PREC_3XTF32: 3e-3, eng.PREC_TF32: 1e-1}
+# split-tf32 C = A B (~7e-4 observed); tf32 = one pass with operands rounded
+# to nearest where the engine writes them (~1.5e-3 observed on this heavily
+# cancelling residual-weighted sum; truncation instead gave 4e-2).
+GRAD_TOL = {eng.PREC_FP32: 2e-5, eng.PREC_3XTF32: 3e-3, eng.PREC_TF32: 1e-2}
 
 
 @pytest.mark.parametrize("prec", PRECS)
