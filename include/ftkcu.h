@@ -117,6 +117,15 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm,
                      int32_t M, float lr_b, float reg_b, int mode,
                      uint64_t seed, float* grad_out, double* ms);
 
+/* DSGD strata support.  Declares that the uploaded entries are sorted into
+ * cells: entries [cell_offsets[c], cell_offsets[c+1]) form cell c.  The
+ * Hogwild stream then shuffles and tiles every cell separately. */
+int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offsets,
+                           int ncells);
+/* Hogwild factor sweep over one cell only (one DSGD stratum on this rank). */
+int ftkcu_factor_phase_cell(ftkcu_session* s, int slot, int cell, float lr_a,
+                            float reg_a, uint64_t seed, double* ms);
+
 /* fp64 metrics of the resident model on tensor `slot`
  * (ftk::loss / ftk::evaluate, evaluation.cpp:36-72, predict_element
  * model.cpp:70-92).  out[0] = sum (x - xhat)^2, out[1] = sum |x - xhat|,
@@ -144,8 +153,22 @@ int ftkcu_comm_unique_id(uint8_t* id128);
 int ftkcu_comm_init(ftkcu_session* s, const uint8_t* id128, int rank,
                     int world);
 /* In-place sum all-reduce of a device-resident core gradient, exposed for
- * tests; the DSGD epoch calls it internally once per core phase. */
+ * tests; ftkcu_core_phase calls it internally once a communicator is set. */
 int ftkcu_comm_allreduce_grad(ftkcu_session* s);
+/* DSGD block rotation: send factor rows [send_row0, +send_nrows) of mode
+ * `mode` to rank dst while receiving rows [recv_row0, +recv_nrows) from src
+ * (one NCCL group on the session stream, no host round trip). */
+int ftkcu_comm_sendrecv_rows(ftkcu_session* s, int mode, int64_t send_row0,
+                             int64_t send_nrows, int dst, int64_t recv_row0,
+                             int64_t recv_nrows, int src);
+/* Every rank r broadcasts its rows [row_off[r], row_off[r+1]) of `mode`
+ * (all-gather of the owned blocks after a DSGD factor sweep). */
+int ftkcu_comm_bcast_rows(ftkcu_session* s, int mode, const int64_t* row_off,
+                          int nblocks);
+/* Sum all-reduce of host fp64 values (metrics partials). */
+int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n);
+/* Waits for all work queued on the session stream. */
+int ftkcu_stream_sync(ftkcu_session* s);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,9 @@ EXPORTS = (
     "ftkcu_tensor_release", "ftkcu_tensor_nnz", "ftkcu_model_upload",
     "ftkcu_model_download", "ftkcu_factor_phase", "ftkcu_core_phase", "ftkcu_eval",
     "ftkcu_batch_probe", "ftkcu_comm_unique_id", "ftkcu_comm_init",
-    "ftkcu_comm_allreduce_grad",
+    "ftkcu_comm_allreduce_grad", "ftkcu_tensor_set_cells", "ftkcu_factor_phase_cell",
+    "ftkcu_comm_sendrecv_rows", "ftkcu_comm_bcast_rows", "ftkcu_comm_allreduce_f64",
+    "ftkcu_stream_sync",
 )
 
 
@@ -86,6 +88,14 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_comm_unique_id.argtypes = [C.c_char_p]
     L.ftkcu_comm_init.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
     L.ftkcu_comm_allreduce_grad.argtypes = [C.c_void_p]
+    L.ftkcu_tensor_set_cells.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int]
+    L.ftkcu_factor_phase_cell.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_float,
+                                          C.c_uint64, _f64p]
+    L.ftkcu_comm_sendrecv_rows.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int,
+                                           C.c_int64, C.c_int64, C.c_int]
+    L.ftkcu_comm_bcast_rows.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int]
+    L.ftkcu_comm_allreduce_f64.argtypes = [C.c_void_p, _f64p, C.c_int]
+    L.ftkcu_stream_sync.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -240,3 +250,31 @@ class Session:
 
     def comm_init(self, uid: bytes, rank: int, world: int):
         self._ck(self.lib.ftkcu_comm_init(self.h, uid, rank, world))
+
+    # -- DSGD strata (paper_2404_10087_b200/dsgd.py drives these)
+    def set_cells(self, slot, cell_offsets):
+        off = np.ascontiguousarray(cell_offsets, np.int64)
+        self._ck(self.lib.ftkcu_tensor_set_cells(self.h, slot, _p(off, _i64p), off.size - 1))
+
+    def factor_phase_cell(self, slot, cell, lr_a=1e-3, reg_a=1e-4, seed=0, timed=False):
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_factor_phase_cell(self.h, slot, cell, lr_a, reg_a,
+                                                  C.c_uint64(seed & (2**64 - 1)),
+                                                  C.byref(ms) if timed else None))
+        return ms.value
+
+    def sendrecv_rows(self, mode, send_row0, send_nrows, dst, recv_row0, recv_nrows, src):
+        self._ck(self.lib.ftkcu_comm_sendrecv_rows(self.h, mode, send_row0, send_nrows, dst,
+                                                   recv_row0, recv_nrows, src))
+
+    def bcast_rows(self, mode, row_off):
+        off = np.ascontiguousarray(row_off, np.int64)
+        self._ck(self.lib.ftkcu_comm_bcast_rows(self.h, mode, _p(off, _i64p), off.size - 1))
+
+    def allreduce_f64(self, values):
+        v = np.ascontiguousarray(values, np.float64).copy()
+        self._ck(self.lib.ftkcu_comm_allreduce_f64(self.h, _p(v, _f64p), v.size))
+        return v
+
+    def sync(self):
+        self._ck(self.lib.ftkcu_stream_sync(self.h))

@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "../../include/ftkcu.h"
 
@@ -31,10 +32,18 @@ struct DevTensor {
   int64_t nnz = 0;
   int32_t* idx[kMaxOrder] = {};  // storage order SoA
   float* vals = nullptr;
-  // Hogwild (shuffled) copy, built lazily by the tiler.
+  // Cells (DSGD strata blocks): entries [cell_off[c], cell_off[c+1]) in
+  // storage order.  Empty = one cell holding everything.
+  std::vector<int64_t> cell_off;
+  // Hogwild stream, built lazily by the tiler: every cell shuffled and padded
+  // to whole tiles; cell c owns physical tiles [cell_tile[c], cell_tile[c+1]).
   bool shuffled = false;
   int32_t* sidx[kMaxOrder] = {};
   float* svals = nullptr;
+  int32_t* tile_rows = nullptr;      // valid rows per physical tile
+  std::vector<int64_t> cell_tile;
+  int64_t stream_tiles = 0;
+  int64_t stream_cap = 0;            // allocated tiles
 };
 
 struct DevModel {
@@ -66,6 +75,10 @@ struct KView {
   const int32_t* idx[kMaxOrder];
   const float* vals;
   int64_t nnz;
+  // Hogwild stream range: physical tiles [tile_base, tile_base + ntiles),
+  // tile_rows[p] valid rows of physical tile p (the rest is padding).
+  const int32_t* tile_rows;
+  int64_t tile_base, ntiles;
 };
 
 // Optional per-batch debug outputs of the deterministic kernels (device
@@ -103,6 +116,11 @@ cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void* scratch, size_t scratch_bytes,
                            cudaStream_t st);
+// physical tile of range position t under the per-epoch affine permutation
+__host__ __device__ inline int64_t stream_tile(const KView& v, int64_t t, int64_t mul,
+                                               int64_t add) {
+  return v.tile_base + (t * mul + add) % v.ntiles;
+}
 size_t shuffle_scratch_bytes(int64_t nnz);
 constexpr int kHogTile = 128;  // nonzeros per Hogwild tile
 

@@ -35,6 +35,7 @@ struct ftkcu_session {
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
   int64_t launches = 0;  // kernels launched by this session (for benches)
 };
 
@@ -163,6 +164,9 @@ KView make_view(const ftkcu_session* s, const DevTensor& t, bool shuffled) {
   }
   v.vals = shuffled ? t.svals : t.vals;
   v.nnz = t.nnz;
+  v.tile_rows = shuffled ? t.tile_rows : nullptr;
+  v.tile_base = 0;
+  v.ntiles = shuffled ? t.stream_tiles : 0;
   return v;
 }
 
@@ -326,6 +330,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_hog_update = value;
   } else if (k == "verbose") {
     s->opt_verbose = value;
+  } else if (k == "global_nnz") {
+    s->global_nnz = value;
   } else if (k == "shuffle_seed") {
     s->opt_shuffle_seed = value;
     for (auto& t : s->slots) t.shuffled = false;
@@ -475,8 +481,9 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
   return FTKCU_OK;
 }
 
-int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_a,
-                       float reg_a, int mode, uint64_t seed, double* ms) {
+static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
+                             float lr_a, float reg_a, int mode, uint64_t seed, int cell,
+                             double* ms) {
   int rc = bind(s);
   if (rc) return rc;
   if ((rc = check_ready(s, slot))) return rc;
@@ -497,10 +504,16 @@ int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t 
   if (mode != FTKCU_MODE_HOGWILD) return fail(s, FTKCU_ERR_ARG, "unknown mode %d", mode);
   if ((rc = prepare_stream(s, t, perm))) return rc;
   KView v = make_view(s, t, true);
-  int64_t ntiles = (t.nnz + kHogTile - 1) / kHogTile, mul = 1, add = 0;
-  if (!perm) tile_perm(seed, ntiles, &mul, &add);
+  if (cell >= 0) {
+    if (cell + 1 >= (int)t.cell_tile.size())
+      return fail(s, FTKCU_ERR_ARG, "cell %d out of range", cell);
+    v.tile_base = t.cell_tile[cell];
+    v.ntiles = t.cell_tile[cell + 1] - t.cell_tile[cell];
+  }
+  int64_t mul = 1, add = 0;
+  if (!perm) tile_perm(seed, v.ntiles, &mul, &add);
   CK(cudaEventRecord(s->ev0, s->stream));
-  if (t.nnz > 0) {
+  if (v.ntiles > 0) {
     if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
       CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                           (int)s->opt_hog_update, s->stream));
@@ -514,6 +527,32 @@ int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t 
     s->launches += 1;
   }
   return finish_timing(s, ms);
+}
+
+int ftkcu_factor_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_a,
+                       float reg_a, int mode, uint64_t seed, double* ms) {
+  return factor_phase_impl(s, slot, perm, M, lr_a, reg_a, mode, seed, -1, ms);
+}
+
+int ftkcu_factor_phase_cell(ftkcu_session* s, int slot, int cell, float lr_a, float reg_a,
+                            uint64_t seed, double* ms) {
+  if (cell < 0) return fail(s, FTKCU_ERR_ARG, "cell must be >= 0");
+  return factor_phase_impl(s, slot, nullptr, 16, lr_a, reg_a, FTKCU_MODE_HOGWILD, seed, cell, ms);
+}
+
+int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offsets, int ncells) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  DevTensor& t = s->slots[slot];
+  if (ncells < 1 || !cell_offsets) return fail(s, FTKCU_ERR_ARG, "need at least one cell");
+  if (cell_offsets[0] != 0 || cell_offsets[ncells] != t.nnz)
+    return fail(s, FTKCU_ERR_ARG, "cell offsets must span [0, nnz]");
+  for (int c = 0; c < ncells; ++c)
+    if (cell_offsets[c + 1] < cell_offsets[c]) return fail(s, FTKCU_ERR_ARG, "cell offsets not sorted");
+  t.cell_off.assign(cell_offsets, cell_offsets + ncells + 1);
+  t.shuffled = false;
+  return FTKCU_OK;
 }
 
 int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_b,
@@ -537,8 +576,8 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
   } else if (mode == FTKCU_MODE_HOGWILD) {
     if ((rc = prepare_stream(s, t, perm))) return rc;
     v = make_view(s, t, true);
-    int64_t ntiles = (t.nnz + kHogTile - 1) / kHogTile, mul = 1, add = 0;
-    if (!perm) tile_perm(seed ^ 0xc0e5ull, ntiles, &mul, &add);
+    int64_t mul = 1, add = 0;
+    if (!perm) tile_perm(seed ^ 0xc0e5ull, v.ntiles, &mul, &add);
     const size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
     if ((rc = ensure_scratch(s, need))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -558,6 +597,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
   }
   if (s->comm && s->world > 1) {
     NK(ncclAllReduce(s->grad, s->grad, glen, ncclFloat, ncclSum, s->comm, s->stream));
+    v.nnz = s->global_nnz > 0 ? s->global_nnz : v.nnz;  // |Omega| over all ranks
   }
   CK(launch_apply_core(v, s->grad, lr_b, reg_b, s->stream));
   s->launches += 1;
@@ -668,6 +708,73 @@ int ftkcu_comm_init(ftkcu_session* s, const uint8_t* id128, int rank, int world)
   NK(ncclCommInitRank(&s->comm, world, id, rank));
   s->rank = rank;
   s->world = world;
+  return FTKCU_OK;
+}
+
+static int rows_of(ftkcu_session* s, int mode, int64_t row0, int64_t nrows, float** ptr,
+                   size_t* count) {
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  const DevModel& m = s->model;
+  if (mode < 0 || mode >= m.order) return fail(s, FTKCU_ERR_ARG, "mode %d out of range", mode);
+  if (row0 < 0 || nrows < 0 || row0 + nrows > m.dims[mode])
+    return fail(s, FTKCU_ERR_ARG, "row range out of bounds");
+  *ptr = m.a[mode] + row0 * m.ranks[mode];
+  *count = (size_t)nrows * m.ranks[mode];
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_sendrecv_rows(ftkcu_session* s, int mode, int64_t send_row0, int64_t send_nrows,
+                             int dst, int64_t recv_row0, int64_t recv_nrows, int src) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->comm) return fail(s, FTKCU_ERR_STATE, "no communicator");
+  float *sp, *rp;
+  size_t sc, rcn;
+  if ((rc = rows_of(s, mode, send_row0, send_nrows, &sp, &sc))) return rc;
+  if ((rc = rows_of(s, mode, recv_row0, recv_nrows, &rp, &rcn))) return rc;
+  NK(ncclGroupStart());
+  if (sc) NK(ncclSend(sp, sc, ncclFloat, dst, s->comm, s->stream));
+  if (rcn) NK(ncclRecv(rp, rcn, ncclFloat, src, s->comm, s->stream));
+  NK(ncclGroupEnd());
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_bcast_rows(ftkcu_session* s, int mode, const int64_t* row_off, int nblocks) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->comm) return fail(s, FTKCU_ERR_STATE, "no communicator");
+  if (nblocks != s->world) return fail(s, FTKCU_ERR_ARG, "need one block per rank");
+  NK(ncclGroupStart());
+  for (int r = 0; r < nblocks; ++r) {
+    float* p;
+    size_t c;
+    if ((rc = rows_of(s, mode, row_off[r], row_off[r + 1] - row_off[r], &p, &c))) {
+      ncclGroupEnd();
+      return rc;
+    }
+    if (c) NK(ncclBroadcast(p, p, c, ncclFloat, r, s->comm, s->stream));
+  }
+  NK(ncclGroupEnd());
+  return FTKCU_OK;
+}
+
+int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->comm) return fail(s, FTKCU_ERR_STATE, "no communicator");
+  if ((rc = ensure_scratch(s, sizeof(double) * (n > 0 ? n : 1)))) return rc;
+  double* d = static_cast<double*>(s->scratch);
+  CK(cudaMemcpyAsync(d, host_inout, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+  NK(ncclAllReduce(d, d, n, ncclDouble, ncclSum, s->comm, s->stream));
+  CK(cudaMemcpyAsync(host_inout, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return FTKCU_OK;
+}
+
+int ftkcu_stream_sync(ftkcu_session* s) {
+  int rc = bind(s);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s->stream));
   return FTKCU_OK;
 }
 

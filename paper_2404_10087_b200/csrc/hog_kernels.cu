@@ -137,7 +137,7 @@ __device__ __forceinline__ float btval(const KView& v, const HogLayout& L, const
 // per-warp scratch `w`: a rows at w[g*sum_j + aoff[n] + j], C at wc, D at wd,
 // residuals at wres.
 __device__ void front(const KView& v, const HogLayout& L, const float* sm, float* w,
-                      int64_t e0, int32_t (&rows)[kG][kMaxOrder]) {
+                      int64_t e0, int nvalid, int32_t (&rows)[kG][kMaxOrder]) {
   const int lane = threadIdx.x & 31;
   const int N = v.order, r = v.r, sj = L.sum_j;
   float* wa = w;
@@ -150,8 +150,8 @@ __device__ void front(const KView& v, const HogLayout& L, const float* sm, float
     int32_t my = 0;
     float xv = 0.0f;
     const int g = lane / N, n = lane - g * N;
-    if (g < kG && e0 + g < v.nnz) my = v.idx[n][e0 + g];
-    if (lane < kG && e0 + lane < v.nnz) xv = v.vals[e0 + lane];
+    if (g < kG && g < nvalid) my = v.idx[n][e0 + g];
+    if (lane < kG && lane < nvalid) xv = v.vals[e0 + lane];
 #pragma unroll
     for (int gg = 0; gg < kG; ++gg)
 #pragma unroll
@@ -162,7 +162,7 @@ __device__ void front(const KView& v, const HogLayout& L, const float* sm, float
   // stage a rows (coalesced: one warp reads whole rows)
 #pragma unroll
   for (int g = 0; g < kG; ++g) {
-    const bool ok = e0 + g < v.nnz;
+    const bool ok = g < nvalid;
     for (int n = 0; n < N; ++n) {
       const int jn = v.j[n];
       const float* src = v.a[n] + (size_t)rows[g][n] * jn;
@@ -208,14 +208,14 @@ __device__ void front(const KView& v, const HogLayout& L, const float* sm, float
     float s = part[g];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) wres[g] = (e0 + g < v.nnz) ? wx[g] - s : 0.0f;
+    if (lane == 0) wres[g] = (g < nvalid) ? wx[g] - s : 0.0f;
   }
   __syncwarp();
 }
 
 __global__ void __launch_bounds__(kHogThreads)
-hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
-                  float reg, int atomic_update) {
+hog_factor_kernel(KView v, int64_t tmul, int64_t tadd, float lr, float reg,
+                  int atomic_update) {
   extern __shared__ float sm[];
   const int warps = blockDim.x / 32;
   const HogLayout L = hog_layout(v, false, warps);
@@ -229,11 +229,12 @@ hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
   const float* wres = wd + kG * N * r + kG;
   const int64_t gw = (int64_t)blockIdx.x * warps + wid, nw = (int64_t)gridDim.x * warps;
   int32_t rows[kG][kMaxOrder];
-  for (int64_t t = gw; t < ntiles; t += nw) {
-    const int64_t tile = (t * tmul + tadd) % ntiles;
+  for (int64_t t = gw; t < v.ntiles; t += nw) {
+    const int64_t tile = stream_tile(v, t, tmul, tadd);
     const int64_t base = tile * kHogTile;
-    for (int g0 = 0; g0 < kHogTile && base + g0 < v.nnz; g0 += kG) {
-      front(v, L, sm, w, base + g0, rows);
+    const int valid = v.tile_rows[tile];
+    for (int g0 = 0; g0 < valid; g0 += kG) {
+      front(v, L, sm, w, base + g0, valid - g0, rows);
       // U^(n)[g][j] = sum_c D[g][n][c] B_n[j][c]; a += lr (r u - reg a)
       for (int n = 0; n < N; ++n) {
         const int jn = v.j[n];
@@ -248,7 +249,7 @@ hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
           }
 #pragma unroll
           for (int g = 0; g < kG; ++g) {
-            if (base + g0 + g < v.nnz) {
+            if (g0 + g < valid) {
               const float a = wa[g * sj + L.aoff[n] + j];
               const float step = lr * (wres[g] * u[g] - reg * a);
               float* dst = v.a[n] + (size_t)rows[g][n] * jn + j;
@@ -267,8 +268,7 @@ hog_factor_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd, float lr,
 }
 
 __global__ void __launch_bounds__(kHogThreads)
-hog_core_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd,
-                float* __restrict__ partials) {
+hog_core_kernel(KView v, int64_t tmul, int64_t tadd, float* __restrict__ partials) {
   extern __shared__ float sm[];
   const int warps = blockDim.x / 32;
   const HogLayout L = hog_layout(v, true, warps);
@@ -284,11 +284,12 @@ hog_core_kernel(KView v, int64_t ntiles, int64_t tmul, int64_t tadd,
   const float* wres = wd + kG * N * r + kG;
   const int64_t gw = (int64_t)blockIdx.x * warps + wid, nw = (int64_t)gridDim.x * warps;
   int32_t rows[kG][kMaxOrder];
-  for (int64_t t = gw; t < ntiles; t += nw) {
-    const int64_t tile = (t * tmul + tadd) % ntiles;
+  for (int64_t t = gw; t < v.ntiles; t += nw) {
+    const int64_t tile = stream_tile(v, t, tmul, tadd);
     const int64_t base = tile * kHogTile;
-    for (int g0 = 0; g0 < kHogTile && base + g0 < v.nnz; g0 += kG) {
-      front(v, L, sm, w, base + g0, rows);
+    const int valid = v.tile_rows[tile];
+    for (int g0 = 0; g0 < valid; g0 += kG) {
+      front(v, L, sm, w, base + g0, valid - g0, rows);
       // grad_n[j][c] += sum_g r_g a_g[j] D_g[c]
       int off = 0;
       for (int n = 0; n < N; ++n) {
@@ -336,38 +337,74 @@ size_t shuffle_scratch_bytes(int64_t) { return 0; }
 
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void*, size_t, cudaStream_t st) {
+  // Cells: every cell is shuffled on its own and padded to whole tiles
+  // (index 0, value 0, masked by tile_rows), so a DSGD stratum is a
+  // contiguous physical tile range.
+  std::vector<int64_t> off = t.cell_off;
+  if (off.empty() || d_perm) off = {0, t.nnz};
+  const int ncell = (int)off.size() - 1;
+  std::vector<int64_t> ctile(ncell + 1, 0);
+  for (int c = 0; c < ncell; ++c)
+    ctile[c + 1] = ctile[c] + (off[c + 1] - off[c] + kHogTile - 1) / kHogTile;
+  const int64_t tiles = ctile[ncell];
   cudaError_t e;
-  // Padded to whole tiles (index 0, value 0) so tile loads never run past
-  // the end; the sweeps mask rows >= nnz.
-  const int64_t padded = ((t.nnz + kHogTile - 1) / kHogTile) * kHogTile;
-  if (!t.svals) {
-    const size_t cnt = padded > 0 ? (size_t)padded : 1;
+  if (tiles > t.stream_cap || !t.svals) {
     for (int n = 0; n < t.order; ++n) {
-      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * cnt);
-      if (e != cudaSuccess) return e;
-      e = cudaMemsetAsync(t.sidx[n], 0, sizeof(int32_t) * cnt, st);
+      if (t.sidx[n]) cudaFree(t.sidx[n]);
+      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * kHogTile * (tiles > 0 ? tiles : 1));
       if (e != cudaSuccess) return e;
     }
-    e = cudaMalloc(&t.svals, sizeof(float) * cnt);
+    if (t.svals) cudaFree(t.svals);
+    if (t.tile_rows) cudaFree(t.tile_rows);
+    e = cudaMalloc(&t.svals, sizeof(float) * kHogTile * (tiles > 0 ? tiles : 1));
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(t.svals, 0, sizeof(float) * cnt, st);
+    e = cudaMalloc(&t.tile_rows, sizeof(int32_t) * (tiles > 0 ? tiles : 1));
     if (e != cudaSuccess) return e;
+    t.stream_cap = tiles;
   }
-  ShuffleView v{};
-  v.order = t.order;
   for (int n = 0; n < t.order; ++n) {
-    v.src_idx[n] = t.idx[n];
-    v.dst_idx[n] = t.sidx[n];
+    e = cudaMemsetAsync(t.sidx[n], 0, sizeof(int32_t) * kHogTile * tiles, st);
+    if (e != cudaSuccess) return e;
   }
-  v.src_vals = t.vals;
-  v.dst_vals = t.svals;
-  v.nnz = t.nnz;
-  int bits = 2;
-  while ((1ll << bits) < t.nnz) bits += 2;
-  if (t.nnz > 0)
-    shuffle_kernel<<<num_sms() * 8, 256, 0, st>>>(v, d_perm, bits, seed);
+  e = cudaMemsetAsync(t.svals, 0, sizeof(float) * kHogTile * tiles, st);
+  if (e != cudaSuccess) return e;
+  std::vector<int32_t> rows(tiles > 0 ? tiles : 1);
+  for (int c = 0; c < ncell; ++c) {
+    const int64_t n = off[c + 1] - off[c];
+    for (int64_t k = ctile[c]; k < ctile[c + 1]; ++k) {
+      const int64_t left = n - (k - ctile[c]) * kHogTile;
+      rows[k] = (int32_t)(left < kHogTile ? left : kHogTile);
+    }
+    if (n == 0) continue;
+    ShuffleView v{};
+    v.order = t.order;
+    for (int i = 0; i < t.order; ++i) {
+      v.src_idx[i] = t.idx[i] + off[c];
+      v.dst_idx[i] = t.sidx[i] + ctile[c] * kHogTile;
+    }
+    v.src_vals = t.vals + off[c];
+    v.dst_vals = t.svals + ctile[c] * kHogTile;
+    v.nnz = n;
+    int bits = 2;
+    while ((1ll << bits) < n) bits += 2;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    shuffle_kernel<<<(int)blocks, 256, 0, st>>>(v, d_perm, bits,
+                                                 seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1)));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (tiles > 0) {
+    e = cudaMemcpyAsync(t.tile_rows, rows.data(), sizeof(int32_t) * tiles, cudaMemcpyHostToDevice,
+                        st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);  // `rows` is a host temporary
+    if (e != cudaSuccess) return e;
+  }
+  t.cell_tile = ctile;
+  t.stream_tiles = tiles;
   t.shuffled = true;
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
@@ -379,10 +416,9 @@ cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add
   cudaError_t e = cudaFuncSetAttribute(hog_factor_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  const int64_t ntiles = (v.nnz + kHogTile - 1) / kHogTile;
-  if (ntiles == 0) return cudaSuccess;
+  if (v.ntiles == 0) return cudaSuccess;
   hog_factor_kernel<<<hog_grid(blocks_per_sm), kHogThreads, bytes, st>>>(
-      v, ntiles, tile_mul, tile_add, lr_a, reg_a, atomic_update);
+      v, tile_mul, tile_add, lr_a, reg_a, atomic_update);
   return cudaGetLastError();
 }
 
@@ -397,8 +433,7 @@ cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
   cudaError_t e = cudaFuncSetAttribute(hog_core_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  const int64_t ntiles = (v.nnz + kHogTile - 1) / kHogTile;
-  hog_core_kernel<<<grid, kHogThreads, bytes, st>>>(v, ntiles, tile_mul, tile_add, scratch);
+  hog_core_kernel<<<grid, kHogThreads, bytes, st>>>(v, tile_mul, tile_add, scratch);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int len = (int)L.acc_floats;

@@ -85,7 +85,8 @@ struct TcParams {
   const float* vals;
   float* a[kMaxOrder];
   const float* b[kMaxOrder];
-  int64_t nnz, ntiles, tmul, tadd;
+  int64_t nnz, ntiles, tmul, tadd, tile_base;
+  const int32_t* tile_rows;
   float lr, reg;
   int atomic_update;
   int prec3;  // split-tf32 (hi*hi + hi*lo + lo*hi) for the C = A B contraction
@@ -124,7 +125,7 @@ template <int N>
 __device__ __forceinline__ Rec<N> load_rec(const TcParams& p, int64_t tile) {
   Rec<N> r;
   const int64_t e = tile * kTileRows + threadIdx.x;
-  r.ok = e < p.nnz;
+  r.ok = (int)threadIdx.x < p.tile_rows[tile];
 #pragma unroll
   for (int n = 0; n < N; ++n) r.idx[n] = r.ok ? __ldcs(p.idx[n] + e) : 0;
   r.x = r.ok ? __ldcs(p.vals + e) : 0.0f;
@@ -133,7 +134,7 @@ __device__ __forceinline__ Rec<N> load_rec(const TcParams& p, int64_t tile) {
 
 __device__ __forceinline__ int64_t phys_tile(const TcParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
-  return (t * p.tmul + p.tadd) % p.ntiles;
+  return p.tile_base + (t * p.tmul + p.tadd) % p.ntiles;
 }
 
 // Stages one tile into `slot`: COO record to smem, factor rows by cp.async
@@ -616,7 +617,9 @@ TcParams make_params(const KView& v, int64_t mul, int64_t add) {
   }
   p.vals = v.vals;
   p.nnz = v.nnz;
-  p.ntiles = (v.nnz + kTileRows - 1) / kTileRows;
+  p.ntiles = v.ntiles;
+  p.tile_base = v.tile_base;
+  p.tile_rows = v.tile_rows;
   p.tmul = mul;
   p.tadd = add;
   return p;

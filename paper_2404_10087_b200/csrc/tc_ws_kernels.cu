@@ -48,7 +48,8 @@ struct __align__(64) WsParams {
   const float* vals;
   float* a[kN];
   const float* b[kN];
-  int64_t nnz, ntiles, tmul, tadd;
+  int64_t nnz, ntiles, tmul, tadd, tile_base;
+  const int32_t* tile_rows;
   float lr, reg;
   int atomic_update, prec3;
   float* partials;
@@ -119,7 +120,7 @@ __device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)
 
 __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
-  return (t * p.tmul + p.tadd) % p.ntiles;
+  return p.tile_base + (t * p.tmul + p.tadd) % p.ntiles;
 }
 
 template <bool kCore>
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if constexpr (kAtomic) {
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);  // slot k may be refilled
       }
-      t.ok = tile * kRows + row < p.nnz;
+      t.ok = row < __ldg(p.tile_rows + tile);
       t.resid = t.ok ? xv - xhat : 0.0f;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
       }
       const float xhat = xhat_full(tl + b * 96 + (h ^ 1) * 16, c);
       if (k + 1 < nk) stage_a(k + 1);  // C(k) is complete: A rows TMEM is free
-      const bool ok = tile * kRows + row < p.nnz;
+      const bool ok = row < __ldg(p.tile_rows + tile);
       const float resid = ok ? s_val[row] - xhat : 0.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);
@@ -671,7 +672,9 @@ bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, 
   }
   p.vals = v.vals;
   p.nnz = v.nnz;
-  p.ntiles = (v.nnz + kRows - 1) / kRows;
+  p.ntiles = v.ntiles;
+  p.tile_base = v.tile_base;
+  p.tile_rows = v.tile_rows;
   p.tmul = mul;
   p.tadd = add;
   return true;

@@ -1,0 +1,240 @@
+"""DSGD stratified multi-GPU FastTuckerPlus epoch.
+
+The reference has no multi-device path: ``ftk::epoch_plus``
+(decomposition.cpp:623-705) runs one Hogwild factor sweep and one core sweep
+over all nonzeros on one host.  Across GPUs, two nonzeros that share an index
+in any mode conflict in the factor sweep, so the nonzeros are stratified:
+
+* every mode's index range is cut into P nnz-balanced blocks
+  (:func:`balanced_blocks`);
+* rank g permanently owns mode-1 block g and holds only the nonzeros with
+  ``i1`` in that block, bucketed into P*P cells by (mode-2 block, mode-3 block)
+  relative to g (:func:`local_cells`): local cell ``s*P + t`` holds the
+  nonzeros in blocks ``(g, (g+s) % P, (g+t) % P)``;
+* stratum (s, t) has every rank sweep its local cell ``s*P + t``.  Within a
+  stratum the P cells touch pairwise-disjoint A rows in every mode
+  (:func:`stratum_blocks`), so the per-rank Hogwild sweeps never conflict;
+* after each stratum the mode-3 block a rank just updated moves one rank down
+  the ring (g -> g-1) and the block it needs next arrives from g+1; after each
+  s-round the mode-2 block does the same.  One extra shift after the last
+  stratum leaves every rank holding the newest copy of its own block g, which
+  an all-gather (one broadcast per block) then replicates.  Mode-1 rows never
+  move during an epoch: only rank g reads or writes block g, in the factor
+  sweep, the core sweep and the evaluation alike; :meth:`DsgdTrainer.finalize`
+  gathers them once for the download;
+* the core sweep is data-parallel: every rank accumulates dB over its own
+  nonzeros, the sum is all-reduced (NCCL inside ``ftkcu_core_phase``) and every
+  rank applies the same update with |Omega| = the global nonzero count, so the
+  replicated B stays bit-identical across ranks.
+
+Semantics: the core phase equals the single-GPU one up to the summation order
+of dB; the factor phase visits the nonzeros in a different (stratified) order,
+so only RMSE parity with the reference applies.  The driver is
+backend-agnostic: :class:`EngineBackend` drives ``libftkcu.so`` (cells,
+``ftkcu_factor_phase_cell``, NCCL row exchange on the session stream, so a
+whole epoch is enqueued without a host sync), and ``tests/test_dsgd.py``
+drives the same schedule with the C oracle over ``gloo`` to prove the
+schedule conflict-free and the exchange exact.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import host
+
+
+def balanced_blocks(col: np.ndarray, dim: int, parts: int) -> np.ndarray:
+    """P+1 row offsets cutting [0, dim) into ``parts`` contiguous blocks with
+    about nnz/P nonzeros each (per-index counts, cut at the nnz quantiles)."""
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    counts = np.bincount(np.asarray(col, np.int64), minlength=dim)[:dim]
+    cum = np.cumsum(counts, dtype=np.int64)
+    total = int(cum[-1]) if dim else 0
+    off = np.zeros(parts + 1, np.int64)
+    for p in range(1, parts):
+        # first row whose prefix count reaches the p-th quantile
+        off[p] = int(np.searchsorted(cum, (total * p + parts - 1) // parts, side="left")) + 1
+    off[parts] = dim
+    off = np.minimum(np.maximum.accumulate(off), dim)
+    if dim >= parts:
+        # every block keeps at least one row so a shift never sends an empty range
+        for p in range(1, parts):
+            off[p] = min(max(off[p], off[p - 1] + 1), dim - (parts - p))
+    return off
+
+
+@dataclass
+class Layout:
+    """Block offsets per mode (P+1 each) for P ranks of an order-3 tensor."""
+
+    parts: int
+    dims: tuple
+    row_off: tuple  # per mode: np.ndarray[int64] of P+1 offsets
+
+    def block_of(self, mode: int, rows: np.ndarray) -> np.ndarray:
+        return np.searchsorted(self.row_off[mode], rows, side="right") - 1
+
+    def rows(self, mode: int, block: int) -> tuple[int, int]:
+        o = self.row_off[mode]
+        return int(o[block]), int(o[block + 1] - o[block])
+
+
+def make_layout(dims, idx: np.ndarray, parts: int) -> Layout:
+    dims = tuple(int(d) for d in dims)
+    if len(dims) != 3:
+        raise ValueError("DSGD stratification is defined for order-3 tensors (SURVEY.md §8e)")
+    offs = tuple(balanced_blocks(idx[:, n], dims[n], parts) for n in range(3))
+    return Layout(parts, dims, offs)
+
+
+def stratum_blocks(parts: int, rank: int, s: int, t: int) -> tuple[int, int, int]:
+    """(mode-1, mode-2, mode-3) blocks rank ``rank`` sweeps in stratum (s, t)."""
+    return rank, (rank + s) % parts, (rank + t) % parts
+
+
+def local_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
+    """This rank's nonzeros (mode-1 block ``rank``), ordered by local cell
+    ``s*P + t``; returns (idx, vals, cell_offsets[P*P + 1], global_positions)."""
+    P = layout.parts
+    b1 = layout.block_of(0, idx[:, 0])
+    pos = np.nonzero(b1 == rank)[0]
+    li = idx[pos]
+    s = (layout.block_of(1, li[:, 1]) - rank) % P
+    t = (layout.block_of(2, li[:, 2]) - rank) % P
+    key = (s * P + t).astype(np.int64)
+    order = np.argsort(key, kind="stable")
+    counts = np.bincount(key, minlength=P * P)
+    off = np.zeros(P * P + 1, np.int64)
+    np.cumsum(counts, out=off[1:])
+    pos = pos[order]
+    return (np.ascontiguousarray(idx[pos]), np.ascontiguousarray(vals[pos]), off, pos)
+
+
+def stratum_seed(epoch_seed: int, s: int, t: int) -> int:
+    return host.derive_seed(epoch_seed, [3, s, t])
+
+
+class DsgdTrainer:
+    """Runs DSGD FastTuckerPlus epochs on one rank through a backend.
+
+    Backend protocol (all calls collective unless noted):
+      ``factor_cell(cell, seed)`` -- local, Hogwild sweep of one cell;
+      ``shift(mode, send_row0, send_n, recv_row0, recv_n)`` -- send rows to
+      rank-1, receive rows from rank+1;
+      ``allgather(mode, row_off)`` -- block r broadcast from rank r;
+      ``core(seed)`` -- local dB, all-reduce, identical B update;
+      ``metrics(slot)`` -- all-reduced (sum sq, sum abs, nnz) of the resident
+      model over the rank's share of a tensor (0 = training cells, 1 = the
+      evaluation tensor registered with ``add_eval``).
+    """
+
+    def __init__(self, backend, layout: Layout, rank: int, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
+                 reg_b=1e-4):
+        self.be = backend
+        self.layout = layout
+        self.rank = rank
+        self.P = layout.parts
+        self.lr_a, self.lr_b, self.reg_a, self.reg_b = lr_a, lr_b, reg_a, reg_b
+
+    def _shift(self, mode: int, held: int):
+        """Ring shift: this rank holds block ``held`` of ``mode`` and needs
+        block ``held + 1`` next, which rank+1 currently holds."""
+        P = self.P
+        s0, sn = self.layout.rows(mode, held % P)
+        r0, rn = self.layout.rows(mode, (held + 1) % P)
+        self.be.shift(mode, s0, sn, r0, rn)
+
+    def factor_phase(self, epoch_seed: int):
+        P, g = self.P, self.rank
+        for s in range(P):
+            for t in range(P):
+                self.be.factor_cell(s * P + t, stratum_seed(epoch_seed, s, t))
+                if P > 1:
+                    self._shift(2, (g + t) % P)
+            if P > 1:
+                self._shift(1, (g + s) % P)
+        if P > 1:
+            # rank g now holds the newest copies of mode-2/3 block g
+            self.be.allgather(1, self.layout.row_off[1])
+            self.be.allgather(2, self.layout.row_off[2])
+
+    def core_phase(self, epoch_seed: int):
+        self.be.core(host.derive_seed(epoch_seed, [2]))
+
+    def epoch(self, epoch_seed: int):
+        self.factor_phase(host.derive_seed(epoch_seed, [1]))
+        self.core_phase(epoch_seed)
+
+    def finalize(self):
+        """Replicates mode-1 rows (kept rank-local during epochs)."""
+        if self.P > 1:
+            self.be.allgather(0, self.layout.row_off[0])
+
+    def rmse_mae(self, slot: int = 1) -> tuple[float, float]:
+        """(RMSE, MAE) over all ranks' shares (ftk::evaluate, evaluation.cpp:55-72)."""
+        sq, ab, n = self.be.metrics(slot)
+        return float(np.sqrt(sq / n)), float(ab / n)
+
+    def loss(self) -> float:
+        """ftk::loss on the training tensor (evaluation.cpp:36-53): sum of squared
+        residuals over all ranks + the replicated regulariser."""
+        sq, _, _ = self.be.metrics(0)
+        return sq + self.be.regularizer()
+
+
+class EngineBackend:
+    """DSGD backend over the C-ABI session (``libftkcu.so``).  Every call only
+    enqueues work on the session stream; NCCL orders kernels and exchanges."""
+
+    def __init__(self, session, slot: int, idx, vals, cell_off, dims, global_nnz: int,
+                 reg_a=1e-4, reg_b=1e-4, lr_a=1e-3, lr_b=1e-3, rank: int = 0,
+                 world: int = 1):
+        from . import MODE_HOGWILD
+
+        self.s = session
+        self.slot = slot
+        self.mode_hog = MODE_HOGWILD
+        self.rank = rank
+        self.world = world
+        self.lr_a, self.lr_b, self.reg_a, self.reg_b = lr_a, lr_b, reg_a, reg_b
+        self.nnz = int(vals.shape[0])
+        session.upload_tensor(slot, dims, idx, vals)
+        session.set_cells(slot, cell_off)
+        session.set_option("global_nnz", int(global_nnz))
+
+    def factor_cell(self, cell, seed):
+        self.s.factor_phase_cell(self.slot, cell, self.lr_a, self.reg_a, seed)
+
+    def shift(self, mode, s0, sn, r0, rn):
+        rank = self.rank
+        self.s.sendrecv_rows(mode, s0, sn, (rank - 1) % self.world, r0, rn,
+                             (rank + 1) % self.world)
+
+    def allgather(self, mode, row_off):
+        self.s.bcast_rows(mode, row_off)
+
+    def core(self, seed):
+        self.s.core_phase(self.slot, None, 16, self.lr_b, self.reg_b, self.mode_hog, seed=seed,
+                          timed=False)
+
+    def add_eval(self, idx, vals, dims):
+        """Registers this rank's share of an evaluation tensor (slot+1)."""
+        self.s.upload_tensor(self.slot + 1, dims, idx, vals)
+        self.eval_nnz = int(vals.shape[0])
+
+    def metrics(self, which):
+        slot = self.slot + (1 if which else 0)
+        n = self.eval_nnz if which else self.nnz
+        out = self.s.eval(slot, 1, 0.0, 0.0) if n else np.zeros(3)
+        v = np.array([out[0], out[1], float(n)], np.float64)
+        if self.world > 1:
+            v = self.s.allreduce_f64(v)
+        return float(v[0]), float(v[1]), float(v[2])
+
+    def regularizer(self):
+        """Needs replicated A: call after DsgdTrainer.finalize()."""
+        return float(self.s.eval(self.slot, 1, self.reg_a, self.reg_b)[2])
+
