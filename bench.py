@@ -15,6 +15,13 @@ barrier + synchronize on both sides, max over ranks.  The COO stream (16 B x
 nnz per sweep, 1.6 GB at Netflix shape) is far larger than the 126 MB L2, so
 no flush is needed between steps.
 
+Multi-GPU (torchrun, N > 1, order-3 configs): DSGD stratification
+(paper_2404_10087_b200/dsgd.py) -- rank g holds the nonzeros of
+mode-1 block g, sweeps one cell per stratum (N*N strata), ring-shifts the
+mode-2/3 blocks over NCCL and all-reduces dB in the core phase.  The total
+tensor is fixed ("scaling": "strong"); `value` = all nonzeros / the slowest
+rank's epoch time.  `--dsgd` runs the cell path at N = 1 as well.
+
 `e2e` re-times the same epochs through the C-ABI from pinned host memory:
 every step uploads the COO tensor and the model (H2D), runs the epoch and
 downloads the model (D2H).  `cpu_baseline` times the reference library
@@ -49,6 +56,8 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
     ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
+    ap.add_argument("--dsgd", action="store_true",
+                    help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
@@ -201,6 +210,83 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class SingleGpu:
+    """Whole tensor on one session: one factor + one core sweep per epoch."""
+
+    scaling = "weak"
+
+    def __init__(self, eng, host, s, coo, ranks, j, a0, b0, world):
+        self.eng, self.host, self.s, self.coo = eng, host, s, coo
+        self.ranks, self.j, self.a0, self.b0, self.world = ranks, j, a0, b0, world
+        self.parallelism = f"replica x{world}" if world > 1 else "1 GPU"
+        self.local_nnz = coo.nnz
+        self.job_nnz = coo.nnz * world  # independent replicas
+
+    def upload(self):
+        self.s.upload_tensor(0, self.coo.dims, self.coo.idx, self.coo.vals)
+
+    def upload_ptr(self, idx_ptr, val_ptr):
+        self.s.upload_tensor_ptr(0, self.coo.dims, self.coo.nnz, idx_ptr, val_ptr)
+
+    def host_arrays(self):
+        return self.coo.idx, self.coo.vals
+
+    def factor(self, es):
+        self.s.factor_phase(0, None, 16, 1e-3, 1e-4, self.eng.MODE_HOGWILD,
+                            seed=self.host.derive_seed(es, [1]), timed=False)
+
+    def core(self, es):
+        self.s.core_phase(0, None, 16, 1e-3, 1e-4, self.eng.MODE_HOGWILD,
+                          seed=self.host.derive_seed(es, [2]), timed=False)
+
+    def train_loss(self):
+        out = self.s.eval(0, 1, 1e-4, 1e-4)
+        return float(out[0] + out[2])
+
+
+class Dsgd(SingleGpu):
+    """DSGD strata over the ranks (paper_2404_10087_b200/dsgd.py): rank g
+    holds mode-1 block g, sweeps one cell per stratum, ring-shifts the mode-2/3
+    blocks over NCCL; the core phase all-reduces dB.  Total work is fixed."""
+
+    scaling = "strong"
+
+    def __init__(self, eng, host, s, coo, ranks, j, a0, b0, world, rank):
+        from paper_2404_10087_b200 import dsgd
+
+        super().__init__(eng, host, s, coo, ranks, j, a0, b0, world)
+        self.parallelism = f"dsgd {world}x{world} strata" if world > 1 else "dsgd 1 cell"
+        self.rank = rank
+        self.layout = dsgd.make_layout(coo.dims, coo.idx, world)
+        self.idx, self.vals, self.off, _ = dsgd.local_cells(self.layout, coo.idx, coo.vals, rank)
+        self.local_nnz = int(self.vals.shape[0])
+        self.job_nnz = coo.nnz
+        self.be = dsgd.EngineBackend(s, 0, self.idx, self.vals, self.off, coo.dims, coo.nnz,
+                                     rank=rank, world=world)
+        self.tr = dsgd.DsgdTrainer(self.be, self.layout, rank)
+
+    def upload(self):
+        self.s.upload_tensor(0, self.coo.dims, self.idx, self.vals)
+        self.s.set_cells(0, self.off)
+
+    def upload_ptr(self, idx_ptr, val_ptr):
+        self.s.upload_tensor_ptr(0, self.coo.dims, self.local_nnz, idx_ptr, val_ptr)
+        self.s.set_cells(0, self.off)
+
+    def host_arrays(self):
+        return self.idx, self.vals
+
+    def factor(self, es):
+        self.tr.factor_phase(self.host.derive_seed(es, [1]))
+
+    def core(self, es):
+        self.tr.core_phase(es)
+
+    def train_loss(self):
+        self.tr.finalize()
+        return float(self.tr.loss())
+
+
 def run_engine(args):
     import torch
 
@@ -209,17 +295,14 @@ def run_engine(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.init_process_group("nccl", device_id=dev)
     cfg, j, coo = make_workload(args.config, args.rank, world, rank, local)
     order = coo.order
     ranks = [j] * order
-    nnz_total = coo.nnz
-    # Weak scaling: every rank holds the full problem shape; with world > 1
-    # each rank trains an independent replica (DSGD stratification in
-    # paper_2404_10087_b200/dsgd.py is exercised by the tests).
     s = eng.Session(local)
     prec = {"fp32": eng.PREC_FP32, "tf32": eng.PREC_TF32, "3xtf32": eng.PREC_3XTF32}[args.precision]
     s.set_option("precision", prec)
@@ -228,16 +311,22 @@ def run_engine(args):
     s.set_option("tc_ws", args.tc_ws)
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
-    s.upload_tensor(0, coo.dims, coo.idx, coo.vals)
     s.upload_model(coo.dims, ranks, j, a0, b0)
-    ext = torch.cuda.ExternalStream(s.stream_handle, device=torch.device(f"cuda:{local}"))
-
-    def epoch(k):
-        es = host.derive_seed(1, [k + 1])
-        s.factor_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=host.derive_seed(es, [1]),
-                       timed=False)
-        s.core_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=host.derive_seed(es, [2]),
-                     timed=False)
+    use_dsgd = (world > 1 or args.dsgd) and order == 3
+    if use_dsgd:
+        if world > 1:
+            # NCCL id for the session's own communicator, shipped over the PG
+            uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(eng.Session.comm_unique_id()),
+                                           dtype=torch.uint8))
+            torch.distributed.broadcast(uid, 0)
+            s.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank)
+    else:
+        job = SingleGpu(eng, host, s, coo, ranks, j, a0, b0, world)
+        job.upload()
+    ext = torch.cuda.ExternalStream(s.stream_handle, device=dev)
 
     def barrier():
         torch.cuda.synchronize()
@@ -246,8 +335,10 @@ def run_engine(args):
             torch.cuda.synchronize()
 
     for k in range(args.warmup):
-        epoch(k)
-    loss0 = s.eval(0, 1, 1e-4, 1e-4)
+        es = host.derive_seed(1, [k + 1])
+        job.factor(es)
+        job.core(es)
+    loss0 = job.train_loss()
     barrier()
     # per-phase events inside the timed region (same stream as the kernels)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
@@ -257,11 +348,9 @@ def run_engine(args):
         evs[0].record(ext)
         for k in range(args.steps):
             es = host.derive_seed(1, [args.warmup + k + 1])
-            s.factor_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD,
-                           seed=host.derive_seed(es, [1]), timed=False)
+            job.factor(es)
             evs[2 * k + 1].record(ext)
-            s.core_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD,
-                         seed=host.derive_seed(es, [2]), timed=False)
+            job.core(es)
             evs[2 * k + 2].record(ext)
         barrier()
     launches = s.get_option("launches") - launches0
@@ -269,17 +358,18 @@ def run_engine(args):
     f_ms = [evs[2 * k].elapsed_time(evs[2 * k + 1]) for k in range(args.steps)]
     c_ms = [evs[2 * k + 1].elapsed_time(evs[2 * k + 2]) for k in range(args.steps)]
     if world > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    loss1 = s.eval(0, 1, 1e-4, 1e-4)
+    loss1 = job.train_loss()
     ms_step = total_ms / args.steps
-    value = nnz_total * world / (ms_step * 1e-3)
+    value = job.job_nnz / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (algorithmic bytes)
+    # roofline of the dominant kernel (algorithmic bytes) on
+    # this rank's share of the nonzeros
     rec = 4 * order + 4
-    f_bytes = nnz_total * (rec + 8 * sum(ranks))
-    c_bytes = nnz_total * (rec + 4 * sum(ranks))
+    f_bytes = job.local_nnz * (rec + 8 * sum(ranks))
+    c_bytes = job.local_nnz * (rec + 4 * sum(ranks))
     f_avg, c_avg = float(np.mean(f_ms)), float(np.mean(c_ms))
     if f_avg >= c_avg:
         dom, dom_bytes, dom_ms = "factor", f_bytes, f_avg
@@ -298,11 +388,11 @@ def run_engine(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = time_e2e(s, coo, ranks, j, a0, b0, args, ext, torch, world)
+        e2e = time_e2e(job, a0, b0, args, torch, world, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = min(args.cpu_sample, nnz_total)
+        sample = min(args.cpu_sample, coo.nnz)
         cpu = cpu_reference_time(cfg, j, sample)
 
     clocks = clk.summary()
@@ -311,14 +401,15 @@ def run_engine(args):
             "metric": "SGD nonzeros/sec per epoch (factor+core) at J=R=32, 1-8 B200; test RMSE",
             "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prec == 0 else args.precision,
+            "scaling": job.scaling, "vs_baseline": None,
+            "dtype": "f32" if prec == 0 else args.precision,
             "data": "synthetic (uniform distinct tuples, values U[lo,hi], seeded)",
-            "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": nnz_total,
+            "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": coo.nnz,
                        "J": j, "R": j, "M": 16, "mode": "hogwild", "precision": args.precision,
-                       "parallelism": f"replica x{world}" if world > 1 else "1 GPU",
+                       "parallelism": job.parallelism, "nnz_per_rank": job.local_nnz,
                        "l2": "inputs larger than L2 (COO stream 16 B/nnz per sweep)"},
             "phases_ms": {"factor": f_avg, "core": c_avg},
-            "train_loss_before_after": [float(loss0[0] + loss0[2]), float(loss1[0] + loss1[2])],
+            "train_loss_before_after": [loss0, loss1],
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": dom_bytes,
@@ -335,38 +426,44 @@ def run_engine(args):
         torch.distributed.destroy_process_group()
 
 
-def time_e2e(s, coo, ranks, j, a0, b0, args, ext, torch, world):
+def time_e2e(job, a0, b0, args, torch, world, dev):
     """Same epochs through the C-ABI from pinned host buffers, host<->device
-    copies of every step's inputs (COO + model) and result (model) inside."""
-    import paper_2404_10087_b200 as eng
+    copies of every step's inputs (this rank's COO share + model) and result
+    (model) inside the timed region; max over ranks."""
     from paper_2404_10087_b200 import host
 
-    idx_h = torch.from_numpy(np.ascontiguousarray(coo.idx)).pin_memory()
-    val_h = torch.from_numpy(np.ascontiguousarray(coo.vals)).pin_memory()
+    idx, vals = job.host_arrays()
+    idx_h = torch.from_numpy(np.ascontiguousarray(idx)).pin_memory()
+    val_h = torch.from_numpy(np.ascontiguousarray(vals)).pin_memory()
     a_h = [torch.from_numpy(x.copy()).pin_memory() for x in a0]
     b_h = [torch.from_numpy(x.copy()).pin_memory() for x in b0]
     a_np = [x.numpy() for x in a_h]
     b_np = [x.numpy() for x in b_h]
     steps = max(1, min(args.steps, 3))
-    h2d = coo.idx.nbytes + coo.vals.nbytes + sum(x.nbytes for x in a_np + b_np)
+    h2d = idx.nbytes + vals.nbytes + sum(x.nbytes for x in a_np + b_np)
     d2h = sum(x.nbytes for x in a_np + b_np)
+    s = job.s
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for k in range(steps):
-        s.upload_tensor_ptr(0, coo.dims, coo.nnz, idx_h.data_ptr(), val_h.data_ptr())
-        s.upload_model(coo.dims, ranks, j, a_np, b_np)
+        job.upload_ptr(idx_h.data_ptr(), val_h.data_ptr())
+        s.upload_model(job.coo.dims, job.ranks, job.j, a_np, b_np)
         es = host.derive_seed(7, [k + 1])
-        s.factor_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=host.derive_seed(es, [1]),
-                       timed=False)
-        s.core_phase(0, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=host.derive_seed(es, [2]),
-                     timed=False)
+        job.factor(es)
+        job.core(es)
         s.download_model(a_np, b_np)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": coo.nnz * world / dt, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": job.job_nnz / dt, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps,
             "path": "ftkcu_tensor_upload + ftkcu_model_upload + factor/core phases + "
-                    "ftkcu_model_download, pinned host buffers"}
+                    "ftkcu_model_download, pinned host buffers (per rank, max over ranks)"}
 
 
 def main():

@@ -70,7 +70,14 @@ const char* ftkcu_last_error(const ftkcu_session* s);
 int ftkcu_abi_version(void);
 
 /* Tunables: "precision" (FTKCU_PREC_*), "eval" (FTKCU_EVAL_*),
- * "hog_blocks_per_sm", "verbose".  Unknown keys are FTKCU_ERR_ARG. */
+ * "hog_blocks_per_sm", "hog_update" (1 = atomic row accumulate, 0 = overwrite),
+ * "tc_ws" (warp-specialised tcgen05 sweeps), "max_ctas" (factor-sweep grid
+ * cap, 0 = one CTA per SM), "staleness" (whole-tensor factor sweeps cap the
+ * grid so at most this many nonzeros per row of the smallest mode are in
+ * flight; default 32, 0 = off), "global_nnz" (|Omega|
+ * over all ranks for the multi-GPU core update), "shuffle_seed", "verbose".
+ * get_option also reads "launches", "stream" (cudaStream_t), "num_sms".
+ * Unknown keys are FTKCU_ERR_ARG. */
 int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value);
 int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value);
 

@@ -79,7 +79,21 @@ struct KView {
   // tile_rows[p] valid rows of physical tile p (the rest is padding).
   const int32_t* tile_rows;
   int64_t tile_base, ntiles;
+  // Factor sweeps: cap on resident CTAs (0 = one per SM), bounds how many
+  // nonzeros are in flight against the same A rows (Hogwild staleness).
+  int max_ctas;
 };
+
+int num_sms();
+
+// Persistent grid for a tile range: one CTA per SM, at most one per tile,
+// at most v.max_ctas when set.
+inline int64_t sweep_grid(const KView& v, int64_t per_sm_ctas = 1) {
+  int64_t g = (int64_t)num_sms() * per_sm_ctas;
+  if (v.max_ctas > 0 && g > v.max_ctas) g = v.max_ctas;
+  if (g > v.ntiles) g = v.ntiles;
+  return g;
+}
 
 // Optional per-batch debug outputs of the deterministic kernels (device
 // pointers, any may be null).  Layouts match ftkcu_batch_probe.

@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,7 +36,12 @@ struct ftkcu_session {
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
-  int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
+  int64_t global_nnz = 0;
+  int64_t opt_max_ctas = 0;  // factor-sweep grid cap (0 = one CTA per SM)
+  // Whole-tensor factor sweeps: cap the grid so that at most this many
+  // nonzeros per row of the smallest mode are in flight (0 = off).  See
+  // dsgd.grid_cap for the measurement behind the default.
+  int64_t opt_staleness = 32;  // |Omega| across ranks for the core update (DSGD)
   int64_t launches = 0;  // kernels launched by this session (for benches)
 };
 
@@ -107,6 +113,7 @@ void free_tensor(DevTensor& t) {
   }
   if (t.vals) cudaFree(t.vals);
   if (t.svals) cudaFree(t.svals);
+  if (t.tile_rows) cudaFree(t.tile_rows);
   t = DevTensor{};
 }
 
@@ -332,6 +339,12 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_verbose = value;
   } else if (k == "global_nnz") {
     s->global_nnz = value;
+  } else if (k == "staleness") {
+    if (value < 0) return fail(s, FTKCU_ERR_ARG, "staleness must be >= 0");
+    s->opt_staleness = value;
+  } else if (k == "max_ctas") {
+    if (value < 0) return fail(s, FTKCU_ERR_ARG, "max_ctas must be >= 0");
+    s->opt_max_ctas = value;
   } else if (k == "shuffle_seed") {
     s->opt_shuffle_seed = value;
     for (auto& t : s->slots) t.shuffled = false;
@@ -351,6 +364,9 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "hog_update") *value = s->opt_hog_update;
   else if (k == "tc_ws") *value = s->opt_tc_ws;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
+  else if (k == "max_ctas") *value = s->opt_max_ctas;
+  else if (k == "staleness") *value = s->opt_staleness;
+  else if (k == "global_nnz") *value = s->global_nnz;
   else if (k == "launches") *value = s->launches;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
   else if (k == "num_sms") *value = num_sms();
@@ -504,6 +520,13 @@ static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, in
   if (mode != FTKCU_MODE_HOGWILD) return fail(s, FTKCU_ERR_ARG, "unknown mode %d", mode);
   if ((rc = prepare_stream(s, t, perm))) return rc;
   KView v = make_view(s, t, true);
+  v.max_ctas = (int)s->opt_max_ctas;
+  if (cell < 0 && s->opt_staleness > 0) {
+    int64_t rows = s->model.dims[0];
+    for (int n = 1; n < s->model.order; ++n) rows = std::min<int64_t>(rows, s->model.dims[n]);
+    const int64_t cap = std::max<int64_t>(1, rows * s->opt_staleness / (3 * kHogTile));
+    if (cap < num_sms() && (v.max_ctas == 0 || cap < v.max_ctas)) v.max_ctas = (int)cap;
+  }
   if (cell >= 0) {
     if (cell + 1 >= (int)t.cell_tile.size())
       return fail(s, FTKCU_ERR_ARG, "cell %d out of range", cell);

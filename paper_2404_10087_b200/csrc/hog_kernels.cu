@@ -417,7 +417,8 @@ cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   if (v.ntiles == 0) return cudaSuccess;
-  hog_factor_kernel<<<hog_grid(blocks_per_sm), kHogThreads, bytes, st>>>(
+  hog_factor_kernel<<<(int)sweep_grid(v, blocks_per_sm < 1 ? 1 : blocks_per_sm), kHogThreads,
+                      bytes, st>>>(
       v, tile_mul, tile_add, lr_a, reg_a, atomic_update);
   return cudaGetLastError();
 }

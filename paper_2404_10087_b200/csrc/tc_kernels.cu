@@ -87,6 +87,7 @@ struct TcParams {
   const float* b[kMaxOrder];
   int64_t nnz, ntiles, tmul, tadd, tile_base;
   const int32_t* tile_rows;
+  int max_ctas;  // factor sweeps: grid cap (KView::max_ctas)
   float lr, reg;
   int atomic_update;
   int prec3;  // split-tf32 (hi*hi + hi*lo + lo*hi) for the C = A B contraction
@@ -620,6 +621,7 @@ TcParams make_params(const KView& v, int64_t mul, int64_t add) {
   p.ntiles = v.ntiles;
   p.tile_base = v.tile_base;
   p.tile_rows = v.tile_rows;
+  p.max_ctas = v.max_ctas;
   p.tmul = mul;
   p.tadd = add;
   return p;
@@ -632,7 +634,8 @@ cudaError_t run_factor(const TcParams& p, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)L::bytes);
   if (e != cudaSuccess) return e;
-  const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
   kern<<<grid, kThreads, L::bytes, st>>>(p);
   return cudaGetLastError();
 }

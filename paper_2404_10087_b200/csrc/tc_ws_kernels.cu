@@ -702,7 +702,7 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   auto kern = atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  const int grid = (int)sweep_grid(v);
   kern<<<grid, kThreadsWs, bytes, st>>>(p);
   return cudaGetLastError();
 }
