@@ -72,7 +72,8 @@ int ftkcu_abi_version(void);
 /* Tunables: "precision" (FTKCU_PREC_*), "eval" (FTKCU_EVAL_*),
  * "hog_blocks_per_sm", "hog_update" (1 = atomic row accumulate, 0 = overwrite),
  * "tc_ws" (warp-specialised tcgen05 sweeps), "max_ctas" (factor-sweep grid
- * cap, 0 = one CTA per SM), "staleness" (whole-tensor factor sweeps cap the
+ * cap, 0 = one CTA per SM), "graphs" (CUDA-graph replay of the DSGD
+ * stratum loop, default 1), "staleness" (whole-tensor factor sweeps cap the
  * grid so at most this many nonzeros per row of the smallest mode are in
  * flight; default 32, 0 = off), "global_nnz" (|Omega|
  * over all ranks for the multi-GPU core update), "shuffle_seed", "verbose".
@@ -172,6 +173,19 @@ int ftkcu_comm_sendrecv_rows(ftkcu_session* s, int mode, int64_t send_row0,
  * (all-gather of the owned blocks after a DSGD factor sweep). */
 int ftkcu_comm_bcast_rows(ftkcu_session* s, int mode, const int64_t* row_off,
                           int nblocks);
+/* One DSGD factor phase of this rank (dsgd.DsgdTrainer.factor_phase): for
+ * stratum (s, t), s, t < parts, sweep local cell s*parts+t with tile
+ * permutation seed cell_seeds[s*parts+t], then ring-shift the mode-3 block
+ * (row_off3, parts+1 offsets) to rank-1 / from rank+1; after each s-round
+ * the mode-2 block (row_off2); finally all-gather the mode-2/3 blocks.  The
+ * whole loop is enqueued on the session stream without a host sync and, with
+ * option "graphs" (default 1), captured once as a CUDA graph and replayed.
+ * Needs ftkcu_tensor_set_cells with parts*parts cells and, for parts > 1, a
+ * communicator (world 1 = one rank emulating `parts`, shifts to itself).
+ * No reference counterpart: the reference is single-host. */
+int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t* row_off2,
+                            const int64_t* row_off3, const uint64_t* cell_seeds, float lr_a,
+                            float reg_a, double* ms);
 /* Sum all-reduce of host fp64 values (metrics partials). */
 int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n);
 /* Waits for all work queued on the session stream. */

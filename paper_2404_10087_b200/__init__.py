@@ -39,7 +39,7 @@ EXPORTS = (
     "ftkcu_batch_probe", "ftkcu_comm_unique_id", "ftkcu_comm_init",
     "ftkcu_comm_allreduce_grad", "ftkcu_tensor_set_cells", "ftkcu_factor_phase_cell",
     "ftkcu_comm_sendrecv_rows", "ftkcu_comm_bcast_rows", "ftkcu_comm_allreduce_f64",
-    "ftkcu_stream_sync",
+    "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch",
 )
 
 
@@ -96,6 +96,8 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_comm_bcast_rows.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int]
     L.ftkcu_comm_allreduce_f64.argtypes = [C.c_void_p, _f64p, C.c_int]
     L.ftkcu_stream_sync.argtypes = [C.c_void_p]
+    L.ftkcu_dsgd_factor_epoch.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
+                                          C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
     _lib = L
     return L
 
@@ -275,6 +277,17 @@ class Session:
         v = np.ascontiguousarray(values, np.float64).copy()
         self._ck(self.lib.ftkcu_comm_allreduce_f64(self.h, _p(v, _f64p), v.size))
         return v
+
+    def dsgd_factor_epoch(self, slot, parts, row_off2, row_off3, cell_seeds, lr_a=1e-3,
+                          reg_a=1e-4, timed=False):
+        o2 = np.ascontiguousarray(row_off2, np.int64)
+        o3 = np.ascontiguousarray(row_off3, np.int64)
+        sd = np.ascontiguousarray(np.asarray(cell_seeds, np.uint64))
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_dsgd_factor_epoch(
+            self.h, slot, parts, _p(o2, _i64p), _p(o3, _i64p), _p(sd, C.POINTER(C.c_uint64)),
+            lr_a, reg_a, C.byref(ms) if timed else None))
+        return ms.value
 
     def sync(self):
         self._ck(self.lib.ftkcu_stream_sync(self.h))

@@ -82,6 +82,9 @@ struct KView {
   // Factor sweeps: cap on resident CTAs (0 = one per SM), bounds how many
   // nonzeros are in flight against the same A rows (Hogwild staleness).
   int max_ctas;
+  // Optional device {mul, add} of the tile permutation (overrides the launch
+  // arguments; lets a captured CUDA graph take a new permutation per epoch).
+  const int64_t* tperm;
 };
 
 int num_sms();

@@ -30,18 +30,27 @@ struct ftkcu_session {
   int64_t opt_precision = FTKCU_PREC_FP32;
   int64_t opt_eval = FTKCU_EVAL_EXACT;
   int64_t opt_hog_bps = 2;
-  int64_t opt_hog_update = 1;
-  int64_t opt_tc_ws = 1;       // warp-specialized tcgen05 sweeps where supported  // 1: atomic accumulate, 0: overwrite (reference rule)
+  int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
+  int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
-  int64_t global_nnz = 0;
+  int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
   int64_t opt_max_ctas = 0;  // factor-sweep grid cap (0 = one CTA per SM)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
   // dsgd.grid_cap for the measurement behind the default.
-  int64_t opt_staleness = 32;  // |Omega| across ranks for the core update (DSGD)
+  int64_t opt_staleness = 32;
+  int64_t opt_graphs = 1;  // capture the DSGD stratum loop in a CUDA graph
+  // DSGD epoch: per-cell tile permutations (device + pinned host staging)
+  // and the captured stratum loop, re-captured when its key changes.
+  int64_t* d_cellperm = nullptr;
+  int64_t* h_cellperm = nullptr;
+  size_t cellperm_cap = 0;
+  cudaGraphExec_t dsgd_exec = nullptr;
+  std::vector<int64_t> dsgd_key;
+  int64_t dsgd_launches = 0;
   int64_t launches = 0;  // kernels launched by this session (for benches)
 };
 
@@ -309,6 +318,8 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   if (s->grad) cudaFree(s->grad);
   if (s->scratch) cudaFree(s->scratch);
   if (s->d_perm) cudaFree(s->d_perm);
+  if (s->d_cellperm) cudaFree(s->d_cellperm);
+  if (s->dsgd_exec) cudaGraphExecDestroy(s->dsgd_exec);
   if (s->comm) ncclCommDestroy(s->comm);
   cudaEventDestroy(s->ev0);
   cudaEventDestroy(s->ev1);
@@ -339,6 +350,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_verbose = value;
   } else if (k == "global_nnz") {
     s->global_nnz = value;
+  } else if (k == "graphs") {
+    s->opt_graphs = value != 0;
   } else if (k == "staleness") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "staleness must be >= 0");
     s->opt_staleness = value;
@@ -366,6 +379,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
   else if (k == "staleness") *value = s->opt_staleness;
+  else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
   else if (k == "launches") *value = s->launches;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
@@ -497,6 +511,24 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
   return FTKCU_OK;
 }
 
+// Hogwild factor sweep over v's tile range: WS tcgen05 -> tcgen05 -> FFMA.
+static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t add,
+                         float lr_a, float reg_a) {
+  if (v.ntiles <= 0) return FTKCU_OK;
+  if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
+    CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
+                        (int)s->opt_hog_update, s->stream));
+  } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+    CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
+                        (int)s->opt_hog_update, s->stream));
+  } else {
+    CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps,
+                         (int)s->opt_hog_update, s->stream));
+  }
+  s->launches += 1;
+  return FTKCU_OK;
+}
+
 static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
                              float lr_a, float reg_a, int mode, uint64_t seed, int cell,
                              double* ms) {
@@ -536,19 +568,7 @@ static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, in
   int64_t mul = 1, add = 0;
   if (!perm) tile_perm(seed, v.ntiles, &mul, &add);
   CK(cudaEventRecord(s->ev0, s->stream));
-  if (v.ntiles > 0) {
-    if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
-      CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
-                          (int)s->opt_hog_update, s->stream));
-    } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
-      CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
-                          (int)s->opt_hog_update, s->stream));
-    } else {
-      CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps,
-                           (int)s->opt_hog_update, s->stream));
-    }
-    s->launches += 1;
-  }
+  if ((rc = launch_factor(s, v, mul, add, lr_a, reg_a))) return rc;
   return finish_timing(s, ms);
 }
 
@@ -746,6 +766,67 @@ static int rows_of(ftkcu_session* s, int mode, int64_t row0, int64_t nrows, floa
   return FTKCU_OK;
 }
 
+// Rank r broadcasts rows [off[r], off[r+1]) of `mode`, for every rank r.
+static int bcast_blocks(ftkcu_session* s, int mode, const int64_t* off) {
+  int rc;
+  NK(ncclGroupStart());
+  for (int r = 0; r < s->world; ++r) {
+    float* p;
+    size_t c;
+    if ((rc = rows_of(s, mode, off[r], off[r + 1] - off[r], &p, &c))) {
+      ncclGroupEnd();
+      return rc;
+    }
+    if (c) NK(ncclBroadcast(p, p, c, ncclFloat, r, s->comm, s->stream));
+  }
+  NK(ncclGroupEnd());
+  return FTKCU_OK;
+}
+
+// Ring shift of one block of `mode`: send block `held` to rank-1, receive
+// block `held`+1 from rank+1 (DSGD, dsgd.DsgdTrainer._shift).
+static int shift_block(ftkcu_session* s, int mode, const int64_t* off, int parts, int held) {
+  const int b0 = held % parts, b1 = (held + 1) % parts;
+  const int dst = (s->rank - 1 + s->world) % s->world, src = (s->rank + 1) % s->world;
+  float *sp, *rp;
+  size_t sc, rcn;
+  int rc;
+  if ((rc = rows_of(s, mode, off[b0], off[b0 + 1] - off[b0], &sp, &sc))) return rc;
+  if ((rc = rows_of(s, mode, off[b1], off[b1 + 1] - off[b1], &rp, &rcn))) return rc;
+  NK(ncclGroupStart());
+  if (sc) NK(ncclSend(sp, sc, ncclFloat, dst, s->comm, s->stream));
+  if (rcn) NK(ncclRecv(rp, rcn, ncclFloat, src, s->comm, s->stream));
+  NK(ncclGroupEnd());
+  return FTKCU_OK;
+}
+
+// One DSGD factor phase on the session stream: P*P cell sweeps, the A3 ring
+// shift after every stratum, the A2 shift after every s-round, then the
+// all-gather of A2/A3 (world > 1).  Tile permutations come from
+// s->d_cellperm so the same enqueue can be captured once and replayed.
+static int enqueue_dsgd(ftkcu_session* s, DevTensor& t, int parts, const int64_t* off2,
+                        const int64_t* off3, float lr_a, float reg_a) {
+  int rc;
+  for (int si = 0; si < parts; ++si) {
+    for (int ti = 0; ti < parts; ++ti) {
+      const int cell = si * parts + ti;
+      KView v = make_view(s, t, true);
+      v.max_ctas = (int)s->opt_max_ctas;
+      v.tile_base = t.cell_tile[cell];
+      v.ntiles = t.cell_tile[cell + 1] - t.cell_tile[cell];
+      v.tperm = s->d_cellperm + 2 * cell;
+      if ((rc = launch_factor(s, v, 1, 0, lr_a, reg_a))) return rc;
+      if (parts > 1 && (rc = shift_block(s, 2, off3, parts, s->rank + ti))) return rc;
+    }
+    if (parts > 1 && (rc = shift_block(s, 1, off2, parts, s->rank + si))) return rc;
+  }
+  if (s->world > 1) {
+    if ((rc = bcast_blocks(s, 1, off2))) return rc;
+    if ((rc = bcast_blocks(s, 2, off3))) return rc;
+  }
+  return FTKCU_OK;
+}
+
 int ftkcu_comm_sendrecv_rows(ftkcu_session* s, int mode, int64_t send_row0, int64_t send_nrows,
                              int dst, int64_t recv_row0, int64_t recv_nrows, int src) {
   int rc = bind(s);
@@ -767,18 +848,7 @@ int ftkcu_comm_bcast_rows(ftkcu_session* s, int mode, const int64_t* row_off, in
   if (rc) return rc;
   if (!s->comm) return fail(s, FTKCU_ERR_STATE, "no communicator");
   if (nblocks != s->world) return fail(s, FTKCU_ERR_ARG, "need one block per rank");
-  NK(ncclGroupStart());
-  for (int r = 0; r < nblocks; ++r) {
-    float* p;
-    size_t c;
-    if ((rc = rows_of(s, mode, row_off[r], row_off[r + 1] - row_off[r], &p, &c))) {
-      ncclGroupEnd();
-      return rc;
-    }
-    if (c) NK(ncclBroadcast(p, p, c, ncclFloat, r, s->comm, s->stream));
-  }
-  NK(ncclGroupEnd());
-  return FTKCU_OK;
+  return bcast_blocks(s, mode, row_off);
 }
 
 int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n) {
@@ -799,6 +869,91 @@ int ftkcu_stream_sync(ftkcu_session* s) {
   if (rc) return rc;
   CK(cudaStreamSynchronize(s->stream));
   return FTKCU_OK;
+}
+
+int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t* row_off2,
+                            const int64_t* row_off3, const uint64_t* cell_seeds, float lr_a,
+                            float reg_a, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  DevTensor& t = s->slots[slot];
+  if (t.order != 3) return fail(s, FTKCU_ERR_ARG, "DSGD strata need an order-3 tensor");
+  if (parts < 1 || !row_off2 || !row_off3 || !cell_seeds)
+    return fail(s, FTKCU_ERR_ARG, "bad DSGD arguments");
+  const int ncell = parts * parts;
+  if ((int)t.cell_off.size() != ncell + 1)
+    return fail(s, FTKCU_ERR_ARG, "tensor has %d cells, DSGD over %d parts needs %d",
+                (int)t.cell_off.size() - 1, parts, ncell);
+  if (parts > 1 && !s->comm) return fail(s, FTKCU_ERR_STATE, "DSGD over > 1 part needs a communicator");
+  if (s->world > 1 && parts != s->world)
+    return fail(s, FTKCU_ERR_ARG, "parts (%d) must equal the communicator size (%d)", parts,
+                s->world);
+  const int64_t* offs[2] = {row_off2, row_off3};
+  for (int m = 0; m < 2; ++m) {
+    if (offs[m][0] != 0 || offs[m][parts] != s->model.dims[m + 1])
+      return fail(s, FTKCU_ERR_ARG, "mode-%d block offsets must span [0, %d]", m + 2,
+                  s->model.dims[m + 1]);
+    for (int p = 0; p < parts; ++p)
+      if (offs[m][p + 1] < offs[m][p]) return fail(s, FTKCU_ERR_ARG, "block offsets not sorted");
+  }
+  if ((rc = prepare_stream(s, t, nullptr))) return rc;
+  if ((size_t)ncell > s->cellperm_cap) {
+    if (s->d_cellperm) CK(cudaFree(s->d_cellperm));
+    s->d_cellperm = nullptr;
+    CK(cudaMalloc(&s->d_cellperm, sizeof(int64_t) * 2 * ncell));
+    s->cellperm_cap = ncell;
+  }
+  std::vector<int64_t> perm(2 * (size_t)ncell);
+  for (int c = 0; c < ncell; ++c)
+    tile_perm(cell_seeds[c], t.cell_tile[c + 1] - t.cell_tile[c], &perm[2 * c], &perm[2 * c + 1]);
+  CK(cudaEventRecord(s->ev0, s->stream));
+  // pageable source: staged before the call returns, so `perm` may go away
+  CK(cudaMemcpyAsync(s->d_cellperm, perm.data(), sizeof(int64_t) * 2 * ncell,
+                     cudaMemcpyHostToDevice, s->stream));
+  if (!s->opt_graphs) {
+    if ((rc = enqueue_dsgd(s, t, parts, row_off2, row_off3, lr_a, reg_a))) return rc;
+    return finish_timing(s, ms);
+  }
+  uint32_t lr_bits, reg_bits;
+  std::memcpy(&lr_bits, &lr_a, 4);
+  std::memcpy(&reg_bits, &reg_a, 4);
+  std::vector<int64_t> key = {slot, parts, s->rank, s->world, (int64_t)lr_bits,
+                              (int64_t)reg_bits, s->opt_precision, s->opt_hog_update,
+                              s->opt_tc_ws, s->opt_max_ctas, s->opt_hog_bps,
+                              (int64_t)(intptr_t)s->comm, (int64_t)(intptr_t)s->d_cellperm,
+                              (int64_t)(intptr_t)t.svals, (int64_t)(intptr_t)t.tile_rows};
+  for (int n = 0; n < 3; ++n) {
+    key.push_back((int64_t)(intptr_t)s->model.a[n]);
+    key.push_back((int64_t)(intptr_t)s->model.b[n]);
+    key.push_back((int64_t)(intptr_t)t.sidx[n]);
+  }
+  key.insert(key.end(), row_off2, row_off2 + parts + 1);
+  key.insert(key.end(), row_off3, row_off3 + parts + 1);
+  key.insert(key.end(), t.cell_tile.begin(), t.cell_tile.end());
+  if (!s->dsgd_exec || key != s->dsgd_key) {
+    if (s->dsgd_exec) CK(cudaGraphExecDestroy(s->dsgd_exec));
+    s->dsgd_exec = nullptr;
+    const int64_t before = s->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed));
+    rc = enqueue_dsgd(s, t, parts, row_off2, row_off3, lr_a, reg_a);
+    const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CK(e);
+    const cudaError_t ei = cudaGraphInstantiate(&s->dsgd_exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(ei);
+    s->dsgd_key = key;
+    s->dsgd_launches = s->launches - before;
+    s->launches = before;
+  }
+  CK(cudaGraphLaunch(s->dsgd_exec, s->stream));
+  s->launches += s->dsgd_launches;
+  return finish_timing(s, ms);
 }
 
 int ftkcu_comm_allreduce_grad(ftkcu_session* s) {

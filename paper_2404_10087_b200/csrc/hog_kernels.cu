@@ -217,6 +217,10 @@ __global__ void __launch_bounds__(kHogThreads)
 hog_factor_kernel(KView v, int64_t tmul, int64_t tadd, float lr, float reg,
                   int atomic_update) {
   extern __shared__ float sm[];
+  if (v.tperm) {
+    tmul = v.tperm[0];
+    tadd = v.tperm[1];
+  }
   const int warps = blockDim.x / 32;
   const HogLayout L = hog_layout(v, false, warps);
   load_b(v, L, sm);

@@ -87,6 +87,7 @@ struct TcParams {
   const float* b[kMaxOrder];
   int64_t nnz, ntiles, tmul, tadd, tile_base;
   const int32_t* tile_rows;
+  const int64_t* tperm;  // device {mul, add} or null (KView::tperm)
   int max_ctas;  // factor sweeps: grid cap (KView::max_ctas)
   float lr, reg;
   int atomic_update;
@@ -135,7 +136,9 @@ __device__ __forceinline__ Rec<N> load_rec(const TcParams& p, int64_t tile) {
 
 __device__ __forceinline__ int64_t phys_tile(const TcParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
-  return p.tile_base + (t * p.tmul + p.tadd) % p.ntiles;
+  const int64_t mul = p.tperm ? __ldg(p.tperm) : p.tmul;
+  const int64_t add = p.tperm ? __ldg(p.tperm + 1) : p.tadd;
+  return p.tile_base + (t * mul + add) % p.ntiles;
 }
 
 // Stages one tile into `slot`: COO record to smem, factor rows by cp.async
@@ -621,6 +624,7 @@ TcParams make_params(const KView& v, int64_t mul, int64_t add) {
   p.ntiles = v.ntiles;
   p.tile_base = v.tile_base;
   p.tile_rows = v.tile_rows;
+  p.tperm = v.tperm;
   p.max_ctas = v.max_ctas;
   p.tmul = mul;
   p.tadd = add;

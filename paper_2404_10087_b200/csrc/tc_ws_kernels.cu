@@ -50,6 +50,7 @@ struct __align__(64) WsParams {
   const float* b[kN];
   int64_t nnz, ntiles, tmul, tadd, tile_base;
   const int32_t* tile_rows;
+  const int64_t* tperm;  // device {mul, add} or null (KView::tperm)
   float lr, reg;
   int atomic_update, prec3;
   float* partials;
@@ -120,7 +121,9 @@ __device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)
 
 __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
-  return p.tile_base + (t * p.tmul + p.tadd) % p.ntiles;
+  const int64_t mul = p.tperm ? __ldg(p.tperm) : p.tmul;
+  const int64_t add = p.tperm ? __ldg(p.tperm + 1) : p.tadd;
+  return p.tile_base + (t * mul + add) % p.ntiles;
 }
 
 template <bool kCore>
@@ -675,6 +678,7 @@ bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, 
   p.ntiles = v.ntiles;
   p.tile_base = v.tile_base;
   p.tile_rows = v.tile_rows;
+  p.tperm = v.tperm;
   p.tmul = mul;
   p.tadd = add;
   return true;

@@ -170,7 +170,19 @@ class DsgdTrainer:
         r0, rn = self.layout.rows(mode, (held + 1) % P)
         self.be.shift(mode, s0, sn, r0, rn)
 
+    def cell_seeds(self, epoch_seed: int) -> np.ndarray:
+        P = self.P
+        return np.array([stratum_seed(epoch_seed, s, t) for s in range(P) for t in range(P)],
+                        np.uint64)
+
     def factor_phase(self, epoch_seed: int):
+        """One factor phase.  A backend with ``factor_epoch`` runs the whole
+        stratum loop natively (one call, CUDA-graph replay); otherwise the
+        loop below drives ``factor_cell``/``shift``/``allgather``."""
+        fused = getattr(self.be, "factor_epoch", None)
+        if fused is not None:
+            fused(self.layout, self.cell_seeds(epoch_seed))
+            return
         P, g = self.P, self.rank
         for s in range(P):
             for t in range(P):
@@ -229,6 +241,11 @@ class EngineBackend:
         session.upload_tensor(slot, dims, idx, vals)
         session.set_cells(slot, cell_off)
         session.set_option("global_nnz", int(global_nnz))
+
+    def factor_epoch(self, layout: Layout, cell_seeds):
+        """The whole stratum loop in libftkcu (ftkcu_dsgd_factor_epoch)."""
+        self.s.dsgd_factor_epoch(self.slot, layout.parts, layout.row_off[1], layout.row_off[2],
+                                 cell_seeds, self.lr_a, self.reg_a)
 
     def set_grid_cap(self, ctas: int):
         self.s.set_option("max_ctas", int(ctas))

@@ -199,6 +199,8 @@ def engine_host_backend_cls():
     from paper_2404_10087_b200.dsgd import EngineBackend
 
     class EngineHostBackend(EngineBackend):
+        factor_epoch = None  # drive the Python stratum loop (host collectives)
+
         def __init__(self, group, *a, **k):
             super().__init__(*a, **k)
             self.g = group

@@ -148,3 +148,39 @@ def test_nccl_row_exchange_plumbing_world1():
             s.sendrecv_rows(1, 35, 10, 0, 0, 10, 0)  # past the end of mode 2
         with pytest.raises(eng.FtkError):
             s.bcast_rows(0, np.array([0, 10, 64], np.int64))  # 2 blocks, world 1
+
+
+@pytest.mark.parametrize("graphs", [1, 0])
+def test_fused_stratum_loop_matches_python_loop(graphs):
+    """ftkcu_dsgd_factor_epoch (native loop, optionally a CUDA graph) runs the
+    same schedule as the Python loop: one rank emulating P=3 parts over a
+    1-rank communicator (shifts to itself), same cell seeds."""
+    t = O.random_tensor([300, 200, 120], 30_000, 6, 0.0, 2.0)
+    m = O.random_model(t.dims, [16] * 3, 16, 5)
+    lay = dsgd.make_layout(t.dims, t.idx, 3)
+    idx, vals, off, _ = dsgd.local_cells(lay, t.idx, t.vals, 0)
+    outs = []
+    for fused in (False, True):
+        with eng.Session(0) as s:
+            s.set_option("graphs", graphs)
+            s.set_option("max_ctas", 1)  # one CTA: tiles in order, close to deterministic
+            s.upload_model(t.dims, m.ranks, m.r, [x.copy() for x in m.a],
+                           [x.copy() for x in m.b])
+            s.comm_init(eng.Session.comm_unique_id(), 0, 1)
+
+            class Self(dsgd.EngineBackend):
+                def allgather(self, mode, row_off):
+                    pass
+
+            be = Self(s, 0, idx, vals, off, t.dims, t.nnz, lr_a=0.02, lr_b=0.02, world=1)
+            if not fused:
+                be.factor_epoch = None
+            tr = dsgd.DsgdTrainer(be, lay, 0)
+            for e in range(3):
+                tr.factor_phase(host.derive_seed(9, [e]))
+            s.sync()
+            outs.append(s.download_model()[0])
+            launches = s.get_option("launches")
+            assert launches == 3 * 9 * 1  # one sweep kernel per cell per epoch
+    for n in range(3):
+        np.testing.assert_allclose(outs[1][n], outs[0][n], rtol=2e-3, atol=2e-5)
