@@ -219,12 +219,26 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
     if (lane == 0) mbar_expect_tx(&bars[B_FULL + s], L::kSlot);
     __syncwarp();
     uint8_t* slot = sm + L::o_a + s * L::kSlot;
+    // One elected thread issues all 96 gathers of the tile: per-lane
+    // operands would make the compiler serialise every TMA issue over the
+    // 32 lanes (R2UR.BROADCAST waterfall).
+    if (elect_one()) {
 #pragma unroll
-    for (int n = 0; n < kN; ++n) {
-      const int4 r = *reinterpret_cast<const int4*>(s_idx + n * kRows + lane * 4);
-      tma_gather4(slot + n * kModeTile + lane * 512, &p.tmap[n], 0, r.x, r.y, r.z, r.w,
-                  &bars[B_FULL + s]);
+      for (int n = 0; n < kN; ++n) {
+#pragma unroll
+        for (int g0 = 0; g0 < kRows / 4; g0 += 8) {
+          int4 r[8];  // 8 index loads in flight before the issues
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            r[g] = *reinterpret_cast<const int4*>(s_idx + n * kRows + (g0 + g) * 4);
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            tma_gather4(slot + n * kModeTile + (g0 + g) * 512, &p.tmap[n], 0, r[g].x, r[g].y,
+                        r[g].z, r[g].w, &bars[B_FULL + s]);
+        }
+      }
     }
+    __syncwarp();
   }
 }
 
