@@ -515,7 +515,8 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
 static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t add,
                          float lr_a, float reg_a) {
   if (v.ntiles <= 0) return FTKCU_OK;
-  if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
+  // the WS factor sweep is single-pass tf32; 3xtf32 runs on the tc sweep
+  if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
   } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {

@@ -68,13 +68,16 @@ struct WsLayout {
   static constexpr uint32_t o_bt = o_d + d_bytes;       // B^T hi  (C GEMM operand)
   static constexpr uint32_t o_btlo = o_bt + kN * 4096;  // B^T lo
   static constexpr uint32_t o_b = o_btlo + kN * 4096;   // B (U GEMM operand, factor)
-  static constexpr uint32_t o_idx = o_b + (kCore ? 0 : kN * 4096);
+  // factor: -lr reg I (K-major), the regulariser as a second U GEMM operand
+  static constexpr uint32_t o_diag = o_b + (kCore ? 0 : kN * 4096);
+  static constexpr uint32_t o_idx = o_diag + (kCore ? 0 : 4096);
   static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
   static constexpr int kI = kCore ? 4 : 6;  // COO-column ring depth (decoupled from A slots)
   static constexpr uint32_t o_stage = o_idx + kI * kIdxSlot;  // factor: per-quarter write-back rows
   static constexpr uint32_t stage_bytes = kCore ? 0 : 4 * 32 * 128;
   static constexpr uint32_t o_xp = o_stage + stage_bytes;  // x_hat halves [2][2][128]
-  static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
+  static constexpr uint32_t o_rows = o_xp + 2 * 2 * kRows * 4;  // [kI] valid rows per COO slot
+  static constexpr uint32_t o_bar = o_rows + 64;
   static constexpr int kBars = 32;
   static constexpr uint32_t o_tmem = o_bar + kBars * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
@@ -90,11 +93,11 @@ enum : int {
   B_IEMPTY = 12,     // [kI <= 6] COO slot free
   B_CFULL = 18,      // [2]  C accumulator ready
   B_DFULL = 20,      // factor [2]: D in TMEM; core [1]: D tile in smem
-  B_UFULL = 22,      // factor [2]: U ready
-  B_TEMPTY = 24,     // factor [2]: TMEM buffer free
-  B_LO = 26,         // factor: A_lo in TMEM (split tf32)
+  B_UFULL = 22,      // factor [1]: U ready
+  B_UEMPTY = 23,     // factor [1]: U read by the epilogue
+  B_CEMPTY = 24,     // factor [2]: C read by the epilogue
   B_AFULL = 27,      // core: A rows copied to TMEM
-  B_DEMPTY = 28,     // core: G GEMM done with the D tile
+  B_DEMPTY = 28,     // core [1]: G GEMM done with the D tile; factor [2]: U done with D[b]
 };
 
 // Round-to-nearest for an operand the tensor core will read as tf32: it
@@ -141,10 +144,18 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
         *reinterpret_cast<float*>(sm + L::o_b + n * 4096 + swz(j, r * 4, 128)) = hi;
     }
   }
+  if constexpr (!kCore)
+    for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
+      const int j = e / kW, jj = e - j * kW;
+      *reinterpret_cast<float*>(sm + L::o_diag + swz(j, jj * 4, 128)) =
+          j == jj ? tf32_rna(-p.lr * p.reg) : 0.0f;
+    }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&bars[B_FULL + s], 1);
-      mbar_init(&bars[B_EMPTY + s], kCore ? 1 : kEpiWarps);
+      // core, and factor with atomic rows: released by the MMA that last
+      // reads the slot; factor overwrite mode: by the epilogue (reads a)
+      mbar_init(&bars[B_EMPTY + s], (kCore || p.atomic_update) ? 1 : kEpiWarps);
     }
     for (int i = 0; i < L::kI; ++i) {
       mbar_init(&bars[B_IFULL + i], 1);
@@ -153,12 +164,12 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[B_CFULL + b], 1);
       mbar_init(&bars[B_DFULL + b], kEpiWarps);
-      mbar_init(&bars[B_UFULL + b], 1);
-      mbar_init(&bars[B_TEMPTY + b], kEpiWarps);
+      mbar_init(&bars[B_CEMPTY + b], kEpiWarps);
+      mbar_init(&bars[B_DEMPTY + b], 1);
     }
-    mbar_init(&bars[B_LO], kEpiWarps);
+    mbar_init(&bars[B_UFULL], 1);
+    mbar_init(&bars[B_UEMPTY], kEpiWarps);
     mbar_init(&bars[B_AFULL], kEpiWarps);
-    mbar_init(&bars[B_DEMPTY], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x / 32 == 1) {
@@ -194,6 +205,9 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
     const int64_t tile = ws_tile(p, k);
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+    // valid-row count of the tile rides with its COO slot (published by the
+    // arrive below), keeping the global load off the epilogue's critical path
+    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
     mbar_expect_tx(&bars[B_IFULL + i], L::kIdxSlot);
     for (int n = 0; n < kN; ++n)
       bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
@@ -255,8 +269,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // TMEM: per buffer b: C/U at 192 b, D at 192 b + 96; A_lo at 384.
-  constexpr uint32_t kLo = 384;
+  // TMEM columns: C[b] at 96 b, D[b] at 192 + 96 b, U at 384 (480 of 512).
+  // Separate C / D / U buffers let C(k+1) and U(k) run on the tensor core
+  // while the epilogue works on the other tile, with no wait in between.
+  constexpr uint32_t kC = 0, kD = 192, kU = 384;
 
   if (warp == 0) {
     ws_idx_producer<false>(p, sm, bars, nk);
@@ -265,40 +281,45 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
-      const uint32_t bt = smem_u32(sm + L::o_bt), btl = smem_u32(sm + L::o_btlo);
-      const uint32_t bb = smem_u32(sm + L::o_b);
-      auto issue_u = [&](int64_t k) {
-        const int b = (int)(k & 1);
-        mbar_wait(&bars[B_DFULL + b], (uint32_t)((k >> 1) & 1));
+      const uint32_t bt = smem_u32(sm + L::o_bt), bb = smem_u32(sm + L::o_b);
+      const uint32_t dg = smem_u32(sm + L::o_diag);
+      // U(j) = (lr r D_j) B^T [+ A_j (-lr reg I)]: the step itself (atomic
+      // rows) or U for the overwrite rule (scaled in the epilogue).
+      auto issue_u = [&](int64_t j) {
+        const int b = (int)(j & 1), s = (int)(j % kS);
+        mbar_wait(&bars[B_DFULL + b], (uint32_t)((j >> 1) & 1));
+        mbar_wait(&bars[B_UEMPTY], (uint32_t)((j & 1) ^ 1));
         tc_after();
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
-        for (int n = 0; n < kN; ++n)
+        for (int n = 0; n < kN; ++n) {
 #pragma unroll
           for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ts(tmem + b * 192 + n * kW, tmem + b * 192 + 96 + n * kW + ks * 8,
+            mma_ts(tmem + kU + n * kW, tmem + kD + b * 96 + n * kW + ks * 8,
                    sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
-        mma_commit(&bars[B_UFULL + b]);
+          if constexpr (kAtomic)
+#pragma unroll
+            for (int ks = 0; ks < kW / 8; ++ks)
+              mma_ss(tmem + kU + n * kW, sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
+                     sdesc(dg + ks * 32, 16, 1024, 128), id, 1);
+        }
+        mma_commit(&bars[B_UFULL]);
+        mma_commit(&bars[B_DEMPTY + b]);
+        if constexpr (kAtomic) mma_commit(&bars[B_EMPTY + s]);  // last read of the A slot
       };
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kS), b = (int)(k & 1);
         mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
-        mbar_wait(&bars[B_TEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
-        if (p.prec3) mbar_wait(&bars[B_LO], (uint32_t)(k & 1));
+        mbar_wait(&bars[B_CEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
         for (int n = 0; n < kN; ++n)
 #pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks) {
-            const uint64_t da = sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128);
-            const uint64_t db = sdesc(bt + n * 4096 + ks * 32, 16, 1024, 128);
-            mma_ss(tmem + b * 192 + n * kW, da, db, id, ks > 0);
-            if (p.prec3) {
-              mma_ss(tmem + b * 192 + n * kW, da, sdesc(btl + n * 4096 + ks * 32, 16, 1024, 128),
-                     id, 1);
-              mma_ts(tmem + b * 192 + n * kW, tmem + kLo + n * kW + ks * 8, db, id, 1);
-            }
-          }
+          for (int ks = 0; ks < kW / 8; ++ks)
+            mma_ss(tmem + kC + b * 96 + n * kW,
+                   sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
+                   sdesc(bt + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
         mma_commit(&bars[B_CFULL + b]);
         if (k >= 1) issue_u(k - 1);
       }
@@ -308,40 +329,11 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
     const int ew = warp - 2, q = warp & 3, h = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    // Split-tf32: this row's (half of the) factor rows minus their truncated
-    // tf32 part, into TMEM for the lo x hi MMA.
-    auto stage_lo = [&](int64_t k) {
-      const int s = (int)(k % kS);
-      mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
-      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
-#pragma unroll
-      for (int n = 0; n < kN; ++n) {
-        uint32_t v[16];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const float4 x =
-              *reinterpret_cast<const float4*>(slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
-          v[q4 * 4 + 0] = __float_as_uint(x.x - tf32_trunc(x.x));
-          v[q4 * 4 + 1] = __float_as_uint(x.y - tf32_trunc(x.y));
-          v[q4 * 4 + 2] = __float_as_uint(x.z - tf32_trunc(x.z));
-          v[q4 * 4 + 3] = __float_as_uint(x.w - tf32_trunc(x.w));
-        }
-        tmem_st16(tl + kLo + n * kW + h * 16, v);
-      }
-      tmem_wait_st();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_LO]);
-    };
     // Software pipeline: epi1(k + 1) runs while U(k) is on the tensor core.
-    // epi1: C -> D (TMEM), residual, and this thread's A snapshot + global
-    // row indices into registers, after which the smem slot is released.
-    // epi2: U -> step -> vector RED (or STG) of the row's column half.
-    // kAtomic: the snapshot only feeds the regulariser lr reg a (~1e-7 a),
-    // so an fp16 copy suffices and the slot is released in epi1.  Overwrite
-    // mode (a' = a + step) keeps the slot until epi2 and reads fp32 there.
+    // epi1: C -> residual -> D' = (lr r) D into TMEM, global row indices into
+    // registers.  epi2: U -> step -> coalesced vector RED (or STG) of the
+    // row's column half.
     struct Tile {
-      __half2 a[kAtomic ? kN : 1][8];
       int32_t g[kN];
       float resid;
       bool ok;
@@ -350,54 +342,49 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
     Tile cur, nxt;
     auto epi1 = [&](int64_t k, Tile& t) {
       const int s = (int)(k % kS), b = (int)(k & 1), ii = (int)(k % L::kI);
-      const int64_t tile = ws_tile(p, k);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
-      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
       mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
       float c[kN][16];
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
-        tmem_ld16(tl + b * 192 + n * kW + h * 16, v);
+        tmem_ld16(tl + kC + b * 96 + n * kW + h * 16, v);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
       }
-      if (p.prec3 && k + 1 < nk) stage_lo(k + 1);
-      const float xhat = xhat_full(tl + b * 192 + (h ^ 1) * 16, c);
+      const float xhat = xhat_full(tl + kC + b * 96 + (h ^ 1) * 16, c);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_CEMPTY + b]);  // C(k + 2) may land
       t.slot = s;
 #pragma unroll
-      for (int n = 0; n < kN; ++n) {
-        t.g[n] = s_idx[n * kRows + row];
-        if constexpr (kAtomic) {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const float4 x = *reinterpret_cast<const float4*>(
-                slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
-            t.a[n][q4 * 2 + 0] = __floats2half2_rn(x.x, x.y);
-            t.a[n][q4 * 2 + 1] = __floats2half2_rn(x.z, x.w);
-          }
-        }
-      }
+      for (int n = 0; n < kN; ++n) t.g[n] = s_idx[n * kRows + row];
       const float xv = s_val[row];
+      const int nvalid = reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);  // COO slot may be refilled
-      if constexpr (kAtomic) {
-        if (lane == 0) mbar_arrive(&bars[B_EMPTY + s]);  // slot k may be refilled
-      }
-      t.ok = row < __ldg(p.tile_rows + tile);
+      t.ok = row < nvalid;
       t.resid = t.ok ? xv - xhat : 0.0f;
+      // kAtomic: D' = lr r D, so the U GEMM (plus A x (-lr reg I)) yields the
+      // step itself; overwrite mode scales in epi2.
+      const float sc = kAtomic ? p.lr * t.resid : 1.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c[0][i] *= sc;  // D'_1 = (sc c0) c2, D'_2 = (sc c0) c1
+      mbar_wait(&bars[B_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // U(k - 2) read D[b]
+      tc_after();
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float d = n == 0 ? c[1][i] * c[2][i] : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
+          const float d = n == 0 ? (c[1][i] * sc) * c[2][i]
+                                 : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
           v[i] = tf32_rn_bits(d);
         }
-        tmem_st16(tl + b * 192 + 96 + n * kW + h * 16, v);
+        tmem_st16(tl + kD + b * 96 + n * kW + h * 16, v);
       }
       tmem_wait_st();
       tc_before();
@@ -405,16 +392,15 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
     };
     auto epi2 = [&](int64_t k, const Tile& t) {
-      const int b = (int)(k & 1);
-      mbar_wait(&bars[B_UFULL + b], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
       tc_after();
       uint32_t u[kN][16];
 #pragma unroll
-      for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 192 + n * kW + h * 16, u[n]);
+      for (int n = 0; n < kN; ++n) tmem_ld16(tl + kU + n * kW + h * 16, u[n]);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_TEMPTY + b]);
+      if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
       const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
       // Per mode: both warps of the quarter write their column half of the
@@ -426,25 +412,17 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       for (int n = 0; n < kN; ++n) {
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          float4 a;
-          if constexpr (kAtomic) {
-            const float2 lo = __half22float2(t.a[n][q4 * 2 + 0]);
-            const float2 hi = __half22float2(t.a[n][q4 * 2 + 1]);
-            a = make_float4(lo.x, lo.y, hi.x, hi.y);
-          } else {
-            a = *reinterpret_cast<const float4*>(slot + n * kModeTile +
-                                                 swz(row, (h * 16 + q4 * 4) * 4, 128));
-          }
           float4 st;
-          st.x = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 0]), -lr_reg * a.x);
-          st.y = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 1]), -lr_reg * a.y);
-          st.z = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
-          st.w = fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
-          if constexpr (!kAtomic) {
-            st.x += a.x;
-            st.y += a.y;
-            st.z += a.z;
-            st.w += a.w;
+          if constexpr (kAtomic) {  // the accumulator already holds the step
+            st = make_float4(__uint_as_float(u[n][q4 * 4 + 0]), __uint_as_float(u[n][q4 * 4 + 1]),
+                             __uint_as_float(u[n][q4 * 4 + 2]), __uint_as_float(u[n][q4 * 4 + 3]));
+          } else {
+            const float4 a = *reinterpret_cast<const float4*>(
+                slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+            st.x = a.x + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 0]), -lr_reg * a.x);
+            st.y = a.y + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 1]), -lr_reg * a.y);
+            st.z = a.z + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
+            st.w = a.w + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
           }
           *reinterpret_cast<float4*>(stage + swz(lane, (h * 16 + q4 * 4) * 4, 128)) = st;
         }
@@ -471,7 +449,6 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);
       }
     };
-    if (p.prec3 && nk > 0) stage_lo(0);
     if (nk > 0) epi1(0, cur);
     for (int64_t k = 0; k < nk; ++k) {
       if (k + 1 < nk) epi1(k + 1, nxt);
@@ -605,7 +582,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
       }
       const float xhat = xhat_full(tl + b * 96 + (h ^ 1) * 16, c);
       if (k + 1 < nk) stage_a(k + 1);  // C(k) is complete: A rows TMEM is free
-      const bool ok = row < __ldg(p.tile_rows + tile);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
       const float resid = ok ? s_val[row] - xhat : 0.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);
