@@ -493,10 +493,11 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
         const uint64_t da = sdesc_l(a0, kModeTile, 512, 1);
         const uint64_t dd = sdesc_l(d0, kModeTile, 512, 1);
+        if (!(p.exp & 4))  // exp 4: no G GEMM (timing only)
 #pragma unroll 4
-        for (int ks = 0; ks < kRows / 8; ++ks)
-          mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
-                 (k > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < kRows / 8; ++ks)
+            mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
+                   (k > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&bars[B_DEMPTY]);
         if (!(p.exp & 1)) mma_commit(&bars[B_EMPTY + s]);
       };
@@ -535,6 +536,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
+        if (p.exp & 8) {  // exp 8: no smem reads of the rows (timing only)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0x3f800000u;
+        } else
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const float4 x = *reinterpret_cast<const float4*>(slot + n * kModeTile +
