@@ -131,16 +131,25 @@ class ClockSampler:
 
 
 def make_workload(cfg_name, rank_override, world, rank, device):
+    """Training tensor of exactly cfg["nnz"] nonzeros plus a held-out test set
+    (fraction cfg["test_frac"] of all generated tuples): the
+    generator's storage order is a uniform shuffle, so its tail is a uniform
+    random split, as split_train_test's (sparse_tensor.cpp:180-196)."""
     from paper_2404_10087_b200 import synth
 
     cfg = dict(synth.CONFIGS[cfg_name])
     j = rank_override or cfg["rank"]
+    frac = cfg.get("test_frac", 0.014)
+    total = int(round(cfg["nnz"] / (1.0 - frac)))
     if cfg["nnz"] >= 10_000_000:
-        coo = synth.uniform_torch(cfg["dims"], cfg["nnz"], cfg["seed"], cfg["lo"], cfg["hi"],
-                                  device=f"cuda:{device}")
+        full = synth.uniform_torch(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"],
+                                   device=f"cuda:{device}")
     else:
-        coo = synth.uniform_numpy(cfg["dims"], cfg["nnz"], cfg["seed"], cfg["lo"], cfg["hi"])
-    return cfg, j, coo
+        full = synth.uniform_numpy(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"])
+    n = cfg["nnz"]
+    coo = synth.Coo(full.dims, full.idx[:n], full.vals[:n])
+    test = synth.Coo(full.dims, np.ascontiguousarray(full.idx[n:]), np.ascontiguousarray(full.vals[n:]))
+    return cfg, j, coo, test
 
 
 def cpu_reference_time(cfg, j, sample_nnz, steps=1, warmup=1):
@@ -243,6 +252,15 @@ class SingleGpu:
         out = self.s.eval(0, 1, 1e-4, 1e-4)
         return float(out[0] + out[2])
 
+    def add_test(self, test):
+        self.n_test = test.nnz
+        self.s.upload_tensor(1, test.dims, test.idx, test.vals)
+
+    def test_rmse_mae(self):
+        """ftk::evaluate on the held-out set (evaluation.cpp:55-72)."""
+        out = self.s.eval(1, 1, 0.0, 0.0)
+        return float(np.sqrt(out[0] / self.n_test)), float(out[1] / self.n_test)
+
 
 class Dsgd(SingleGpu):
     """DSGD strata over the ranks (paper_2404_10087_b200/dsgd.py): rank g
@@ -286,6 +304,15 @@ class Dsgd(SingleGpu):
         self.tr.finalize()
         return float(self.tr.loss())
 
+    def add_test(self, test):
+        # after finalize() every rank holds the whole model: any share works
+        self.n_test = test.nnz
+        self.be.add_eval(np.ascontiguousarray(test.idx[self.rank::self.world]),
+                         np.ascontiguousarray(test.vals[self.rank::self.world]), test.dims)
+
+    def test_rmse_mae(self):
+        return self.tr.rmse_mae(1)
+
 
 def run_engine(args):
     import torch
@@ -300,7 +327,7 @@ def run_engine(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    cfg, j, coo = make_workload(args.config, args.rank, world, rank, local)
+    cfg, j, coo, test = make_workload(args.config, args.rank, world, rank, local)
     order = coo.order
     ranks = [j] * order
     s = eng.Session(local)
@@ -326,6 +353,7 @@ def run_engine(args):
     else:
         job = SingleGpu(eng, host, s, coo, ranks, j, a0, b0, world)
         job.upload()
+    job.add_test(test)
     ext = torch.cuda.ExternalStream(s.stream_handle, device=dev)
 
     def barrier():
@@ -339,6 +367,7 @@ def run_engine(args):
         job.factor(es)
         job.core(es)
     loss0 = job.train_loss()
+    test0 = job.test_rmse_mae()
     barrier()
     # per-phase events inside the timed region (same stream as the kernels)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
@@ -362,6 +391,7 @@ def run_engine(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     loss1 = job.train_loss()
+    test1 = job.test_rmse_mae()
     ms_step = total_ms / args.steps
     value = job.job_nnz / (ms_step * 1e-3)
 
@@ -407,9 +437,13 @@ def run_engine(args):
             "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": coo.nnz,
                        "J": j, "R": j, "M": 16, "mode": "hogwild", "precision": args.precision,
                        "parallelism": job.parallelism, "nnz_per_rank": job.local_nnz,
+                       "test_frac": cfg.get("test_frac", 0.014),
                        "l2": "inputs larger than L2 (COO stream 16 B/nnz per sweep)"},
             "phases_ms": {"factor": f_avg, "core": c_avg},
             "train_loss_before_after": [loss0, loss1],
+            "test_rmse_before_after": [test0[0], test1[0]],
+            "test_mae_before_after": [test0[1], test1[1]],
+            "test_nnz": test.nnz,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": dom_bytes,

@@ -125,6 +125,7 @@ cudaError_t launch_apply_core(const KView& v, float* grad, float lr_b,
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
                               float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
                               cudaStream_t st);
+size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm);
 cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                             float* grad, int blocks_per_sm, float* scratch,
                             size_t scratch_bytes, cudaStream_t st);

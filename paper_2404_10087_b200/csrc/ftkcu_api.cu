@@ -74,9 +74,11 @@ int fail(ftkcu_session* s, int code, const char* fmt, ...) {
 #define CK(call)                                                              \
   do {                                                                        \
     cudaError_t e_ = (call);                                                  \
-    if (e_ != cudaSuccess)                                                    \
+    if (e_ != cudaSuccess) {                                                  \
+      (void)cudaGetLastError(); /* clear a non-sticky launch error */         \
       return fail(s, FTKCU_ERR_CUDA, "%s: %s (%s:%d)", #call,                 \
                   cudaGetErrorString(e_), __FILE__, __LINE__);                \
+    }                                                                         \
   } while (0)
 
 #define NK(call)                                                              \
@@ -622,7 +624,9 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     v = make_view(s, t, true);
     int64_t mul = 1, add = 0;
     if (!perm) tile_perm(seed ^ 0xc0e5ull, v.ntiles, &mul, &add);
-    const size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
+    size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
+    const size_t hog_need = hog_core_scratch_bytes(v, (int)s->opt_hog_bps);
+    if (hog_need > need) need = hog_need;
     if ((rc = ensure_scratch(s, need))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
     if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {

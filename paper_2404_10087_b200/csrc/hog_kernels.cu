@@ -79,7 +79,10 @@ struct HogLayout {
   int aoff[kMaxOrder];  // offsets of mode blocks inside one G-row of a
   size_t o_b[kMaxOrder], o_bt[kMaxOrder];
   size_t o_warp, warp_floats, o_acc, acc_floats, end;  // floats
+  int acc_global;  // per-warp gradient accumulators in global scratch (large J R)
 };
+
+constexpr size_t kHogSmemCap = 200 * 1024;
 
 __host__ __device__ inline HogLayout hog_layout(const KView& v, bool core, int warps) {
   HogLayout L{};
@@ -105,7 +108,11 @@ __host__ __device__ inline HogLayout hog_layout(const KView& v, bool core, int w
   o += L.warp_floats * warps;
   L.o_acc = o;
   L.acc_floats = core ? (size_t)s * v.r : 0;
-  o += L.acc_floats * warps;
+  // J = R = 64 / 128: a warp's gradient (sum J x R floats) no longer fits
+  // next to its siblings' in shared memory; it then lives in global scratch
+  // (still one private accumulator per warp, so the sum stays deterministic).
+  L.acc_global = (o + L.acc_floats * warps) * sizeof(float) > kHogSmemCap;
+  if (!L.acc_global) o += L.acc_floats * warps;
   L.end = o;
   return L;
 }
@@ -272,13 +279,15 @@ hog_factor_kernel(KView v, int64_t tmul, int64_t tadd, float lr, float reg,
 }
 
 __global__ void __launch_bounds__(kHogThreads)
-hog_core_kernel(KView v, int64_t tmul, int64_t tadd, float* __restrict__ partials) {
+hog_core_kernel(KView v, int64_t tmul, int64_t tadd, float* __restrict__ partials,
+                float* __restrict__ gacc) {
   extern __shared__ float sm[];
   const int warps = blockDim.x / 32;
   const HogLayout L = hog_layout(v, true, warps);
   load_b(v, L, sm);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  float* acc = sm + L.o_acc + L.acc_floats * wid;
+  float* acc = L.acc_global ? gacc + ((size_t)blockIdx.x * warps + wid) * L.acc_floats
+                            : sm + L.o_acc + L.acc_floats * wid;
   for (size_t e = lane; e < L.acc_floats; e += 32) acc[e] = 0.0f;
   __syncthreads();
   float* w = sm + L.o_warp + L.warp_floats * wid;
@@ -316,9 +325,10 @@ hog_core_kernel(KView v, int64_t tmul, int64_t tadd, float* __restrict__ partial
   }
   __syncthreads();
   // CTA reduction in warp order, then one partial per CTA.
+  const float* accs = L.acc_global ? gacc + (size_t)blockIdx.x * warps * L.acc_floats : sm + L.o_acc;
   for (size_t e = threadIdx.x; e < L.acc_floats; e += blockDim.x) {
     float s = 0.0f;
-    for (int k = 0; k < warps; ++k) s += sm[L.o_acc + L.acc_floats * k + e];
+    for (int k = 0; k < warps; ++k) s += accs[L.acc_floats * k + e];
     partials[(size_t)blockIdx.x * L.acc_floats + e] = s;
   }
 }
@@ -338,6 +348,13 @@ int hog_grid(int blocks_per_sm) { return num_sms() * (blocks_per_sm < 1 ? 1 : bl
 }  // namespace
 
 size_t shuffle_scratch_bytes(int64_t) { return 0; }
+
+size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm) {
+  const int warps = kHogThreads / 32;
+  const HogLayout L = hog_layout(v, true, warps);
+  const size_t grid = (size_t)hog_grid(blocks_per_sm);
+  return grid * L.acc_floats * sizeof(float) * (1 + (L.acc_global ? warps : 0));
+}
 
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void*, size_t, cudaStream_t st) {
@@ -434,11 +451,12 @@ cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
   const HogLayout L = hog_layout(v, true, warps);
   const size_t bytes = L.end * sizeof(float);
   const int grid = hog_grid(blocks_per_sm);
-  if (scratch_bytes < (size_t)grid * L.acc_floats * sizeof(float)) return cudaErrorInvalidValue;
+  if (scratch_bytes < hog_core_scratch_bytes(v, blocks_per_sm)) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(hog_core_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  hog_core_kernel<<<grid, kHogThreads, bytes, st>>>(v, tile_mul, tile_add, scratch);
+  float* gacc = scratch + (size_t)grid * L.acc_floats;
+  hog_core_kernel<<<grid, kHogThreads, bytes, st>>>(v, tile_mul, tile_add, scratch, gacc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int len = (int)L.acc_floats;

@@ -39,18 +39,22 @@ constexpr int kStages = 3;
 
 static_assert(kTileRows == kHogTile, "tile size shared with the CUDA-core path");
 
+// Ranks below 16 (J or R = 8) run padded to 16: the padding columns of the
+// operand tiles are zero (set once, never written), so they add exact zeros
+// to every contraction; the C GEMM skips the all-zero K steps.
 template <int N, int J, int R, bool kCore>
 struct TcLayout {
-  static constexpr uint32_t PJ = J * 4, PR = R * 4;
+  static constexpr int JP = J < 16 ? 16 : J, RP = R < 16 ? 16 : R;
+  static constexpr uint32_t PJ = JP * 4, PR = RP * 4;
   // factor sweep: per-mode K-major tiles of 128 rows x PJ bytes (SW128/SW64)
   static constexpr uint32_t kA = kTileRows * PJ;
   // core sweep: stacked rows j' = n J + j in 128-B segments (BASE32B layout)
   static constexpr uint32_t kSeg = kTileRows * 128;
-  static constexpr uint32_t NS = (N * J + 31) / 32;   // A segments per row
-  static constexpr uint32_t NSD = (N * R + 31) / 32;  // D segments per row
+  static constexpr uint32_t NS = (N * JP + 31) / 32;   // A segments per row
+  static constexpr uint32_t NSD = (N * RP + 31) / 32;  // D segments per row
   static constexpr uint32_t kSlot = kCore ? NS * kSeg : N * kA;
-  static constexpr uint32_t kBt = R * PJ;                // B^T per mode (C GEMM operand)
-  static constexpr uint32_t kB = kCore ? 0 : J * PR;     // B per mode (U GEMM operand)
+  static constexpr uint32_t kBt = RP * PJ;               // B^T per mode (C GEMM operand)
+  static constexpr uint32_t kB = kCore ? 0 : JP * PR;    // B per mode (U GEMM operand)
   // The core G GEMM reads M = 128 stacked rows = 4 segments: the (4 - NS)
   // garbage segments past a slot must still be inside shared memory.
   static constexpr uint32_t kOverrun = kCore ? (4 - NS) * kSeg : 0;
@@ -69,15 +73,15 @@ struct TcLayout {
   // TMEM columns: C (then U in the factor sweep); D (factor) or G (core);
   // the core sweep's copy of the gathered rows (A operand of its C GEMM).
   static constexpr uint32_t t_c = 0;
-  static constexpr uint32_t t_x = kCore ? N * R : N * (R > J ? R : J);
-  static constexpr uint32_t t_a = t_x + N * R;                       // core: A rows (hi)
+  static constexpr uint32_t t_x = kCore ? N * RP : N * (RP > JP ? RP : JP);
+  static constexpr uint32_t t_a = t_x + N * RP;                      // core: A rows (hi)
   static constexpr uint32_t t_alo = t_a + (kCore ? NS * 32 : 0);     // A rows, low part
-  static constexpr uint32_t cols_used = t_alo + (kCore ? NS * 32 : N * J);
+  static constexpr uint32_t cols_used = t_alo + (kCore ? NS * 32 : N * JP);
   static constexpr uint32_t cols = cols_used <= 32 ? 32 : cols_used <= 64 ? 64
                                    : cols_used <= 128 ? 128 : cols_used <= 256 ? 256 : 512;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
   static_assert(cols_used <= 512, "TMEM budget");
-  static_assert(!kCore || N * J <= 128, "stacked core-gradient rows exceed M = 128");
+  static_assert(!kCore || N * JP <= 128, "stacked core-gradient rows exceed M = 128");
 };
 
 struct TcParams {
@@ -102,9 +106,9 @@ __device__ void load_b_tiles(const TcParams& p, uint8_t* sm) {
   using L = TcLayout<N, J, R, kCore>;
   for (int n = 0; n < N; ++n) {
     const float* b = p.b[n];
-    for (int e = threadIdx.x; e < J * R; e += kThreads) {
-      const int j = e / R, r = e - j * R;
-      const float x = b[e];
+    for (int e = threadIdx.x; e < L::JP * L::RP; e += kThreads) {
+      const int j = e / L::RP, r = e - j * L::RP;
+      const float x = (j < J && r < R) ? b[j * R + r] : 0.0f;
       const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
       // C GEMM B operand: rows r, K = j (hi and lo tf32 halves).
       *reinterpret_cast<float*>(sm + L::o_bt + n * L::kBt + swz(r, j * 4, L::PJ)) = hi;
@@ -168,7 +172,7 @@ __device__ void stage_tile(const TcParams& p, uint8_t* sm, int slot, const Rec<N
       const int row = warp * 32 + rl;
       uint32_t dst;
       if constexpr (kCore) {  // stacked row byte n J 4 + 16 ch, BASE32B segments
-        const uint32_t byte = n * J * 4 + ch * 16;
+        const uint32_t byte = n * L::JP * 4 + ch * 16;
         dst = (byte >> 7) * L::kSeg + swz32(row, byte & 127);
       } else {
         dst = n * L::kA + swz(row, ch * 16, L::PJ);
@@ -183,6 +187,9 @@ template <int N, int J, int R, bool kCore>
 __device__ void cta_setup(const TcParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tmem_slot) {
   using L = TcLayout<N, J, R, kCore>;
   load_b_tiles<N, J, R, kCore>(p, sm);
+  if constexpr (J < 16)  // padding columns of the gathered rows stay zero
+    for (uint32_t o = threadIdx.x * 16; o < kStages * L::kSlot; o += kThreads * 16)
+      *reinterpret_cast<int4*>(sm + L::o_a + o) = make_int4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], kThreads);
     mbar_init(&bars[kStages], 1);
@@ -215,7 +222,7 @@ __device__ void cta_teardown(uint32_t tmem) {
 template <int N, int J, int R, bool kCore>
 __device__ __forceinline__ void issue_c(uint8_t* sm, int slot, uint32_t tmem, int prec3) {
   using L = TcLayout<N, J, R, kCore>;
-  constexpr uint32_t id = idesc_tf32(128, R, 0, 0);
+  constexpr uint32_t id = idesc_tf32(128, L::RP, 0, 0);
   const uint32_t a0 = smem_u32(sm + L::o_a + slot * L::kSlot);
   const uint32_t b0 = smem_u32(sm + L::o_bt);
   const uint32_t bl = smem_u32(sm + L::o_btlo);
@@ -224,12 +231,12 @@ __device__ __forceinline__ void issue_c(uint8_t* sm, int slot, uint32_t tmem, in
 #pragma unroll
     for (int ks = 0; ks < J / 8; ++ks) {
       const uint64_t da = sdesc(a0 + n * L::kA + ks * 32, 16, 8 * L::PJ, L::PJ);
-      mma_ss(tmem + L::t_c + n * R, da, sdesc(b0 + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ),
+      mma_ss(tmem + L::t_c + n * L::RP, da, sdesc(b0 + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ),
              id, ks > 0);
       if (prec3) {
-        mma_ss(tmem + L::t_c + n * R, da,
+        mma_ss(tmem + L::t_c + n * L::RP, da,
                sdesc(bl + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ), id, 1);
-        mma_ts(tmem + L::t_c + n * R, tmem + L::t_alo + n * J + ks * 8,
+        mma_ts(tmem + L::t_c + n * L::RP, tmem + L::t_alo + n * L::JP + ks * 8,
                sdesc(b0 + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ), id, 1);
       }
     }
@@ -244,7 +251,7 @@ __device__ __forceinline__ void stage_alo_factor(const uint8_t* tile, uint32_t t
 #pragma unroll
   for (int n = 0; n < N; ++n)
 #pragma unroll
-    for (int h = 0; h < J / 16; ++h) {
+    for (int h = 0; h < L::JP / 16; ++h) {
       uint32_t v[16];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
@@ -255,7 +262,7 @@ __device__ __forceinline__ void stage_alo_factor(const uint8_t* tile, uint32_t t
         v[q4 * 4 + 2] = __float_as_uint(x.z - tf32_trunc(x.z));
         v[q4 * 4 + 3] = __float_as_uint(x.w - tf32_trunc(x.w));
       }
-      tmem_st16(tlane + L::t_alo + n * J + h * 16, v);
+      tmem_st16(tlane + L::t_alo + n * L::JP + h * 16, v);
     }
   tmem_wait_st();
 }
@@ -340,31 +347,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_factor_kernel(TcParams p) {
     const float* s_val = reinterpret_cast<const float*>(sm + L::o_val) + slot * kTileRows;
     const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx) + slot * N * kTileRows;
     const bool ok = s_idx[t] >= 0;
-    float c[N][R], xhat;
-    load_c_form_d<N, R>(tlane + L::t_c, c, xhat);
+    constexpr int RP = L::RP, JP = L::JP;
+    float c[N][RP], xhat;
+    load_c_form_d<N, RP>(tlane + L::t_c, c, xhat);
     const float resid = ok ? s_val[t] - xhat : 0.0f;
     // D^(n) -> TMEM (A operand of the U GEMM).
 #pragma unroll
     for (int n = 0; n < N; ++n)
 #pragma unroll
-      for (int h = 0; h < R / 16; ++h) {
+      for (int h = 0; h < RP / 16; ++h) {
         uint32_t v[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = __float_as_uint(d_of<N, R>(c, n, h * 16 + q)) + 0x1000u;
-        tmem_st16(tlane + L::t_x + n * R + h * 16, v);
+        for (int q = 0; q < 16; ++q) v[q] = __float_as_uint(d_of<N, RP>(c, n, h * 16 + q)) + 0x1000u;
+        tmem_st16(tlane + L::t_x + n * RP + h * 16, v);
       }
     tmem_wait_st();
     tc_before();
     __syncthreads();
     if (t == 0) {
       tc_after();
-      constexpr uint32_t id = idesc_tf32(128, J, 0, 0);
+      constexpr uint32_t id = idesc_tf32(128, JP, 0, 0);
       const uint32_t b0 = smem_u32(sm + L::o_b);
 #pragma unroll
       for (int n = 0; n < N; ++n)
 #pragma unroll
         for (int ks = 0; ks < R / 8; ++ks)
-          mma_ts(tmem + L::t_c + n * J, tmem + L::t_x + n * R + ks * 8,
+          mma_ts(tmem + L::t_c + n * JP, tmem + L::t_x + n * RP + ks * 8,
                  sdesc(b0 + n * L::kB + ks * 32, 16, 8 * L::PR, L::PR), id, ks > 0);
       mma_commit(&bars[kStages]);
     }
@@ -377,9 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_factor_kernel(TcParams p) {
 #pragma unroll
     for (int n = 0; n < N; ++n) {
 #pragma unroll
-      for (int h = 0; h < J / 16; ++h) {
+      for (int h = 0; h < JP / 16; ++h) {
         uint32_t v[16];
-        tmem_ld16(tlane + L::t_c + n * J + h * 16, v);
+        tmem_ld16(tlane + L::t_c + n * JP + h * 16, v);
         tmem_wait_ld();
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
     __syncthreads();
     if (t == 0) {
       tc_after();
-      constexpr uint32_t id = idesc_tf32(128, R, 0, 0);
+      constexpr uint32_t id = idesc_tf32(128, L::RP, 0, 0);
       const uint32_t b0 = smem_u32(sm + L::o_bt);
       const uint32_t bl = smem_u32(sm + L::o_btlo);
 #pragma unroll
@@ -510,11 +518,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
         for (int ks = 0; ks < J / 8; ++ks)
         {
           const uint64_t db = sdesc(b0 + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ);
-          mma_ts(tmem + L::t_c + n * R, tmem + L::t_a + n * J + ks * 8, db, id, ks > 0);
+          mma_ts(tmem + L::t_c + n * L::RP, tmem + L::t_a + n * L::JP + ks * 8, db, id, ks > 0);
           if (p.prec3) {
-            mma_ts(tmem + L::t_c + n * R, tmem + L::t_a + n * J + ks * 8,
+            mma_ts(tmem + L::t_c + n * L::RP, tmem + L::t_a + n * L::JP + ks * 8,
                    sdesc(bl + n * L::kBt + ks * 32, 16, 8 * L::PJ, L::PJ), id, 1);
-            mma_ts(tmem + L::t_c + n * R, tmem + L::t_alo + n * J + ks * 8, db, id, 1);
+            mma_ts(tmem + L::t_c + n * L::RP, tmem + L::t_alo + n * L::JP + ks * 8, db, id, 1);
           }
         }
       mma_commit(&bars[kStages]);
@@ -526,8 +534,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
     const float* s_val = reinterpret_cast<const float*>(sm + L::o_val) + slot * kTileRows;
     const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx) + slot * N * kTileRows;
     const bool ok = s_idx[t] >= 0;
-    float c[N][R], xhat;
-    load_c_form_d<N, R>(tlane + L::t_c, c, xhat);
+    constexpr int RP = L::RP, JP = L::JP;
+    float c[N][RP], xhat;
+    load_c_form_d<N, RP>(tlane + L::t_c, c, xhat);
     const float resid = ok ? s_val[t] - xhat : 0.0f;
     if (p.dbg && blockIdx.x == 0 && k == 0) {
       p.dbg[t * 8 + 0] = resid;
@@ -541,14 +550,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
 #pragma unroll
     for (int n = 0; n < N; ++n)
 #pragma unroll
-      for (int q4 = 0; q4 < R / 4; ++q4) {
+      for (int q4 = 0; q4 < RP / 4; ++q4) {
         float4 d;
         // + half a tf32 ulp: the tensor core's truncation becomes rounding
-        d.x = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 0)) + 0x1000u);
-        d.y = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 1)) + 0x1000u);
-        d.z = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 2)) + 0x1000u);
-        d.w = __uint_as_float(__float_as_uint(resid * d_of<N, R>(c, n, q4 * 4 + 3)) + 0x1000u);
-        const uint32_t byte = (n * R + q4 * 4) * 4;
+        d.x = __uint_as_float(__float_as_uint(resid * d_of<N, RP>(c, n, q4 * 4 + 0)) + 0x1000u);
+        d.y = __uint_as_float(__float_as_uint(resid * d_of<N, RP>(c, n, q4 * 4 + 1)) + 0x1000u);
+        d.z = __uint_as_float(__float_as_uint(resid * d_of<N, RP>(c, n, q4 * 4 + 2)) + 0x1000u);
+        d.w = __uint_as_float(__float_as_uint(resid * d_of<N, RP>(c, n, q4 * 4 + 3)) + 0x1000u);
+        const uint32_t byte = (n * RP + q4 * 4) * 4;
         *reinterpret_cast<float4*>(sm + L::o_d + (byte >> 7) * L::kSeg + swz32(t, byte & 127)) = d;
       }
     fence_proxy_async();
@@ -559,16 +568,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
       // G[j'][r] += sum_t A[t][j'] (r_t D_n[t][r]): A = the gathered tile read
       // MN-major (M-blocks = modes, LBO = one mode tile), K = 8 nonzeros per
       // instruction (one swizzle atom of rows, SBO).
-      constexpr uint32_t id = idesc_tf32(128, R, 1, 1);
+      constexpr uint32_t id = idesc_tf32(128, RP, 1, 1);
       const uint32_t a0 = smem_u32(sm + L::o_a + slot * L::kSlot);
       const uint32_t d0 = smem_u32(sm + L::o_d);
 #pragma unroll
       for (int n = 0; n < N; ++n) {
-        const uint32_t dbyte = n * R * 4;
+        const uint32_t dbyte = n * RP * 4;
         const uint32_t dn = d0 + (dbyte >> 7) * L::kSeg + (dbyte & 127);
 #pragma unroll 4
         for (int ks = 0; ks < kTileRows / 8; ++ks)
-          mma_ss(tmem + L::t_x + n * R, sdesc_l(a0 + ks * 1024, L::kSeg, 512, 1),
+          mma_ss(tmem + L::t_x + n * RP, sdesc_l(a0 + ks * 1024, L::kSeg, 512, 1),
                  sdesc_l(dn + ks * 1024, L::kSeg, 512, 1), id, (k > 0 || ks > 0) ? 1u : 0u);
       }
       mma_commit(&bars[kStages]);
@@ -580,23 +589,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_core_kernel(TcParams p) {
   }
   // Publish this CTA's gradient: TMEM lane j' (stacked mode rows) holds
   // G_{mode(j')}[j' mod J][:] in column block mode(j').
+  constexpr int JP = L::JP, RP = L::RP;
   const int jrow = t;  // lane
-  const int mode = jrow / J;
+  const int mode = jrow / JP, jj = jrow - mode * JP;
   float* out = p.partials + (size_t)blockIdx.x * (N * J * R);
 #pragma unroll
   for (int n = 0; n < N; ++n) {
-    if (n * J >= (warp + 1) * 32 || (n + 1) * J <= warp * 32) continue;  // warp-uniform
+    if (n * JP >= (warp + 1) * 32 || (n + 1) * JP <= warp * 32) continue;  // warp-uniform
 #pragma unroll
-    for (int h = 0; h < R / 16; ++h) {
+    for (int h = 0; h < RP / 16; ++h) {
       uint32_t v[16];
-      tmem_ld16(tlane + L::t_x + n * R + h * 16, v);
+      tmem_ld16(tlane + L::t_x + n * RP + h * 16, v);
       tmem_wait_ld();
       if (p.dbg && blockIdx.x == 0 && h == 0) p.dbg[t * 8 + 6 + (n & 1)] = __uint_as_float(v[0]);
-      if (mode == n) {
+      if (mode == n && jj < J) {
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          out[((size_t)n * J + (jrow - n * J)) * R + h * 16 + q] =
-              nk > 0 ? __uint_as_float(v[q]) : 0.0f;
+          if (h * 16 + q < R)
+            out[((size_t)n * J + jj) * R + h * 16 + q] = nk > 0 ? __uint_as_float(v[q]) : 0.0f;
       }
     }
   }
@@ -680,15 +690,17 @@ cudaError_t run_core(TcParams p, float* grad, float* scratch, size_t scratch_byt
   return cudaGetLastError();
 }
 
-// Shape dispatch: uniform ranks J_n = J, J, R in {16, 32}, N in {3..6},
-// sum J <= 128 (the core sweep's stacked M).
+// Shape dispatch: uniform ranks J_n = J; (J, R) in {16, 32}^2 at N = 3,
+// J = R = 16 at N = 4..6, J = R = 8 (padded to 16) at N = 3..6; sum of the
+// padded J <= 128 (the core sweep's stacked M).
 template <bool kCore, typename F>
 cudaError_t dispatch(const KView& v, F&& f) {
   const int j = v.j[0], r = v.r, n = v.order;
 #define FTK_CASE(NN, JJ, RR) \
   if (n == NN && j == JJ && r == RR) return f.template operator()<NN, JJ, RR>();
   FTK_CASE(3, 32, 32) FTK_CASE(3, 16, 16) FTK_CASE(4, 16, 16) FTK_CASE(5, 16, 16)
-  FTK_CASE(6, 16, 16) FTK_CASE(3, 16, 32) FTK_CASE(3, 32, 16)
+  FTK_CASE(6, 16, 16) FTK_CASE(3, 16, 32) FTK_CASE(3, 32, 16) FTK_CASE(3, 8, 8)
+  FTK_CASE(4, 8, 8) FTK_CASE(5, 8, 8) FTK_CASE(6, 8, 8)
 #undef FTK_CASE
   return cudaErrorNotSupported;
 }
@@ -700,7 +712,7 @@ bool tc_supported(const KView& v) {
     if (v.j[n] != v.j[0]) return false;
   const int n = v.order, j = v.j[0], r = v.r;
   return (n == 3 && (j == 16 || j == 32) && (r == 16 || r == 32)) ||
-         (n >= 4 && n <= 6 && j == 16 && r == 16);
+         (n >= 4 && n <= 6 && j == 16 && r == 16) || (n >= 3 && n <= 6 && j == 8 && r == 8);
 }
 
 struct FactorLaunch {

@@ -24,7 +24,7 @@ CONFIGS = {
     "c1": dict(dims=(10000, 10000, 1000), nnz=1_000_000, rank=16, lo=1.0, hi=5.0, seed=1),
     "netflix": dict(dims=(480189, 17770, 2182), nnz=99_072_112, rank=32, lo=1.0, hi=5.0, seed=2),
     "yahoo": dict(dims=(1000990, 624961, 3075), nnz=250_272_286, rank=32, lo=0.025, hi=5.0,
-                  seed=3),
+                  seed=3, test_frac=0.01),
     "order6": dict(dims=(16384,) * 6, nnz=100_000_000, rank=16, lo=1.0, hi=5.0, seed=4),
 }
 
@@ -53,21 +53,52 @@ def _decode(keys, dims):
     return out
 
 
+# Mixed-radix keys must fit in int64; beyond that (order 6 at 2^14 per mode
+# is 2^84 cells) tuples are drawn per mode and deduplicated by a 64-bit hash
+# of the tuple (a hash collision only drops a tuple, never admits a repeat).
+_KEY_CELLS = float(2 ** 62)
+
+
+def _mix64(h):
+    """splitmix64 finaliser on uint64 (numpy, wrapping)."""
+    h = (h ^ (h >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    h = (h ^ (h >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return h ^ (h >> np.uint64(31))
+
+
+def _tuple_hash(idx):
+    h = np.zeros(idx.shape[0], np.uint64)
+    with np.errstate(over="ignore"):
+        for n in range(idx.shape[1]):
+            h = _mix64(h ^ (idx[:, n].astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)))
+    return h
+
+
 def uniform_numpy(dims, nnz, seed, lo=1.0, hi=5.0) -> Coo:
     dims = [int(d) for d in dims]
     cells = float(np.prod(np.array(dims, np.float64)))
     if nnz > cells:
         raise ValueError("nnz exceeds cell count")
     rng = np.random.default_rng(seed)
-    keys = np.empty(0, np.int64)
-    while keys.size < nnz:
-        need = nnz - keys.size
-        k = np.zeros(need + need // 64 + 16, np.int64)
-        for d in dims:
-            k = k * d + rng.integers(0, d, size=k.size)
-        keys = np.unique(np.concatenate([keys, k]))
-    keys = keys[rng.permutation(keys.size)[:nnz]]
-    idx = _decode(keys, dims)
+    if cells < _KEY_CELLS:
+        keys = np.empty(0, np.int64)
+        while keys.size < nnz:
+            need = nnz - keys.size
+            k = np.zeros(need + need // 64 + 16, np.int64)
+            for d in dims:
+                k = k * d + rng.integers(0, d, size=k.size)
+            keys = np.unique(np.concatenate([keys, k]))
+        keys = keys[rng.permutation(keys.size)[:nnz]]
+        idx = _decode(keys, dims)
+    else:
+        idx = np.empty((0, len(dims)), np.int32)
+        while idx.shape[0] < nnz:
+            need = nnz - idx.shape[0]
+            new = np.stack([rng.integers(0, d, size=need + 16) for d in dims], 1).astype(np.int32)
+            idx = np.concatenate([idx, new])
+            _, first = np.unique(_tuple_hash(idx), return_index=True)
+            idx = idx[np.sort(first)]
+        idx = idx[rng.permutation(idx.shape[0])[:nnz]]
     vals = rng.uniform(lo, hi, size=nnz).astype(np.float32)
     return Coo(np.array(dims, np.int32), idx, vals)
 
@@ -97,6 +128,8 @@ def uniform_torch(dims, nnz, seed, lo=1.0, hi=5.0, device="cuda") -> Coo:
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     dims = [int(d) for d in dims]
+    if float(np.prod(np.array(dims, np.float64))) >= _KEY_CELLS:
+        return _uniform_torch_hashed(dims, nnz, g, lo, hi, device)
     keys = torch.empty(0, dtype=torch.int64, device=device)
     while keys.numel() < nnz:
         need = nnz - keys.numel()
@@ -116,6 +149,43 @@ def uniform_torch(dims, nnz, seed, lo=1.0, hi=5.0, device="cuda") -> Coo:
     vals = torch.empty(nnz, dtype=torch.float32, device=device).uniform_(lo, hi, generator=g)
     out = Coo(np.array(dims, np.int32), idx.cpu().numpy(), vals.cpu().numpy())
     del idx, vals
+    torch.cuda.empty_cache()
+    return out
+
+
+def _uniform_torch_hashed(dims, nnz, g, lo, hi, device) -> Coo:
+    """uniform_torch for tensors whose cell count overflows int64 keys: per-mode
+    draws, deduplicated on a 64-bit tuple hash (see _KEY_CELLS)."""
+    import torch
+
+    def mix(h):  # splitmix64 finaliser on int64 (wrapping; logical shifts)
+        m = (1 << 64) - 1
+        c1 = torch.tensor(0xBF58476D1CE4E5B9 - (1 << 64), dtype=torch.int64, device=device)
+        c2 = torch.tensor(0x94D049BB133111EB - (1 << 64), dtype=torch.int64, device=device)
+        srl = lambda x, k: (x >> k) & ((1 << (64 - k)) - 1)
+        h = (h ^ srl(h, 30)) * c1
+        h = (h ^ srl(h, 27)) * c2
+        return h ^ srl(h, 31)
+
+    idx = torch.empty((0, len(dims)), dtype=torch.int32, device=device)
+    while idx.shape[0] < nnz:
+        need = nnz - idx.shape[0]
+        new = torch.stack([torch.randint(0, d, (need + 16,), generator=g, device=device,
+                                         dtype=torch.int32) for d in dims], 1)
+        idx = torch.cat([idx, new])
+        h = torch.zeros(idx.shape[0], dtype=torch.int64, device=device)
+        for n in range(len(dims)):
+            h = mix(h ^ (idx[:, n].to(torch.int64) + 0x1E3779B97F4A7C15))
+        _, inv = torch.unique(h, return_inverse=True)
+        first = torch.full((int(inv.max()) + 1,), idx.shape[0], dtype=torch.int64, device=device)
+        first.scatter_reduce_(0, inv, torch.arange(idx.shape[0], device=device), "amin")
+        idx = idx[torch.sort(first).values]
+        del h, inv, first
+    perm = torch.randperm(idx.shape[0], generator=g, device=device)[:nnz]
+    idx = idx[perm]
+    vals = torch.empty(nnz, dtype=torch.float32, device=device).uniform_(lo, hi, generator=g)
+    out = Coo(np.array(dims, np.int32), idx.cpu().numpy(), vals.cpu().numpy())
+    del idx, vals, perm
     torch.cuda.empty_cache()
     return out
 
