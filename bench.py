@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
     ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
+    ap.add_argument("--store-c", type=int, default=0,
+                    help="core sweep storage scheme: C rows from a C cache rebuilt every core "
+                         "phase (inside the timed region), EpochOptions.store_c")
     ap.add_argument("--dsgd", action="store_true",
                     help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -336,6 +339,7 @@ def run_engine(args):
     s.set_option("eval", eng.EVAL_FAST)
     s.set_option("hog_update", args.hog_update)
     s.set_option("tc_ws", args.tc_ws)
+    s.set_option("store_c", args.store_c)
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
     s.upload_model(coo.dims, ranks, j, a0, b0)
@@ -436,6 +440,7 @@ def run_engine(args):
             "data": "synthetic (uniform distinct tuples, values U[lo,hi], seeded)",
             "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": coo.nnz,
                        "J": j, "R": j, "M": 16, "mode": "hogwild", "precision": args.precision,
+                       "core_scheme": "storage" if args.store_c else "calculation",
                        "parallelism": job.parallelism, "nnz_per_rank": job.local_nnz,
                        "test_frac": cfg.get("test_frac", 0.014),
                        "l2": "inputs larger than L2 (COO stream 16 B/nnz per sweep)"},

@@ -25,7 +25,7 @@ struct EpochOptions {
   int workers = 1;               // 1: deterministic sweeps; > 1: Hogwild
   bool canonical_order = false;  // storage order, single-entry batches
   bool eager_refresh = false;    // FasterTucker hook (ignored)
-  bool store_c = false;          // billed as the storage scheme; computed live
+  bool store_c = false;          // storage scheme: core phase reads C rows from a C cache
 };
 
 struct EpochStats {

@@ -127,7 +127,7 @@ class _COracle:
         L.fo_factor_phase.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
                                       _f32p, _i64p, C.c_int, C.c_float, C.c_float]
         L.fo_core_phase.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
-                                    _f32p, _i64p, C.c_int, C.c_float, C.c_float, _f32p]
+                                    _f32p, _i64p, C.c_int, C.c_float, C.c_float, _f32p, C.c_int]
         L.fo_predict.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, _i32p]
         L.fo_predict.restype = C.c_double
         L.fo_loss.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
@@ -148,13 +148,14 @@ class _COracle:
                                       _p(t.vals, _f32p), _p(perm, _i64p), cap, lr_a, reg_a)
         assert rc == 0
 
-    def core_phase(self, t: Tensor, m: Model, perm, cap, lr_b, reg_b):
+    def core_phase(self, t: Tensor, m: Model, perm, cap, lr_b, reg_b, store_c=False):
+        """store_c: storage scheme (C rows from the C cache, decomposition.cpp:668-691)."""
         perm = np.ascontiguousarray(perm, dtype=np.int64)
         g = np.zeros(int(np.sum(m.ranks)) * m.r, dtype=np.float32)
         rc = self.lib.fo_core_phase(m.order, _p(m.ranks, _i32p), m.r, _ptr_array(m.a),
                                     _ptr_array(m.b), t.nnz, _p(t.idx, _i32p),
                                     _p(t.vals, _f32p), _p(perm, _i64p), cap, lr_b, reg_b,
-                                    _p(g, _f32p))
+                                    _p(g, _f32p), int(store_c))
         if rc != 0:
             raise RuntimeError("apply_core_update: empty tensor")
         return g

@@ -126,6 +126,41 @@ static void fo_stage_cd(fo_ws* w, float* const* amat, const int32_t* idx,
   }
 }
 
+/* Storage scheme (store_c): C rows taken from the C cache instead of the
+ * tile product.  A cache row is CCache::refresh's sum over the unpadded J,
+ * j ascending, multiply then add (decomposition.cpp:89-107), copied in for
+ * m < m_eff and zero below (stage_c_rows_from_cache, :299-314); computing the
+ * touched rows on the fly gives the same values as building the whole cache. */
+static void fo_stage_cd_cached(fo_ws* w, float* const* amat, float* const* bmat,
+                               const int32_t* idx, int m_eff) {
+  const int order = w->order;
+  for (int n = 0; n < order; ++n) {
+    memset(w->a[n], 0, sizeof(float) * w->capp * w->jp[n]);
+    memset(w->c[n], 0, sizeof(float) * w->capp * w->rp);
+    for (int m = 0; m < m_eff; ++m) {
+      const float* row = amat[n] + (size_t)idx[n * w->cap + m] * w->j[n];
+      for (int j = 0; j < w->j[n]; ++j) w->a[n][m * w->jp[n] + j] = row[j];
+      for (int c = 0; c < w->r; ++c) {
+        float acc = 0.0f;
+        for (int j = 0; j < w->j[n]; ++j) {
+          float p = row[j] * bmat[n][(size_t)j * w->r + c];
+          acc = acc + p;
+        }
+        w->c[n][m * w->rp + c] = acc;
+      }
+    }
+  }
+  for (int k = 0; k < order; ++k) {
+    int first = (k == 0) ? 1 : 0;
+    if (order == 1) first = 0;
+    memcpy(w->d[k], w->c[first], sizeof(float) * w->capp * w->rp);
+    for (int n = first + 1; n < order; ++n) {
+      if (n == k) continue;
+      for (int i = 0; i < w->capp * w->rp; ++i) w->d[k][i] = w->d[k][i] * w->c[n][i];
+    }
+  }
+}
+
 /* U^(n) = D^(n) B^(n)T (decomposition.cpp:226-232). */
 static void fo_u(fo_ws* w) {
   for (int n = 0; n < w->order; ++n)
@@ -297,7 +332,7 @@ int fo_factor_phase(int order, const int32_t* ranks, int r, float* const* amat,
 int fo_core_phase(int order, const int32_t* ranks, int r, float* const* amat,
                   float* const* bmat, int64_t nnz, const int32_t* idx_aos,
                   const float* vals, const int64_t* perm, int cap, float lr_b,
-                  float reg_b, float* grad_out) {
+                  float reg_b, float* grad_out, int store_c) {
   if (nnz <= 0) return 2; /* apply_core_update: empty tensor */
   fo_ws w;
   if (ws_init(&w, order, ranks, r, cap)) return 1;
@@ -309,7 +344,8 @@ int fo_core_phase(int order, const int32_t* ranks, int r, float* const* amat,
   for (int64_t off = 0; off < nnz; off += cap) {
     int m_eff = (int)((nnz - off) < cap ? (nnz - off) : cap);
     gather_batch(order, idx_aos, vals, perm + off, m_eff, cap, idx, x);
-    fo_stage_cd(&w, amat, idx, m_eff);
+    if (store_c) fo_stage_cd_cached(&w, amat, bmat, idx, m_eff);
+    else fo_stage_cd(&w, amat, idx, m_eff);
     fo_predict_c_side(&w, x, m_eff);
     fo_core_grads(&w, acc);
   }

@@ -42,6 +42,15 @@ EPOCHS = [
 ]
 
 
+# Storage scheme (EpochOptions.store_c, §8 f1): same epoch fixtures with the
+# core phase reading C rows from the CCache.  (name, dims, nnz, ranks, R, cap, seed)
+STOREC = [
+    ("storec_j16", [30, 20, 10], 1000, [16, 16, 16], 16, 16, 1234),
+    ("storec_ragged", [30, 20, 10], 1000, [5, 4, 3], 4, 16, 99),
+    ("storec_order4", [9, 8, 7, 6], 800, [8, 4, 8, 4], 8, 9, 5),
+]
+
+
 def tensor_fields(t):
     return dict(dims=t.dims, idx=t.idx, vals=t.vals)
 
@@ -54,11 +63,28 @@ def model_fields(m, prefix):
     return out
 
 
+def storec(R):
+    for k, (name, dims, nnz, ranks, r, cap, seed) in enumerate(STOREC):
+        t = O.random_tensor(dims, nnz, 600 + k, 1.0, 5.0)
+        m = O.random_model(dims, ranks, r, 700 + k, 0.3)
+        hp = dict(lr_a=1e-2, lr_b=1e-2, reg_a=1e-3, reg_b=1e-3)
+        new, _, cnt = R.epoch_plus(t, m, seed, batch=cap, workers=1, store_c=True, **hp)
+        p1 = R.global_plan(t.nnz, cap, derive_seed(seed, [1]))
+        p2 = R.global_plan(t.nnz, cap, derive_seed(seed, [2]))
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **tensor_fields(t),
+                            **model_fields(m, "m_"), **model_fields(new, "new_"),
+                            cap=np.int32(cap), seed=np.uint64(seed), plan1=p1, plan2=p2,
+                            counters=cnt, hp=np.array(list(hp.values()), np.float32))
+
+
 def main():
     R = O.REF
     if R is None:
         raise SystemExit("oracle/_ref/libftkref.so missing: run make -C oracle first")
     os.makedirs(OUT, exist_ok=True)
+    storec(R)
+    if "--storec-only" in sys.argv:
+        return
     lr_a, reg_a = 0.05, 0.01
     for k, (name, dims, nnz, (lo, hi), ranks, r, cap, rows) in enumerate(PROBES):
         t = O.random_tensor(dims, nnz, 100 + k, lo, hi)

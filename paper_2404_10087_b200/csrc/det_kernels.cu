@@ -100,11 +100,19 @@ __device__ void compute_c(const KView& v, const DetLayout& L, float* sm,
                           int m_eff) {
   const int r = v.r;
   float* s_c = sm + L.o_c;
+  const int* s_idx = reinterpret_cast<const int*>(sm + L.o_idx);
   for (int n = 0; n < v.order; ++n) {
     const int jn = v.j[n];
     const bool pad = (jn % kTile) != 0;
     const float* a = sm + L.o_a + L.aoff[n];
     const float* __restrict__ b = v.b[n];
+    if (v.cc[n]) {  // storage scheme: copy the cached row (decomposition.cpp:299-314)
+      for (int e = threadIdx.x; e < m_eff * r; e += blockDim.x) {
+        const int m = e / r, c = e - m * r;
+        s_c[(n * L.cap + m) * r + c] = v.cc[n][(size_t)s_idx[n * L.cap + m] * r + c];
+      }
+      continue;
+    }
     for (int e = threadIdx.x; e < m_eff * r; e += blockDim.x) {
       const int m = e / r, c = e - m * r;
       const float* arow = a + m * jn;
@@ -327,7 +335,43 @@ __global__ void apply_core_kernel(KView v, float* __restrict__ grad, float lr,
   }
 }
 
+// One thread per (row, column) of the cache; B_n staged in shared memory.
+__global__ void ccache_kernel(const float* __restrict__ a, const float* __restrict__ b, int64_t rows,
+                              int jn, int r, float* __restrict__ out) {
+  extern __shared__ float sb[];
+  for (int e = threadIdx.x; e < jn * r; e += blockDim.x) sb[e] = b[e];
+  __syncthreads();
+  const int64_t total = rows * r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / r;
+    const int c = (int)(e - i * r);
+    const float* arow = a + i * jn;
+    float acc = 0.0f;
+    for (int j = 0; j < jn; ++j) acc = fadd(acc, fmul(__ldg(arow + j), sb[j * r + c]));
+    out[e] = acc;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_ccache(const KView& v, const int32_t* dims, float* const* out,
+                          cudaStream_t st) {
+  for (int n = 0; n < v.order; ++n) {
+    const int64_t total = (int64_t)dims[n] * v.r;
+    if (total == 0) continue;
+    const size_t bytes = sizeof(float) * v.j[n] * v.r;
+    cudaError_t e = cudaFuncSetAttribute(ccache_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+    ccache_kernel<<<(int)blocks, 256, bytes, st>>>(v.a[n], v.b[n], dims[n], v.j[n], v.r, out[n]);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 cudaError_t launch_det_factor(const KView& v, const int64_t* perm, int cap,
                               float lr_a, float reg_a, const DetDebug& dbg,

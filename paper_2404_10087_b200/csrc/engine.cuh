@@ -53,6 +53,9 @@ struct DevModel {
   int32_t r = 0;
   float* a[kMaxOrder] = {};
   float* b[kMaxOrder] = {};
+  // Storage scheme (EpochOptions.store_c): C_n = A_n B_n per mode, I_n x R,
+  // rebuilt at the start of every core phase (CCache, decomposition.cpp:74-107).
+  float* cc[kMaxOrder] = {};
   int sum_j() const {
     int s = 0;
     for (int n = 0; n < order; ++n) s += ranks[n];
@@ -85,6 +88,10 @@ struct KView {
   // Optional device {mul, add} of the tile permutation (overrides the launch
   // arguments; lets a captured CUDA graph take a new permutation per epoch).
   const int64_t* tperm;
+  // Core sweeps, storage scheme: C rows gathered from the cache instead of
+  // computed (stage_c_rows_from_cache, decomposition.cpp:299-314); null =
+  // calculation scheme.
+  const float* cc[kMaxOrder];
 };
 
 int num_sms();
@@ -126,6 +133,10 @@ cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add
                               float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
                               cudaStream_t st);
 size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm);
+// CCache::refresh for every mode (decomposition.cpp:89-107): out[n][i][r] =
+// sum_j A_n[i][j] B_n[j][r], j ascending, fp32 multiply then add (no FMA).
+cudaError_t launch_ccache(const KView& v, const int32_t* dims, float* const* out,
+                          cudaStream_t st);
 cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                             float* grad, int blocks_per_sm, float* scratch,
                             size_t scratch_bytes, cudaStream_t st);

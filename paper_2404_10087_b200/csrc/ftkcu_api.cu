@@ -32,6 +32,7 @@ struct ftkcu_session {
   int64_t opt_hog_bps = 2;
   int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
+  int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -132,6 +133,7 @@ void free_model(DevModel& m) {
   for (int n = 0; n < kMaxOrder; ++n) {
     if (m.a[n]) cudaFree(m.a[n]);
     if (m.b[n]) cudaFree(m.b[n]);
+    if (m.cc[n]) cudaFree(m.cc[n]);
   }
   m = DevModel{};
 }
@@ -345,6 +347,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_hog_bps = value;
   } else if (k == "tc_ws") {
     s->opt_tc_ws = value != 0;
+  } else if (k == "store_c") {
+    s->opt_store_c = value != 0;
   } else if (k == "hog_update") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "bad hog_update");
     s->opt_hog_update = value;
@@ -378,6 +382,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "verbose") *value = s->opt_verbose;
   else if (k == "hog_update") *value = s->opt_hog_update;
   else if (k == "tc_ws") *value = s->opt_tc_ws;
+  else if (k == "store_c") *value = s->opt_store_c;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
   else if (k == "staleness") *value = s->opt_staleness;
@@ -601,6 +606,19 @@ int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offse
   return FTKCU_OK;
 }
 
+// Storage scheme: (re)builds C_n = A_n B_n for every mode from the current
+// model, as the reference does at the start of each core phase (outside its
+// timed region, decomposition.cpp:668-670), and points the view at it.
+int prepare_ccache(ftkcu_session* s, KView& v) {
+  DevModel& m = s->model;
+  for (int n = 0; n < m.order; ++n)
+    if (!m.cc[n]) CK(cudaMalloc(&m.cc[n], sizeof(float) * ((size_t)m.dims[n] * m.r + 1)));
+  CK(launch_ccache(v, m.dims, m.cc, s->stream));
+  s->launches += m.order;
+  for (int n = 0; n < m.order; ++n) v.cc[n] = m.cc[n];
+  return FTKCU_OK;
+}
+
 int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M, float lr_b,
                      float reg_b, int mode, uint64_t seed, float* grad_out, double* ms) {
   int rc = bind(s);
@@ -615,6 +633,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     if (!perm) return fail(s, FTKCU_ERR_ARG, "deterministic mode needs a permutation");
     if ((rc = upload_perm(s, perm, t.nnz))) return rc;
     v = make_view(s, t, false);
+    if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
     CK(cudaMemsetAsync(s->grad, 0, sizeof(float) * glen, s->stream));
     CK(launch_det_core(v, s->d_perm, M, s->grad, DetDebug{}, s->stream));
@@ -628,11 +647,14 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     const size_t hog_need = hog_core_scratch_bytes(v, (int)s->opt_hog_bps);
     if (hog_need > need) need = hog_need;
     if ((rc = ensure_scratch(s, need))) return rc;
+    if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
+    // Storage scheme: the WS sweep reads C rows from the cache (no C GEMM);
+    // other tensor-core shapes take the CUDA-core sweep, which reads them too.
     if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
       CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
-    } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
+    } else if (s->opt_precision != FTKCU_PREC_FP32 && !s->opt_store_c && tc_supported(v)) {
       CK(launch_tc_core(v, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
     } else {

@@ -177,9 +177,16 @@ __device__ void front(const KView& v, const HogLayout& L, const float* sm, float
     }
   }
   __syncwarp();
-  // C^(n)[g][c] = sum_j a[g][n][j] B_n[j][c]
+  // C^(n)[g][c] = sum_j a[g][n][j] B_n[j][c] (or the cached row, storage scheme)
   for (int n = 0; n < N; ++n) {
     const int jn = v.j[n];
+    if (v.cc[n]) {
+      for (int c = lane; c < r; c += 32)
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+          wc[(g * N + n) * r + c] = g < nvalid ? v.cc[n][(size_t)rows[g][n] * r + c] : 0.0f;
+      continue;
+    }
     for (int c = lane; c < r; c += 32) {
       float acc[kG];
 #pragma unroll

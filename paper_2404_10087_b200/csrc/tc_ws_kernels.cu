@@ -54,6 +54,7 @@ struct __align__(64) WsParams {
   float lr, reg;
   int atomic_update, prec3;
   float* partials;
+  const float* cc[kN];  // core sweep, storage scheme: C-row cache (KView::cc)
   int exp;  // timing experiments (FTKCU_WS_EXP), never set in production
 };
 
@@ -627,6 +628,133 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
   ws_teardown(tmem);
 }
 
+// ---- core sweep, storage scheme -------------------------------------------------
+//
+// Same sweep with C rows read from the C cache (CCache, decomposition.cpp:
+// 299-314) instead of computed: no C GEMM and no TMEM copy of the rows.  The
+// epilogue loads its half of every C row straight from the (L2-resident)
+// cache one tile ahead, exchanges the x_hat halves through shared memory,
+// and writes r D for the G GEMM, the MMA warp's only work.
+
+__global__ void __launch_bounds__(kThreadsWs, 1) ws_core_cc_kernel(const __grid_constant__ WsParams p) {
+  using L = WsLayout<true>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  ws_setup<true>(p, sm, bars, tslot);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kG = 0;  // TMEM: G only
+
+  if (warp == 0) {
+    ws_idx_producer<true>(p, sm, bars, nk);
+  } else if (warp == kGatherWarp) {
+    ws_gather_producer<true>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idg = idesc_tf32(128, kN * kW, 1, 1);
+      const uint32_t d0 = smem_u32(sm + L::o_d);
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kS);
+        mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+        mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
+        tc_after();
+        const uint64_t da = sdesc_l(smem_u32(sm + L::o_a + s * L::kSlot), kModeTile, 512, 1);
+        const uint64_t dd = sdesc_l(d0, kModeTile, 512, 1);
+#pragma unroll 4
+        for (int ks = 0; ks < kRows / 8; ++ks)
+          mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
+                 (k > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&bars[B_DEMPTY]);
+        mma_commit(&bars[B_EMPTY + s]);
+      }
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* xp = reinterpret_cast<float*>(sm + L::o_xp);  // [2 tiles][2 halves][128]
+    // This thread's column half of the tile's C rows, from the cache.
+    auto fetch = [&](int64_t k, float (&c)[kN][16]) {
+      const int ii = (int)(k % L::kI);
+      mbar_wait(&bars[B_IFULL + ii], (uint32_t)((k / L::kI) & 1));
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        const float4* src =
+            reinterpret_cast<const float4*>(p.cc[n] + (size_t)s_idx[n * kRows + row] * kW + h * 16);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 x = __ldg(src + q4);
+          c[n][q4 * 4 + 0] = x.x;
+          c[n][q4 * 4 + 1] = x.y;
+          c[n][q4 * 4 + 2] = x.z;
+          c[n][q4 * 4 + 3] = x.w;
+        }
+      }
+    };
+    float cur[kN][16], nxt[kN][16];
+    if (nk > 0) fetch(0, cur);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int b = (int)(k & 1), ii = (int)(k % L::kI), s = (int)(k % kS);
+      if (k + 1 < nk) fetch(k + 1, nxt);
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(cur[0][i], cur[1][i] * cur[2][i], part);
+      xp[(b * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
+      const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
+      const float resid = ok ? s_val[row] - xhat : 0.0f;
+      // The gather warp reads this COO slot's indices: hold it until the
+      // tile's rows have landed.
+      mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);
+      mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with the D tile
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float4 d;
+          const int i = q4 * 4;
+#define FTK_D(ii) (n == 0 ? cur[1][ii] * cur[2][ii] : (n == 1 ? cur[0][ii] * cur[2][ii] : cur[0][ii] * cur[1][ii]))
+          d.x = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 0)));
+          d.y = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 1)));
+          d.z = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 2)));
+          d.w = __uint_as_float(tf32_rn_bits(resid * FTK_D(i + 3)));
+#undef FTK_D
+          *reinterpret_cast<float4*>(sm + L::o_d + n * kModeTile +
+                                     swz32(row, (h * 16 + i) * 4)) = d;
+        }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DFULL]);
+      if (k + 1 < nk) {
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) cur[n][i] = nxt[n][i];
+      }
+    }
+    if (nk > 0) mbar_wait(&bars[B_DEMPTY], (uint32_t)((nk - 1) & 1));
+    tc_after();
+    if (q < kN) {
+      uint32_t v[16];
+      tmem_ld16(tl + kG + q * kW + h * 16, v);
+      tmem_wait_ld();
+      float* out = p.partials + (size_t)blockIdx.x * (kN * kW * kW) + ((size_t)q * kW + lane) * kW + h * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = nk > 0 ? __uint_as_float(v[i]) : 0.0f;
+    }
+  }
+  ws_teardown(tmem);
+}
+
 __global__ void ws_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
                                  float* __restrict__ grad) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
@@ -719,11 +847,12 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   if (grid < 1) return cudaErrorInvalidValue;
   if (scratch_bytes < (size_t)grid * len * sizeof(float)) return cudaErrorInvalidValue;
   p.partials = scratch;
+  for (int n = 0; n < kN; ++n) p.cc[n] = v.cc[n];
   const int bytes = (int)WsLayout<true>::bytes;
-  cudaError_t e = cudaFuncSetAttribute(ws_core_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  auto kern = v.cc[0] ? ws_core_cc_kernel : ws_core_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  ws_core_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+  kern<<<grid, kThreadsWs, bytes, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ws_reduce_kernel<<<(len + 255) / 256, 256, 0, st>>>(scratch, grid, len, grad);

@@ -201,6 +201,8 @@ EpochStats run_epoch(const SparseTensor& t, int slot, const Model& m, const Hype
       plan = opts.canonical_order ? EpochPlan::canonical(t) : EpochPlan::global(t, cap, rng);
       perm = plan.positions().data();
     }
+    // storage scheme (CCache) or calculation scheme, decomposition.cpp:668-691
+    check(ftkcu_set_option(s, "store_c", opts.store_c ? 1 : 0));
     check(ftkcu_core_phase(s, slot, perm, cap, h.lr_b, h.reg_b, mode, derive_seed(seed, {2}),
                            nullptr, &ms_c));
   }

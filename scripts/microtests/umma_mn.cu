@@ -30,7 +30,9 @@ __global__ void kern(const float* a, const float* b, float* out, int a_mn, int b
   // A operand
   if (!a_mn) {  // K-major: rows m, K contiguous (K=32 -> 128 B rows)
     for (int e = t; e < M * K; e += 128) { int m = e / K, k = e % K;
-      *(float*)(sA + swz(m, k * 4, 128)) = a[e]; }
+      uint32_t off = lbo_sel >= 3 && lbo_sel != 8 ? m * 128 + ((((k * 4) >> 5) ^ (m & 3)) << 5) + ((k * 4) & 31)
+                                  : swz(m, k * 4, 128);
+      *(float*)(sA + off) = a[e]; }
   } else {      // MN-major: rows k, M contiguous; M blocks of 32 at stride K*128
     for (int e = t; e < M * K; e += 128) { int m = e / K, k = e % K;
       int blk = m / 32, mm = m % 32;
@@ -61,7 +63,12 @@ __global__ void kern(const float* a, const float* b, float* out, int a_mn, int b
     uint32_t id = idesc_tf32(M, NN, a_mn, b_mn);
     for (int ks = 0; ks < K / 8; ++ks) {
       uint64_t da, db;
-      if (!a_mn) da = sdesc(smem_u32(sA) + ks * 32, 16, 1024, 2);
+      if (!a_mn && lbo_sel == 3) da = sdesc(smem_u32(sA) + ks * 32, 16, 1024, 1);
+      else if (!a_mn && lbo_sel == 4) da = sdesc(smem_u32(sA) + ks * 32, 16, 512, 1);
+      else if (!a_mn && lbo_sel == 5) da = sdesc(smem_u32(sA) + ks * 32, 128, 1024, 1);
+      else if (!a_mn && lbo_sel == 6) da = sdesc(smem_u32(sA), 16, 1024, 1) + ((uint64_t)ks << 49);
+      else if (!a_mn && lbo_sel == 7) da = sdesc(smem_u32(sA) + ks * 16, 16, 1024, 1);
+      else if (!a_mn) da = sdesc(smem_u32(sA) + ks * 32, 16, 1024, 2);
       else if (lbo_sel == 2) da = sdesc(smem_u32(sA) + ks * 1024, K * 128, 512, 1);
       else {
         uint32_t l = K * 128, s = 1024;  // block stride, k-group stride
@@ -94,15 +101,18 @@ __global__ void kern(const float* a, const float* b, float* out, int a_mn, int b
   __syncthreads();
   if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" :: "r"(tm));
 }
-int main() {
+int main(int argc, char** argv) {
+  int only = argc > 1 ? atoi(argv[1]) : -1;
   float *a, *b, *o;
   cudaMallocManaged(&a, M * K * 4); cudaMallocManaged(&b, K * NN * 4); cudaMallocManaged(&o, M * NN * 4);
   srand(1);
   for (int i = 0; i < M * K; ++i) a[i] = (rand() % 17) / 8.0f - 1.0f;
   for (int i = 0; i < K * NN; ++i) b[i] = (rand() % 13) / 4.0f - 1.5f;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  for (int am = 0; am < 2; ++am) for (int bm = 0; bm < 2; ++bm) for (int sel = 0; sel < 3; ++sel) {
-    if (!am && !bm && sel) continue;
+  for (int am = 0; am < 2; ++am) for (int bm = 0; bm < 2; ++bm) for (int sel = 0; sel < 8; ++sel) {
+    if (!am && !bm && sel && sel < 3) continue;
+    if (sel >= 3 && (am || bm)) continue;
+    if (only >= 0 && sel != only) continue;
     for (int i = 0; i < M * NN; ++i) o[i] = -777.0f;
     kern<<<1, 128, 100 * 1024>>>(a, b, o, am, bm, sel);
     cudaError_t e = cudaDeviceSynchronize();

@@ -114,3 +114,34 @@ def test_plans_fixture_matches_reference_live():
     z = load("plans")
     assert np.array_equal(O.REF.global_plan(100, 16, 3), z["p100_16_3"])
     assert np.array_equal(O.REF.global_plan(37, 5, 9), z["p37_5_9"])
+
+
+@pytest.mark.parametrize("name", names("storec_"))
+def test_storage_scheme_epoch_matches_golden(name):
+    """store_c (§8 f1): C rows from the CCache (decomposition.cpp:74-107,
+    299-314) in the core phase; bit-exact against the reference's epoch."""
+    z = load(name)
+    t, m = tensor(z), model(z, "m_")
+    lr_a, lr_b, reg_a, reg_b = (float(x) for x in z["hp"])
+    cap = int(z["cap"])
+    C.factor_phase(t, m, z["plan1"], cap, lr_a, reg_a)
+    C.core_phase(t, m, z["plan2"], cap, lr_b, reg_b, store_c=True)
+    want = model(z, "new_")
+    for n in range(m.order):
+        assert bits_equal(m.a[n], want.a[n]), f"A{n}"
+        assert bits_equal(m.b[n], want.b[n]), f"B{n}"
+
+
+@needs_ref
+def test_storage_scheme_matches_reference_live():
+    t = O.random_tensor([25, 15, 12], 900, 3, 1.0, 5.0)
+    m = O.random_model(t.dims, [12, 8, 16], 10, 4, 0.4)
+    seed = 777
+    new, _, _ = O.REF.epoch_plus(t, m, seed, 1e-2, 1e-2, 1e-3, 1e-3, 16, 1, store_c=True)
+    mc = m.copy()
+    C.factor_phase(t, mc, O.REF.global_plan(t.nnz, 16, derive_seed(seed, [1])), 16, 1e-2, 1e-3)
+    C.core_phase(t, mc, O.REF.global_plan(t.nnz, 16, derive_seed(seed, [2])), 16, 1e-2, 1e-3,
+                 store_c=True)
+    for n in range(3):
+        assert bits_equal(mc.a[n], new.a[n])
+        assert bits_equal(mc.b[n], new.b[n])
