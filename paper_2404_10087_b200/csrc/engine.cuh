@@ -133,6 +133,15 @@ cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add
                               float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
                               cudaStream_t st);
 size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm);
+// Large ranks (N = 3, J = R in {64, 128}): mode-serial tcgen05 sweeps
+// (tc_big_kernels.cu).  Scratch: B operand images (+ core partials).
+bool big_supported(const KView& v);
+size_t big_scratch_bytes(const KView& v, const int32_t* dims, bool core);
+cudaError_t launch_big_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                              float lr, float reg, int atomic_update, float* scratch,
+                              size_t scratch_bytes, cudaStream_t st);
+cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                            float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st);
 // CCache::refresh for every mode (decomposition.cpp:89-107): out[n][i][r] =
 // sum_j A_n[i][j] B_n[j][r], j ascending, fp32 multiply then add (no FMA).
 cudaError_t launch_ccache(const KView& v, const int32_t* dims, float* const* out,

@@ -526,6 +526,13 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
   if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
+  } else if (s->opt_precision == FTKCU_PREC_TF32 && big_supported(v)) {
+    // large ranks: B operand images in the session scratch (allocated
+    // before any graph capture, see ftkcu_dsgd_factor_epoch)
+    int rc = ensure_scratch(s, big_scratch_bytes(v, s->model.dims, false));
+    if (rc) return rc;
+    CK(launch_big_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_hog_update,
+                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
   } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
     CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
@@ -646,6 +653,8 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
     const size_t hog_need = hog_core_scratch_bytes(v, (int)s->opt_hog_bps);
     if (hog_need > need) need = hog_need;
+    if (big_supported(v) && big_scratch_bytes(v, s->model.dims, true) > need)
+      need = big_scratch_bytes(v, s->model.dims, true);
     if ((rc = ensure_scratch(s, need))) return rc;
     if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -654,6 +663,9 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
       CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+    } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && big_supported(v)) {
+      CK(launch_big_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
+                         s->scratch_bytes, s->stream));
     } else if (s->opt_precision != FTKCU_PREC_FP32 && !s->opt_store_c && tc_supported(v)) {
       CK(launch_tc_core(v, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
@@ -925,6 +937,11 @@ int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t
       if (offs[m][p + 1] < offs[m][p]) return fail(s, FTKCU_ERR_ARG, "block offsets not sorted");
   }
   if ((rc = prepare_stream(s, t, nullptr))) return rc;
+  {
+    const KView v = make_view(s, t, true);
+    if (big_supported(v) && (rc = ensure_scratch(s, big_scratch_bytes(v, s->model.dims, false))))
+      return rc;
+  }
   if ((size_t)ncell > s->cellperm_cap) {
     if (s->d_cellperm) CK(cudaFree(s->d_cellperm));
     s->d_cellperm = nullptr;

@@ -1,0 +1,619 @@
+// tcgen05 Hogwild sweeps for the large ranks of the rank sweep (BASELINE C5:
+// N = 3, J = R = W in {64, 128}).  At these ranks one tile's factor rows no
+// longer fit next to B in shared memory (W = 128: A rows 3 x 64 KB, B and B^T
+// 6 x 64 KB), so the sweeps run MODE-SERIAL over a ring of stages, each stage
+// = one mode's gathered rows (128 x W) + one pre-swizzled B operand image
+// (W x W), with the per-tile accumulators in TMEM:
+//
+//   factor   C_n = A_n B_n        n = 0..2 -> TMEM [nW, (n+1)W)  (3 stages)
+//            epilogue: x_hat, r, D'_n = lr r prod_{m!=n} C_m, in place
+//            U_n = D'_n B_n^T     n = 0..2 -> TMEM [3W, 4W)     (3 stages,
+//            the stage's rows give the regulariser term); a += U - lr reg a
+//            as vector RED (Hogwild accumulate) or STG (overwrite rule)
+//   core     one launch per mode p (TMEM holds C for all modes plus G_p):
+//            C_n as above, D'_p = r prod_{m!=p} C_m into shared memory,
+//            G_p += A_p^T D'_p    (A_p gathered again in the MN-major layout)
+//
+// Warp roles: warp 0 producer (COO record by bulk copy, rows by TMA gather4,
+// B images by bulk copy), warp 1 MMA issuer, warps 2-5 epilogue (thread =
+// nonzero = TMEM lane).  Algebra as tc_ws_kernels.cu (decomposition.cpp:
+// 644-658 / :678-698); B operands and D' are rounded to nearest tf32.
+#include <cudaTypedefs.h>
+
+#include "engine.cuh"
+#include "tc_common.cuh"
+
+namespace ftkcu {
+namespace {
+using namespace tc;
+
+constexpr int kN = 3;
+constexpr int kRows = 128;
+constexpr int kThreads = 6 * 32;
+constexpr uint32_t kBlk = kRows * 128;  // one 32-column block of a row tile: 16 KB
+
+template <int W, bool kCore>
+struct BigLayout {
+  static constexpr uint32_t kA = kRows * W * 4;  // row tile: W / 32 blocks of 16 KB
+  static constexpr uint32_t kB = W * W * 4;      // B image: W / 32 blocks of W x 128 B
+  static constexpr uint32_t kStage = kA + kB;
+  static constexpr int kStages = W == 64 ? (kCore ? 3 : 4) : 1;
+  static constexpr uint32_t o_st = 0;
+  static constexpr uint32_t o_d = o_st + kStages * kStage;  // core: D' tile (MN-major)
+  static constexpr uint32_t d_bytes = kCore ? kA : 0;
+  // the G GEMM reads M = 128 rows = 4 blocks of the A part: past a W = 64
+  // tile it runs into the stage's B image / the next stage / the D' tile
+  static constexpr uint32_t o_idx = o_d + d_bytes;
+  static constexpr uint32_t kIdx = (kN + 1) * kRows * 4;
+  static constexpr uint32_t o_rows = o_idx + 2 * kIdx;
+  static constexpr uint32_t o_bar = o_rows + 16;
+  static constexpr uint32_t o_tmem = o_bar + 32 * 8;
+  static constexpr uint32_t bytes = o_tmem + 16;
+  static constexpr uint32_t tcols = W == 64 ? 256 : 512;  // C/D 3W + U or G W
+  static_assert(bytes <= 227 * 1024, "shared-memory budget");
+  static_assert(4 * W <= 512, "TMEM budget");
+};
+
+enum : int {
+  B_FULL = 0,    // [4] stage loaded
+  B_EMPTY = 4,   // [4] stage free
+  B_IFULL = 8,   // [2] COO record landed
+  B_IEMPTY = 10, // [2] COO record consumed
+  B_CFULL = 12,  // C for all modes in TMEM
+  B_DFULL = 13,  // D' ready (TMEM in place: factor; smem: core)
+  B_UFULL = 14,  // factor: U_n in TMEM
+  B_UEMPTY = 15, // factor: U_n read
+  B_DEMPTY = 16, // core: G GEMM done with the D' tile
+};
+
+struct BigParams {
+  CUtensorMap tmap[kN];  // K-major rows (SW128); core: [pass] MN-major (ATOM_32B) in tmap_mn
+  CUtensorMap tmap_mn;
+  const int32_t* idx[kN];
+  const float* vals;
+  float* a[kN];
+  const float* bt_img[kN];  // C GEMM operand images (rows r, K = j)
+  const float* b_img[kN];   // U GEMM operand images (rows j, K = r)
+  const int32_t* tile_rows;
+  const int64_t* tperm;
+  int64_t ntiles, tmul, tadd, tile_base;
+  float lr, reg;
+  int atomic_update, pass;
+  float* partials;
+};
+
+__device__ __forceinline__ int64_t big_tile(const BigParams& p, int64_t k) {
+  const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
+  const int64_t mul = p.tperm ? __ldg(p.tperm) : p.tmul;
+  const int64_t add = p.tperm ? __ldg(p.tperm + 1) : p.tadd;
+  return p.tile_base + (t * mul + add) % p.ntiles;
+}
+
+__device__ __forceinline__ uint32_t rn_bits(float x) { return __float_as_uint(x) + 0x1000u; }
+
+// Producer: gathers the W / 32 column blocks of a mode's 128 rows.
+template <int W>
+__device__ __forceinline__ void gather_rows(uint8_t* dst, const CUtensorMap* tm,
+                                            const int32_t* s_idx, uint64_t* bar) {
+#pragma unroll 1
+  for (int g = 0; g < kRows / 4; ++g) {
+    const int4 r = *reinterpret_cast<const int4*>(s_idx + g * 4);
+#pragma unroll
+    for (int cb = 0; cb < W / 32; ++cb)
+      tma_gather4(dst + cb * kBlk + g * 512, tm, cb * 32, r.x, r.y, r.z, r.w, bar);
+  }
+}
+
+template <int W, bool kCore>
+__device__ void big_setup(uint8_t* sm, uint64_t* bars, uint32_t* tslot, const BigParams& p) {
+  using L = BigLayout<W, kCore>;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kStages; ++s) {
+      mbar_init(&bars[B_FULL + s], 1);
+      mbar_init(&bars[B_EMPTY + s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars[B_IFULL + i], 1);
+      mbar_init(&bars[B_IEMPTY + i], 1);
+    }
+    mbar_init(&bars[B_CFULL], 1);
+    mbar_init(&bars[B_DFULL], 1);
+    mbar_init(&bars[B_UFULL], 1);
+    mbar_init(&bars[B_UEMPTY], 1);
+    mbar_init(&bars[B_DEMPTY], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+    if (kCore) prefetch_tmap(&p.tmap_mn);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(L::tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+}
+
+template <int W, bool kCore>
+__device__ void big_teardown(uint32_t tmem) {
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(BigLayout<W, kCore>::tcols));
+}
+
+// Warp 0: per tile the COO record, then one stage per job.  Jobs per tile:
+// factor C0 C1 C2 U0 U1 U2; core C0 C1 C2 G.
+template <int W, bool kCore>
+__device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
+  using L = BigLayout<W, kCore>;
+  if ((threadIdx.x & 31) != 0) return;
+  constexpr int kJobs = kCore ? kN + 1 : 2 * kN;
+  int64_t job = 0;
+  for (int64_t k = 0; k < nk; ++k) {
+    const int i = (int)(k & 1);
+    const int64_t tile = big_tile(p, k);
+    mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k >> 1) & 1) ^ 1));
+    int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdx);
+    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+    mbar_expect_tx(&bars[B_IFULL + i], L::kIdx);
+    for (int n = 0; n < kN; ++n)
+      bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+    bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+    mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
+    for (int j = 0; j < kJobs; ++j, ++job) {
+      const int s = (int)(job % L::kStages);
+      mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((job / L::kStages) & 1) ^ 1));
+      uint8_t* st = sm + L::o_st + s * L::kStage;
+      if (kCore && j == kN) {  // G operand: A_pass rows, MN-major
+        mbar_expect_tx(&bars[B_FULL + s], L::kA);
+        gather_rows<W>(st, &p.tmap_mn, s_idx + p.pass * kRows, &bars[B_FULL + s]);
+        continue;
+      }
+      const int n = j % kN;
+      const bool u = !kCore && j >= kN;
+      mbar_expect_tx(&bars[B_FULL + s], L::kStage);
+      gather_rows<W>(st, &p.tmap[n], s_idx + n * kRows, &bars[B_FULL + s]);
+      bulk_g2s(st + L::kA, u ? p.b_img[n] : p.bt_img[n], L::kB, &bars[B_FULL + s]);
+    }
+  }
+}
+
+// C_n = A_n B_n for the three modes of one tile (stages job..job+2).
+template <int W, bool kCore>
+__device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tmem, int64_t& job) {
+  using L = BigLayout<W, kCore>;
+  constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
+  for (int n = 0; n < kN; ++n, ++job) {
+    const int s = (int)(job % L::kStages);
+    mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
+    tc_after();
+    const uint32_t a0 = smem_u32(sm + L::o_st + s * L::kStage);
+    const uint32_t b0 = a0 + L::kA;
+#pragma unroll
+    for (int ks = 0; ks < W / 8; ++ks)
+      mma_ss(tmem + n * W, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
+             sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
+    mma_commit(&bars[B_EMPTY + s]);
+  }
+  mma_commit(&bars[B_CFULL]);
+}
+
+// Epilogue: x_hat = sum_r prod_n C_n and the residual of this thread's row.
+template <int W>
+__device__ __forceinline__ float big_xhat(uint32_t tl) {
+  float x = 0.0f;
+#pragma unroll 1
+  for (int c = 0; c < W / 16; ++c) {
+    uint32_t v0[16], v1[16], v2[16];
+    tmem_ld16(tl + 0 * W + c * 16, v0);
+    tmem_ld16(tl + 1 * W + c * 16, v1);
+    tmem_ld16(tl + 2 * W + c * 16, v2);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      x = fmaf(__uint_as_float(v0[i]), __uint_as_float(v1[i]) * __uint_as_float(v2[i]), x);
+  }
+  return x;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_constant__ BigParams p) {
+  using L = BigLayout<W, false>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  big_setup<W, false>(sm, bars, tslot, p);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kU = 3 * W;
+
+  if (warp == 0) {
+    big_producer<W, false>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
+      int64_t job = 0;
+      for (int64_t k = 0; k < nk; ++k) {
+        issue_c<W, false>(sm, bars, tmem, job);
+        mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
+        for (int n = 0; n < kN; ++n, ++job) {
+          const int s = (int)(job % L::kStages);
+          const int64_t u = k * kN + n;
+          mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
+          mbar_wait(&bars[B_UEMPTY], (uint32_t)((u & 1) ^ 1));
+          tc_after();
+          const uint32_t b0 = smem_u32(sm + L::o_st + s * L::kStage) + L::kA;
+#pragma unroll
+          for (int ks = 0; ks < W / 8; ++ks)
+            mma_ts(tmem + kU, tmem + n * W + ks * 8,
+                   sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
+          mma_commit(&bars[B_UFULL]);
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3, row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const float lr_reg = p.lr * p.reg;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int i = (int)(k & 1);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
+      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&bars[B_CFULL], (uint32_t)(k & 1));
+      tc_after();
+      const float xhat = big_xhat<W>(tl);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
+      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
+      const float sc = p.lr * resid;
+      // D'_n = lr r prod_{m != n} C_m, in place over C (A operand of U_n)
+#pragma unroll 1
+      for (int c = 0; c < W / 16; ++c) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(tl + 0 * W + c * 16, v0);
+        tmem_ld16(tl + 1 * W + c * 16, v1);
+        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_wait_ld();
+        uint32_t d0[16], d1[16], d2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float c0 = __uint_as_float(v0[e]) * sc, c1 = __uint_as_float(v1[e]),
+                      c2 = __uint_as_float(v2[e]);
+          d0[e] = rn_bits(c1 * sc * c2);
+          d1[e] = rn_bits(c0 * c2);
+          d2[e] = rn_bits(c0 * c1);
+        }
+        tmem_st16(tl + 0 * W + c * 16, d0);
+        tmem_st16(tl + 1 * W + c * 16, d1);
+        tmem_st16(tl + 2 * W + c * 16, d2);
+      }
+      tmem_wait_st();
+      tc_before();
+      named_bar(1, 128);
+      if (warp == 2 && lane == 0) mbar_arrive(&bars[B_DFULL]);
+      int32_t g[kN];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
+      for (int n = 0; n < kN; ++n) {
+        const int64_t job = k * 2 * kN + kN + n, u = k * kN + n;
+        const int s = (int)(job % L::kStages);
+        mbar_wait(&bars[B_UFULL], (uint32_t)(u & 1));
+        tc_after();
+        const uint8_t* at = sm + L::o_st + s * L::kStage;  // this mode's rows (for reg a)
+        float* dst = p.a[n] + (size_t)g[n] * W;
+#pragma unroll 1
+        for (int c = 0; c < W / 16; ++c) {
+          uint32_t v[16];
+          tmem_ld16(tl + kU + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int col = c * 16 + q4 * 4;
+            const float4 a = *reinterpret_cast<const float4*>(
+                at + (col / 32) * kBlk + swz(row, (col % 32) * 4, 128));
+            float4 st;
+            st.x = __uint_as_float(v[q4 * 4 + 0]) - lr_reg * a.x;
+            st.y = __uint_as_float(v[q4 * 4 + 1]) - lr_reg * a.y;
+            st.z = __uint_as_float(v[q4 * 4 + 2]) - lr_reg * a.z;
+            st.w = __uint_as_float(v[q4 * 4 + 3]) - lr_reg * a.w;
+            if (ok) {
+              if (p.atomic_update) {
+                red_add_v4(dst + col, st);
+              } else {
+                st.x += a.x;
+                st.y += a.y;
+                st.z += a.z;
+                st.w += a.w;
+                *reinterpret_cast<float4*>(dst + col) = st;
+              }
+            }
+          }
+        }
+        tc_before();
+        named_bar(1, 128);
+        if (warp == 2 && lane == 0) {
+          mbar_arrive(&bars[B_UEMPTY]);
+          mbar_arrive(&bars[B_EMPTY + s]);
+          if (n == kN - 1) mbar_arrive(&bars[B_IEMPTY + i]);
+        }
+      }
+    }
+  }
+  big_teardown<W, false>(tmem);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_constant__ BigParams p) {
+  using L = BigLayout<W, true>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  big_setup<W, true>(sm, bars, tslot, p);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kG = 3 * W;
+  const int pm = p.pass;
+
+  if (warp == 0) {
+    big_producer<W, true>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idg = idesc_tf32(128, W, 1, 1);
+      const uint32_t d0 = smem_u32(sm + L::o_d);
+      int64_t job = 0;
+      for (int64_t k = 0; k < nk; ++k) {
+        issue_c<W, true>(sm, bars, tmem, job);
+        const int s = (int)(job % L::kStages);
+        mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
+        mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
+        tc_after();
+        // G[j][r] += sum_t A[t][j] D'[t][r]: M = 128 rows j (W real), N = W,
+        // K = 8 nonzeros per instruction; both operands MN-major.
+        const uint64_t da = sdesc_l(smem_u32(sm + L::o_st + s * L::kStage), kBlk, 512, 1);
+        const uint64_t dd = sdesc_l(d0, kBlk, 512, 1);
+#pragma unroll 4
+        for (int ks = 0; ks < kRows / 8; ++ks)
+          mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
+                 (k > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&bars[B_EMPTY + s]);
+        mma_commit(&bars[B_DEMPTY]);
+        ++job;
+      }
+    }
+  } else {
+    const int q = warp & 3, row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int i = (int)(k & 1);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
+      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&bars[B_CFULL], (uint32_t)(k & 1));
+      tc_after();
+      const float xhat = big_xhat<W>(tl);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
+      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
+      mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with D'
+      const int m0 = pm == 0 ? 1 : 0, m1 = pm == 2 ? 1 : 2;
+#pragma unroll 1
+      for (int c = 0; c < W / 16; ++c) {
+        uint32_t v0[16], v1[16];
+        tmem_ld16(tl + m0 * W + c * 16, v0);
+        tmem_ld16(tl + m1 * W + c * 16, v1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float4 d;
+          const int e = q4 * 4;
+          d.x = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 0]) * __uint_as_float(v1[e + 0])));
+          d.y = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 1]) * __uint_as_float(v1[e + 1])));
+          d.z = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 2]) * __uint_as_float(v1[e + 2])));
+          d.w = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 3]) * __uint_as_float(v1[e + 3])));
+          const int col = c * 16 + e;
+          *reinterpret_cast<float4*>(sm + L::o_d + (col / 32) * kBlk + swz32(row, (col % 32) * 4)) = d;
+        }
+      }
+      fence_proxy_async();
+      tc_before();
+      named_bar(1, 128);
+      if (warp == 2 && lane == 0) {
+        mbar_arrive(&bars[B_DFULL]);
+        mbar_arrive(&bars[B_IEMPTY + i]);
+      }
+    }
+    if (nk > 0) mbar_wait(&bars[B_DEMPTY], (uint32_t)((nk - 1) & 1));
+    tc_after();
+    // TMEM lane j (< W) holds G_pass[j][:]
+    float* out = p.partials + (size_t)blockIdx.x * (kN * W * W) + (size_t)pm * W * W;
+    if (row < W) {
+#pragma unroll 1
+      for (int c = 0; c < W / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16(tl + kG + c * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          out[(size_t)row * W + c * 16 + e] = nk > 0 ? __uint_as_float(v[e]) : 0.0f;
+      }
+    }  // (warp-uniform: lanes W..127 of a W = 64 tile hold no gradient)
+  }
+  big_teardown<W, true>(tmem);
+}
+
+// B operand images, rounded to nearest tf32: bt (C GEMM: rows r, K = j) and
+// b (U GEMM: rows j, K = r), K-major SW128 in 32-column blocks.
+template <int W>
+__global__ void big_images_kernel(const float* __restrict__ b, float* __restrict__ bt_img,
+                                  float* __restrict__ b_img) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < W * W; e += gridDim.x * blockDim.x) {
+    const int j = e / W, r = e - j * W;
+    const float x = __uint_as_float(rn_bits(b[e]));
+    *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bt_img) + (j / 32) * (W * 128) +
+                              swz(r, (j % 32) * 4, 128)) = x;
+    *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(b_img) + (r / 32) * (W * 128) +
+                              swz(j, (r % 32) * 4, 128)) = x;
+  }
+}
+
+// Core sweep operand copy of A_n, rounded to nearest tf32: the tensor core
+// truncates fp32 operands, and a truncated A biases every C (and so every
+// residual of the core gradient) low by ~2^-12 relative.
+__global__ void big_round_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = __uint_as_float(rn_bits(src[e]));
+}
+
+__global__ void big_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
+                                  float* __restrict__ grad) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int k = 0; k < nparts; ++k) s += partials[(size_t)k * len + e];
+    grad[e] = s;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 big_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn),
+                            cudaEnableDefault, &q);
+  }
+  return fn;
+}
+
+// Row-gather map of A_n (rows x W fp32): box of 32 columns x 1 row.
+bool big_row_map(CUtensorMap* tm, const float* a, int64_t rows, int w, bool atom32) {
+  auto fn = big_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)w * 4};
+  cuuint32_t box[2] = {32, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int W>
+cudaError_t prepare(BigParams& p, const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                    float* img, cudaStream_t st) {
+  for (int n = 0; n < kN; ++n) {
+    if (!big_row_map(&p.tmap[n], v.a[n], dims[n], W, false)) return cudaErrorNotSupported;
+    p.idx[n] = v.idx[n];
+    p.a[n] = v.a[n];
+    float* bt = img + (size_t)(2 * n) * W * W;
+    float* bb = img + (size_t)(2 * n + 1) * W * W;
+    p.bt_img[n] = bt;
+    p.b_img[n] = bb;
+    big_images_kernel<W><<<(W * W + 255) / 256, 256, 0, st>>>(v.b[n], bt, bb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  p.vals = v.vals;
+  p.ntiles = v.ntiles;
+  p.tile_base = v.tile_base;
+  p.tile_rows = v.tile_rows;
+  p.tperm = v.tperm;
+  p.tmul = mul;
+  p.tadd = add;
+  return cudaSuccess;
+}
+
+template <int W>
+cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float lr,
+                       float reg, int atomic_update, float* img, cudaStream_t st) {
+  BigParams p{};
+  cudaError_t e = prepare<W>(p, v, dims, mul, add, img, st);
+  if (e != cudaSuccess) return e;
+  p.lr = lr;
+  p.reg = reg;
+  p.atomic_update = atomic_update;
+  const int bytes = (int)BigLayout<W, false>::bytes;
+  e = cudaFuncSetAttribute(big_factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  big_factor_kernel<W><<<(int)sweep_grid(v), kThreads, bytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t run_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float* grad,
+                     float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  const int grid = (int)(v.ntiles < num_sms() ? v.ntiles : num_sms());
+  const size_t len = (size_t)kN * W * W;
+  if (grid < 1) return cudaErrorInvalidValue;
+  if (scratch_bytes < big_scratch_bytes(v, dims, true)) return cudaErrorInvalidValue;
+  float* img = scratch + (size_t)num_sms() * len;
+  float* arn = img + 2 * kN * (size_t)W * W;
+  KView vr = v;
+  for (int n = 0; n < kN; ++n) {
+    const int64_t cnt = (int64_t)dims[n] * W;
+    int64_t blocks = (cnt + 255) / 256;
+    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+    big_round_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], arn, cnt);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    vr.a[n] = arn;
+    arn += cnt;
+  }
+  BigParams p{};
+  cudaError_t e = prepare<W>(p, vr, dims, mul, add, img, st);
+  if (e != cudaSuccess) return e;
+  p.partials = scratch;
+  const int bytes = (int)BigLayout<W, true>::bytes;
+  e = cudaFuncSetAttribute(big_core_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  // one pass per mode: TMEM holds C of all modes plus one mode's gradient
+  for (int pass = 0; pass < kN; ++pass) {
+    p.pass = pass;
+    if (!big_row_map(&p.tmap_mn, vr.a[pass], dims[pass], W, true)) return cudaErrorNotSupported;
+    big_core_kernel<W><<<grid, kThreads, bytes, st>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  big_reduce_kernel<<<(int)((len + 255) / 256), 256, 0, st>>>(scratch, grid, (int)len, grad);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool big_supported(const KView& v) {
+  return v.order == kN && (v.r == 64 || v.r == 128) && v.j[0] == v.r && v.j[1] == v.r &&
+         v.j[2] == v.r && big_encode_fn() != nullptr;
+}
+
+size_t big_scratch_bytes(const KView& v, const int32_t* dims, bool core) {
+  const size_t w = (size_t)v.r;
+  size_t f = 2 * kN * w * w;  // B operand images
+  if (core) {
+    f += (size_t)num_sms() * kN * w * w;  // per-CTA gradients
+    for (int n = 0; n < kN; ++n) f += (size_t)dims[n] * w;  // rounded A copies
+  }
+  return f * sizeof(float);
+}
+
+cudaError_t launch_big_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                              float lr, float reg, int atomic_update, float* scratch,
+                              size_t scratch_bytes, cudaStream_t st) {
+  if (v.ntiles == 0) return cudaSuccess;
+  if (scratch_bytes < 2 * kN * (size_t)v.r * v.r * sizeof(float)) return cudaErrorInvalidValue;
+  return v.r == 64 ? run_factor<64>(v, dims, mul, add, lr, reg, atomic_update, scratch, st)
+                   : run_factor<128>(v, dims, mul, add, lr, reg, atomic_update, scratch, st);
+}
+
+cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                            float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  return v.r == 64 ? run_core<64>(v, dims, mul, add, grad, scratch, scratch_bytes, st)
+                   : run_core<128>(v, dims, mul, add, grad, scratch, scratch_bytes, st);
+}
+
+}  // namespace ftkcu
