@@ -7,9 +7,9 @@
 //
 //   factor   C_n = A_n B_n        n = 0..2 -> TMEM [nW, (n+1)W)  (3 stages)
 //            epilogue: x_hat, r, D'_n = lr r prod_{m!=n} C_m, in place
-//            U_n = D'_n B_n^T     n = 0..2 -> TMEM [3W, 4W)     (3 stages,
-//            the stage's rows give the regulariser term); a += U - lr reg a
-//            as vector RED (Hogwild accumulate) or STG (overwrite rule)
+//            U_n = D'_n B_n^T     n = 0..2 -> TMEM [3W, 4W)     (3 stages of
+//            B images only); a += U - lr reg a, a re-read through L2, as
+//            vector RED (Hogwild accumulate) or STG (overwrite rule)
 //   core     one launch per mode p (TMEM holds C for all modes plus G_p):
 //            C_n as above, D'_p = r prod_{m!=p} C_m into shared memory,
 //            G_p += A_p^T D'_p    (A_p gathered again in the MN-major layout)
@@ -45,25 +45,34 @@ struct BigLayout {
   // tile it runs into the stage's B image / the next stage / the D' tile
   static constexpr uint32_t o_idx = o_d + d_bytes;
   static constexpr uint32_t kIdx = (kN + 1) * kRows * 4;
-  static constexpr uint32_t o_rows = o_idx + 2 * kIdx;
+  static constexpr int kI = 4;  // COO-record ring depth
+  static constexpr uint32_t o_rows = o_idx + kI * kIdx;
   static constexpr uint32_t o_bar = o_rows + 16;
   static constexpr uint32_t o_tmem = o_bar + 32 * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
-  static constexpr uint32_t tcols = W == 64 ? 256 : 512;  // C/D 3W + U or G W
+  // TMEM: factor C/D [0, 3W) + U regions (one per mode at W = 64, so U_0..2
+  // issue back to back; one shared at W = 128); core: C buffers (two at
+  // W = 64, so C(k+1) overlaps the epilogue of k) + G_pass.
+  static constexpr int kUN = W == 64 ? kN : 1;
+  static constexpr int kCB = W == 64 ? 2 : 1;
+  static constexpr uint32_t t_u = 3 * W;
+  static constexpr uint32_t t_g = kCB * 3 * W;
+  static constexpr uint32_t tcols = 512;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
-  static_assert(4 * W <= 512, "TMEM budget");
+  static_assert((kCore ? t_g + W : t_u + kUN * W) <= tcols, "TMEM budget");
 };
 
 enum : int {
   B_FULL = 0,    // [4] stage loaded
-  B_EMPTY = 4,   // [4] stage free
-  B_IFULL = 8,   // [2] COO record landed
-  B_IEMPTY = 10, // [2] COO record consumed
-  B_CFULL = 12,  // C for all modes in TMEM
-  B_DFULL = 13,  // D' ready (TMEM in place: factor; smem: core)
-  B_UFULL = 14,  // factor: U_n in TMEM
-  B_UEMPTY = 15, // factor: U_n read
-  B_DEMPTY = 16, // core: G GEMM done with the D' tile
+  B_EMPTY = 4,   // [4] stage free (released by the MMA that read it)
+  B_IFULL = 8,   // [4] COO record landed
+  B_IEMPTY = 12, // [4] COO record consumed
+  B_CFULL = 16,  // [2] C for all modes in TMEM buffer b
+  B_DFULL = 18,  // D' ready (TMEM in place: factor; smem: core)
+  B_UFULL = 19,  // [3] factor: U_n in TMEM
+  B_UEMPTY = 22, // factor, one U region: U read
+  B_DEMPTY = 23, // core: G GEMM done with the D' tile
+  B_CEMPTY = 24, // [2] core: C buffer b read by the epilogue
 };
 
 struct BigParams {
@@ -91,16 +100,23 @@ __device__ __forceinline__ int64_t big_tile(const BigParams& p, int64_t k) {
 
 __device__ __forceinline__ uint32_t rn_bits(float x) { return __float_as_uint(x) + 0x1000u; }
 
-// Producer: gathers the W / 32 column blocks of a mode's 128 rows.
+// Producer (one elected lane of a converged warp, so every TMA operand is
+// warp-uniform): gathers the W / 32 column blocks of a mode's 128 rows, eight
+// index loads in flight ahead of their issues.
 template <int W>
 __device__ __forceinline__ void gather_rows(uint8_t* dst, const CUtensorMap* tm,
                                             const int32_t* s_idx, uint64_t* bar) {
 #pragma unroll 1
-  for (int g = 0; g < kRows / 4; ++g) {
-    const int4 r = *reinterpret_cast<const int4*>(s_idx + g * 4);
+  for (int g0 = 0; g0 < kRows / 4; g0 += 8) {
+    int4 r[8];
 #pragma unroll
-    for (int cb = 0; cb < W / 32; ++cb)
-      tma_gather4(dst + cb * kBlk + g * 512, tm, cb * 32, r.x, r.y, r.z, r.w, bar);
+    for (int g = 0; g < 8; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+#pragma unroll
+      for (int cb = 0; cb < W / 32; ++cb)
+        tma_gather4(dst + cb * kBlk + (g0 + g) * 512, tm, cb * 32, r[g].x, r[g].y, r[g].z,
+                    r[g].w, bar);
   }
 }
 
@@ -112,13 +128,16 @@ __device__ void big_setup(uint8_t* sm, uint64_t* bars, uint32_t* tslot, const Bi
       mbar_init(&bars[B_FULL + s], 1);
       mbar_init(&bars[B_EMPTY + s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::kI; ++i) {
       mbar_init(&bars[B_IFULL + i], 1);
       mbar_init(&bars[B_IEMPTY + i], 1);
     }
-    mbar_init(&bars[B_CFULL], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[B_CFULL + b], 1);
+      mbar_init(&bars[B_CEMPTY + b], 1);
+    }
+    for (int n = 0; n < kN; ++n) mbar_init(&bars[B_UFULL + n], 1);
     mbar_init(&bars[B_DFULL], 1);
-    mbar_init(&bars[B_UFULL], 1);
     mbar_init(&bars[B_UEMPTY], 1);
     mbar_init(&bars[B_DEMPTY], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -146,46 +165,94 @@ __device__ void big_teardown(uint32_t tmem) {
                  "r"(BigLayout<W, kCore>::tcols));
 }
 
-// Warp 0: per tile the COO record, then one stage per job.  Jobs per tile:
-// factor C0 C1 C2 U0 U1 U2; core C0 C1 C2 G.
+// Warp 0 (all lanes wait, one elected lane issues): per tile the COO
+// record, then one stage per job.  Job order = the MMA warp's: factor
+// C(0) [U(k) C(k+1)]...; core C(0) [C(k+1) G(k)]...
 template <int W, bool kCore>
 __device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = BigLayout<W, kCore>;
-  if ((threadIdx.x & 31) != 0) return;
-  constexpr int kJobs = kCore ? kN + 1 : 2 * kN;
   int64_t job = 0;
-  for (int64_t k = 0; k < nk; ++k) {
-    const int i = (int)(k & 1);
+  // COO records are requested kAhead tiles before their rows are gathered
+  // (the stream comes from HBM: ~1 us per request)
+  constexpr int kAhead = 2;
+  auto request = [&](int64_t k) {  // tile k's COO record -> ring slot
+    if (k >= nk) return;
+    const int i = (int)(k % L::kI);
     const int64_t tile = big_tile(p, k);
-    mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k >> 1) & 1) ^ 1));
+    mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdx);
-    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
-    mbar_expect_tx(&bars[B_IFULL + i], L::kIdx);
-    for (int n = 0; n < kN; ++n)
-      bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
-    bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
-    mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
-    for (int j = 0; j < kJobs; ++j, ++job) {
-      const int s = (int)(job % L::kStages);
-      mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((job / L::kStages) & 1) ^ 1));
+    if (elect_one()) {
+      reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+      mbar_expect_tx(&bars[B_IFULL + i], L::kIdx);
+      for (int n = 0; n < kN; ++n)
+        bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+      bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
+    }
+    __syncwarp();
+  };
+  auto record = [&](int64_t k) {  // request k + kAhead, wait for k
+    request(k + kAhead);
+    mbar_wait(&bars[B_IFULL + (int)(k % L::kI)], (uint32_t)((k / L::kI) & 1));
+  };
+  auto stage = [&]() {
+    const int s = (int)(job % L::kStages);
+    mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((job / L::kStages) & 1) ^ 1));
+    ++job;
+    return s;
+  };
+  auto idx_of = [&](int64_t k) {
+    return reinterpret_cast<const int32_t*>(sm + L::o_idx + (k % L::kI) * L::kIdx);
+  };
+  auto c_jobs = [&](int64_t k) {  // rows of every mode + the C GEMM's B images
+    for (int n = 0; n < kN; ++n) {
+      const int s = stage();
       uint8_t* st = sm + L::o_st + s * L::kStage;
-      if (kCore && j == kN) {  // G operand: A_pass rows, MN-major
-        mbar_expect_tx(&bars[B_FULL + s], L::kA);
-        gather_rows<W>(st, &p.tmap_mn, s_idx + p.pass * kRows, &bars[B_FULL + s]);
-        continue;
+      if (elect_one()) {
+        mbar_expect_tx(&bars[B_FULL + s], L::kStage);
+        gather_rows<W>(st, &p.tmap[n], idx_of(k) + n * kRows, &bars[B_FULL + s]);
+        bulk_g2s(st + L::kA, p.bt_img[n], L::kB, &bars[B_FULL + s]);
       }
-      const int n = j % kN;
-      const bool u = !kCore && j >= kN;
-      mbar_expect_tx(&bars[B_FULL + s], L::kStage);
-      gather_rows<W>(st, &p.tmap[n], s_idx + n * kRows, &bars[B_FULL + s]);
-      bulk_g2s(st + L::kA, u ? p.b_img[n] : p.bt_img[n], L::kB, &bars[B_FULL + s]);
+      __syncwarp();
+    }
+  };
+  if (nk == 0) return;
+  for (int64_t k = 0; k < kAhead; ++k) request(k);
+  record(0);
+  c_jobs(0);
+  for (int64_t k = 0; k < nk; ++k) {
+    if constexpr (kCore) {  // C(k + 1) ahead of G(k), the MMA warp's order
+      if (k + 1 < nk) {
+        record(k + 1);
+        c_jobs(k + 1);
+      }
+      const int s = stage();  // G operand: A_pass rows, MN-major
+      if (elect_one()) {
+        mbar_expect_tx(&bars[B_FULL + s], L::kA);
+        gather_rows<W>(sm + L::o_st + s * L::kStage, &p.tmap_mn, idx_of(k) + p.pass * kRows,
+                       &bars[B_FULL + s]);
+      }
+      __syncwarp();
+    } else {
+      for (int n = 0; n < kN; ++n) {  // U jobs: the B images only
+        const int s = stage();
+        if (elect_one()) {
+          mbar_expect_tx(&bars[B_FULL + s], L::kB);
+          bulk_g2s(sm + L::o_st + s * L::kStage + L::kA, p.b_img[n], L::kB, &bars[B_FULL + s]);
+        }
+        __syncwarp();
+      }
+      if (k + 1 < nk) {
+        record(k + 1);
+        c_jobs(k + 1);
+      }
     }
   }
 }
 
 // C_n = A_n B_n for the three modes of one tile (stages job..job+2).
 template <int W, bool kCore>
-__device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tmem, int64_t& job) {
+__device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tmem, int64_t& job,
+                                        int cb) {
   using L = BigLayout<W, kCore>;
   constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
   for (int n = 0; n < kN; ++n, ++job) {
@@ -200,7 +267,7 @@ __device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tm
              sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
     mma_commit(&bars[B_EMPTY + s]);
   }
-  mma_commit(&bars[B_CFULL]);
+  mma_commit(&bars[B_CFULL + cb]);
 }
 
 // Epilogue: x_hat = sum_r prod_n C_n and the residual of this thread's row.
@@ -232,8 +299,6 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kU = 3 * W;
-
   if (warp == 0) {
     big_producer<W, false>(p, sm, bars, nk);
   } else if (warp == 1) {
@@ -241,20 +306,23 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
       constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
       int64_t job = 0;
       for (int64_t k = 0; k < nk; ++k) {
-        issue_c<W, false>(sm, bars, tmem, job);
+        // C(k) overwrites D'(k - 1): in-order behind U(k - 1) on the tensor pipe
+        issue_c<W, false>(sm, bars, tmem, job, 0);
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n, ++job) {
           const int s = (int)(job % L::kStages);
           const int64_t u = k * kN + n;
           mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
-          mbar_wait(&bars[B_UEMPTY], (uint32_t)((u & 1) ^ 1));
+          if (L::kUN == 1) mbar_wait(&bars[B_UEMPTY], (uint32_t)((u & 1) ^ 1));
           tc_after();
           const uint32_t b0 = smem_u32(sm + L::o_st + s * L::kStage) + L::kA;
+          const uint32_t tu = tmem + L::t_u + (n % L::kUN) * W;
 #pragma unroll
           for (int ks = 0; ks < W / 8; ++ks)
-            mma_ts(tmem + kU, tmem + n * W + ks * 8,
+            mma_ts(tu, tmem + n * W + ks * 8,
                    sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
-          mma_commit(&bars[B_UFULL]);
+          mma_commit(&bars[B_EMPTY + s]);
+          mma_commit(&bars[B_UFULL + n % L::kUN]);
         }
       }
     }
@@ -263,15 +331,16 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const float lr_reg = p.lr * p.reg;
     for (int64_t k = 0; k < nk; ++k) {
-      const int i = (int)(k & 1);
+      const int i = (int)(k % L::kI);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
-      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
       mbar_wait(&bars[B_CFULL], (uint32_t)(k & 1));
       tc_after();
       const float xhat = big_xhat<W>(tl);
       const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
       const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
       const float sc = p.lr * resid;
+      constexpr int kH = W < 64 ? W : 64;  // columns per prefetched half-row
       // D'_n = lr r prod_{m != n} C_m, in place over C (A operand of U_n)
 #pragma unroll 1
       for (int c = 0; c < W / 16; ++c) {
@@ -301,22 +370,30 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
 #pragma unroll
       for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
       for (int n = 0; n < kN; ++n) {
-        const int64_t job = k * 2 * kN + kN + n, u = k * kN + n;
-        const int s = (int)(job % L::kStages);
-        mbar_wait(&bars[B_UFULL], (uint32_t)(u & 1));
-        tc_after();
-        const uint8_t* at = sm + L::o_st + s * L::kStage;  // this mode's rows (for reg a)
+        const int64_t u = k * kN + n;
         float* dst = p.a[n] + (size_t)g[n] * W;
 #pragma unroll 1
-        for (int c = 0; c < W / 16; ++c) {
+        for (int hh = 0; hh < W / kH; ++hh) {
+        // the live row (through L2) for the regulariser term, loaded ahead of
+        // the U wait so its latency overlaps the U GEMM
+        float4 a4[kH / 4];
+#pragma unroll
+        for (int q = 0; q < kH / 4; ++q)
+          a4[q] = ok ? __ldcg(reinterpret_cast<const float4*>(dst + hh * kH + q * 4))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hh == 0) {
+          mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
+          tc_after();
+        }
+#pragma unroll
+        for (int c = 0; c < kH / 16; ++c) {
           uint32_t v[16];
-          tmem_ld16(tl + kU + c * 16, v);
+          tmem_ld16(tl + L::t_u + (n % L::kUN) * W + hh * kH + c * 16, v);
           tmem_wait_ld();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const int col = c * 16 + q4 * 4;
-            const float4 a = *reinterpret_cast<const float4*>(
-                at + (col / 32) * kBlk + swz(row, (col % 32) * 4, 128));
+            const int col = hh * kH + c * 16 + q4 * 4;
+            const float4 a = a4[c * 4 + q4];
             float4 st;
             st.x = __uint_as_float(v[q4 * 4 + 0]) - lr_reg * a.x;
             st.y = __uint_as_float(v[q4 * 4 + 1]) - lr_reg * a.y;
@@ -335,11 +412,11 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
             }
           }
         }
+        }
         tc_before();
         named_bar(1, 128);
         if (warp == 2 && lane == 0) {
-          mbar_arrive(&bars[B_UEMPTY]);
-          mbar_arrive(&bars[B_EMPTY + s]);
+          if (L::kUN == 1) mbar_arrive(&bars[B_UEMPTY]);
           if (n == kN - 1) mbar_arrive(&bars[B_IEMPTY + i]);
         }
       }
@@ -359,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_cons
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kG = 3 * W;
+  constexpr uint32_t kG = L::t_g;
   const int pm = p.pass;
 
   if (warp == 0) {
@@ -369,8 +446,16 @@ __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_cons
       constexpr uint32_t idg = idesc_tf32(128, W, 1, 1);
       const uint32_t d0 = smem_u32(sm + L::o_d);
       int64_t job = 0;
+      // order C(0), then per tile C(k + 1) (into the other buffer at W = 64)
+      // ahead of G(k), so the C GEMMs overlap the epilogue
+      auto c_of = [&](int64_t k) {
+        const int cb = (int)(k % L::kCB);
+        mbar_wait(&bars[B_CEMPTY + cb], (uint32_t)(((k / L::kCB) & 1) ^ 1));
+        issue_c<W, true>(sm, bars, tmem + cb * 3 * W, job, cb);
+      };
+      if (nk > 0) c_of(0);
       for (int64_t k = 0; k < nk; ++k) {
-        issue_c<W, true>(sm, bars, tmem, job);
+        if (k + 1 < nk) c_of(k + 1);
         const int s = (int)(job % L::kStages);
         mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
@@ -392,12 +477,14 @@ __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_cons
     const int q = warp & 3, row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     for (int64_t k = 0; k < nk; ++k) {
-      const int i = (int)(k & 1);
+      const int i = (int)(k % L::kI);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
-      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k >> 1) & 1));
-      mbar_wait(&bars[B_CFULL], (uint32_t)(k & 1));
+      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
+      const int cb = (int)(k % L::kCB);
+      const uint32_t tc = tl + cb * 3 * W;
+      mbar_wait(&bars[B_CFULL + cb], (uint32_t)((k / L::kCB) & 1));
       tc_after();
-      const float xhat = big_xhat<W>(tl);
+      const float xhat = big_xhat<W>(tc);
       const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
       const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
       mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with D'
@@ -405,8 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_cons
 #pragma unroll 1
       for (int c = 0; c < W / 16; ++c) {
         uint32_t v0[16], v1[16];
-        tmem_ld16(tl + m0 * W + c * 16, v0);
-        tmem_ld16(tl + m1 * W + c * 16, v1);
+        tmem_ld16(tc + m0 * W + c * 16, v0);
+        tmem_ld16(tc + m1 * W + c * 16, v1);
         tmem_wait_ld();
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -424,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_cons
       tc_before();
       named_bar(1, 128);
       if (warp == 2 && lane == 0) {
+        mbar_arrive(&bars[B_CEMPTY + cb]);
         mbar_arrive(&bars[B_DFULL]);
         mbar_arrive(&bars[B_IEMPTY + i]);
       }
