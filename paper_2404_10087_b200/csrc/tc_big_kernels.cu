@@ -39,8 +39,10 @@ struct BigLayout {
   static constexpr uint32_t kStage = kA + kB;
   static constexpr int kStages = W == 64 ? (kCore ? 3 : 4) : 1;
   static constexpr uint32_t o_st = 0;
-  static constexpr uint32_t o_d = o_st + kStages * kStage;  // core: D' tile (MN-major)
-  static constexpr uint32_t d_bytes = kCore ? kA : 0;
+  // core: D' tile (MN-major); factor at W = 64: -lr reg I, the regulariser
+  // as a second U GEMM operand (the C stages stay alive until U_n)
+  static constexpr uint32_t o_d = o_st + kStages * kStage;
+  static constexpr uint32_t d_bytes = kCore ? kA : (W == 64 ? kB : 0);
   // the G GEMM reads M = 128 rows = 4 blocks of the A part: past a W = 64
   // tile it runs into the stage's B image / the next stage / the D' tile
   static constexpr uint32_t o_idx = o_d + d_bytes;
@@ -252,11 +254,12 @@ __device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, in
 // C_n = A_n B_n for the three modes of one tile (stages job..job+2).
 template <int W, bool kCore>
 __device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tmem, int64_t& job,
-                                        int cb) {
+                                        int cb, bool release = true, int* cs = nullptr) {
   using L = BigLayout<W, kCore>;
   constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
   for (int n = 0; n < kN; ++n, ++job) {
     const int s = (int)(job % L::kStages);
+    if (cs) cs[n] = s;
     mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
     tc_after();
     const uint32_t a0 = smem_u32(sm + L::o_st + s * L::kStage);
@@ -265,7 +268,7 @@ __device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tm
     for (int ks = 0; ks < W / 8; ++ks)
       mma_ss(tmem + n * W, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
              sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
-    mma_commit(&bars[B_EMPTY + s]);
+    if (release) mma_commit(&bars[B_EMPTY + s]);
   }
   mma_commit(&bars[B_CFULL + cb]);
 }
@@ -288,13 +291,26 @@ __device__ __forceinline__ float big_xhat(uint32_t tl) {
   return x;
 }
 
-template <int W>
+// kFold (W = 64, Hogwild accumulate): U_n' = D'_n B_n^T + A_n (-lr reg I)
+// is the whole step, so the epilogue only issues REDs; otherwise it re-reads
+// the row through L2 for the regulariser (and the overwrite rule).
+template <int W, bool kFold>
 __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_constant__ BigParams p) {
   using L = BigLayout<W, false>;
+  static_assert(!kFold || L::d_bytes == L::kB, "regulariser operand");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  if constexpr (kFold) {
+    const float dv = __uint_as_float(rn_bits(-p.lr * p.reg));
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+      const int j = e / W, jj = e - j * W;
+      *reinterpret_cast<float*>(sm + L::o_d + (jj / 32) * (W * 128) + swz(j, (jj % 32) * 4, 128)) =
+          j == jj ? dv : 0.0f;
+    }
+    fence_proxy_async();
+  }
   big_setup<W, false>(sm, bars, tslot, p);
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -305,9 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
       int64_t job = 0;
+      const uint32_t dg = smem_u32(sm + L::o_d);
       for (int64_t k = 0; k < nk; ++k) {
         // C(k) overwrites D'(k - 1): in-order behind U(k - 1) on the tensor pipe
-        issue_c<W, false>(sm, bars, tmem, job, 0);
+        int cs[kN];
+        issue_c<W, false>(sm, bars, tmem, job, 0, !kFold, cs);
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n, ++job) {
           const int s = (int)(job % L::kStages);
@@ -321,6 +339,14 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
           for (int ks = 0; ks < W / 8; ++ks)
             mma_ts(tu, tmem + n * W + ks * 8,
                    sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
+          if constexpr (kFold) {  // + A_n (-lr reg I), A_n from its C stage, then free it
+            const uint32_t a0 = smem_u32(sm + L::o_st + cs[n] * L::kStage);
+#pragma unroll
+            for (int ks = 0; ks < W / 8; ++ks)
+              mma_ss(tu, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
+                     sdesc(dg + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, 1);
+            mma_commit(&bars[B_EMPTY + cs[n]]);
+          }
           mma_commit(&bars[B_EMPTY + s]);
           mma_commit(&bars[B_UFULL + n % L::kUN]);
         }
@@ -379,8 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
         float4 a4[kH / 4];
 #pragma unroll
         for (int q = 0; q < kH / 4; ++q)
-          a4[q] = ok ? __ldcg(reinterpret_cast<const float4*>(dst + hh * kH + q * 4))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          a4[q] = (ok && !kFold) ? __ldcg(reinterpret_cast<const float4*>(dst + hh * kH + q * 4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         if (hh == 0) {
           mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
           tc_after();
@@ -394,13 +420,13 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
           for (int q4 = 0; q4 < 4; ++q4) {
             const int col = hh * kH + c * 16 + q4 * 4;
             const float4 a = a4[c * 4 + q4];
-            float4 st;
+            float4 st;  // kFold: a = 0, U' already holds the regulariser
             st.x = __uint_as_float(v[q4 * 4 + 0]) - lr_reg * a.x;
             st.y = __uint_as_float(v[q4 * 4 + 1]) - lr_reg * a.y;
             st.z = __uint_as_float(v[q4 * 4 + 2]) - lr_reg * a.z;
             st.w = __uint_as_float(v[q4 * 4 + 3]) - lr_reg * a.w;
             if (ok) {
-              if (p.atomic_update) {
+              if (kFold || p.atomic_update) {
                 red_add_v4(dst + col, st);
               } else {
                 st.x += a.x;
@@ -627,9 +653,10 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
   p.reg = reg;
   p.atomic_update = atomic_update;
   const int bytes = (int)BigLayout<W, false>::bytes;
-  e = cudaFuncSetAttribute(big_factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  auto kern = (W == 64 && atomic_update) ? big_factor_kernel<W, W == 64> : big_factor_kernel<W, false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  big_factor_kernel<W><<<(int)sweep_grid(v), kThreads, bytes, st>>>(p);
+  kern<<<(int)sweep_grid(v), kThreads, bytes, st>>>(p);
   return cudaGetLastError();
 }
 
