@@ -38,8 +38,11 @@ constexpr int kRows = 128;       // nonzeros per tile == TMEM lanes
 constexpr int kS = 3;            // A-slot ring depth
 constexpr int kEpiWarps = 8;
 // warp 0 COO-column producer, warp 1 MMA, warps 2-9 epilogue, warp 10 gather producer
-constexpr int kThreadsWs = (3 + kEpiWarps) * 32;
-constexpr int kGatherWarp = 2 + kEpiWarps;
+// Gather producers: the tile's 96 TMA gather4 issues are split over kGW
+// warps (one elected lane each) -- a single issuing thread serialises them.
+constexpr int kGW = 2;
+constexpr int kThreadsWs = (2 + kEpiWarps + kGW) * 32;
+constexpr int kGatherWarp = 2 + kEpiWarps;  // first of the kGW gather warps
 constexpr uint32_t kModeTile = kRows * 128;  // 128 rows x 32 fp32 = 16 KB
 
 struct __align__(64) WsParams {
@@ -153,7 +156,7 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
     }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kS; ++s) {
-      mbar_init(&bars[B_FULL + s], 1);
+      mbar_init(&bars[B_FULL + s], kGW);  // one expect_tx arrival per gather warp
       // core, and factor with atomic rows: released by the MMA that last
       // reads the slot; factor overwrite mode: by the epilogue (reads a)
       mbar_init(&bars[B_EMPTY + s], (kCore || p.atomic_update) ? 1 : kEpiWarps);
@@ -216,12 +219,15 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
   }
 }
 
-// Gather warp: as soon as an A slot is free, TMA gather4 of the tile's factor
-// rows (32 lanes x N modes x 4 rows) into it.
+// Gather warps: as soon as an A slot is free, TMA gather4 of the tile's
+// factor rows (N modes x 32 groups of 4 rows) into it; gather warp w issues
+// groups [w * 96 / kGW, (w + 1) * 96 / kGW) and arrives with its own bytes.
 template <bool kCore>
 __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsLayout<kCore>;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, gw = (int)(threadIdx.x >> 5) - kGatherWarp;
+  constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
+  static_assert(kGroups % (kGW * 8) == 0, "whole batches of 8 groups per gather warp");
   for (int64_t k = 0; k < nk; ++k) {
     const int s = (int)(k % kS), i = (int)(k % L::kI);
     mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
@@ -231,26 +237,24 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
       if (lane == 0) mbar_arrive(&bars[B_FULL + s]);
       continue;
     }
-    if (lane == 0) mbar_expect_tx(&bars[B_FULL + s], L::kSlot);
     __syncwarp();
     uint8_t* slot = sm + L::o_a + s * L::kSlot;
-    // One elected thread issues all 96 gathers of the tile: per-lane
-    // operands would make the compiler serialise every TMA issue over the
-    // 32 lanes (R2UR.BROADCAST waterfall).
+    // One elected thread per warp issues: per-lane operands would make the
+    // compiler serialise every TMA issue over the 32 lanes (R2UR waterfall).
     if (elect_one()) {
+      mbar_expect_tx(&bars[B_FULL + s], kPer * 512);
+#pragma unroll 1
+      for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 8) {
+        int4 r[8];  // 8 index loads in flight before the issues
 #pragma unroll
-      for (int n = 0; n < kN; ++n) {
+        for (int g = 0; g < 8; ++g)
+          r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+        const int n = g0 / (kRows / 4);  // a batch of 8 never straddles modes
+        const int gm = g0 - n * (kRows / 4);
 #pragma unroll
-        for (int g0 = 0; g0 < kRows / 4; g0 += 8) {
-          int4 r[8];  // 8 index loads in flight before the issues
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            r[g] = *reinterpret_cast<const int4*>(s_idx + n * kRows + (g0 + g) * 4);
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            tma_gather4(slot + n * kModeTile + (g0 + g) * 512, &p.tmap[n], 0, r[g].x, r[g].y,
-                        r[g].z, r[g].w, &bars[B_FULL + s]);
-        }
+        for (int g = 0; g < 8; ++g)
+          tma_gather4(slot + n * kModeTile + (gm + g) * 512, &p.tmap[n], 0, r[g].x, r[g].y,
+                      r[g].z, r[g].w, &bars[B_FULL + s]);
       }
     }
     __syncwarp();
@@ -277,7 +281,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
 
   if (warp == 0) {
     ws_idx_producer<false>(p, sm, bars, nk);
-  } else if (warp == kGatherWarp) {
+  } else if (warp >= kGatherWarp) {
     ws_gather_producer<false>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
 
   if (warp == 0) {
     ws_idx_producer<true>(p, sm, bars, nk);
-  } else if (warp == kGatherWarp) {
+  } else if (warp >= kGatherWarp) {
     ws_gather_producer<true>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_cc_kernel(const __grid_
 
   if (warp == 0) {
     ws_idx_producer<true>(p, sm, bars, nk);
-  } else if (warp == kGatherWarp) {
+  } else if (warp >= kGatherWarp) {
     ws_gather_producer<true>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
