@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
     ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
+    ap.add_argument("--core16", type=int, default=1,
+                    help="tf32 core sweep on an fp16 copy of A (kind::f16, 10-bit mantissa)")
     ap.add_argument("--store-c", type=int, default=0,
                     help="core sweep storage scheme: C rows from a C cache rebuilt every core "
                          "phase (inside the timed region), EpochOptions.store_c")
@@ -186,6 +188,15 @@ def cpu_reference_time(cfg, j, sample_nnz, steps=1, warmup=1):
     dt = time.perf_counter() - t0
     return {"value": sample_nnz / dt, "unit": "nnz/s", "cores": 1, "kind": "port",
             "sample": sample}
+
+
+def dtype_of(args, order, j):
+    """Operand types of the tensor-core sweeps (all accumulate in fp32)."""
+    if args.precision != "tf32":
+        return "f32" if args.precision == "fp32" else args.precision
+    if order == 3 and j == 32 and args.core16 and not args.store_c and args.tc_ws:
+        return "tf32+f16"  # factor: tf32 operands; core: fp16 copy of A
+    return "tf32"
 
 
 def cfg_name_of(cfg):
@@ -340,6 +351,7 @@ def run_engine(args):
     s.set_option("hog_update", args.hog_update)
     s.set_option("tc_ws", args.tc_ws)
     s.set_option("store_c", args.store_c)
+    s.set_option("core16", args.core16)
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
     s.upload_model(coo.dims, ranks, j, a0, b0)
@@ -436,11 +448,15 @@ def run_engine(args):
             "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": job.scaling, "vs_baseline": None,
-            "dtype": "f32" if prec == 0 else args.precision,
+            "dtype": dtype_of(args, order, j),
             "data": "synthetic (uniform distinct tuples, values U[lo,hi], seeded)",
             "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": coo.nnz,
                        "J": j, "R": j, "M": 16, "mode": "hogwild", "precision": args.precision,
                        "core_scheme": "storage" if args.store_c else "calculation",
+                       "operands": {"factor": args.precision,
+                                    "core": "f16 (RN copy of A, 10-bit mantissa)"
+                                    if dtype_of(args, order, j) == "tf32+f16" else args.precision,
+                                    "accumulate": "f32"},
                        "parallelism": job.parallelism, "nnz_per_rank": job.local_nnz,
                        "test_frac": cfg.get("test_frac", 0.014),
                        "l2": "inputs larger than L2 (COO stream 16 B/nnz per sweep)"},

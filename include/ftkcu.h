@@ -49,7 +49,10 @@ extern "C" {
 
 /* contraction precision for FTKCU_MODE_HOGWILD (ftkcu_set_option) */
 #define FTKCU_PREC_FP32 0   /* FFMA, no tensor cores                        */
-#define FTKCU_PREC_TF32 1   /* tcgen05 kind::tf32, fp32 accumulate          */
+#define FTKCU_PREC_TF32 1   /* single-pass tensor cores, fp32 accumulate:   */
+                            /* 10-bit-mantissa operands rounded to nearest; */
+                            /* kind::tf32, except the N=3 J=R=32 core sweep */
+                            /* (kind::f16 on an fp16 copy of A, "core16")   */
 #define FTKCU_PREC_3XTF32 2 /* tcgen05 split-tf32 (hi*hi + hi*lo + lo*hi)   */
 
 /* evaluation reduction order */
@@ -76,7 +79,9 @@ int ftkcu_abi_version(void);
  * stratum loop, default 1), "staleness" (whole-tensor factor sweeps cap the
  * grid so at most this many nonzeros per row of the smallest mode are in
  * flight; default 32, 0 = off), "global_nnz" (|Omega|
- * over all ranks for the multi-GPU core update), "shuffle_seed", "verbose".
+ * over all ranks for the multi-GPU core update), "store_c" (core phase:
+ * storage scheme, C rows from a C cache), "core16" (default 1; 0 keeps the
+ * N=3 J=R=32 tf32 core sweep on kind::tf32), "shuffle_seed", "verbose".
  * get_option also reads "launches", "stream" (cudaStream_t), "num_sms".
  * Unknown keys are FTKCU_ERR_ARG. */
 int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value);

@@ -173,12 +173,17 @@ cudaError_t launch_tc_core(const KView& v, int64_t tile_mul, int64_t tile_add,
 
 // ---- warp-specialized tensor-core sweeps, N = 3, J = R = 32 (tc_ws_kernels.cu)
 bool ws_supported(const KView& v);
+// Core sweep scratch: per-CTA gradients + the RN-rounded tf32 copy of A.
+size_t ws_core_scratch_bytes(const KView& v, const int32_t* dims);
 cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                              float lr, float reg, int precision, int atomic_update,
                              cudaStream_t st);
+// core16: the single-pass sweep gathers an fp16 copy of A (ws_core16_kernel);
+// 0 = tf32 rows copied into TMEM (ws_core_kernel).  3xtf32 and the storage
+// scheme have their own kernels.
 cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
-                           float* grad, int precision, float* scratch, size_t scratch_bytes,
-                           cudaStream_t st);
+                           float* grad, int precision, int core16, float* scratch,
+                           size_t scratch_bytes, cudaStream_t st);
 
 // ---- evaluation (eval_kernels.cu) ---------------------------------------------
 // out3 = {sum sq, sum abs, reg}; exact = reference slab order.

@@ -33,6 +33,7 @@ struct ftkcu_session {
   int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
+  int64_t opt_core16 = 1;   // WS core sweep (tf32 precision): gather an fp16 copy of A
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -349,6 +350,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_tc_ws = value != 0;
   } else if (k == "store_c") {
     s->opt_store_c = value != 0;
+  } else if (k == "core16") {
+    s->opt_core16 = value != 0;
   } else if (k == "hog_update") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "bad hog_update");
     s->opt_hog_update = value;
@@ -383,6 +386,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "hog_update") *value = s->opt_hog_update;
   else if (k == "tc_ws") *value = s->opt_tc_ws;
   else if (k == "store_c") *value = s->opt_store_c;
+  else if (k == "core16") *value = s->opt_core16;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
   else if (k == "staleness") *value = s->opt_staleness;
@@ -655,6 +659,8 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     if (hog_need > need) need = hog_need;
     if (big_supported(v) && big_scratch_bytes(v, s->model.dims, true) > need)
       need = big_scratch_bytes(v, s->model.dims, true);
+    if (ws_supported(v) && ws_core_scratch_bytes(v, s->model.dims) > need)
+      need = ws_core_scratch_bytes(v, s->model.dims);
     if ((rc = ensure_scratch(s, need))) return rc;
     if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -662,7 +668,8 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     // other tensor-core shapes take the CUDA-core sweep, which reads them too.
     if (s->opt_precision != FTKCU_PREC_FP32 && s->opt_tc_ws && ws_supported(v)) {
       CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
-                        static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+                        (int)s->opt_core16, static_cast<float*>(s->scratch), s->scratch_bytes,
+                        s->stream));
     } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && big_supported(v)) {
       CK(launch_big_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
                          s->scratch_bytes, s->stream));

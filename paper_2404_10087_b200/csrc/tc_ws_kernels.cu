@@ -759,6 +759,267 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_cc_kernel(const __grid_
   ws_teardown(tmem);
 }
 
+// ---- core sweep, fp16 operand tile ------------------------------------------------
+//
+// The gathered rows feed two GEMMs that contract over different indices:
+// C = A B over j (A K-major) and G += A^T (r D) over the nonzeros (A
+// MN-major).  For tf32 tcgen05 reads MN-major operands only in the
+// 128B_BASE32B swizzle, which ws_core_kernel gathers into and then copies row
+// by row into TMEM for the C GEMM (the epilogue on the C GEMM's critical
+// path).  For 16-bit operands any swizzle serves both majors, so this sweep
+// gathers the rows of an fp16 copy of A (round-to-nearest, 10-bit mantissa
+// like tf32; rebuilt per core phase, A is read-only here) ONCE into a
+// 64-B-row SWIZZLE_64B tile that the C GEMM reads K-major and the G GEMM
+// reads MN-major (scripts/microtests/umma_f16.cu), both kind::f16 with fp32
+// accumulation.  Half the bytes per slot buys a 6-deep slot ring.
+//
+//   warp 0     COO columns (ring of kI)       warps 10-11  gathers (half each)
+//   warp 1     MMA: C(k), then G(k - 1)       warps 2-9    epilogue: C -> r D (fp16)
+
+constexpr uint32_t kModeTile16 = kRows * 64;  // 128 rows x 32 fp16
+
+struct Ws16Layout {
+  static constexpr uint32_t kSlot = kN * kModeTile16;  // 24 KB
+  static constexpr int kS = 6;
+  static constexpr uint32_t o_a = 0;
+  // r D tiles (double-buffered); the G GEMM's 4th M segment of the last slot
+  // reads into them
+  static constexpr uint32_t o_d = o_a + kS * kSlot;
+  static constexpr uint32_t o_bt = o_d + 2 * kSlot;  // B^T fp16, C GEMM operand
+  static constexpr uint32_t o_idx = o_bt + kN * 2048;
+  static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
+  static constexpr int kI = 6;
+  static constexpr uint32_t o_rows = o_idx + kI * kIdxSlot;
+  static constexpr uint32_t o_bar = o_rows + 64;
+  static constexpr uint32_t o_tmem = o_bar + 32 * 8;
+  static constexpr uint32_t bytes = o_tmem + 16;
+  static_assert(bytes <= 227 * 1024, "shared-memory budget");
+};
+
+enum : int {
+  H_FULL = 0,     // [6] slot landed (one expect_tx arrival per gather warp)
+  H_EMPTY = 6,    // [6] slot read by the G GEMM
+  H_IFULL = 12,   // [6] COO columns landed
+  H_IEMPTY = 18,  // [6] COO columns consumed (8 epilogue warps + 2 gather warps)
+  H_CFULL = 24,   // [2] C accumulator ready
+  H_CEMPTY = 26,  // [2] C accumulator read
+  H_DFULL = 28,   // [2] r D tile written
+  H_DEMPTY = 30,  // [2] G GEMM done with the r D tile
+};
+
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// Two floats -> f16x2 (lo, hi), round to nearest, saturating to +-65504
+// instead of overflowing to inf.
+__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__global__ void ws_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  const int64_t n2 = n / 2;  // n = rows x 32: even
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float2 x = reinterpret_cast<const float2*>(src)[e];
+    reinterpret_cast<uint32_t*>(dst)[e] = f16x2_sat(x.x, x.y);
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_constant__ WsParams p) {
+  using L = Ws16Layout;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  for (int n = 0; n < kN; ++n)
+    for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
+      const int j = e / kW, r = e - j * kW;
+      *reinterpret_cast<__half*>(sm + L::o_bt + n * 2048 + swz(r, j * 2, 64)) =
+          __float2half_rn(p.b[n][e]);
+    }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kS; ++s) {
+      mbar_init(&bars[H_FULL + s], kGW);
+      mbar_init(&bars[H_EMPTY + s], 1);
+    }
+    for (int i = 0; i < L::kI; ++i) {
+      mbar_init(&bars[H_IFULL + i], 1);
+      mbar_init(&bars[H_IEMPTY + i], kEpiWarps + kGW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[H_CFULL + b], 1);
+      mbar_init(&bars[H_CEMPTY + b], kEpiWarps);
+      mbar_init(&bars[H_DFULL + b], kEpiWarps);
+      mbar_init(&bars[H_DEMPTY + b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kG = 192;  // TMEM: C[b] at 96 b, G at 192
+
+  if (warp == 0) {
+    if (lane == 0)
+      for (int64_t k = 0; k < nk; ++k) {
+        const int i = (int)(k % L::kI);
+        const int64_t tile = ws_tile(p, k);
+        mbar_wait(&bars[H_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
+        int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+        mbar_expect_tx(&bars[H_IFULL + i], L::kIdxSlot);
+        for (int n = 0; n < kN; ++n)
+          bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
+        bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
+      }
+  } else if (warp >= kGatherWarp) {
+    const int gw = warp - kGatherWarp;
+    constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % L::kS), i = (int)(k % L::kI);
+      mbar_wait(&bars[H_EMPTY + s], (uint32_t)(((k / L::kS) & 1) ^ 1));
+      mbar_wait(&bars[H_IFULL + i], (uint32_t)((k / L::kI) & 1));
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+      uint8_t* slot = sm + L::o_a + s * L::kSlot;
+      __syncwarp();
+      if (elect_one()) {
+        mbar_expect_tx(&bars[H_FULL + s], kPer * 256);
+#pragma unroll 1
+        for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 8) {
+          int4 r[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+          const int n = g0 / (kRows / 4), gm = g0 - n * (kRows / 4);
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            tma_gather4(slot + n * kModeTile16 + (gm + g) * 256, &p.tmap[n], 0, r[g].x, r[g].y,
+                        r[g].z, r[g].w, &bars[H_FULL + s]);
+        }
+        mbar_arrive(&bars[H_IEMPTY + i]);  // indices read before the issues
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idc = idesc_f16(128, kW, 0, 0);
+      constexpr uint32_t idg = idesc_f16(128, kN * kW, 1, 1);
+      const uint32_t bt = smem_u32(sm + L::o_bt), d0 = smem_u32(sm + L::o_d);
+      auto issue_g = [&](int64_t k) {
+        const int s = (int)(k % L::kS), db = (int)(k & 1);
+        mbar_wait(&bars[H_DFULL + db], (uint32_t)((k >> 1) & 1));
+        tc_after();
+        // G[j'][n R + r] += sum_t A[t][j'] (r D_n)[t][r]: M = 3 stacked modes
+        // (+ one garbage block), N = 96, K = 16 nonzeros per instruction
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot), dd = d0 + db * L::kSlot;
+#pragma unroll
+        for (int ks = 0; ks < kRows / 16; ++ks)
+          mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
+                  sdesc_l(dd + ks * 1024, kModeTile16, 512, 4), idg, (k > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&bars[H_DEMPTY + db]);
+        mma_commit(&bars[H_EMPTY + s]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % L::kS), b = (int)(k & 1);
+        mbar_wait(&bars[H_FULL + s], (uint32_t)((k / L::kS) & 1));
+        mbar_wait(&bars[H_CEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 16; ++ks)
+            mma_f16(tmem + b * 96 + n * kW, sdesc_l(a0 + n * kModeTile16 + ks * 32, 16, 512, 4),
+                    sdesc_l(bt + n * 2048 + ks * 32, 16, 512, 4), idc, ks > 0);
+        mma_commit(&bars[H_CFULL + b]);
+        if (k >= 1) issue_g(k - 1);
+      }
+      if (nk >= 1) issue_g(nk - 1);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int b = (int)(k & 1), ii = (int)(k % L::kI);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
+      const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
+      mbar_wait(&bars[H_IFULL + ii], (uint32_t)((k / L::kI) & 1));
+      mbar_wait(&bars[H_CFULL + b], (uint32_t)((k >> 1) & 1));
+      tc_after();
+      float c[kN][16];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+        tmem_ld16(tl + b * 96 + n * kW + h * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
+      }
+      const float xhat = xhat_full(tl + b * 96 + (h ^ 1) * 16, c);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[H_CEMPTY + b]);  // C(k + 2) may land
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
+      const float resid = ok ? s_val[row] - xhat : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[H_IEMPTY + ii]);
+      mbar_wait(&bars[H_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // G(k - 2) done with D[b]
+      uint8_t* dt = sm + L::o_d + b * L::kSlot;
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {  // 8 fp16 = one 16-B chunk
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i0 = q2 * 8 + e * 2;
+#define FTK_D(ii) (n == 0 ? c[1][ii] * c[2][ii] : (n == 1 ? c[0][ii] * c[2][ii] : c[0][ii] * c[1][ii]))
+            w[e] = f16x2_sat(resid * FTK_D(i0), resid * FTK_D(i0 + 1));
+#undef FTK_D
+          }
+          *reinterpret_cast<uint4*>(dt + n * kModeTile16 + swz(row, (h * 16 + q2 * 8) * 2, 64)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[H_DFULL + b]);
+    }
+    if (nk > 0) mbar_wait(&bars[H_DEMPTY + (int)((nk - 1) & 1)], (uint32_t)(((nk - 1) >> 1) & 1));
+    tc_after();
+    if (q < kN) {
+      uint32_t v[16];
+      tmem_ld16(tl + kG + q * kW + h * 16, v);
+      tmem_wait_ld();
+      float* out = p.partials + (size_t)blockIdx.x * (kN * kW * kW) + ((size_t)q * kW + lane) * kW + h * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = nk > 0 ? __uint_as_float(v[i]) : 0.0f;
+    }
+  }
+  ws_teardown(tmem);
+}
+
 __global__ void ws_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
                                  float* __restrict__ grad) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
@@ -793,6 +1054,19 @@ bool make_row_map(CUtensorMap* tm, const float* a, int64_t rows, bool atom32) {
   return r == CUDA_SUCCESS;
 }
 
+// Row-gather map of an fp16 copy of A_n (rows x 32 fp16): box of one 64-B row.
+bool make_row_map16(CUtensorMap* tm, const __half* a, int64_t rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)kW, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kW * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kW, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                  bool core) {
   for (int n = 0; n < kN; ++n) {
@@ -813,6 +1087,14 @@ bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, 
 }
 
 }  // namespace
+
+size_t ws_core_scratch_bytes(const KView& v, const int32_t* dims) {
+  size_t f = (size_t)num_sms() * kN * kW * kW;  // per-CTA gradients
+  size_t h = 0;
+  for (int n = 0; n < v.order && n < kN; ++n) h += (size_t)dims[n] * kW;  // fp16 copy of A
+  f += (h + 1) / 2;
+  return f * sizeof(float);
+}
 
 bool ws_supported(const KView& v) {
   return v.order == kN && v.r == kW && v.j[0] == kW && v.j[1] == kW && v.j[2] == kW &&
@@ -840,8 +1122,8 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
 }
 
 cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
-                           float* grad, int precision, float* scratch, size_t scratch_bytes,
-                           cudaStream_t st) {
+                           float* grad, int precision, int core16, float* scratch,
+                           size_t scratch_bytes, cudaStream_t st) {
   WsParams p{};
   if (!make_params(p, v, dims, mul, add, true)) return cudaErrorNotSupported;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
@@ -852,11 +1134,32 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   if (scratch_bytes < (size_t)grid * len * sizeof(float)) return cudaErrorInvalidValue;
   p.partials = scratch;
   for (int n = 0; n < kN; ++n) p.cc[n] = v.cc[n];
-  const int bytes = (int)WsLayout<true>::bytes;
-  auto kern = v.cc[0] ? ws_core_cc_kernel : ws_core_kernel;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kThreadsWs, bytes, st>>>(p);
+  cudaError_t e;
+  if (!v.cc[0] && !p.prec3 && core16) {
+    // fp16 copy of A (after the partials), gathered once per tile
+    if (scratch_bytes < ws_core_scratch_bytes(v, dims)) return cudaErrorInvalidValue;
+    __half* a16 = reinterpret_cast<__half*>(scratch + (size_t)num_sms() * len);
+    for (int n = 0; n < kN; ++n) {
+      const int64_t cnt = (int64_t)dims[n] * kW;
+      int64_t blocks = (cnt + 255) / 256;
+      if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+      ws_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, cnt);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (!make_row_map16(&p.tmap[n], a16, dims[n])) return cudaErrorNotSupported;
+      a16 += cnt;
+    }
+    const int bytes = (int)Ws16Layout::bytes;
+    e = cudaFuncSetAttribute(ws_core16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    ws_core16_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+  } else {
+    const int bytes = (int)WsLayout<true>::bytes;
+    auto kern = v.cc[0] ? ws_core_cc_kernel : ws_core_kernel;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreadsWs, bytes, st>>>(p);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ws_reduce_kernel<<<(len + 255) / 256, 256, 0, st>>>(scratch, grid, len, grad);
