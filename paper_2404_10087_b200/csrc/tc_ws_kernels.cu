@@ -408,11 +408,11 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
       const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
-      // Per mode: both warps of the quarter write their column half of the
-      // step rows into the quarter's 4 KB staging tile, then each warp sends
-      // 16 whole 128-B rows (8 lanes per row) -- one coalesced RED (or STG)
-      // request per row instead of eight 16-B ones.
-      uint8_t* stage = sm + L::o_stage + q * 4096;
+      // Per mode: the warp writes its column half of its 32 step rows into a
+      // private 2 KB staging tile (64-B rows, 16-B chunks XOR (row/2) % 4:
+      // conflict-free both ways), then sends them as 64-B row segments, 8
+      // rows per RED (or STG) instruction -- no cross-warp barrier.
+      uint8_t* stage = sm + L::o_stage + ew * 2048;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
 #pragma unroll
@@ -429,25 +429,25 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
             st.z = a.z + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
             st.w = a.w + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
           }
-          *reinterpret_cast<float4*>(stage + swz(lane, (h * 16 + q4 * 4) * 4, 128)) = st;
+          *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
         }
-        named_bar(1 + q, 64);
+        __syncwarp();
         float* dst = p.a[n];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
+          const int rl = i * 8 + (lane >> 2), ch = lane & 3;
           const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
           const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
-          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
+          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
           if (okr) {
-            float* gp = dst + (size_t)g * kW + ch * 4;
+            float* gp = dst + (size_t)g * kW + h * 16 + ch * 4;
             if constexpr (kAtomic)
               red_add_v4(gp, v);
             else
               *reinterpret_cast<float4*>(gp) = v;
           }
         }
-        named_bar(1 + q, 64);
+        __syncwarp();
       }
       if constexpr (!kAtomic) {
         __syncwarp();
