@@ -69,9 +69,11 @@ struct WsLayout {
   // (garbage) M segment of the last slot then still reads shared memory.
   static constexpr uint32_t o_d = o_a + kS * kSlot;
   static constexpr uint32_t d_bytes = kCore ? kN * kModeTile : 0;
-  static constexpr uint32_t o_bt = o_d + d_bytes;       // B^T hi  (C GEMM operand)
-  static constexpr uint32_t o_btlo = o_bt + kN * 4096;  // B^T lo
-  static constexpr uint32_t o_b = o_btlo + kN * 4096;   // B (U GEMM operand, factor)
+  // C GEMM operand per mode: core B^T (hi, then lo); factor [B^T ; I], the
+  // identity rows copying the A rows into TMEM for the regulariser GEMM
+  static constexpr uint32_t o_bt = o_d + d_bytes;
+  static constexpr uint32_t o_btlo = o_bt + kN * (kCore ? 4096 : 8192);
+  static constexpr uint32_t o_b = o_btlo + (kCore ? kN * 4096 : 0);  // B (U GEMM operand, factor)
   // factor: -lr reg I (K-major), the regulariser as a second U GEMM operand
   static constexpr uint32_t o_diag = o_b + (kCore ? 0 : kN * 4096);
   static constexpr uint32_t o_idx = o_diag + (kCore ? 0 : 4096);
@@ -110,12 +112,14 @@ enum : int {
 __device__ __forceinline__ uint32_t tf32_rn_bits(float x) { return __float_as_uint(x) + 0x1000u; }
 
 // x_hat = sum_r C0 C1 C2 over all 32 columns of this row: the warp's own
-// column half c[][] plus the other half, loaded and consumed here.
-__device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)[kN][16]) {
+// column half c[][] plus the other half, loaded and consumed here (modes
+// `stride` TMEM columns apart).
+__device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)[kN][16],
+                                           uint32_t stride = kW) {
   uint32_t o0[16], o1[16], o2[16];
   tmem_ld16(tcol_other, o0);
-  tmem_ld16(tcol_other + kW, o1);
-  tmem_ld16(tcol_other + 2 * kW, o2);
+  tmem_ld16(tcol_other + stride, o1);
+  tmem_ld16(tcol_other + 2 * stride, o2);
   tmem_wait_ld();
   float x = 0.0f;
 #pragma unroll
@@ -142,10 +146,15 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
       const int j = e / kW, r = e - j * kW;
       const float x = b[e];
       const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
-      *reinterpret_cast<float*>(sm + L::o_bt + n * 4096 + swz(r, j * 4, 128)) = hi;
-      *reinterpret_cast<float*>(sm + L::o_btlo + n * 4096 + swz(r, j * 4, 128)) = lo;
-      if constexpr (!kCore)
+      if constexpr (kCore) {
+        *reinterpret_cast<float*>(sm + L::o_bt + n * 4096 + swz(r, j * 4, 128)) = hi;
+        *reinterpret_cast<float*>(sm + L::o_btlo + n * 4096 + swz(r, j * 4, 128)) = lo;
+      } else {
+        *reinterpret_cast<float*>(sm + L::o_bt + n * 8192 + swz(r, j * 4, 128)) = hi;
+        *reinterpret_cast<float*>(sm + L::o_bt + n * 8192 + swz(kW + r, j * 4, 128)) =
+            r == j ? 1.0f : 0.0f;  // identity row r: copies a[j = r]
         *reinterpret_cast<float*>(sm + L::o_b + n * 4096 + swz(j, r * 4, 128)) = hi;
+      }
     }
   }
   if constexpr (!kCore)
@@ -274,10 +283,12 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // TMEM columns: C[b] at 96 b, D[b] at 192 + 96 b, U at 384 (480 of 512).
-  // Separate C / D / U buffers let C(k+1) and U(k) run on the tensor core
-  // while the epilogue works on the other tile, with no wait in between.
-  constexpr uint32_t kC = 0, kD = 192, kU = 384;
+  // TMEM: tile k in buffer b = k & 1 at 192 b; mode n at +64 n holds C_n
+  // (overwritten in place by D'_n) and, with atomic rows, a copy of the A
+  // rows (+32, from the identity half of the C GEMM's B operand) for the
+  // regulariser GEMM; U at 384.  C(k + 2) reuses buffer b only after U(k):
+  // the MMA warp issues U(k) first and the tensor pipe runs in order.
+  constexpr uint32_t kC = 0, kU = 384, kBuf = 192, kMs = 64;
 
   if (warp == 0) {
     ws_idx_producer<false>(p, sm, bars, nk);
@@ -286,46 +297,46 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
+      // atomic rows: N = 64, [C | A] = A [B | I]
+      constexpr uint32_t idc = idesc_tf32(128, kAtomic ? 2 * kW : kW, 0, 0);
       const uint32_t bt = smem_u32(sm + L::o_bt), bb = smem_u32(sm + L::o_b);
       const uint32_t dg = smem_u32(sm + L::o_diag);
       // U(j) = (lr r D_j) B^T [+ A_j (-lr reg I)]: the step itself (atomic
       // rows) or U for the overwrite rule (scaled in the epilogue).
       auto issue_u = [&](int64_t j) {
-        const int b = (int)(j & 1), s = (int)(j % kS);
+        const int b = (int)(j & 1);
         mbar_wait(&bars[B_DFULL + b], (uint32_t)((j >> 1) & 1));
         mbar_wait(&bars[B_UEMPTY], (uint32_t)((j & 1) ^ 1));
         tc_after();
-        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+        const uint32_t tb = tmem + kC + b * kBuf;
 #pragma unroll
         for (int n = 0; n < kN; ++n) {
 #pragma unroll
           for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ts(tmem + kU + n * kW, tmem + kD + b * 96 + n * kW + ks * 8,
+            mma_ts(tmem + kU + n * kW, tb + n * kMs + ks * 8,
                    sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
           if constexpr (kAtomic)
 #pragma unroll
             for (int ks = 0; ks < kW / 8; ++ks)
-              mma_ss(tmem + kU + n * kW, sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
+              mma_ts(tmem + kU + n * kW, tb + n * kMs + kW + ks * 8,
                      sdesc(dg + ks * 32, 16, 1024, 128), id, 1);
         }
         mma_commit(&bars[B_UFULL]);
-        mma_commit(&bars[B_DEMPTY + b]);
-        if constexpr (kAtomic) mma_commit(&bars[B_EMPTY + s]);  // last read of the A slot
       };
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kS), b = (int)(k & 1);
         mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
-        mbar_wait(&bars[B_CEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
         for (int n = 0; n < kN; ++n)
 #pragma unroll
           for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ss(tmem + kC + b * 96 + n * kW,
+            mma_ss(tmem + kC + b * kBuf + n * kMs,
                    sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
-                   sdesc(bt + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
+                   sdesc(bt + n * 8192 + ks * 32, 16, 1024, 128), idc, ks > 0);
         mma_commit(&bars[B_CFULL + b]);
+        if constexpr (kAtomic) mma_commit(&bars[B_EMPTY + s]);  // the only read of the A slot
         if (k >= 1) issue_u(k - 1);
       }
       if (nk >= 1) issue_u(nk - 1);
@@ -351,19 +362,25 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
       mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
+      const uint32_t tb = tl + kC + b * kBuf;
       float c[kN][16];
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
-        tmem_ld16(tl + kC + b * 96 + n * kW + h * 16, v);
+        tmem_ld16(tb + n * kMs + h * 16, v);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
       }
-      const float xhat = xhat_full(tl + kC + b * 96 + (h ^ 1) * 16, c);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_CEMPTY + b]);  // C(k + 2) may land
+      // x_hat halves exchanged with the sibling warp of this lane quarter
+      // (each warp reads only its own half of C, so D' can go over it in place)
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      float* xp = reinterpret_cast<float*>(sm + L::o_xp);  // [2 tiles][2 halves][128]
+      xp[(b * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
       t.slot = s;
 #pragma unroll
       for (int n = 0; n < kN; ++n) t.g[n] = s_idx[n * kRows + row];
@@ -378,8 +395,6 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       const float sc = kAtomic ? p.lr * t.resid : 1.0f;
 #pragma unroll
       for (int i = 0; i < 16; ++i) c[0][i] *= sc;  // D'_1 = (sc c0) c2, D'_2 = (sc c0) c1
-      mbar_wait(&bars[B_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // U(k - 2) read D[b]
-      tc_after();
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
                                  : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
           v[i] = tf32_rn_bits(d);
         }
-        tmem_st16(tl + kD + b * 96 + n * kW + h * 16, v);
+        tmem_st16(tb + n * kMs + h * 16, v);
       }
       tmem_wait_st();
       tc_before();
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
           const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
           const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
           const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
-          if (okr) {
+          if (okr && !(p.exp & 16)) {  // exp 16: no write-back (timing only)
             float* gp = dst + (size_t)g * kW + h * 16 + ch * 4;
             if constexpr (kAtomic)
               red_add_v4(gp, v);

@@ -1,3 +1,4 @@
 #!/bin/bash
-# Timing experiments of the WS sweeps (FTKCU_WS_EXP bits; never production).
-for e in 0 1 2 4 8 12 14; do FTKCU_WS_EXP=$e bash scripts/bench_brief.sh "$@" | sed "s/^/exp=$e /"; done
+# Timing experiments of the WS sweeps (FTKCU_WS_EXP bits; never production):
+# 2 = no gathers, 16 = no factor write-back.
+for e in ${EXPS:-0 2 16 18}; do FTKCU_WS_EXP=$e bash scripts/bench_brief.sh "$@" | sed "s/^/exp=$e /"; done
