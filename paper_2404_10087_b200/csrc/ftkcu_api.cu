@@ -411,13 +411,23 @@ int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order, const int32_t* di
   for (int n = 0; n < order; ++n)
     if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
   DevTensor& t = s->slots[slot];
-  free_tensor(t);
-  t.order = order;
-  t.nnz = nnz;
-  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
   const size_t cnt = nnz > 0 ? (size_t)nnz : 1;
-  for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * cnt));
-  CK(cudaMalloc(&t.vals, sizeof(float) * cnt));
+  if (t.vals && t.order == order && t.nnz == nnz) {
+    // same extent (e.g. a new epoch's data): keep every device buffer,
+    // including the tiled stream, which is rebuilt lazily
+    CK(cudaStreamSynchronize(s->stream));
+    t.cell_off.clear();
+    t.cell_tile.clear();
+    t.shuffled = false;
+    t.stream_tiles = 0;
+  } else {
+    free_tensor(t);
+    t.order = order;
+    t.nnz = nnz;
+    for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * cnt));
+    CK(cudaMalloc(&t.vals, sizeof(float) * cnt));
+  }
+  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
   if (nnz > 0) {
     int rc2 = ensure_scratch(s, sizeof(int32_t) * (size_t)nnz * order + 256);
     if (rc2) return rc2;

@@ -39,7 +39,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum",
         "lts__t_sectors_srcunit_tex_op_red.sum", "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 traffic = {}
-for kern in ("ws_factor", "ws_core"):
+for kern in ("ws_factor", "ws_core16"):
     raw = subprocess.run(["ncu", "-i", os.path.join(go, f"{tag}_{kern}.ncu-rep"), "--page", "raw", "--csv"],
                          capture_output=True, text=True).stdout
     r = list(csv.reader(raw.splitlines()))
@@ -59,7 +59,7 @@ for kern in ("ws_factor", "ws_core"):
         x = float(val.replace(",", ""))
         return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
     b = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
-    traffic[f"netflix_j32_tf32_{kern.split('_')[1]}"] = b
+    traffic[f"netflix_j32_tf32_{'core' if 'core' in kern else 'factor'}"] = b
 json.dump(traffic, open(os.path.join(pr, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(pr, f"{tag}_launches.txt")).read())
 print(json.dumps(traffic))
