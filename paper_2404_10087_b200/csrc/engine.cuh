@@ -173,6 +173,14 @@ cudaError_t launch_tc_core(const KView& v, int64_t tile_mul, int64_t tile_add,
 
 // ---- warp-specialized tensor-core sweeps, N = 3, J = R = 32 (tc_ws_kernels.cu)
 bool ws_supported(const KView& v);
+// J = R = 16 at order 3..6 (tc_wsg_kernels.cu): warp-specialised factor
+// (tf32, Hogwild accumulate) and core (fp16 copy of A) sweeps.
+bool wsg_supported(const KView& v);
+size_t wsg_core_scratch_bytes(const KView& v, const int32_t* dims);
+cudaError_t launch_wsg_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                              float lr, float reg, cudaStream_t st);
+cudaError_t launch_wsg_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                            float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st);
 // Core sweep scratch: per-CTA gradients + the RN-rounded tf32 copy of A.
 size_t ws_core_scratch_bytes(const KView& v, const int32_t* dims);
 cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,

@@ -540,6 +540,9 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
   if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
+  } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
+             wsg_supported(v)) {
+    CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));
   } else if (s->opt_precision == FTKCU_PREC_TF32 && big_supported(v)) {
     // large ranks: B operand images in the session scratch (allocated
     // before any graph capture, see ftkcu_dsgd_factor_epoch)
@@ -671,6 +674,8 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
       need = big_scratch_bytes(v, s->model.dims, true);
     if (ws_supported(v) && ws_core_scratch_bytes(v, s->model.dims) > need)
       need = ws_core_scratch_bytes(v, s->model.dims);
+    if (wsg_supported(v) && wsg_core_scratch_bytes(v, s->model.dims) > need)
+      need = wsg_core_scratch_bytes(v, s->model.dims);
     if ((rc = ensure_scratch(s, need))) return rc;
     if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -680,6 +685,10 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
       CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
                         (int)s->opt_core16, static_cast<float*>(s->scratch), s->scratch_bytes,
                         s->stream));
+    } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && s->opt_tc_ws &&
+               s->opt_core16 && wsg_supported(v)) {
+      CK(launch_wsg_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
+                         s->scratch_bytes, s->stream));
     } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && big_supported(v)) {
       CK(launch_big_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
                          s->scratch_bytes, s->stream));
