@@ -99,6 +99,14 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value);
 int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order,
                         const int32_t* dims, int64_t nnz,
                         const int32_t* idx_rowmajor, const float* values);
+/* Same as ftkcu_tensor_upload, asynchronous: the host-to-device copy and
+ * the layout transpose run on the session's copy stream and overlap work
+ * already enqueued on other slots.  `idx_rowmajor` / `values` (pinned host
+ * memory for a true overlap) must stay valid until the slot's next use,
+ * which waits for the copy and reports an out-of-range index then.  No
+ * reference counterpart (engine addition for pipelined epochs). */
+int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                              int64_t nnz, const int32_t* idx_rowmajor, const float* values);
 int ftkcu_tensor_release(ftkcu_session* s, int slot);
 int64_t ftkcu_tensor_nnz(ftkcu_session* s, int slot);
 

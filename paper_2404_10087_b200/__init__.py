@@ -34,6 +34,7 @@ EVAL_EXACT, EVAL_FAST = 0, 1
 EXPORTS = (
     "ftkcu_abi_version", "ftkcu_session_create", "ftkcu_session_destroy",
     "ftkcu_last_error", "ftkcu_set_option", "ftkcu_get_option", "ftkcu_tensor_upload",
+    "ftkcu_tensor_upload_async",
     "ftkcu_tensor_release", "ftkcu_tensor_nnz", "ftkcu_model_upload",
     "ftkcu_model_download", "ftkcu_factor_phase", "ftkcu_core_phase", "ftkcu_eval",
     "ftkcu_batch_probe", "ftkcu_comm_unique_id", "ftkcu_comm_init",
@@ -73,6 +74,8 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_get_option.argtypes = [C.c_void_p, C.c_char_p, _i64p]
     L.ftkcu_tensor_upload.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, C.c_int64, _i32p,
                                       _f32p]
+    L.ftkcu_tensor_upload_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, C.c_int64,
+                                            _i32p, _f32p]
     L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.restype = C.c_int64
@@ -181,6 +184,14 @@ class Session:
         dims = np.ascontiguousarray(dims, np.int32)
         self._ck(self.lib.ftkcu_tensor_upload(self.h, slot, dims.shape[0], _p(dims, _i32p), nnz,
                                               C.cast(idx_ptr, _i32p), C.cast(vals_ptr, _f32p)))
+
+    def upload_tensor_ptr_async(self, slot, dims, nnz, idx_ptr: int, vals_ptr: int):
+        """Asynchronous upload from pinned host pointers (copy stream); the
+        slot's next use waits for it.  The host buffers must stay alive."""
+        dims = np.ascontiguousarray(dims, np.int32)
+        self._ck(self.lib.ftkcu_tensor_upload_async(self.h, slot, dims.shape[0],
+                                                    _p(dims, _i32p), nnz, C.cast(idx_ptr, _i32p),
+                                                    C.cast(vals_ptr, _f32p)))
 
     def release_tensor(self, slot):
         self._ck(self.lib.ftkcu_tensor_release(self.h, slot))

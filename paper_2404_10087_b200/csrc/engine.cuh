@@ -44,6 +44,13 @@ struct DevTensor {
   std::vector<int64_t> cell_tile;
   int64_t stream_tiles = 0;
   int64_t stream_cap = 0;            // allocated tiles
+  // Asynchronous upload (ftkcu_tensor_upload_async): AoS staging on the
+  // copy stream, completion event, index-range flag checked at first use.
+  int32_t* staging = nullptr;
+  size_t staging_cap = 0;
+  int* d_bad = nullptr;
+  cudaEvent_t ready = nullptr;
+  bool pending = false;
 };
 
 struct DevModel {

@@ -16,6 +16,7 @@ using namespace ftkcu;
 struct ftkcu_session {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // asynchronous tensor uploads
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
   DevTensor slots[8];
@@ -127,6 +128,9 @@ void free_tensor(DevTensor& t) {
   if (t.vals) cudaFree(t.vals);
   if (t.svals) cudaFree(t.svals);
   if (t.tile_rows) cudaFree(t.tile_rows);
+  if (t.staging) cudaFree(t.staging);
+  if (t.d_bad) cudaFree(t.d_bad);
+  if (t.ready) cudaEventDestroy(t.ready);
   t = DevTensor{};
 }
 
@@ -191,8 +195,25 @@ KView make_view(const ftkcu_session* s, const DevTensor& t, bool shuffled) {
   return v;
 }
 
+// Completes an asynchronous upload before the slot's first use: the session
+// stream waits for it, and the deferred index-range check runs.
+int finish_upload(ftkcu_session* s, DevTensor& t) {
+  if (!t.pending) return FTKCU_OK;
+  t.pending = false;
+  CK(cudaStreamWaitEvent(s->stream, t.ready, 0));
+  CK(cudaEventSynchronize(t.ready));
+  int h_bad = 0;
+  CK(cudaMemcpy(&h_bad, t.d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h_bad) {
+    free_tensor(t);
+    return fail(s, FTKCU_ERR_ARG, "index out of range in tensor upload");
+  }
+  return FTKCU_OK;
+}
+
 int check_ready(ftkcu_session* s, int slot) {
   if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (int rc = finish_upload(s, s->slots[slot])) return rc;
   if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
   const DevTensor& t = s->slots[slot];
   if (!t.vals && t.nnz == 0 && t.order == 0)
@@ -306,6 +327,7 @@ int ftkcu_session_create(int device, ftkcu_session** out) {
                 device, major);
   }
   if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
     delete s;
     return fail(nullptr, FTKCU_ERR_CUDA, "stream/event creation failed");
@@ -318,6 +340,7 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   if (!s) return;
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
+  cudaStreamSynchronize(s->copy_stream);
   for (auto& t : s->slots) free_tensor(t);
   free_model(s->model);
   if (s->grad) cudaFree(s->grad);
@@ -329,6 +352,7 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   cudaEventDestroy(s->ev0);
   cudaEventDestroy(s->ev1);
   cudaStreamDestroy(s->stream);
+  cudaStreamDestroy(s->copy_stream);
   delete s;
 }
 
@@ -411,6 +435,7 @@ int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order, const int32_t* di
   for (int n = 0; n < order; ++n)
     if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
   DevTensor& t = s->slots[slot];
+  if ((rc = finish_upload(s, t))) return rc;
   const size_t cnt = nnz > 0 ? (size_t)nnz : 1;
   if (t.vals && t.order == order && t.nnz == nnz) {
     // same extent (e.g. a new epoch's data): keep every device buffer,
@@ -458,10 +483,67 @@ int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order, const int32_t* di
   return FTKCU_OK;
 }
 
+int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                              int64_t nnz, const int32_t* idx_rowmajor, const float* values) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (order < 1 || order > kMaxOrder)
+    return fail(s, FTKCU_ERR_ARG, "order %d unsupported (1..%d)", order, kMaxOrder);
+  if (nnz < 1 || !idx_rowmajor || !values)
+    return fail(s, FTKCU_ERR_ARG, "asynchronous upload needs a non-empty tensor");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
+  DevTensor& t = s->slots[slot];
+  if ((rc = finish_upload(s, t))) return rc;
+  // the copies overwrite the slot's buffers: order them after every kernel
+  // already enqueued on the session stream
+  CK(cudaEventRecord(s->ev1, s->stream));
+  CK(cudaStreamWaitEvent(s->copy_stream, s->ev1, 0));
+  if (!(t.vals && t.order == order && t.nnz == nnz)) {
+    CK(cudaStreamSynchronize(s->stream));
+    free_tensor(t);
+    t.order = order;
+    t.nnz = nnz;
+    for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * (size_t)nnz));
+    CK(cudaMalloc(&t.vals, sizeof(float) * (size_t)nnz));
+  }
+  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
+  t.cell_off.clear();
+  t.cell_tile.clear();
+  t.shuffled = false;
+  t.stream_tiles = 0;
+  const size_t aos = sizeof(int32_t) * (size_t)nnz * order;
+  if (t.staging_cap < aos) {
+    if (t.staging) CK(cudaFree(t.staging));
+    t.staging = nullptr;
+    CK(cudaMalloc(&t.staging, aos));
+    t.staging_cap = aos;
+  }
+  if (!t.d_bad) CK(cudaMalloc(&t.d_bad, sizeof(int)));
+  if (!t.ready) CK(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+  CK(cudaMemcpyAsync(t.staging, idx_rowmajor, aos, cudaMemcpyHostToDevice, s->copy_stream));
+  CK(cudaMemcpyAsync(t.vals, values, sizeof(float) * nnz, cudaMemcpyHostToDevice, s->copy_stream));
+  CK(cudaMemsetAsync(t.d_bad, 0, sizeof(int), s->copy_stream));
+  SoAView v{};
+  v.order = order;
+  for (int n = 0; n < order; ++n) {
+    v.dims[n] = dims[n];
+    v.col[n] = t.idx[n];
+  }
+  aos_to_soa_kernel<<<num_sms() * 8, 256, 0, s->copy_stream>>>(t.staging, nnz, v, t.d_bad);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(t.ready, s->copy_stream));
+  t.pending = true;
+  return FTKCU_OK;
+}
+
 int ftkcu_tensor_release(ftkcu_session* s, int slot) {
   int rc = bind(s);
   if (rc) return rc;
   if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  CK(cudaStreamSynchronize(s->copy_stream));
+  s->slots[slot].pending = false;
   CK(cudaStreamSynchronize(s->stream));
   free_tensor(s->slots[slot]);
   return FTKCU_OK;
@@ -620,6 +702,7 @@ int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offse
   if (rc) return rc;
   if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
   DevTensor& t = s->slots[slot];
+  if ((rc = finish_upload(s, t))) return rc;
   if (ncells < 1 || !cell_offsets) return fail(s, FTKCU_ERR_ARG, "need at least one cell");
   if (cell_offsets[0] != 0 || cell_offsets[ncells] != t.nnz)
     return fail(s, FTKCU_ERR_ARG, "cell offsets must span [0, nnz]");

@@ -1,0 +1,58 @@
+"""Asynchronous tensor upload (ftkcu_tensor_upload_async): the copy stream's
+transpose must give the same device tensor as the synchronous upload (so a
+deterministic epoch is bit-identical), the slot's first use waits for the
+copy, and an out-of-range index is reported at that first use."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2404_10087_b200 as eng
+from paper_2404_10087_b200 import host
+
+pytestmark = pytest.mark.gpu
+DET = eng.MODE_DETERMINISTIC
+
+
+def _problem():
+    t = O.random_tensor([50, 40, 30], 5000, 11, 1.0, 5.0)
+    ranks, r = [8, 8, 8], 8
+    scale = host.default_init_scale(float(np.mean(np.abs(t.vals))), 3, r, ranks)
+    a, b = host.init_model(t.dims, ranks, r, 5, scale)
+    return t, ranks, r, a, b
+
+
+def _pinned(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+
+
+def test_async_upload_epoch_bit_identical(session):
+    t, ranks, r, a, b = _problem()
+    plan1 = host.global_plan(t.nnz, 16, 3)
+    plan2 = host.global_plan(t.nnz, 16, 4)
+    out = []
+    for asynchronous in (False, True):
+        session.upload_model(t.dims, ranks, r, a, b)
+        if asynchronous:
+            ih, vh = _pinned(t.idx), _pinned(t.vals)
+            session.upload_tensor_ptr_async(2, t.dims, t.nnz, ih.data_ptr(), vh.data_ptr())
+        else:
+            session.upload_tensor(2, t.dims, t.idx, t.vals)
+        session.factor_phase(2, plan1, 16, 1e-3, 1e-4, DET)
+        session.core_phase(2, plan2, 16, 1e-3, 1e-4, DET)
+        out.append(session.download_model())
+        session.release_tensor(2)
+    for n in range(3):
+        assert np.array_equal(out[0][0][n], out[1][0][n])
+        assert np.array_equal(out[0][1][n], out[1][1][n])
+
+
+def test_async_upload_bad_index_reported_at_first_use(session):
+    t, ranks, r, a, b = _problem()
+    idx = t.idx.copy()
+    idx[17, 1] = 40  # == dims[1]: out of range
+    session.upload_model(t.dims, ranks, r, a, b)
+    ih, vh = _pinned(idx), _pinned(t.vals)
+    session.upload_tensor_ptr_async(3, t.dims, t.nnz, ih.data_ptr(), vh.data_ptr())
+    with pytest.raises(eng.FtkError, match="out of range"):
+        session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
