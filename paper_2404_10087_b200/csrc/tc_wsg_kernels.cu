@@ -20,6 +20,12 @@
 // accumulate); G stacks the N modes' 16-row blocks in M (N <= 8) and is
 // accumulated in TMEM over the CTA's tiles.
 //
+// J = R = 8 (C5 rank 8) runs padded to 16: the row-gather maps have 8
+// columns and a 16-column box, so TMA zero-fills columns 8..15 of every
+// gathered row (out of bounds); the padding rows / columns of the B operands
+// are zero, so every padded C, D', U and G entry is exactly zero, and only
+// the 8 real columns are written back.
+//
 // Reference: decomposition.cpp:644-658 / :678-698 (per-batch pipeline),
 // PAPER.md Alg. 4 / Alg. 5.
 #include <cuda_fp16.h>
@@ -51,6 +57,7 @@ struct __align__(64) WsgParams {
   const int64_t* tperm;
   float lr, reg;
   float* partials;
+  int jr;  // real J = R (16, or 8 padded to 16)
 };
 
 __device__ __forceinline__ int64_t wsg_tile(const WsgParams& p, int64_t k) {
@@ -142,7 +149,7 @@ __device__ void wsg_setup(const WsgParams& p, uint8_t* sm, uint64_t* bars, uint3
     const float* b = p.b[n];
     for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
       const int j = e / kW, r = e - j * kW;
-      const float x = b[e];
+      const float x = (j < p.jr && r < p.jr) ? b[j * p.jr + r] : 0.0f;
       if constexpr (kCore) {
         *reinterpret_cast<__half*>(sm + L::o_bt + n * L::bt_mode + swz32b(r, j * 2)) =
             __float2half_rn(x);
@@ -150,7 +157,7 @@ __device__ void wsg_setup(const WsgParams& p, uint8_t* sm, uint64_t* bars, uint3
         const float hi = __uint_as_float(rn_bits(x));
         *reinterpret_cast<float*>(sm + L::o_bt + n * L::bt_mode + swz(r, j * 4, 64)) = hi;
         *reinterpret_cast<float*>(sm + L::o_bt + n * L::bt_mode + swz(kW + r, j * 4, 64)) =
-            r == j ? 1.0f : 0.0f;
+            (r == j && j < p.jr) ? 1.0f : 0.0f;
         *reinterpret_cast<float*>(sm + L::o_b + n * kW * 64 + swz(j, r * 4, 64)) = hi;
       }
     }
@@ -159,7 +166,7 @@ __device__ void wsg_setup(const WsgParams& p, uint8_t* sm, uint64_t* bars, uint3
     for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
       const int j = e / kW, jj = e - j * kW;
       *reinterpret_cast<float*>(sm + L::o_diag + swz(j, jj * 4, 64)) =
-          j == jj ? __uint_as_float(rn_bits(-p.lr * p.reg)) : 0.0f;
+          (j == jj && j < p.jr) ? __uint_as_float(rn_bits(-p.lr * p.reg)) : 0.0f;
     }
   if constexpr (kCore)  // the G GEMM's garbage M blocks read zeros
     for (uint32_t o = threadIdx.x * 16; o < L::d_bytes; o += blockDim.x * 16)
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
           const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
           const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
           const float4 v = *reinterpret_cast<const float4*>(stage + swz32b(rl, ch * 16));
-          if (okr) red_add_v4(dst + (size_t)g * kW + h * 8 + ch * 4, v);
+          if (okr && h * 8 < p.jr) red_add_v4(dst + (size_t)g * p.jr + h * 8 + ch * 4, v);
         }
         __syncwarp();
       }
@@ -538,8 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_core_kernel(const __grid_cons
       uint32_t v2[8];
       tmem_ld8(tl + L::t_g + (q * 2 + 1) * kW + h * 8, v2);  // ... and mode q*2+1
       tmem_wait_ld();
-      if (n < N) {
-        float* out = p.partials + (size_t)blockIdx.x * (N * kW * kW) + ((size_t)n * kW + j) * kW + h * 8;
+      const int jr = p.jr;
+      if (n < N && j < jr && h * 8 < jr) {
+        float* out = p.partials + (size_t)blockIdx.x * (N * jr * jr) + ((size_t)n * jr + j) * jr + h * 8;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           out[i] = nk > 0 ? __uint_as_float((lane >> 4) ? v2[i] : v[i]) : 0.0f;
@@ -576,13 +584,14 @@ PFN_cuTensorMapEncodeTiled_v12000 wsg_encode_fn() {
   return fn;
 }
 
-// Row-gather map: rows x 16 elements (fp32: 64-B rows, SWIZZLE_64B; fp16:
-// 32-B rows, SWIZZLE_32B), box of one row.
-bool wsg_row_map(CUtensorMap* tm, const void* a, int64_t rows, bool half) {
+// Row-gather map: rows x jr elements, box of one row of 16 (fp32: 64-B rows,
+// SWIZZLE_64B; fp16: 32-B rows, SWIZZLE_32B); at jr = 8 the box's upper
+// half is out of bounds and arrives zero-filled.
+bool wsg_row_map(CUtensorMap* tm, const void* a, int64_t rows, bool half, int jr) {
   auto fn = wsg_encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)kW, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kW * (half ? 2 : 4)};
+  cuuint64_t dims[2] = {(cuuint64_t)jr, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)jr * (half ? 2 : 4)};
   cuuint32_t box[2] = {(cuuint32_t)kW, 1};
   cuuint32_t es[2] = {1, 1};
   return fn(tm, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -605,6 +614,7 @@ WsgParams base_params(const KView& v, int64_t mul, int64_t add) {
   p.tperm = v.tperm;
   p.tmul = mul;
   p.tadd = add;
+  p.jr = v.r;
   return p;
 }
 
@@ -613,7 +623,7 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
                        float reg, cudaStream_t st) {
   WsgParams p = base_params(v, mul, add);
   for (int n = 0; n < N; ++n)
-    if (!wsg_row_map(&p.tmap[n], v.a[n], dims[n], false)) return cudaErrorNotSupported;
+    if (!wsg_row_map(&p.tmap[n], v.a[n], dims[n], false, p.jr)) return cudaErrorNotSupported;
   p.lr = lr;
   p.reg = reg;
   const int bytes = (int)WsgLayout<N, false>::bytes;
@@ -628,21 +638,21 @@ template <int N>
 cudaError_t run_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float* grad,
                      float* scratch, size_t scratch_bytes, cudaStream_t st) {
   const int grid = (int)(v.ntiles < num_sms() ? v.ntiles : num_sms());
-  const int len = N * kW * kW;
+  const int len = N * v.r * v.r;
   if (grid < 1) return cudaErrorInvalidValue;
   if (scratch_bytes < wsg_core_scratch_bytes(v, dims)) return cudaErrorInvalidValue;
   WsgParams p = base_params(v, mul, add);
   p.partials = scratch;
-  __half* a16 = reinterpret_cast<__half*>(scratch + (size_t)num_sms() * len);
+  __half* a16 = reinterpret_cast<__half*>(scratch + (size_t)num_sms() * N * kW * kW);
   for (int n = 0; n < N; ++n) {
-    const int64_t cnt2 = (int64_t)dims[n] * kW / 2;
+    const int64_t cnt2 = (int64_t)dims[n] * p.jr / 2;
     int64_t blocks = (cnt2 + 255) / 256;
     if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
     wsg_half_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, st>>>(v.a[n], a16, cnt2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (!wsg_row_map(&p.tmap[n], a16, dims[n], true)) return cudaErrorNotSupported;
-    a16 += (int64_t)dims[n] * kW;
+    if (!wsg_row_map(&p.tmap[n], a16, dims[n], true, p.jr)) return cudaErrorNotSupported;
+    a16 += ((int64_t)dims[n] * p.jr + 7) / 8 * 8;  // keep every copy 16-B aligned
   }
   const int bytes = (int)WsgLayout<N, true>::bytes;
   cudaError_t e = cudaFuncSetAttribute(wsg_core_kernel<N>,
@@ -658,16 +668,16 @@ cudaError_t run_core(const KView& v, const int32_t* dims, int64_t mul, int64_t a
 }  // namespace
 
 bool wsg_supported(const KView& v) {
-  if (v.order < 3 || v.order > kMaxN || v.r != kW) return false;
+  if (v.order < 3 || v.order > kMaxN || (v.r != 16 && v.r != 8)) return false;
   for (int n = 0; n < v.order; ++n)
-    if (v.j[n] != kW) return false;
+    if (v.j[n] != v.r) return false;
   return wsg_encode_fn() != nullptr;
 }
 
 size_t wsg_core_scratch_bytes(const KView& v, const int32_t* dims) {
   size_t f = (size_t)num_sms() * v.order * kW * kW;  // per-CTA gradients
   size_t h = 0;
-  for (int n = 0; n < v.order; ++n) h += (size_t)dims[n] * kW;  // fp16 copy of A
+  for (int n = 0; n < v.order; ++n) h += ((size_t)dims[n] * kW + 7) / 8 * 8;  // fp16 copy of A
   return (f + (h + 1) / 2 + 64) * sizeof(float);
 }
 
