@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32", "3xtf32"])
     ap.add_argument("--hog-update", type=int, default=1, help="1: atomic RED rows, 0: overwrite")
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
+    ap.add_argument("--factor-warps", type=int, default=8, choices=[8, 16],
+                    help="epilogue warps of the N=3 J=R=32 factor sweep")
     ap.add_argument("--core16", type=int, default=1,
                     help="tf32 core sweep on an fp16 copy of A (kind::f16, 10-bit mantissa)")
     ap.add_argument("--store-c", type=int, default=0,
@@ -358,6 +360,7 @@ def run_engine(args):
     s.set_option("tc_ws", args.tc_ws)
     s.set_option("store_c", args.store_c)
     s.set_option("core16", args.core16)
+    s.set_option("factor_warps", args.factor_warps)
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
     s.upload_model(coo.dims, ranks, j, a0, b0)

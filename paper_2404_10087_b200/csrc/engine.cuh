@@ -183,6 +183,7 @@ bool ws_supported(const KView& v);
 // J = R = 16 at order 3..6 (tc_wsg_kernels.cu): warp-specialised factor
 // (tf32, Hogwild accumulate) and core (fp16 copy of A) sweeps.
 bool wsg_supported(const KView& v);
+bool wsf32_supported(const KView& v);  // N = 3, J = R = 32 on 16 epilogue warps
 size_t wsg_core_scratch_bytes(const KView& v, const int32_t* dims);
 cudaError_t launch_wsg_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                               float lr, float reg, cudaStream_t st);

@@ -35,6 +35,7 @@ struct ftkcu_session {
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
   int64_t opt_core16 = 1;   // WS core sweep (tf32 precision): gather an fp16 copy of A
+  int64_t opt_factor_warps = 8;  // N=3 J=R=32 factor sweep: 8 or 16 epilogue warps
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -376,6 +377,9 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->opt_store_c = value != 0;
   } else if (k == "core16") {
     s->opt_core16 = value != 0;
+  } else if (k == "factor_warps") {
+    if (value != 8 && value != 16) return fail(s, FTKCU_ERR_ARG, "factor_warps must be 8 or 16");
+    s->opt_factor_warps = value;
   } else if (k == "hog_update") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "bad hog_update");
     s->opt_hog_update = value;
@@ -411,6 +415,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "tc_ws") *value = s->opt_tc_ws;
   else if (k == "store_c") *value = s->opt_store_c;
   else if (k == "core16") *value = s->opt_core16;
+  else if (k == "factor_warps") *value = s->opt_factor_warps;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
   else if (k == "staleness") *value = s->opt_staleness;
@@ -619,7 +624,10 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
                          float lr_a, float reg_a) {
   if (v.ntiles <= 0) return FTKCU_OK;
   // the WS factor sweep is single-pass tf32; 3xtf32 runs on the tc sweep
-  if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
+  if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
+      s->opt_factor_warps == 16 && wsf32_supported(v)) {
+    CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));
+  } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&

@@ -284,29 +284,163 @@ __device__ __forceinline__ float prods(const float (&c)[N][8], float (&d)[N][8])
 }
 
 // ---- factor sweep ---------------------------------------------------------------
+//
+// Templated over the column count W (16, or 32 for the headline shape): the
+// epilogue has W / 8 warps per TMEM lane quarter, each owning 8 columns, so
+// W = 32 runs 16 epilogue warps (4 per scheduler) -- the latency hiding the
+// 8-warp tc_ws_kernels.cu factor sweep lacks.
 
-template <int N>
-__global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_constant__ WsgParams p) {
-  using L = WsgLayout<N, false>;
+template <int W>
+struct FW {
+  static constexpr int E = 4 * (W / 8);         // epilogue warps
+  static constexpr int GWarp = 2 + E;           // first gather warp
+  static constexpr int Threads = (2 + E + kGW) * 32;
+  static constexpr uint32_t RowB = W * 4;       // fp32 row bytes (64 | 128)
+  static constexpr uint32_t Sbo = 8 * RowB;     // 8-row group stride
+  static constexpr uint64_t Lay = W == 16 ? 4 : 2;  // SWIZZLE_64B | SWIZZLE_128B
+};
+
+template <int N, int W>
+struct WsfLayout {
+  using F = FW<W>;
+  static constexpr uint32_t kModeTile = kRows * F::RowB;
+  static constexpr uint32_t kSlot = N * kModeTile;
+  static constexpr int kS = W == 32 ? 3 : (N <= 4 ? 4 : 3);
+  static constexpr uint32_t o_a = 0;
+  static constexpr uint32_t o_bt = o_a + kS * kSlot;  // [B^T ; I] per mode: 2W rows
+  static constexpr uint32_t bt_mode = 2 * W * F::RowB;
+  static constexpr uint32_t o_b = o_bt + N * bt_mode;  // B (rows j, K = r): W rows
+  static constexpr uint32_t o_diag = o_b + N * W * F::RowB;
+  static constexpr uint32_t o_idx = o_diag + W * F::RowB;
+  static constexpr uint32_t kIdxSlot = (N + 1) * kRows * 4;
+  static constexpr int kI = 6;
+  static constexpr uint32_t o_stage = o_idx + kI * kIdxSlot;  // per-warp 32 rows x 32 B
+  static constexpr uint32_t o_xp = o_stage + F::E * 1024;     // [2][W/8][128] x_hat parts
+  static constexpr uint32_t o_rows = o_xp + 2 * (W / 8) * kRows * 4;
+  static constexpr uint32_t o_bar = o_rows + 64;
+  static constexpr uint32_t o_tmem = o_bar + 32 * 8;
+  static constexpr uint32_t bytes = (o_tmem + 16 + 1023) / 1024 * 1024;
+  static constexpr uint32_t t_u = 2 * N * 2 * W;  // buffers [C|A] x 2, then U
+  static constexpr uint32_t tcols_used = t_u + N * W;
+  static constexpr uint32_t tcols = tcols_used <= 256 ? 256 : 512;
+  static_assert(bytes <= 227 * 1024, "shared-memory budget");
+  static_assert(tcols_used <= 512, "TMEM budget");
+};
+
+template <int N, int W>
+__device__ void wsf_setup(const WsgParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tslot) {
+  using L = WsfLayout<N, W>;
+  using F = FW<W>;
+  for (int n = 0; n < N; ++n) {
+    const float* b = p.b[n];
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+      const int j = e / W, r = e - j * W;
+      const float x = (j < p.jr && r < p.jr) ? b[j * p.jr + r] : 0.0f;
+      const float hi = __uint_as_float(rn_bits(x));
+      *reinterpret_cast<float*>(sm + L::o_bt + n * L::bt_mode + swz(r, j * 4, F::RowB)) = hi;
+      *reinterpret_cast<float*>(sm + L::o_bt + n * L::bt_mode + swz(W + r, j * 4, F::RowB)) =
+          (r == j && j < p.jr) ? 1.0f : 0.0f;
+      *reinterpret_cast<float*>(sm + L::o_b + n * W * F::RowB + swz(j, r * 4, F::RowB)) = hi;
+    }
+  }
+  for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+    const int j = e / W, jj = e - j * W;
+    *reinterpret_cast<float*>(sm + L::o_diag + swz(j, jj * 4, F::RowB)) =
+        (j == jj && j < p.jr) ? __uint_as_float(rn_bits(-p.lr * p.reg)) : 0.0f;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kS; ++s) {
+      mbar_init(&bars[G_FULL + s], kGW);
+      mbar_init(&bars[G_EMPTY + s], 1);
+    }
+    for (int i = 0; i < L::kI; ++i) {
+      mbar_init(&bars[G_IFULL + i], 1);
+      mbar_init(&bars[G_IEMPTY + i], F::E + kGW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[G_CFULL + b], 1);
+      mbar_init(&bars[G_DFULL + b], F::E);
+    }
+    mbar_init(&bars[G_UFULL], 1);
+    mbar_init(&bars[G_UEMPTY], F::E);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < N; ++n) prefetch_tmap(&p.tmap[n]);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(L::tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+}
+
+template <int N, int W>
+__global__ void __launch_bounds__(FW<W>::Threads, 1)
+    wsf_factor_kernel(const __grid_constant__ WsgParams p) {
+  using L = WsfLayout<N, W>;
+  using F = FW<W>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
-  wsg_setup<N, false>(p, sm, bars, tslot);
+  wsf_setup<N, W>(p, sm, bars, tslot);
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kBuf = N * 2 * kW, kMs = 2 * kW;
+  constexpr uint32_t kBuf = N * 2 * W, kMs = 2 * W;
+  constexpr int kH = W / 8;  // epilogue warps per lane quarter
 
   if (warp == 0) {
-    wsg_idx_producer<N, false>(p, sm, bars, nk);
-  } else if (warp >= kGatherWarp) {
-    wsg_gather<N, false>(p, sm, bars, nk);
+    if (lane == 0)
+      for (int64_t k = 0; k < nk; ++k) {
+        const int i = (int)(k % L::kI);
+        const int64_t tile = wsg_tile(p, k);
+        mbar_wait(&bars[G_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
+        int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+        mbar_expect_tx(&bars[G_IFULL + i], L::kIdxSlot);
+        for (int n = 0; n < N; ++n)
+          bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[G_IFULL + i]);
+        bulk_g2s(s_idx + N * kRows, p.vals + tile * kRows, kRows * 4, &bars[G_IFULL + i]);
+      }
+  } else if (warp >= F::GWarp) {
+    const int gw = warp - F::GWarp;
+    constexpr int kGroups = N * kRows / 4, kPer = kGroups / kGW;
+    static_assert(kPer % 4 == 0, "whole batches of 4 groups per gather warp");
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % L::kS), i = (int)(k % L::kI);
+      mbar_wait(&bars[G_EMPTY + s], (uint32_t)(((k / L::kS) & 1) ^ 1));
+      mbar_wait(&bars[G_IFULL + i], (uint32_t)((k / L::kI) & 1));
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
+      uint8_t* slot = sm + L::o_a + s * L::kSlot;
+      __syncwarp();
+      if (elect_one()) {
+        mbar_expect_tx(&bars[G_FULL + s], kPer * 4 * F::RowB);
+#pragma unroll 1
+        for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 4) {
+          int4 r[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+          const int n = g0 / (kRows / 4), gm = g0 - n * (kRows / 4);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            tma_gather4(slot + n * L::kModeTile + (gm + g) * 4 * F::RowB, &p.tmap[n], 0, r[g].x,
+                        r[g].y, r[g].z, r[g].w, &bars[G_FULL + s]);
+        }
+        mbar_arrive(&bars[G_IEMPTY + i]);
+      }
+      __syncwarp();
+    }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idc = idesc_tf32(128, 2 * kW, 0, 0), idu = idesc_tf32(128, kW, 0, 0);
+      constexpr uint32_t idc = idesc_tf32(128, 2 * W, 0, 0), idu = idesc_tf32(128, W, 0, 0);
       const uint32_t bt = smem_u32(sm + L::o_bt), bb = smem_u32(sm + L::o_b);
       const uint32_t dg = smem_u32(sm + L::o_diag);
+      auto kadr = [](uint32_t base, int ks) { return base + ks * 32; };  // 8 fp32 per K step
       auto issue_u = [&](int64_t j) {
         const int b = (int)(j & 1);
         mbar_wait(&bars[G_DFULL + b], (uint32_t)((j >> 1) & 1));
@@ -316,13 +450,13 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
 #pragma unroll
         for (int n = 0; n < N; ++n) {
 #pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ts(tmem + L::t_u + n * kW, tb + n * kMs + ks * 8,
-                   sdesc_l(bb + n * kW * 64 + ks * 32, 16, 512, 4), idu, ks > 0);
+          for (int ks = 0; ks < W / 8; ++ks)
+            mma_ts(tmem + L::t_u + n * W, tb + n * kMs + ks * 8,
+                   sdesc_l(kadr(bb + n * W * F::RowB, ks), 16, F::Sbo, F::Lay), idu, ks > 0);
 #pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ts(tmem + L::t_u + n * kW, tb + n * kMs + kW + ks * 8,
-                   sdesc_l(dg + ks * 32, 16, 512, 4), idu, 1);
+          for (int ks = 0; ks < W / 8; ++ks)
+            mma_ts(tmem + L::t_u + n * W, tb + n * kMs + W + ks * 8,
+                   sdesc_l(kadr(dg, ks), 16, F::Sbo, F::Lay), idu, 1);
         }
         mma_commit(&bars[G_UFULL]);
       };
@@ -334,9 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
 #pragma unroll
         for (int n = 0; n < N; ++n)
 #pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ss(tmem + b * kBuf + n * kMs, sdesc_l(a0 + n * L::kModeTile + ks * 32, 16, 512, 4),
-                   sdesc_l(bt + n * L::bt_mode + ks * 32, 16, 512, 4), idc, ks > 0);
+          for (int ks = 0; ks < W / 8; ++ks)
+            mma_ss(tmem + b * kBuf + n * kMs,
+                   sdesc_l(kadr(a0 + n * L::kModeTile, ks), 16, F::Sbo, F::Lay),
+                   sdesc_l(kadr(bt + n * L::bt_mode, ks), 16, F::Sbo, F::Lay), idc, ks > 0);
         mma_commit(&bars[G_CFULL + b]);
         mma_commit(&bars[G_EMPTY + s]);
         if (k >= 1) issue_u(k - 1);
@@ -344,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
       if (nk >= 1) issue_u(nk - 1);
     }
   } else {
-    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;  // h: 8-column block
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     float* xp = reinterpret_cast<float*>(sm + L::o_xp);
@@ -372,9 +507,12 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
       tmem_wait_ld();
       float d[N][8];
       const float part = prods<N>(c, d);
-      xp[(b * 2 + h) * kRows + row] = part;
-      named_bar(1 + q, 64);
-      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
+      // x_hat: the kH column blocks of this row are summed through shared memory
+      xp[(b * kH + h) * kRows + row] = part;
+      named_bar(1 + q, 32 * kH);
+      float xhat = 0.0f;
+#pragma unroll
+      for (int hh = 0; hh < kH; ++hh) xhat += xp[(b * kH + hh) * kRows + row];
 #pragma unroll
       for (int n = 0; n < N; ++n) t.g[n] = s_idx[n * kRows + row];
       const float xv = reinterpret_cast<const float*>(s_idx + N * kRows)[row];
@@ -399,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
       tc_after();
       uint32_t u[N][8];
 #pragma unroll
-      for (int n = 0; n < N; ++n) tmem_ld8(tl + L::t_u + n * kW + h * 8, u[n]);
+      for (int n = 0; n < N; ++n) tmem_ld8(tl + L::t_u + n * W + h * 8, u[n]);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
@@ -433,7 +571,11 @@ __global__ void __launch_bounds__(kThreads, 1) wsg_factor_kernel(const __grid_co
       cur = nxt;
     }
   }
-  wsg_teardown<N, false>(tmem);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::tcols));
 }
 
 // ---- core sweep (fp16 copy of A) ------------------------------------------------
@@ -584,19 +726,21 @@ PFN_cuTensorMapEncodeTiled_v12000 wsg_encode_fn() {
   return fn;
 }
 
-// Row-gather map: rows x jr elements, box of one row of 16 (fp32: 64-B rows,
-// SWIZZLE_64B; fp16: 32-B rows, SWIZZLE_32B); at jr = 8 the box's upper
-// half is out of bounds and arrives zero-filled.
-bool wsg_row_map(CUtensorMap* tm, const void* a, int64_t rows, bool half, int jr) {
+// Row-gather map: rows x jr elements, box of one row of `box` elements
+// (fp32 16: 64-B rows, SWIZZLE_64B; fp32 32: 128-B rows, SWIZZLE_128B; fp16
+// 16: 32-B rows, SWIZZLE_32B); at jr = 8 the box's upper half is out of
+// bounds and arrives zero-filled.
+bool wsg_row_map(CUtensorMap* tm, const void* a, int64_t rows, bool half, int jr, int box_cols = kW) {
   auto fn = wsg_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)jr, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)jr * (half ? 2 : 4)};
-  cuuint32_t box[2] = {(cuuint32_t)kW, 1};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 1};
   cuuint32_t es[2] = {1, 1};
   return fn(tm, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
             const_cast<void*>(a), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            half ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+            half ? CU_TENSOR_MAP_SWIZZLE_32B
+                 : (box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -618,19 +762,19 @@ WsgParams base_params(const KView& v, int64_t mul, int64_t add) {
   return p;
 }
 
-template <int N>
+template <int N, int W>
 cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float lr,
                        float reg, cudaStream_t st) {
   WsgParams p = base_params(v, mul, add);
   for (int n = 0; n < N; ++n)
-    if (!wsg_row_map(&p.tmap[n], v.a[n], dims[n], false, p.jr)) return cudaErrorNotSupported;
+    if (!wsg_row_map(&p.tmap[n], v.a[n], dims[n], false, p.jr, W)) return cudaErrorNotSupported;
   p.lr = lr;
   p.reg = reg;
-  const int bytes = (int)WsgLayout<N, false>::bytes;
-  cudaError_t e = cudaFuncSetAttribute(wsg_factor_kernel<N>,
+  const int bytes = (int)WsfLayout<N, W>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(wsf_factor_kernel<N, W>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  wsg_factor_kernel<N><<<(int)sweep_grid(v), kThreads, bytes, st>>>(p);
+  wsf_factor_kernel<N, W><<<(int)sweep_grid(v), FW<W>::Threads, bytes, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -667,6 +811,12 @@ cudaError_t run_core(const KView& v, const int32_t* dims, int64_t mul, int64_t a
 
 }  // namespace
 
+// N = 3, J = R = 32 on the 16-epilogue-warp factor sweep (wsf_factor_kernel)
+bool wsf32_supported(const KView& v) {
+  return v.order == 3 && v.r == 32 && v.j[0] == 32 && v.j[1] == 32 && v.j[2] == 32 &&
+         wsg_encode_fn() != nullptr;
+}
+
 bool wsg_supported(const KView& v) {
   if (v.order < 3 || v.order > kMaxN || (v.r != 16 && v.r != 8)) return false;
   for (int n = 0; n < v.order; ++n)
@@ -684,11 +834,12 @@ size_t wsg_core_scratch_bytes(const KView& v, const int32_t* dims) {
 cudaError_t launch_wsg_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                               float lr, float reg, cudaStream_t st) {
   if (v.ntiles == 0) return cudaSuccess;
+  if (v.r == 32) return run_factor<3, 32>(v, dims, mul, add, lr, reg, st);
   switch (v.order) {
-    case 3: return run_factor<3>(v, dims, mul, add, lr, reg, st);
-    case 4: return run_factor<4>(v, dims, mul, add, lr, reg, st);
-    case 5: return run_factor<5>(v, dims, mul, add, lr, reg, st);
-    case 6: return run_factor<6>(v, dims, mul, add, lr, reg, st);
+    case 3: return run_factor<3, 16>(v, dims, mul, add, lr, reg, st);
+    case 4: return run_factor<4, 16>(v, dims, mul, add, lr, reg, st);
+    case 5: return run_factor<5, 16>(v, dims, mul, add, lr, reg, st);
+    case 6: return run_factor<6, 16>(v, dims, mul, add, lr, reg, st);
   }
   return cudaErrorNotSupported;
 }

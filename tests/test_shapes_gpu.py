@@ -113,3 +113,30 @@ def test_core_gradient_tf32_and_f16_operand_paths(session, core16):
     want = O.COracle.core_phase(t, m.copy(), host.global_plan(t.nnz, 16, 1), 16, 1e-3, 1e-4)
     tol = GRAD_TOL[eng.PREC_TF32]
     np.testing.assert_allclose(g, want, rtol=tol, atol=tol * np.abs(want).max())
+
+
+@pytest.mark.parametrize("warps", [8, 16])
+def test_factor_steps_8_and_16_epilogue_warps(session, warps):
+    """N = 3, J = R = 32 has two factor sweeps: 8 epilogue warps (tc_ws) and
+    16 (tc_wsg, 8 columns per warp).  Distinct rows: every step must match."""
+    n = 1000
+    idx = np.stack([(np.arange(n) * p) % n for p in (1, 7, 13)], 1).astype(np.int32)
+    vals = np.linspace(1, 5, n).astype(np.float32)
+    t = O.Tensor(np.array([n] * 3, np.int32), idx, vals)
+    m = _model(t, 32, 32)
+    session.set_option("precision", eng.PREC_TF32)
+    session.set_option("factor_warps", warps)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.factor_phase(0, None, 16, 1e-2, 1e-3, HOG, seed=3)
+    finally:
+        session.set_option("factor_warps", 8)
+        session.set_option("precision", eng.PREC_FP32)
+    a, _ = session.download_model()
+    mc = m.copy()
+    O.COracle.factor_phase(t, mc, np.arange(n), 16, 1e-2, 1e-3)
+    tol = STEP_TOL[eng.PREC_TF32]
+    for k in range(3):
+        got, want = a[k] - m.a[k], mc.a[k] - m.a[k]
+        np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
