@@ -18,7 +18,10 @@
 // B images by bulk copy), warp 1 MMA issuer, warps 2-5 epilogue (thread =
 // nonzero = TMEM lane).  Algebra as tc_ws_kernels.cu (decomposition.cpp:
 // 644-658 / :678-698); B operands and D' are rounded to nearest tf32.
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "tc_common.cuh"
@@ -594,6 +597,273 @@ __global__ void big_reduce_kernel(const float* __restrict__ partials, int nparts
   }
 }
 
+// ---- J = R = 64 core sweep in one pass, fp16 copy of A ---------------------------
+//
+// With fp16 rows (128 B at W = 64) one SWIZZLE_128B tile per mode serves the
+// K-major C GEMM and the MN-major G GEMM (16-bit operands take any swizzle in
+// both majors), and TMEM holds C for all modes (192 columns) next to G for
+// all modes (192): G stacks modes {0, 1} in M against [D'_0 | D'_1] (N = 128)
+// and mode 2 (plus 64 ignored rows) against D'_2 (N = 64); only the diagonal
+// blocks are read back.  One gather of 48 KB per tile replaces the three
+// passes x four gathers of the tf32 sweep above.
+//
+//   warp 0  COO columns      warps 10-11  gathers (fp16 rows, half each)
+//   warp 1  MMA issuer       warps 2-9    epilogue, two warps per lane quarter
+
+namespace b16 {
+constexpr int W = 64;
+constexpr int kEpi = 8, kGW = 2, kGWarp = 2 + kEpi;
+constexpr int kThreads = (2 + kEpi + kGW) * 32;
+constexpr uint32_t kModeTile = kRows * 128;  // 128 rows x 64 fp16
+constexpr uint32_t kSlot = kN * kModeTile;   // 48 KB
+constexpr int kS = 3, kI = 3;
+constexpr uint32_t o_a = 0;
+constexpr uint32_t o_d = o_a + kS * kSlot;            // r D tiles (fp16, MN-major)
+constexpr uint32_t o_bt = o_d + kSlot;                // B^T fp16 images, 8 KB per mode
+constexpr uint32_t o_idx = o_bt + kN * W * 128;
+constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
+constexpr uint32_t o_rows = o_idx + kI * kIdxSlot;
+constexpr uint32_t o_xp = o_rows + 64;                // x_hat halves [2][128]
+constexpr uint32_t o_bar = o_xp + 2 * kRows * 4;
+constexpr uint32_t o_tmem = o_bar + 16 * 8;
+constexpr uint32_t bytes = o_tmem + 16;
+static_assert(bytes <= 227 * 1024, "shared-memory budget");
+enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 9, CFULL = 12, CEMPTY = 13, DFULL = 14, DEMPTY = 15 };
+constexpr uint32_t t_c = 0, t_g = 3 * W;  // C: 192 columns; G: [stack01: 128][stack2: 64]
+
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+}  // namespace b16
+
+__global__ void __launch_bounds__(b16::kThreads, 1) big16_core_kernel(const __grid_constant__ BigParams p) {
+  using namespace b16;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + o_tmem);
+  for (int n = 0; n < kN; ++n)
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+      const int j = e / W, r = e - j * W;  // B^T: rows r, K = j
+      *reinterpret_cast<__half*>(sm + o_bt + n * W * 128 + swz(r, j * 2, 128)) =
+          __float2half_rn(p.bt_img[n][e]);
+    }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&bars[FULL + s], kGW);
+      mbar_init(&bars[EMPTY + s], 1);
+    }
+    for (int i = 0; i < kI; ++i) {
+      mbar_init(&bars[IFULL + i], 1);
+      mbar_init(&bars[IEMPTY + i], kEpi + kGW);
+    }
+    mbar_init(&bars[CFULL], 1);
+    mbar_init(&bars[CEMPTY], kEpi);
+    mbar_init(&bars[DFULL], kEpi);
+    mbar_init(&bars[DEMPTY], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    if (lane == 0)
+      for (int64_t k = 0; k < nk; ++k) {
+        const int i = (int)(k % kI);
+        const int64_t tile = big_tile(p, k);
+        mbar_wait(&bars[IEMPTY + i], (uint32_t)(((k / kI) & 1) ^ 1));
+        int32_t* s_idx = reinterpret_cast<int32_t*>(sm + o_idx + i * kIdxSlot);
+        reinterpret_cast<int32_t*>(sm + o_rows)[i] = __ldg(p.tile_rows + tile);
+        mbar_expect_tx(&bars[IFULL + i], kIdxSlot);
+        for (int n = 0; n < kN; ++n)
+          bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[IFULL + i]);
+        bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[IFULL + i]);
+      }
+  } else if (warp >= kGWarp) {
+    const int gw = warp - kGWarp;
+    constexpr int kPer = kN * kRows / 4 / kGW;  // 48 groups of 4 rows
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kS), i = (int)(k % kI);
+      mbar_wait(&bars[EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
+      mbar_wait(&bars[IFULL + i], (uint32_t)((k / kI) & 1));
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + o_idx + i * kIdxSlot);
+      uint8_t* slot = sm + o_a + s * kSlot;
+      __syncwarp();
+      if (elect_one()) {
+        mbar_expect_tx(&bars[FULL + s], kPer * 512);
+#pragma unroll 1
+        for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 8) {
+          int4 r[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+          const int n = g0 / (kRows / 4), gm = g0 - n * (kRows / 4);
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            tma_gather4(slot + n * kModeTile + (gm + g) * 512, &p.tmap[n], 0, r[g].x, r[g].y,
+                        r[g].z, r[g].w, &bars[FULL + s]);
+        }
+        mbar_arrive(&bars[IEMPTY + i]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idc = idesc_f16(128, W, 0, 0);
+      const uint32_t bt = smem_u32(sm + o_bt), d0 = smem_u32(sm + o_d);
+      auto issue_g = [&](int64_t k) {
+        const int s = (int)(k % kS);
+        mbar_wait(&bars[DFULL], (uint32_t)(k & 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + o_a + s * kSlot);
+#pragma unroll
+        for (int ks = 0; ks < kRows / 16; ++ks) {
+          // stack {0, 1}: M = A_0^T ; A_1^T, N = D'_0 | D'_1
+          mma_f16(tmem + t_g, sdesc_l(a0 + ks * 2048, kModeTile, 1024, 2),
+                  sdesc_l(d0 + ks * 2048, kModeTile, 1024, 2), idesc_f16(128, 2 * W, 1, 1),
+                  (k > 0 || ks > 0) ? 1u : 0u);
+          // stack {2, -}: M = A_2^T (+ 64 ignored rows), N = D'_2
+          mma_f16(tmem + t_g + 2 * W, sdesc_l(a0 + 2 * kModeTile + ks * 2048, kModeTile, 1024, 2),
+                  sdesc_l(d0 + 2 * kModeTile + ks * 2048, kModeTile, 1024, 2),
+                  idesc_f16(128, W, 1, 1), (k > 0 || ks > 0) ? 1u : 0u);
+        }
+        mma_commit(&bars[DEMPTY]);
+        mma_commit(&bars[EMPTY + s]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kS);
+        mbar_wait(&bars[FULL + s], (uint32_t)((k / kS) & 1));
+        mbar_wait(&bars[CEMPTY], (uint32_t)((k & 1) ^ 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + o_a + s * kSlot);
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < W / 16; ++ks)
+            mma_f16(tmem + t_c + n * W, sdesc_l(a0 + n * kModeTile + ks * 32, 16, 1024, 2),
+                    sdesc_l(bt + n * W * 128 + ks * 32, 16, 1024, 2), idc, ks > 0);
+        mma_commit(&bars[CFULL]);
+        if (k >= 1) issue_g(k - 1);
+      }
+      if (nk >= 1) issue_g(nk - 1);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;  // h: 32-column half
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* xp = reinterpret_cast<float*>(sm + o_xp);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int ii = (int)(k % kI);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + o_idx + ii * kIdxSlot);
+      mbar_wait(&bars[IFULL + ii], (uint32_t)((k / kI) & 1));
+      mbar_wait(&bars[CFULL], (uint32_t)(k & 1));
+      tc_after();
+      float c[kN][32];
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          uint32_t v[16];
+          tmem_ld16(tl + t_c + n * W + h * 32 + c2 * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) c[n][c2 * 16 + i] = __uint_as_float(v[i]);
+        }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[CEMPTY]);  // C(k + 1) may land
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      xp[h * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(h ^ 1) * kRows + row];
+      named_bar(1 + q, 64);  // both halves read before the next tile's writes
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + o_rows)[ii];
+      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[IEMPTY + ii]);
+      mbar_wait(&bars[DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k - 1) done with D'
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {  // 8 columns = one 16-B chunk of fp16
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i0 = q8 * 8 + e * 2;
+#define FTK_D(ii) (n == 0 ? c[1][ii] * c[2][ii] : (n == 1 ? c[0][ii] * c[2][ii] : c[0][ii] * c[1][ii]))
+            w[e] = f16x2_sat(resid * FTK_D(i0), resid * FTK_D(i0 + 1));
+#undef FTK_D
+          }
+          *reinterpret_cast<uint4*>(sm + o_d + n * kModeTile + swz(row, (h * 32 + q8 * 8) * 2, 128)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[DFULL]);
+    }
+    if (nk > 0) mbar_wait(&bars[DEMPTY], (uint32_t)((nk - 1) & 1));
+    tc_after();
+    // diagonal blocks: lanes 0..63 -> G_0 (cols t_g) and G_2 (t_g + 128);
+    // lanes 64..127 -> G_1 (t_g + 64); this warp: its 32 lanes, columns h*32..
+    float* outb = p.partials + (size_t)blockIdx.x * (kN * W * W);
+    const int modes[2] = {q < 2 ? 0 : 1, q < 2 ? 2 : -1};
+    const uint32_t cols[2] = {q < 2 ? t_g : t_g + W, t_g + 2 * W};
+    const int j = (q & 1) * 32 + lane;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      if (modes[mi] < 0) continue;  // warp-uniform
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint32_t v[16];
+        tmem_ld16(tl + cols[mi] + h * 32 + c2 * 16, v);
+        tmem_wait_ld();
+        float* out = outb + ((size_t)modes[mi] * W + j) * W + h * 32 + c2 * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) out[i] = nk > 0 ? __uint_as_float(v[i]) : 0.0f;
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+__global__ void big_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n2) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float2 x = reinterpret_cast<const float2*>(src)[e];
+    reinterpret_cast<uint32_t*>(dst)[e] = b16::f16x2_sat(x.x, x.y);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 big_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -616,6 +886,58 @@ bool big_row_map(CUtensorMap* tm, const float* a, int64_t rows, int w, bool atom
             CU_TENSOR_MAP_INTERLEAVE_NONE,
             atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Row-gather map of an fp16 copy of A_n (rows x 64 fp16): box of one 128-B row.
+bool big_row_map16(CUtensorMap* tm, const __half* a, int64_t rows) {
+  auto fn = big_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {64, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t run_core16(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float* grad,
+                       float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  constexpr int W = 64;
+  const int grid = (int)(v.ntiles < num_sms() ? v.ntiles : num_sms());
+  const size_t len = (size_t)kN * W * W;
+  if (grid < 1) return cudaErrorInvalidValue;
+  if (scratch_bytes < big_scratch_bytes(v, dims, true)) return cudaErrorInvalidValue;
+  BigParams p{};
+  __half* a16 = reinterpret_cast<__half*>(scratch + (size_t)num_sms() * len);
+  for (int n = 0; n < kN; ++n) {
+    const int64_t n2 = (int64_t)dims[n] * W / 2;
+    int64_t blocks = (n2 + 255) / 256;
+    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (!big_row_map16(&p.tmap[n], a16, dims[n])) return cudaErrorNotSupported;
+    p.idx[n] = v.idx[n];
+    p.bt_img[n] = v.b[n];  // raw B (J x R), rounded to fp16 in the kernel
+    a16 += (int64_t)dims[n] * W;
+  }
+  p.vals = v.vals;
+  p.ntiles = v.ntiles;
+  p.tile_base = v.tile_base;
+  p.tile_rows = v.tile_rows;
+  p.tperm = v.tperm;
+  p.tmul = mul;
+  p.tadd = add;
+  p.partials = scratch;
+  cudaError_t e = cudaFuncSetAttribute(big16_core_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b16::bytes);
+  if (e != cudaSuccess) return e;
+  big16_core_kernel<<<grid, b16::kThreads, b16::bytes, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  big_reduce_kernel<<<(int)((len + 255) / 256), 256, 0, st>>>(scratch, grid, (int)len, grad);
+  return cudaGetLastError();
 }
 
 template <int W>
@@ -727,6 +1049,8 @@ cudaError_t launch_big_factor(const KView& v, const int32_t* dims, int64_t mul, 
 
 cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                             float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  static const bool tf32_core = std::getenv("FTKCU_BIG_CORE_TF32") != nullptr;  // A/B only
+  if (v.r == 64 && !tf32_core) return run_core16(v, dims, mul, add, grad, scratch, scratch_bytes, st);
   return v.r == 64 ? run_core<64>(v, dims, mul, add, grad, scratch, scratch_bytes, st)
                    : run_core<128>(v, dims, mul, add, grad, scratch, scratch_bytes, st);
 }
