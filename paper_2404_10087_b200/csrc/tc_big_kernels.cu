@@ -32,7 +32,10 @@ using namespace tc;
 
 constexpr int kN = 3;
 constexpr int kRows = 128;
-constexpr int kThreads = 6 * 32;
+constexpr int kThreads = 6 * 32;   // core: producer, MMA, 4 epilogue warps
+// factor: producer, MMA, 8 epilogue warps (column halves), second producer
+// (warp 10) issuing half of every tile's row gathers
+constexpr int kThreadsF = 11 * 32;
 constexpr uint32_t kBlk = kRows * 128;  // one 32-column block of a row tile: 16 KB
 
 template <int W, bool kCore>
@@ -52,7 +55,8 @@ struct BigLayout {
   static constexpr uint32_t kIdx = (kN + 1) * kRows * 4;
   static constexpr int kI = 4;  // COO-record ring depth
   static constexpr uint32_t o_rows = o_idx + kI * kIdx;
-  static constexpr uint32_t o_bar = o_rows + 16;
+  static constexpr uint32_t o_xp = o_rows + 16;  // factor: x_hat halves [2][128]
+  static constexpr uint32_t o_bar = o_xp + 2 * kRows * 4;
   static constexpr uint32_t o_tmem = o_bar + 32 * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
   // TMEM: factor C/D [0, 3W) + U regions (one per mode at W = 64, so U_0..2
@@ -110,9 +114,11 @@ __device__ __forceinline__ uint32_t rn_bits(float x) { return __float_as_uint(x)
 // index loads in flight ahead of their issues.
 template <int W>
 __device__ __forceinline__ void gather_rows(uint8_t* dst, const CUtensorMap* tm,
-                                            const int32_t* s_idx, uint64_t* bar) {
+                                            const int32_t* s_idx, uint64_t* bar, int part = 0,
+                                            int nparts = 1) {
+  const int per = kRows / 4 / nparts;  // 4-row groups of this producer
 #pragma unroll 1
-  for (int g0 = 0; g0 < kRows / 4; g0 += 8) {
+  for (int g0 = part * per; g0 < (part + 1) * per; g0 += 8) {
     int4 r[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
@@ -125,12 +131,12 @@ __device__ __forceinline__ void gather_rows(uint8_t* dst, const CUtensorMap* tm,
   }
 }
 
-template <int W, bool kCore>
+template <int W, bool kCore, int kP = 1>
 __device__ void big_setup(uint8_t* sm, uint64_t* bars, uint32_t* tslot, const BigParams& p) {
   using L = BigLayout<W, kCore>;
   if (threadIdx.x == 0) {
     for (int s = 0; s < L::kStages; ++s) {
-      mbar_init(&bars[B_FULL + s], 1);
+      mbar_init(&bars[B_FULL + s], kP);
       mbar_init(&bars[B_EMPTY + s], 1);
     }
     for (int i = 0; i < L::kI; ++i) {
@@ -173,15 +179,20 @@ __device__ void big_teardown(uint32_t tmem) {
 // Warp 0 (all lanes wait, one elected lane issues): per tile the COO
 // record, then one stage per job.  Job order = the MMA warp's: factor
 // C(0) [U(k) C(k+1)]...; core C(0) [C(k+1) G(k)]...
-template <int W, bool kCore>
-__device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
+// kP producers walk the same job sequence: part 0 also fetches the COO
+// records and issues the bulk copies, every part gathers 1 / kP of the rows
+// and arrives once per job (FULL barriers count kP arrivals).
+template <int W, bool kCore, int kP = 1>
+__device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, int64_t nk,
+                             int part = 0) {
   using L = BigLayout<W, kCore>;
   int64_t job = 0;
+  constexpr uint32_t kHalfA = L::kA / kP;
   // COO records are requested kAhead tiles before their rows are gathered
   // (the stream comes from HBM: ~1 us per request)
   constexpr int kAhead = 2;
   auto request = [&](int64_t k) {  // tile k's COO record -> ring slot
-    if (k >= nk) return;
+    if (k >= nk || part != 0) return;
     const int i = (int)(k % L::kI);
     const int64_t tile = big_tile(p, k);
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
@@ -213,9 +224,9 @@ __device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, in
       const int s = stage();
       uint8_t* st = sm + L::o_st + s * L::kStage;
       if (elect_one()) {
-        mbar_expect_tx(&bars[B_FULL + s], L::kStage);
-        gather_rows<W>(st, &p.tmap[n], idx_of(k) + n * kRows, &bars[B_FULL + s]);
-        bulk_g2s(st + L::kA, p.bt_img[n], L::kB, &bars[B_FULL + s]);
+        mbar_expect_tx(&bars[B_FULL + s], kHalfA + (part == 0 ? L::kB : 0));
+        gather_rows<W>(st, &p.tmap[n], idx_of(k) + n * kRows, &bars[B_FULL + s], part, kP);
+        if (part == 0) bulk_g2s(st + L::kA, p.bt_img[n], L::kB, &bars[B_FULL + s]);
       }
       __syncwarp();
     }
@@ -241,8 +252,12 @@ __device__ void big_producer(const BigParams& p, uint8_t* sm, uint64_t* bars, in
       for (int n = 0; n < kN; ++n) {  // U jobs: the B images only
         const int s = stage();
         if (elect_one()) {
-          mbar_expect_tx(&bars[B_FULL + s], L::kB);
-          bulk_g2s(sm + L::o_st + s * L::kStage + L::kA, p.b_img[n], L::kB, &bars[B_FULL + s]);
+          if (part == 0) {
+            mbar_expect_tx(&bars[B_FULL + s], L::kB);
+            bulk_g2s(sm + L::o_st + s * L::kStage + L::kA, p.b_img[n], L::kB, &bars[B_FULL + s]);
+          } else {
+            mbar_arrive(&bars[B_FULL + s]);
+          }
         }
         __syncwarp();
       }
@@ -298,7 +313,7 @@ __device__ __forceinline__ float big_xhat(uint32_t tl) {
 // is the whole step, so the epilogue only issues REDs; otherwise it re-reads
 // the row through L2 for the regulariser (and the overwrite rule).
 template <int W, bool kFold>
-__global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_constant__ BigParams p) {
+__global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_constant__ BigParams p) {
   using L = BigLayout<W, false>;
   static_assert(!kFold || L::d_bytes == L::kB, "regulariser operand");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -314,12 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
     }
     fence_proxy_async();
   }
-  big_setup<W, false>(sm, bars, tslot, p);
+  big_setup<W, false, 2>(sm, bars, tslot, p);
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (warp == 0) {
-    big_producer<W, false>(p, sm, bars, nk);
+  if (warp == 0 || warp == 10) {
+    big_producer<W, false, 2>(p, sm, bars, nk, warp == 0 ? 0 : 1);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
@@ -356,23 +371,41 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
       }
     }
   } else {
-    const int q = warp & 3, row = q * 32 + lane;
+    // two warps per TMEM lane quarter, each owning half of the W columns
+    const int q = warp & 3, h = (warp - 2) >> 2, row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const float lr_reg = p.lr * p.reg;
+    constexpr int kHalf = W / 2;
+    float* xp = reinterpret_cast<float*>(sm + L::o_xp);  // x_hat halves [2][128]
     for (int64_t k = 0; k < nk; ++k) {
       const int i = (int)(k % L::kI);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
       mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
       mbar_wait(&bars[B_CFULL], (uint32_t)(k & 1));
       tc_after();
-      const float xhat = big_xhat<W>(tl);
+      float part = 0.0f;
+#pragma unroll 1
+      for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(tl + 0 * W + c * 16, v0);
+        tmem_ld16(tl + 1 * W + c * 16, v1);
+        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          part = fmaf(__uint_as_float(v0[e]), __uint_as_float(v1[e]) * __uint_as_float(v2[e]), part);
+      }
+      xp[h * kRows + row] = part;
+      named_bar(2 + q, 64);
+      const float xhat = part + xp[(h ^ 1) * kRows + row];
+      named_bar(2 + q, 64);  // both halves read before the next tile's writes
       const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
       const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
       const float sc = p.lr * resid;
-      constexpr int kH = W < 64 ? W : 64;  // columns per prefetched half-row
-      // D'_n = lr r prod_{m != n} C_m, in place over C (A operand of U_n)
+      // D'_n = lr r prod_{m != n} C_m, in place over this warp's half of C
+      // (A operand of U_n)
 #pragma unroll 1
-      for (int c = 0; c < W / 16; ++c) {
+      for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
         uint32_t v0[16], v1[16], v2[16];
         tmem_ld16(tl + 0 * W + c * 16, v0);
         tmem_ld16(tl + 1 * W + c * 16, v1);
@@ -393,35 +426,32 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
       }
       tmem_wait_st();
       tc_before();
-      named_bar(1, 128);
+      named_bar(1, 256);
       if (warp == 2 && lane == 0) mbar_arrive(&bars[B_DFULL]);
       int32_t g[kN];
 #pragma unroll
       for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
       for (int n = 0; n < kN; ++n) {
         const int64_t u = k * kN + n;
-        float* dst = p.a[n] + (size_t)g[n] * W;
-#pragma unroll 1
-        for (int hh = 0; hh < W / kH; ++hh) {
-        // the live row (through L2) for the regulariser term, loaded ahead of
-        // the U wait so its latency overlaps the U GEMM
-        float4 a4[kH / 4];
+        float* dst = p.a[n] + (size_t)g[n] * W + h * kHalf;
+        // the live half-row (through L2) for the regulariser term, loaded
+        // ahead of the U wait so its latency overlaps the U GEMM
+        float4 a4[kHalf / 4];
 #pragma unroll
-        for (int q = 0; q < kH / 4; ++q)
-          a4[q] = (ok && !kFold) ? __ldcg(reinterpret_cast<const float4*>(dst + hh * kH + q * 4))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (hh == 0) {
-          mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
-          tc_after();
-        }
+        for (int qq = 0; qq < kHalf / 4; ++qq)
+          a4[qq] = (ok && !kFold) ? __ldcg(reinterpret_cast<const float4*>(dst + qq * 4))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
+        tc_after();
+        {
 #pragma unroll
-        for (int c = 0; c < kH / 16; ++c) {
+        for (int c = 0; c < kHalf / 16; ++c) {
           uint32_t v[16];
-          tmem_ld16(tl + L::t_u + (n % L::kUN) * W + hh * kH + c * 16, v);
+          tmem_ld16(tl + L::t_u + (n % L::kUN) * W + h * kHalf + c * 16, v);
           tmem_wait_ld();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const int col = hh * kH + c * 16 + q4 * 4;
+            const int col = c * 16 + q4 * 4;
             const float4 a = a4[c * 4 + q4];
             float4 st;  // kFold: a = 0, U' already holds the regulariser
             st.x = __uint_as_float(v[q4 * 4 + 0]) - lr_reg * a.x;
@@ -443,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) big_factor_kernel(const __grid_co
         }
         }
         tc_before();
-        named_bar(1, 128);
+        named_bar(1, 256);
         if (warp == 2 && lane == 0) {
           if (L::kUN == 1) mbar_arrive(&bars[B_UEMPTY]);
           if (n == kN - 1) mbar_arrive(&bars[B_IEMPTY + i]);
@@ -978,7 +1008,7 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
   auto kern = (W == 64 && atomic_update) ? big_factor_kernel<W, W == 64> : big_factor_kernel<W, false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  kern<<<(int)sweep_grid(v), kThreads, bytes, st>>>(p);
+  kern<<<(int)sweep_grid(v), kThreadsF, bytes, st>>>(p);
   return cudaGetLastError();
 }
 
