@@ -35,7 +35,7 @@ def main():
     ap.add_argument("--no-graphs", action="store_true")
     args = ap.parse_args()
     P = args.parts
-    cfg, j, coo = bench.make_workload(args.config, 0, 1, 0, 0)
+    cfg, j, coo, _ = bench.make_workload(args.config, 0, 1, 0, 0)
     ranks = [j] * 3
     s = eng.Session(0)
     s.set_option("precision", {"fp32": 0, "tf32": 1, "3xtf32": 2}[args.precision])
