@@ -390,6 +390,9 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);  // COO slot may be refilled
       t.ok = row < nvalid;
       t.resid = t.ok ? xv - xhat : 0.0f;
+      // padding rows carry row index -1: epi2 then needs one shuffle per row
+#pragma unroll
+      for (int n = 0; n < kN; ++n) t.g[n] = t.ok ? t.g[n] : -1;
       // kAtomic: D' = lr r D, so the U GEMM (plus A x (-lr reg I)) yields the
       // step itself; overwrite mode scales in epi2.
       const float sc = kAtomic ? p.lr * t.resid : 1.0f;
@@ -452,9 +455,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         for (int i = 0; i < 4; ++i) {
           const int rl = i * 8 + (lane >> 2), ch = lane & 3;
           const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
-          const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
           const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
-          if (okr && !(p.exp & 16)) {  // exp 16: no write-back (timing only)
+          if (g >= 0 && !(p.exp & 16)) {  // exp 16: no write-back (timing only)
             float* gp = dst + (size_t)g * kW + h * 16 + ch * 4;
             if constexpr (kAtomic)
               red_add_v4(gp, v);

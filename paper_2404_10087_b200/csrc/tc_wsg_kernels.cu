@@ -517,6 +517,8 @@ __global__ void __launch_bounds__(FW<W>::Threads, 1)
       for (int n = 0; n < N; ++n) t.g[n] = s_idx[n * kRows + row];
       const float xv = reinterpret_cast<const float*>(s_idx + N * kRows)[row];
       t.ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
+#pragma unroll
+      for (int n = 0; n < N; ++n) t.g[n] = t.ok ? t.g[n] : -1;  // one shuffle per row in epi2
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[G_IEMPTY + ii]);
       const float sc = t.ok ? p.lr * (xv - xhat) : 0.0f;
@@ -557,9 +559,8 @@ __global__ void __launch_bounds__(FW<W>::Threads, 1)
         for (int i = 0; i < 2; ++i) {
           const int rl = i * 16 + (lane >> 1), ch = lane & 1;
           const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
-          const int okr = __shfl_sync(0xffffffffu, (int)t.ok, rl);
           const float4 v = *reinterpret_cast<const float4*>(stage + swz32b(rl, ch * 16));
-          if (okr && h * 8 < p.jr) red_add_v4(dst + (size_t)g * p.jr + h * 8 + ch * 4, v);
+          if (g >= 0 && h * 8 < p.jr) red_add_v4(dst + (size_t)g * p.jr + h * 8 + ch * 4, v);
         }
         __syncwarp();
       }
