@@ -43,12 +43,15 @@ struct BigLayout {
   static constexpr uint32_t kA = kRows * W * 4;  // row tile: W / 32 blocks of 16 KB
   static constexpr uint32_t kB = W * W * 4;      // B image: W / 32 blocks of W x 128 B
   static constexpr uint32_t kStage = kA + kB;
-  static constexpr int kStages = W == 64 ? (kCore ? 3 : 4) : 1;
+  static constexpr int kStages = W == 64 ? 3 : 1;
   static constexpr uint32_t o_st = 0;
-  // core: D' tile (MN-major); factor at W = 64: -lr reg I, the regulariser
-  // as a second U GEMM operand (the C stages stay alive until U_n)
+  // core: D' tile (MN-major).  factor at W = 64: I (a second C GEMM per
+  // mode copies the gathered rows into TMEM) and -lr reg I (the regulariser
+  // as a second U GEMM operand, A from that TMEM copy), so a stage is free as
+  // soon as its C GEMM has run
+  static constexpr bool kACopy = !kCore && W == 64;
   static constexpr uint32_t o_d = o_st + kStages * kStage;
-  static constexpr uint32_t d_bytes = kCore ? kA : (W == 64 ? kB : 0);
+  static constexpr uint32_t d_bytes = kCore ? kA : (kACopy ? 2 * kB : 0);
   // the G GEMM reads M = 128 rows = 4 blocks of the A part: past a W = 64
   // tile it runs into the stage's B image / the next stage / the D' tile
   static constexpr uint32_t o_idx = o_d + d_bytes;
@@ -62,9 +65,10 @@ struct BigLayout {
   // TMEM: factor C/D [0, 3W) + U regions (one per mode at W = 64, so U_0..2
   // issue back to back; one shared at W = 128); core: C buffers (two at
   // W = 64, so C(k+1) overlaps the epilogue of k) + G_pass.
-  static constexpr int kUN = W == 64 ? kN : 1;
+  static constexpr int kUN = 1;
   static constexpr int kCB = W == 64 ? 2 : 1;
-  static constexpr uint32_t t_u = 3 * W;
+  static constexpr uint32_t kMS = kACopy ? 2 * W : W;  // factor TMEM per mode: C [| A copy]
+  static constexpr uint32_t t_u = 3 * kMS;
   static constexpr uint32_t t_g = kCB * 3 * W;
   static constexpr uint32_t tcols = 512;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
@@ -283,9 +287,15 @@ __device__ __forceinline__ void issue_c(uint8_t* sm, uint64_t* bars, uint32_t tm
     const uint32_t a0 = smem_u32(sm + L::o_st + s * L::kStage);
     const uint32_t b0 = a0 + L::kA;
 #pragma unroll
-    for (int ks = 0; ks < W / 8; ++ks)
-      mma_ss(tmem + n * W, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
+    for (int ks = 0; ks < W / 8; ++ks) {
+      const uint64_t da = sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128);
+      mma_ss(tmem + n * L::kMS, da,
              sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
+      if constexpr (L::kACopy)  // A_n I: the rows into TMEM for the regulariser GEMM
+        mma_ss(tmem + n * L::kMS + W, da,
+               sdesc(smem_u32(sm + L::o_d) + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128),
+               id, ks > 0);
+    }
     if (release) mma_commit(&bars[B_EMPTY + s]);
   }
   mma_commit(&bars[B_CFULL + cb]);
@@ -309,23 +319,25 @@ __device__ __forceinline__ float big_xhat(uint32_t tl) {
   return x;
 }
 
-// kFold (W = 64, Hogwild accumulate): U_n' = D'_n B_n^T + A_n (-lr reg I)
-// is the whole step, so the epilogue only issues REDs; otherwise it re-reads
-// the row through L2 for the regulariser (and the overwrite rule).
-template <int W, bool kFold>
+// W = 64 (L::kACopy): U_n' = D'_n B_n^T + A_n (-lr reg I) with A_n from its
+// TMEM copy is the whole Hogwild step, so the epilogue only issues REDs;
+// W = 128 (and the overwrite rule) re-reads the row through L2 for the
+// regulariser.
+template <int W>
 __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_constant__ BigParams p) {
   using L = BigLayout<W, false>;
-  static_assert(!kFold || L::d_bytes == L::kB, "regulariser operand");
+  constexpr bool kFold = L::kACopy;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
-  if constexpr (kFold) {
+  if constexpr (L::kACopy) {  // I, then -lr reg I (rows j, K = j', K-major SW128 blocks)
     const float dv = __uint_as_float(rn_bits(-p.lr * p.reg));
     for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
       const int j = e / W, jj = e - j * W;
-      *reinterpret_cast<float*>(sm + L::o_d + (jj / 32) * (W * 128) + swz(j, (jj % 32) * 4, 128)) =
-          j == jj ? dv : 0.0f;
+      const uint32_t off = (jj / 32) * (W * 128) + swz(j, (jj % 32) * 4, 128);
+      *reinterpret_cast<float*>(sm + L::o_d + off) = j == jj ? 1.0f : 0.0f;
+      *reinterpret_cast<float*>(sm + L::o_d + L::kB + off) = j == jj ? dv : 0.0f;
     }
     fence_proxy_async();
   }
@@ -339,11 +351,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
       int64_t job = 0;
-      const uint32_t dg = smem_u32(sm + L::o_d);
+      const uint32_t dg = smem_u32(sm + L::o_d) + L::kB;
       for (int64_t k = 0; k < nk; ++k) {
         // C(k) overwrites D'(k - 1): in-order behind U(k - 1) on the tensor pipe
-        int cs[kN];
-        issue_c<W, false>(sm, bars, tmem, job, 0, !kFold, cs);
+        issue_c<W, false>(sm, bars, tmem, job, 0);
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n, ++job) {
           const int s = (int)(job % L::kStages);
@@ -355,16 +366,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           const uint32_t tu = tmem + L::t_u + (n % L::kUN) * W;
 #pragma unroll
           for (int ks = 0; ks < W / 8; ++ks)
-            mma_ts(tu, tmem + n * W + ks * 8,
+            mma_ts(tu, tmem + n * L::kMS + ks * 8,
                    sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, ks > 0);
-          if constexpr (kFold) {  // + A_n (-lr reg I), A_n from its C stage, then free it
-            const uint32_t a0 = smem_u32(sm + L::o_st + cs[n] * L::kStage);
+          if constexpr (kFold)  // + A_n (-lr reg I), A_n from its TMEM copy
 #pragma unroll
             for (int ks = 0; ks < W / 8; ++ks)
-              mma_ss(tu, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
+              mma_ts(tu, tmem + n * L::kMS + W + ks * 8,
                      sdesc(dg + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, 1);
-            mma_commit(&bars[B_EMPTY + cs[n]]);
-          }
           mma_commit(&bars[B_EMPTY + s]);
           mma_commit(&bars[B_UFULL + n % L::kUN]);
         }
@@ -387,9 +395,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
 #pragma unroll 1
       for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
         uint32_t v0[16], v1[16], v2[16];
-        tmem_ld16(tl + 0 * W + c * 16, v0);
-        tmem_ld16(tl + 1 * W + c * 16, v1);
-        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_ld16(tl + 0 * L::kMS + c * 16, v0);
+        tmem_ld16(tl + 1 * L::kMS + c * 16, v1);
+        tmem_ld16(tl + 2 * L::kMS + c * 16, v2);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 16; ++e)
@@ -407,9 +415,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
 #pragma unroll 1
       for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
         uint32_t v0[16], v1[16], v2[16];
-        tmem_ld16(tl + 0 * W + c * 16, v0);
-        tmem_ld16(tl + 1 * W + c * 16, v1);
-        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_ld16(tl + 0 * L::kMS + c * 16, v0);
+        tmem_ld16(tl + 1 * L::kMS + c * 16, v1);
+        tmem_ld16(tl + 2 * L::kMS + c * 16, v2);
         tmem_wait_ld();
         uint32_t d0[16], d1[16], d2[16];
 #pragma unroll
@@ -420,9 +428,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           d1[e] = rn_bits(c0 * c2);
           d2[e] = rn_bits(c0 * c1);
         }
-        tmem_st16(tl + 0 * W + c * 16, d0);
-        tmem_st16(tl + 1 * W + c * 16, d1);
-        tmem_st16(tl + 2 * W + c * 16, d2);
+        tmem_st16(tl + 0 * L::kMS + c * 16, d0);
+        tmem_st16(tl + 1 * L::kMS + c * 16, d1);
+        tmem_st16(tl + 2 * L::kMS + c * 16, d2);
       }
       tmem_wait_st();
       tc_before();
@@ -439,8 +447,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
         float4 a4[kHalf / 4];
 #pragma unroll
         for (int qq = 0; qq < kHalf / 4; ++qq)
-          a4[qq] = (ok && !kFold) ? __ldcg(reinterpret_cast<const float4*>(dst + qq * 4))
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          a4[qq] = (ok && (!kFold || !p.atomic_update))
+                       ? __ldcg(reinterpret_cast<const float4*>(dst + qq * 4))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
         tc_after();
         {
@@ -453,13 +462,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           for (int q4 = 0; q4 < 4; ++q4) {
             const int col = c * 16 + q4 * 4;
             const float4 a = a4[c * 4 + q4];
-            float4 st;  // kFold: a = 0, U' already holds the regulariser
-            st.x = __uint_as_float(v[q4 * 4 + 0]) - lr_reg * a.x;
-            st.y = __uint_as_float(v[q4 * 4 + 1]) - lr_reg * a.y;
-            st.z = __uint_as_float(v[q4 * 4 + 2]) - lr_reg * a.z;
-            st.w = __uint_as_float(v[q4 * 4 + 3]) - lr_reg * a.w;
+            float4 st;  // kFold: U' already holds the regulariser
+            const float rg = kFold ? 0.0f : lr_reg;
+            st.x = __uint_as_float(v[q4 * 4 + 0]) - rg * a.x;
+            st.y = __uint_as_float(v[q4 * 4 + 1]) - rg * a.y;
+            st.z = __uint_as_float(v[q4 * 4 + 2]) - rg * a.z;
+            st.w = __uint_as_float(v[q4 * 4 + 3]) - rg * a.w;
             if (ok) {
-              if (kFold || p.atomic_update) {
+              if (p.atomic_update) {
                 red_add_v4(dst + col, st);
               } else {
                 st.x += a.x;
@@ -1005,7 +1015,7 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
   p.reg = reg;
   p.atomic_update = atomic_update;
   const int bytes = (int)BigLayout<W, false>::bytes;
-  auto kern = (W == 64 && atomic_update) ? big_factor_kernel<W, W == 64> : big_factor_kernel<W, false>;
+  auto kern = big_factor_kernel<W>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   kern<<<(int)sweep_grid(v), kThreadsF, bytes, st>>>(p);
