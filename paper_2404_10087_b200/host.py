@@ -71,6 +71,10 @@ def lib():
     L.ftkh_tensor_copy.argtypes = [C.c_void_p, _i32p, _i32p, _f32p]
     L.ftkh_tensor_free.argtypes = [C.c_void_p]
     L.ftkh_save_coo.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, _f32p, C.c_char_p]
+    L.ftkh_load_coo_binary.restype = C.c_void_p
+    L.ftkh_load_coo_binary.argtypes = [C.c_char_p]
+    L.ftkh_tensor_order.argtypes = [C.c_void_p]
+    L.ftkh_save_coo_binary.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, _f32p, C.c_char_p]
     L.ftkh_set_device_options.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     L.ftkh_epoch_plus.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p,
                                   _fpp, _fpp, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
@@ -165,6 +169,30 @@ def load_coo(path: str, order: int = 0):
         return dims, idx, vals
     finally:
         L.ftkh_tensor_free(h)
+
+
+def load_coo_binary(path: str):
+    """ftk::load_coo_binary (FTKC1): (dims, idx [nnz x order], vals)."""
+    L = lib()
+    h = L.ftkh_load_coo_binary(path.encode())
+    if not h:
+        raise HostError(L.ftkh_last_error().decode())
+    try:
+        order, nnz = L.ftkh_tensor_order(h), L.ftkh_tensor_nnz(h)
+        dims = np.empty(order, np.int32)
+        idx = np.empty((nnz, order), np.int32)
+        vals = np.empty(nnz, np.float32)
+        L.ftkh_tensor_copy(h, _p(dims, _i32p), _p(idx, _i32p), _p(vals, _f32p))
+        return dims, idx, vals
+    finally:
+        L.ftkh_tensor_free(h)
+
+
+def save_coo_binary(dims, idx, vals, path):
+    dims, idx = _i32(dims), _i32(idx)
+    vals = np.ascontiguousarray(vals, np.float32)
+    _ck(lib().ftkh_save_coo_binary(dims.size, _p(dims, _i32p), vals.size, _p(idx, _i32p),
+                                   _p(vals, _f32p), path.encode()))
 
 
 def save_coo(dims, idx, vals, path):

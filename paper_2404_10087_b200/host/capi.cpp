@@ -123,6 +123,19 @@ void* ftkh_load_coo(const char* path, int order) {
   return rc ? nullptr : t;
 }
 
+void* ftkh_load_coo_binary(const char* path) {
+  SparseTensor* t = nullptr;
+  int rc = guarded([&] { t = new SparseTensor(load_coo_binary(path)); });
+  return rc ? nullptr : t;
+}
+
+int ftkh_tensor_order(void* h) { return static_cast<SparseTensor*>(h)->order; }
+
+int ftkh_save_coo_binary(int order, const int32_t* dims, int64_t nnz, const int32_t* idx,
+                         const float* vals, const char* path) {
+  return guarded([&] { save_coo_binary(make_tensor(order, dims, nnz, idx, vals), path); });
+}
+
 int ftkh_infer_coo_order(const char* path) {
   int o = -1;
   guarded([&] { o = infer_coo_order(path); });

@@ -95,6 +95,33 @@ def test_coo_roundtrip(tmp_path):
     assert np.array_equal(idx, t.idx) and np.array_equal(vals, t.vals)
 
 
+def test_binary_coo_roundtrip_matches_text(tmp_path):
+    """FTKC1 (engine addition): exact round trip, and the same
+    tensor as the FROSTT text path; corrupt files are errors."""
+    t = O.random_tensor([40, 30, 20, 10], 2000, 3, -1.0, 4.0)
+    binp, txtp = str(tmp_path / "t.ftkc"), str(tmp_path / "t.tns")
+    host.save_coo_binary(t.dims, t.idx, t.vals, binp)
+    host.save_coo(t.dims, t.idx, t.vals, txtp)
+    dims, idx, vals = host.load_coo_binary(binp)
+    assert np.array_equal(dims, t.dims) and np.array_equal(idx, t.idx)
+    assert np.array_equal(vals.view(np.uint32), t.vals.view(np.uint32))
+    d2, i2, v2 = host.load_coo(txtp)
+    assert np.array_equal(d2, dims) and np.array_equal(i2, idx) and np.array_equal(v2, vals)
+    raw = open(binp, "rb").read()
+    bad = tmp_path / "bad.ftkc"
+    bad.write_bytes(raw[:-4])
+    with pytest.raises(host.HostError, match="truncated"):
+        host.load_coo_binary(str(bad))
+    bad.write_bytes(b"XXXXXXXX" + raw[8:])
+    with pytest.raises(host.HostError, match="not an FTKC1"):
+        host.load_coo_binary(str(bad))
+    dup = t.idx.copy()
+    dup[1] = dup[0]
+    host.save_coo_binary(t.dims, dup, t.vals, str(bad))
+    with pytest.raises(host.HostError, match="duplicate"):
+        host.load_coo_binary(str(bad))
+
+
 @pytest.mark.parametrize("text,msg", [
     ("# dims: 2 2 2\n1 1 3 1.0\n", "exceeds declared dims"),
     ("# only comments\n", "empty tensor"),
