@@ -671,22 +671,6 @@ static_assert(bytes <= 227 * 1024, "shared-memory budget");
 enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 9, CFULL = 12, CEMPTY = 13, DFULL = 14, DEMPTY = 15 };
 constexpr uint32_t t_c = 0, t_g = 3 * W;  // C: 192 columns; G: [stack01: 128][stack2: 64]
 
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
 }  // namespace b16
 
 __global__ void __launch_bounds__(b16::kThreads, 1) big16_core_kernel(const __grid_constant__ BigParams p) {
@@ -900,7 +884,7 @@ __global__ void big_half_kernel(const float* __restrict__ src, __half* __restric
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
        e += (int64_t)gridDim.x * blockDim.x) {
     const float2 x = reinterpret_cast<const float2*>(src)[e];
-    reinterpret_cast<uint32_t*>(dst)[e] = b16::f16x2_sat(x.x, x.y);
+    reinterpret_cast<uint32_t*>(dst)[e] = f16x2_sat(x.x, x.y);
   }
 }
 
@@ -1089,9 +1073,8 @@ cudaError_t launch_big_factor(const KView& v, const int32_t* dims, int64_t mul, 
 
 cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                             float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st) {
-  static const bool tf32_core = std::getenv("FTKCU_BIG_CORE_TF32") != nullptr;  // A/B only
-  if (v.r == 64 && !tf32_core) return run_core16(v, dims, mul, add, grad, scratch, scratch_bytes, st);
-  return v.r == 64 ? run_core<64>(v, dims, mul, add, grad, scratch, scratch_bytes, st)
+  // W = 64: one pass on the fp16 copy; W = 128: one tf32 pass per mode
+  return v.r == 64 ? run_core16(v, dims, mul, add, grad, scratch, scratch_bytes, st)
                    : run_core<128>(v, dims, mul, add, grad, scratch, scratch_bytes, st);
 }
 

@@ -120,6 +120,28 @@ __device__ __forceinline__ void red_add_v4(float* gptr, float4 v) {
                : "memory");
 }
 
+// ---- 16-bit operands (kind::f16) ---------------------------------------------------
+
+// Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// Two floats -> f16x2 (lo, hi), round to nearest, saturating to +-65504
+// instead of overflowing to inf.
+__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // ---- layouts -------------------------------------------------------------------
 
 // Byte offset of (row, byte) in a tile of P-byte rows (P = 64 or 128) in the

@@ -824,25 +824,7 @@ enum : int {
   H_DEMPTY = 30,  // [2] G GEMM done with the r D tile
 };
 
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
 
-// Two floats -> f16x2 (lo, hi), round to nearest, saturating to +-65504
-// instead of overflowing to inf.
-__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
 
 __global__ void ws_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
   const int64_t n2 = n / 2;  // n = rows x 32: even
@@ -1084,6 +1066,17 @@ bool make_row_map16(CUtensorMap* tm, const __half* a, int64_t rows) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Timing experiments only (never set in production): FTKCU_WS_EXP bits
+// 1 / 2 / 4 / 8 / 16 drop the core slot hold / gathers / G GEMM / row copy /
+// factor write-back (scripts/ws_exp.sh).
+int ws_exp_bits() {
+  static const int bits = [] {
+    const char* e = std::getenv("FTKCU_WS_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return bits;
+}
+
 bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                  bool core) {
   for (int n = 0; n < kN; ++n) {
@@ -1127,7 +1120,7 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   p.reg = reg;
   p.atomic_update = atomic_update;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
-  if (const char* e = std::getenv("FTKCU_WS_EXP")) p.exp = std::atoi(e);
+  p.exp = ws_exp_bits();
   if (p.ntiles == 0) return cudaSuccess;
   const int bytes = (int)WsLayout<false>::bytes;
   auto kern = atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>;
@@ -1144,7 +1137,7 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   WsParams p{};
   if (!make_params(p, v, dims, mul, add, true)) return cudaErrorNotSupported;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
-  if (const char* e = std::getenv("FTKCU_WS_EXP")) p.exp = std::atoi(e);
+  p.exp = ws_exp_bits();
   const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
   const int len = kN * kW * kW;
   if (grid < 1) return cudaErrorInvalidValue;

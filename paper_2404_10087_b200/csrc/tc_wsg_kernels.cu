@@ -74,23 +74,7 @@ __host__ __device__ constexpr uint32_t swz32b(uint32_t row, uint32_t byte) {
   return row * 32 + ((((byte >> 4) ^ ((row >> 2) & 1))) << 4) + (byte & 15);
 }
 
-__device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
 
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
 
 // Layout per (order, sweep).  Row tiles: 128 rows x (64 B fp32 | 32 B fp16).
 template <int N, bool kCore>
