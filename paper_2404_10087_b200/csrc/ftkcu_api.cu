@@ -47,6 +47,7 @@ struct ftkcu_session {
   // dsgd.grid_cap for the measurement behind the default.
   int64_t opt_staleness = 32;
   int64_t opt_graphs = 1;  // capture the DSGD stratum loop in a CUDA graph
+  int64_t opt_dsgd_shift = 1;  // 0: skip the DSGD ring shifts (cost breakdown only)
   // DSGD epoch: per-cell tile permutations (device + pinned host staging)
   // and the captured stratum loop, re-captured when its key changes.
   int64_t* d_cellperm = nullptr;
@@ -389,6 +390,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     s->global_nnz = value;
   } else if (k == "graphs") {
     s->opt_graphs = value != 0;
+  } else if (k == "dsgd_shift") {
+    s->opt_dsgd_shift = value != 0;
   } else if (k == "staleness") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "staleness must be >= 0");
     s->opt_staleness = value;
@@ -972,9 +975,12 @@ static int enqueue_dsgd(ftkcu_session* s, DevTensor& t, int parts, const int64_t
       v.ntiles = t.cell_tile[cell + 1] - t.cell_tile[cell];
       v.tperm = s->d_cellperm + 2 * cell;
       if ((rc = launch_factor(s, v, 1, 0, lr_a, reg_a))) return rc;
-      if (parts > 1 && (rc = shift_block(s, 2, off3, parts, s->rank + ti))) return rc;
+      if (parts > 1 && s->opt_dsgd_shift &&
+          (rc = shift_block(s, 2, off3, parts, s->rank + ti)))
+        return rc;
     }
-    if (parts > 1 && (rc = shift_block(s, 1, off2, parts, s->rank + si))) return rc;
+    if (parts > 1 && s->opt_dsgd_shift && (rc = shift_block(s, 1, off2, parts, s->rank + si)))
+      return rc;
   }
   if (s->world > 1) {
     if ((rc = bcast_blocks(s, 1, off2))) return rc;

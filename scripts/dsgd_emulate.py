@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--precision", default="tf32")
     ap.add_argument("--loop", action="store_true", help="Python stratum loop (no fused call)")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--no-shift", action="store_true", help="skip the ring shifts (cost breakdown)")
     args = ap.parse_args()
     P = args.parts
     cfg, j, coo, _ = bench.make_workload(args.config, 0, 1, 0, 0)
@@ -56,6 +57,7 @@ def main():
     if args.loop:
         be.factor_epoch = None
     s.set_option("graphs", 0 if args.no_graphs else 1)
+    s.set_option("dsgd_shift", 0 if args.no_shift else 1)
     tr = dsgd.DsgdTrainer(be, lay, 0, staleness=args.staleness or None)
     ext = torch.cuda.ExternalStream(s.stream_handle, device=torch.device("cuda:0"))
     for k in range(args.warmup):
@@ -80,7 +82,7 @@ def main():
            "epoch_ms": float(np.mean(f_ms) + np.mean(c_ms)),
            "implied_job_nnz_per_s": coo.nnz / ((np.mean(f_ms) + np.mean(c_ms)) * 1e-3),
            "grid_cap": s.get_option("max_ctas"), "loop": args.loop,
-           "graphs": not args.no_graphs}
+           "graphs": not args.no_graphs, "shifts": not args.no_shift}
     print(json.dumps(out), flush=True)
     s.close()
 
