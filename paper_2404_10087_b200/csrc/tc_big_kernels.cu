@@ -880,6 +880,250 @@ __global__ void __launch_bounds__(b16::kThreads, 1) big16_core_kernel(const __gr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---- J = R = 128 core sweep: one pass per mode on the fp16 copy of A -----------
+//
+// TMEM fits C for all modes (384 columns) next to one mode's G (128), so the
+// core runs one launch per mode p.  Per tile the three C jobs gather each
+// mode's fp16 rows (32 KB, two 128-B column blocks per row) into a 2-stage
+// ring, mode p last; its stage is then also the MN-major A of G_p += A_p^T
+// D'_p (kind::f16), so no second gather.  The B^T images stay resident.
+
+namespace b16p {
+constexpr int W = 128;
+constexpr int kEpi = 8, kGW = 2, kGWarp = 2 + kEpi;
+constexpr int kThreads = (2 + kEpi + kGW) * 32;
+constexpr uint32_t kBlk16 = kRows * 128;          // 64 fp16 columns of 128 rows
+constexpr uint32_t kStage = 2 * kBlk16;           // one mode's rows: 32 KB
+constexpr int kS = 2, kI = 3;
+constexpr uint32_t o_a = 0;
+constexpr uint32_t o_d = o_a + kS * kStage;       // D'_p (fp16, MN-major, 2 blocks)
+constexpr uint32_t o_bt = o_d + kStage;           // B^T fp16 images: 32 KB per mode
+constexpr uint32_t o_idx = o_bt + kN * W * 256;
+constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
+constexpr uint32_t o_rows = o_idx + kI * kIdxSlot;
+constexpr uint32_t o_xp = o_rows + 64;
+constexpr uint32_t o_bar = o_xp + 2 * kRows * 4;
+constexpr uint32_t o_tmem = o_bar + 16 * 8;
+constexpr uint32_t bytes = o_tmem + 16;
+static_assert(bytes <= 227 * 1024, "shared-memory budget");
+enum : int { FULL = 0, EMPTY = 2, IFULL = 4, IEMPTY = 7, CFULL = 10, CEMPTY = 11, DFULL = 12, DEMPTY = 13 };
+constexpr uint32_t t_c = 0, t_g = 3 * W;  // C: 384 columns; G_p: 128
+}  // namespace b16p
+
+__global__ void __launch_bounds__(b16p::kThreads, 1) big16p_core_kernel(const __grid_constant__ BigParams p) {
+  using namespace b16p;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + o_tmem);
+  const int pm = p.pass;
+  for (int n = 0; n < kN; ++n)
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
+      const int j = e / W, r = e - j * W;  // B^T: rows r, K = j (two 64-column blocks)
+      *reinterpret_cast<__half*>(sm + o_bt + n * W * 256 + (j / 64) * (W * 128) +
+                                 swz(r, (j % 64) * 2, 128)) = __float2half_rn(p.bt_img[n][e]);
+    }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&bars[FULL + s], kGW);
+      mbar_init(&bars[EMPTY + s], 1);
+    }
+    for (int i = 0; i < kI; ++i) {
+      mbar_init(&bars[IFULL + i], 1);
+      mbar_init(&bars[IEMPTY + i], kEpi + kGW);
+    }
+    mbar_init(&bars[CFULL], 1);
+    mbar_init(&bars[CEMPTY], kEpi);
+    mbar_init(&bars[DFULL], kEpi);
+    mbar_init(&bars[DEMPTY], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // per tile the modes are gathered in the order m0, m1, pm (pm last)
+  const int m0 = pm == 0 ? 1 : 0, m1 = pm == 2 ? 1 : 2;
+  auto mode_of = [&](int j) { return j == 0 ? m0 : (j == 1 ? m1 : pm); };
+
+  if (warp == 0) {
+    if (lane == 0)
+      for (int64_t k = 0; k < nk; ++k) {
+        const int i = (int)(k % kI);
+        const int64_t tile = big_tile(p, k);
+        mbar_wait(&bars[IEMPTY + i], (uint32_t)(((k / kI) & 1) ^ 1));
+        int32_t* s_idx = reinterpret_cast<int32_t*>(sm + o_idx + i * kIdxSlot);
+        reinterpret_cast<int32_t*>(sm + o_rows)[i] = __ldg(p.tile_rows + tile);
+        mbar_expect_tx(&bars[IFULL + i], kIdxSlot);
+        for (int n = 0; n < kN; ++n)
+          bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[IFULL + i]);
+        bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[IFULL + i]);
+      }
+  } else if (warp >= kGWarp) {
+    const int gw = warp - kGWarp;
+    constexpr int kPer = kRows / 4 / kGW;  // 16 groups of 4 rows per warp per mode
+    int64_t job = 0;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int i = (int)(k % kI);
+      mbar_wait(&bars[IFULL + i], (uint32_t)((k / kI) & 1));
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + o_idx + i * kIdxSlot);
+      for (int j = 0; j < kN; ++j, ++job) {
+        const int s = (int)(job % kS), n = mode_of(j);
+        mbar_wait(&bars[EMPTY + s], (uint32_t)(((job / kS) & 1) ^ 1));
+        uint8_t* st = sm + o_a + s * kStage;
+        __syncwarp();
+        if (elect_one()) {
+          mbar_expect_tx(&bars[FULL + s], kPer * 4 * 256);
+#pragma unroll 1
+          for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 8) {
+            int4 r[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              r[g] = *reinterpret_cast<const int4*>(s_idx + n * kRows + (g0 + g) * 4);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+#pragma unroll
+              for (int cb = 0; cb < 2; ++cb)
+                tma_gather4(st + cb * kBlk16 + (g0 + g) * 512, &p.tmap[n], cb * 64, r[g].x,
+                            r[g].y, r[g].z, r[g].w, &bars[FULL + s]);
+          }
+          if (j == kN - 1) mbar_arrive(&bars[IEMPTY + i]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idc = idesc_f16(128, W, 0, 0), idg = idesc_f16(128, W, 1, 1);
+      const uint32_t bt = smem_u32(sm + o_bt), d0 = smem_u32(sm + o_d);
+      int64_t job = 0;
+      int sp_prev = 0;
+      // G(k - 1) holds the previous pm stage, which is also job 1's stage of tile k:
+      // issue it between jobs 0 and 1 (D'(k - 1) is written before C(k) may land)
+      auto issue_g = [&](int64_t kg, int sg) {
+        mbar_wait(&bars[DFULL], (uint32_t)(kg & 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + o_a + sg * kStage);
+#pragma unroll
+        for (int ks = 0; ks < kRows / 16; ++ks)
+          mma_f16(tmem + t_g, sdesc_l(a0 + ks * 2048, kBlk16, 1024, 2),
+                  sdesc_l(d0 + ks * 2048, kBlk16, 1024, 2), idg, (kg > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&bars[DEMPTY]);
+        mma_commit(&bars[EMPTY + sg]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        mbar_wait(&bars[CEMPTY], (uint32_t)((k & 1) ^ 1));
+        int sp = 0;
+        for (int j = 0; j < kN; ++j, ++job) {
+          const int s = (int)(job % kS), n = mode_of(j);
+          mbar_wait(&bars[FULL + s], (uint32_t)((job / kS) & 1));
+          tc_after();
+          const uint32_t a0 = smem_u32(sm + o_a + s * kStage);
+#pragma unroll
+          for (int ks = 0; ks < W / 16; ++ks)
+            mma_f16(tmem + t_c + n * W,
+                    sdesc_l(a0 + (ks / 4) * kBlk16 + (ks % 4) * 32, 16, 1024, 2),
+                    sdesc_l(bt + n * W * 256 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 2),
+                    idc, ks > 0);
+          if (j < kN - 1) mma_commit(&bars[EMPTY + s]);  // pm's stage waits for G
+          else sp = s;
+          if (j == 0 && k >= 1) issue_g(k - 1, sp_prev);
+        }
+        mma_commit(&bars[CFULL]);
+        sp_prev = sp;
+      }
+      if (nk >= 1) issue_g(nk - 1, sp_prev);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;  // h: 64-column half
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* xp = reinterpret_cast<float*>(sm + o_xp);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int ii = (int)(k % kI);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + o_idx + ii * kIdxSlot);
+      mbar_wait(&bars[IFULL + ii], (uint32_t)((k / kI) & 1));
+      mbar_wait(&bars[CFULL], (uint32_t)(k & 1));
+      tc_after();
+      float part = 0.0f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(tl + t_c + 0 * W + h * 64 + c * 16, v0);
+        tmem_ld16(tl + t_c + 1 * W + h * 64 + c * 16, v1);
+        tmem_ld16(tl + t_c + 2 * W + h * 64 + c * 16, v2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          part = fmaf(__uint_as_float(v0[e]), __uint_as_float(v1[e]) * __uint_as_float(v2[e]), part);
+      }
+      xp[h * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(h ^ 1) * kRows + row];
+      named_bar(1 + q, 64);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + o_rows)[ii];
+      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[IEMPTY + ii]);
+      mbar_wait(&bars[DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k - 1) done with D'
+      // D'_pm = r C_m0 C_m1 over this warp's 64 columns, fp16, MN-major
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v0[16], v1[16];
+        tmem_ld16(tl + t_c + m0 * W + h * 64 + c * 16, v0);
+        tmem_ld16(tl + t_c + m1 * W + h * 64 + c * 16, v1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q8 = 0; q8 < 2; ++q8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i0 = q8 * 8 + e * 2;
+            w[e] = f16x2_sat(resid * __uint_as_float(v0[i0]) * __uint_as_float(v1[i0]),
+                             resid * __uint_as_float(v0[i0 + 1]) * __uint_as_float(v1[i0 + 1]));
+          }
+          *reinterpret_cast<uint4*>(sm + o_d + h * kBlk16 + swz(row, (c * 16 + q8 * 8) * 2, 128)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[CEMPTY]);  // C(k + 1) may land
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[DFULL]);
+    }
+    if (nk > 0) mbar_wait(&bars[DEMPTY], (uint32_t)((nk - 1) & 1));
+    tc_after();
+    // G_pm: TMEM lane j (all 128), columns t_g + r; this warp: its lanes, half h
+    float* out = p.partials + (size_t)blockIdx.x * (kN * W * W) + (size_t)pm * W * W +
+                 (size_t)row * W + h * 64;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[16];
+      tmem_ld16(tl + t_g + h * 64 + c * 16, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) out[c * 16 + e] = nk > 0 ? __uint_as_float(v[e]) : 0.0f;
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 __global__ void big_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n2) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -912,12 +1156,13 @@ bool big_row_map(CUtensorMap* tm, const float* a, int64_t rows, int w, bool atom
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Row-gather map of an fp16 copy of A_n (rows x 64 fp16): box of one 128-B row.
-bool big_row_map16(CUtensorMap* tm, const __half* a, int64_t rows) {
+// Row-gather map of an fp16 copy of A_n (rows x w fp16): box of 64 columns
+// (one 128-B row block).
+bool big_row_map16(CUtensorMap* tm, const __half* a, int64_t rows, int w = 64) {
   auto fn = big_encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {64, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {128};
+  cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)w * 2};
   cuuint32_t box[2] = {64, 1};
   cuuint32_t es[2] = {1, 1};
   return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a), dims, strides, box, es,
@@ -960,6 +1205,48 @@ cudaError_t run_core16(const KView& v, const int32_t* dims, int64_t mul, int64_t
   big16_core_kernel<<<grid, b16::kThreads, b16::bytes, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  big_reduce_kernel<<<(int)((len + 255) / 256), 256, 0, st>>>(scratch, grid, (int)len, grad);
+  return cudaGetLastError();
+}
+
+cudaError_t run_core16p(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float* grad,
+                        float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  constexpr int W = 128;
+  const int grid = (int)(v.ntiles < num_sms() ? v.ntiles : num_sms());
+  const size_t len = (size_t)kN * W * W;
+  if (grid < 1) return cudaErrorInvalidValue;
+  if (scratch_bytes < big_scratch_bytes(v, dims, true)) return cudaErrorInvalidValue;
+  BigParams p{};
+  __half* a16 = reinterpret_cast<__half*>(scratch + (size_t)num_sms() * len);
+  for (int n = 0; n < kN; ++n) {
+    const int64_t n2 = (int64_t)dims[n] * W / 2;
+    int64_t blocks = (n2 + 255) / 256;
+    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (!big_row_map16(&p.tmap[n], a16, dims[n], W)) return cudaErrorNotSupported;
+    p.idx[n] = v.idx[n];
+    p.bt_img[n] = v.b[n];
+    a16 += (int64_t)dims[n] * W;
+  }
+  p.vals = v.vals;
+  p.ntiles = v.ntiles;
+  p.tile_base = v.tile_base;
+  p.tile_rows = v.tile_rows;
+  p.tperm = v.tperm;
+  p.tmul = mul;
+  p.tadd = add;
+  p.partials = scratch;
+  cudaError_t e = cudaFuncSetAttribute(big16p_core_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b16p::bytes);
+  if (e != cudaSuccess) return e;
+  for (int pass = 0; pass < kN; ++pass) {
+    p.pass = pass;
+    big16p_core_kernel<<<grid, b16p::kThreads, b16p::bytes, st>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   big_reduce_kernel<<<(int)((len + 255) / 256), 256, 0, st>>>(scratch, grid, (int)len, grad);
   return cudaGetLastError();
 }
@@ -1073,9 +1360,9 @@ cudaError_t launch_big_factor(const KView& v, const int32_t* dims, int64_t mul, 
 
 cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                             float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st) {
-  // W = 64: one pass on the fp16 copy; W = 128: one tf32 pass per mode
+  // fp16 copy of A: W = 64 in one pass, W = 128 in one pass per mode
   return v.r == 64 ? run_core16(v, dims, mul, add, grad, scratch, scratch_bytes, st)
-                   : run_core<128>(v, dims, mul, add, grad, scratch, scratch_bytes, st);
+                   : run_core16p(v, dims, mul, add, grad, scratch, scratch_bytes, st);
 }
 
 }  // namespace ftkcu

@@ -140,3 +140,53 @@ def test_factor_steps_8_and_16_epilogue_warps(session, warps):
     for k in range(3):
         got, want = a[k] - m.a[k], mc.a[k] - m.a[k]
         np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
+
+
+MULTI = [(3, 32, 32), (3, 64, 64), (3, 128, 128), (4, 16, 16)]
+
+
+@pytest.mark.parametrize("shape", MULTI, ids=_id)
+def test_core_gradient_many_tiles_per_cta(session, shape):
+    """Enough nonzeros that every persistent CTA runs several tiles (> 2 x 148
+    tiles of 128): the pipelines' stage reuse across tiles (C of tile k while
+    G of tile k - 1 still holds its stage) is exercised, not just one pass."""
+    order, j, r = shape
+    t = _planted(order, j, r, 148 * 128 * 3 + 77)
+    m = _model(t, j, r)
+    session.set_option("precision", eng.PREC_TF32)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        _, g = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=5, want_grad=True)
+    finally:
+        session.set_option("precision", eng.PREC_FP32)
+    want = O.COracle.core_phase(t, m.copy(), host.global_plan(t.nnz, 16, 1), 16, 1e-3, 1e-4)
+    tol = GRAD_TOL[eng.PREC_TF32]
+    assert np.isfinite(g).all()
+    np.testing.assert_allclose(g, want, rtol=tol, atol=tol * np.abs(want).max())
+
+
+@pytest.mark.parametrize("shape", MULTI, ids=_id)
+def test_factor_distinct_rows_many_tiles_per_cta(session, shape):
+    order, j, r = shape
+    n = 148 * 128 * 2 + 51
+    mult = (1, 7, 13, 17)[:order]
+    idx = np.stack([(np.arange(n) * p) % n for p in mult], 1).astype(np.int32)
+    vals = np.linspace(1, 5, n).astype(np.float32)
+    t = O.Tensor(np.array([n] * order, np.int32), idx, vals)
+    m = _model(t, j, r)
+    session.set_option("precision", eng.PREC_TF32)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.factor_phase(0, None, 16, 1e-2, 1e-3, HOG, seed=3)
+    finally:
+        session.set_option("precision", eng.PREC_FP32)
+    a, _ = session.download_model()
+    mc = m.copy()
+    O.COracle.factor_phase(t, mc, np.arange(n), 16, 1e-2, 1e-3)
+    tol = STEP_TOL[eng.PREC_TF32]
+    for k in range(order):
+        got, want = a[k] - m.a[k], mc.a[k] - m.a[k]
+        assert np.isfinite(got).all()
+        np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
