@@ -494,6 +494,318 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
   big_teardown<W, false>(tmem);
 }
 
+// ---- J = R = 128 factor sweep: K-split half jobs -------------------------------
+//
+// A whole-mode job (128 rows + a 64 KB B image) leaves room for one stage, so
+// every TMA, MMA and epilogue step would serialise.  Here each GEMM is split
+// along K into two half jobs of 64 KB (32 KB of rows or D' columns + 32 KB of
+// the B image), three in flight.  A U half job also re-gathers the live rows
+// of its column half, so the regulariser / overwrite term is read from shared
+// memory instead of through L2 in the epilogue; its stage is released by the
+// epilogue warps that read it, not by the MMA.
+
+namespace f128 {
+constexpr int W = 128;
+constexpr uint32_t kHalfX = kRows * 64 * 4;  // rows of a 64-column half: 32 KB
+constexpr uint32_t kHalfY = W * 64 * 4;      // B image half: 32 KB
+constexpr uint32_t kStage = kHalfX + kHalfY;
+constexpr int kS = 3, kI = 4;
+constexpr uint32_t o_st = 0;
+constexpr uint32_t kIdx = (kN + 1) * kRows * 4;
+constexpr uint32_t o_idx = o_st + kS * kStage;
+constexpr uint32_t o_rows = o_idx + kI * kIdx;
+constexpr uint32_t o_xp = o_rows + 16;
+constexpr uint32_t o_stage = o_xp + 2 * kRows * 4;  // per epilogue warp: 32 rows x 64 B
+constexpr uint32_t o_bar = o_stage + 8 * 2048;
+constexpr uint32_t o_tmem = o_bar + 24 * 8;
+constexpr uint32_t bytes = o_tmem + 16;
+static_assert(bytes <= 227 * 1024, "shared-memory budget");
+constexpr int kJobs = 4 * kN;  // per tile: C and U, two halves per mode
+enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 10, CFULL = 14, DFULL = 15, UFULL = 16, UEMPTY = 17 };
+constexpr uint32_t t_u = kN * W;
+// job index of the first job of tile k's U phase (C(0) comes first)
+__device__ __forceinline__ int64_t u_job(int64_t k) { return 2 * kN + k * kJobs; }
+}  // namespace f128
+
+__global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __grid_constant__ BigParams p) {
+  using namespace f128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + o_tmem);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&bars[FULL + s], 2);
+      mbar_init(&bars[EMPTY + s], 1);
+    }
+    for (int i = 0; i < kI; ++i) {
+      mbar_init(&bars[IFULL + i], 1);
+      mbar_init(&bars[IEMPTY + i], 1);
+    }
+    mbar_init(&bars[CFULL], 1);
+    mbar_init(&bars[DFULL], 1);
+    mbar_init(&bars[UFULL], 1);
+    mbar_init(&bars[UEMPTY], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
+  }
+  if (threadIdx.x / 32 == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto idx_of = [&](int64_t k) {
+    return reinterpret_cast<const int32_t*>(sm + o_idx + (k % kI) * kIdx);
+  };
+
+  if (warp == 0 || warp == 10) {
+    // two producers walk the same job sequence, each gathering half the rows;
+    // part 0 also fetches the COO records and the B image halves
+    const int part = warp == 0 ? 0 : 1;
+    int64_t job = 0;
+    constexpr int kAhead = 2;
+    auto request = [&](int64_t k) {
+      if (k >= nk || part != 0) return;
+      const int i = (int)(k % kI);
+      const int64_t tile = big_tile(p, k);
+      mbar_wait(&bars[IEMPTY + i], (uint32_t)(((k / kI) & 1) ^ 1));
+      int32_t* s_idx = reinterpret_cast<int32_t*>(sm + o_idx + i * kIdx);
+      if (elect_one()) {
+        reinterpret_cast<int32_t*>(sm + o_rows)[i] = __ldg(p.tile_rows + tile);
+        mbar_expect_tx(&bars[IFULL + i], kIdx);
+        for (int n = 0; n < kN; ++n)
+          bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[IFULL + i]);
+        bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[IFULL + i]);
+      }
+      __syncwarp();
+    };
+    // one half job: rows n, columns [64 hh, 64 hh + 64) + half hh of image img
+    auto half_job = [&](int64_t k, int n, int hh, const float* img) {
+      const int s = (int)(job % kS);
+      mbar_wait(&bars[EMPTY + s], (uint32_t)(((job / kS) & 1) ^ 1));
+      ++job;
+      uint8_t* st = sm + o_st + s * kStage;
+      if (elect_one()) {
+        mbar_expect_tx(&bars[FULL + s], kHalfX / 2 + (part == 0 ? kHalfY : 0));
+        const int32_t* s_idx = idx_of(k) + n * kRows;
+        constexpr int per = kRows / 4 / 2;
+#pragma unroll 1
+        for (int g0 = part * per; g0 < (part + 1) * per; g0 += 8) {
+          int4 r[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) r[g] = *reinterpret_cast<const int4*>(s_idx + (g0 + g) * 4);
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int cb = 0; cb < 2; ++cb)
+              tma_gather4(st + cb * kBlk + (g0 + g) * 512, &p.tmap[n], (hh * 2 + cb) * 32, r[g].x,
+                          r[g].y, r[g].z, r[g].w, &bars[FULL + s]);
+        }
+        if (part == 0) bulk_g2s(st + kHalfX, img + hh * (kHalfY / 4), kHalfY, &bars[FULL + s]);
+      }
+      __syncwarp();
+    };
+    if (nk > 0) {
+      for (int64_t k = 0; k < kAhead; ++k) request(k);
+      auto c_jobs = [&](int64_t k) {
+        request(k + kAhead);
+        mbar_wait(&bars[IFULL + (int)(k % kI)], (uint32_t)((k / kI) & 1));
+        for (int n = 0; n < kN; ++n)
+          for (int hh = 0; hh < 2; ++hh) half_job(k, n, hh, p.bt_img[n]);
+      };
+      c_jobs(0);
+      for (int64_t k = 0; k < nk; ++k) {
+        for (int n = 0; n < kN; ++n)
+          for (int hh = 0; hh < 2; ++hh) half_job(k, n, hh, p.b_img[n]);
+        if (k + 1 < nk) c_jobs(k + 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id = idesc_tf32(128, W, 0, 0);
+      int64_t job = 0;
+      auto wait_full = [&]() {
+        const int s = (int)(job % kS);
+        mbar_wait(&bars[FULL + s], (uint32_t)((job / kS) & 1));
+        tc_after();
+        ++job;
+        return s;
+      };
+      auto issue_c = [&]() {
+        for (int n = 0; n < kN; ++n)
+          for (int hh = 0; hh < 2; ++hh) {
+            const int s = wait_full();
+            const uint32_t a0 = smem_u32(sm + o_st + s * kStage), b0 = a0 + kHalfX;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              mma_ss(tmem + n * W, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
+                     sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id,
+                     (hh > 0 || ks > 0) ? 1u : 0u);
+            mma_commit(&bars[EMPTY + s]);
+          }
+        mma_commit(&bars[CFULL]);
+      };
+      if (nk > 0) issue_c();
+      for (int64_t k = 0; k < nk; ++k) {
+        mbar_wait(&bars[DFULL], (uint32_t)(k & 1));
+        for (int n = 0; n < kN; ++n) {
+          mbar_wait(&bars[UEMPTY], (uint32_t)(((k * kN + n) & 1) ^ 1));
+          for (int hh = 0; hh < 2; ++hh) {
+            const int s = wait_full();
+            const uint32_t b0 = smem_u32(sm + o_st + s * kStage) + kHalfX;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              mma_ts(tmem + t_u, tmem + n * W + (hh * 8 + ks) * 8,
+                     sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id,
+                     (hh > 0 || ks > 0) ? 1u : 0u);
+            // the stage is released by the epilogue (it reads the rows)
+          }
+          mma_commit(&bars[UFULL]);
+        }
+        if (k + 1 < nk) issue_c();  // C(k + 1) overwrites D'(k): behind U(k) in order
+      }
+    }
+  } else {
+    const int q = warp & 3, h = (warp - 2) >> 2, row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const float lr_reg = p.lr * p.reg;
+    constexpr int kHalf = W / 2;
+    float* xp = reinterpret_cast<float*>(sm + o_xp);
+    for (int64_t k = 0; k < nk; ++k) {
+      const int i = (int)(k % kI);
+      const int32_t* s_idx = idx_of(k);
+      mbar_wait(&bars[IFULL + i], (uint32_t)((k / kI) & 1));
+      mbar_wait(&bars[CFULL], (uint32_t)(k & 1));
+      tc_after();
+      float part = 0.0f;
+#pragma unroll 1
+      for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(tl + 0 * W + c * 16, v0);
+        tmem_ld16(tl + 1 * W + c * 16, v1);
+        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          part = fmaf(__uint_as_float(v0[e]), __uint_as_float(v1[e]) * __uint_as_float(v2[e]), part);
+      }
+      xp[h * kRows + row] = part;
+      named_bar(2 + q, 64);
+      const float xhat = part + xp[(h ^ 1) * kRows + row];
+      named_bar(2 + q, 64);
+      const bool ok = row < reinterpret_cast<const int32_t*>(sm + o_rows)[i];
+      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
+      const float sc = p.lr * resid;
+#pragma unroll 1
+      for (int c = h * kHalf / 16; c < (h + 1) * kHalf / 16; ++c) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(tl + 0 * W + c * 16, v0);
+        tmem_ld16(tl + 1 * W + c * 16, v1);
+        tmem_ld16(tl + 2 * W + c * 16, v2);
+        tmem_wait_ld();
+        uint32_t d0[16], d1[16], d2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float c0 = __uint_as_float(v0[e]) * sc, c1 = __uint_as_float(v1[e]),
+                      c2 = __uint_as_float(v2[e]);
+          d0[e] = rn_bits(c1 * sc * c2);
+          d1[e] = rn_bits(c0 * c2);
+          d2[e] = rn_bits(c0 * c1);
+        }
+        tmem_st16(tl + 0 * W + c * 16, d0);
+        tmem_st16(tl + 1 * W + c * 16, d1);
+        tmem_st16(tl + 2 * W + c * 16, d2);
+      }
+      tmem_wait_st();
+      tc_before();
+      named_bar(1, 256);
+      if (warp == 2 && lane == 0) mbar_arrive(&bars[DFULL]);
+      int32_t g[kN];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
+      for (int n = 0; n < kN; ++n) {
+        const int64_t u = k * kN + n;
+        // this warp's column half h came with U half job h of mode n
+        const int64_t job = u_job(k) + 2 * n + h;
+        const int s = (int)(job % kS);
+        mbar_wait(&bars[UFULL], (uint32_t)(u & 1));
+        mbar_wait(&bars[FULL + s], (uint32_t)((job / kS) & 1));  // rows visible to this thread
+        tc_after();
+        uint32_t v[kHalf];
+#pragma unroll
+        for (int c = 0; c < kHalf / 16; ++c) tmem_ld16(tl + t_u + h * kHalf + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
+        tmem_wait_ld();
+        const uint8_t* xs = sm + o_st + s * kStage;
+        float4 a4[kHalf / 4];
+#pragma unroll
+        for (int qq = 0; qq < kHalf / 4; ++qq)  // column 4 qq of the half: block qq / 8
+          a4[qq] = *reinterpret_cast<const float4*>(xs + (qq / 8) * kBlk + swz(row, (qq % 8) * 16, 128));
+        tc_before();
+        named_bar(6 + h, 128);  // the four warps of this half have read the stage
+        if (q == 0 && lane == 0) mbar_arrive(&bars[EMPTY + s]);
+        named_bar(1, 256);
+        if (warp == 2 && lane == 0) {
+          mbar_arrive(&bars[UEMPTY]);
+          if (n == kN - 1) mbar_arrive(&bars[IEMPTY + i]);
+        }
+        // write-back through a private 2 KB staging tile per warp: 16 columns
+        // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
+        uint8_t* stage = sm + o_stage + (warp - 2) * 2048;
+        int32_t gr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gr[i] = __shfl_sync(0xffffffffu, ok ? g[n] : -1, i * 8 + (lane >> 2));
+        float* dst = p.a[n] + h * kHalf + (lane & 3) * 4;
+#pragma unroll
+        for (int c = 0; c < kHalf / 16; ++c) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int qq = c * 4 + q4;
+            const float4 a = a4[qq];
+            float4 st;
+            st.x = __uint_as_float(v[qq * 4 + 0]) - lr_reg * a.x;
+            st.y = __uint_as_float(v[qq * 4 + 1]) - lr_reg * a.y;
+            st.z = __uint_as_float(v[qq * 4 + 2]) - lr_reg * a.z;
+            st.w = __uint_as_float(v[qq * 4 + 3]) - lr_reg * a.w;
+            if (!p.atomic_update) {
+              st.x += a.x;
+              st.y += a.y;
+              st.z += a.z;
+              st.w += a.w;
+            }
+            *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 sv =
+                *reinterpret_cast<const float4*>(stage + swz(i * 8 + (lane >> 2), (lane & 3) * 16, 64));
+            if (gr[i] >= 0) {
+              float* gp = dst + (size_t)gr[i] * W + c * 16;
+              if (p.atomic_update)
+                red_add_v4(gp, sv);
+              else
+                *reinterpret_cast<float4*>(gp) = sv;
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x / 32 == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_constant__ BigParams p) {
   using L = BigLayout<W, true>;
@@ -1285,8 +1597,9 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
   p.lr = lr;
   p.reg = reg;
   p.atomic_update = atomic_update;
-  const int bytes = (int)BigLayout<W, false>::bytes;
-  auto kern = big_factor_kernel<W>;
+  // W = 128: the K-split half-job sweep
+  const int bytes = W == 128 ? (int)f128::bytes : (int)BigLayout<W, false>::bytes;
+  auto kern = W == 128 ? big128_factor_kernel : big_factor_kernel<W>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   kern<<<(int)sweep_grid(v), kThreadsF, bytes, st>>>(p);
