@@ -59,7 +59,9 @@ struct BigLayout {
   static constexpr int kI = 4;  // COO-record ring depth
   static constexpr uint32_t o_rows = o_idx + kI * kIdx;
   static constexpr uint32_t o_xp = o_rows + 16;  // factor: x_hat halves [2][128]
-  static constexpr uint32_t o_bar = o_xp + 2 * kRows * 4;
+  // factor: per epilogue warp a 2 KB staging tile for the 64-B write-back
+  static constexpr uint32_t o_stage = o_xp + 2 * kRows * 4;
+  static constexpr uint32_t o_bar = o_stage + (kCore ? 0 : 8 * 2048);
   static constexpr uint32_t o_tmem = o_bar + 32 * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
   // TMEM: factor C/D [0, 3W) + U regions (one per mode at W = 64, so U_0..2
@@ -452,7 +454,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
                        : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
         tc_after();
-        {
+        // write-back through a private 2 KB staging tile per warp: 16 columns
+        // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
+        uint8_t* stage = sm + L::o_stage + (warp - 2) * 2048;
+        int32_t gr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gr[i] = __shfl_sync(0xffffffffu, ok ? g[n] : -1, i * 8 + (lane >> 2));
+        float* dsw = p.a[n] + h * kHalf + (lane & 3) * 4;
 #pragma unroll
         for (int c = 0; c < kHalf / 16; ++c) {
           uint32_t v[16];
@@ -460,7 +468,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           tmem_wait_ld();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const int col = c * 16 + q4 * 4;
             const float4 a = a4[c * 4 + q4];
             float4 st;  // kFold: U' already holds the regulariser
             const float rg = kFold ? 0.0f : lr_reg;
@@ -468,19 +475,28 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
             st.y = __uint_as_float(v[q4 * 4 + 1]) - rg * a.y;
             st.z = __uint_as_float(v[q4 * 4 + 2]) - rg * a.z;
             st.w = __uint_as_float(v[q4 * 4 + 3]) - rg * a.w;
-            if (ok) {
-              if (p.atomic_update) {
-                red_add_v4(dst + col, st);
-              } else {
-                st.x += a.x;
-                st.y += a.y;
-                st.z += a.z;
-                st.w += a.w;
-                *reinterpret_cast<float4*>(dst + col) = st;
-              }
+            if (!p.atomic_update) {
+              st.x += a.x;
+              st.y += a.y;
+              st.z += a.z;
+              st.w += a.w;
+            }
+            *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 sv =
+                *reinterpret_cast<const float4*>(stage + swz(i * 8 + (lane >> 2), (lane & 3) * 16, 64));
+            if (gr[i] >= 0) {
+              float* gp = dsw + (size_t)gr[i] * W + c * 16;
+              if (p.atomic_update)
+                red_add_v4(gp, sv);
+              else
+                *reinterpret_cast<float4*>(gp) = sv;
             }
           }
-        }
+          __syncwarp();
         }
         tc_before();
         named_bar(1, 256);
@@ -806,115 +822,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int W>
-__global__ void __launch_bounds__(kThreads, 1) big_core_kernel(const __grid_constant__ BigParams p) {
-  using L = BigLayout<W, true>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
-  big_setup<W, true>(sm, bars, tslot, p);
-  const uint32_t tmem = *tslot;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kG = L::t_g;
-  const int pm = p.pass;
-
-  if (warp == 0) {
-    big_producer<W, true>(p, sm, bars, nk);
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idg = idesc_tf32(128, W, 1, 1);
-      const uint32_t d0 = smem_u32(sm + L::o_d);
-      int64_t job = 0;
-      // order C(0), then per tile C(k + 1) (into the other buffer at W = 64)
-      // ahead of G(k), so the C GEMMs overlap the epilogue
-      auto c_of = [&](int64_t k) {
-        const int cb = (int)(k % L::kCB);
-        mbar_wait(&bars[B_CEMPTY + cb], (uint32_t)(((k / L::kCB) & 1) ^ 1));
-        issue_c<W, true>(sm, bars, tmem + cb * 3 * W, job, cb);
-      };
-      if (nk > 0) c_of(0);
-      for (int64_t k = 0; k < nk; ++k) {
-        if (k + 1 < nk) c_of(k + 1);
-        const int s = (int)(job % L::kStages);
-        mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
-        mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
-        tc_after();
-        // G[j][r] += sum_t A[t][j] D'[t][r]: M = 128 rows j (W real), N = W,
-        // K = 8 nonzeros per instruction; both operands MN-major.
-        const uint64_t da = sdesc_l(smem_u32(sm + L::o_st + s * L::kStage), kBlk, 512, 1);
-        const uint64_t dd = sdesc_l(d0, kBlk, 512, 1);
-#pragma unroll 4
-        for (int ks = 0; ks < kRows / 8; ++ks)
-          mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
-                 (k > 0 || ks > 0) ? 1u : 0u);
-        mma_commit(&bars[B_EMPTY + s]);
-        mma_commit(&bars[B_DEMPTY]);
-        ++job;
-      }
-    }
-  } else {
-    const int q = warp & 3, row = q * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    for (int64_t k = 0; k < nk; ++k) {
-      const int i = (int)(k % L::kI);
-      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdx);
-      mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
-      const int cb = (int)(k % L::kCB);
-      const uint32_t tc = tl + cb * 3 * W;
-      mbar_wait(&bars[B_CFULL + cb], (uint32_t)((k / L::kCB) & 1));
-      tc_after();
-      const float xhat = big_xhat<W>(tc);
-      const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[i];
-      const float resid = ok ? reinterpret_cast<const float*>(s_idx + kN * kRows)[row] - xhat : 0.0f;
-      mbar_wait(&bars[B_DEMPTY], (uint32_t)((k & 1) ^ 1));  // G(k-1) done with D'
-      const int m0 = pm == 0 ? 1 : 0, m1 = pm == 2 ? 1 : 2;
-#pragma unroll 1
-      for (int c = 0; c < W / 16; ++c) {
-        uint32_t v0[16], v1[16];
-        tmem_ld16(tc + m0 * W + c * 16, v0);
-        tmem_ld16(tc + m1 * W + c * 16, v1);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          float4 d;
-          const int e = q4 * 4;
-          d.x = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 0]) * __uint_as_float(v1[e + 0])));
-          d.y = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 1]) * __uint_as_float(v1[e + 1])));
-          d.z = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 2]) * __uint_as_float(v1[e + 2])));
-          d.w = __uint_as_float(rn_bits(resid * __uint_as_float(v0[e + 3]) * __uint_as_float(v1[e + 3])));
-          const int col = c * 16 + e;
-          *reinterpret_cast<float4*>(sm + L::o_d + (col / 32) * kBlk + swz32(row, (col % 32) * 4)) = d;
-        }
-      }
-      fence_proxy_async();
-      tc_before();
-      named_bar(1, 128);
-      if (warp == 2 && lane == 0) {
-        mbar_arrive(&bars[B_CEMPTY + cb]);
-        mbar_arrive(&bars[B_DFULL]);
-        mbar_arrive(&bars[B_IEMPTY + i]);
-      }
-    }
-    if (nk > 0) mbar_wait(&bars[B_DEMPTY], (uint32_t)((nk - 1) & 1));
-    tc_after();
-    // TMEM lane j (< W) holds G_pass[j][:]
-    float* out = p.partials + (size_t)blockIdx.x * (kN * W * W) + (size_t)pm * W * W;
-    if (row < W) {
-#pragma unroll 1
-      for (int c = 0; c < W / 16; ++c) {
-        uint32_t v[16];
-        tmem_ld16(tl + kG + c * 16, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          out[(size_t)row * W + c * 16 + e] = nk > 0 ? __uint_as_float(v[e]) : 0.0f;
-      }
-    }  // (warp-uniform: lanes W..127 of a W = 64 tile hold no gradient)
-  }
-  big_teardown<W, true>(tmem);
-}
 
 // B operand images, rounded to nearest tf32: bt (C GEMM: rows r, K = j) and
 // b (U GEMM: rows j, K = r), K-major SW128 in 32-column blocks.
@@ -929,15 +836,6 @@ __global__ void big_images_kernel(const float* __restrict__ b, float* __restrict
     *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(b_img) + (r / 32) * (W * 128) +
                               swz(j, (r % 32) * 4, 128)) = x;
   }
-}
-
-// Core sweep operand copy of A_n, rounded to nearest tf32: the tensor core
-// truncates fp32 operands, and a truncated A biases every C (and so every
-// residual of the core gradient) low by ~2^-12 relative.
-__global__ void big_round_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    dst[e] = __uint_as_float(rn_bits(src[e]));
 }
 
 __global__ void big_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
@@ -1598,52 +1496,21 @@ cudaError_t run_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t
   p.reg = reg;
   p.atomic_update = atomic_update;
   // W = 128: the K-split half-job sweep
-  const int bytes = W == 128 ? (int)f128::bytes : (int)BigLayout<W, false>::bytes;
-  auto kern = W == 128 ? big128_factor_kernel : big_factor_kernel<W>;
+  int bytes;
+  void (*kern)(BigParams);
+  if constexpr (W == 128) {
+    bytes = (int)f128::bytes;
+    kern = big128_factor_kernel;
+  } else {
+    bytes = (int)BigLayout<W, false>::bytes;
+    kern = big_factor_kernel<W>;
+  }
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   kern<<<(int)sweep_grid(v), kThreadsF, bytes, st>>>(p);
   return cudaGetLastError();
 }
 
-template <int W>
-cudaError_t run_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add, float* grad,
-                     float* scratch, size_t scratch_bytes, cudaStream_t st) {
-  const int grid = (int)(v.ntiles < num_sms() ? v.ntiles : num_sms());
-  const size_t len = (size_t)kN * W * W;
-  if (grid < 1) return cudaErrorInvalidValue;
-  if (scratch_bytes < big_scratch_bytes(v, dims, true)) return cudaErrorInvalidValue;
-  float* img = scratch + (size_t)num_sms() * len;
-  float* arn = img + 2 * kN * (size_t)W * W;
-  KView vr = v;
-  for (int n = 0; n < kN; ++n) {
-    const int64_t cnt = (int64_t)dims[n] * W;
-    int64_t blocks = (cnt + 255) / 256;
-    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-    big_round_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], arn, cnt);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    vr.a[n] = arn;
-    arn += cnt;
-  }
-  BigParams p{};
-  cudaError_t e = prepare<W>(p, vr, dims, mul, add, img, st);
-  if (e != cudaSuccess) return e;
-  p.partials = scratch;
-  const int bytes = (int)BigLayout<W, true>::bytes;
-  e = cudaFuncSetAttribute(big_core_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return e;
-  // one pass per mode: TMEM holds C of all modes plus one mode's gradient
-  for (int pass = 0; pass < kN; ++pass) {
-    p.pass = pass;
-    if (!big_row_map(&p.tmap_mn, vr.a[pass], dims[pass], W, true)) return cudaErrorNotSupported;
-    big_core_kernel<W><<<grid, kThreads, bytes, st>>>(p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  big_reduce_kernel<<<(int)((len + 255) / 256), 256, 0, st>>>(scratch, grid, (int)len, grad);
-  return cudaGetLastError();
-}
 
 }  // namespace
 
