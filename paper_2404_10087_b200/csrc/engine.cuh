@@ -51,6 +51,11 @@ struct DevTensor {
   int* d_bad = nullptr;
   cudaEvent_t ready = nullptr;
   bool pending = false;
+  // Recorded on the session stream when another slot's work begins: every
+  // kernel that read this slot precedes it, so an asynchronous re-upload
+  // waits for exactly that (and not for work on other slots).
+  cudaEvent_t used = nullptr;
+  bool used_rec = false;
 };
 
 struct DevModel {

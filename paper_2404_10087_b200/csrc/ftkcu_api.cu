@@ -20,6 +20,7 @@ struct ftkcu_session {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
   DevTensor slots[8];
+  int last_slot = -1;  // slot of the most recent phase / evaluation
   DevModel model;
   bool have_model = false;
   float* grad = nullptr;
@@ -133,6 +134,7 @@ void free_tensor(DevTensor& t) {
   if (t.staging) cudaFree(t.staging);
   if (t.d_bad) cudaFree(t.d_bad);
   if (t.ready) cudaEventDestroy(t.ready);
+  if (t.used) cudaEventDestroy(t.used);
   t = DevTensor{};
 }
 
@@ -225,6 +227,13 @@ int check_ready(ftkcu_session* s, int slot) {
   for (int n = 0; n < t.order; ++n)
     if (s->model.dims[n] < t.dims[n])
       return fail(s, FTKCU_ERR_ARG, "model dims too small for tensor");
+  if (s->last_slot >= 0 && s->last_slot != slot) {
+    DevTensor& p = s->slots[s->last_slot];
+    if (!p.used) CK(cudaEventCreateWithFlags(&p.used, cudaEventDisableTiming));
+    CK(cudaEventRecord(p.used, s->stream));
+    p.used_rec = true;
+  }
+  s->last_slot = slot;
   return FTKCU_OK;
 }
 
@@ -504,10 +513,16 @@ int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32
     if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
   DevTensor& t = s->slots[slot];
   if ((rc = finish_upload(s, t))) return rc;
-  // the copies overwrite the slot's buffers: order them after every kernel
-  // already enqueued on the session stream
-  CK(cudaEventRecord(s->ev1, s->stream));
-  CK(cudaStreamWaitEvent(s->copy_stream, s->ev1, 0));
+  // the copies overwrite the slot's buffers: order them after the kernels
+  // enqueued on the session stream that read this slot -- all of them if it
+  // is the slot in use, else those up to its last use (so a caller can
+  // enqueue slot k's epoch first and the copy into slot k + 1 still overlaps it)
+  if (slot == s->last_slot || (t.used_rec && !t.used)) {
+    CK(cudaEventRecord(s->ev1, s->stream));
+    CK(cudaStreamWaitEvent(s->copy_stream, s->ev1, 0));
+  } else if (t.used_rec) {
+    CK(cudaStreamWaitEvent(s->copy_stream, t.used, 0));
+  }
   if (!(t.vals && t.order == order && t.nnz == nnz)) {
     CK(cudaStreamSynchronize(s->stream));
     free_tensor(t);
@@ -541,6 +556,8 @@ int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32
   }
   aos_to_soa_kernel<<<num_sms() * 8, 256, 0, s->copy_stream>>>(t.staging, nnz, v, t.d_bad);
   CK(cudaGetLastError());
+  // the tile stream is built lazily on the session stream (prepare_stream), so
+  // the copy stream is free for the next upload as soon as this one is checked
   CK(cudaEventRecord(t.ready, s->copy_stream));
   t.pending = true;
   return FTKCU_OK;

@@ -363,6 +363,15 @@ size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm) {
   return grid * L.acc_floats * sizeof(float) * (1 + (L.acc_global ? warps : 0));
 }
 
+// Rows of each tile of a cell of n nonzeros: kHogTile, the last one the rest.
+__global__ void tile_rows_kernel(int32_t* __restrict__ rows, int64_t nt, int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < nt) {
+    const int64_t left = n - k * kHogTile;
+    rows[k] = (int32_t)(left < kHogTile ? left : kHogTile);
+  }
+}
+
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void*, size_t, cudaStream_t st) {
   // Cells: every cell is shuffled on its own and padded to whole tiles
@@ -396,14 +405,15 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
   }
   e = cudaMemsetAsync(t.svals, 0, sizeof(float) * kHogTile * tiles, st);
   if (e != cudaSuccess) return e;
-  std::vector<int32_t> rows(tiles > 0 ? tiles : 1);
   for (int c = 0; c < ncell; ++c) {
     const int64_t n = off[c + 1] - off[c];
-    for (int64_t k = ctile[c]; k < ctile[c + 1]; ++k) {
-      const int64_t left = n - (k - ctile[c]) * kHogTile;
-      rows[k] = (int32_t)(left < kHogTile ? left : kHogTile);
-    }
     if (n == 0) continue;
+    // rows per tile, written on the device: a host copy would queue behind
+    // any bulk upload in flight on the copy engine
+    const int64_t nt = ctile[c + 1] - ctile[c];
+    tile_rows_kernel<<<(int)((nt + 255) / 256), 256, 0, st>>>(t.tile_rows + ctile[c], nt, n);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     ShuffleView v{};
     v.order = t.order;
     for (int i = 0; i < t.order; ++i) {
@@ -420,13 +430,6 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     shuffle_kernel<<<(int)blocks, 256, 0, st>>>(v, d_perm, bits,
                                                  seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1)));
     e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  if (tiles > 0) {
-    e = cudaMemcpyAsync(t.tile_rows, rows.data(), sizeof(int32_t) * tiles, cudaMemcpyHostToDevice,
-                        st);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(st);  // `rows` is a host temporary
     if (e != cudaSuccess) return e;
   }
   t.cell_tile = ctile;

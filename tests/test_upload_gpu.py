@@ -56,3 +56,34 @@ def test_async_upload_bad_index_reported_at_first_use(session):
     session.upload_tensor_ptr_async(3, t.dims, t.nnz, ih.data_ptr(), vh.data_ptr())
     with pytest.raises(eng.FtkError, match="out of range"):
         session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
+
+
+def test_async_upload_into_idle_slot_while_other_slot_runs(session):
+    """The double-buffered e2e order: slot 3's epoch is enqueued, then the
+    next data is uploaded asynchronously into slot 2 (last read by an earlier
+    epoch) without a host sync.  The copy waits only for slot 2's last use;
+    slot 3's epoch and the following slot-2 epoch must both be bit-identical
+    to the same sequence with synchronous uploads."""
+    t1, ranks, r, a, b = _problem()
+    t2 = O.random_tensor([50, 40, 30], 5000, 12, 1.0, 5.0)
+    p = [host.global_plan(t1.nnz, 16, s) for s in (3, 4, 5, 6)]
+    out = []
+    for asynchronous in (False, True):
+        session.upload_model(t1.dims, ranks, r, a, b)
+        session.upload_tensor(2, t1.dims, t1.idx, t1.vals)
+        session.upload_tensor(3, t1.dims, t1.idx, t1.vals)
+        session.factor_phase(2, p[0], 16, 1e-3, 1e-4, DET)
+        session.factor_phase(3, p[1], 16, 1e-3, 1e-4, DET)
+        session.core_phase(3, p[2], 16, 1e-3, 1e-4, DET)
+        if asynchronous:
+            ih, vh = _pinned(t2.idx), _pinned(t2.vals)
+            session.upload_tensor_ptr_async(2, t2.dims, t2.nnz, ih.data_ptr(), vh.data_ptr())
+        else:
+            session.upload_tensor(2, t2.dims, t2.idx, t2.vals)
+        session.factor_phase(2, p[3], 16, 1e-3, 1e-4, DET)
+        out.append(session.download_model())
+        session.release_tensor(2)
+        session.release_tensor(3)
+    for n in range(3):
+        assert np.array_equal(out[0][0][n], out[1][0][n])
+        assert np.array_equal(out[0][1][n], out[1][1][n])
