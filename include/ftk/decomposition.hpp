@@ -38,8 +38,16 @@ struct EpochStats {
 EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
                       const EpochOptions& opts, std::uint64_t seed);
 
+// The FastTucker baseline (decomposition.hpp:194-199 of the reference):
+// factor blocks over per-bucket plans of the fixed-mode indices, then core
+// blocks with B^(n) moving every batch.  Runs on the device in the
+// workers == 1 arithmetic (bit-identical to the reference with workers = 1).
+EpochStats epoch_fasttucker(const SparseTensor& t, const std::vector<ModeIndex>& fixed_mode,
+                            Model& m, const Hyperparams& h, const EpochOptions& opts,
+                            std::uint64_t seed);
+
 struct TrainOptions {
-  Variant variant = Variant::kPlus;  // only kPlus is implemented
+  Variant variant = Variant::kPlus;  // kPlus or kFastTucker (kFasterTucker: not built)
   bool store_c = false;
   int workers = 1;
   std::uint64_t seed = 0;

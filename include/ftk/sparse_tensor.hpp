@@ -3,8 +3,7 @@
 // sparse_tensor.hpp:14-121).
 //
 // The per-mode bucket samplers (Keying / ModeIndex / EpochPlan::per_bucket)
-// only serve the convex FastTucker / FasterTucker baselines, which are out of
-// the engine's scope and are not declared here.
+// serve the convex FastTucker baseline.
 #pragma once
 
 #include <span>
@@ -75,6 +74,27 @@ struct BatchDesc {
   size64 bucket = -1;
 };
 
+// Entry positions grouped into buckets for one mode (sparse_tensor.hpp:50-72
+// of the reference): kFixedMode buckets share the mode-n index,
+// kFixedComplement buckets share every other index.  Positions inside a
+// bucket stay in storage order; buckets are in key order.
+enum class Keying { kFixedMode, kFixedComplement };
+
+struct ModeIndex {
+  int mode = 0;
+  Keying keying = Keying::kFixedMode;
+  std::vector<size64> positions;
+  std::vector<size64> offsets;  // bucket b spans [offsets[b], offsets[b+1])
+
+  size64 buckets() const { return static_cast<size64>(offsets.size()) - 1; }
+  std::span<const size64> bucket(size64 b) const {
+    return {positions.data() + offsets[b], static_cast<std::size_t>(offsets[b + 1] - offsets[b])};
+  }
+  size64 representative(size64 b) const { return positions[offsets[b]]; }
+};
+
+ModeIndex build_mode_index(const SparseTensor& t, int mode, Keying keying);
+
 // The FastTuckerPlus (global) sampler: a uniform permutation of all entries
 // cut into batches of m, the last one short.  Bit-identical to the
 // reference's plans for the same Rng state (same libstdc++ std::shuffle).
@@ -82,6 +102,9 @@ class EpochPlan {
  public:
   static EpochPlan global(const SparseTensor& t, index_t m, Rng& rng);
   static EpochPlan canonical(const SparseTensor& t);  // storage order, m = 1
+  // Bucket order shuffled, then each bucket's entries, cut into batches of m
+  // that never cross a bucket (the FastTucker / FasterTucker samplers).
+  static EpochPlan per_bucket(const SparseTensor& t, const ModeIndex& idx, index_t m, Rng& rng);
 
   size64 batches() const { return static_cast<size64>(descs_.size()); }
   const BatchDesc& desc(size64 b) const { return descs_[b]; }
@@ -90,11 +113,15 @@ class EpochPlan {
   // Engine additions: the flat permutation handed to the device sweeps.
   const std::vector<size64>& positions() const { return perm_; }
   index_t batch_size() const { return m_; }
+  // per_bucket plans: offsets of the buckets (in plan order) in positions(),
+  // with a final nnz; empty for global / canonical plans.
+  const std::vector<size64>& bucket_offsets() const { return boff_; }
 
  private:
   index_t m_ = 0;
   std::vector<size64> perm_;
   std::vector<BatchDesc> descs_;
+  std::vector<size64> boff_;
 };
 
 }  // namespace ftk

@@ -138,6 +138,24 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm,
                      int32_t M, float lr_b, float reg_b, int mode,
                      uint64_t seed, float* grad_out, double* ms);
 
+/* ---- FastTucker baseline --------------------------
+ * ftk::epoch_fasttucker (decomposition.cpp:707-770) one block at a time, in
+ * the reference's workers == 1 arithmetic (bit-identical models).
+ *
+ * Factor block of `mode`: perm = EpochPlan::per_bucket(fixed-mode index)
+ * positions (nnz entries, plan order), bucket_off = the nbuckets + 1 offsets
+ * of its buckets in perm (bucket_off[0] = 0, bucket_off[nbuckets] = nnz);
+ * batches are cut from each bucket in M-entry chunks.  Replaces the
+ * parallel_for over update_factor_fasttucker_impl (decomposition.cpp:729-742,
+ * 316-371).  Core block of `mode`: perm = the global plan;
+ * update_core_fasttucker_impl per batch (:752-766, 373-417), B^(mode)
+ * updated in place after every batch.  ms: device time of the block. */
+int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                            const int64_t* bucket_off, int64_t nbuckets, int32_t M, float lr_a,
+                            float reg_a, double* ms);
+int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm, int32_t M,
+                          float lr_b, float reg_b, double* ms);
+
 /* DSGD strata support.  Declares that the uploaded entries are sorted into
  * cells: entries [cell_offsets[c], cell_offsets[c+1]) form cell c.  The
  * Hogwild stream then shuffles and tiles every cell separately. */

@@ -128,6 +128,12 @@ class _COracle:
                                       _f32p, _i64p, C.c_int, C.c_float, C.c_float]
         L.fo_core_phase.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
                                     _f32p, _i64p, C.c_int, C.c_float, C.c_float, _f32p, C.c_int]
+        L.fo_fasttucker_factor_block.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, _i32p,
+                                                 _f32p, _i64p, _i64p, C.c_int64, C.c_int,
+                                                 C.c_int, C.c_float, C.c_float]
+        L.fo_fasttucker_core_block.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, C.c_int64,
+                                               _i32p, _f32p, _i64p, C.c_int, C.c_int, C.c_float,
+                                               C.c_float]
         L.fo_predict.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, _i32p]
         L.fo_predict.restype = C.c_double
         L.fo_loss.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
@@ -146,6 +152,24 @@ class _COracle:
         rc = self.lib.fo_factor_phase(m.order, _p(m.ranks, _i32p), m.r, _ptr_array(m.a),
                                       _ptr_array(m.b), t.nnz, _p(t.idx, _i32p),
                                       _p(t.vals, _f32p), _p(perm, _i64p), cap, lr_a, reg_a)
+        assert rc == 0
+
+    def fasttucker_factor_block(self, t: Tensor, m: Model, perm, boff, cap, mode, lr_a, reg_a):
+        """FastTucker factor block of `mode` over a per-bucket plan (in place)."""
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        boff = np.ascontiguousarray(boff, dtype=np.int64)
+        rc = self.lib.fo_fasttucker_factor_block(
+            m.order, _p(m.ranks, _i32p), m.r, _ptr_array(m.a), _ptr_array(m.b),
+            _p(t.idx, _i32p), _p(t.vals, _f32p), _p(perm, _i64p), _p(boff, _i64p),
+            boff.size - 1, cap, mode, lr_a, reg_a)
+        assert rc == 0
+
+    def fasttucker_core_block(self, t: Tensor, m: Model, perm, cap, mode, lr_b, reg_b):
+        """FastTucker core block of `mode` over a global plan (in place)."""
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        rc = self.lib.fo_fasttucker_core_block(
+            m.order, _p(m.ranks, _i32p), m.r, _ptr_array(m.a), _ptr_array(m.b), t.nnz,
+            _p(t.idx, _i32p), _p(t.vals, _f32p), _p(perm, _i64p), cap, mode, lr_b, reg_b)
         assert rc == 0
 
     def core_phase(self, t: Tensor, m: Model, perm, cap, lr_b, reg_b, store_c=False):
@@ -247,6 +271,11 @@ class _Ref:
         L.ref_batch_probe.argtypes = [C.c_void_p, C.c_void_p, _i64p, C.c_int, C.c_int, C.c_float,
                                       C.c_float] + [_f32p] * 9
         L.ref_predicted_costs.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _i64p]
+        L.ref_per_bucket_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                          _i64p, _i64p, _i64p]
+        L.ref_epoch_fasttucker.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float,
+                                           C.c_float, C.c_float, C.c_int, C.c_int, C.c_int,
+                                           C.c_uint64, _f64p, _i64p]
 
     def _check(self, rc):
         if rc != 0:
@@ -333,6 +362,35 @@ class _Ref:
                                                 workers, int(store_c), seed, _p(secs, _f64p),
                                                 _p(cnt, _i64p)))
             return self.model_to_np(mh, m), secs, cnt
+        finally:
+            self.free_tensor(th)
+            self.free_model(mh)
+
+    def per_bucket_plan(self, t: Tensor, mode, m, seed, keying=0):
+        """EpochPlan::per_bucket positions and bucket offsets (plan order)."""
+        th = self.tensor(t)
+        perm = np.zeros(t.nnz, np.int64)
+        boff = np.zeros(t.nnz + 2, np.int64)
+        nb = np.zeros(1, np.int64)
+        try:
+            self._check(self.lib.ref_per_bucket_plan(th, mode, keying, m, seed, _p(perm, _i64p),
+                                                     _p(boff, _i64p), _p(nb, _i64p)))
+            return perm, boff[: int(nb[0]) + 1].copy()
+        finally:
+            self.free_tensor(th)
+
+    def epoch_fasttucker(self, t: Tensor, m: Model, seed, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
+                         reg_b=1e-4, batch=16, workers=1, canonical=False):
+        """Runs ftkref::epoch_fasttucker (fixed-mode indices); returns (new model,
+        counters[10])."""
+        th, mh = self.tensor(t), self.model(m)
+        secs = np.zeros(2, np.float64)
+        cnt = np.zeros(10, np.int64)
+        try:
+            self._check(self.lib.ref_epoch_fasttucker(th, mh, lr_a, lr_b, reg_a, reg_b, batch,
+                                                      workers, int(canonical), seed,
+                                                      _p(secs, _f64p), _p(cnt, _i64p)))
+            return self.model_to_np(mh, m), cnt
         finally:
             self.free_tensor(th)
             self.free_model(mh)

@@ -371,6 +371,137 @@ int fo_core_phase(int order, const int32_t* ranks, int r, float* const* amat,
 }
 
 /* ------------------------------------------------------------------------ */
+/* FastTucker baseline (decomposition.cpp:707-770), workers = 1.            */
+
+/* Rows of every mode except `skip` staged (zero padding), C = A_psi B from
+ * the padded snapshot (stage_factor_rows_impl / compute_c_batch_impl with a
+ * skip mode, decomposition.cpp:170-196), and D of `mode` alone
+ * (compute_d_single_impl, :214-224). */
+static void ft_stage_cd(fo_ws* w, float* const* amat, const int32_t* idx, int m_eff,
+                        int skip, int mode) {
+  for (int n = 0; n < w->order; ++n) {
+    memset(w->a[n], 0, sizeof(float) * w->capp * w->jp[n]);
+    for (int m = 0; m < m_eff; ++m) {
+      const float* row = amat[n] + (size_t)idx[n * w->cap + m] * w->j[n];
+      for (int j = 0; j < w->j[n]; ++j) w->a[n][m * w->jp[n] + j] = row[j];
+    }
+    if (n == mode && skip == mode) continue;
+    if (n != mode) mm(w->a[n], w->bp[n], w->c[n], w->capp, w->jp[n], w->rp);
+  }
+  int first = (mode == 0) ? 1 : 0;
+  memcpy(w->d[mode], w->c[first], sizeof(float) * w->capp * w->rp);
+  for (int n = first + 1; n < w->order; ++n) {
+    if (n == mode) continue;
+    for (int i = 0; i < w->capp * w->rp; ++i) w->d[mode][i] = w->d[mode][i] * w->c[n][i];
+  }
+}
+
+/* Factor block of `mode` over a per-bucket plan: bucket b's entries are
+ * perm[boff[b] .. boff[b+1]), cut into batches of cap; each batch moves the
+ * bucket's shared row by the 1/M-mean gradient (update_factor_fasttucker_impl,
+ * :316-371). */
+int fo_fasttucker_factor_block(int order, const int32_t* ranks, int r, float* const* amat,
+                               float* const* bmat, const int32_t* idx_aos, const float* vals,
+                               const int64_t* perm, const int64_t* boff, int64_t nb, int cap,
+                               int mode, float lr_a, float reg_a) {
+  fo_ws w;
+  if (order < 2 || ws_init(&w, order, ranks, r, cap)) return 1;
+  int32_t* idx = malloc(sizeof(int32_t) * order * cap);
+  float* x = malloc(sizeof(float) * cap);
+  const int jn = ranks[mode];
+  float* snap = malloc(sizeof(float) * jn);
+  float* cs = malloc(sizeof(float) * r);
+  ws_snapshot_b(&w, bmat);
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t off = boff[b]; off < boff[b + 1]; off += cap) {
+      int m_eff = (int)((boff[b + 1] - off) < cap ? (boff[b + 1] - off) : cap);
+      gather_batch(order, idx_aos, vals, perm + off, m_eff, cap, idx, x);
+      const int32_t row = idx[mode * cap];
+      ft_stage_cd(&w, amat, idx, m_eff, mode, mode);
+      mm(w.d[mode], w.btp[mode], w.u[mode], w.capp, w.rp, w.jp[mode]);
+      float* dst = amat[mode] + (size_t)row * jn;
+      for (int j = 0; j < jn; ++j) snap[j] = dst[j];
+      for (int c = 0; c < r; ++c) { /* c = a B^(n), unpadded j */
+        float acc = 0.0f;
+        for (int j = 0; j < jn; ++j) {
+          float p = snap[j] * bmat[mode][(size_t)j * r + c];
+          acc = acc + p;
+        }
+        cs[c] = acc;
+      }
+      for (int m = 0; m < m_eff; ++m) { /* x_hat = c . d_m, unpadded R */
+        float acc = 0.0f;
+        for (int c = 0; c < r; ++c) {
+          float p = cs[c] * w.d[mode][m * w.rp + c];
+          acc = acc + p;
+        }
+        w.resid[m] = x[m] - acc;
+      }
+      const float inv = 1.0f / (float)m_eff;
+      for (int j = 0; j < jn; ++j) {
+        float g = 0.0f;
+        for (int m = 0; m < m_eff; ++m) {
+          float p = w.resid[m] * w.u[mode][m * w.jp[mode] + j];
+          g = g + p;
+        }
+        float gi = g * inv;
+        float rg = reg_a * snap[j];
+        float step = lr_a * (gi - rg);
+        dst[j] = snap[j] + step;
+      }
+    }
+  free(idx); free(x); free(snap); free(cs);
+  ws_free(&w);
+  return 0;
+}
+
+/* Core block of `mode` over a global plan: C of the other modes from the
+ * block-entry snapshot, C^(n) from the current B^(n), C-side residual,
+ * G = (r (x) A_psi)^T D over the padded batch, and B^(n) moves after every
+ * batch (update_core_fasttucker_impl, :373-417). */
+int fo_fasttucker_core_block(int order, const int32_t* ranks, int r, float* const* amat,
+                             float* const* bmat, int64_t nnz, const int32_t* idx_aos,
+                             const float* vals, const int64_t* perm, int cap, int mode,
+                             float lr_b, float reg_b) {
+  fo_ws w;
+  if (order < 2 || ws_init(&w, order, ranks, r, cap)) return 1;
+  int32_t* idx = malloc(sizeof(int32_t) * order * cap);
+  float* x = malloc(sizeof(float) * cap);
+  const int jn = ranks[mode];
+  ws_snapshot_b(&w, bmat);
+  for (int64_t off = 0; off < nnz; off += cap) {
+    int m_eff = (int)((nnz - off) < cap ? (nnz - off) : cap);
+    gather_batch(order, idx_aos, vals, perm + off, m_eff, cap, idx, x);
+    ft_stage_cd(&w, amat, idx, m_eff, -1, mode);
+    /* the current B^(n), padded */
+    memset(w.bp[mode], 0, sizeof(float) * w.jp[mode] * w.rp);
+    for (int j = 0; j < jn; ++j)
+      for (int c = 0; c < r; ++c) w.bp[mode][j * w.rp + c] = bmat[mode][(size_t)j * r + c];
+    mm(w.a[mode], w.bp[mode], w.c[mode], w.capp, w.jp[mode], w.rp);
+    fo_predict_rows(&w, x, w.c[mode], w.d[mode], w.rp, m_eff);
+    const float inv = 1.0f / (float)m_eff;
+    for (int j = 0; j < jn; ++j)
+      for (int c = 0; c < r; ++c) {
+        float g = 0.0f;
+        for (int m = 0; m < w.capp; ++m) {
+          float rm = (m < w.cap) ? w.resid[m] : 0.0f;
+          float e = rm * w.a[mode][m * w.jp[mode] + j];
+          float p = e * w.d[mode][m * w.rp + c];
+          g = g + p;
+        }
+        float* bb = bmat[mode] + (size_t)j * r + c;
+        float gi = g * inv;
+        float rb = reg_b * *bb;
+        float step = lr_b * (gi - rb);
+        *bb = *bb + step;
+      }
+  }
+  free(idx); free(x);
+  ws_free(&w);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* fp64 evaluation (model.cpp:70-92, evaluation.cpp:10-72).                 */
 
 double fo_predict(int order, const int32_t* ranks, int r, float* const* amat,

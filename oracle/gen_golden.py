@@ -77,12 +77,43 @@ def storec(R):
                             counters=cnt, hp=np.array(list(hp.values()), np.float32))
 
 
+# FastTucker baseline (§8 f4): (name, dims, nnz, ranks, R, cap, seed, canonical)
+FASTTUCKER = [
+    ("fasttucker_j16", [30, 20, 10], 1000, [16, 16, 16], 16, 16, 1234, False),
+    ("fasttucker_ragged", [30, 20, 10], 1000, [5, 4, 3], 4, 16, 99, False),
+    ("fasttucker_cap5", [30, 20, 10], 1000, [8, 12, 4], 6, 5, 7, False),
+    ("fasttucker_order4", [9, 8, 7, 6], 800, [8, 4, 8, 4], 8, 9, 5, False),
+    ("fasttucker_canonical", [20, 15, 10], 500, [8, 8, 8], 8, 16, 3, True),
+]
+
+
+def fasttucker(R):
+    for k, (name, dims, nnz, ranks, r, cap, seed, canon) in enumerate(FASTTUCKER):
+        t = O.random_tensor(dims, nnz, 800 + k, 1.0, 5.0)
+        m = O.random_model(dims, ranks, r, 900 + k, 0.3)
+        hp = dict(lr_a=1e-2, lr_b=1e-2, reg_a=1e-3, reg_b=1e-3)
+        new, cnt = R.epoch_fasttucker(t, m, seed, batch=cap, workers=1, canonical=canon, **hp)
+        plans = {}
+        for n in range(t.order):  # the reference's own sampler streams
+            perm, boff = R.per_bucket_plan(t, n, cap, derive_seed(seed, [1, n]))
+            plans[f"fplan{n}"], plans[f"fboff{n}"] = perm, boff
+            plans[f"cplan{n}"] = R.global_plan(t.nnz, cap, derive_seed(seed, [2, n]))
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **tensor_fields(t),
+                            **model_fields(m, "m_"), **model_fields(new, "new_"),
+                            cap=np.int32(cap), seed=np.uint64(seed), canonical=np.int32(canon),
+                            counters=cnt, hp=np.array(list(hp.values()), np.float32), **plans)
+
+
 def main():
     R = O.REF
     if R is None:
         raise SystemExit("oracle/_ref/libftkref.so missing: run make -C oracle first")
     os.makedirs(OUT, exist_ok=True)
+    if "--fasttucker-only" in sys.argv:
+        fasttucker(R)
+        return
     storec(R)
+    fasttucker(R)
     if "--storec-only" in sys.argv:
         return
     lr_a, reg_a = 0.05, 0.01

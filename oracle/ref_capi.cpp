@@ -142,6 +142,40 @@ int ref_global_plan(int64_t nnz, int m, uint64_t seed, int64_t* perm_out) {
   });
 }
 
+// EpochPlan::per_bucket over build_mode_index(t, mode, keying) for Rng(seed)
+// (sparse_tensor.cpp:200-240, 284-308): the visited positions in batch order
+// and the offsets of the buckets in that order (a bucket's batches are
+// consecutive; recovered from Batch::bucket), through a position tensor as
+// in ref_global_plan.
+int ref_per_bucket_plan(void* tp, int mode, int keying, int m, uint64_t seed, int64_t* perm_out,
+                        int64_t* boff_out, int64_t* nb_out) {
+  return guarded([&] {
+    const auto& t = *static_cast<ftkref::SparseTensor*>(tp);
+    const auto idx = ftkref::build_mode_index(
+        t, mode, keying ? ftkref::Keying::kFixedComplement : ftkref::Keying::kFixedMode);
+    ftkref::SparseTensor pos;
+    pos.order = 1;
+    pos.dims = {static_cast<int32_t>(t.nnz())};
+    pos.indices.resize(t.nnz());
+    pos.values.assign(t.nnz(), 0.0f);
+    for (int64_t i = 0; i < t.nnz(); ++i) pos.indices[i] = static_cast<int32_t>(i);
+    ftkref::Rng rng(seed);
+    ftkref::EpochPlan plan = ftkref::EpochPlan::per_bucket(pos, idx, m, rng);
+    ftkref::Batch b;
+    int64_t k = 0, nb = 0, last = -1;
+    for (int64_t bi = 0; bi < plan.batches(); ++bi) {
+      plan.gather(pos, bi, b);
+      if (static_cast<int64_t>(b.bucket) != last) {
+        boff_out[nb++] = k;
+        last = static_cast<int64_t>(b.bucket);
+      }
+      for (int r = 0; r < b.m_eff; ++r) perm_out[k++] = b.idx[0][r];
+    }
+    boff_out[nb] = k;
+    *nb_out = nb;
+  });
+}
+
 // ---- models ----------------------------------------------------------------
 
 void* ref_model_new(int order, const int32_t* dims, const int32_t* ranks,
@@ -214,6 +248,34 @@ int ref_epoch_plus(void* t, void* m, float lr_a, float lr_b, float reg_a,
         for (int s = 0; s < ftkref::kStages; ++s)
           counters_out[p * ftkref::kStages + s] =
               cs[p]->total(static_cast<ftkref::Stage>(s));
+    }
+  });
+}
+
+// ftkref::epoch_fasttucker with fixed-mode indices of every mode
+// (decomposition.cpp:707-770).
+int ref_epoch_fasttucker(void* t, void* m, float lr_a, float lr_b, float reg_a, float reg_b,
+                         int batch, int workers, int canonical, uint64_t seed, double* seconds2,
+                         int64_t* counters_out) {
+  return guarded([&] {
+    const auto& ts = *static_cast<ftkref::SparseTensor*>(t);
+    std::vector<ftkref::ModeIndex> fixed;
+    for (int n = 0; n < ts.order; ++n)
+      fixed.push_back(ftkref::build_mode_index(ts, n, ftkref::Keying::kFixedMode));
+    ftkref::EpochOptions eo;
+    eo.workers = workers;
+    eo.canonical_order = canonical != 0;
+    auto st = ftkref::epoch_fasttucker(ts, fixed, *static_cast<ftkref::Model*>(m),
+                                       hyper(lr_a, lr_b, reg_a, reg_b, 1, batch), eo, seed);
+    if (seconds2) {
+      seconds2[0] = st.seconds_factor;
+      seconds2[1] = st.seconds_core;
+    }
+    if (counters_out) {
+      const ftkref::CostCounters* cs[2] = {&st.factor, &st.core};
+      for (int p = 0; p < 2; ++p)
+        for (int s = 0; s < ftkref::kStages; ++s)
+          counters_out[p * ftkref::kStages + s] = cs[p]->total(static_cast<ftkref::Stage>(s));
     }
   });
 }

@@ -40,7 +40,8 @@ EXPORTS = (
     "ftkcu_batch_probe", "ftkcu_comm_unique_id", "ftkcu_comm_init",
     "ftkcu_comm_allreduce_grad", "ftkcu_tensor_set_cells", "ftkcu_factor_phase_cell",
     "ftkcu_comm_sendrecv_rows", "ftkcu_comm_bcast_rows", "ftkcu_comm_allreduce_f64",
-    "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch",
+    "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch", "ftkcu_fasttucker_factor",
+    "ftkcu_fasttucker_core",
 )
 
 
@@ -76,6 +77,10 @@ def load_library(path: str = LIB_PATH):
                                       _f32p]
     L.ftkcu_tensor_upload_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, C.c_int64,
                                             _i32p, _f32p]
+    L.ftkcu_fasttucker_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p, C.c_int64,
+                                          C.c_int32, C.c_float, C.c_float, _f64p]
+    L.ftkcu_fasttucker_core.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, C.c_int32,
+                                        C.c_float, C.c_float, _f64p]
     L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.restype = C.c_int64
@@ -230,6 +235,26 @@ class Session:
                                            C.c_uint64(seed & (2**64 - 1)), _p(g, _f32p),
                                            C.byref(ms) if timed else None))
         return (ms.value, g) if want_grad else ms.value
+
+    def fasttucker_factor(self, slot, mode, perm, bucket_off, M=16, lr_a=1e-3, reg_a=1e-4,
+                          timed=True):
+        """FastTucker factor block of `mode` over a per-bucket plan
+        (ftkcu_fasttucker_factor)."""
+        pa = np.ascontiguousarray(perm, np.int64)
+        bo = np.ascontiguousarray(bucket_off, np.int64)
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_fasttucker_factor(self.h, slot, mode, _p(pa, _i64p), _p(bo, _i64p),
+                                                  bo.size - 1, M, lr_a, reg_a,
+                                                  C.byref(ms) if timed else None))
+        return ms.value
+
+    def fasttucker_core(self, slot, mode, perm, M=16, lr_b=1e-3, reg_b=1e-4, timed=True):
+        """FastTucker core block of `mode` over a global plan (ftkcu_fasttucker_core)."""
+        pa = np.ascontiguousarray(perm, np.int64)
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_fasttucker_core(self.h, slot, mode, _p(pa, _i64p), M, lr_b,
+                                                reg_b, C.byref(ms) if timed else None))
+        return ms.value
 
     def eval(self, slot=1, workers=1, reg_a=0.0, reg_b=0.0):
         out = np.zeros(3, np.float64)

@@ -140,6 +140,18 @@ cudaError_t launch_det_core(const KView& v, const int64_t* perm, int cap,
 cudaError_t launch_apply_core(const KView& v, float* grad, float lr_b,
                               float reg_b, cudaStream_t st);
 
+// ---- FastTucker baseline (ft_kernels.cu) -----------
+// Factor block of `mode`: perm holds the per-bucket plan's positions, boff
+// the nbuckets + 1 bucket offsets into it (plan order); one warp per bucket.
+size_t ft_factor_smem(const KView& v, int cap, int mode);
+cudaError_t launch_ft_factor(const KView& v, int mode, const int64_t* perm, const int64_t* boff,
+                             int64_t nbuckets, int cap, float lr_a, float reg_a, cudaStream_t st);
+// Core block of `mode`: the global plan's batches in order, B^(mode) updated
+// after every batch.
+size_t ft_core_smem(const KView& v, int cap);
+cudaError_t launch_ft_core(const KView& v, int mode, const int64_t* perm, int cap, float lr_b,
+                           float reg_b, cudaStream_t st);
+
 // ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
                               float lr_a, float reg_a, int blocks_per_sm, int atomic_update,

@@ -29,6 +29,8 @@ struct ftkcu_session {
   size_t scratch_bytes = 0;
   int64_t* d_perm = nullptr;
   size_t perm_cap = 0;
+  int64_t* d_boff = nullptr;  // FastTucker bucket offsets
+  size_t boff_cap = 0;
   int64_t opt_precision = FTKCU_PREC_FP32;
   int64_t opt_eval = FTKCU_EVAL_EXACT;
   int64_t opt_hog_bps = 2;
@@ -357,6 +359,7 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   if (s->grad) cudaFree(s->grad);
   if (s->scratch) cudaFree(s->scratch);
   if (s->d_perm) cudaFree(s->d_perm);
+  if (s->d_boff) cudaFree(s->d_boff);
   if (s->d_cellperm) cudaFree(s->d_cellperm);
   if (s->dsgd_exec) cudaGraphExecDestroy(s->dsgd_exec);
   if (s->comm) ncclCommDestroy(s->comm);
@@ -723,6 +726,58 @@ int ftkcu_factor_phase_cell(ftkcu_session* s, int slot, int cell, float lr_a, fl
                             uint64_t seed, double* ms) {
   if (cell < 0) return fail(s, FTKCU_ERR_ARG, "cell must be >= 0");
   return factor_phase_impl(s, slot, nullptr, 16, lr_a, reg_a, FTKCU_MODE_HOGWILD, seed, cell, ms);
+}
+
+// ---- FastTucker baseline (epoch_fasttucker, decomposition.cpp:707-770) ----
+
+int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                            const int64_t* bucket_off, int64_t nbuckets, int32_t M, float lr_a,
+                            float reg_a, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  DevTensor& t = s->slots[slot];
+  if (M < 1) return fail(s, FTKCU_ERR_ARG, "batch size must be positive");
+  if (mode < 0 || mode >= t.order) return fail(s, FTKCU_ERR_ARG, "mode %d out of range", mode);
+  if (nbuckets < 0 || (t.nnz > 0 && (!perm || !bucket_off)))
+    return fail(s, FTKCU_ERR_ARG, "per-bucket plan missing");
+  if (nbuckets > 0 && (bucket_off[0] != 0 || bucket_off[nbuckets] != t.nnz))
+    return fail(s, FTKCU_ERR_ARG, "bucket offsets must span [0, nnz]");
+  KView v = make_view(s, t, false);
+  if (ft_factor_smem(v, M, mode) > 227 * 1024)
+    return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker factor block");
+  if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+  if ((size_t)(nbuckets + 1) > s->boff_cap) {
+    if (s->d_boff) CK(cudaFree(s->d_boff));
+    s->d_boff = nullptr;
+    CK(cudaMalloc(&s->d_boff, sizeof(int64_t) * (nbuckets + 1)));
+    s->boff_cap = nbuckets + 1;
+  }
+  CK(cudaMemcpyAsync(s->d_boff, bucket_off, sizeof(int64_t) * (nbuckets + 1),
+                     cudaMemcpyHostToDevice, s->stream));
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(launch_ft_factor(v, mode, s->d_perm, s->d_boff, nbuckets, M, lr_a, reg_a, s->stream));
+  s->launches += 1;
+  return finish_timing(s, ms);
+}
+
+int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm, int32_t M,
+                          float lr_b, float reg_b, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  DevTensor& t = s->slots[slot];
+  if (M < 1) return fail(s, FTKCU_ERR_ARG, "batch size must be positive");
+  if (mode < 0 || mode >= t.order) return fail(s, FTKCU_ERR_ARG, "mode %d out of range", mode);
+  if (t.nnz > 0 && !perm) return fail(s, FTKCU_ERR_ARG, "global plan missing");
+  KView v = make_view(s, t, false);
+  if (ft_core_smem(v, M) > 227 * 1024)
+    return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker core block");
+  if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(launch_ft_core(v, mode, s->d_perm, M, lr_b, reg_b, s->stream));
+  s->launches += 1;
+  return finish_timing(s, ms);
 }
 
 int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offsets, int ncells) {

@@ -57,6 +57,8 @@ def lib():
     L.ftkh_derive_seed.restype = C.c_uint64
     L.ftkh_derive_seed.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.c_int]
     L.ftkh_global_plan.argtypes = [C.c_int64, C.c_int, C.c_uint64, _i64p]
+    L.ftkh_per_bucket_plan.argtypes = [C.c_int, C.c_int64, _i32p, C.c_int, C.c_int, C.c_int,
+                                       C.c_uint64, _i64p, _i64p, _i64p]
     L.ftkh_init_model.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_uint64, C.c_float, _fpp,
                                   _fpp]
     L.ftkh_default_init_scale.restype = C.c_float
@@ -79,6 +81,9 @@ def lib():
     L.ftkh_epoch_plus.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p,
                                   _fpp, _fpp, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
                                   C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p, _i64p]
+    L.ftkh_epoch_fasttucker.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p,
+                                        _f32p, _fpp, _fpp, C.c_float, C.c_float, C.c_float,
+                                        C.c_float, C.c_int, C.c_int, C.c_uint64, _f64p, _i64p]
     L.ftkh_train.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p,
                              C.c_int64, _i32p, _f32p, _fpp, _fpp, C.c_float, C.c_float,
                              C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -119,6 +124,20 @@ def global_plan(nnz: int, m: int, seed: int) -> np.ndarray:
     out = np.empty(nnz, np.int64)
     _ck(lib().ftkh_global_plan(nnz, m, seed & M64, _p(out, _i64p)))
     return out
+
+
+def per_bucket_plan(idx, mode: int, m: int, seed: int, keying: int = 0):
+    """EpochPlan::per_bucket over build_mode_index(mode, keying) for Rng(seed):
+    (positions in plan order, bucket offsets in plan order incl. nnz).
+    keying 0 = fixed mode (FastTucker), 1 = fixed complement."""
+    idx = np.ascontiguousarray(idx, np.int32)
+    nnz, order = idx.shape
+    perm = np.empty(nnz, np.int64)
+    boff = np.empty(nnz + 2, np.int64)
+    nb = C.c_int64(0)
+    _ck(lib().ftkh_per_bucket_plan(order, nnz, _p(idx, _i32p), mode, keying, m, seed & M64,
+                                   _p(perm, _i64p), _p(boff, _i64p), C.byref(nb)))
+    return perm, boff[: nb.value + 1].copy()
 
 
 def init_model(dims, ranks, r, seed, scale):
@@ -218,6 +237,21 @@ def epoch_plus(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e-3, reg_
                               _p(idx, _i32p), _p(vals, _f32p), _ptrs(a), _ptrs(b), lr_a, lr_b,
                               reg_a, reg_b, m, workers, int(store_c), int(canonical), seed & M64,
                               _p(secs, _f64p), _p(cnt, _i64p)))
+    return secs, cnt
+
+
+def epoch_fasttucker(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
+                     reg_b=1e-4, m=16, canonical=False):
+    """ftk::epoch_fasttucker through the C++ API (fixed-mode indices built
+    there); mutates a/b in place; returns (seconds[2], counters[10])."""
+    dims, ranks, idx = _i32(dims), _i32(ranks), _i32(idx)
+    vals = np.ascontiguousarray(vals, np.float32)
+    secs = np.zeros(2, np.float64)
+    cnt = np.zeros(10, np.int64)
+    _ck(lib().ftkh_epoch_fasttucker(dims.size, _p(dims, _i32p), _p(ranks, _i32p), r, vals.size,
+                                    _p(idx, _i32p), _p(vals, _f32p), _ptrs(a), _ptrs(b), lr_a,
+                                    lr_b, reg_a, reg_b, m, int(canonical), seed & M64,
+                                    _p(secs, _f64p), _p(cnt, _i64p)))
     return secs, cnt
 
 

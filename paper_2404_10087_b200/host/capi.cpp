@@ -89,6 +89,26 @@ int ftkh_global_plan(int64_t nnz, int m, uint64_t seed, int64_t* out) {
   });
 }
 
+// EpochPlan::per_bucket positions and bucket offsets (plan order) of an
+// AoS index set, for Rng(seed); nb_out receives the bucket count.
+int ftkh_per_bucket_plan(int order, int64_t nnz, const int32_t* idx, int mode, int keying, int m,
+                         uint64_t seed, int64_t* perm_out, int64_t* boff_out, int64_t* nb_out) {
+  return guarded([&] {
+    SparseTensor t;
+    t.order = order;
+    t.indices.assign(idx, idx + nnz * order);
+    t.values.assign(static_cast<std::size_t>(nnz), 0.0f);
+    const ModeIndex mi =
+        build_mode_index(t, mode, keying ? Keying::kFixedComplement : Keying::kFixedMode);
+    Rng rng(seed);
+    const EpochPlan p = EpochPlan::per_bucket(t, mi, m, rng);
+    std::memcpy(perm_out, p.positions().data(), sizeof(int64_t) * nnz);
+    const auto& bo = p.bucket_offsets();
+    std::memcpy(boff_out, bo.data(), sizeof(int64_t) * bo.size());
+    *nb_out = static_cast<int64_t>(bo.size()) - 1;
+  });
+}
+
 int ftkh_init_model(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
                     uint64_t seed, float scale, float* const* a, float* const* b) {
   return guarded([&] {
@@ -166,6 +186,39 @@ int ftkh_set_device_options(int device, int mode, int precision, int exact_eval)
     o.precision = static_cast<DevicePrecision>(precision);
     o.exact_eval = exact_eval != 0;
     set_device_options(o);
+  });
+}
+
+// ftk::epoch_fasttucker with fixed-mode indices of every mode built here.
+int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
+                          int64_t nnz, const int32_t* idx, const float* vals, float* const* a,
+                          float* const* b, float lr_a, float lr_b, float reg_a, float reg_b,
+                          int m, int canonical, uint64_t seed, double* seconds2,
+                          int64_t* counters) {
+  return guarded([&] {
+    SparseTensor t = make_tensor(order, dims, nnz, idx, vals);
+    Model md = make_model(order, dims, ranks, r, a, b);
+    std::vector<ModeIndex> fixed;
+    for (int n = 0; n < order; ++n) fixed.push_back(build_mode_index(t, n, Keying::kFixedMode));
+    EpochOptions eo;
+    eo.canonical_order = canonical != 0;
+    EpochStats st;
+    try {
+      st = epoch_fasttucker(t, fixed, md, hyper(lr_a, lr_b, reg_a, reg_b, 1, m), eo, seed);
+    } catch (...) {
+      copy_back(md, a, b);
+      throw;
+    }
+    copy_back(md, a, b);
+    if (seconds2) {
+      seconds2[0] = st.seconds_factor;
+      seconds2[1] = st.seconds_core;
+    }
+    if (counters)
+      for (int s = 0; s < kStages; ++s) {
+        counters[s] = st.factor.total(static_cast<Stage>(s));
+        counters[kStages + s] = st.core.total(static_cast<Stage>(s));
+      }
   });
 }
 

@@ -213,6 +213,97 @@ EpochStats run_epoch(const SparseTensor& t, int slot, const Model& m, const Hype
   return st;
 }
 
+// FastTucker's per-batch billing (update_factor_fasttucker_impl /
+// update_core_fasttucker_impl, decomposition.cpp:316-417) summed over a
+// plan's batches: every tally is a per-batch constant plus a multiple of
+// m_eff, and all of it lands on the block's mode.
+void bill_fasttucker(CostCounters& cc, const Model& m, int mode, const EpochPlan& plan,
+                     bool factor) {
+  const int N = m.order();
+  const size64 R = m.r, Jn = m.ranks[mode];
+  size64 sum_other_j = 0, sum_all_j = 0, other_jr = 0;
+  for (int n = 0; n < N; ++n) {
+    sum_all_j += m.ranks[n];
+    if (n != mode) {
+      sum_other_j += m.ranks[n];
+      other_jr += static_cast<size64>(m.ranks[n]) * R;
+    }
+  }
+  const size64 combine = N >= 2 ? N - 2 : 0;
+  for (size64 b = 0; b < plan.batches(); ++b) {
+    const size64 me = plan.desc(b).len;
+    const bool full = me == static_cast<size64>(plan.batch_size());
+    cc.count_batch(mode, full);
+    if (factor) {
+      cc.add(mode, kRead, Jn + Jn * R + me * sum_other_j, full);
+      cc.add(mode, kDStage, me * other_jr + combine * me * R, full);
+      cc.add(mode, kBdtStage, me * R * Jn, full);
+      cc.add(mode, kOther, Jn * R + me * R + me * Jn, full);
+      cc.add(mode, kUpdate, Jn, full);
+    } else {
+      cc.add(mode, kRead, me * sum_all_j + Jn * R, full);
+      cc.add(mode, kDStage, me * other_jr + combine * me * R, full);
+      cc.add(mode, kOther, me * Jn * R + me * R + me * Jn, full);
+      cc.add(mode, kBdtStage, me * Jn * R, full);
+      cc.add(mode, kUpdate, Jn * R, full);
+    }
+  }
+}
+
+// One FastTucker epoch on the resident model (epoch_fasttucker,
+// decomposition.cpp:707-770): factor blocks over per-bucket plans of the
+// fixed-mode indices, then core blocks over global plans, mode by mode.  The
+// device runs the workers == 1 schedule (the factor block is
+// schedule-invariant; the core block is one chain of B^(n) updates).
+EpochStats run_epoch_fasttucker(const SparseTensor& t, int slot, const Model& m,
+                                const std::vector<ModeIndex>& fixed_mode, const Hyperparams& h,
+                                const EpochOptions& opts, std::uint64_t seed) {
+  ftkcu_session* s = session();
+  const int N = m.order();
+  require(static_cast<int>(fixed_mode.size()) == N, "need one fixed-mode index per mode");
+  const index_t cap = opts.canonical_order ? 1 : h.batch_size;
+  EpochStats st;
+  st.factor.reset(N);
+  st.core.reset(N);
+  double total_f = 0.0, total_c = 0.0;
+  for (int mode = 0; mode < N; ++mode) {
+    Rng rng(derive_seed(seed, {1, static_cast<std::uint64_t>(mode)}));
+    double ms = 0.0;
+    if (opts.canonical_order) {
+      // storage order, one entry per batch: the fixed-mode index's buckets
+      // hold each row's entries in storage order, and rows are independent
+      EpochPlan plan = EpochPlan::canonical(t);
+      const ModeIndex& mi = fixed_mode[mode];
+      std::vector<int64_t> boff(mi.offsets.begin(), mi.offsets.end());
+      check(ftkcu_fasttucker_factor(s, slot, mode,
+                                    reinterpret_cast<const int64_t*>(mi.positions.data()),
+                                    boff.data(), static_cast<int64_t>(mi.buckets()), 1, h.lr_a,
+                                    h.reg_a, &ms));
+      bill_fasttucker(st.factor, m, mode, plan, true);
+    } else {
+      EpochPlan plan = EpochPlan::per_bucket(t, fixed_mode[mode], cap, rng);
+      const auto& bo = plan.bucket_offsets();
+      check(ftkcu_fasttucker_factor(s, slot, mode, plan.positions().data(), bo.data(),
+                                    static_cast<int64_t>(bo.size()) - 1, cap, h.lr_a, h.reg_a,
+                                    &ms));
+      bill_fasttucker(st.factor, m, mode, plan, true);
+    }
+    total_f += ms;
+  }
+  for (int mode = 0; mode < N; ++mode) {
+    Rng rng(derive_seed(seed, {2, static_cast<std::uint64_t>(mode)}));
+    EpochPlan plan = opts.canonical_order ? EpochPlan::canonical(t) : EpochPlan::global(t, cap, rng);
+    double ms = 0.0;
+    check(ftkcu_fasttucker_core(s, slot, mode, plan.positions().data(), cap, h.lr_b, h.reg_b,
+                                &ms));
+    bill_fasttucker(st.core, m, mode, plan, false);
+    total_c += ms;
+  }
+  st.seconds_factor = total_f * 1e-3;
+  st.seconds_core = total_c * 1e-3;
+  return st;
+}
+
 std::string num_json(double v) {
   if (!std::isfinite(v)) return "null";
   char buf[64];
@@ -246,6 +337,26 @@ EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
     st = run_epoch(t, slot, m, h, opts, seed);
   } catch (...) {
     download_model(m);  // the reference mutates m in place before throwing
+    throw;
+  }
+  download_model(m);
+  return st;
+}
+
+EpochStats epoch_fasttucker(const SparseTensor& t, const std::vector<ModeIndex>& fixed_mode,
+                            Model& m, const Hyperparams& h, const EpochOptions& opts,
+                            std::uint64_t seed) {
+  require(static_cast<int>(fixed_mode.size()) == m.order(),
+          "need one fixed-mode index per mode");
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(t);
+  upload_model(m);
+  EpochStats st;
+  try {
+    st = run_epoch_fasttucker(t, slot, m, fixed_mode, h, opts, seed);
+  } catch (...) {
+    download_model(m);
     throw;
   }
   download_model(m);
@@ -306,9 +417,9 @@ History train(const SparseTensor& train_set, const SparseTensor* test_set, Model
   require(m.order() == train_set.order, "model/tensor order mismatch");
   for (int n = 0; n < m.order(); ++n)
     require(m.dims[n] >= train_set.dims[n], "model dims too small for tensor");
-  require(opts.variant == Variant::kPlus,
-          "the B200 engine implements the plus variant only (fasttucker/fastertucker are "
-          "out of scope)");
+  require(opts.variant != Variant::kFasterTucker,
+          "the B200 engine implements the plus and fasttucker variants (fastertucker is not "
+          "built yet)");
   const int workers = resolve_workers(opts.workers);
   EpochOptions eo;
   eo.workers = workers;
@@ -322,12 +433,18 @@ History train(const SparseTensor& train_set, const SparseTensor* test_set, Model
   if (test_set != nullptr && test_set->nnz() > 0) {
     test_slot = ensure_tensor(*test_set);
   }
+  std::vector<ModeIndex> fixed;  // FastTucker: fixed-mode indices, built once
+  if (opts.variant == Variant::kFastTucker)
+    for (int n = 0; n < m.order(); ++n)
+      fixed.push_back(build_mode_index(train_set, n, Keying::kFixedMode));
   upload_model(m);
   for (int epoch = 1; epoch <= h.epochs; ++epoch) {
     const std::uint64_t es = derive_seed(opts.seed, {static_cast<std::uint64_t>(epoch)});
     EpochRecord rec;
     rec.epoch = epoch;
-    rec.stats = run_epoch(train_set, slot, m, h, eo, es);
+    rec.stats = opts.variant == Variant::kFastTucker
+                    ? run_epoch_fasttucker(train_set, slot, m, fixed, h, eo, es)
+                    : run_epoch(train_set, slot, m, h, eo, es);
     rec.seconds = rec.stats.seconds_factor + rec.stats.seconds_core;
     rec.train_loss = device_loss(slot, h.reg_a, h.reg_b, workers);
     if (test_slot >= 0) {
