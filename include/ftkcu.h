@@ -149,12 +149,16 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm,
  * parallel_for over update_factor_fasttucker_impl (decomposition.cpp:729-742,
  * 316-371).  Core block of `mode`: perm = the global plan;
  * update_core_fasttucker_impl per batch (:752-766, 373-417), B^(mode)
- * updated in place after every batch.  ms: device time of the block. */
+ * updated in place after every batch.  schedule FTKCU_MODE_DETERMINISTIC:
+ * the workers == 1 chain (bit-identical); FTKCU_MODE_HOGWILD: the workers > 1
+ * schedule (batches spread over CTAs, B steps added atomically).  The
+ * factor block has no such choice: its buckets are independent, so it is
+ * parallel and bit-identical at once.  ms: device time of the block. */
 int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
                             const int64_t* bucket_off, int64_t nbuckets, int32_t M, float lr_a,
                             float reg_a, double* ms);
 int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm, int32_t M,
-                          float lr_b, float reg_b, double* ms);
+                          float lr_b, float reg_b, int schedule, double* ms);
 
 /* DSGD strata support.  Declares that the uploaded entries are sorted into
  * cells: entries [cell_offsets[c], cell_offsets[c+1]) form cell c.  The

@@ -80,7 +80,7 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_fasttucker_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p, C.c_int64,
                                           C.c_int32, C.c_float, C.c_float, _f64p]
     L.ftkcu_fasttucker_core.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, C.c_int32,
-                                        C.c_float, C.c_float, _f64p]
+                                        C.c_float, C.c_float, C.c_int, _f64p]
     L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.restype = C.c_int64
@@ -248,12 +248,13 @@ class Session:
                                                   C.byref(ms) if timed else None))
         return ms.value
 
-    def fasttucker_core(self, slot, mode, perm, M=16, lr_b=1e-3, reg_b=1e-4, timed=True):
+    def fasttucker_core(self, slot, mode, perm, M=16, lr_b=1e-3, reg_b=1e-4,
+                        schedule=MODE_DETERMINISTIC, timed=True):
         """FastTucker core block of `mode` over a global plan (ftkcu_fasttucker_core)."""
         pa = np.ascontiguousarray(perm, np.int64)
         ms = C.c_double(0.0)
         self._ck(self.lib.ftkcu_fasttucker_core(self.h, slot, mode, _p(pa, _i64p), M, lr_b,
-                                                reg_b, C.byref(ms) if timed else None))
+                                                reg_b, schedule, C.byref(ms) if timed else None))
         return ms.value
 
     def eval(self, slot=1, workers=1, reg_a=0.0, reg_b=0.0):

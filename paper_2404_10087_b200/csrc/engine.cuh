@@ -147,10 +147,10 @@ size_t ft_factor_smem(const KView& v, int cap, int mode);
 cudaError_t launch_ft_factor(const KView& v, int mode, const int64_t* perm, const int64_t* boff,
                              int64_t nbuckets, int cap, float lr_a, float reg_a, cudaStream_t st);
 // Core block of `mode`: the global plan's batches in order, B^(mode) updated
-// after every batch.
+// after every batch (hogwild: by many CTAs at once, atomically).
 size_t ft_core_smem(const KView& v, int cap);
 cudaError_t launch_ft_core(const KView& v, int mode, const int64_t* perm, int cap, float lr_b,
-                           float reg_b, cudaStream_t st);
+                           float reg_b, bool hogwild, cudaStream_t st);
 
 // ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,

@@ -11,8 +11,9 @@
 //
 // Core block of mode n: a global plan, and B^(n) moves after every batch
 // (update_core_fasttucker_impl, :373-417), so the batches form one chain.
-// One CTA walks it and spreads each batch's C, D, x̂, G and B update over
-// its threads.
+// Deterministic schedule: one CTA walks it and spreads each batch's C, D, x̂,
+// G and B update over its threads.  Hogwild schedule (the reference's
+// workers > 1): CTAs share the chain and add their B steps atomically.
 //
 // Arithmetic: the reference's fp32 sequence, each
 // product and sum rounded on its own (__fmul_rn / __fadd_rn: the reference
@@ -266,6 +267,75 @@ ft_core_kernel(KView v, int mode, const int64_t* __restrict__ perm, int cap, flo
   }
 }
 
+// Hogwild core block (the reference's workers > 1 schedule, where the
+// parallel_for workers update B^(n) concurrently, decomposition.cpp:752-766):
+// CTAs take interleaved batches of the plan, read B^(n) through L2 and add
+// their step lr (g / M - reg b) atomically.
+__global__ void __launch_bounds__(256)
+ft_core_hog_kernel(KView v, int mode, const int64_t* __restrict__ perm, int cap, float lr,
+                   float reg) {
+  extern __shared__ float sm[];
+  const FtcLayout L = ftc_layout(v, cap);
+  int* s_idx = reinterpret_cast<int*>(sm + L.o_idx);
+  const int r = v.r, jn = v.j[mode];
+  float* bm = const_cast<float*>(v.b[mode]);
+  const int64_t nb = (v.nnz + cap - 1) / cap;
+  for (int64_t bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+    const int64_t off = bi * cap;
+    const int m_eff = (int)((v.nnz - off) < cap ? (v.nnz - off) : cap);
+    for (int m = threadIdx.x; m < m_eff; m += blockDim.x) {
+      const int64_t pos = perm[off + m];
+      sm[L.o_x + m] = v.vals[pos];
+      for (int n = 0; n < v.order; ++n) s_idx[n * cap + m] = v.idx[n][pos];
+    }
+    __syncthreads();
+    for (int n = 0; n < v.order; ++n) {
+      const int j = v.j[n];
+      for (int e = threadIdx.x; e < m_eff * j; e += blockDim.x) {
+        const int m = e / j, k = e - m * j;
+        sm[L.aoff[n] + e] = __ldg(v.a[n] + (size_t)s_idx[n * cap + m] * j + k);
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < v.order * m_eff * r; e += blockDim.x) {
+      const int n = e / (m_eff * r), rem = e - n * m_eff * r;
+      const int m = rem / r, c = rem - m * r;
+      const int j = v.j[n];
+      const float* a = sm + L.aoff[n] + m * j;
+      float acc = 0.0f;
+      if (n == mode)
+        for (int k = 0; k < j; ++k) acc = fmaf(a[k], __ldcg(v.b[n] + (size_t)k * r + c), acc);
+      else
+        for (int k = 0; k < j; ++k) acc = fmaf(a[k], __ldg(v.b[n] + (size_t)k * r + c), acc);
+      sm[L.o_c + (n * cap + m) * r + c] = acc;
+    }
+    __syncthreads();
+    const int first = (mode == 0) ? 1 : 0;
+    for (int e = threadIdx.x; e < m_eff * r; e += blockDim.x) {
+      float acc = sm[L.o_c + first * cap * r + e];
+      for (int n = first + 1; n < v.order; ++n)
+        if (n != mode) acc *= sm[L.o_c + n * cap * r + e];
+      sm[L.o_d + e] = acc;
+    }
+    __syncthreads();
+    for (int m = threadIdx.x; m < m_eff; m += blockDim.x) {
+      float acc = 0.0f;
+      for (int c = 0; c < r; ++c) acc = fmaf(sm[L.o_c + (mode * cap + m) * r + c], sm[L.o_d + m * r + c], acc);
+      sm[L.o_res + m] = sm[L.o_x + m] - acc;
+    }
+    __syncthreads();
+    const float inv = 1.0f / (float)m_eff;
+    const float* a = sm + L.aoff[mode];
+    for (int e = threadIdx.x; e < jn * r; e += blockDim.x) {
+      const int k = e / r, c = e - k * r;
+      float g = 0.0f;
+      for (int m = 0; m < m_eff; ++m) g = fmaf(sm[L.o_res + m] * a[m * jn + k], sm[L.o_d + m * r + c], g);
+      atomicAdd(bm + e, lr * (g * inv - reg * __ldcg(bm + e)));
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 size_t ft_factor_smem(const KView& v, int cap, int mode) {
@@ -292,10 +362,20 @@ size_t ft_core_smem(const KView& v, int cap) {
 }
 
 cudaError_t launch_ft_core(const KView& v, int mode, const int64_t* perm, int cap, float lr_b,
-                           float reg_b, cudaStream_t st) {
+                           float reg_b, bool hogwild, cudaStream_t st) {
   if (v.nnz == 0) return cudaSuccess;
   const size_t bytes = ft_core_smem(v, cap);
   if (bytes > 227 * 1024) return cudaErrorInvalidValue;
+  if (hogwild) {
+    cudaError_t e = cudaFuncSetAttribute(ft_core_hog_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    const int64_t nb = (v.nnz + cap - 1) / cap;
+    int64_t grid = (int64_t)num_sms() * 4;
+    if (grid > nb) grid = nb;
+    ft_core_hog_kernel<<<(int)grid, 256, bytes, st>>>(v, mode, perm, cap, lr_b, reg_b);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(ft_core_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;

@@ -762,7 +762,7 @@ int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t*
 }
 
 int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm, int32_t M,
-                          float lr_b, float reg_b, double* ms) {
+                          float lr_b, float reg_b, int schedule, double* ms) {
   int rc = bind(s);
   if (rc) return rc;
   if ((rc = check_ready(s, slot))) return rc;
@@ -775,7 +775,10 @@ int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* p
     return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker core block");
   if ((rc = upload_perm(s, perm, t.nnz))) return rc;
   CK(cudaEventRecord(s->ev0, s->stream));
-  CK(launch_ft_core(v, mode, s->d_perm, M, lr_b, reg_b, s->stream));
+  if (schedule != FTKCU_MODE_DETERMINISTIC && schedule != FTKCU_MODE_HOGWILD)
+    return fail(s, FTKCU_ERR_ARG, "unknown schedule %d", schedule);
+  CK(launch_ft_core(v, mode, s->d_perm, M, lr_b, reg_b, schedule == FTKCU_MODE_HOGWILD,
+                    s->stream));
   s->launches += 1;
   return finish_timing(s, ms);
 }

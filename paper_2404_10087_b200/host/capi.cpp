@@ -193,7 +193,7 @@ int ftkh_set_device_options(int device, int mode, int precision, int exact_eval)
 int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
                           int64_t nnz, const int32_t* idx, const float* vals, float* const* a,
                           float* const* b, float lr_a, float lr_b, float reg_a, float reg_b,
-                          int m, int canonical, uint64_t seed, double* seconds2,
+                          int m, int workers, int canonical, uint64_t seed, double* seconds2,
                           int64_t* counters) {
   return guarded([&] {
     SparseTensor t = make_tensor(order, dims, nnz, idx, vals);
@@ -201,6 +201,7 @@ int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, 
     std::vector<ModeIndex> fixed;
     for (int n = 0; n < order; ++n) fixed.push_back(build_mode_index(t, n, Keying::kFixedMode));
     EpochOptions eo;
+    eo.workers = workers;
     eo.canonical_order = canonical != 0;
     EpochStats st;
     try {

@@ -253,8 +253,9 @@ void bill_fasttucker(CostCounters& cc, const Model& m, int mode, const EpochPlan
 // One FastTucker epoch on the resident model (epoch_fasttucker,
 // decomposition.cpp:707-770): factor blocks over per-bucket plans of the
 // fixed-mode indices, then core blocks over global plans, mode by mode.  The
-// device runs the workers == 1 schedule (the factor block is
-// schedule-invariant; the core block is one chain of B^(n) updates).
+// factor block is schedule-invariant (bit-identical at any parallelism); the
+// core block runs the workers == 1 chain, or for workers > 1 the Hogwild
+// schedule like the reference's parallel_for.
 EpochStats run_epoch_fasttucker(const SparseTensor& t, int slot, const Model& m,
                                 const std::vector<ModeIndex>& fixed_mode, const Hyperparams& h,
                                 const EpochOptions& opts, std::uint64_t seed) {
@@ -262,6 +263,7 @@ EpochStats run_epoch_fasttucker(const SparseTensor& t, int slot, const Model& m,
   const int N = m.order();
   require(static_cast<int>(fixed_mode.size()) == N, "need one fixed-mode index per mode");
   const index_t cap = opts.canonical_order ? 1 : h.batch_size;
+  const int workers = resolve_workers(opts.workers);
   EpochStats st;
   st.factor.reset(N);
   st.core.reset(N);
@@ -295,7 +297,7 @@ EpochStats run_epoch_fasttucker(const SparseTensor& t, int slot, const Model& m,
     EpochPlan plan = opts.canonical_order ? EpochPlan::canonical(t) : EpochPlan::global(t, cap, rng);
     double ms = 0.0;
     check(ftkcu_fasttucker_core(s, slot, mode, plan.positions().data(), cap, h.lr_b, h.reg_b,
-                                &ms));
+                                device_mode(workers), &ms));
     bill_fasttucker(st.core, m, mode, plan, false);
     total_c += ms;
   }

@@ -77,3 +77,25 @@ def test_plan_errors_are_reported(session):
         session.fasttucker_factor(0, 0, perm, boff[:-1], 16)
     with pytest.raises(eng.FtkError, match="mode"):
         session.fasttucker_factor(0, 3, perm, boff, 16)
+
+
+def test_hogwild_core_block_tracks_the_chain(session):
+    """The workers > 1 core schedule (CTAs share the B^(n) chain, atomic
+    steps) moves B like the sequential chain up to staleness: same step
+    direction, magnitude within a few percent at this learning rate."""
+    import paper_2404_10087_b200 as eng
+
+    t = O.random_tensor([300, 200, 100], 40000, 23, 1.0, 5.0)
+    m = O.random_model(t.dims, [16, 16, 16], 16, 24, 0.3)
+    perm = host.global_plan(t.nnz, 16, 77)
+    out = []
+    for sched in (eng.MODE_DETERMINISTIC, eng.MODE_HOGWILD):
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.fasttucker_core(0, 1, perm, 16, 1e-3, 1e-4, schedule=sched)
+        out.append(session.download_model()[1][1] - m.b[1])
+    det, hog = out
+    assert np.isfinite(hog).all()
+    cos = float(np.sum(det * hog) / (np.linalg.norm(det) * np.linalg.norm(hog)))
+    assert cos > 0.99
+    assert abs(np.linalg.norm(hog) / np.linalg.norm(det) - 1.0) < 0.05
