@@ -21,10 +21,36 @@
 
 namespace ftk {
 
+// Cached C rows C_n = A_n B_n of every mode, for the FasterTucker baseline
+// (decomposition.hpp:26-44 of the reference).  build / refresh compute on the
+// host; epoch_fastertucker keeps the device copy in step and writes the
+// refreshed rows back.
+class CCache {
+ public:
+  void init(const Model& m);
+  void build(const Model& m, CostCounters* cc);
+  void refresh(const Model& m, int mode, CostCounters* cc);
+  void mark_stale(int mode) { fresh_[mode] = 0; }
+  bool fresh(int mode) const { return fresh_[mode] != 0; }
+  bool ready() const { return !c_.empty(); }
+  std::span<const real> row(int mode, index_t i) const {
+    return {c_[mode].data() + static_cast<std::size_t>(i) * r_, static_cast<std::size_t>(r_)};
+  }
+  // Engine additions: the per-mode row storage (dims[n] x R, row-major), and
+  // marking rows refreshed on the device.
+  std::vector<std::vector<real>>& storage() { return c_; }
+  void mark_fresh(int mode) { fresh_[mode] = 1; }
+
+ private:
+  std::vector<std::vector<real>> c_;
+  std::vector<char> fresh_;
+  index_t r_ = 0;
+};
+
 struct EpochOptions {
   int workers = 1;               // 1: deterministic sweeps; > 1: Hogwild
   bool canonical_order = false;  // storage order, single-entry batches
-  bool eager_refresh = false;    // FasterTucker hook (ignored)
+  bool eager_refresh = false;    // FasterTucker per-batch refresh hook (not supported)
   bool store_c = false;          // storage scheme: core phase reads C rows from a C cache
 };
 
@@ -38,6 +64,14 @@ struct EpochStats {
 EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
                       const EpochOptions& opts, std::uint64_t seed);
 
+// The FasterTucker baseline (decomposition.hpp:201-206 of the reference):
+// complement-keyed buckets, d rows from the C cache (which must be built),
+// the block's cache rows refreshed at each block barrier.  Bit-identical to
+// the reference with workers = 1 (the device schedule is order-equivalent).
+EpochStats epoch_fastertucker(const SparseTensor& t, const std::vector<ModeIndex>& complement,
+                              Model& m, CCache& cache, const Hyperparams& h,
+                              const EpochOptions& opts, std::uint64_t seed);
+
 // The FastTucker baseline (decomposition.hpp:194-199 of the reference):
 // factor blocks over per-bucket plans of the fixed-mode indices, then core
 // blocks with B^(n) moving every batch.  Runs on the device in the
@@ -47,7 +81,7 @@ EpochStats epoch_fasttucker(const SparseTensor& t, const std::vector<ModeIndex>&
                             std::uint64_t seed);
 
 struct TrainOptions {
-  Variant variant = Variant::kPlus;  // kPlus or kFastTucker (kFasterTucker: not built)
+  Variant variant = Variant::kPlus;  // kPlus, kFastTucker or kFasterTucker
   bool store_c = false;
   int workers = 1;
   std::uint64_t seed = 0;

@@ -160,6 +160,30 @@ int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t*
 int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm, int32_t M,
                           float lr_b, float reg_b, int schedule, double* ms);
 
+/* ---- FasterTucker baseline ------------------------
+ * ftk::epoch_fastertucker (decomposition.cpp:772-843) one block at a time,
+ * bit-identical to the reference's workers == 1 epoch.  The C cache
+ * (CCache, decomposition.cpp:74-107: C_n = A_n B_n, dims[n] x R fp32) lives
+ * on the device next to the model: upload it before the first block (the
+ * reference requires cache.ready()), download it to keep a host copy.  Each
+ * block ends with the refresh of its mode's cache rows (the block barrier,
+ * :810, :837), inside the timed region as in the reference.
+ *
+ * Factor block: perm = EpochPlan::per_bucket(complement index of `mode`)
+ * positions regrouped by mode-`mode` row, plan order kept inside a row;
+ * row_off = the nrows + 1 group offsets.  (A step touches only its own row,
+ * so rows are independent chains.)  Core block: perm = that plan for the
+ * core seed, batch_off = its nbatches + 1 batch offsets (batches never cross
+ * a bucket).  Core block supports J <= 128. */
+int ftkcu_ccache_upload(ftkcu_session* s, const float* const* C);
+int ftkcu_ccache_download(ftkcu_session* s, float* const* C);
+int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                              const int64_t* row_off, int64_t nrows, float lr_a, float reg_a,
+                              double* ms);
+int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                            const int64_t* batch_off, int64_t nbatches, float lr_b, float reg_b,
+                            double* ms);
+
 /* DSGD strata support.  Declares that the uploaded entries are sorted into
  * cells: entries [cell_offsets[c], cell_offsets[c+1]) form cell c.  The
  * Hogwild stream then shuffles and tiles every cell separately. */

@@ -134,6 +134,11 @@ class _COracle:
         L.fo_fasttucker_core_block.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, C.c_int64,
                                                _i32p, _f32p, _i64p, C.c_int, C.c_int, C.c_float,
                                                C.c_float]
+        L.fo_ccache_refresh.argtypes = [C.c_int32, C.c_int, C.c_int, _f32p, _f32p, _f32p]
+        for fn in ("fo_fastertucker_factor_block", "fo_fastertucker_core_block"):
+            getattr(L, fn).argtypes = [C.c_int, _i32p, _i32p, C.c_int, _fpp, _fpp, _fpp, _i32p,
+                                       _f32p, _i64p, _i64p, C.c_int64, C.c_int, C.c_float,
+                                       C.c_float]
         L.fo_predict.argtypes = [C.c_int, _i32p, C.c_int, _fpp, _fpp, _i32p]
         L.fo_predict.restype = C.c_double
         L.fo_loss.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _fpp, _fpp, C.c_int64, _i32p,
@@ -170,6 +175,30 @@ class _COracle:
         rc = self.lib.fo_fasttucker_core_block(
             m.order, _p(m.ranks, _i32p), m.r, _ptr_array(m.a), _ptr_array(m.b), t.nnz,
             _p(t.idx, _i32p), _p(t.vals, _f32p), _p(perm, _i64p), cap, mode, lr_b, reg_b)
+        assert rc == 0
+
+    def ccache_build(self, m: Model):
+        """CCache::build (decomposition.cpp:84-87): C_n = A_n B_n for every mode."""
+        out = []
+        for n in range(m.order):
+            c = np.zeros((int(m.dims[n]), m.r), np.float32)
+            self.lib.fo_ccache_refresh(int(m.dims[n]), int(m.ranks[n]), m.r,
+                                       _p(np.ascontiguousarray(m.a[n]), _f32p),
+                                       _p(np.ascontiguousarray(m.b[n]), _f32p), _p(c, _f32p))
+            out.append(c)
+        return out
+
+    def fastertucker_block(self, factor, t: Tensor, m: Model, cache, perm, batch_off, mode, lr,
+                           reg):
+        """FasterTucker factor (factor=True) or core block of `mode` over a
+        complement-keyed per-bucket plan cut into batches (in place; the
+        mode's cache rows are refreshed at the end)."""
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        bo = np.ascontiguousarray(batch_off, dtype=np.int64)
+        fn = self.lib.fo_fastertucker_factor_block if factor else self.lib.fo_fastertucker_core_block
+        rc = fn(m.order, _p(m.dims, _i32p), _p(m.ranks, _i32p), m.r, _ptr_array(m.a),
+                _ptr_array(m.b), _ptr_array(cache), _p(t.idx, _i32p), _p(t.vals, _f32p),
+                _p(perm, _i64p), _p(bo, _i64p), bo.size - 1, mode, lr, reg)
         assert rc == 0
 
     def core_phase(self, t: Tensor, m: Model, perm, cap, lr_b, reg_b, store_c=False):
@@ -271,6 +300,9 @@ class _Ref:
         L.ref_batch_probe.argtypes = [C.c_void_p, C.c_void_p, _i64p, C.c_int, C.c_int, C.c_float,
                                       C.c_float] + [_f32p] * 9
         L.ref_predicted_costs.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _i64p]
+        L.ref_epoch_fastertucker.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float,
+                                             C.c_float, C.c_float, C.c_int, C.c_int, C.c_int,
+                                             C.c_uint64, _i64p]
         L.ref_per_bucket_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64,
                                           _i64p, _i64p, _i64p]
         L.ref_epoch_fasttucker.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float,
@@ -390,6 +422,21 @@ class _Ref:
             self._check(self.lib.ref_epoch_fasttucker(th, mh, lr_a, lr_b, reg_a, reg_b, batch,
                                                       workers, int(canonical), seed,
                                                       _p(secs, _f64p), _p(cnt, _i64p)))
+            return self.model_to_np(mh, m), cnt
+        finally:
+            self.free_tensor(th)
+            self.free_model(mh)
+
+    def epoch_fastertucker(self, t: Tensor, m: Model, seed, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
+                           reg_b=1e-4, batch=16, workers=1, canonical=False):
+        """Runs ftkref::epoch_fastertucker (complement indices, fresh C cache);
+        returns (new model, counters[10])."""
+        th, mh = self.tensor(t), self.model(m)
+        cnt = np.zeros(10, np.int64)
+        try:
+            self._check(self.lib.ref_epoch_fastertucker(th, mh, lr_a, lr_b, reg_a, reg_b, batch,
+                                                        workers, int(canonical), seed,
+                                                        _p(cnt, _i64p)))
             return self.model_to_np(mh, m), cnt
         finally:
             self.free_tensor(th)

@@ -502,6 +502,137 @@ int fo_fasttucker_core_block(int order, const int32_t* ranks, int r, float* cons
 }
 
 /* ------------------------------------------------------------------------ */
+/* FasterTucker baseline (decomposition.cpp:772-843), workers = 1.          */
+
+/* CCache::refresh of one mode (decomposition.cpp:89-107): C_n[i][c] = sum_j
+ * A_n[i][j] B_n[j][c], j ascending over the unpadded J. */
+void fo_ccache_refresh(int32_t rows, int jn, int r, const float* a, const float* b, float* c) {
+  for (int32_t i = 0; i < rows; ++i)
+    for (int col = 0; col < r; ++col) {
+      float acc = 0.0f;
+      for (int j = 0; j < jn; ++j) {
+        float p = a[(size_t)i * jn + j] * b[(size_t)j * r + col];
+        acc = acc + p;
+      }
+      c[(size_t)i * r + col] = acc;
+    }
+}
+
+/* The batch's shared d row: the cached C rows of every other mode, first
+ * copied, the rest multiplied in, modes ascending (:420-449). */
+static void fst_d_row(int order, int r, int mode, float* const* cmat, const int32_t* e, float* d) {
+  int first = 1;
+  for (int k = 0; k < order; ++k) {
+    if (k == mode) continue;
+    const float* crow = cmat[k] + (size_t)e[k] * r;
+    for (int c = 0; c < r; ++c) d[c] = first ? crow[c] : d[c] * crow[c];
+    first = 0;
+  }
+}
+
+/* Factor block over a complement-keyed per-bucket plan: batch b is
+ * perm[boff[b] .. boff[b+1]); t = B^(n) d, then per-row single-sample steps
+ * from the staged rows (update_factor_fastertucker_impl, :451-489); the
+ * mode's cache rows are refreshed at the end (:810). */
+int fo_fastertucker_factor_block(int order, const int32_t* dims, const int32_t* ranks, int r,
+                                 float* const* amat, float* const* bmat, float* const* cmat,
+                                 const int32_t* idx_aos, const float* vals, const int64_t* perm,
+                                 const int64_t* boff, int64_t nb, int mode, float lr_a,
+                                 float reg_a) {
+  const int jn = ranks[mode];
+  float* d = malloc(sizeof(float) * r);
+  float* t = malloc(sizeof(float) * jn);
+  int64_t cap = 1;
+  for (int64_t b = 0; b < nb; ++b) if (boff[b + 1] - boff[b] > cap) cap = boff[b + 1] - boff[b];
+  float* snap = malloc(sizeof(float) * cap * jn);
+  float* res = malloc(sizeof(float) * cap);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t beg = boff[b];
+    const int m_eff = (int)(boff[b + 1] - beg);
+    fst_d_row(order, r, mode, cmat, idx_aos + (size_t)perm[beg] * order, d);
+    for (int m = 0; m < m_eff; ++m) {
+      const float* row = amat[mode] + (size_t)idx_aos[(size_t)perm[beg + m] * order + mode] * jn;
+      for (int j = 0; j < jn; ++j) snap[m * jn + j] = row[j];
+    }
+    for (int j = 0; j < jn; ++j) {
+      float acc = 0.0f;
+      for (int c = 0; c < r; ++c) {
+        float p = bmat[mode][(size_t)j * r + c] * d[c];
+        acc = acc + p;
+      }
+      t[j] = acc;
+    }
+    for (int m = 0; m < m_eff; ++m) {
+      float acc = 0.0f;
+      for (int j = 0; j < jn; ++j) {
+        float p = snap[m * jn + j] * t[j];
+        acc = acc + p;
+      }
+      res[m] = vals[perm[beg + m]] - acc;
+    }
+    for (int m = 0; m < m_eff; ++m) {
+      float* dst = amat[mode] + (size_t)idx_aos[(size_t)perm[beg + m] * order + mode] * jn;
+      for (int j = 0; j < jn; ++j) {
+        float g = res[m] * t[j];
+        float rg = reg_a * snap[m * jn + j];
+        float step = lr_a * (g - rg);
+        dst[j] = snap[m * jn + j] + step;
+      }
+    }
+  }
+  fo_ccache_refresh(dims[mode], jn, r, amat[mode], bmat[mode], cmat[mode]);
+  free(d); free(t); free(snap); free(res);
+  return 0;
+}
+
+/* Core block: residuals from the block-entry cache rows of the mode,
+ * g = A_psi^T r, B^(n) += lr (g d^T / M - reg B) after every batch
+ * (update_core_fastertucker_impl, :491-533); refresh at the end (:837). */
+int fo_fastertucker_core_block(int order, const int32_t* dims, const int32_t* ranks, int r,
+                               float* const* amat, float* const* bmat, float* const* cmat,
+                               const int32_t* idx_aos, const float* vals, const int64_t* perm,
+                               const int64_t* boff, int64_t nb, int mode, float lr_b,
+                               float reg_b) {
+  const int jn = ranks[mode];
+  float* d = malloc(sizeof(float) * r);
+  float* g = malloc(sizeof(float) * jn);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t beg = boff[b];
+    const int m_eff = (int)(boff[b + 1] - beg);
+    fst_d_row(order, r, mode, cmat, idx_aos + (size_t)perm[beg] * order, d);
+    for (int j = 0; j < jn; ++j) g[j] = 0.0f;
+    for (int m = 0; m < m_eff; ++m) {
+      const int32_t i = idx_aos[(size_t)perm[beg + m] * order + mode];
+      const float* crow = cmat[mode] + (size_t)i * r;
+      float acc = 0.0f;
+      for (int c = 0; c < r; ++c) {
+        float p = crow[c] * d[c];
+        acc = acc + p;
+      }
+      const float rm = vals[perm[beg + m]] - acc;
+      const float* arow = amat[mode] + (size_t)i * jn;
+      for (int j = 0; j < jn; ++j) {
+        float p = rm * arow[j];
+        g[j] = g[j] + p;
+      }
+    }
+    const float inv = 1.0f / (float)m_eff;
+    for (int j = 0; j < jn; ++j)
+      for (int c = 0; c < r; ++c) {
+        float* bb = bmat[mode] + (size_t)j * r + c;
+        float gd = g[j] * d[c];
+        float x = gd * inv;
+        float rb = reg_b * *bb;
+        float step = lr_b * (x - rb);
+        *bb = *bb + step;
+      }
+  }
+  fo_ccache_refresh(dims[mode], jn, r, amat[mode], bmat[mode], cmat[mode]);
+  free(d); free(g);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* fp64 evaluation (model.cpp:70-92, evaluation.cpp:10-72).                 */
 
 double fo_predict(int order, const int32_t* ranks, int r, float* const* amat,

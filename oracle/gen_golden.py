@@ -104,6 +104,33 @@ def fasttucker(R):
                             counters=cnt, hp=np.array(list(hp.values()), np.float32), **plans)
 
 
+# FasterTucker baseline (§8 f4): (name, dims, nnz, ranks, R, cap, seed, canonical)
+FASTERTUCKER = [
+    ("fastertucker_j16", [30, 20, 10], 1000, [16, 16, 16], 16, 16, 1234, False),
+    ("fastertucker_ragged", [8, 6, 5], 200, [5, 4, 3], 4, 2, 99, False),
+    ("fastertucker_cap5", [30, 20, 10], 1000, [8, 12, 4], 6, 5, 7, False),
+    ("fastertucker_order4", [6, 5, 4, 3], 300, [4, 6, 4, 2], 5, 16, 5, False),
+    ("fastertucker_canonical", [20, 15, 10], 500, [8, 8, 8], 8, 16, 3, True),
+]
+
+
+def fastertucker(R):
+    for k, (name, dims, nnz, ranks, r, cap, seed, canon) in enumerate(FASTERTUCKER):
+        t = O.random_tensor(dims, nnz, 850 + k, 1.0, 5.0)
+        m = O.random_model(dims, ranks, r, 950 + k, 0.3)
+        hp = dict(lr_a=1e-2, lr_b=1e-2, reg_a=1e-3, reg_b=1e-3)
+        new, cnt = R.epoch_fastertucker(t, m, seed, batch=cap, workers=1, canonical=canon, **hp)
+        plans = {}
+        for n in range(t.order):  # the reference's complement-keyed sampler streams
+            for tag in (1, 2):
+                perm, boff = R.per_bucket_plan(t, n, cap, derive_seed(seed, [tag, n]), keying=1)
+                plans[f"plan{tag}_{n}"], plans[f"boff{tag}_{n}"] = perm, boff
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **tensor_fields(t),
+                            **model_fields(m, "m_"), **model_fields(new, "new_"),
+                            cap=np.int32(cap), seed=np.uint64(seed), canonical=np.int32(canon),
+                            counters=cnt, hp=np.array(list(hp.values()), np.float32), **plans)
+
+
 def main():
     R = O.REF
     if R is None:
@@ -111,9 +138,11 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     if "--fasttucker-only" in sys.argv:
         fasttucker(R)
+        fastertucker(R)
         return
     storec(R)
     fasttucker(R)
+    fastertucker(R)
     if "--storec-only" in sys.argv:
         return
     lr_a, reg_a = 0.05, 0.01

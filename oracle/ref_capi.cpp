@@ -280,6 +280,33 @@ int ref_epoch_fasttucker(void* t, void* m, float lr_a, float lr_b, float reg_a, 
   });
 }
 
+// ftkref::epoch_fastertucker with complement indices of every mode and a
+// freshly built C cache (as train() sets it up, decomposition.cpp:869-874).
+int ref_epoch_fastertucker(void* t, void* m, float lr_a, float lr_b, float reg_a, float reg_b,
+                           int batch, int workers, int canonical, uint64_t seed,
+                           int64_t* counters_out) {
+  return guarded([&] {
+    const auto& ts = *static_cast<ftkref::SparseTensor*>(t);
+    auto& md = *static_cast<ftkref::Model*>(m);
+    std::vector<ftkref::ModeIndex> comp;
+    for (int n = 0; n < ts.order; ++n)
+      comp.push_back(ftkref::build_mode_index(ts, n, ftkref::Keying::kFixedComplement));
+    ftkref::CCache cache;
+    cache.build(md, nullptr);
+    ftkref::EpochOptions eo;
+    eo.workers = workers;
+    eo.canonical_order = canonical != 0;
+    auto st = ftkref::epoch_fastertucker(ts, comp, md, cache,
+                                         hyper(lr_a, lr_b, reg_a, reg_b, 1, batch), eo, seed);
+    if (counters_out) {
+      const ftkref::CostCounters* cs[2] = {&st.factor, &st.core};
+      for (int p = 0; p < 2; ++p)
+        for (int s = 0; s < ftkref::kStages; ++s)
+          counters_out[p * ftkref::kStages + s] = cs[p]->total(static_cast<ftkref::Stage>(s));
+    }
+  });
+}
+
 // Per-epoch trajectory of ftkref::train (plus variant).
 int ref_train(void* train, void* test, void* m, float lr_a, float lr_b,
               float reg_a, float reg_b, int epochs, int batch, int workers,

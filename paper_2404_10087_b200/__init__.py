@@ -41,7 +41,8 @@ EXPORTS = (
     "ftkcu_comm_allreduce_grad", "ftkcu_tensor_set_cells", "ftkcu_factor_phase_cell",
     "ftkcu_comm_sendrecv_rows", "ftkcu_comm_bcast_rows", "ftkcu_comm_allreduce_f64",
     "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch", "ftkcu_fasttucker_factor",
-    "ftkcu_fasttucker_core",
+    "ftkcu_fasttucker_core", "ftkcu_ccache_upload", "ftkcu_ccache_download",
+    "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core",
 )
 
 
@@ -81,6 +82,12 @@ def load_library(path: str = LIB_PATH):
                                           C.c_int32, C.c_float, C.c_float, _f64p]
     L.ftkcu_fasttucker_core.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, C.c_int32,
                                         C.c_float, C.c_float, C.c_int, _f64p]
+    L.ftkcu_ccache_upload.argtypes = [C.c_void_p, _fpp]
+    L.ftkcu_ccache_download.argtypes = [C.c_void_p, _fpp]
+    L.ftkcu_fastertucker_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
+                                            C.c_int64, C.c_float, C.c_float, _f64p]
+    L.ftkcu_fastertucker_core.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
+                                          C.c_int64, C.c_float, C.c_float, _f64p]
     L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.restype = C.c_int64
@@ -255,6 +262,34 @@ class Session:
         ms = C.c_double(0.0)
         self._ck(self.lib.ftkcu_fasttucker_core(self.h, slot, mode, _p(pa, _i64p), M, lr_b,
                                                 reg_b, schedule, C.byref(ms) if timed else None))
+        return ms.value
+
+    def ccache_upload(self, cache):
+        """The FasterTucker C cache (list of dims[n] x R fp32 arrays) to the device."""
+        cs = [np.ascontiguousarray(c, np.float32) for c in cache]
+        self._ck(self.lib.ftkcu_ccache_upload(self.h, _ptrs(cs)))
+
+    def ccache_download(self):
+        out = [np.empty((int(d), self.r), np.float32) for d in self.dims]
+        self._ck(self.lib.ftkcu_ccache_download(self.h, _ptrs(out)))
+        return out
+
+    def fastertucker_factor(self, slot, mode, perm, row_off, lr_a=1e-3, reg_a=1e-4, timed=True):
+        pa = np.ascontiguousarray(perm, np.int64)
+        ro = np.ascontiguousarray(row_off, np.int64)
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_fastertucker_factor(self.h, slot, mode, _p(pa, _i64p),
+                                                    _p(ro, _i64p), ro.size - 1, lr_a, reg_a,
+                                                    C.byref(ms) if timed else None))
+        return ms.value
+
+    def fastertucker_core(self, slot, mode, perm, batch_off, lr_b=1e-3, reg_b=1e-4, timed=True):
+        pa = np.ascontiguousarray(perm, np.int64)
+        bo = np.ascontiguousarray(batch_off, np.int64)
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_fastertucker_core(self.h, slot, mode, _p(pa, _i64p),
+                                                  _p(bo, _i64p), bo.size - 1, lr_b, reg_b,
+                                                  C.byref(ms) if timed else None))
         return ms.value
 
     def eval(self, slot=1, workers=1, reg_a=0.0, reg_b=0.0):

@@ -356,8 +356,9 @@ __global__ void ccache_kernel(const float* __restrict__ a, const float* __restri
 }  // namespace
 
 cudaError_t launch_ccache(const KView& v, const int32_t* dims, float* const* out,
-                          cudaStream_t st) {
+                          cudaStream_t st, int only_mode) {
   for (int n = 0; n < v.order; ++n) {
+    if (only_mode >= 0 && n != only_mode) continue;
     const int64_t total = (int64_t)dims[n] * v.r;
     if (total == 0) continue;
     const size_t bytes = sizeof(float) * v.j[n] * v.r;

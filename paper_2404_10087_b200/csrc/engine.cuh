@@ -152,6 +152,19 @@ size_t ft_core_smem(const KView& v, int cap);
 cudaError_t launch_ft_core(const KView& v, int mode, const int64_t* perm, int cap, float lr_b,
                            float reg_b, bool hogwild, cudaStream_t st);
 
+// ---- FasterTucker baseline (fst_kernels.cu) -------
+// Factor block of `mode`: perm = the complement-keyed per-bucket plan's
+// positions regrouped by mode-n row (plan order inside a row), goff the
+// ngroups + 1 group offsets.  v.cc: the C cache of every mode.
+cudaError_t launch_fst_factor(const KView& v, int mode, const int64_t* perm, const int64_t* goff,
+                              int64_t ngroups, float lr_a, float reg_a, cudaStream_t st);
+// Core block of `mode`: batches [boff[b], boff[b+1]) of perm in order.
+// scratch: at least fst_core_scratch_floats(v, mode) floats.
+size_t fst_core_scratch_floats(const KView& v, int mode);
+cudaError_t launch_fst_core(const KView& v, int mode, const int64_t* perm, const int64_t* boff,
+                            int64_t nbatches, float lr_b, float reg_b, float* scratch,
+                            cudaStream_t st);
+
 // ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,
                               float lr_a, float reg_a, int blocks_per_sm, int atomic_update,
@@ -169,7 +182,7 @@ cudaError_t launch_big_core(const KView& v, const int32_t* dims, int64_t mul, in
 // CCache::refresh for every mode (decomposition.cpp:89-107): out[n][i][r] =
 // sum_j A_n[i][j] B_n[j][r], j ascending, fp32 multiply then add (no FMA).
 cudaError_t launch_ccache(const KView& v, const int32_t* dims, float* const* out,
-                          cudaStream_t st);
+                          cudaStream_t st, int only_mode = -1);
 cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                             float* grad, int blocks_per_sm, float* scratch,
                             size_t scratch_bytes, cudaStream_t st);

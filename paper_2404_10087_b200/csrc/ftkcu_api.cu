@@ -783,6 +783,112 @@ int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* p
   return finish_timing(s, ms);
 }
 
+// ---- FasterTucker baseline (epoch_fastertucker, decomposition.cpp:772-843) --
+
+static int ensure_ccache(ftkcu_session* s) {
+  DevModel& m = s->model;
+  for (int n = 0; n < m.order; ++n)
+    if (!m.cc[n]) CK(cudaMalloc(&m.cc[n], sizeof(float) * ((size_t)m.dims[n] * m.r + 1)));
+  return FTKCU_OK;
+}
+
+int ftkcu_ccache_upload(ftkcu_session* s, const float* const* C) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  if (!C) return fail(s, FTKCU_ERR_ARG, "null cache");
+  if ((rc = ensure_ccache(s))) return rc;
+  const DevModel& m = s->model;
+  for (int n = 0; n < m.order; ++n)
+    CK(cudaMemcpyAsync(m.cc[n], C[n], sizeof(float) * (size_t)m.dims[n] * m.r,
+                       cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return FTKCU_OK;
+}
+
+int ftkcu_ccache_download(ftkcu_session* s, float* const* C) {
+  int rc = bind(s);
+  if (rc) return rc;
+  const DevModel& m = s->model;
+  if (!s->have_model || !m.cc[0]) return fail(s, FTKCU_ERR_STATE, "no C cache on the device");
+  if (!C) return fail(s, FTKCU_ERR_ARG, "null cache");
+  for (int n = 0; n < m.order; ++n)
+    CK(cudaMemcpyAsync(C[n], m.cc[n], sizeof(float) * (size_t)m.dims[n] * m.r,
+                       cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return FTKCU_OK;
+}
+
+static int fst_view(ftkcu_session* s, int slot, int mode, KView* out) {
+  int rc = check_ready(s, slot);
+  if (rc) return rc;
+  DevTensor& t = s->slots[slot];
+  if (t.order < 2) return fail(s, FTKCU_ERR_ARG, "FasterTucker needs order >= 2");
+  if (mode < 0 || mode >= t.order) return fail(s, FTKCU_ERR_ARG, "mode %d out of range", mode);
+  if (!s->model.cc[0]) return fail(s, FTKCU_ERR_STATE, "C cache must be uploaded first");
+  *out = make_view(s, t, false);
+  for (int n = 0; n < t.order; ++n) out->cc[n] = s->model.cc[n];
+  return FTKCU_OK;
+}
+
+int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                              const int64_t* row_off, int64_t nrows, float lr_a, float reg_a,
+                              double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  KView v;
+  if ((rc = fst_view(s, slot, mode, &v))) return rc;
+  if (nrows < 0 || (v.nnz > 0 && (!perm || !row_off)))
+    return fail(s, FTKCU_ERR_ARG, "row-grouped plan missing");
+  if (nrows > 0 && (row_off[0] != 0 || row_off[nrows] != v.nnz))
+    return fail(s, FTKCU_ERR_ARG, "row offsets must span [0, nnz]");
+  if ((rc = upload_perm(s, perm, v.nnz))) return rc;
+  if ((size_t)(nrows + 1) > s->boff_cap) {
+    if (s->d_boff) CK(cudaFree(s->d_boff));
+    s->d_boff = nullptr;
+    CK(cudaMalloc(&s->d_boff, sizeof(int64_t) * (nrows + 1)));
+    s->boff_cap = nrows + 1;
+  }
+  CK(cudaMemcpyAsync(s->d_boff, row_off, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice,
+                     s->stream));
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(launch_fst_factor(v, mode, s->d_perm, s->d_boff, nrows, lr_a, reg_a, s->stream));
+  // the block barrier's cache refresh of this mode (decomposition.cpp:810)
+  CK(launch_ccache(v, s->model.dims, s->model.cc, s->stream, mode));
+  s->launches += 2;
+  return finish_timing(s, ms);
+}
+
+int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm,
+                            const int64_t* batch_off, int64_t nbatches, float lr_b, float reg_b,
+                            double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  KView v;
+  if ((rc = fst_view(s, slot, mode, &v))) return rc;
+  if (nbatches < 0 || (v.nnz > 0 && (!perm || !batch_off)))
+    return fail(s, FTKCU_ERR_ARG, "plan missing");
+  if (nbatches > 0 && (batch_off[0] != 0 || batch_off[nbatches] != v.nnz))
+    return fail(s, FTKCU_ERR_ARG, "batch offsets must span [0, nnz]");
+  if (v.j[mode] > 128) return fail(s, FTKCU_ERR_ARG, "FasterTucker core block supports J <= 128");
+  if ((rc = upload_perm(s, perm, v.nnz))) return rc;
+  if ((size_t)(nbatches + 1) > s->boff_cap) {
+    if (s->d_boff) CK(cudaFree(s->d_boff));
+    s->d_boff = nullptr;
+    CK(cudaMalloc(&s->d_boff, sizeof(int64_t) * (nbatches + 1)));
+    s->boff_cap = nbatches + 1;
+  }
+  CK(cudaMemcpyAsync(s->d_boff, batch_off, sizeof(int64_t) * (nbatches + 1),
+                     cudaMemcpyHostToDevice, s->stream));
+  if ((rc = ensure_scratch(s, sizeof(float) * fst_core_scratch_floats(v, mode)))) return rc;
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(launch_fst_core(v, mode, s->d_perm, s->d_boff, nbatches, lr_b, reg_b,
+                     static_cast<float*>(s->scratch), s->stream));
+  CK(launch_ccache(v, s->model.dims, s->model.cc, s->stream, mode));
+  s->launches += 2 + 2 * ((nbatches + (1 << 20) - 1) >> 20);
+  return finish_timing(s, ms);
+}
+
 int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offsets, int ncells) {
   int rc = bind(s);
   if (rc) return rc;

@@ -223,6 +223,43 @@ int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, 
   });
 }
 
+// ftk::epoch_fastertucker with complement indices and a freshly built C cache.
+int ftkh_epoch_fastertucker(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
+                            int64_t nnz, const int32_t* idx, const float* vals, float* const* a,
+                            float* const* b, float lr_a, float lr_b, float reg_a, float reg_b,
+                            int m, int canonical, uint64_t seed, double* seconds2,
+                            int64_t* counters) {
+  return guarded([&] {
+    SparseTensor t = make_tensor(order, dims, nnz, idx, vals);
+    Model md = make_model(order, dims, ranks, r, a, b);
+    std::vector<ModeIndex> comp;
+    for (int n = 0; n < order; ++n)
+      comp.push_back(build_mode_index(t, n, Keying::kFixedComplement));
+    CCache cache;
+    cache.build(md, nullptr);
+    EpochOptions eo;
+    eo.canonical_order = canonical != 0;
+    EpochStats st;
+    try {
+      st = epoch_fastertucker(t, comp, md, cache, hyper(lr_a, lr_b, reg_a, reg_b, 1, m), eo,
+                              seed);
+    } catch (...) {
+      copy_back(md, a, b);
+      throw;
+    }
+    copy_back(md, a, b);
+    if (seconds2) {
+      seconds2[0] = st.seconds_factor;
+      seconds2[1] = st.seconds_core;
+    }
+    if (counters)
+      for (int s = 0; s < kStages; ++s) {
+        counters[s] = st.factor.total(static_cast<Stage>(s));
+        counters[kStages + s] = st.core.total(static_cast<Stage>(s));
+      }
+  });
+}
+
 int ftkh_epoch_plus(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
                     int64_t nnz, const int32_t* idx, const float* vals, float* const* a,
                     float* const* b, float lr_a, float lr_b, float reg_a, float reg_b, int m,

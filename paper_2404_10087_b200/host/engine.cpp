@@ -306,6 +306,115 @@ EpochStats run_epoch_fasttucker(const SparseTensor& t, int slot, const Model& m,
   return st;
 }
 
+// FasterTucker's per-batch billing (update_factor_fastertucker_impl /
+// update_core_fastertucker_impl, decomposition.cpp:420-533) over the plan's
+// batches, plus the block barrier's cache refresh as overhead (:810, :837).
+void bill_fastertucker(CostCounters& cc, const Model& m, int mode, const EpochPlan& plan,
+                       bool factor) {
+  const int N = m.order();
+  const size64 R = m.r, Jn = m.ranks[mode];
+  const size64 combine = N >= 2 ? N - 2 : 0;
+  for (size64 b = 0; b < plan.batches(); ++b) {
+    const size64 me = plan.desc(b).len;
+    const bool full = me == static_cast<size64>(plan.batch_size());
+    cc.count_batch(mode, full);
+    cc.add(mode, kDStage, combine * R, full);
+    if (factor) {
+      cc.add(mode, kRead, (N - 1) * R + me * Jn + Jn * R, full);
+      cc.add(mode, kBdtStage, Jn * R, full);
+      cc.add(mode, kOther, me * Jn, full);
+      cc.add(mode, kUpdate, me * Jn, full);
+    } else {
+      cc.add(mode, kRead, (N - 1) * R + me * Jn + me * R + Jn * R, full);
+      cc.add(mode, kOther, me * R + me * Jn, full);
+      cc.add(mode, kBdtStage, Jn * R, full);
+      cc.add(mode, kUpdate, Jn * R, full);
+    }
+  }
+  cc.add_overhead(kOther, static_cast<size64>(m.dims[mode]) * Jn * R);
+}
+
+// Plan positions regrouped by mode-n row, plan order kept inside a row
+// (stable counting sort); out_off gets the group offsets.
+void group_by_row(const SparseTensor& t, const std::vector<size64>& plan, int mode,
+                  std::vector<int64_t>& out, std::vector<int64_t>& out_off) {
+  const index_t rows = t.dims[mode];
+  std::vector<int64_t> count(static_cast<std::size_t>(rows) + 1, 0);
+  for (size64 p : plan) ++count[t.entry(p)[mode] + 1];
+  for (index_t i = 0; i < rows; ++i) count[i + 1] += count[i];
+  out.assign(plan.size(), 0);
+  std::vector<int64_t> at(count.begin(), count.end() - 1);
+  for (size64 p : plan) out[at[t.entry(p)[mode]]++] = static_cast<int64_t>(p);
+  out_off.clear();
+  out_off.push_back(0);
+  for (index_t i = 0; i < rows; ++i)
+    if (count[i + 1] > count[i]) out_off.push_back(count[i + 1]);
+}
+
+std::vector<int64_t> batch_offsets(const EpochPlan& plan) {
+  std::vector<int64_t> off;
+  off.reserve(static_cast<std::size_t>(plan.batches()) + 1);
+  for (size64 b = 0; b < plan.batches(); ++b) off.push_back(plan.desc(b).offset);
+  off.push_back(static_cast<int64_t>(plan.positions().size()));
+  return off;
+}
+
+// One FasterTucker epoch on the resident model and device C cache
+// (epoch_fastertucker, decomposition.cpp:772-843).
+EpochStats run_epoch_fastertucker(const SparseTensor& t, int slot, const Model& m,
+                                  const std::vector<ModeIndex>& complement, const Hyperparams& h,
+                                  const EpochOptions& opts, std::uint64_t seed) {
+  ftkcu_session* s = session();
+  const int N = m.order();
+  require(static_cast<int>(complement.size()) == N, "need one complement index per mode");
+  require(!opts.eager_refresh, "eager_refresh is not supported by the device FasterTucker");
+  const index_t cap = opts.canonical_order ? 1 : h.batch_size;
+  EpochStats st;
+  st.factor.reset(N);
+  st.core.reset(N);
+  double total[2] = {0.0, 0.0};
+  std::vector<int64_t> perm, off;
+  for (int phase = 0; phase < 2; ++phase) {
+    for (int mode = 0; mode < N; ++mode) {
+      Rng rng(derive_seed(seed, {static_cast<std::uint64_t>(phase + 1),
+                                 static_cast<std::uint64_t>(mode)}));
+      EpochPlan plan = opts.canonical_order ? EpochPlan::canonical(t)
+                                            : EpochPlan::per_bucket(t, complement[mode], cap, rng);
+      double ms = 0.0;
+      if (phase == 0) {
+        group_by_row(t, plan.positions(), mode, perm, off);
+        check(ftkcu_fastertucker_factor(s, slot, mode, perm.data(), off.data(),
+                                        static_cast<int64_t>(off.size()) - 1, h.lr_a, h.reg_a,
+                                        &ms));
+        bill_fastertucker(st.factor, m, mode, plan, true);
+      } else {
+        off = batch_offsets(plan);
+        check(ftkcu_fastertucker_core(s, slot, mode, plan.positions().data(), off.data(),
+                                      static_cast<int64_t>(off.size()) - 1, h.lr_b, h.reg_b, &ms));
+        bill_fastertucker(st.core, m, mode, plan, false);
+      }
+      total[phase] += ms;
+    }
+  }
+  st.seconds_factor = total[0] * 1e-3;
+  st.seconds_core = total[1] * 1e-3;
+  return st;
+}
+
+void upload_cache(CCache& cache) {
+  auto& c = cache.storage();
+  std::vector<const float*> p(c.size());
+  for (std::size_t n = 0; n < c.size(); ++n) p[n] = c[n].data();
+  check(ftkcu_ccache_upload(session(), p.data()));
+}
+
+void download_cache(CCache& cache) {
+  auto& c = cache.storage();
+  std::vector<float*> p(c.size());
+  for (std::size_t n = 0; n < c.size(); ++n) p[n] = c[n].data();
+  check(ftkcu_ccache_download(session(), p.data()));
+}
+
 std::string num_json(double v) {
   if (!std::isfinite(v)) return "null";
   char buf[64];
@@ -342,6 +451,60 @@ EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
     throw;
   }
   download_model(m);
+  return st;
+}
+
+void CCache::init(const Model& m) {
+  const int n = m.order();
+  r_ = m.r;
+  c_.assign(n, {});
+  for (int k = 0; k < n; ++k) c_[k].assign(static_cast<std::size_t>(m.dims[k]) * m.r, 0.0f);
+  fresh_.assign(n, 0);
+}
+
+void CCache::build(const Model& m, CostCounters* cc) {
+  if (c_.empty()) init(m);
+  for (int k = 0; k < m.order(); ++k) refresh(m, k, cc);
+}
+
+void CCache::refresh(const Model& m, int mode, CostCounters* cc) {
+  require(!c_.empty(), "cache not initialized");
+  const index_t jn = m.ranks[mode], r = m.r;
+  const real* b = m.b[mode].data();
+  for (index_t i = 0; i < m.dims[mode]; ++i) {
+    const real* arow = m.a_row(mode, i);
+    real* crow = c_[mode].data() + static_cast<std::size_t>(i) * r;
+    for (index_t col = 0; col < r; ++col) {
+      real acc = 0.0f;
+      for (index_t j = 0; j < jn; ++j) acc += arow[j] * b[static_cast<std::size_t>(j) * r + col];
+      crow[col] = acc;
+    }
+  }
+  fresh_[mode] = 1;
+  if (cc) cc->add_overhead(kOther, static_cast<size64>(m.dims[mode]) * jn * r);
+}
+
+EpochStats epoch_fastertucker(const SparseTensor& t, const std::vector<ModeIndex>& complement,
+                              Model& m, CCache& cache, const Hyperparams& h,
+                              const EpochOptions& opts, std::uint64_t seed) {
+  require(static_cast<int>(complement.size()) == m.order(),
+          "need one complement index per mode");
+  require(cache.ready(), "C cache must be built before the first epoch");
+  std::lock_guard<std::mutex> lk(g_mu);
+  apply_options(session());
+  const int slot = ensure_tensor(t);
+  upload_model(m);
+  upload_cache(cache);
+  EpochStats st;
+  try {
+    st = run_epoch_fastertucker(t, slot, m, complement, h, opts, seed);
+  } catch (...) {
+    download_model(m);
+    throw;
+  }
+  download_model(m);
+  download_cache(cache);
+  for (int n = 0; n < m.order(); ++n) cache.mark_fresh(n);  // each block refreshed its mode
   return st;
 }
 
@@ -419,9 +582,7 @@ History train(const SparseTensor& train_set, const SparseTensor* test_set, Model
   require(m.order() == train_set.order, "model/tensor order mismatch");
   for (int n = 0; n < m.order(); ++n)
     require(m.dims[n] >= train_set.dims[n], "model dims too small for tensor");
-  require(opts.variant != Variant::kFasterTucker,
-          "the B200 engine implements the plus and fasttucker variants (fastertucker is not "
-          "built yet)");
+
   const int workers = resolve_workers(opts.workers);
   EpochOptions eo;
   eo.workers = workers;
@@ -435,17 +596,27 @@ History train(const SparseTensor& train_set, const SparseTensor* test_set, Model
   if (test_set != nullptr && test_set->nnz() > 0) {
     test_slot = ensure_tensor(*test_set);
   }
-  std::vector<ModeIndex> fixed;  // FastTucker: fixed-mode indices, built once
-  if (opts.variant == Variant::kFastTucker)
+  std::vector<ModeIndex> fixed;  // fixed-mode (FastTucker) / complement (FasterTucker)
+  if (opts.variant != Variant::kPlus)
     for (int n = 0; n < m.order(); ++n)
-      fixed.push_back(build_mode_index(train_set, n, Keying::kFixedMode));
+      fixed.push_back(build_mode_index(train_set, n,
+                                       opts.variant == Variant::kFastTucker
+                                           ? Keying::kFixedMode
+                                           : Keying::kFixedComplement));
   upload_model(m);
+  if (opts.variant == Variant::kFasterTucker) {  // cache.build once (decomposition.cpp:873)
+    CCache cache;
+    cache.build(m, nullptr);
+    upload_cache(cache);
+  }
   for (int epoch = 1; epoch <= h.epochs; ++epoch) {
     const std::uint64_t es = derive_seed(opts.seed, {static_cast<std::uint64_t>(epoch)});
     EpochRecord rec;
     rec.epoch = epoch;
     rec.stats = opts.variant == Variant::kFastTucker
                     ? run_epoch_fasttucker(train_set, slot, m, fixed, h, eo, es)
+                : opts.variant == Variant::kFasterTucker
+                    ? run_epoch_fastertucker(train_set, slot, m, fixed, h, eo, es)
                     : run_epoch(train_set, slot, m, h, eo, es);
     rec.seconds = rec.stats.seconds_factor + rec.stats.seconds_core;
     rec.train_loss = device_loss(slot, h.reg_a, h.reg_b, workers);

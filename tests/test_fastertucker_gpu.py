@@ -1,0 +1,64 @@
+"""FasterTucker baseline on the device (fst_kernels.cu): bit-identical to the
+reference's workers = 1 epoch, at full parallelism (row chains in the
+factor block, per-element B recurrences in the core block)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from golden_io import bits_equal, load, model, names, tensor
+from paper_2404_10087_b200 import host
+from test_fastertucker import group_by_row, plan
+
+pytestmark = pytest.mark.gpu
+CO = O.COracle
+
+
+@pytest.mark.parametrize("name", names("fastertucker_"))
+def test_epoch_fastertucker_matches_reference(name):
+    z = load(name)
+    t, m = tensor(z), model(z, "m_")
+    lr_a, lr_b, reg_a, reg_b = (float(x) for x in z["hp"])
+    secs, cnt = host.epoch_fastertucker(t.dims, m.ranks, m.r, t.idx, t.vals, m.a, m.b,
+                                        int(z["seed"]), lr_a, lr_b, reg_a, reg_b, int(z["cap"]),
+                                        bool(z["canonical"]))
+    want = model(z, "new_")
+    for n in range(m.order):
+        assert bits_equal(m.a[n], want.a[n]), f"A{n}"
+        assert bits_equal(m.b[n], want.b[n]), f"B{n}"
+    assert np.array_equal(cnt, z["counters"])
+
+
+CASES = [  # dims, nnz, ranks, R, cap
+    ([400, 300, 50], 40000, [32, 32, 32], 32, 16),
+    ([60, 50, 40], 30000, [20, 12, 7], 9, 3),
+    ([30, 25, 20, 15], 20000, [8, 16, 4, 8], 8, 16),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"N{len(c[0])}-J{c[2][0]}-R{c[3]}-M{c[4]}")
+def test_blocks_match_oracle(session, case):
+    dims, nnz, ranks, r, cap = case
+    t = O.random_tensor(dims, nnz, 31, 1.0, 5.0)
+    m = O.random_model(dims, ranks, r, 32, 0.1)
+    want = m.copy()
+    cache = CO.ccache_build(want)
+    session.upload_tensor(0, t.dims, t.idx, t.vals)
+    session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+    session.ccache_upload(cache)
+    for factor, tag in ((True, 1), (False, 2)):
+        for mode in range(t.order):
+            perm, bo = plan(t, mode, cap, 55, tag, False)
+            if factor:
+                g, off = group_by_row(t, perm, mode)
+                session.fastertucker_factor(0, mode, g, off, 1e-3, 1e-4)
+            else:
+                session.fastertucker_core(0, mode, perm, bo, 1e-3, 1e-4)
+            CO.fastertucker_block(factor, t, want, cache, perm, bo, mode, 1e-3, 1e-4)
+    a, b = session.download_model()
+    dev_cache = session.ccache_download()
+    for n in range(t.order):
+        assert np.isfinite(want.b[n]).all() and np.isfinite(want.a[n]).all()
+        assert bits_equal(a[n], want.a[n]), f"A{n}"
+        assert bits_equal(b[n], want.b[n]), f"B{n}"
+        assert bits_equal(dev_cache[n], cache[n]), f"cache {n}"
+        assert not np.array_equal(want.b[n], m.b[n])
