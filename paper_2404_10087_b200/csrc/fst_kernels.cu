@@ -97,24 +97,25 @@ fst_factor_kernel(KView v, int mode, const int64_t* __restrict__ perm,
 }
 
 // Per batch: d, residuals from the block-entry cache of mode n
-// (:506-512), g = A_psi^T r rows ascending (:515-522), 1/M.  One warp per
-// batch; out rows [g (J) | d (R) | inv].
+// (:506-512), g = A_psi^T r rows ascending (:515-522), and the step input
+// x[j][c] = (g_j d_c) (1/M) of every element of B^(n) (:529).  One warp per
+// batch; out row b holds the J x R values of x.
 __global__ void __launch_bounds__(kFstWarps * 32)
 fst_core_prep_kernel(KView v, int mode, const int64_t* __restrict__ perm,
                      const int64_t* __restrict__ boff, int64_t b0, int64_t nb,
                      float* __restrict__ out) {
   extern __shared__ float smem[];
-  const int r = v.r, jn = v.j[mode], stride = jn + r + 1;
+  const int r = v.r, jn = v.j[mode];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float* d = smem + (size_t)wib * (r + 32);
-  float* res = d + r;  // 32 residuals at a time
+  float* d = smem + (size_t)wib * (r + jn + 32);
+  float* g = d + r;
+  float* res = g + jn;  // 32 residuals at a time
   for (int64_t b = (int64_t)blockIdx.x * kFstWarps + wib; b < nb;
        b += (int64_t)gridDim.x * kFstWarps) {
     const int64_t beg = boff[b0 + b], end = boff[b0 + b + 1];
     const int m_eff = (int)(end - beg);
     d_row(v, mode, perm[beg], d, lane, 32);
     __syncwarp();
-    float* o = out + (size_t)b * stride;
     // g accumulates over rows ascending; lanes own j, rows come 32 at a time
     float gacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     for (int m0 = 0; m0 < m_eff; m0 += 32) {
@@ -140,32 +141,58 @@ fst_core_prep_kernel(KView v, int mode, const int64_t* __restrict__ perm,
     }
     for (int q = 0; q < 4; ++q) {
       const int k = lane + 32 * q;
-      if (k < jn) o[k] = gacc[q];
+      if (k < jn) g[k] = gacc[q];
     }
-    for (int c = lane; c < r; c += 32) o[jn + c] = d[c];
-    if (lane == 0) o[jn + r] = __fdiv_rn(1.0f, (float)m_eff);
+    __syncwarp();
+    const float inv = __fdiv_rn(1.0f, (float)m_eff);
+    float* o = out + (size_t)b * jn * r;
+    for (int e = lane; e < jn * r; e += 32) {
+      const int k = e / r, c = e - k * r;
+      o[e] = fmul(fmul(g[k], d[c]), inv);
+    }
     __syncwarp();
   }
 }
 
-// b <- b + lr ((g_j d_c) (1/M) - reg b) over the batches in order
-// (:525-532), one thread per element of B^(n).
-__global__ void fst_core_chain_kernel(float* __restrict__ bm, int jn, int r,
-                                      const float* __restrict__ rows, int64_t nb, float lr,
-                                      float reg) {
+// b <- b + lr (x - reg b) over the batches in order (:525-532), one thread
+// per element of B^(n).  The x stream is triple-buffered in registers, two
+// 32-step rounds ahead (one block reads 1 KB per step at J = R = 16: the
+// loads, not the 4-op dependent chain, would otherwise set the pace).
+constexpr int kAhead = 32;
+
+__global__ void __launch_bounds__(256)
+fst_core_chain_kernel(float* __restrict__ bm, int elems, const float* __restrict__ xs, int64_t nb,
+                      float lr, float reg) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= jn * r) return;
-  const int k = e / r, c = e - k * r, stride = jn + r + 1;
+  if (e >= elems) return;
   float b = bm[e];
-  for (int64_t t = 0; t < nb; ++t) {
-    const float* o = rows + (size_t)t * stride;
-    const float x = fmul(fmul(__ldg(o + k), __ldg(o + jn + c)), __ldg(o + jn + r));
-    b = fadd(b, fmul(lr, fsub(x, fmul(reg, b))));
+  float cur[kAhead], nx1[kAhead], nx2[kAhead];
+  const float* p = xs + e;
+  // unpredicated: the scratch holds 2 kAhead steps of slack past any chunk
+  // (steps past nb are loaded but never used)
+  auto load = [&](float (&dst)[kAhead], int64_t t0) {
+    const float* q = p + (size_t)t0 * elems;
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i) dst[i] = __ldcs(q + i * elems);
+  };
+  load(cur, 0);
+  load(nx1, kAhead);
+  for (int64_t t0 = 0; t0 < nb; t0 += kAhead) {
+    load(nx2, t0 + 2 * kAhead);  // two rounds ahead: covers the L2 latency
+    const int n = (nb - t0) < kAhead ? (int)(nb - t0) : kAhead;
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i)
+      if (i < n) b = fadd(b, fmul(lr, fsub(cur[i], fmul(reg, b))));
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i) {
+      cur[i] = nx1[i];
+      nx1[i] = nx2[i];
+    }
   }
   bm[e] = b;
 }
 
-constexpr int64_t kChunk = 1 << 20;  // batches per prep / chain round
+constexpr size_t kScratchFloats = (size_t)16 << 20;  // 64 MB of step inputs per round (L2-resident)
 
 }  // namespace
 
@@ -186,29 +213,30 @@ cudaError_t launch_fst_factor(const KView& v, int mode, const int64_t* perm, con
 }
 
 size_t fst_core_scratch_floats(const KView& v, int mode) {
-  return (size_t)kChunk * (v.j[mode] + v.r + 1);
+  return kScratchFloats + (size_t)3 * kAhead * v.j[mode] * v.r;
 }
 
 cudaError_t launch_fst_core(const KView& v, int mode, const int64_t* perm, const int64_t* boff,
                             int64_t nbatches, float lr_b, float reg_b, float* scratch,
                             cudaStream_t st) {
   if (v.j[mode] > 128) return cudaErrorInvalidValue;
-  const size_t bytes = sizeof(float) * (v.r + 32) * kFstWarps;
+  const size_t bytes = sizeof(float) * (v.r + v.j[mode] + 32) * kFstWarps;
   cudaError_t e = cudaFuncSetAttribute(fst_core_prep_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   float* bm = const_cast<float*>(v.b[mode]);
   const int elems = v.j[mode] * v.r;
-  for (int64_t b0 = 0; b0 < nbatches; b0 += kChunk) {
-    const int64_t nb = (nbatches - b0) < kChunk ? (nbatches - b0) : kChunk;
+  const int64_t chunk = (int64_t)(kScratchFloats / (size_t)elems);
+  for (int64_t b0 = 0; b0 < nbatches; b0 += chunk) {
+    const int64_t nb = (nbatches - b0) < chunk ? (nbatches - b0) : chunk;
     int64_t blocks = (nb + kFstWarps - 1) / kFstWarps;
     if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
     fst_core_prep_kernel<<<(int)blocks, kFstWarps * 32, bytes, st>>>(v, mode, perm, boff, b0, nb,
                                                                       scratch);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fst_core_chain_kernel<<<(elems + 127) / 128, 128, 0, st>>>(bm, v.j[mode], v.r, scratch, nb,
-                                                                lr_b, reg_b);
+    fst_core_chain_kernel<<<(elems + 255) / 256, 256, 0, st>>>(bm, elems, scratch, nb, lr_b,
+                                                                reg_b);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
