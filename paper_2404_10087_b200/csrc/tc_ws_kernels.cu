@@ -1066,15 +1066,20 @@ bool make_row_map16(CUtensorMap* tm, const __half* a, int64_t rows) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Timing experiments only (never set in production): FTKCU_WS_EXP bits
-// 1 / 2 / 4 / 8 / 16 drop the core slot hold / gathers / G GEMM / row copy /
-// factor write-back (scripts/ws_exp.sh).
+// Timing experiments only: FTKCU_WS_EXP bits 1 / 2 / 4 / 8 / 16 drop the
+// core slot hold / gathers / G GEMM / row copy / factor write-back
+// (scripts/ws_exp.sh).  Read only in an experiments build
+// (make EXPERIMENTS=1); the production library ignores the variable.
 int ws_exp_bits() {
+#ifdef FTKCU_EXPERIMENTS
   static const int bits = [] {
     const char* e = std::getenv("FTKCU_WS_EXP");
     return e ? std::atoi(e) : 0;
   }();
   return bits;
+#else
+  return 0;
+#endif
 }
 
 bool make_params(WsParams& p, const KView& v, const int32_t* dims, int64_t mul, int64_t add,
