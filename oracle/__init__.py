@@ -295,6 +295,7 @@ class _Ref:
         L.ref_train.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float,
                                 C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.c_uint64, _f64p, _f64p, _f64p, _f64p, _i64p, _i64p]
+        L.ref_train_variant.argtypes = list(L.ref_train.argtypes) + [C.c_int]
         L.ref_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int, _f64p]
         L.ref_evaluate.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _f64p, _f64p]
         L.ref_batch_probe.argtypes = [C.c_void_p, C.c_void_p, _i64p, C.c_int, C.c_int, C.c_float,
@@ -443,7 +444,8 @@ class _Ref:
             self.free_model(mh)
 
     def train(self, train: Tensor, test, m: Model, epochs, seed, lr_a=1e-3, lr_b=1e-3,
-              reg_a=1e-4, reg_b=1e-4, batch=16, workers=1, store_c=False):
+              reg_a=1e-4, reg_b=1e-4, batch=16, workers=1, store_c=False, variant=0):
+        """ftkref::train; variant 0 plus, 1 fasttucker, 2 fastertucker."""
         th = self.tensor(train)
         teh = self.tensor(test) if test is not None else None
         mh = self.model(m)
@@ -451,11 +453,10 @@ class _Ref:
         reads = np.zeros(epochs, np.int64)
         mults = np.zeros(epochs, np.int64)
         try:
-            self._check(self.lib.ref_train(th, teh, mh, lr_a, lr_b, reg_a, reg_b, epochs, batch,
-                                           workers, int(store_c), seed,
-                                           _p(out["loss"], _f64p), _p(out["rmse"], _f64p),
-                                           _p(out["mae"], _f64p), _p(out["seconds"], _f64p),
-                                           _p(reads, _i64p), _p(mults, _i64p)))
+            self._check(self.lib.ref_train_variant(
+                th, teh, mh, lr_a, lr_b, reg_a, reg_b, epochs, batch, workers, int(store_c),
+                seed, _p(out["loss"], _f64p), _p(out["rmse"], _f64p), _p(out["mae"], _f64p),
+                _p(out["seconds"], _f64p), _p(reads, _i64p), _p(mults, _i64p), int(variant)))
             out["reads"], out["mults"] = reads, mults
             out["model"] = self.model_to_np(mh, m)
             return out

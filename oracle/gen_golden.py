@@ -131,6 +131,22 @@ def fastertucker(R):
                             counters=cnt, hp=np.array(list(hp.values()), np.float32), **plans)
 
 
+def train_variants(R):
+    """Short train() trajectories of the convex baselines (variant 1, 2)."""
+    full = O.random_tensor([30, 25, 20], 2500, 510, 1.0, 5.0)
+    tr, te = R.split(full, 0.1, 9)
+    ranks, r = [8, 8, 8], 8
+    scale = R.default_init_scale(float(np.mean(np.abs(tr.vals))), 3, r, ranks)
+    m0 = R.init_model(full.dims, ranks, r, derive_seed(2, [77]), scale)
+    for variant, name in ((1, "fasttucker"), (2, "fastertucker")):
+        hist = R.train(tr, te, m0, epochs=3, seed=2, workers=1, variant=variant)
+        np.savez_compressed(os.path.join(OUT, f"train_{name}.npz"), full_dims=full.dims,
+                            tr_idx=tr.idx, tr_vals=tr.vals, te_idx=te.idx, te_vals=te.vals,
+                            **model_fields(m0, "m0_"), **model_fields(hist["model"], "final_"),
+                            loss=hist["loss"], rmse=hist["rmse"], mae=hist["mae"],
+                            reads=hist["reads"], mults=hist["mults"])
+
+
 def main():
     R = O.REF
     if R is None:
@@ -139,10 +155,12 @@ def main():
     if "--fasttucker-only" in sys.argv:
         fasttucker(R)
         fastertucker(R)
+        train_variants(R)
         return
     storec(R)
     fasttucker(R)
     fastertucker(R)
+    train_variants(R)
     if "--storec-only" in sys.argv:
         return
     lr_a, reg_a = 0.05, 0.01

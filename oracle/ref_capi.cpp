@@ -308,13 +308,16 @@ int ref_epoch_fastertucker(void* t, void* m, float lr_a, float lr_b, float reg_a
 }
 
 // Per-epoch trajectory of ftkref::train (plus variant).
-int ref_train(void* train, void* test, void* m, float lr_a, float lr_b,
-              float reg_a, float reg_b, int epochs, int batch, int workers,
-              int store_c, uint64_t seed, double* loss, double* rmse,
-              double* mae, double* seconds, int64_t* reads, int64_t* mults) {
+int ref_train_variant(void* train, void* test, void* m, float lr_a, float lr_b,
+                      float reg_a, float reg_b, int epochs, int batch, int workers,
+                      int store_c, uint64_t seed, double* loss, double* rmse,
+                      double* mae, double* seconds, int64_t* reads, int64_t* mults,
+                      int variant) {
   return guarded([&] {
     ftkref::TrainOptions to;
-    to.variant = ftkref::Variant::kPlus;
+    to.variant = variant == 1   ? ftkref::Variant::kFastTucker
+                 : variant == 2 ? ftkref::Variant::kFasterTucker
+                                : ftkref::Variant::kPlus;
     to.workers = workers;
     to.store_c = store_c != 0;
     to.seed = seed;
@@ -332,6 +335,14 @@ int ref_train(void* train, void* test, void* m, float lr_a, float lr_b,
       if (mults) mults[e] = hist[e].mults;
     }
   });
+}
+
+int ref_train(void* train, void* test, void* m, float lr_a, float lr_b,
+              float reg_a, float reg_b, int epochs, int batch, int workers,
+              int store_c, uint64_t seed, double* loss, double* rmse,
+              double* mae, double* seconds, int64_t* reads, int64_t* mults) {
+  return ref_train_variant(train, test, m, lr_a, lr_b, reg_a, reg_b, epochs, batch, workers,
+                           store_c, seed, loss, rmse, mae, seconds, reads, mults, 0);
 }
 
 int ref_loss(void* m, void* t, double reg_a, double reg_b, int workers,

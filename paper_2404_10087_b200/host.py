@@ -93,6 +93,7 @@ def lib():
                              C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_uint64, _f64p, _f64p, _f64p, _f64p, _i64p, _i64p, C.c_char_p,
                              C.c_int]
+    L.ftkh_train_variant.argtypes = list(L.ftkh_train.argtypes) + [C.c_int]
     L.ftkh_loss.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p, _fpp,
                             _fpp, C.c_double, C.c_double, C.c_int, _f64p]
     L.ftkh_evaluate.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p, _fpp,
@@ -274,9 +275,14 @@ def epoch_fastertucker(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e
     return secs, cnt
 
 
+VARIANTS = {"plus": 0, "fasttucker": 1, "fastertucker": 2}
+
+
 def train(dims, ranks, r, train_idx, train_vals, test_idx, test_vals, a, b, epochs, seed,
-          lr_a=1e-3, lr_b=1e-3, reg_a=1e-4, reg_b=1e-4, m=16, workers=1, store_c=False):
-    """ftk::train through the C++ API; mutates a/b; returns per-epoch history."""
+          lr_a=1e-3, lr_b=1e-3, reg_a=1e-4, reg_b=1e-4, m=16, workers=1, store_c=False,
+          variant="plus"):
+    """ftk::train through the C++ API (TrainOptions.variant); mutates a/b;
+    returns per-epoch history."""
     dims, ranks = _i32(dims), _i32(ranks)
     tri, trv = _i32(train_idx), np.ascontiguousarray(train_vals, np.float32)
     if test_idx is None:
@@ -289,13 +295,14 @@ def train(dims, ranks, r, train_idx, train_vals, test_idx, test_vals, a, b, epoc
     mults = np.zeros(epochs, np.int64)
     cap = 256 * max(epochs, 1) + 64
     buf = C.create_string_buffer(cap)
-    _ck(lib().ftkh_train(dims.size, _p(dims, _i32p), _p(ranks, _i32p), r, trv.size,
-                         _p(tri, _i32p), _p(trv, _f32p), nte, _p(tei, _i32p), _p(tev, _f32p),
-                         _ptrs(a), _ptrs(b), lr_a, lr_b, reg_a, reg_b, epochs, m, workers,
-                         int(store_c), seed & M64, _p(out["loss"], _f64p),
-                         _p(out["rmse"], _f64p), _p(out["mae"], _f64p),
-                         _p(out["seconds"], _f64p), _p(reads, _i64p), _p(mults, _i64p), buf,
-                         cap))
+    _ck(lib().ftkh_train_variant(dims.size, _p(dims, _i32p), _p(ranks, _i32p), r, trv.size,
+                                 _p(tri, _i32p), _p(trv, _f32p), nte, _p(tei, _i32p),
+                                 _p(tev, _f32p), _ptrs(a), _ptrs(b), lr_a, lr_b, reg_a, reg_b,
+                                 epochs, m, workers, int(store_c), seed & M64,
+                                 _p(out["loss"], _f64p), _p(out["rmse"], _f64p),
+                                 _p(out["mae"], _f64p), _p(out["seconds"], _f64p),
+                                 _p(reads, _i64p), _p(mults, _i64p), buf, cap,
+                                 VARIANTS[variant]))
     out["reads"], out["mults"] = reads, mults
     out["jsonl"] = buf.value.decode()
     return out

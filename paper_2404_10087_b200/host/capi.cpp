@@ -292,13 +292,15 @@ int ftkh_epoch_plus(int order, const int32_t* dims, const int32_t* ranks, int32_
   });
 }
 
-int ftkh_train(int order, const int32_t* dims, const int32_t* ranks, int32_t r, int64_t nnz,
-               const int32_t* idx, const float* vals, int64_t nnz_test, const int32_t* idx_test,
-               const float* vals_test, float* const* a, float* const* b, float lr_a, float lr_b,
-               float reg_a, float reg_b, int epochs, int m, int workers, int store_c,
-               uint64_t seed, double* loss_out, double* rmse_out, double* mae_out,
-               double* seconds_out, int64_t* reads_out, int64_t* mults_out, char* jsonl,
-               int jsonl_cap) {
+// ftk::train for a variant (0 plus, 1 fasttucker, 2 fastertucker).
+int ftkh_train_variant(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
+                       int64_t nnz, const int32_t* idx, const float* vals, int64_t nnz_test,
+                       const int32_t* idx_test, const float* vals_test, float* const* a,
+                       float* const* b, float lr_a, float lr_b, float reg_a, float reg_b,
+                       int epochs, int m, int workers, int store_c, uint64_t seed,
+                       double* loss_out, double* rmse_out, double* mae_out, double* seconds_out,
+                       int64_t* reads_out, int64_t* mults_out, char* jsonl, int jsonl_cap,
+                       int variant) {
   return guarded([&] {
     SparseTensor t = make_tensor(order, dims, nnz, idx, vals);
     SparseTensor te;
@@ -308,6 +310,9 @@ int ftkh_train(int order, const int32_t* dims, const int32_t* ranks, int32_t r, 
     to.workers = workers;
     to.store_c = store_c != 0;
     to.seed = seed;
+    to.variant = variant == 1   ? Variant::kFastTucker
+                 : variant == 2 ? Variant::kFasterTucker
+                                : Variant::kPlus;
     History h;
     try {
       h = train(t, nnz_test > 0 ? &te : nullptr, md, hyper(lr_a, lr_b, reg_a, reg_b, epochs, m),
@@ -332,6 +337,19 @@ int ftkh_train(int order, const int32_t* dims, const int32_t* ranks, int32_t r, 
       jsonl[jsonl_cap - 1] = '\0';
     }
   });
+}
+
+int ftkh_train(int order, const int32_t* dims, const int32_t* ranks, int32_t r, int64_t nnz,
+               const int32_t* idx, const float* vals, int64_t nnz_test, const int32_t* idx_test,
+               const float* vals_test, float* const* a, float* const* b, float lr_a, float lr_b,
+               float reg_a, float reg_b, int epochs, int m, int workers, int store_c,
+               uint64_t seed, double* loss_out, double* rmse_out, double* mae_out,
+               double* seconds_out, int64_t* reads_out, int64_t* mults_out, char* jsonl,
+               int jsonl_cap) {
+  return ftkh_train_variant(order, dims, ranks, r, nnz, idx, vals, nnz_test, idx_test, vals_test,
+                            a, b, lr_a, lr_b, reg_a, reg_b, epochs, m, workers, store_c, seed,
+                            loss_out, rmse_out, mae_out, seconds_out, reads_out, mults_out, jsonl,
+                            jsonl_cap, 0);
 }
 
 int ftkh_loss(int order, const int32_t* dims, const int32_t* ranks, int32_t r, int64_t nnz,

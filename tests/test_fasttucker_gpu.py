@@ -99,3 +99,22 @@ def test_hogwild_core_block_tracks_the_chain(session):
     cos = float(np.sum(det * hog) / (np.linalg.norm(det) * np.linalg.norm(hog)))
     assert cos > 0.99
     assert abs(np.linalg.norm(hog) / np.linalg.norm(det) - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("variant", ["fasttucker", "fastertucker"])
+def test_cxx_api_train_variant_matches_golden_trajectory(variant):
+    """ftk::train with TrainOptions.variant = kFastTucker / kFasterTucker
+    (decomposition.cpp:849-917): per-epoch loss, test RMSE / MAE, cost
+    tallies and the final model equal the reference's train() bit for bit."""
+    z = load(f"train_{variant}")
+    a = [z[f"m0_a{n}"].copy() for n in range(3)]
+    b = [z[f"m0_b{n}"].copy() for n in range(3)]
+    host.set_device_options(mode=0, precision=0, exact_eval=True)
+    h = host.train(z["full_dims"], [8, 8, 8], 8, z["tr_idx"], z["tr_vals"], z["te_idx"],
+                   z["te_vals"], a, b, epochs=3, seed=2, workers=1, variant=variant)
+    for n in range(3):
+        assert bits_equal(a[n], z[f"final_a{n}"]) and bits_equal(b[n], z[f"final_b{n}"])
+    assert np.array_equal(h["loss"], z["loss"])
+    assert np.array_equal(h["rmse"], z["rmse"])
+    assert np.array_equal(h["mae"], z["mae"])
+    assert np.array_equal(h["reads"], z["reads"]) and np.array_equal(h["mults"], z["mults"])
