@@ -67,7 +67,9 @@ struct BigLayout {
   // TMEM: factor C/D [0, 3W) + U regions (one per mode at W = 64, so U_0..2
   // issue back to back; one shared at W = 128); core: C buffers (two at
   // W = 64, so C(k+1) overlaps the epilogue of k) + G_pass.
-  static constexpr int kUN = 1;
+  // W = 64: two U regions (TMEM 3 x 2W + 2W = 512), so U(n + 1) runs while
+  // the epilogue writes U(n) back
+  static constexpr int kUN = kACopy ? 2 : 1;
   static constexpr int kCB = W == 64 ? 2 : 1;
   static constexpr uint32_t kMS = kACopy ? 2 * W : W;  // factor TMEM per mode: C [| A copy]
   static constexpr uint32_t t_u = 3 * kMS;
@@ -88,6 +90,7 @@ enum : int {
   B_UEMPTY = 22, // factor, one U region: U read
   B_DEMPTY = 23, // core: G GEMM done with the D' tile
   B_CEMPTY = 24, // [2] core: C buffer b read by the epilogue
+  B_UEMPTY2 = 26, // factor, second U region
 };
 
 struct BigParams {
@@ -155,7 +158,8 @@ __device__ void big_setup(uint8_t* sm, uint64_t* bars, uint32_t* tslot, const Bi
     }
     for (int n = 0; n < kN; ++n) mbar_init(&bars[B_UFULL + n], 1);
     mbar_init(&bars[B_DFULL], 1);
-    mbar_init(&bars[B_UEMPTY], 1);
+    mbar_init(&bars[B_UEMPTY], 8);  // one arrival per epilogue warp
+    mbar_init(&bars[B_UEMPTY2], 8);
     mbar_init(&bars[B_DEMPTY], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
@@ -361,11 +365,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
         for (int n = 0; n < kN; ++n, ++job) {
           const int s = (int)(job % L::kStages);
           const int64_t u = k * kN + n;
+          const int uq = (int)(u % L::kUN);  // U region of this job
           mbar_wait(&bars[B_FULL + s], (uint32_t)((job / L::kStages) & 1));
-          if (L::kUN == 1) mbar_wait(&bars[B_UEMPTY], (uint32_t)((u & 1) ^ 1));
+          mbar_wait(&bars[uq ? B_UEMPTY2 : B_UEMPTY], (uint32_t)(((u / L::kUN) & 1) ^ 1));
           tc_after();
           const uint32_t b0 = smem_u32(sm + L::o_st + s * L::kStage) + L::kA;
-          const uint32_t tu = tmem + L::t_u + (n % L::kUN) * W;
+          const uint32_t tu = tmem + L::t_u + uq * W;
 #pragma unroll
           for (int ks = 0; ks < W / 8; ++ks)
             mma_ts(tu, tmem + n * L::kMS + ks * 8,
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
               mma_ts(tu, tmem + n * L::kMS + W + ks * 8,
                      sdesc(dg + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id, 1);
           mma_commit(&bars[B_EMPTY + s]);
-          mma_commit(&bars[B_UFULL + n % L::kUN]);
+          mma_commit(&bars[B_UFULL + uq]);
         }
       }
     }
@@ -434,15 +439,19 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
         tmem_st16(tl + 1 * L::kMS + c * 16, d1);
         tmem_st16(tl + 2 * L::kMS + c * 16, d2);
       }
+      int32_t g[kN];  // read before the barrier: the COO record is then free
+#pragma unroll
+      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
       tmem_wait_st();
       tc_before();
       named_bar(1, 256);
-      if (warp == 2 && lane == 0) mbar_arrive(&bars[B_DFULL]);
-      int32_t g[kN];
-#pragma unroll
-      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
+      if (warp == 2 && lane == 0) {
+        mbar_arrive(&bars[B_DFULL]);
+        mbar_arrive(&bars[B_IEMPTY + i]);
+      }
       for (int n = 0; n < kN; ++n) {
         const int64_t u = k * kN + n;
+        const int uq = (int)(u % L::kUN);
         float* dst = p.a[n] + (size_t)g[n] * W + h * kHalf;
         // the live half-row (through L2) for the regulariser term, loaded
         // ahead of the U wait so its latency overlaps the U GEMM
@@ -452,8 +461,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           a4[qq] = (ok && (!kFold || !p.atomic_update))
                        ? __ldcg(reinterpret_cast<const float4*>(dst + qq * 4))
                        : make_float4(0.f, 0.f, 0.f, 0.f);
-        mbar_wait(&bars[B_UFULL + n % L::kUN], (uint32_t)((L::kUN == 1 ? u : k) & 1));
+        mbar_wait(&bars[B_UFULL + uq], (uint32_t)((u / L::kUN) & 1));
         tc_after();
+        // U into registers, then the region is free for U(n + 2)
+        uint32_t v[kHalf];
+#pragma unroll
+        for (int c = 0; c < kHalf / 16; ++c)
+          tmem_ld16(tl + L::t_u + uq * W + h * kHalf + c * 16,
+                    *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
+        tmem_wait_ld();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[uq ? B_UEMPTY2 : B_UEMPTY]);
         // write-back through a private 2 KB staging tile per warp: 16 columns
         // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
         uint8_t* stage = sm + L::o_stage + (warp - 2) * 2048;
@@ -463,18 +482,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
         float* dsw = p.a[n] + h * kHalf + (lane & 3) * 4;
 #pragma unroll
         for (int c = 0; c < kHalf / 16; ++c) {
-          uint32_t v[16];
-          tmem_ld16(tl + L::t_u + (n % L::kUN) * W + h * kHalf + c * 16, v);
-          tmem_wait_ld();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             const float4 a = a4[c * 4 + q4];
             float4 st;  // kFold: U' already holds the regulariser
             const float rg = kFold ? 0.0f : lr_reg;
-            st.x = __uint_as_float(v[q4 * 4 + 0]) - rg * a.x;
-            st.y = __uint_as_float(v[q4 * 4 + 1]) - rg * a.y;
-            st.z = __uint_as_float(v[q4 * 4 + 2]) - rg * a.z;
-            st.w = __uint_as_float(v[q4 * 4 + 3]) - rg * a.w;
+            st.x = __uint_as_float(v[c * 16 + q4 * 4 + 0]) - rg * a.x;
+            st.y = __uint_as_float(v[c * 16 + q4 * 4 + 1]) - rg * a.y;
+            st.z = __uint_as_float(v[c * 16 + q4 * 4 + 2]) - rg * a.z;
+            st.w = __uint_as_float(v[c * 16 + q4 * 4 + 3]) - rg * a.w;
             if (!p.atomic_update) {
               st.x += a.x;
               st.y += a.y;
@@ -497,12 +513,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
             }
           }
           __syncwarp();
-        }
-        tc_before();
-        named_bar(1, 256);
-        if (warp == 2 && lane == 0) {
-          if (L::kUN == 1) mbar_arrive(&bars[B_UEMPTY]);
-          if (n == kN - 1) mbar_arrive(&bars[B_IEMPTY + i]);
         }
       }
     }
