@@ -562,7 +562,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
   if (threadIdx.x == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&bars[FULL + s], 2);
-      mbar_init(&bars[EMPTY + s], 1);
+      // C half jobs: released by the MMA commit (1 arrival); U half jobs: by
+      // the 4 epilogue warps that read the rows -- both count as 4
+      mbar_init(&bars[EMPTY + s], 4);
     }
     for (int i = 0; i < kI; ++i) {
       mbar_init(&bars[IFULL + i], 1);
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
     mbar_init(&bars[CFULL], 1);
     mbar_init(&bars[DFULL], 1);
     mbar_init(&bars[UFULL], 1);
-    mbar_init(&bars[UEMPTY], 1);
+    mbar_init(&bars[UEMPTY], 8);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
   }
@@ -674,7 +676,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
               mma_ss(tmem + n * W, sdesc(a0 + (ks / 4) * kBlk + (ks % 4) * 32, 16, 1024, 128),
                      sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id,
                      (hh > 0 || ks > 0) ? 1u : 0u);
-            mma_commit(&bars[EMPTY + s]);
+#pragma unroll
+            for (int a4 = 0; a4 < 4; ++a4) mma_commit(&bars[EMPTY + s]);
           }
         mma_commit(&bars[CFULL]);
       };
@@ -749,13 +752,16 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
         tmem_st16(tl + 1 * W + c * 16, d1);
         tmem_st16(tl + 2 * W + c * 16, d2);
       }
+      int32_t g[kN];  // read before the barrier: the COO record is then free
+#pragma unroll
+      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
       tmem_wait_st();
       tc_before();
       named_bar(1, 256);
-      if (warp == 2 && lane == 0) mbar_arrive(&bars[DFULL]);
-      int32_t g[kN];
-#pragma unroll
-      for (int n = 0; n < kN; ++n) g[n] = s_idx[n * kRows + row];
+      if (warp == 2 && lane == 0) {
+        mbar_arrive(&bars[DFULL]);
+        mbar_arrive(&bars[IEMPTY + i]);
+      }
       for (int n = 0; n < kN; ++n) {
         const int64_t u = k * kN + n;
         // this warp's column half h came with U half job h of mode n
@@ -774,12 +780,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
         for (int qq = 0; qq < kHalf / 4; ++qq)  // column 4 qq of the half: block qq / 8
           a4[qq] = *reinterpret_cast<const float4*>(xs + (qq / 8) * kBlk + swz(row, (qq % 8) * 16, 128));
         tc_before();
-        named_bar(6 + h, 128);  // the four warps of this half have read the stage
-        if (q == 0 && lane == 0) mbar_arrive(&bars[EMPTY + s]);
-        named_bar(1, 256);
-        if (warp == 2 && lane == 0) {
+        __syncwarp();
+        if (lane == 0) {  // this warp has read its U columns and its rows
+          mbar_arrive(&bars[EMPTY + s]);
           mbar_arrive(&bars[UEMPTY]);
-          if (n == kN - 1) mbar_arrive(&bars[IEMPTY + i]);
         }
         // write-back through a private 2 KB staging tile per warp: 16 columns
         // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
