@@ -62,3 +62,35 @@ def test_blocks_match_oracle(session, case):
         assert bits_equal(b[n], want.b[n]), f"B{n}"
         assert bits_equal(dev_cache[n], cache[n]), f"cache {n}"
         assert not np.array_equal(want.b[n], m.b[n])
+
+
+EDGE = [  # fewer nonzeros than a batch, one nonzero, batch 1, order 5
+    ([5, 4, 3], 7, [3, 5, 2], 4, 16),
+    ([2, 2, 2], 1, [4, 4, 4], 4, 16),
+    ([6, 5, 4], 40, [3, 5, 2], 4, 1),
+    ([6, 5, 4, 3, 3], 150, [3, 2, 4, 2, 3], 5, 4),
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: f"nnz{c[1]}-M{c[4]}-N{len(c[0])}")
+def test_fastertucker_edge_cases_match_oracle(session, case):
+    dims, nnz, ranks, r, cap = case
+    t = O.random_tensor(dims, nnz, nnz + 5, 0.0, 2.0)
+    m = O.random_model(dims, ranks, r, nnz + 6, 0.4)
+    want = m.copy()
+    cache = CO.ccache_build(want)
+    session.upload_tensor(0, t.dims, t.idx, t.vals)
+    session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+    session.ccache_upload(cache)
+    for factor, tag in ((True, 1), (False, 2)):
+        for mode in range(t.order):
+            perm, bo = plan(t, mode, cap, 13, tag, False)
+            if factor:
+                g, off = group_by_row(t, perm, mode)
+                session.fastertucker_factor(0, mode, g, off, 5e-2, 1e-2)
+            else:
+                session.fastertucker_core(0, mode, perm, bo, 5e-2, 1e-2)
+            CO.fastertucker_block(factor, t, want, cache, perm, bo, mode, 5e-2, 1e-2)
+    a, b = session.download_model()
+    for n in range(t.order):
+        assert bits_equal(a[n], want.a[n]) and bits_equal(b[n], want.b[n])

@@ -118,3 +118,34 @@ def test_cxx_api_train_variant_matches_golden_trajectory(variant):
     assert np.array_equal(h["rmse"], z["rmse"])
     assert np.array_equal(h["mae"], z["mae"])
     assert np.array_equal(h["reads"], z["reads"]) and np.array_equal(h["mults"], z["mults"])
+
+
+EDGE = [  # dims, nnz, ranks, R, cap: fewer nonzeros than a batch, one nonzero,
+    # batch 1, batch larger than any bucket, order 5
+    ([5, 4, 3], 7, [3, 5, 2], 4, 16),
+    ([2, 2, 2], 1, [4, 4, 4], 4, 16),
+    ([6, 5, 4], 40, [3, 5, 2], 4, 1),
+    ([8, 6, 4], 60, [4, 4, 4], 3, 64),
+    ([6, 5, 4, 3, 3], 150, [3, 2, 4, 2, 3], 5, 4),
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: f"nnz{c[1]}-M{c[4]}-N{len(c[0])}")
+def test_fasttucker_edge_cases_match_oracle(session, case):
+    dims, nnz, ranks, r, cap = case
+    t = O.random_tensor(dims, nnz, nnz + 3, 0.0, 2.0)
+    m = O.random_model(dims, ranks, r, nnz + 4, 0.4)
+    session.upload_tensor(0, t.dims, t.idx, t.vals)
+    session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+    want = m.copy()
+    for mode in range(t.order):
+        perm, boff = fixed_mode_plan(t, mode, cap, 7, False)
+        session.fasttucker_factor(0, mode, perm, boff, cap, 5e-2, 1e-2)
+        CO.fasttucker_factor_block(t, want, perm, boff, cap, mode, 5e-2, 1e-2)
+    for mode in range(t.order):
+        perm = host.global_plan(t.nnz, cap, 40 + mode)
+        session.fasttucker_core(0, mode, perm, cap, 5e-2, 1e-2)
+        CO.fasttucker_core_block(t, want, perm, cap, mode, 5e-2, 1e-2)
+    a, b = session.download_model()
+    for n in range(t.order):
+        assert bits_equal(a[n], want.a[n]) and bits_equal(b[n], want.b[n])
