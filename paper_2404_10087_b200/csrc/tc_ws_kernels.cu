@@ -807,7 +807,8 @@ struct Ws16Layout {
   static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
   static constexpr int kI = 6;
   static constexpr uint32_t o_rows = o_idx + kI * kIdxSlot;
-  static constexpr uint32_t o_bar = o_rows + 64;
+  static constexpr uint32_t o_xp = o_rows + 64;  // x_hat halves [2 tiles][2 halves][128]
+  static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
   static constexpr uint32_t o_tmem = o_bar + 32 * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
@@ -976,10 +977,17 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
 #pragma unroll
         for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
       }
-      const float xhat = xhat_full(tl + b * 96 + (h ^ 1) * 16, c);
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[H_CEMPTY + b]);  // C(k + 2) may land
+      // x_hat halves exchanged with the sibling warp of this lane quarter
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      float* xp = reinterpret_cast<float*>(sm + L::o_xp);
+      xp[(b * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
       const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
       const float resid = ok ? s_val[row] - xhat : 0.0f;
       __syncwarp();
