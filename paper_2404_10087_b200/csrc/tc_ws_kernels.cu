@@ -994,6 +994,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[H_IEMPTY + ii]);
       mbar_wait(&bars[H_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // G(k - 2) done with D[b]
       uint8_t* dt = sm + L::o_d + b * L::kSlot;
+      // r D'_n: r (C_1 C_2), (r C_0) C_2, (r C_0) C_1 -- five products per column
+      float rc0[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rc0[i] = resid * c[0][i];
 #pragma unroll
       for (int n = 0; n < kN; ++n)
 #pragma unroll
@@ -1002,8 +1006,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int i0 = q2 * 8 + e * 2;
-#define FTK_D(ii) (n == 0 ? c[1][ii] * c[2][ii] : (n == 1 ? c[0][ii] * c[2][ii] : c[0][ii] * c[1][ii]))
-            w[e] = f16x2_sat(resid * FTK_D(i0), resid * FTK_D(i0 + 1));
+#define FTK_D(ii) (n == 0 ? resid * (c[1][ii] * c[2][ii]) : (n == 1 ? rc0[ii] * c[2][ii] : rc0[ii] * c[1][ii]))
+            w[e] = f16x2_sat(FTK_D(i0), FTK_D(i0 + 1));
 #undef FTK_D
           }
           *reinterpret_cast<uint4*>(dt + n * kModeTile16 + swz(row, (h * 16 + q2 * 8) * 2, 64)) =
