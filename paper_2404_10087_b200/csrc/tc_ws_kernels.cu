@@ -969,13 +969,15 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
       mbar_wait(&bars[H_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
       float c[kN][16];
+      {  // the three modes' columns in flight before one wait
+        uint32_t v[kN][16];
 #pragma unroll
-      for (int n = 0; n < kN; ++n) {
-        uint32_t v[16];
-        tmem_ld16(tl + b * 96 + n * kW + h * 16, v);
+        for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 96 + n * kW + h * 16, v[n]);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[n][i]);
       }
       tc_before();
       __syncwarp();
