@@ -415,6 +415,12 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
     };
     auto epi2 = [&](int64_t k, const Tile& t) {
+      // the row indices of the 8-row RED groups, shuffled before the wait
+      int32_t gq[kN][4];
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], i * 8 + (lane >> 2));
       mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
       tc_after();
       uint32_t u[kN][16];
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int rl = i * 8 + (lane >> 2), ch = lane & 3;
-          const int32_t g = __shfl_sync(0xffffffffu, t.g[n], rl);
+          const int32_t g = gq[n][i];
           const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
           if (g >= 0 && !(p.exp & 16)) {  // exp 16: no write-back (timing only)
             float* gp = dst + (size_t)g * kW + h * 16 + ch * 4;
