@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
           a4[qq] = (ok && (!kFold || !p.atomic_update))
                        ? __ldcg(reinterpret_cast<const float4*>(dst + qq * 4))
                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t gr[4];  // row indices of the 8-row RED groups, shuffled before the wait
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gr[i] = __shfl_sync(0xffffffffu, ok ? g[n] : -1, i * 8 + (lane >> 2));
         mbar_wait(&bars[B_UFULL + uq], (uint32_t)((u / L::kUN) & 1));
         tc_after();
         // U into registers, then the region is free for U(n + 2)
@@ -476,9 +479,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
         // write-back through a private 2 KB staging tile per warp: 16 columns
         // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
         uint8_t* stage = sm + L::o_stage + (warp - 2) * 2048;
-        int32_t gr[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) gr[i] = __shfl_sync(0xffffffffu, ok ? g[n] : -1, i * 8 + (lane >> 2));
         float* dsw = p.a[n] + h * kHalf + (lane & 3) * 4;
 #pragma unroll
         for (int c = 0; c < kHalf / 16; ++c) {
