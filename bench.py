@@ -545,7 +545,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     # Single GPU: double-buffered tensor slots 2 / 3, step k + 1's COO copy
     # (ftkcu_tensor_upload_async, copy stream) overlapping step k's epoch.
     pipelined = type(job) is SingleGpu and not args.e2e_sync
-    steps = max(1, min(args.steps, 5 if pipelined else 3))
+    steps = max(1, args.steps if pipelined else min(args.steps, 3))
     h2d = idx.nbytes + vals.nbytes + sum(x.nbytes for x in a_np + b_np)
     d2h = sum(x.nbytes for x in a_np + b_np)
     s = job.s
