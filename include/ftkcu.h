@@ -174,7 +174,11 @@ int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* p
  * row_off = the nrows + 1 group offsets.  (A step touches only its own row,
  * so rows are independent chains.)  Core block: perm = that plan for the
  * core seed, batch_off = its nbatches + 1 batch offsets (batches never cross
- * a bucket).  Core block supports J <= 128. */
+ * a bucket).  Core block supports J <= 128.  schedule
+ * FTKCU_MODE_DETERMINISTIC: the workers == 1 recurrence, bit-identical;
+ * FTKCU_MODE_HOGWILD (workers > 1): the block's linear B recurrence summed in
+ * closed form over all batches in parallel (same mathematics, fp32 sums in
+ * another order; falls back to the recurrence when J x R is too large). */
 int ftkcu_ccache_upload(ftkcu_session* s, const float* const* C);
 int ftkcu_ccache_download(ftkcu_session* s, float* const* C);
 int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
@@ -182,7 +186,7 @@ int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_
                               double* ms);
 int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm,
                             const int64_t* batch_off, int64_t nbatches, float lr_b, float reg_b,
-                            double* ms);
+                            int schedule, double* ms);
 
 /* DSGD strata support.  Declares that the uploaded entries are sorted into
  * cells: entries [cell_offsets[c], cell_offsets[c+1]) form cell c.  The

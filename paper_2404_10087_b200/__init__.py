@@ -87,7 +87,7 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_fastertucker_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
                                             C.c_int64, C.c_float, C.c_float, _f64p]
     L.ftkcu_fastertucker_core.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
-                                          C.c_int64, C.c_float, C.c_float, _f64p]
+                                          C.c_int64, C.c_float, C.c_float, C.c_int, _f64p]
     L.ftkcu_tensor_release.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.argtypes = [C.c_void_p, C.c_int]
     L.ftkcu_tensor_nnz.restype = C.c_int64
@@ -283,13 +283,14 @@ class Session:
                                                     C.byref(ms) if timed else None))
         return ms.value
 
-    def fastertucker_core(self, slot, mode, perm, batch_off, lr_b=1e-3, reg_b=1e-4, timed=True):
+    def fastertucker_core(self, slot, mode, perm, batch_off, lr_b=1e-3, reg_b=1e-4,
+                          schedule=MODE_DETERMINISTIC, timed=True):
         pa = np.ascontiguousarray(perm, np.int64)
         bo = np.ascontiguousarray(batch_off, np.int64)
         ms = C.c_double(0.0)
         self._ck(self.lib.ftkcu_fastertucker_core(self.h, slot, mode, _p(pa, _i64p),
                                                   _p(bo, _i64p), bo.size - 1, lr_b, reg_b,
-                                                  C.byref(ms) if timed else None))
+                                                  schedule, C.byref(ms) if timed else None))
         return ms.value
 
     def eval(self, slot=1, workers=1, reg_a=0.0, reg_b=0.0):

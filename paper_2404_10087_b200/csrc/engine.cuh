@@ -164,6 +164,12 @@ size_t fst_core_scratch_floats(const KView& v, int mode);
 cudaError_t launch_fst_core(const KView& v, int mode, const int64_t* perm, const int64_t* boff,
                             int64_t nbatches, float lr_b, float reg_b, float* scratch,
                             cudaStream_t st);
+// workers > 1: the block's linear B recurrence summed in closed form, batches
+// in parallel (scratch: 2 x num_sms() x J x R floats).
+bool fst_scan_supported(const KView& v, int mode);
+cudaError_t launch_fst_core_scan(const KView& v, int mode, const int64_t* perm,
+                                 const int64_t* boff, int64_t nbatches, float lr_b, float reg_b,
+                                 float* scratch, cudaStream_t st);
 
 // ---- Hogwild sweeps (hog_kernels.cu) -----------------------------------------
 cudaError_t launch_hog_factor(const KView& v, int64_t tile_mul, int64_t tile_add,

@@ -17,7 +17,8 @@
 //   product g d^T with g = A_psi^T r.  Neither depends on B^(n), so each B
 //   element's per-batch recurrence b <- b + lr (g_j d_c / M - reg b) runs on
 //   its own thread over the batch sequence, after one parallel pass forms
-//   every batch's (g, d, 1/M).
+//   every batch's (g, d, 1/M).  For workers > 1 the recurrence, being
+//   linear, is instead summed in closed form over all batches in parallel.
 //
 // Arithmetic: the reference's fp32 sequence, each product and sum rounded on
 // its own (__fmul_rn / __fadd_rn), sums in the reference's order; these
@@ -192,6 +193,83 @@ fst_core_chain_kernel(float* __restrict__ bm, int elems, const float* __restrict
   bm[e] = b;
 }
 
+// Parallel schedule of the core block (workers > 1).  The recurrence is
+// linear, b_T = a^T b_0 + lr sum_t a^(T-1-t) (g_t d_t^T) / M_t with
+// a = 1 - lr reg, so every batch contributes an outer product with a known
+// weight: warps take batches in any order and accumulate w g d^T into
+// private shared-memory sums, one partial per CTA; fst_scan_apply adds them.
+// Same mathematics as the chain, fp32 sums in a different order.
+__global__ void __launch_bounds__(kFstWarps * 32)
+fst_core_scan_kernel(KView v, int mode, const int64_t* __restrict__ perm,
+                     const int64_t* __restrict__ boff, int64_t nb, double a,
+                     float* __restrict__ partials) {
+  extern __shared__ float smem[];
+  const int r = v.r, jn = v.j[mode], elems = jn * r;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* acc = smem + (size_t)wib * elems;
+  float* d = smem + (size_t)kFstWarps * elems + (size_t)wib * (r + jn + 32);
+  float* g = d + r;
+  float* res = g + jn;
+  for (int e = lane; e < elems; e += 32) acc[e] = 0.0f;
+  for (int64_t b = (int64_t)blockIdx.x * kFstWarps + wib; b < nb;
+       b += (int64_t)gridDim.x * kFstWarps) {
+    const int64_t beg = boff[b], end = boff[b + 1];
+    const int m_eff = (int)(end - beg);
+    d_row(v, mode, perm[beg], d, lane, 32);
+    __syncwarp();
+    float gacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int m0 = 0; m0 < m_eff; m0 += 32) {
+      const int m = m0 + lane;
+      if (m < m_eff) {
+        const int64_t pos = perm[beg + m];
+        const float* crow = v.cc[mode] + (size_t)v.idx[mode][pos] * r;
+        float s = 0.0f;
+        for (int c = 0; c < r; ++c) s = fmaf(crow[c], d[c], s);
+        res[lane] = v.vals[pos] - s;
+      }
+      __syncwarp();
+      const int mm = (m_eff - m0) < 32 ? (m_eff - m0) : 32;
+      for (int q = 0; q < 4; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= jn) break;
+        for (int i = 0; i < mm; ++i) {
+          const int64_t pos = perm[beg + m0 + i];
+          gacc[q] = fmaf(res[i], v.a[mode][(size_t)v.idx[mode][pos] * jn + k], gacc[q]);
+        }
+      }
+      __syncwarp();
+    }
+    const float w = (float)(pow(a, (double)(nb - 1 - b)) / (double)m_eff);
+    for (int q = 0; q < 4; ++q) {
+      const int k = lane + 32 * q;
+      if (k < jn) g[k] = w * gacc[q];
+    }
+    __syncwarp();
+    for (int e = lane; e < elems; e += 32) {
+      const int k = e / r, c = e - k * r;
+      acc[e] = fmaf(g[k], d[c], acc[e]);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+    float t = 0.0f;
+    for (int w = 0; w < kFstWarps; ++w) t += smem[(size_t)w * elems + e];
+    partials[(size_t)blockIdx.x * elems + e] = t;
+  }
+}
+
+// b <- a^T b + lr sum_ctas partial
+__global__ void fst_scan_apply_kernel(float* __restrict__ bm, int elems,
+                                      const float* __restrict__ partials, int nparts, float aT,
+                                      float lr) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= elems) return;
+  float t = 0.0f;
+  for (int p = 0; p < nparts; ++p) t += partials[(size_t)p * elems + e];
+  bm[e] = fmaf(lr, t, aT * bm[e]);
+}
+
 constexpr size_t kScratchFloats = (size_t)16 << 20;  // 64 MB of step inputs per round (L2-resident)
 
 }  // namespace
@@ -214,6 +292,36 @@ cudaError_t launch_fst_factor(const KView& v, int mode, const int64_t* perm, con
 
 size_t fst_core_scratch_floats(const KView& v, int mode) {
   return kScratchFloats + (size_t)3 * kAhead * v.j[mode] * v.r;
+}
+
+bool fst_scan_supported(const KView& v, int mode) {
+  const size_t elems = (size_t)v.j[mode] * v.r;
+  return sizeof(float) * (kFstWarps * elems + kFstWarps * (v.r + v.j[mode] + 32)) <= 200 * 1024 &&
+         v.j[mode] <= 128;
+}
+
+cudaError_t launch_fst_core_scan(const KView& v, int mode, const int64_t* perm,
+                                 const int64_t* boff, int64_t nbatches, float lr_b, float reg_b,
+                                 float* scratch, cudaStream_t st) {
+  if (!fst_scan_supported(v, mode)) return cudaErrorInvalidValue;
+  if (nbatches == 0) return cudaSuccess;
+  const int elems = v.j[mode] * v.r;
+  const size_t bytes = sizeof(float) * (kFstWarps * (size_t)elems + kFstWarps * (v.r + v.j[mode] + 32));
+  cudaError_t e = cudaFuncSetAttribute(fst_core_scan_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (nbatches + kFstWarps - 1) / kFstWarps;
+  if (blocks > (int64_t)num_sms() * 2) blocks = (int64_t)num_sms() * 2;
+  const float lr = lr_b;
+  const double a = 1.0 - (double)lr_b * (double)reg_b;
+  fst_core_scan_kernel<<<(int)blocks, kFstWarps * 32, bytes, st>>>(v, mode, perm, boff, nbatches,
+                                                                    a, scratch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const float aT = (float)pow(a, (double)nbatches);
+  fst_scan_apply_kernel<<<(elems + 255) / 256, 256, 0, st>>>(const_cast<float*>(v.b[mode]), elems,
+                                                              scratch, (int)blocks, aT, lr);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fst_core(const KView& v, int mode, const int64_t* perm, const int64_t* boff,

@@ -861,7 +861,7 @@ int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_
 
 int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t* perm,
                             const int64_t* batch_off, int64_t nbatches, float lr_b, float reg_b,
-                            double* ms) {
+                            int schedule, double* ms) {
   int rc = bind(s);
   if (rc) return rc;
   KView v;
@@ -880,10 +880,19 @@ int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t*
   }
   CK(cudaMemcpyAsync(s->d_boff, batch_off, sizeof(int64_t) * (nbatches + 1),
                      cudaMemcpyHostToDevice, s->stream));
-  if ((rc = ensure_scratch(s, sizeof(float) * fst_core_scratch_floats(v, mode)))) return rc;
+  if (schedule != FTKCU_MODE_DETERMINISTIC && schedule != FTKCU_MODE_HOGWILD)
+    return fail(s, FTKCU_ERR_ARG, "unknown schedule %d", schedule);
+  const bool scan = schedule == FTKCU_MODE_HOGWILD && fst_scan_supported(v, mode);
+  const size_t need = scan ? (size_t)2 * num_sms() * v.j[mode] * v.r
+                           : fst_core_scratch_floats(v, mode);
+  if ((rc = ensure_scratch(s, sizeof(float) * need))) return rc;
   CK(cudaEventRecord(s->ev0, s->stream));
-  CK(launch_fst_core(v, mode, s->d_perm, s->d_boff, nbatches, lr_b, reg_b,
-                     static_cast<float*>(s->scratch), s->stream));
+  if (scan)
+    CK(launch_fst_core_scan(v, mode, s->d_perm, s->d_boff, nbatches, lr_b, reg_b,
+                            static_cast<float*>(s->scratch), s->stream));
+  else
+    CK(launch_fst_core(v, mode, s->d_perm, s->d_boff, nbatches, lr_b, reg_b,
+                       static_cast<float*>(s->scratch), s->stream));
   CK(launch_ccache(v, s->model.dims, s->model.cc, s->stream, mode));
   s->launches += 2;
   return finish_timing(s, ms);

@@ -87,7 +87,8 @@ def lib():
                                         _i64p]
     L.ftkh_epoch_fastertucker.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p,
                                           _f32p, _fpp, _fpp, C.c_float, C.c_float, C.c_float,
-                                          C.c_float, C.c_int, C.c_int, C.c_uint64, _f64p, _i64p]
+                                          C.c_float, C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p,
+                                          _i64p]
     L.ftkh_train.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p,
                              C.c_int64, _i32p, _f32p, _fpp, _fpp, C.c_float, C.c_float,
                              C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -261,7 +262,7 @@ def epoch_fasttucker(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e-3
 
 
 def epoch_fastertucker(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e-3,
-                       reg_a=1e-4, reg_b=1e-4, m=16, canonical=False):
+                       reg_a=1e-4, reg_b=1e-4, m=16, canonical=False, workers=1):
     """ftk::epoch_fastertucker through the C++ API (complement indices and a
     fresh C cache built there); mutates a/b; returns (seconds[2], counters[10])."""
     dims, ranks, idx = _i32(dims), _i32(ranks), _i32(idx)
@@ -270,7 +271,7 @@ def epoch_fastertucker(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e
     cnt = np.zeros(10, np.int64)
     _ck(lib().ftkh_epoch_fastertucker(dims.size, _p(dims, _i32p), _p(ranks, _i32p), r, vals.size,
                                       _p(idx, _i32p), _p(vals, _f32p), _ptrs(a), _ptrs(b), lr_a,
-                                      lr_b, reg_a, reg_b, m, int(canonical), seed & M64,
+                                      lr_b, reg_a, reg_b, m, workers, int(canonical), seed & M64,
                                       _p(secs, _f64p), _p(cnt, _i64p)))
     return secs, cnt
 

@@ -227,7 +227,7 @@ int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, 
 int ftkh_epoch_fastertucker(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
                             int64_t nnz, const int32_t* idx, const float* vals, float* const* a,
                             float* const* b, float lr_a, float lr_b, float reg_a, float reg_b,
-                            int m, int canonical, uint64_t seed, double* seconds2,
+                            int m, int workers, int canonical, uint64_t seed, double* seconds2,
                             int64_t* counters) {
   return guarded([&] {
     SparseTensor t = make_tensor(order, dims, nnz, idx, vals);
@@ -238,6 +238,7 @@ int ftkh_epoch_fastertucker(int order, const int32_t* dims, const int32_t* ranks
     CCache cache;
     cache.build(md, nullptr);
     EpochOptions eo;
+    eo.workers = workers;
     eo.canonical_order = canonical != 0;
     EpochStats st;
     try {

@@ -369,6 +369,7 @@ EpochStats run_epoch_fastertucker(const SparseTensor& t, int slot, const Model& 
   require(static_cast<int>(complement.size()) == N, "need one complement index per mode");
   require(!opts.eager_refresh, "eager_refresh is not supported by the device FasterTucker");
   const index_t cap = opts.canonical_order ? 1 : h.batch_size;
+  const int workers = resolve_workers(opts.workers);
   EpochStats st;
   st.factor.reset(N);
   st.core.reset(N);
@@ -390,7 +391,8 @@ EpochStats run_epoch_fastertucker(const SparseTensor& t, int slot, const Model& 
       } else {
         off = batch_offsets(plan);
         check(ftkcu_fastertucker_core(s, slot, mode, plan.positions().data(), off.data(),
-                                      static_cast<int64_t>(off.size()) - 1, h.lr_b, h.reg_b, &ms));
+                                      static_cast<int64_t>(off.size()) - 1, h.lr_b, h.reg_b,
+                                      device_mode(workers), &ms));
         bill_fastertucker(st.core, m, mode, plan, false);
       }
       total[phase] += ms;

@@ -29,7 +29,9 @@ for factor, tag in ((True, 1), (False, 2)):
             print(f"fastertucker factor mode {mode}: {ms:.2f} ms ({off.size - 1} row chains)")
         else:
             ms = s.fastertucker_core(0, mode, perm, bo)
-            print(f"fastertucker core mode {mode}: {ms:.2f} ms ({bo.size - 1} batches)")
+            ms2 = s.fastertucker_core(0, mode, perm, bo, schedule=eng.MODE_HOGWILD)
+            print(f"fastertucker core mode {mode}: {ms:.2f} ms chain, {ms2:.2f} ms parallel "
+                  f"({bo.size - 1} batches)")
 for mode in range(3):
     perm, boff = host.per_bucket_plan(t.idx, mode, 16, 5)
     ms = s.fasttucker_factor(0, mode, perm, boff)

@@ -94,3 +94,28 @@ def test_fastertucker_edge_cases_match_oracle(session, case):
     a, b = session.download_model()
     for n in range(t.order):
         assert bits_equal(a[n], want.a[n]) and bits_equal(b[n], want.b[n])
+
+
+def test_parallel_core_schedule_matches_the_recurrence(session):
+    """workers > 1: the core block's linear B recurrence summed in closed form
+    over all batches in parallel.  Same mathematics as the bit-identical
+    chain; only fp32 rounding order differs."""
+    import paper_2404_10087_b200 as eng
+
+    t = O.random_tensor([300, 200, 100], 40000, 41, 1.0, 5.0)
+    m = O.random_model(t.dims, [16, 16, 16], 16, 42, 0.1)
+    cache = CO.ccache_build(m)
+    out = []
+    for sched in (eng.MODE_DETERMINISTIC, eng.MODE_HOGWILD):
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.ccache_upload(cache)
+        for mode in range(t.order):
+            perm, bo = plan(t, mode, 4, 77, 2, False)
+            session.fastertucker_core(0, mode, perm, bo, 1e-2, 1e-3, schedule=sched)
+        out.append(session.download_model()[1])
+    for n in range(t.order):
+        det, par = out[0][n], out[1][n]
+        step = det - m.b[n]
+        assert np.abs(step).max() > 1e-4
+        np.testing.assert_allclose(par, det, rtol=0, atol=2e-4 * np.abs(step).max() + 1e-7)
