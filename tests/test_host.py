@@ -168,3 +168,50 @@ def test_predicted_costs_table():
     p = host.predicted_costs(3, 16, 16, [16, 16, 16])
     assert p.tolist() == [1536, 13056, 12288, 768]
     assert np.array_equal(p, O.COracle.predicted_costs(3, 16, 16, [16, 16, 16]))
+
+
+def test_reference_style_caller_compiles_and_links(tmp_path):
+    """A caller written against the reference's headers (proj/include/ftk):
+    the plus epoch, both convex baselines with their ModeIndex / CCache
+    setup, and train() with a variant, compiled against include/ftk and
+    linked with libftk.so + libftkcu.so (nothing runs: no GPU here)."""
+    import os
+    import shutil
+    import subprocess
+
+    if shutil.which("g++") is None:
+        pytest.skip("no C++ compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2404_10087_b200")
+    src = tmp_path / "caller.cpp"
+    src.write_text(r"""
+#include "ftk/decomposition.hpp"
+#include "ftk/evaluation.hpp"
+#include "ftk/model.hpp"
+#include "ftk/sparse_tensor.hpp"
+int main() {
+  ftk::SparseTensor t = ftk::load_coo("x.tns", 3);
+  std::vector<ftk::index_t> ranks{8, 8, 8};
+  ftk::Model m = ftk::init_model(t.dims, ranks, 8, 1, 0.5f);
+  ftk::Hyperparams h;
+  ftk::EpochOptions eo;
+  std::vector<ftk::ModeIndex> fixed, comp;
+  for (int n = 0; n < 3; ++n) {
+    fixed.push_back(ftk::build_mode_index(t, n, ftk::Keying::kFixedMode));
+    comp.push_back(ftk::build_mode_index(t, n, ftk::Keying::kFixedComplement));
+  }
+  ftk::epoch_plus(t, m, h, eo, 1);
+  ftk::epoch_fasttucker(t, fixed, m, h, eo, 2);
+  ftk::CCache cache;
+  cache.build(m, nullptr);
+  ftk::epoch_fastertucker(t, comp, m, cache, h, eo, 3);
+  ftk::TrainOptions to;
+  to.variant = ftk::Variant::kFasterTucker;
+  ftk::Metrics mt = ftk::evaluate(m, t, 1);
+  return (int)ftk::train(t, nullptr, m, h, to).size() + (int)mt.samples;
+}
+""")
+    out = subprocess.run(["g++", "-std=gnu++20", "-I", os.path.join(root, "include"), str(src),
+                          "-L", lib, "-lftk", "-lftkcu", f"-Wl,-rpath,{lib}", "-o",
+                          str(tmp_path / "caller")], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
