@@ -364,13 +364,15 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       tc_after();
       const uint32_t tb = tl + kC + b * kBuf;
       float c[kN][16];
+      {  // the three modes' columns in flight before one wait
+        uint32_t v[kN][16];
 #pragma unroll
-      for (int n = 0; n < kN; ++n) {
-        uint32_t v[16];
-        tmem_ld16(tb + n * kMs + h * 16, v);
+        for (int n = 0; n < kN; ++n) tmem_ld16(tb + n * kMs + h * 16, v[n]);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[i]);
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[n][i]);
       }
       // x_hat halves exchanged with the sibling warp of this lane quarter
       // (each warp reads only its own half of C, so D' can go over it in place)
