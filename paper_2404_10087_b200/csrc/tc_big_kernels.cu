@@ -547,8 +547,15 @@ constexpr uint32_t o_tmem = o_bar + 24 * 8;
 constexpr uint32_t bytes = o_tmem + 16;
 static_assert(bytes <= 227 * 1024, "shared-memory budget");
 constexpr int kJobs = 4 * kN;  // per tile: C and U, two halves per mode
-enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 10, CFULL = 14, DFULL = 15, UFULL = 16, UEMPTY = 17 };
+// UFULL[n]: U_n in TMEM; U0READ: the epilogue has read U_0 (its region
+// takes the next U_0); UREAD: it has read U_1 and U_2 (their regions, C
+// regions 0 and 1, take the next tile's C)
+enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 10, CFULL = 14, DFULL = 15, UFULL = 16, U0READ = 19, UREAD = 20 };
 constexpr uint32_t t_u = kN * W;
+// U_0 goes to the spare region, U_n (n > 0) over C region n - 1, whose D'
+// the in-order tensor pipe has already consumed: the three U GEMMs of a tile
+// issue back to back
+__device__ __forceinline__ uint32_t u_col(int n) { return n == 0 ? t_u : (uint32_t)(n - 1) * W; }
 // job index of the first job of tile k's U phase (C(0) comes first)
 __device__ __forceinline__ int64_t u_job(int64_t k) { return 2 * kN + k * kJobs; }
 }  // namespace f128
@@ -572,8 +579,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
     }
     mbar_init(&bars[CFULL], 1);
     mbar_init(&bars[DFULL], 1);
-    mbar_init(&bars[UFULL], 1);
-    mbar_init(&bars[UEMPTY], 8);  // one arrival per epilogue warp
+    for (int n = 0; n < kN; ++n) mbar_init(&bars[UFULL + n], 1);
+    mbar_init(&bars[U0READ], 8);  // one arrival per epilogue warp
+    mbar_init(&bars[UREAD], 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
   }
@@ -685,20 +693,23 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
       for (int64_t k = 0; k < nk; ++k) {
         mbar_wait(&bars[DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n) {
-          mbar_wait(&bars[UEMPTY], (uint32_t)(((k * kN + n) & 1) ^ 1));
+          if (n == 0) mbar_wait(&bars[U0READ], (uint32_t)((k & 1) ^ 1));
           for (int hh = 0; hh < 2; ++hh) {
             const int s = wait_full();
             const uint32_t b0 = smem_u32(sm + o_st + s * kStage) + kHalfX;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              mma_ts(tmem + t_u, tmem + n * W + (hh * 8 + ks) * 8,
+              mma_ts(tmem + u_col(n), tmem + n * W + (hh * 8 + ks) * 8,
                      sdesc(b0 + (ks / 4) * (W * 128) + (ks % 4) * 32, 16, 1024, 128), id,
                      (hh > 0 || ks > 0) ? 1u : 0u);
             // the stage is released by the epilogue (it reads the rows)
           }
-          mma_commit(&bars[UFULL]);
+          mma_commit(&bars[UFULL + n]);
         }
-        if (k + 1 < nk) issue_c();  // C(k + 1) overwrites D'(k): behind U(k) in order
+        if (k + 1 < nk) {  // C(k + 1) overwrites U_1(k), U_2(k): after the epilogue read them
+          mbar_wait(&bars[UREAD], (uint32_t)(k & 1));
+          issue_c();
+        }
       }
     }
   } else {
@@ -767,12 +778,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
         // this warp's column half h came with U half job h of mode n
         const int64_t job = u_job(k) + 2 * n + h;
         const int s = (int)(job % kS);
-        mbar_wait(&bars[UFULL], (uint32_t)(u & 1));
+        (void)u;
+        mbar_wait(&bars[UFULL + n], (uint32_t)(k & 1));
         mbar_wait(&bars[FULL + s], (uint32_t)((job / kS) & 1));  // rows visible to this thread
         tc_after();
         uint32_t v[kHalf];
 #pragma unroll
-        for (int c = 0; c < kHalf / 16; ++c) tmem_ld16(tl + t_u + h * kHalf + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
+        for (int c = 0; c < kHalf / 16; ++c) tmem_ld16(tl + u_col(n) + h * kHalf + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
         tmem_wait_ld();
         const uint8_t* xs = sm + o_st + s * kStage;
         float4 a4[kHalf / 4];
@@ -783,7 +795,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
         __syncwarp();
         if (lane == 0) {  // this warp has read its U columns and its rows
           mbar_arrive(&bars[EMPTY + s]);
-          mbar_arrive(&bars[UEMPTY]);
+          if (n == 0) mbar_arrive(&bars[U0READ]);
+          if (n == kN - 1) mbar_arrive(&bars[UREAD]);
         }
         // write-back through a private 2 KB staging tile per warp: 16 columns
         // of its 32 rows at a time, sent as 64-B row segments (8 rows per RED)
