@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--e2e-sync", action="store_true",
                     help="e2e without the double-buffered asynchronous tensor upload")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rmse-check", action="store_true",
+                    help="skip the test-RMSE trajectory against tests/golden/c2_trajectory.json")
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
     return ap.parse_args()
 
@@ -178,53 +180,33 @@ class ClockSampler:
                 "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
-def make_workload(cfg_name, rank_override, world, rank, device):
-    """Training tensor of exactly cfg["nnz"] nonzeros plus a held-out test set
-    (fraction cfg["test_frac"] of all generated tuples): the
-    generator's storage order is a uniform shuffle, so its tail is a uniform
-    random split, as split_train_test's (sparse_tensor.cpp:180-196)."""
-    from paper_2404_10087_b200 import synth
-
-    cfg = dict(synth.CONFIGS[cfg_name])
-    j = rank_override or cfg["rank"]
-    frac = cfg.get("test_frac", 0.014)
-    total = int(round(cfg["nnz"] / (1.0 - frac)))
-    if cfg["nnz"] >= 10_000_000:
-        full = synth.uniform_torch(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"],
-                                   device=f"cuda:{device}")
-    else:
-        full = synth.uniform_numpy(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"])
-    n = cfg["nnz"]
-    coo = synth.Coo(full.dims, full.idx[:n], full.vals[:n])
-    test = synth.Coo(full.dims, np.ascontiguousarray(full.idx[n:]), np.ascontiguousarray(full.vals[n:]))
-    return cfg, j, coo, test
-
-
 def cpu_reference_time(cfg, j, sample_nnz, steps=1, warmup=1):
-    """Times ftkref::epoch_plus (the unmodified reference) on this host's cores
-    on a bounded sample of the workload; falls back to the C oracle port."""
+    """Times ftkref::epoch_plus (the unmodified reference, oracle/_ref) on this
+    host's cores on a bounded sample of the workload; falls back to the C
+    oracle port.  Data from datagen, model from ftkref::init_model: nothing
+    of the engine package is loaded."""
+    import datagen
     import oracle as O
-    from paper_2404_10087_b200 import host, synth
 
     cores = os.cpu_count() or 1
-    t = synth.uniform_numpy(cfg["dims"], sample_nnz, cfg["seed"] + 100, cfg["lo"], cfg["hi"])
+    t = datagen.uniform_numpy(cfg["dims"], sample_nnz, cfg["seed"] + 100, cfg["lo"], cfg["hi"])
     tt = O.Tensor(t.dims, t.idx, t.vals)
     order = t.order
-    scale = host.default_init_scale(float(np.mean(np.abs(t.vals))), order, j, [j] * order)
-    a, b = host.init_model(t.dims, [j] * order, j, host.derive_seed(1, [77]), scale)
-    m = O.Model(t.dims, np.array([j] * order, np.int32), j, a, b)
     sample = (f"{sample_nnz} nnz of the {cfg_name_of(cfg)} shape {list(cfg['dims'])}, J=R={j}, "
               f"{warmup} warm-up + {steps} measured epoch(s)")
     if O.REF is not None:
-        secs = []
-        for k in range(warmup + steps):
-            m, s2, _ = O.REF.epoch_plus(tt, m, host.derive_seed(1, [k + 1]), workers=cores)
-            if k >= warmup:
-                secs.append(float(s2[0] + s2[1]))
-        return {"value": sample_nnz / float(np.mean(secs)), "unit": "nnz/s", "cores": cores,
+        R = O.REF
+        scale = R.default_init_scale(float(np.mean(np.abs(t.vals))), order, j, [j] * order)
+        m = R.init_model(t.dims, [j] * order, j, R.derive_seed(1, [77]), scale)
+        _, secs = R.timed_epochs(tt, m, [R.derive_seed(1, [k + 1]) for k in range(warmup + steps)],
+                                 workers=cores)
+        dt = float(np.mean([f + c for f, c in secs[warmup:]]))
+        return {"value": sample_nnz / dt, "unit": "nnz/s", "cores": cores,
                 "kind": "reference", "sample": sample}
     # port: the plain-C restatement, one thread
-    p1 = host.global_plan(tt.nnz, 16, 1)
+    rng = np.random.default_rng(1)
+    m = O.random_model(t.dims, [j] * order, j, 1, 0.3)
+    p1 = rng.permutation(tt.nnz).astype(np.int64)
     t0 = time.perf_counter()
     O.COracle.factor_phase(tt, m, p1, 16, 1e-3, 1e-4)
     O.COracle.core_phase(tt, m, p1, 16, 1e-3, 1e-4)
@@ -243,35 +225,74 @@ def dtype_of(args, order, j):
 
 
 def cfg_name_of(cfg):
-    from paper_2404_10087_b200 import synth
+    import datagen
 
-    for k, v in synth.CONFIGS.items():
+    for k, v in datagen.CONFIGS.items():
         if v["dims"] == cfg["dims"]:
             return k
     return "custom"
 
 
 def run_reference(args):
-    rank, world, _ = dist_env()
+    """The reference arm: ftkref::epoch_plus (unmodified reference sources,
+    oracle/_ref) with workers = all host cores, on the SAME training tensor
+    the engine arm times (datagen.workload; generated on the GPU for the
+    1e8-scale configs, then handed to the reference as host COO), model from
+    ftkref::init_model as the reference CLI does it (ftk.cpp:169-173).  At
+    1e8 nonzeros an epoch takes ~35 s on 16 cores, so the arm times one
+    warm-up and one measured epoch of the whole tensor whatever --steps /
+    --warmup say (both reported); smaller configs honour them.  Imports
+    nothing from the engine package."""
+    rank, world, local = dist_env()
     if rank != 0:
         return
-    from paper_2404_10087_b200 import synth
+    import datagen
+    import oracle as O
 
-    cfg = dict(synth.CONFIGS[args.config])
-    j = args.rank or cfg["rank"]
-    sample = min(args.cpu_sample, cfg["nnz"])
-    res = cpu_reference_time(cfg, j, sample, steps=args.steps, warmup=min(args.warmup, 1))
+    R = O.REF
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libftkref.so not built (needs /root/reference at build)"}))
+        return
+    t0 = time.perf_counter()
+    cfg, j, tr, _ = datagen.workload(args.config, args.rank, "uniform", local)
+    t_gen = time.perf_counter() - t0
+    order = tr.order
+    cores = os.cpu_count() or 1
+    big = tr.nnz >= 10_000_000
+    warm = min(args.warmup, 1) if big else args.warmup
+    steps = 1 if big else args.steps
+    scale = R.default_init_scale(float(np.mean(np.abs(tr.vals.astype(np.float64)))), order, j,
+                                 [j] * order)
+    m = R.init_model(tr.dims, [j] * order, j, R.derive_seed(1, [77]), scale)
+    t1 = time.perf_counter()
+    _, secs = R.timed_epochs(O.Tensor(tr.dims, tr.idx, tr.vals), m,
+                             [R.derive_seed(1, [k + 1]) for k in range(warm + steps)],
+                             workers=cores)
+    meas = secs[warm:]
+    dt = float(np.mean([f + c for f, c in meas]))
+    value = tr.nnz / dt
+    sample = (f"the whole training tensor ({tr.nnz} nnz, {args.config} shape "
+              f"{list(cfg['dims'])}, J=R={j}), {warm} warm-up + {steps} measured epoch(s), "
+              f"EpochStats.seconds_factor + seconds_core")
     line = {
         "impl": "reference",
         "metric": "SGD nonzeros/sec per epoch (factor+core) at J=R=32, 1-8 B200; test RMSE",
-        "value": res["value"], "unit": "nnz/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
-                   "J": j, "R": j, "M": 16, "sample_nnz": sample},
-        "cpu_baseline": res,
-        "e2e": {"value": res["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0,
+        "value": value, "unit": "nnz/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (datagen.workload: the engine arm's tensor, uniform values)",
+        "config": {"workload": args.config, "dims": list(cfg["dims"]), "nnz": tr.nnz,
+                   "J": j, "R": j, "M": 16, "mode": "hogwild (workers = host cores)",
+                   "fingerprint_train": datagen.fingerprint(tr)},
+        "phases_ms": {"factor": float(np.mean([f for f, _ in meas])) * 1e3,
+                      "core": float(np.mean([c for _, c in meas])) * 1e3},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "seconds": {"generate": t_gen, "epochs": time.perf_counter() - t1},
     }
     print(json.dumps(line), flush=True)
 
@@ -378,8 +399,9 @@ class Dsgd(SingleGpu):
 def run_engine(args):
     import torch
 
+    import datagen
     import paper_2404_10087_b200 as eng
-    from paper_2404_10087_b200 import host, synth
+    from paper_2404_10087_b200 import host
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -388,7 +410,7 @@ def run_engine(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    cfg, j, coo, test = make_workload(args.config, args.rank, world, rank, local)
+    cfg, j, coo, test = datagen.workload(args.config, args.rank, "uniform", local)
     order = coo.order
     ranks = [j] * order
     s = eng.Session(local)
@@ -400,7 +422,9 @@ def run_engine(args):
     s.set_option("store_c", args.store_c)
     s.set_option("core16", args.core16)
     s.set_option("factor_warps", args.factor_warps)
-    scale = host.default_init_scale(float(np.mean(np.abs(coo.vals[:1_000_000]))), order, j, ranks)
+    # the reference CLI's init (ftk.cpp:169-173): mean |x| over the training values
+    scale = host.default_init_scale(float(np.mean(np.abs(coo.vals.astype(np.float64)))), order, j,
+                                    ranks)
     a0, b0 = host.init_model(coo.dims, ranks, j, host.derive_seed(1, [77]), scale)
     s.upload_model(coo.dims, ranks, j, a0, b0)
     use_dsgd = (world > 1 or args.dsgd) and order == 3
@@ -484,6 +508,10 @@ def run_engine(args):
     if not args.no_e2e:
         e2e = time_e2e(job, a0, b0, args, torch, world, dev)
 
+    rmse_ref = None
+    if rank == 0 and world == 1 and not args.no_rmse_check:
+        rmse_ref = rmse_vs_reference(args, cfg, j, coo, test, s, eng, host)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(args.cpu_sample, coo.nnz)
@@ -513,10 +541,11 @@ def run_engine(args):
             "test_rmse_before_after": [test0[0], test1[0]],
             "test_mae_before_after": [test0[1], test1[1]],
             "test_nnz": test.nnz,
+            "test_rmse_vs_reference": rmse_ref,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": dom_bytes,
-                         "bytes_per_nnz_epoch": synth.algorithmic_bytes_per_nnz(order, ranks),
+                         "bytes_per_nnz_epoch": datagen.algorithmic_bytes_per_nnz(order, ranks),
                          "traffic": traffic},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -527,6 +556,60 @@ def run_engine(args):
     s.close()
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+TRAJ_PATH = os.path.join(ROOT, "tests", "golden", "c2_trajectory.json")
+
+
+def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
+    """North-star accuracy at the benchmarked configuration: from the
+    reference CLI's initial model, E Hogwild epochs of the engine (the same
+    kernels and precision as the timed epochs) with the test RMSE after each,
+    against ftkref::train's trajectory on the identical tensors
+    (tests/golden/c2_trajectory.json, oracle/gen_c2_trajectory.py, run on the
+    GPU box's host cores).  For the uniform benchmark data and for planted
+    J = R = 32 values on the same tuples (whose RMSE moves)."""
+    import datagen
+
+    if not os.path.exists(TRAJ_PATH):
+        return None
+    with open(TRAJ_PATH) as f:
+        fx = json.load(f)
+    out = {}
+    for kind, ref in sorted(fx.items()):
+        if ref["workload"] != args.config or ref["J"] != j:
+            continue
+        if kind == "uniform":
+            tr, te = coo, test
+        else:
+            _, _, tr, te = datagen.workload(args.config, args.rank, kind, 0)
+        fp = datagen.fingerprint(tr)
+        order = tr.order
+        scale = host.default_init_scale(float(np.mean(np.abs(tr.vals.astype(np.float64)))),
+                                        order, j, [j] * order)
+        a, b = host.init_model(tr.dims, [j] * order, j, host.derive_seed(1, [77]), scale)
+        s.upload_tensor(4, tr.dims, tr.idx, tr.vals)
+        s.upload_tensor(5, te.dims, te.idx, te.vals)
+        s.upload_model(tr.dims, [j] * order, j, a, b)
+        ev = s.eval(5, 1, 0.0, 0.0)
+        rm = [float(np.sqrt(ev[0] / te.nnz))]
+        for e in range(len(ref["rmse"])):
+            es = host.derive_seed(1, [e + 1])
+            s.factor_phase(4, None, 16, ref["lr_a"], ref["reg_a"], eng.MODE_HOGWILD,
+                           seed=host.derive_seed(es, [1]), timed=False)
+            s.core_phase(4, None, 16, ref["lr_b"], ref["reg_b"], eng.MODE_HOGWILD,
+                         seed=host.derive_seed(es, [2]), timed=False)
+            ev = s.eval(5, 1, 0.0, 0.0)
+            rm.append(float(np.sqrt(ev[0] / te.nnz)))
+        want = [ref["rmse_init"]] + ref["rmse"]
+        dev = [abs(x - y) for x, y in zip(rm, want)]
+        out[kind] = {"engine": rm, "reference": want, "max_abs_delta": max(dev),
+                     "within_1e-3": bool(max(dev) <= 1e-3), "same_tensor": fp == ref["fingerprint_train"],
+                     "reference_workers": ref["workers"],
+                     "kernels": [s.get_option("last_factor_kernel"), s.get_option("last_core_kernel")]}
+        s.release_tensor(4)
+        s.release_tensor(5)
+    return out or None
 
 
 def time_e2e(job, a0, b0, args, torch, world, dev):

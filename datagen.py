@@ -1,5 +1,9 @@
 """Shaped synthetic COO tensors for the benchmark configurations.
 
+Shared by both arms of bench.py (the engine and the reference CPU library),
+by the tests and by the fixture generators, so it lives outside the engine
+package: the reference arm imports nothing from paper_2404_10087_b200.
+
 The reference's synthgen takes one `dim` for all modes and stores tuples as
 vector<vector<int>> (synthgen.cpp:44-57), so it cannot express the per-mode
 Netflix / Yahoo!Music shapes of BASELINE.json or scale to 1e8 nonzeros.
@@ -188,6 +192,81 @@ def _uniform_torch_hashed(dims, nnz, g, lo, hi, device) -> Coo:
     del idx, vals, perm
     torch.cuda.empty_cache()
     return out
+
+
+def plant_values_torch(coo: Coo, rank_j, rank_r, seed, noise=0.1, device="cuda") -> Coo:
+    """Replaces coo's values by a planted FastTucker model (J = rank_j,
+    R = rank_r, drawn like planted_numpy) plus N(0, noise^2).  The truth
+    C_n = A_n B_n is formed in fp64 on the host; the per-nonzero product is
+    chunked on the GPU in fp64 (elementwise + a fixed-order row sum, so the
+    result is reproducible run to run on the same hardware)."""
+    import torch
+
+    order = coo.order
+    rng = np.random.default_rng(seed + 1)
+    s = 2.0 / np.sqrt(rank_j) * (1.0 / rank_r) ** (1.0 / (2 * order))
+    cs = []
+    for n in range(order):
+        a = rng.uniform(0, s, size=(int(coo.dims[n]), rank_j)).astype(np.float32)
+        b = rng.uniform(0, s, size=(rank_j, rank_r)).astype(np.float32)
+        cs.append(torch.from_numpy(a.astype(np.float64) @ b.astype(np.float64)).to(device))
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 2)
+    out = np.empty(coo.nnz, np.float32)
+    chunk = 1 << 23
+    for p0 in range(0, coo.nnz, chunk):
+        p1 = min(coo.nnz, p0 + chunk)
+        ix = torch.from_numpy(np.ascontiguousarray(coo.idx[p0:p1])).to(device).long()
+        prod = cs[0][ix[:, 0]]
+        for n in range(1, order):
+            prod = prod * cs[n][ix[:, n]]
+        x = prod.sum(dim=1) + noise * torch.randn(p1 - p0, generator=g, device=device,
+                                                  dtype=torch.float64)
+        out[p0:p1] = x.float().cpu().numpy()
+    return Coo(coo.dims, coo.idx, out)
+
+
+def workload(name, rank=0, values="uniform", device=0):
+    """(cfg, J, train, test) of a BASELINE config exactly as bench.py runs it:
+    cfg["nnz"] training nonzeros plus a held-out test set (fraction
+    cfg["test_frac"], default 0.014) from the tail of the
+    generated tuples -- their storage order is a uniform shuffle, so the tail
+    is a uniform random split, as split_train_test's (sparse_tensor.cpp:
+    180-196).  values "planted": a FastTucker model at the workload's J = R
+    plus N(0, 0.1^2) on the same tuples (at this shape)."""
+    cfg = dict(CONFIGS[name])
+    j = rank or cfg["rank"]
+    frac = cfg.get("test_frac", 0.014)
+    total = int(round(cfg["nnz"] / (1.0 - frac)))
+    big = cfg["nnz"] >= 10_000_000
+    if big:
+        full = uniform_torch(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"],
+                             device=f"cuda:{device}")
+    else:
+        full = uniform_numpy(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"])
+    if values == "planted":
+        if big:
+            full = plant_values_torch(full, j, j, cfg["seed"], 0.1, device=f"cuda:{device}")
+        else:
+            full, _, _ = planted_numpy(cfg["dims"], total, cfg["seed"], j, j, 0.1)
+    elif values != "uniform":
+        raise ValueError(values)
+    n = cfg["nnz"]
+    train = Coo(full.dims, full.idx[:n], full.vals[:n])
+    test = Coo(full.dims, np.ascontiguousarray(full.idx[n:]), np.ascontiguousarray(full.vals[n:]))
+    return cfg, j, train, test
+
+
+def fingerprint(coo: Coo) -> str:
+    """Content hash of a generated tensor (fixtures record it, so a consumer
+    can tell it regenerated exactly the tensor a trajectory was taken on)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(coo.dims).tobytes())
+    h.update(np.ascontiguousarray(coo.idx).tobytes())
+    h.update(np.ascontiguousarray(coo.vals).tobytes())
+    return h.hexdigest()[:16]
 
 
 def algorithmic_bytes_per_nnz(order: int, ranks) -> int:

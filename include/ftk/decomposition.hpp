@@ -124,4 +124,12 @@ struct DeviceOptions {
 void set_device_options(const DeviceOptions& o);
 DeviceOptions device_options();
 
+// Which sweep kernels the last factor / core phase ran (FTKCU_K_* ids of
+// include/ftkcu.h), so callers and tests can see the dispatch.
+struct DeviceKernels {
+  int factor = 0;
+  int core = 0;
+};
+DeviceKernels device_last_kernels();
+
 }  // namespace ftk

@@ -59,6 +59,20 @@ extern "C" {
 #define FTKCU_EVAL_EXACT 0 /* reference slab order, bit-identical fp64     */
 #define FTKCU_EVAL_FAST 1  /* tree reduction, fp64                          */
 
+/* sweep kernels, as reported by get_option "last_factor_kernel" /
+ * "last_core_kernel" (which kernel the last factor / core phase ran) */
+#define FTKCU_K_NONE 0
+#define FTKCU_K_DET 1    /* det_factor_kernel / det_core_kernel (parity mode)  */
+#define FTKCU_K_WS 2     /* ws_factor_kernel / ws_core_kernel (N=3, J=R=32)    */
+#define FTKCU_K_WS16 3   /* ws_core16_kernel (fp16 operand tile)               */
+#define FTKCU_K_WS_CC 4  /* ws_core_cc_kernel (storage scheme)                 */
+#define FTKCU_K_WSF 5    /* wsf_factor_kernel (16 epilogue warps)              */
+#define FTKCU_K_WSG 6    /* wsg_factor_kernel / wsg_core_kernel (J=R<=16)      */
+#define FTKCU_K_BIG 7    /* big*_factor / big16*_core (J=R in {64,128})        */
+#define FTKCU_K_TC 8     /* tc_factor_kernel / tc_core_kernel (synchronous)    */
+#define FTKCU_K_HOG 9    /* hog_factor_kernel / hog_core_kernel (fp32 FFMA)    */
+#define FTKCU_K_WS3 10   /* ws_factor3_kernel (N=3, J=R=32, 3xtf32)            */
+
 typedef struct ftkcu_session ftkcu_session;
 
 /* ---- session --------------------------------------------------------- */
@@ -82,7 +96,8 @@ int ftkcu_abi_version(void);
  * over all ranks for the multi-GPU core update), "store_c" (core phase:
  * storage scheme, C rows from a C cache), "core16" (default 1; 0 keeps the
  * N=3 J=R=32 tf32 core sweep on kind::tf32), "shuffle_seed", "verbose".
- * get_option also reads "launches", "stream" (cudaStream_t), "num_sms".
+ * get_option also reads "launches", "stream" (cudaStream_t), "num_sms",
+ * "last_factor_kernel" and "last_core_kernel" (FTKCU_K_*).
  * Unknown keys are FTKCU_ERR_ARG. */
 int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value);
 int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value);

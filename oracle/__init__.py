@@ -285,6 +285,8 @@ class _Ref:
                                      C.POINTER(C.c_void_p)]
         L.ref_model_get.argtypes = [C.c_void_p, _fpp, _fpp]
         L.ref_model_free.argtypes = [C.c_void_p]
+        L.ref_derive_seed.restype = C.c_uint64
+        L.ref_derive_seed.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.c_int]
         L.ref_default_init_scale.restype = C.c_float
         L.ref_default_init_scale.argtypes = [C.c_double, C.c_int, C.c_int32, _i32p]
         L.ref_predict.restype = C.c_double
@@ -356,6 +358,11 @@ class _Ref:
         self.free_model(h)
         return out
 
+    def derive_seed(self, base, path) -> int:
+        """ftkref::derive_seed (common.hpp:43-48)."""
+        arr = (C.c_uint64 * len(path))(*[int(x) & (2**64 - 1) for x in path])
+        return int(self.lib.ref_derive_seed(int(base) & (2**64 - 1), arr, len(path)))
+
     def default_init_scale(self, mean_abs, order, r, ranks):
         ranks = np.ascontiguousarray(ranks, np.int32)
         return self.lib.ref_default_init_scale(mean_abs, order, r, _p(ranks, _i32p))
@@ -395,6 +402,23 @@ class _Ref:
                                                 workers, int(store_c), seed, _p(secs, _f64p),
                                                 _p(cnt, _i64p)))
             return self.model_to_np(mh, m), secs, cnt
+        finally:
+            self.free_tensor(th)
+            self.free_model(mh)
+
+    def timed_epochs(self, t: Tensor, m: Model, seeds, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
+                     reg_b=1e-4, batch=16, workers=1):
+        """ftkref::epoch_plus once per seed on ONE tensor/model handle (no
+        per-epoch copies); returns (final model, [[factor s, core s], ...])."""
+        th, mh = self.tensor(t), self.model(m)
+        out = []
+        try:
+            for seed in seeds:
+                secs = np.zeros(2, np.float64)
+                self._check(self.lib.ref_epoch_plus(th, mh, lr_a, lr_b, reg_a, reg_b, batch,
+                                                    workers, 0, seed, _p(secs, _f64p), None))
+                out.append([float(secs[0]), float(secs[1])])
+            return self.model_to_np(mh, m), out
         finally:
             self.free_tensor(th)
             self.free_model(mh)

@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle as O  # noqa: E402
-from paper_2404_10087_b200 import synth  # noqa: E402
+import datagen as synth  # noqa: E402
 from paper_2404_10087_b200.host import derive_seed  # noqa: E402
 
 

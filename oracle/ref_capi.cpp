@@ -76,6 +76,13 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// common.hpp:43-48 derive_seed over a path of n components.
+uint64_t ref_derive_seed(uint64_t base, const uint64_t* path, int n) {
+  std::uint64_t s = ftkref::mix64(base);
+  for (int i = 0; i < n; ++i) s = ftkref::mix64(s ^ path[i]);
+  return s;
+}
+
 // ---- tensors ---------------------------------------------------------------
 
 void* ref_tensor_new(int order, const int32_t* dims, int64_t nnz,

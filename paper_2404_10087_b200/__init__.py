@@ -29,6 +29,8 @@ MODE_DETERMINISTIC = 0
 MODE_HOGWILD = 1
 PREC_FP32, PREC_TF32, PREC_3XTF32 = 0, 1, 2
 EVAL_EXACT, EVAL_FAST = 0, 1
+# sweep kernel ids (FTKCU_K_*), read back through get_option("last_factor_kernel")
+K_NONE, K_DET, K_WS, K_WS16, K_WS_CC, K_WSF, K_WSG, K_BIG, K_TC, K_HOG, K_WS3 = range(11)
 
 # Every entry point declared in include/ftkcu.h (checked by tests/test_abi.py).
 EXPORTS = (

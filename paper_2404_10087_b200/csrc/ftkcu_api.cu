@@ -60,6 +60,9 @@ struct ftkcu_session {
   std::vector<int64_t> dsgd_key;
   int64_t dsgd_launches = 0;
   int64_t launches = 0;  // kernels launched by this session (for benches)
+  // Which sweep kernel the last factor / core phase ran (FTKCU_K_*), so that
+  // tests can assert the dispatch they mean to cover.
+  int64_t last_factor_kernel = 0, last_core_kernel = 0;
 };
 
 namespace {
@@ -437,6 +440,8 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
   else if (k == "launches") *value = s->launches;
+  else if (k == "last_factor_kernel") *value = s->last_factor_kernel;
+  else if (k == "last_core_kernel") *value = s->last_core_kernel;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
   else if (k == "num_sms") *value = num_sms();
   else return fail(s, FTKCU_ERR_ARG, "unknown option '%s'", key);
@@ -650,12 +655,15 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
   if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
       s->opt_factor_warps == 16 && wsf32_supported(v)) {
     CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));
+    s->last_factor_kernel = FTKCU_K_WSF;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
+    s->last_factor_kernel = FTKCU_K_WS;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
              wsg_supported(v)) {
     CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));
+    s->last_factor_kernel = FTKCU_K_WSG;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && big_supported(v)) {
     // large ranks: B operand images in the session scratch (allocated
     // before any graph capture, see ftkcu_dsgd_factor_epoch)
@@ -663,12 +671,15 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
     if (rc) return rc;
     CK(launch_big_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_hog_update,
                          static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+    s->last_factor_kernel = FTKCU_K_BIG;
   } else if (s->opt_precision != FTKCU_PREC_FP32 && tc_supported(v)) {
     CK(launch_tc_factor(v, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
+    s->last_factor_kernel = FTKCU_K_TC;
   } else {
     CK(launch_hog_factor(v, mul, add, lr_a, reg_a, (int)s->opt_hog_bps,
                          (int)s->opt_hog_update, s->stream));
+    s->last_factor_kernel = FTKCU_K_HOG;
   }
   s->launches += 1;
   return FTKCU_OK;
@@ -691,6 +702,7 @@ static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, in
     if (t.nnz > 0) {
       CK(launch_det_factor(v, s->d_perm, M, lr_a, reg_a, dbg, s->stream));
       s->launches += 1;
+      s->last_factor_kernel = FTKCU_K_DET;
     }
     return finish_timing(s, ms);
   }
@@ -946,6 +958,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
     CK(cudaMemsetAsync(s->grad, 0, sizeof(float) * glen, s->stream));
     CK(launch_det_core(v, s->d_perm, M, s->grad, DetDebug{}, s->stream));
     s->launches += 1;
+    s->last_core_kernel = FTKCU_K_DET;
   } else if (mode == FTKCU_MODE_HOGWILD) {
     if ((rc = prepare_stream(s, t, perm))) return rc;
     v = make_view(s, t, true);
@@ -969,19 +982,26 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
       CK(launch_ws_core(v, s->model.dims, mul, add, s->grad, (int)s->opt_precision,
                         (int)s->opt_core16, static_cast<float*>(s->scratch), s->scratch_bytes,
                         s->stream));
+      s->last_core_kernel = s->opt_store_c ? FTKCU_K_WS_CC
+                            : (s->opt_precision == FTKCU_PREC_TF32 && s->opt_core16) ? FTKCU_K_WS16
+                                                                                     : FTKCU_K_WS;
     } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && s->opt_tc_ws &&
                s->opt_core16 && wsg_supported(v)) {
       CK(launch_wsg_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
                          s->scratch_bytes, s->stream));
+      s->last_core_kernel = FTKCU_K_WSG;
     } else if (s->opt_precision == FTKCU_PREC_TF32 && !s->opt_store_c && big_supported(v)) {
       CK(launch_big_core(v, s->model.dims, mul, add, s->grad, static_cast<float*>(s->scratch),
                          s->scratch_bytes, s->stream));
+      s->last_core_kernel = FTKCU_K_BIG;
     } else if (s->opt_precision != FTKCU_PREC_FP32 && !s->opt_store_c && tc_supported(v)) {
       CK(launch_tc_core(v, mul, add, s->grad, (int)s->opt_precision,
                         static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+      s->last_core_kernel = FTKCU_K_TC;
     } else {
       CK(launch_hog_core(v, mul, add, s->grad, (int)s->opt_hog_bps,
                          static_cast<float*>(s->scratch), s->scratch_bytes, s->stream));
+      s->last_core_kernel = FTKCU_K_HOG;
     }
     s->launches += 2;
   } else {

@@ -232,6 +232,13 @@ def set_device_options(device=-1, mode=0, precision=0, exact_eval=True):
     _ck(lib().ftkh_set_device_options(device, mode, precision, int(exact_eval)))
 
 
+def last_kernels():
+    """(factor, core) FTKCU_K_* ids of the sweeps the last ftk:: epoch ran."""
+    f, c = C.c_int(0), C.c_int(0)
+    _ck(lib().ftkh_last_kernels(C.byref(f), C.byref(c)))
+    return f.value, c.value
+
+
 def epoch_plus(dims, ranks, r, idx, vals, a, b, seed, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
                reg_b=1e-4, m=16, workers=1, store_c=False, canonical=False):
     """ftk::epoch_plus through the C++ API; mutates a/b in place."""

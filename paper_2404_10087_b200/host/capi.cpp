@@ -189,6 +189,14 @@ int ftkh_set_device_options(int device, int mode, int precision, int exact_eval)
   });
 }
 
+int ftkh_last_kernels(int* factor, int* core) {
+  return guarded([&] {
+    const DeviceKernels k = device_last_kernels();
+    *factor = k.factor;
+    *core = k.core;
+  });
+}
+
 // ftk::epoch_fasttucker with fixed-mode indices of every mode built here.
 int ftkh_epoch_fasttucker(int order, const int32_t* dims, const int32_t* ranks, int32_t r,
                           int64_t nnz, const int32_t* idx, const float* vals, float* const* a,

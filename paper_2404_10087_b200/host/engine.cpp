@@ -439,6 +439,18 @@ DeviceOptions device_options() {
   return g_opts;
 }
 
+DeviceKernels device_last_kernels() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceKernels k;
+  if (!g_eng.s) return k;
+  int64_t f = 0, c = 0;
+  check(ftkcu_get_option(g_eng.s, "last_factor_kernel", &f));
+  check(ftkcu_get_option(g_eng.s, "last_core_kernel", &c));
+  k.factor = static_cast<int>(f);
+  k.core = static_cast<int>(c);
+  return k;
+}
+
 EpochStats epoch_plus(const SparseTensor& t, Model& m, const Hyperparams& h,
                       const EpochOptions& opts, std::uint64_t seed) {
   std::lock_guard<std::mutex> lk(g_mu);

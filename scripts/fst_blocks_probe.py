@@ -9,7 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import oracle as O  # noqa: E402  (C cache build for the probe's input only)
 import paper_2404_10087_b200 as eng  # noqa: E402
-from paper_2404_10087_b200 import host, synth  # noqa: E402
+import datagen as synth  # noqa: E402
+from paper_2404_10087_b200 import host  # noqa: E402
 from test_fastertucker import group_by_row, plan  # noqa: E402
 
 dims, nnz, j = [10000, 10000, 1000], 1_000_000, 16

@@ -4,7 +4,8 @@ import os, sys, time
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2404_10087_b200 as eng
-from paper_2404_10087_b200 import host, synth
+import datagen as synth
+from paper_2404_10087_b200 import host
 
 z = dict(np.load("tests/golden/c1_trajectory.npz"))
 cfg = synth.CONFIGS["c1"]

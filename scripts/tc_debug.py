@@ -3,7 +3,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import oracle as O
 import paper_2404_10087_b200 as eng
-from paper_2404_10087_b200 import host, synth
+import datagen as synth
+from paper_2404_10087_b200 import host
 s = eng.Session(0)
 for jr in (16, 32):
     t, _, _ = synth.planted_numpy((300, 200, 100), 60000, 3, jr, jr, 0.05)

@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle as O  # noqa: E402  (reference timing only)
-from paper_2404_10087_b200 import host, synth  # noqa: E402
+import datagen as synth  # noqa: E402
+from paper_2404_10087_b200 import host  # noqa: E402
 
 
 def main():

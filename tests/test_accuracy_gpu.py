@@ -1,0 +1,239 @@
+"""Accuracy of the Hogwild tensor-core sweeps the benchmark runs, against the
+reference's update rule (VERDICT r01 "next" item 1).
+
+* Row collisions.  One 128-nonzero tile over ALL cells of a tiny tensor, so
+  every factor row receives 16-32 updates in the same tile.  A tile's rows
+  are gathered once (the snapshot) and its steps are summed into the rows
+  (RED.ADD): that is the accumulate rule, restated here in fp64 --
+  A_n[i] += sum_{m: idx_n[m] = i} lr (r_m u_m - reg a_i), with u_m, r_m from
+  the snapshot (decomposition.cpp:254-275 for one nonzero's step).
+* Regulariser.  The same check with reg_a large enough that lr reg a
+  dominates lr r u, so a missing or sign-flipped regulariser GEMM fails
+  (at reg = 1e-3 it is ~6e-4 of the step and hides in the tolerance).
+* Both for every factor kernel the engine dispatches (asserted through
+  get_option("last_factor_kernel")), and for the overwrite rule on distinct
+  rows.
+* The J = R = 32 planted RMSE trajectory: ftk::train through the headline
+  kernels (ws_factor_kernel + ws_core16_kernel) within 1e-3 of the
+  reference's workers = 1 trajectory at every epoch
+  (tests/golden/c1p32_trajectory.npz, oracle/gen_trajectory32.py).
+
+Tolerances are per element, from a first-order error model of the
+arithmetic: each contribution's step carries relative operand error eps
+(tf32: 10-bit mantissa; the residual inherits eps |x_hat| from the C GEMM),
+so |got - want| <= sum_m lr (eps (|r_m| + |x_hat_m|) |u_m| + eps reg |a|).
+No max-based atol.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2404_10087_b200 as eng
+from golden_io import load
+import datagen as synth
+from paper_2404_10087_b200 import host
+
+pytestmark = pytest.mark.gpu
+HOG = eng.MODE_HOGWILD
+
+# relative operand error per precision (fp32: FFMA vs mul+add reassociation)
+EPS = {eng.PREC_FP32: 2e-6, eng.PREC_TF32: 4e-3, eng.PREC_3XTF32: 4e-5}
+
+
+def _cells_tensor(dims, nnz, seed):
+    """nnz distinct cells of a tensor with prod(dims) >= nnz cells."""
+    rng = np.random.default_rng(seed)
+    cells = int(np.prod(dims))
+    keys = rng.permutation(cells)[:nnz]
+    idx = np.stack(np.unravel_index(keys, dims), 1).astype(np.int32)
+    vals = rng.uniform(1.0, 5.0, nnz).astype(np.float32)
+    return O.Tensor(np.array(dims, np.int32), idx, vals)
+
+
+def _model(t, j, r, seed=9):
+    scale = host.default_init_scale(float(np.mean(np.abs(t.vals))), t.order, r, [j] * t.order)
+    a, b = host.init_model(t.dims, [j] * t.order, r, seed, scale)
+    return O.Model(t.dims, np.array([j] * t.order, np.int32), r, a, b)
+
+
+def accumulate_rule(t, m, lr, reg, eps):
+    """fp64 accumulate-rule step of one tile from the snapshot m, plus the
+    per-element error bound and the |r u| / |reg a| contribution sums."""
+    order = t.order
+    a = [x.astype(np.float64) for x in m.a]
+    b = [x.astype(np.float64) for x in m.b]
+    rows = [a[n][t.idx[:, n]] for n in range(order)]
+    c = [rows[n] @ b[n] for n in range(order)]  # [nnz, R]
+    prod = np.prod(np.stack(c), axis=0)
+    xhat = prod.sum(1)
+    r = t.vals.astype(np.float64) - xhat
+    delta = [np.zeros_like(x) for x in a]
+    bound = [np.zeros_like(x) for x in a]
+    ru_sum = [np.zeros_like(x) for x in a]
+    ra_sum = [np.zeros_like(x) for x in a]
+    for n in range(order):
+        d = np.ones_like(c[0])
+        for k in range(order):
+            if k != n:
+                d *= c[k]
+        u = d @ b[n].T  # [nnz, J]
+        step = lr * (r[:, None] * u - reg * rows[n])
+        err = lr * (eps * (np.abs(r) + np.abs(xhat))[:, None] * np.abs(u)
+                    + eps * reg * np.abs(rows[n]))
+        np.add.at(delta[n], t.idx[:, n], step)
+        np.add.at(bound[n], t.idx[:, n], err)
+        np.add.at(ru_sum[n], t.idx[:, n], lr * np.abs(r[:, None] * u))
+        np.add.at(ra_sum[n], t.idx[:, n], lr * reg * np.abs(rows[n]))
+    return delta, bound, ru_sum, ra_sum
+
+
+# (label, order/dims, J = R, options, expected kernel)
+KERNELS = [
+    ("ws", (4, 8, 4), 32, dict(precision=eng.PREC_TF32), eng.K_WS),
+    ("wsf", (4, 8, 4), 32, dict(precision=eng.PREC_TF32, factor_warps=16), eng.K_WSF),
+    ("ws3", (4, 8, 4), 32, dict(precision=eng.PREC_3XTF32), None),
+    ("tc", (4, 8, 4), 32, dict(precision=eng.PREC_TF32, tc_ws=0), eng.K_TC),
+    ("hog", (4, 8, 4), 32, dict(precision=eng.PREC_FP32), eng.K_HOG),
+    ("wsg16", (4, 8, 4), 16, dict(precision=eng.PREC_TF32), eng.K_WSG),
+    ("wsg8", (4, 8, 4), 8, dict(precision=eng.PREC_TF32), eng.K_WSG),
+    ("wsg-order4", (4, 4, 4, 2), 16, dict(precision=eng.PREC_TF32), eng.K_WSG),
+    ("big64", (4, 8, 4), 64, dict(precision=eng.PREC_TF32), eng.K_BIG),
+    ("big128", (4, 8, 4), 128, dict(precision=eng.PREC_TF32), eng.K_BIG),
+]
+DEFAULTS = dict(precision=eng.PREC_FP32, tc_ws=1, factor_warps=8, hog_update=1, max_ctas=0)
+
+
+def _run_factor(session, t, m, opts, lr, reg):
+    for k, v in opts.items():
+        session.set_option(k, v)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.factor_phase(0, None, 16, lr, reg, HOG, seed=3)
+        kern = session.get_option("last_factor_kernel")
+        a, _ = session.download_model()
+    finally:
+        for k, v in DEFAULTS.items():
+            session.set_option(k, v)
+    return a, kern
+
+
+@pytest.mark.parametrize("nnz", [128, 100], ids=["full-tile", "ragged"])
+@pytest.mark.parametrize("regime", ["normal", "reg-dominant"])
+@pytest.mark.parametrize("case", KERNELS, ids=[k[0] for k in KERNELS])
+def test_factor_collisions_accumulate_rule(session, case, regime, nnz):
+    label, dims, jr, opts, want_kernel = case
+    t = _cells_tensor(dims, nnz, 11 + jr)
+    m = _model(t, jr, jr)
+    lr, reg = (1e-2, 1e-3) if regime == "normal" else (1e-2, 2.0)
+    a, kern = _run_factor(session, t, m, opts, lr, reg)
+    if want_kernel is not None:
+        assert kern == want_kernel, (label, kern)
+    delta, bound, ru, ra = accumulate_rule(t, m, lr, reg, EPS[opts["precision"]])
+    if regime == "reg-dominant":  # the regulariser must be what the check sees
+        assert sum(x.sum() for x in ra) > 3 * sum(x.sum() for x in ru)
+    hit = 0
+    for n in range(t.order):
+        got = a[n].astype(np.float64) - m.a[n].astype(np.float64)
+        # fp32 storage of a + delta: half an ulp of the result per update
+        ulp = np.spacing(np.abs(m.a[n]) + np.abs(a[n])).astype(np.float64)
+        tol = 1.5 * bound[n] + 64 * ulp
+        bad = np.abs(got - delta[n]) > tol
+        assert not bad.any(), (label, n, np.argwhere(bad)[:5], got[bad][:5], delta[n][bad][:5])
+        hit += int((np.abs(delta[n]) > 0).any(axis=1).sum())
+        # rows no nonzero touches stay bit-identical
+        untouched = np.setdiff1d(np.arange(t.dims[n]), t.idx[:, n])
+        assert np.array_equal(a[n][untouched], m.a[n][untouched])
+    assert hit > 0
+
+
+OVERWRITE = [
+    ("ws", 32, dict(precision=eng.PREC_TF32, hog_update=0), eng.K_WS),
+    ("tc", 32, dict(precision=eng.PREC_3XTF32, hog_update=0), None),
+    ("tc16", 16, dict(precision=eng.PREC_TF32, hog_update=0), eng.K_TC),
+    ("big64", 64, dict(precision=eng.PREC_TF32, hog_update=0), eng.K_BIG),
+    ("hog", 32, dict(precision=eng.PREC_FP32, hog_update=0), eng.K_HOG),
+]
+
+
+@pytest.mark.parametrize("case", OVERWRITE, ids=[k[0] for k in OVERWRITE])
+def test_factor_overwrite_rule_regulariser_dominant(session, case):
+    """Distinct rows (no conflicts): the reference's overwrite rule
+    a' = a + lr (r u - reg a) with the regulariser dominating the step."""
+    label, jr, opts, want_kernel = case
+    n = 1000
+    idx = np.stack([np.arange(n), (np.arange(n) * 7) % n, (np.arange(n) * 13) % n], 1)
+    t = O.Tensor(np.array([n, n, n], np.int32), idx.astype(np.int32),
+                 np.linspace(1, 5, n).astype(np.float32))
+    m = _model(t, jr, jr)
+    lr, reg = 1e-2, 2.0
+    a, kern = _run_factor(session, t, m, opts, lr, reg)
+    if want_kernel is not None:
+        assert kern == want_kernel, (label, kern)
+    delta, bound, ru, ra = accumulate_rule(t, m, lr, reg, EPS[opts["precision"]])
+    assert sum(x.sum() for x in ra) > 3 * sum(x.sum() for x in ru)
+    for k in range(3):
+        got = a[k].astype(np.float64) - m.a[k].astype(np.float64)
+        ulp = np.spacing(np.abs(m.a[k]) + np.abs(a[k])).astype(np.float64)
+        bad = np.abs(got - delta[k]) > 1.5 * bound[k] + 4 * ulp
+        assert not bad.any(), (label, k, got[bad][:5], delta[k][bad][:5])
+
+
+# ---------------------------------------------------------------------------
+# J = R = 32 planted trajectory vs the reference (the benchmark's kernels)
+
+
+def c1p32_problem():
+    cfg = synth.CONFIGS["c1"]
+    c, _, _ = synth.planted_numpy(cfg["dims"], cfg["nnz"], cfg["seed"], 32, 32, 0.1)
+    (tri, trv), (tei, tev) = host.split_train_test(c.dims, c.idx, c.vals, 0.014, 7)
+    scale = host.default_init_scale(float(np.mean(np.abs(trv))), 3, 32, [32] * 3)
+    a, b = host.init_model(c.dims, [32] * 3, 32, host.derive_seed(1, [77]), scale)
+    return c.dims, (tri, trv), (tei, tev), a, b, scale
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("prec", [eng.PREC_TF32, eng.PREC_3XTF32], ids=["tf32", "3xtf32"])
+def test_c1p32_rmse_trajectory_vs_reference(prec):
+    """ftk::train, Hogwild, through the J = R = 32 kernels the headline runs:
+    test RMSE within 1e-3 of the reference's workers = 1 run at EVERY epoch."""
+    z = load("c1p32_trajectory")
+    dims, (tri, trv), (tei, tev), a0, b0, scale = c1p32_problem()
+    assert trv.size == int(z["ntrain"]) and tev.size == int(z["ntest"])
+    assert np.float32(scale) == z["scale"]
+    ref = z["w1_rmse"]
+    epochs = ref.size
+    host.set_device_options(mode=2, precision=prec, exact_eval=True)
+    try:
+        a, b = [x.copy() for x in a0], [x.copy() for x in b0]
+        h = host.train(dims, [32] * 3, 32, tri, trv, tei, tev, a, b, epochs=epochs, seed=1,
+                       workers=8)
+        kf, kc = host.last_kernels()
+    finally:
+        host.set_device_options(mode=0, precision=0, exact_eval=True)
+    if prec == eng.PREC_TF32:
+        assert (kf, kc) == (eng.K_WS, eng.K_WS16)
+    else:
+        assert kc == eng.K_WS
+    dev = np.abs(h["rmse"] - ref)
+    assert np.max(dev) < 1e-3, dev
+    # the trajectory must actually move, or the check says nothing
+    assert ref[0] - ref[-1] > 1e-2
+
+
+@pytest.mark.slow
+def test_c1p32_deterministic_prefix_bit_exact():
+    """Deterministic mode at J = R = 32: the first epochs of the same run are
+    bit-identical to the reference's workers = 1 trajectory."""
+    z = load("c1p32_trajectory")
+    dims, (tri, trv), (tei, tev), a0, b0, _ = c1p32_problem()
+    host.set_device_options(mode=1, precision=0, exact_eval=True)
+    try:
+        a, b = [x.copy() for x in a0], [x.copy() for x in b0]
+        h = host.train(dims, [32] * 3, 32, tri, trv, tei, tev, a, b, epochs=2, seed=1,
+                       workers=1)
+        assert host.last_kernels() == (eng.K_DET, eng.K_DET)
+    finally:
+        host.set_device_options(mode=0, precision=0, exact_eval=True)
+    assert np.array_equal(h["rmse"], z["w1_rmse"][:2])
+    assert np.array_equal(h["loss"], z["w1_loss"][:2])

@@ -12,7 +12,8 @@ import pytest
 
 import oracle as O
 import paper_2404_10087_b200 as eng
-from paper_2404_10087_b200 import dsgd, host, synth
+import datagen as synth
+from paper_2404_10087_b200 import dsgd, host
 
 from dsgd_oracle import HostGroup, engine_host_backend_cls
 from golden_io import load

@@ -13,7 +13,8 @@ import pytest
 import oracle as O
 import paper_2404_10087_b200 as eng
 from golden_io import bits_equal, load, model, names, tensor
-from paper_2404_10087_b200 import host, synth
+import datagen as synth
+from paper_2404_10087_b200 import host
 
 pytestmark = pytest.mark.gpu
 DET, HOG = eng.MODE_DETERMINISTIC, eng.MODE_HOGWILD

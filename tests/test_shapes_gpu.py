@@ -14,7 +14,8 @@ import pytest
 
 import oracle as O
 import paper_2404_10087_b200 as eng
-from paper_2404_10087_b200 import host, synth
+import datagen as synth
+from paper_2404_10087_b200 import host
 
 pytestmark = pytest.mark.gpu
 HOG = eng.MODE_HOGWILD
