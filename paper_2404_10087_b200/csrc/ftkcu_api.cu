@@ -651,7 +651,8 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
 static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t add,
                          float lr_a, float reg_a) {
   if (v.ntiles <= 0) return FTKCU_OK;
-  // the WS factor sweep is single-pass tf32; 3xtf32 runs on the tc sweep
+  // WS factor sweeps: single-pass tf32 (atomic or overwrite rows) and
+  // 3xtf32 (atomic rows); everything else on the synchronous tc sweep
   if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
       s->opt_factor_warps == 16 && wsf32_supported(v)) {
     CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));
@@ -660,6 +661,11 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
                         (int)s->opt_hog_update, s->stream));
     s->last_factor_kernel = FTKCU_K_WS;
+  } else if (s->opt_precision == FTKCU_PREC_3XTF32 && s->opt_tc_ws && s->opt_hog_update &&
+             ws_supported(v)) {
+    CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision, 1,
+                        s->stream));
+    s->last_factor_kernel = FTKCU_K_WS3;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&
              wsg_supported(v)) {
     CK(launch_wsg_factor(v, s->model.dims, mul, add, lr_a, reg_a, s->stream));

@@ -359,7 +359,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) big_factor_kernel(const __grid_c
       int64_t job = 0;
       const uint32_t dg = smem_u32(sm + L::o_d) + L::kB;
       for (int64_t k = 0; k < nk; ++k) {
-        // C(k) overwrites D'(k - 1): in-order behind U(k - 1) on the tensor pipe
+        // C(k) overwrites D'(k - 1), the A operand of tile k - 1's U GEMMs:
+        // issue it only once the last of them has completed (its commit
+        // covers all earlier MMAs of this thread).  PTX orders MMAs only per
+        // accumulator, so issue order alone would not protect D'(k - 1).
+        if (k >= 1) {
+          const int64_t u = k * kN - 1;
+          mbar_wait(&bars[B_UFULL + (int)(u % L::kUN)], (uint32_t)((u / L::kUN) & 1));
+          tc_after();
+        }
         issue_c<W, false>(sm, bars, tmem, job, 0);
         mbar_wait(&bars[B_DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n, ++job) {
@@ -553,8 +561,8 @@ constexpr int kJobs = 4 * kN;  // per tile: C and U, two halves per mode
 enum : int { FULL = 0, EMPTY = 3, IFULL = 6, IEMPTY = 10, CFULL = 14, DFULL = 15, UFULL = 16, U0READ = 19, UREAD = 20 };
 constexpr uint32_t t_u = kN * W;
 // U_0 goes to the spare region, U_n (n > 0) over C region n - 1, whose D'
-// the in-order tensor pipe has already consumed: the three U GEMMs of a tile
-// issue back to back
+// U_{n-1} has consumed (the MMA thread waits for U_{n-1} to complete before
+// it issues U_n)
 __device__ __forceinline__ uint32_t u_col(int n) { return n == 0 ? t_u : (uint32_t)(n - 1) * W; }
 // job index of the first job of tile k's U phase (C(0) comes first)
 __device__ __forceinline__ int64_t u_job(int64_t k) { return 2 * kN + k * kJobs; }
@@ -694,6 +702,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) big128_factor_kernel(const __gri
         mbar_wait(&bars[DFULL], (uint32_t)(k & 1));
         for (int n = 0; n < kN; ++n) {
           if (n == 0) mbar_wait(&bars[U0READ], (uint32_t)((k & 1) ^ 1));
+          // U_n (n > 0) accumulates over C region n - 1, whose D'_{n-1} is
+          // U_{n-1}'s A operand: wait for U_{n-1} to complete first (PTX
+          // orders MMAs only per accumulator)
+          if (n > 0) {
+            mbar_wait(&bars[UFULL + n - 1], (uint32_t)(k & 1));
+            tc_after();
+          }
           for (int hh = 0; hh < 2; ++hh) {
             const int s = wait_full();
             const uint32_t b0 = smem_u32(sm + o_st + s * kStage) + kHalfX;

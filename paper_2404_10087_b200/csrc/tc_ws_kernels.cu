@@ -61,7 +61,10 @@ struct __align__(64) WsParams {
   int exp;  // timing experiments (FTKCU_WS_EXP), never set in production
 };
 
-template <bool kCore>
+// k3: the 3xtf32 factor sweep (ws_factor3_kernel): the C GEMM operand holds
+// [B^T hi ; B^T lo] instead of [B^T ; I], and the -lr reg I region holds the
+// U GEMM's B lo.
+template <bool kCore, bool k3 = false>
 struct WsLayout {
   static constexpr uint32_t kSlot = kN * kModeTile;
   static constexpr uint32_t o_a = 0;
@@ -74,9 +77,10 @@ struct WsLayout {
   static constexpr uint32_t o_bt = o_d + d_bytes;
   static constexpr uint32_t o_btlo = o_bt + kN * (kCore ? 4096 : 8192);
   static constexpr uint32_t o_b = o_btlo + (kCore ? kN * 4096 : 0);  // B (U GEMM operand, factor)
-  // factor: -lr reg I (K-major), the regulariser as a second U GEMM operand
+  // factor: -lr reg I (K-major), the regulariser as a second U GEMM operand;
+  // 3xtf32 factor: B lo, the U GEMM's second B operand
   static constexpr uint32_t o_diag = o_b + (kCore ? 0 : kN * 4096);
-  static constexpr uint32_t o_idx = o_diag + (kCore ? 0 : 4096);
+  static constexpr uint32_t o_idx = o_diag + (kCore ? 0 : (k3 ? kN * 4096 : 4096));
   static constexpr uint32_t kIdxSlot = (kN + 1) * kRows * 4;
   static constexpr int kI = kCore ? 4 : 6;  // COO-column ring depth (decoupled from A slots)
   static constexpr uint32_t o_stage = o_idx + kI * kIdxSlot;  // factor: per-quarter write-back rows
@@ -104,6 +108,7 @@ enum : int {
   B_CEMPTY = 24,     // factor [2]: C read by the epilogue
   B_AFULL = 27,      // core: A rows copied to TMEM
   B_DEMPTY = 28,     // core [1]: G GEMM done with the D tile; factor [2]: U done with D[b]
+  B_LOFULL = 30,     // 3xtf32 factor [2]: A lo rows of tile k staged in TMEM buffer k & 1
 };
 
 // Round-to-nearest for an operand the tensor core will read as tf32: it
@@ -137,9 +142,9 @@ __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   return p.tile_base + (t * mul + add) % p.ntiles;
 }
 
-template <bool kCore>
+template <bool kCore, bool k3 = false>
 __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tslot) {
-  using L = WsLayout<kCore>;
+  using L = WsLayout<kCore, k3>;
   for (int n = 0; n < kN; ++n) {
     const float* b = p.b[n];
     for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
@@ -151,13 +156,16 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
         *reinterpret_cast<float*>(sm + L::o_btlo + n * 4096 + swz(r, j * 4, 128)) = lo;
       } else {
         *reinterpret_cast<float*>(sm + L::o_bt + n * 8192 + swz(r, j * 4, 128)) = hi;
+        // identity row r: copies a[j = r]; 3xtf32: B^T lo
         *reinterpret_cast<float*>(sm + L::o_bt + n * 8192 + swz(kW + r, j * 4, 128)) =
-            r == j ? 1.0f : 0.0f;  // identity row r: copies a[j = r]
+            k3 ? lo : (r == j ? 1.0f : 0.0f);
         *reinterpret_cast<float*>(sm + L::o_b + n * 4096 + swz(j, r * 4, 128)) = hi;
+        if constexpr (k3)
+          *reinterpret_cast<float*>(sm + L::o_diag + n * 4096 + swz(j, r * 4, 128)) = lo;
       }
     }
   }
-  if constexpr (!kCore)
+  if constexpr (!kCore && !k3)
     for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
       const int j = e / kW, jj = e - j * kW;
       *reinterpret_cast<float*>(sm + L::o_diag + swz(j, jj * 4, 128)) =
@@ -168,7 +176,8 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
       mbar_init(&bars[B_FULL + s], kGW);  // one expect_tx arrival per gather warp
       // core, and factor with atomic rows: released by the MMA that last
       // reads the slot; factor overwrite mode: by the epilogue (reads a)
-      mbar_init(&bars[B_EMPTY + s], (kCore || p.atomic_update) ? 1 : kEpiWarps);
+      // (3xtf32 factor: by the epilogue, whose fp32 step reads a)
+      mbar_init(&bars[B_EMPTY + s], (kCore || (p.atomic_update && !k3)) ? 1 : kEpiWarps);
     }
     for (int i = 0; i < L::kI; ++i) {
       mbar_init(&bars[B_IFULL + i], 1);
@@ -183,6 +192,7 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
     mbar_init(&bars[B_UFULL], 1);
     mbar_init(&bars[B_UEMPTY], kEpiWarps);
     mbar_init(&bars[B_AFULL], kEpiWarps);
+    for (int b = 0; b < 2; ++b) mbar_init(&bars[B_LOFULL + b], kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x / 32 == 1) {
@@ -209,9 +219,9 @@ __device__ void ws_teardown(uint32_t tmem) {
 
 // Warp 0: the tile's COO columns (N index columns + values, 512 B each) by
 // 1-D bulk copies into a kI-deep ring, running ahead of the gathers.
-template <bool kCore>
+template <bool kCore, bool k3 = false>
 __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
-  using L = WsLayout<kCore>;
+  using L = WsLayout<kCore, k3>;
   if ((threadIdx.x & 31) != 0) return;
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
@@ -231,9 +241,9 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
 // Gather warps: as soon as an A slot is free, TMA gather4 of the tile's
 // factor rows (N modes x 32 groups of 4 rows) into it; gather warp w issues
 // groups [w * 96 / kGW, (w + 1) * 96 / kGW) and arrives with its own bytes.
-template <bool kCore>
+template <bool kCore, bool k3 = false>
 __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
-  using L = WsLayout<kCore>;
+  using L = WsLayout<kCore, k3>;
   const int lane = threadIdx.x & 31, gw = (int)(threadIdx.x >> 5) - kGatherWarp;
   constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
   static_assert(kGroups % (kGW * 8) == 0, "whole batches of 8 groups per gather warp");
@@ -286,8 +296,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   // TMEM: tile k in buffer b = k & 1 at 192 b; mode n at +64 n holds C_n
   // (overwritten in place by D'_n) and, with atomic rows, a copy of the A
   // rows (+32, from the identity half of the C GEMM's B operand) for the
-  // regulariser GEMM; U at 384.  C(k + 2) reuses buffer b only after U(k):
-  // the MMA warp issues U(k) first and the tensor pipe runs in order.
+  // regulariser GEMM; U at 384.  C(k + 2) reuses buffer b only after U(k)
+  // has completed (the MMA thread waits for its commit).
   constexpr uint32_t kC = 0, kU = 384, kBuf = 192, kMs = 64;
 
   if (warp == 0) {
@@ -326,6 +336,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kS), b = (int)(k & 1);
         mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+        // C(k) overwrites buffer b, whose D'(k - 2) is U(k - 2)'s A operand:
+        // issue it once U(k - 2) has completed (PTX orders MMAs only per
+        // accumulator; U(k - 1) is not issued yet, so the phase is exact)
+        if (k >= 2) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
@@ -483,6 +497,232 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
     for (int64_t k = 0; k < nk; ++k) {
       if (k + 1 < nk) epi1(k + 1, nxt);
       epi2(k, cur);
+      cur = nxt;
+    }
+  }
+  ws_teardown(tmem);
+}
+
+// ---- factor sweep, 3xtf32 ----------------------------------------------------------
+//
+// fp32-equivalent products on the tf32 tensor cores (hi*hi + hi*lo + lo*hi,
+// the split of ws_core_kernel / tc_factor_kernel) for the headline shape:
+//   C_n = A B_n:    A straight from the slot (the tensor core reads its tf32
+//                   truncation A_hi); A_lo = A - A_hi staged into TMEM by the
+//                   epilogue; B hi / lo in shared memory;
+//   U_n = D_n B_n^T with D_n = prod_{m != n} C_m split hi / lo by the
+//                   epilogue into TMEM (hi over C_n, lo over A_lo_n);
+//   step           = lr (r u - reg a) in fp32 in the epilogue with a from the
+//                   slot -- the reference's own expression
+//                   (decomposition.cpp:257-270) -- then RED.ADD (the Hogwild
+//                   accumulate rule).
+// TMEM: buffer b = k & 1 at 192 b; mode n at +64 n: C_n / D_hi_n (32
+// columns), then A_lo_n / D_lo_n (32); U at 384.  The epilogue releases the
+// slot after the step (it reads a there), and stages A_lo(k + 2) only after
+// epi2(k) has seen U(k) complete, so C(k + 2) is never issued into buffer
+// k & 1 before U(k) has read D(k) from it: no reliance on execution order
+// between MMAs of different accumulators.
+__global__ void __launch_bounds__(kThreadsWs, 1) ws_factor3_kernel(const __grid_constant__ WsParams p) {
+  using L = WsLayout<false, true>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
+  ws_setup<false, true>(p, sm, bars, tslot);
+  const uint32_t tmem = *tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kU = 384, kBuf = 192, kMs = 64;
+
+  if (warp == 0) {
+    ws_idx_producer<false, true>(p, sm, bars, nk);
+  } else if (warp >= kGatherWarp) {
+    ws_gather_producer<false, true>(p, sm, bars, nk);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
+      const uint32_t bt = smem_u32(sm + L::o_bt), bb = smem_u32(sm + L::o_b);
+      const uint32_t bl = smem_u32(sm + L::o_diag);
+      auto issue_u = [&](int64_t j) {
+        const int b = (int)(j & 1);
+        mbar_wait(&bars[B_DFULL + b], (uint32_t)((j >> 1) & 1));
+        mbar_wait(&bars[B_UEMPTY], (uint32_t)((j & 1) ^ 1));
+        tc_after();
+        const uint32_t tb = tmem + b * kBuf;
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 8; ++ks) {
+            const uint64_t dh = sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128);
+            mma_ts(tmem + kU + n * kW, tb + n * kMs + ks * 8, dh, id, ks > 0);
+            mma_ts(tmem + kU + n * kW, tb + n * kMs + ks * 8,
+                   sdesc(bl + n * 4096 + ks * 32, 16, 1024, 128), id, 1);
+            mma_ts(tmem + kU + n * kW, tb + n * kMs + kW + ks * 8, dh, id, 1);
+          }
+        mma_commit(&bars[B_UFULL]);
+      };
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kS), b = (int)(k & 1);
+        mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+        mbar_wait(&bars[B_LOFULL + b], (uint32_t)((k >> 1) & 1));
+        tc_after();
+        const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+        const uint32_t tb = tmem + b * kBuf;
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int ks = 0; ks < kW / 8; ++ks) {
+            const uint64_t da = sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128);
+            const uint64_t dh = sdesc(bt + n * 8192 + ks * 32, 16, 1024, 128);
+            mma_ss(tb + n * kMs, da, dh, id, ks > 0);
+            mma_ss(tb + n * kMs, da, sdesc(bt + n * 8192 + 4096 + ks * 32, 16, 1024, 128), id, 1);
+            mma_ts(tb + n * kMs, tb + n * kMs + kW + ks * 8, dh, id, 1);
+          }
+        mma_commit(&bars[B_CFULL + b]);
+        if (k >= 1) issue_u(k - 1);
+      }
+      if (nk >= 1) issue_u(nk - 1);
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    struct Tile {
+      int32_t g[kN];
+      float resid;
+      int slot;
+    };
+    Tile cur, nxt;
+    // A_lo of this thread's row (column half h) -> TMEM buffer k & 1
+    auto stage_lo = [&](int64_t k) {
+      const int s = (int)(k % kS), b = (int)(k & 1);
+      mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
+      const uint8_t* slot = sm + L::o_a + s * L::kSlot;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 x = *reinterpret_cast<const float4*>(
+              slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+          v[q4 * 4 + 0] = tf32_rn_bits(x.x - tf32_trunc(x.x));
+          v[q4 * 4 + 1] = tf32_rn_bits(x.y - tf32_trunc(x.y));
+          v[q4 * 4 + 2] = tf32_rn_bits(x.z - tf32_trunc(x.z));
+          v[q4 * 4 + 3] = tf32_rn_bits(x.w - tf32_trunc(x.w));
+        }
+        tmem_st16(tl + b * kBuf + n * kMs + kW + h * 16, v);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_LOFULL + b]);
+    };
+    auto epi1 = [&](int64_t k, Tile& t) {
+      const int s = (int)(k % kS), b = (int)(k & 1), ii = (int)(k % L::kI);
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
+      const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
+      mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
+      tc_after();
+      const uint32_t tb = tl + b * kBuf;
+      float c[kN][16];
+      {
+        uint32_t v[kN][16];
+#pragma unroll
+        for (int n = 0; n < kN; ++n) tmem_ld16(tb + n * kMs + h * 16, v[n]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int n = 0; n < kN; ++n)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[n][i]);
+      }
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      float* xp = reinterpret_cast<float*>(sm + L::o_xp);
+      xp[(b * 2 + h) * kRows + row] = part;
+      named_bar(1 + q, 64);
+      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
+      t.slot = s;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) t.g[n] = s_idx[n * kRows + row];
+      const float xv = s_val[row];
+      const int nvalid = reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_IEMPTY + ii]);
+      const bool ok = row < nvalid;
+      t.resid = ok ? xv - xhat : 0.0f;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) t.g[n] = ok ? t.g[n] : -1;
+      // D_n split: hi = the tf32 the tensor core reads (round to nearest),
+      // lo = the exact remainder (rounded to tf32 in turn)
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float d = n == 0 ? c[1][i] * c[2][i] : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
+          hi[i] = tf32_rn_bits(d) & 0xFFFFE000u;
+          lo[i] = tf32_rn_bits(d - __uint_as_float(hi[i]));
+        }
+        tmem_st16(tb + n * kMs + h * 16, hi);
+        tmem_st16(tb + n * kMs + kW + h * 16, lo);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
+    };
+    auto epi2 = [&](int64_t k, const Tile& t) {
+      int32_t gq[kN][4];
+#pragma unroll
+      for (int n = 0; n < kN; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], i * 8 + (lane >> 2));
+      mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
+      tc_after();
+      uint32_t u[kN][16];
+#pragma unroll
+      for (int n = 0; n < kN; ++n) tmem_ld16(tl + kU + n * kW + h * 16, u[n]);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
+      const float r = t.resid, lr = p.lr, reg = p.reg;
+      const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
+      uint8_t* stage = sm + L::o_stage + ew * 2048;
+#pragma unroll
+      for (int n = 0; n < kN; ++n) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 a = *reinterpret_cast<const float4*>(
+              slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+          float4 st;
+          st.x = lr * (r * __uint_as_float(u[n][q4 * 4 + 0]) - reg * a.x);
+          st.y = lr * (r * __uint_as_float(u[n][q4 * 4 + 1]) - reg * a.y);
+          st.z = lr * (r * __uint_as_float(u[n][q4 * 4 + 2]) - reg * a.z);
+          st.w = lr * (r * __uint_as_float(u[n][q4 * 4 + 3]) - reg * a.w);
+          *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
+        }
+        __syncwarp();
+        float* dst = p.a[n];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rl = i * 8 + (lane >> 2), ch = lane & 3;
+          const int32_t g = gq[n][i];
+          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
+          if (g >= 0) red_add_v4(dst + (size_t)g * kW + h * 16 + ch * 4, v);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);  // a read: the slot is free
+    };
+    if (nk > 0) stage_lo(0);
+    if (nk > 1) stage_lo(1);
+    if (nk > 0) epi1(0, cur);
+    for (int64_t k = 0; k < nk; ++k) {
+      if (k + 1 < nk) epi1(k + 1, nxt);
+      epi2(k, cur);
+      if (k + 2 < nk) stage_lo(k + 2);  // U(k) has completed: buffer k & 1 is free
       cur = nxt;
     }
   }
@@ -1149,8 +1389,10 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   p.prec3 = precision == FTKCU_PREC_3XTF32;
   p.exp = ws_exp_bits();
   if (p.ntiles == 0) return cudaSuccess;
-  const int bytes = (int)WsLayout<false>::bytes;
-  auto kern = atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>;
+  const bool k3 = p.prec3 && atomic_update;
+  const int bytes = (int)(k3 ? WsLayout<false, true>::bytes : WsLayout<false>::bytes);
+  auto kern = k3 ? ws_factor3_kernel
+                 : (atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   const int grid = (int)sweep_grid(v);

@@ -447,6 +447,9 @@ __global__ void __launch_bounds__(FW<W>::Threads, 1)
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % L::kS), b = (int)(k & 1);
         mbar_wait(&bars[G_FULL + s], (uint32_t)((k / L::kS) & 1));
+        // C(k) overwrites buffer b, whose D'(k - 2) is U(k - 2)'s A operand:
+        // wait for U(k - 2) to complete (PTX orders MMAs only per accumulator)
+        if (k >= 2) mbar_wait(&bars[G_UFULL], (uint32_t)((k - 2) & 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
