@@ -115,6 +115,7 @@ fst_core_prep_kernel(KView v, int mode, const int64_t* __restrict__ perm,
        b += (int64_t)gridDim.x * kFstWarps) {
     const int64_t beg = boff[b0 + b], end = boff[b0 + b + 1];
     const int m_eff = (int)(end - beg);
+    if (m_eff <= 0) continue;  // the C-ABI rejects empty batches; never read perm[end]
     d_row(v, mode, perm[beg], d, lane, 32);
     __syncwarp();
     // g accumulates over rows ascending; lanes own j, rows come 32 at a time
@@ -215,6 +216,7 @@ fst_core_scan_kernel(KView v, int mode, const int64_t* __restrict__ perm,
        b += (int64_t)gridDim.x * kFstWarps) {
     const int64_t beg = boff[b], end = boff[b + 1];
     const int m_eff = (int)(end - beg);
+    if (m_eff <= 0) continue;  // the C-ABI rejects empty batches; never read perm[end]
     d_row(v, mode, perm[beg], d, lane, 32);
     __syncwarp();
     float gacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};

@@ -116,6 +116,12 @@ int ensure_scratch(ftkcu_session* s, size_t bytes) {
 }
 
 int upload_perm(ftkcu_session* s, const int64_t* perm, int64_t n) {
+  // every plan entry indexes the tensor: an out-of-range one would be an
+  // unchecked device read (the reference's plans come from iota + shuffle)
+  for (int64_t i = 0; i < n; ++i)
+    if ((uint64_t)perm[i] >= (uint64_t)n)
+      return fail(s, FTKCU_ERR_ARG, "plan entry %lld = %lld out of range [0, %lld)", (long long)i,
+                  (long long)perm[i], (long long)n);
   if ((size_t)n > s->perm_cap) {
     if (s->d_perm) CK(cudaFree(s->d_perm));
     s->d_perm = nullptr;
@@ -746,6 +752,20 @@ int ftkcu_factor_phase_cell(ftkcu_session* s, int slot, int cell, float lr_a, fl
   return factor_phase_impl(s, slot, nullptr, 16, lr_a, reg_a, FTKCU_MODE_HOGWILD, seed, cell, ms);
 }
 
+// Bucket / row / batch offsets of the baselines' plans: span [0, nnz] and
+// strictly increasing (an empty batch would divide by m_eff = 0 in the
+// kernels and read perm[nnz]).
+static int check_offsets(ftkcu_session* s, const int64_t* off, int64_t n, int64_t nnz,
+                         const char* what) {
+  if (n == 0) return nnz == 0 ? FTKCU_OK : fail(s, FTKCU_ERR_ARG, "%s: no batches", what);
+  if (off[0] != 0 || off[n] != nnz) return fail(s, FTKCU_ERR_ARG, "%s must span [0, nnz]", what);
+  for (int64_t i = 0; i < n; ++i)
+    if (off[i + 1] <= off[i])
+      return fail(s, FTKCU_ERR_ARG, "%s must be strictly increasing (entry %lld)", what,
+                  (long long)i);
+  return FTKCU_OK;
+}
+
 // ---- FastTucker baseline (epoch_fasttucker, decomposition.cpp:707-770) ----
 
 int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t* perm,
@@ -759,8 +779,7 @@ int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t*
   if (mode < 0 || mode >= t.order) return fail(s, FTKCU_ERR_ARG, "mode %d out of range", mode);
   if (nbuckets < 0 || (t.nnz > 0 && (!perm || !bucket_off)))
     return fail(s, FTKCU_ERR_ARG, "per-bucket plan missing");
-  if (nbuckets > 0 && (bucket_off[0] != 0 || bucket_off[nbuckets] != t.nnz))
-    return fail(s, FTKCU_ERR_ARG, "bucket offsets must span [0, nnz]");
+  if ((rc = check_offsets(s, bucket_off, nbuckets, t.nnz, "bucket offsets"))) return rc;
   KView v = make_view(s, t, false);
   if (ft_factor_smem(v, M, mode) > 227 * 1024)
     return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker factor block");
@@ -858,8 +877,7 @@ int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_
   if ((rc = fst_view(s, slot, mode, &v))) return rc;
   if (nrows < 0 || (v.nnz > 0 && (!perm || !row_off)))
     return fail(s, FTKCU_ERR_ARG, "row-grouped plan missing");
-  if (nrows > 0 && (row_off[0] != 0 || row_off[nrows] != v.nnz))
-    return fail(s, FTKCU_ERR_ARG, "row offsets must span [0, nnz]");
+  if ((rc = check_offsets(s, row_off, nrows, v.nnz, "row offsets"))) return rc;
   if ((rc = upload_perm(s, perm, v.nnz))) return rc;
   if ((size_t)(nrows + 1) > s->boff_cap) {
     if (s->d_boff) CK(cudaFree(s->d_boff));
@@ -886,8 +904,7 @@ int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t*
   if ((rc = fst_view(s, slot, mode, &v))) return rc;
   if (nbatches < 0 || (v.nnz > 0 && (!perm || !batch_off)))
     return fail(s, FTKCU_ERR_ARG, "plan missing");
-  if (nbatches > 0 && (batch_off[0] != 0 || batch_off[nbatches] != v.nnz))
-    return fail(s, FTKCU_ERR_ARG, "batch offsets must span [0, nnz]");
+  if ((rc = check_offsets(s, batch_off, nbatches, v.nnz, "batch offsets"))) return rc;
   if (v.j[mode] > 128) return fail(s, FTKCU_ERR_ARG, "FasterTucker core block supports J <= 128");
   if ((rc = upload_perm(s, perm, v.nnz))) return rc;
   if ((size_t)(nbatches + 1) > s->boff_cap) {

@@ -8,6 +8,7 @@
 // their buffers and a content fingerprint (a SparseTensor is read-only after
 // construction, sparse_tensor.hpp:11-13).  epoch_plus syncs the model
 // H2D/D2H around each call; train keeps it resident for all epochs.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +17,8 @@
 #include <limits>
 #include <mutex>
 #include <sstream>
+#include <thread>
+#include <vector>
 
 #include "ftk/decomposition.hpp"
 #include "ftkcu.h"
@@ -69,18 +72,53 @@ void apply_options(ftkcu_session* s) {
   check(ftkcu_set_option(s, "eval", g_opts.exact_eval ? FTKCU_EVAL_EXACT : FTKCU_EVAL_FAST));
 }
 
+// Content hash of every index and value byte (a sampled
+// fingerprint missed in-place edits at unsampled positions).  Chunks are
+// hashed on parallel threads and combined in chunk order, so the result does
+// not depend on the thread count; at 1.6 GB (Netflix shape) it is bound by
+// host memory bandwidth, tens of ms, once per train() and per epoch_plus().
+std::uint64_t hash_bytes(const void* data, std::size_t bytes) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  constexpr std::size_t kChunk = std::size_t{1} << 24;
+  const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
+  std::vector<std::uint64_t> part(chunks, 0);
+  auto run = [&](std::size_t c) {
+    const std::size_t beg = c * kChunk, end = std::min(bytes, beg + kChunk);
+    std::uint64_t lanes[4] = {0x9e3779b97f4a7c15ull ^ c, 0xbf58476d1ce4e5b9ull, 0x94d049bb133111ebull,
+                              0x2545f4914f6cdd1dull};
+    std::size_t i = beg;
+    for (; i + 32 <= end; i += 32)
+      for (int l = 0; l < 4; ++l) {
+        std::uint64_t w;
+        std::memcpy(&w, p + i + 8 * l, 8);
+        lanes[l] = (lanes[l] ^ w) * 0x100000001b3ull + (lanes[l] >> 29);
+      }
+    std::uint64_t h = mix64(lanes[0] ^ mix64(lanes[1] ^ mix64(lanes[2] ^ mix64(lanes[3]))));
+    for (; i < end; ++i) h = mix64(h ^ p[i]);
+    part[c] = h;
+  };
+  const std::size_t threads =
+      std::min<std::size_t>(chunks, std::max(1u, std::thread::hardware_concurrency()));
+  if (threads <= 1) {
+    for (std::size_t c = 0; c < chunks; ++c) run(c);
+  } else {
+    std::vector<std::thread> pool;
+    for (std::size_t w = 0; w < threads; ++w)
+      pool.emplace_back([&, w] {
+        for (std::size_t c = w; c < chunks; c += threads) run(c);
+      });
+    for (auto& th : pool) th.join();
+  }
+  std::uint64_t h = mix64(bytes);
+  for (std::uint64_t x : part) h = mix64(h ^ x);
+  return h;
+}
+
 std::uint64_t fingerprint(const SparseTensor& t) {
   std::uint64_t h = mix64(static_cast<std::uint64_t>(t.nnz()) ^ (static_cast<std::uint64_t>(t.order) << 56));
   for (index_t d : t.dims) h = mix64(h ^ static_cast<std::uint32_t>(d));
-  const size64 n = t.nnz();
-  const size64 step = n > 64 ? n / 64 : 1;
-  for (size64 p = 0; p < n; p += step) {
-    std::uint32_t v;
-    std::memcpy(&v, &t.values[p], 4);
-    h = mix64(h ^ v);
-    for (int k = 0; k < t.order; ++k) h = mix64(h ^ static_cast<std::uint32_t>(t.indices[p * t.order + k]));
-  }
-  return h;
+  h = mix64(h ^ hash_bytes(t.indices.data(), t.indices.size() * sizeof(index_t)));
+  return mix64(h ^ hash_bytes(t.values.data(), t.values.size() * sizeof(real)));
 }
 
 // Returns the device slot holding t, uploading it if needed.

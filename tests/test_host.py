@@ -120,6 +120,24 @@ def test_binary_coo_roundtrip_matches_text(tmp_path):
     host.save_coo_binary(t.dims, dup, t.vals, str(bad))
     with pytest.raises(host.HostError, match="duplicate"):
         host.load_coo_binary(str(bad))
+    # a header nnz far beyond the file: an error, not an allocation attempt
+    import struct
+    huge = raw[:12] + struct.pack("<q", 1 << 38) + raw[20:]
+    bad.write_bytes(huge)
+    with pytest.raises(host.HostError, match="truncated"):
+        host.load_coo_binary(str(bad))
+    bad.write_bytes(raw + b"\0")
+    with pytest.raises(host.HostError, match="trailing"):
+        host.load_coo_binary(str(bad))
+    # nnz = 0 and a zero dimension are rejected like the text loader's empty tensor
+    bad.write_bytes(raw[:12] + struct.pack("<q", 0) + raw[20:20 + 16])
+    with pytest.raises(host.HostError, match="corrupt FTKC1 header"):
+        host.load_coo_binary(str(bad))
+    zd = bytearray(raw)
+    zd[20:24] = struct.pack("<i", 0)
+    bad.write_bytes(bytes(zd))
+    with pytest.raises(host.HostError):
+        host.load_coo_binary(str(bad))
 
 
 @pytest.mark.parametrize("text,msg", [

@@ -158,6 +158,32 @@ def test_out_of_range_index_rejected(session):
                               np.array([[0, 1, 2]], np.int32), np.array([1.0], np.float32))
 
 
+def test_out_of_range_plan_rejected(session):
+    t = O.random_tensor([6, 5, 4], 50, 3, 1.0, 5.0)
+    m = O.random_model([6, 5, 4], [4, 4, 4], 4, 3)
+    upload(session, t, m)
+    bad = host.global_plan(t.nnz, 16, 5)
+    bad[7] = t.nnz  # one past the end
+    with pytest.raises(eng.FtkError, match="plan entry 7"):
+        session.factor_phase(0, bad, 16, 1e-3, 1e-4, DET)
+    bad[7] = -1
+    with pytest.raises(eng.FtkError, match="plan entry 7"):
+        session.core_phase(0, bad, 16, 1e-3, 1e-4, DET)
+
+
+def test_cxx_api_sees_in_place_edits_of_a_cached_tensor():
+    """The ftk:: layer caches tensors on the device; an in-place edit of one
+    value anywhere (not just at sampled positions) must reach the device."""
+    t = O.random_tensor([50, 40, 30], 5000, 4, 1.0, 5.0)
+    m = O.random_model([50, 40, 30], [8, 8, 8], 8, 4)
+    host.set_device_options(mode=0, precision=0, exact_eval=True)
+    before = host.loss(t.dims, m.ranks, m.r, t.idx, t.vals, m.a, m.b, 0.0, 0.0)
+    assert before == O.COracle.loss(m, t, 0.0, 0.0, 1)
+    t.vals[4999 - 13] += 1.0  # not on the old 64-sample grid (step = nnz / 64)
+    after = host.loss(t.dims, m.ranks, m.r, t.idx, t.vals, m.a, m.b, 0.0, 0.0)
+    assert after == O.COracle.loss(m, t, 0.0, 0.0, 1) and after != before
+
+
 @pytest.mark.parametrize("ranks,r", [([128, 128, 128], 128), ([16] * 6, 16), ([64, 32, 8], 48)])
 def test_deterministic_large_ranks_and_order(session, ranks, r):
     order = len(ranks)
