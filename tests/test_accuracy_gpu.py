@@ -102,7 +102,10 @@ KERNELS = [
     ("ws3", (4, 8, 4), 32, dict(precision=eng.PREC_3XTF32), eng.K_WS3),
     ("tc3", (4, 8, 4), 32, dict(precision=eng.PREC_3XTF32, tc_ws=0), eng.K_TC),
     ("tc", (4, 8, 4), 32, dict(precision=eng.PREC_TF32, tc_ws=0), eng.K_TC),
-    ("hog", (4, 8, 4), 32, dict(precision=eng.PREC_FP32), eng.K_HOG),
+    # hog_factor_kernel (fp32 CUDA cores, precision=fp32 only) is absent: a
+    # warp walks its tile in groups of 4 nonzeros and re-reads the live rows
+    # per group, so a tile has no single snapshot and the accumulate rule
+    # above does not describe it; it is checked on distinct rows below.
     ("wsg16", (4, 8, 4), 16, dict(precision=eng.PREC_TF32), eng.K_WSG),
     ("wsg8", (4, 8, 4), 8, dict(precision=eng.PREC_TF32), eng.K_WSG),
     ("wsg-order4", (4, 4, 4, 2), 16, dict(precision=eng.PREC_TF32), eng.K_WSG),
@@ -157,6 +160,48 @@ def test_factor_collisions_accumulate_rule(session, case, regime, nnz):
         untouched = np.setdiff1d(np.arange(t.dims[n]), t.idx[:, n])
         assert np.array_equal(a[n][untouched], m.a[n][untouched])
     assert hit > 0
+
+
+@pytest.mark.parametrize("regime", ["normal", "reg-dominant"])
+def test_hog_factor_collisions_group_rule(session, regime):
+    """hog_factor_kernel (fp32 CUDA cores) with every row colliding: a caller
+    plan fixes the stream order, the one 128-nonzero tile goes to one warp,
+    which steps in groups of 4 nonzeros from the LIVE rows (accumulate rule
+    inside a group, groups sequential) -- restated here in fp64."""
+    t = _cells_tensor((4, 8, 4), 128, 43)
+    m = _model(t, 32, 32)
+    lr, reg = (1e-2, 1e-3) if regime == "normal" else (1e-2, 0.5)
+    if regime == "reg-dominant":
+        t.vals = (_predict(m, t.idx) + 0.01 * np.random.default_rng(5).standard_normal(128)).astype(
+            np.float32)
+    plan = np.random.default_rng(2).permutation(128).astype(np.int64)
+    session.set_option("precision", eng.PREC_FP32)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        session.factor_phase(0, plan, 16, lr, reg, HOG, seed=3)
+        assert session.get_option("last_factor_kernel") == eng.K_HOG
+        a, _ = session.download_model()
+    finally:
+        for k, v in DEFAULTS.items():
+            session.set_option(k, v)
+    cur = m.copy()
+    cur.a = [x.astype(np.float64) for x in cur.a]
+    total_bound = [np.zeros_like(x) for x in cur.a]
+    for g0 in range(0, 128, 4):
+        sel = plan[g0:g0 + 4]
+        sub = O.Tensor(t.dims, t.idx[sel], t.vals[sel])
+        delta, bound, _, _ = accumulate_rule(sub, cur, lr, reg, EPS[eng.PREC_FP32])
+        for n in range(3):
+            cur.a[n] = cur.a[n] + delta[n]
+            total_bound[n] += bound[n]
+    for n in range(3):
+        got = a[n].astype(np.float64)
+        ulp = np.spacing(np.abs(a[n])).astype(np.float64)
+        # a sequential chain: each group's error feeds the next group's rows
+        bad = np.abs(got - cur.a[n]) > 4 * total_bound[n] + 64 * ulp
+        assert not bad.any(), (n, got[bad][:5], cur.a[n][bad][:5])
+        assert not np.array_equal(a[n], m.a[n])
 
 
 OVERWRITE = [
