@@ -231,7 +231,8 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
                              float lr, float reg, int precision, int atomic_update,
                              cudaStream_t st);
 // core16: the single-pass sweep gathers an fp16 copy of A (ws_core16_kernel);
-// 0 = tf32 rows copied into TMEM (ws_core_kernel).  3xtf32 and the storage
+// 2 = the same with two epilogue warp groups taking alternate tiles; 0 = tf32
+// rows copied into TMEM (ws_core_kernel).  3xtf32 and the storage
 // scheme have their own kernels.
 cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                            float* grad, int precision, int core16, float* scratch,

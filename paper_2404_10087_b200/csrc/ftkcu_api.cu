@@ -37,14 +37,14 @@ struct ftkcu_session {
   int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
-  int64_t opt_core16 = 1;   // WS core sweep (tf32 precision): gather an fp16 copy of A
+  int64_t opt_core16 = 1;   // WS core sweep (tf32 precision): gather an fp16 copy of A (2: two epilogue groups)
   int64_t opt_factor_warps = 8;  // N=3 J=R=32 factor sweep: 8 or 16 epilogue warps
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
-  int64_t opt_max_ctas = 0;  // factor-sweep grid cap (0 = one CTA per SM)
+  int64_t opt_max_ctas = 0;  // sweep grid cap (0 = one CTA per SM)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
   // dsgd.grid_cap for the measurement behind the default.
@@ -115,13 +115,14 @@ int ensure_scratch(ftkcu_session* s, size_t bytes) {
   return FTKCU_OK;
 }
 
-int upload_perm(ftkcu_session* s, const int64_t* perm, int64_t n) {
+// n plan entries, each a nonzero position in [0, bound) (bound = nnz)
+int upload_perm(ftkcu_session* s, const int64_t* perm, int64_t n, int64_t bound) {
   // every plan entry indexes the tensor: an out-of-range one would be an
   // unchecked device read (the reference's plans come from iota + shuffle)
   for (int64_t i = 0; i < n; ++i)
-    if ((uint64_t)perm[i] >= (uint64_t)n)
+    if ((uint64_t)perm[i] >= (uint64_t)bound)
       return fail(s, FTKCU_ERR_ARG, "plan entry %lld = %lld out of range [0, %lld)", (long long)i,
-                  (long long)perm[i], (long long)n);
+                  (long long)perm[i], (long long)bound);
   if ((size_t)n > s->perm_cap) {
     if (s->d_perm) CK(cudaFree(s->d_perm));
     s->d_perm = nullptr;
@@ -283,7 +284,7 @@ void tile_perm(uint64_t seed, int64_t ntiles, int64_t* mul, int64_t* add) {
 // order (one gather pass, plan-generation cost, outside the sweep timing).
 int prepare_stream(ftkcu_session* s, DevTensor& t, const int64_t* perm) {
   if (perm) {
-    int rc = upload_perm(s, perm, t.nnz);
+    int rc = upload_perm(s, perm, t.nnz, t.nnz);
     if (rc) return rc;
     CK(build_shuffled(t, s->d_perm, 0, nullptr, 0, s->stream));
     t.shuffled = false;  // stream is in a caller order, not the session shuffle
@@ -398,7 +399,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "store_c") {
     s->opt_store_c = value != 0;
   } else if (k == "core16") {
-    s->opt_core16 = value != 0;
+    if (value < 0 || value > 2) return fail(s, FTKCU_ERR_ARG, "core16 must be 0, 1 or 2");
+    s->opt_core16 = value;
   } else if (k == "factor_warps") {
     if (value != 8 && value != 16) return fail(s, FTKCU_ERR_ARG, "factor_warps must be 8 or 16");
     s->opt_factor_warps = value;
@@ -707,7 +709,7 @@ static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, in
   DevTensor& t = s->slots[slot];
   if (mode == FTKCU_MODE_DETERMINISTIC) {
     if (!perm && t.nnz > 0) return fail(s, FTKCU_ERR_ARG, "deterministic mode needs a permutation");
-    if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+    if ((rc = upload_perm(s, perm, t.nnz, t.nnz))) return rc;
     KView v = make_view(s, t, false);
     DetDebug dbg{};
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -783,7 +785,7 @@ int ftkcu_fasttucker_factor(ftkcu_session* s, int slot, int mode, const int64_t*
   KView v = make_view(s, t, false);
   if (ft_factor_smem(v, M, mode) > 227 * 1024)
     return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker factor block");
-  if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+  if ((rc = upload_perm(s, perm, t.nnz, t.nnz))) return rc;
   if ((size_t)(nbuckets + 1) > s->boff_cap) {
     if (s->d_boff) CK(cudaFree(s->d_boff));
     s->d_boff = nullptr;
@@ -810,7 +812,7 @@ int ftkcu_fasttucker_core(ftkcu_session* s, int slot, int mode, const int64_t* p
   KView v = make_view(s, t, false);
   if (ft_core_smem(v, M) > 227 * 1024)
     return fail(s, FTKCU_ERR_ARG, "batch too large for the FastTucker core block");
-  if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+  if ((rc = upload_perm(s, perm, t.nnz, t.nnz))) return rc;
   CK(cudaEventRecord(s->ev0, s->stream));
   if (schedule != FTKCU_MODE_DETERMINISTIC && schedule != FTKCU_MODE_HOGWILD)
     return fail(s, FTKCU_ERR_ARG, "unknown schedule %d", schedule);
@@ -878,7 +880,7 @@ int ftkcu_fastertucker_factor(ftkcu_session* s, int slot, int mode, const int64_
   if (nrows < 0 || (v.nnz > 0 && (!perm || !row_off)))
     return fail(s, FTKCU_ERR_ARG, "row-grouped plan missing");
   if ((rc = check_offsets(s, row_off, nrows, v.nnz, "row offsets"))) return rc;
-  if ((rc = upload_perm(s, perm, v.nnz))) return rc;
+  if ((rc = upload_perm(s, perm, v.nnz, v.nnz))) return rc;
   if ((size_t)(nrows + 1) > s->boff_cap) {
     if (s->d_boff) CK(cudaFree(s->d_boff));
     s->d_boff = nullptr;
@@ -906,7 +908,7 @@ int ftkcu_fastertucker_core(ftkcu_session* s, int slot, int mode, const int64_t*
     return fail(s, FTKCU_ERR_ARG, "plan missing");
   if ((rc = check_offsets(s, batch_off, nbatches, v.nnz, "batch offsets"))) return rc;
   if (v.j[mode] > 128) return fail(s, FTKCU_ERR_ARG, "FasterTucker core block supports J <= 128");
-  if ((rc = upload_perm(s, perm, v.nnz))) return rc;
+  if ((rc = upload_perm(s, perm, v.nnz, v.nnz))) return rc;
   if ((size_t)(nbatches + 1) > s->boff_cap) {
     if (s->d_boff) CK(cudaFree(s->d_boff));
     s->d_boff = nullptr;
@@ -974,7 +976,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
   KView v;
   if (mode == FTKCU_MODE_DETERMINISTIC) {
     if (!perm) return fail(s, FTKCU_ERR_ARG, "deterministic mode needs a permutation");
-    if ((rc = upload_perm(s, perm, t.nnz))) return rc;
+    if ((rc = upload_perm(s, perm, t.nnz, t.nnz))) return rc;
     v = make_view(s, t, false);
     if (s->opt_store_c && (rc = prepare_ccache(s, v))) return rc;
     CK(cudaEventRecord(s->ev0, s->stream));
@@ -985,6 +987,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
   } else if (mode == FTKCU_MODE_HOGWILD) {
     if ((rc = prepare_stream(s, t, perm))) return rc;
     v = make_view(s, t, true);
+    v.max_ctas = (int)s->opt_max_ctas;  // grid cap (tests: many tiles per CTA)
     int64_t mul = 1, add = 0;
     if (!perm) tile_perm(seed ^ 0xc0e5ull, v.ntiles, &mul, &add);
     size_t need = (size_t)num_sms() * 16 * glen * sizeof(float);
@@ -1066,7 +1069,7 @@ int ftkcu_batch_probe(ftkcu_session* s, int slot, const int64_t* rows, int m_eff
   if (rc) return rc;
   if ((rc = check_ready(s, slot))) return rc;
   if (cap < 1 || m_eff < 0 || m_eff > cap) return fail(s, FTKCU_ERR_ARG, "batch overflow");
-  if ((rc = upload_perm(s, rows, m_eff))) return rc;
+  if ((rc = upload_perm(s, rows, m_eff, s->slots[slot].nnz))) return rc;
   const DevModel& m = s->model;
   const int order = m.order, r = m.r, jmax = m.max_j();
   const size_t n_cr = (size_t)order * cap * r, n_cj = (size_t)order * cap * jmax;

@@ -1084,7 +1084,14 @@ __global__ void ws_half_kernel(const float* __restrict__ src, __half* __restrict
   }
 }
 
-__global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_constant__ WsParams p) {
+// kEG epilogue groups of 8 warps: group g takes the tiles k = g (mod kEG), so
+// two tiles' epilogues run concurrently (the TMEM C buffer, r D tile and x_hat
+// exchange are already double-buffered by k & 1); gather warps follow them.
+template <int kEG>
+__global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
+    ws_core16_kernel(const __grid_constant__ WsParams p) {
+  static_assert(kEG == 1 || kEG == 2, "one or two epilogue groups (two C buffers)");
+  constexpr int kGather16 = 2 + kEG * kEpiWarps;
   using L = Ws16Layout;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
@@ -1142,8 +1149,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
           bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
         bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
       }
-  } else if (warp >= kGatherWarp) {
-    const int gw = warp - kGatherWarp;
+  } else if (warp >= kGather16) {
+    const int gw = warp - kGather16;
     constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % L::kS), i = (int)(k % L::kI);
@@ -1206,10 +1213,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
       if (nk >= 1) issue_g(nk - 1);
     }
   } else {
-    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int ew = warp - 2, q = warp & 3, eg = ew / kEpiWarps, h = (ew >> 2) & 1;
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    for (int64_t k = 0; k < nk; ++k) {
+    for (int64_t k = eg; k < nk; k += kEG) {
       const int b = (int)(k & 1), ii = (int)(k % L::kI);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
@@ -1236,7 +1243,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
       for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
       float* xp = reinterpret_cast<float*>(sm + L::o_xp);
       xp[(b * 2 + h) * kRows + row] = part;
-      named_bar(1 + q, 64);
+      named_bar(1 + q + 4 * eg, 64);
       const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
       const bool ok = row < reinterpret_cast<const int32_t*>(sm + L::o_rows)[ii];
       const float resid = ok ? s_val[row] - xhat : 0.0f;
@@ -1269,7 +1276,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core16_kernel(const __grid_c
     }
     if (nk > 0) mbar_wait(&bars[H_DEMPTY + (int)((nk - 1) & 1)], (uint32_t)(((nk - 1) >> 1) & 1));
     tc_after();
-    if (q < kN) {
+    if (eg == 0 && q < kN) {
       uint32_t v[16];
       tmem_ld16(tl + kG + q * kW + h * 16, v);
       tmem_wait_ld();
@@ -1407,7 +1414,7 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   if (!make_params(p, v, dims, mul, add, true)) return cudaErrorNotSupported;
   p.prec3 = precision == FTKCU_PREC_3XTF32;
   p.exp = ws_exp_bits();
-  const int grid = (int)(p.ntiles < num_sms() ? p.ntiles : num_sms());
+  const int grid = (int)sweep_grid(v);
   const int len = kN * kW * kW;
   if (grid < 1) return cudaErrorInvalidValue;
   if (scratch_bytes < (size_t)grid * len * sizeof(float)) return cudaErrorInvalidValue;
@@ -1429,9 +1436,11 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
       a16 += cnt;
     }
     const int bytes = (int)Ws16Layout::bytes;
-    e = cudaFuncSetAttribute(ws_core16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    const int groups = core16 >= 2 ? 2 : 1;
+    auto kern = groups == 2 ? ws_core16_kernel<2> : ws_core16_kernel<1>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
-    ws_core16_kernel<<<grid, kThreadsWs, bytes, st>>>(p);
+    kern<<<grid, (2 + groups * kEpiWarps + kGW) * 32, bytes, st>>>(p);
   } else {
     const int bytes = (int)WsLayout<true>::bytes;
     auto kern = v.cc[0] ? ws_core_cc_kernel : ws_core_kernel;

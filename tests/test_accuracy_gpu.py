@@ -296,3 +296,61 @@ def test_c1p32_deterministic_prefix_bit_exact():
         host.set_device_options(mode=0, precision=0, exact_eval=True)
     assert np.array_equal(h["rmse"], z["w1_rmse"][:2])
     assert np.array_equal(h["loss"], z["w1_loss"][:2])
+
+
+# ---------------------------------------------------------------------------
+# Core gradient of the J = R = 32 core sweeps, per element
+
+
+def core_grad_fp64(t, m):
+    """G_n[j][r] = sum_t r_t A_n[t][j] D_n[t][r] (accumulate_core_grads_plus,
+    decomposition.cpp:277-296) in fp64, plus the first-order error scale
+    sum_t (|r_t| + |x_hat_t|) |A_n[t][j]| |D_n[t][r]| (every operand carries
+    relative error eps; the residual inherits eps |x_hat| from the C GEMM)."""
+    a = [x.astype(np.float64) for x in m.a]
+    b = [x.astype(np.float64) for x in m.b]
+    rows = [a[n][t.idx[:, n]] for n in range(t.order)]
+    c = [rows[n] @ b[n] for n in range(t.order)]
+    xhat = np.prod(np.stack(c), axis=0).sum(1)
+    r = t.vals.astype(np.float64) - xhat
+    g, scale = [], []
+    for n in range(t.order):
+        d = np.ones_like(c[0])
+        for k in range(t.order):
+            if k != n:
+                d *= c[k]
+        g.append(rows[n].T @ (r[:, None] * d))
+        scale.append(np.abs(rows[n]).T @ ((np.abs(r) + np.abs(xhat))[:, None] * np.abs(d)))
+    return np.concatenate([x.ravel() for x in g]), np.concatenate([x.ravel() for x in scale])
+
+
+@pytest.mark.parametrize("core16,max_ctas", [(1, 0), (2, 0), (2, 1), (2, 3), (0, 0)],
+                         ids=["ws16", "ws16x2", "ws16x2-1cta", "ws16x2-3cta", "ws-tf32"])
+def test_core32_gradient_per_element(session, core16, max_ctas):
+    """The headline core sweep (ws_core16_kernel: fp16 copy of A, fp32
+    accumulate), with one or two epilogue groups and many tiles per CTA
+    (max_ctas = 1: every tile on one CTA, both groups and every ring slot
+    reused), against the fp64 gradient element by element."""
+    c = synth.planted_numpy((300, 200, 100), 300000, 4, 32, 32, 0.05)[0]
+    t = O.Tensor(c.dims, c.idx, c.vals)  # 2344 tiles: 16 per CTA on 148 SMs
+    m = _model(t, 32, 32)
+    session.set_option("precision", eng.PREC_TF32)
+    session.set_option("core16", core16)
+    session.set_option("max_ctas", max_ctas)
+    try:
+        session.upload_tensor(0, t.dims, t.idx, t.vals)
+        session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
+        _, g = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=5, want_grad=True)
+        kern = session.get_option("last_core_kernel")
+    finally:
+        for k, v in DEFAULTS.items():
+            session.set_option(k, v)
+        session.set_option("core16", 1)
+    assert kern == (eng.K_WS16 if core16 else eng.K_WS)
+    want, scale = core_grad_fp64(t, m)
+    eps = 2.0 ** -10  # fp16 / tf32 operands (10-bit mantissa), rounded to nearest
+    err = np.abs(g.astype(np.float64) - want)
+    bad = err > 2 * eps * scale + 1e-6 * np.abs(want).max()
+    assert not bad.any(), (np.argwhere(bad)[:5], g[bad][:5], want[bad][:5])
+    # the bound is meaningful: the typical error is well inside it
+    assert np.median(err / (eps * scale)) < 0.5
