@@ -267,6 +267,11 @@ int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t
 /* Sum all-reduce of host fp64 values (metrics partials). */
 int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n);
 /* Waits for all work queued on the session stream. */
+// Measurement only (no reference counterpart): the J = R = 32 factor
+// sweep's RED.v4 write-back alone over slot's Hogwild tile stream, into
+// scratch rows (the model is untouched); *ms = device time.  bench.py uses it
+// as the roofline ceiling of the factor sweep at L2-resident shapes.
+int ftkcu_writeback_ceiling(ftkcu_session* s, int slot, uint64_t seed, double* ms);
 int ftkcu_stream_sync(ftkcu_session* s);
 
 #ifdef __cplusplus

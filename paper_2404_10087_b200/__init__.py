@@ -44,7 +44,7 @@ EXPORTS = (
     "ftkcu_comm_sendrecv_rows", "ftkcu_comm_bcast_rows", "ftkcu_comm_allreduce_f64",
     "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch", "ftkcu_fasttucker_factor",
     "ftkcu_fasttucker_core", "ftkcu_ccache_upload", "ftkcu_ccache_download",
-    "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core",
+    "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core", "ftkcu_writeback_ceiling",
 )
 
 
@@ -113,6 +113,7 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_comm_bcast_rows.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_int]
     L.ftkcu_comm_allreduce_f64.argtypes = [C.c_void_p, _f64p, C.c_int]
     L.ftkcu_stream_sync.argtypes = [C.c_void_p]
+    L.ftkcu_writeback_ceiling.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _f64p]
     L.ftkcu_dsgd_factor_epoch.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
                                           C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
     _lib = L
@@ -366,3 +367,11 @@ class Session:
 
     def sync(self):
         self._ck(self.lib.ftkcu_stream_sync(self.h))
+
+    def writeback_ceiling(self, slot=0, seed=0) -> float:
+        """Device ms of the J = R = 32 factor sweep's RED write-back alone over
+        slot's tile stream (measurement; the model is untouched)."""
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_writeback_ceiling(self.h, slot, C.c_uint64(seed & (2**64 - 1)),
+                                                  C.byref(ms)))
+        return ms.value

@@ -238,6 +238,11 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
                            float* grad, int precision, int core16, float* scratch,
                            size_t scratch_bytes, cudaStream_t st);
 
+// Measurement: the headline factor sweep's RED write-back alone (roofline
+// ceiling at L2-resident shapes); dst_dev: device array of order pointers.
+cudaError_t launch_ws_writeback(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                                float* const* dst_dev, cudaStream_t st);
+
 // ---- evaluation (eval_kernels.cu) ---------------------------------------------
 // out3 = {sum sq, sum abs, reg}; exact = reference slab order.
 cudaError_t run_eval(const DevModel& m, const DevTensor& t, int workers,

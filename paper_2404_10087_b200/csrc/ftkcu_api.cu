@@ -754,6 +754,46 @@ int ftkcu_factor_phase_cell(ftkcu_session* s, int slot, int cell, float lr_a, fl
   return factor_phase_impl(s, slot, nullptr, 16, lr_a, reg_a, FTKCU_MODE_HOGWILD, seed, cell, ms);
 }
 
+// Measurement only: the headline factor sweep's RED write-back alone over
+// slot's Hogwild tile stream (same grid and tile order as
+// ftkcu_factor_phase with this seed), into scratch rows -- the model is not
+// touched.  *ms = its device time.
+int ftkcu_writeback_ceiling(ftkcu_session* s, int slot, uint64_t seed, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  DevTensor& t = s->slots[slot];
+  if ((rc = prepare_stream(s, t, nullptr))) return rc;
+  KView v = make_view(s, t, true);
+  v.max_ctas = (int)s->opt_max_ctas;
+  if (!ws_supported(v)) return fail(s, FTKCU_ERR_ARG, "write-back ceiling: N = 3, J = R = 32 only");
+  int64_t mul = 1, add = 0;
+  tile_perm(seed, v.ntiles, &mul, &add);
+  const DevModel& m = s->model;
+  size_t total = 0;
+  for (int n = 0; n < m.order; ++n) total += (size_t)m.dims[n] * 32;
+  float* buf = nullptr;
+  float** ptrs = nullptr;
+  CK(cudaMalloc(&buf, sizeof(float) * total));
+  CK(cudaMalloc(&ptrs, sizeof(float*) * m.order));
+  float* h[kMaxOrder];
+  size_t off = 0;
+  for (int n = 0; n < m.order; ++n) {
+    h[n] = buf + off;
+    off += (size_t)m.dims[n] * 32;
+  }
+  CK(cudaMemcpyAsync(ptrs, h, sizeof(float*) * m.order, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemsetAsync(buf, 0, sizeof(float) * total, s->stream));
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(launch_ws_writeback(v, m.dims, mul, add, ptrs, s->stream));
+  s->launches += 1;
+  rc = finish_timing(s, ms);
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaFree(ptrs));
+  CK(cudaFree(buf));
+  return rc;
+}
+
 // Bucket / row / batch offsets of the baselines' plans: span [0, nnz] and
 // strictly increasing (an empty batch would divide by m_eff = 0 in the
 // kernels and read perm[nnz]).

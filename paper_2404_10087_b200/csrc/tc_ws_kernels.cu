@@ -1158,6 +1158,13 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       mbar_wait(&bars[H_IFULL + i], (uint32_t)((k / L::kI) & 1));
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
       uint8_t* slot = sm + L::o_a + s * L::kSlot;
+      if (p.exp & 2) {  // exp 2: no gathers (timing only)
+        if (lane == 0) {
+          mbar_arrive(&bars[H_IEMPTY + i]);
+          mbar_arrive(&bars[H_FULL + s]);
+        }
+        continue;
+      }
       __syncwarp();
       if (elect_one()) {
         mbar_expect_tx(&bars[H_FULL + s], kPer * 256);
@@ -1188,10 +1195,11 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         // G[j'][n R + r] += sum_t A[t][j'] (r D_n)[t][r]: M = 3 stacked modes
         // (+ one garbage block), N = 96, K = 16 nonzeros per instruction
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot), dd = d0 + db * L::kSlot;
+        if (!(p.exp & 4))  // exp 4: no G GEMM (timing only)
 #pragma unroll
-        for (int ks = 0; ks < kRows / 16; ++ks)
-          mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
-                  sdesc_l(dd + ks * 1024, kModeTile16, 512, 4), idg, (k > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < kRows / 16; ++ks)
+            mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
+                    sdesc_l(dd + ks * 1024, kModeTile16, 512, 4), idg, (k > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&bars[H_DEMPTY + db]);
         mma_commit(&bars[H_EMPTY + s]);
       };
@@ -1227,8 +1235,15 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       {  // the three modes' columns in flight before one wait
         uint32_t v[kN][16];
 #pragma unroll
-        for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 96 + n * kW + h * 16, v[n]);
-        tmem_wait_ld();
+        if (!(p.exp & 128)) {  // exp 128: no TMEM loads (timing only)
+          for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 96 + n * kW + h * 16, v[n]);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int n = 0; n < kN; ++n)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[n][i] = __float_as_uint((float)(row + i));
+        }
 #pragma unroll
         for (int n = 0; n < kN; ++n)
 #pragma unroll
@@ -1251,6 +1266,11 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       if (lane == 0) mbar_arrive(&bars[H_IEMPTY + ii]);
       mbar_wait(&bars[H_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // G(k - 2) done with D[b]
       uint8_t* dt = sm + L::o_d + b * L::kSlot;
+      if (p.exp & 32) {  // exp 32: no r D tile (timing only)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[H_DFULL + b]);
+        continue;
+      }
       // r D'_n: r (C_1 C_2), (r C_0) C_2, (r C_0) C_1 -- five products per column
       float rc0[16];
 #pragma unroll
@@ -1286,6 +1306,52 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
     }
   }
   ws_teardown(tmem);
+}
+
+// ---- write-back ceiling (measurement) ------------------------------------------
+//
+// The factor sweep's write-back alone, for the roofline that binds at
+// L2-resident shapes: same tile stream, thread -> (row, column half) map,
+// 2 KB per-warp staging tiles and 8-row RED.v4 groups as epi2 of
+// ws_factor_kernel<true> -- no gathers, no MMA, no TMEM -- at full occupancy
+// (8 CTAs per SM, so index-load latency is hidden), adding 1.0f to
+// every element of each nonzero's three rows of `dst` (a scratch copy of the
+// factor shapes).  Its time is the floor the full sweep's RED stream sets.
+__global__ void __launch_bounds__(kEpiWarps * 32, 8)
+    ws_writeback_kernel(const __grid_constant__ WsParams p, float* const* dst) {
+  __shared__ __align__(16) uint8_t stage_all[kEpiWarps * 2048];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = (warp + 2) & 3, h = warp >> 2;  // the epilogue warps' map (warp 2 + w)
+  const int row = q * 32 + lane;
+  uint8_t* stage = stage_all + warp * 2048;
+  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  for (int64_t k = 0; k < nk; ++k) {
+    const int64_t tile = ws_tile(p, k);
+    const bool ok = row < __ldg(p.tile_rows + tile);
+    int32_t g[kN];
+#pragma unroll
+    for (int n = 0; n < kN; ++n) g[n] = ok ? __ldg(p.idx[n] + tile * kRows + row) : -1;
+    int32_t gq[kN][4];
+#pragma unroll
+    for (int n = 0; n < kN; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, g[n], i * 8 + (lane >> 2));
+#pragma unroll
+    for (int n = 0; n < kN; ++n) {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = make_float4(1.f, 1.f, 1.f, 1.f);
+      __syncwarp();
+      float* d = dst[n];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rl = i * 8 + (lane >> 2), ch = lane & 3;
+        const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
+        if (gq[n][i] >= 0) red_add_v4(d + (size_t)gq[n][i] * kW + h * 16 + ch * 4, v);
+      }
+      __syncwarp();
+    }
+  }
 }
 
 __global__ void ws_reduce_kernel(const float* __restrict__ partials, int nparts, int len,
@@ -1451,6 +1517,19 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ws_reduce_kernel<<<(len + 255) / 256, 256, 0, st>>>(scratch, grid, len, grad);
+  return cudaGetLastError();
+}
+
+// Write-back ceiling of the N = 3, J = R = 32 factor sweep on this tile
+// stream (see ws_writeback_kernel); dst[n] = I_n x 32 fp32 scratch.
+cudaError_t launch_ws_writeback(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
+                                float* const* dst_dev, cudaStream_t st) {
+  WsParams p{};
+  if (!make_params(p, v, dims, mul, add, false)) return cudaErrorNotSupported;
+  if (p.ntiles == 0) return cudaSuccess;
+  // full occupancy (8 CTAs of 8 warps per SM): the ceiling is the RED rate
+  // of this address stream, not the latency of the probe's own index loads
+  ws_writeback_kernel<<<(int)sweep_grid(v, 8), kEpiWarps * 32, 0, st>>>(p, dst_dev);
   return cudaGetLastError();
 }
 
