@@ -117,7 +117,13 @@ enum class DevicePrecision { kFp32, kTf32, k3xTf32 };
 struct DeviceOptions {
   int device = -1;                 // -1: $FTK_DEVICE, else 0
   DeviceMode mode = DeviceMode::kAuto;  // kAuto: workers == 1 -> deterministic
-  DevicePrecision precision = DevicePrecision::kFp32;
+  // Hogwild sweeps (workers > 1): tf32 factor / fp16-copy core operands with
+  // fp32 accumulate on the tensor cores -- test-RMSE parity with the
+  // reference is tests/test_accuracy_gpu.py and bench.py's
+  // test_rmse_vs_reference; kFp32 runs the fp32 CUDA-core sweeps, k3xTf32
+  // fp32-equivalent split products.  Deterministic mode (workers == 1) is
+  // bit-exact fp32 whatever this says.
+  DevicePrecision precision = DevicePrecision::kTf32;
   bool exact_eval = true;          // reference slab order in loss/evaluate
 };
 

@@ -227,8 +227,9 @@ def save_coo(dims, idx, vals, path):
                             _p(vals, _f32p), path.encode()))
 
 
-def set_device_options(device=-1, mode=0, precision=0, exact_eval=True):
-    """mode 0 auto / 1 deterministic / 2 hogwild; precision 0 fp32 / 1 tf32 / 2 3xtf32."""
+def set_device_options(device=-1, mode=0, precision=1, exact_eval=True):
+    """mode 0 auto / 1 deterministic / 2 hogwild; precision 0 fp32 / 1 tf32
+    (the C++ default) / 2 3xtf32."""
     _ck(lib().ftkh_set_device_options(device, mode, precision, int(exact_eval)))
 
 
