@@ -324,13 +324,14 @@ def core_grad_fp64(t, m):
     return np.concatenate([x.ravel() for x in g]), np.concatenate([x.ravel() for x in scale])
 
 
-@pytest.mark.parametrize("core16,max_ctas", [(1, 0), (2, 0), (2, 1), (2, 3), (0, 0)],
-                         ids=["ws16", "ws16x2", "ws16x2-1cta", "ws16x2-3cta", "ws-tf32"])
+@pytest.mark.parametrize("core16,max_ctas", [(1, 0), (1, 1), (1, 3), (2, 0), (2, 1), (0, 0)],
+                         ids=["ws16", "ws16-1cta", "ws16-3cta", "ws16x2", "ws16x2-1cta", "ws-tf32"])
 def test_core32_gradient_per_element(session, core16, max_ctas):
     """The headline core sweep (ws_core16_kernel: fp16 copy of A, fp32
-    accumulate), with one or two epilogue groups and many tiles per CTA
-    (max_ctas = 1: every tile on one CTA, both groups and every ring slot
-    reused), against the fp64 gradient element by element."""
+    accumulate) with one (core16 = 1) or two (core16 = 2) epilogue warp
+    groups and many tiles per CTA (max_ctas = 1: all 2344 tiles on one CTA,
+    both C buffers, D tiles and every ring slot reused), against the fp64
+    gradient element by element."""
     c = synth.planted_numpy((300, 200, 100), 300000, 4, 32, 32, 0.05)[0]
     t = O.Tensor(c.dims, c.idx, c.vals)  # 2344 tiles: 16 per CTA on 148 SMs
     m = _model(t, 32, 32)
