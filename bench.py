@@ -571,7 +571,8 @@ def run_engine(args):
             "roofline": roofline_of(dom, dom_ms, dom_bytes, achieved, peak, peak_kind, traffic,
                                     wb, datagen.algorithmic_bytes_per_nnz(order, ranks),
                                     {"factor": f_avg, "core": c_avg},
-                                    {"factor": f_bytes, "core": c_bytes}),
+                                    {"factor": f_bytes, "core": c_bytes,
+                                     "core_rows": job.local_nnz * order}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -582,6 +583,10 @@ def run_engine(args):
     if world > 1:
         torch.distributed.destroy_process_group()
 
+
+# TMA tile::gather4 row-rate ceiling measured on this pool's B200 (rows/s,
+# profiles/r02_gather_rate.txt): the core sweep's binding limit.
+GATHER_ROW_CEILING = 59.3e9
 
 KERNEL_NAMES = {  # FTKCU_K_* (include/ftkcu.h) per sweep
     "factor": {1: "det_factor_kernel", 2: "ws_factor_kernel", 5: "wsf_factor_kernel",
@@ -645,8 +650,18 @@ def roofline_of(dom, dom_ms, dom_bytes, achieved, peak, peak_kind, traffic, wb, 
         return out
     ach = wb["bytes"] / (dom_ms * 1e-3) / 1e9
     ceil = wb["bytes"] / (wb["ms"] * 1e-3) / 1e9
+    kernels = {"factor": {"bound": "l2_red", "achieved_GBs": ach, "peak_GBs": ceil,
+                          "frac": ach / ceil}}
+    if "core" in ms and ms["core"] > 0 and nbytes.get("core_rows"):
+        rows_s = nbytes["core_rows"] / (ms["core"] * 1e-3)
+        kernels["core"] = {
+            "bound": "tma_gather_rows", "achieved_rows_per_s": rows_s,
+            "peak_rows_per_s": GATHER_ROW_CEILING, "frac": rows_s / GATHER_ROW_CEILING,
+            "peak_source": "profiles/r02_gather_rate.txt (TMA tile::gather4 row-rate ceiling, "
+                           "scripts/microtests/gather_rate.cu on this pool's B200)",
+            "rows_note": "3 gathered rows (one per mode) per nonzero"}
     return {"bound": "l2_red", "kernel": dom, "achieved": ach, "peak": ceil, "unit": "GB/s",
-            "frac": ach / ceil,
+            "frac": ach / ceil, "kernels": kernels,
             "peak_source": ("measured live: ftkcu_writeback_ceiling, the sweep's RED.v4 "
                             "write-back alone on the same tile stream "
                             f"({wb['ms']:.3f} ms for {wb['bytes']} B)"),
