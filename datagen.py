@@ -227,6 +227,8 @@ def plant_values_torch(coo: Coo, rank_j, rank_r, seed, noise=0.1, device="cuda")
 
 
 def workload(name, rank=0, values="uniform", device=0):
+    # device: a CUDA ordinal, or "cpu" (torch's CPU generator: a statistically
+    # equivalent tensor, not the bench's bytes) for the 1e8-scale configs
     """(cfg, J, train, test) of a BASELINE config exactly as bench.py runs it:
     cfg["nnz"] training nonzeros plus a held-out test set (fraction
     cfg["test_frac"], default 0.014) from the tail of the
@@ -239,14 +241,14 @@ def workload(name, rank=0, values="uniform", device=0):
     frac = cfg.get("test_frac", 0.014)
     total = int(round(cfg["nnz"] / (1.0 - frac)))
     big = cfg["nnz"] >= 10_000_000
+    dev = device if isinstance(device, str) else f"cuda:{device}"
     if big:
-        full = uniform_torch(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"],
-                             device=f"cuda:{device}")
+        full = uniform_torch(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"], device=dev)
     else:
         full = uniform_numpy(cfg["dims"], total, cfg["seed"], cfg["lo"], cfg["hi"])
     if values == "planted":
         if big:
-            full = plant_values_torch(full, j, j, cfg["seed"], 0.1, device=f"cuda:{device}")
+            full = plant_values_torch(full, j, j, cfg["seed"], 0.1, device=dev)
         else:
             full, _, _ = planted_numpy(cfg["dims"], total, cfg["seed"], j, j, 0.1)
     elif values != "uniform":

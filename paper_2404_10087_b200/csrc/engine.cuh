@@ -97,6 +97,12 @@ struct KView {
   // Factor sweeps: cap on resident CTAs (0 = one per SM), bounds how many
   // nonzeros are in flight against the same A rows (Hogwild staleness).
   int max_ctas;
+  // Headline factor sweep (ws_factor_kernel): 0 = a tile's row slot is freed
+  // when its C GEMM completes (gathers run up to kS tiles ahead of the
+  // write-back); W in {2, 3} = freed only after the tile's write-back is
+  // issued and a gather waits for tile k - W to retire, so at most W tiles
+  // per CTA are between reading and writing their rows (Hogwild staleness).
+  int window;
   // Optional device {mul, add} of the tile permutation (overrides the launch
   // arguments; lets a captured CUDA graph take a new permutation per epoch).
   const int64_t* tperm;

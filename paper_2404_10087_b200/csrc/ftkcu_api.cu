@@ -45,6 +45,7 @@ struct ftkcu_session {
   int rank = 0, world = 1;
   int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
   int64_t opt_max_ctas = 0;  // sweep grid cap (0 = one CTA per SM)
+  int64_t opt_window = 0;  // headline factor sweep read-to-write window in tiles (0 = ring depth)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
   // dsgd.grid_cap for the measurement behind the default.
@@ -421,6 +422,10 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "max_ctas") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "max_ctas must be >= 0");
     s->opt_max_ctas = value;
+  } else if (k == "window") {
+    if (value != 0 && value != 2 && value != 3)
+      return fail(s, FTKCU_ERR_ARG, "window must be 0, 2 or 3");
+    s->opt_window = value;
   } else if (k == "shuffle_seed") {
     s->opt_shuffle_seed = value;
     for (auto& t : s->slots) t.shuffled = false;
@@ -444,6 +449,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "factor_warps") *value = s->opt_factor_warps;
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
+  else if (k == "window") *value = s->opt_window;
   else if (k == "staleness") *value = s->opt_staleness;
   else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
@@ -724,6 +730,7 @@ static int factor_phase_impl(ftkcu_session* s, int slot, const int64_t* perm, in
   if ((rc = prepare_stream(s, t, perm))) return rc;
   KView v = make_view(s, t, true);
   v.max_ctas = (int)s->opt_max_ctas;
+  v.window = (int)s->opt_window;
   if (cell < 0 && s->opt_staleness > 0) {
     int64_t rows = s->model.dims[0];
     for (int n = 1; n < s->model.order; ++n) rows = std::min<int64_t>(rows, s->model.dims[n]);

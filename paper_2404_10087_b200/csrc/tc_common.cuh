@@ -142,6 +142,29 @@ __device__ __forceinline__ uint32_t f16x2_sat(float lo, float hi) {
   return r;
 }
 
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two IEEE round-to-nearest fp32
+// operations per instruction, lane for lane the scalar result).
+struct f2 {
+  float x, y;
+};
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("{.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mov.b64 c, {%6, %7};\n\tfma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ uint32_t f16x2_sat(f2 v) { return f16x2_sat(v.x, v.y); }
+
 // ---- layouts -------------------------------------------------------------------
 
 // Byte offset of (row, byte) in a tile of P-byte rows (P = 64 or 128) in the

@@ -59,7 +59,19 @@ struct __align__(64) WsParams {
   float* partials;
   const float* cc[kN];  // core sweep, storage scheme: C-row cache (KView::cc)
   int exp;  // timing experiments (FTKCU_WS_EXP), never set in production
+  int window;  // ws_factor_kernel<true>: KView::window (0, 2 or 3)
 };
+
+// Timing-experiment bits: a compile-time 0 in the production build, so the
+// experiment branches (and the stand-in values some of them would need,
+// re-materialised every tile) vanish from the kernels.
+__device__ __forceinline__ int ws_exp(const WsParams& p) {
+#ifdef FTKCU_EXPERIMENTS
+  return p.exp;
+#else
+  return 0;
+#endif
+}
 
 // k3: the 3xtf32 factor sweep (ws_factor3_kernel): the C GEMM operand holds
 // [B^T hi ; B^T lo] instead of [B^T ; I], and the -lr reg I region holds the
@@ -177,7 +189,9 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
       // core, and factor with atomic rows: released by the MMA that last
       // reads the slot; factor overwrite mode: by the epilogue (reads a)
       // (3xtf32 factor: by the epilogue, whose fp32 step reads a)
-      mbar_init(&bars[B_EMPTY + s], (kCore || (p.atomic_update && !k3)) ? 1 : kEpiWarps);
+      // (window: by the epilogue once the tile's write-back is issued)
+      mbar_init(&bars[B_EMPTY + s],
+                (kCore || (p.atomic_update && !k3 && !p.window)) ? 1 : kEpiWarps);
     }
     for (int i = 0; i < L::kI; ++i) {
       mbar_init(&bars[B_IFULL + i], 1);
@@ -250,9 +264,13 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
   for (int64_t k = 0; k < nk; ++k) {
     const int s = (int)(k % kS), i = (int)(k % L::kI);
     mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
+    // window 2: tile k - 2 retired as well (its slot's completion (k - 2) / kS;
+    // the slot's next completion needs tile k + 1's gathers, so no aliasing)
+    if (!kCore && !k3 && p.window == 2 && k >= 2)
+      mbar_wait(&bars[B_EMPTY + (int)((k - 2) % kS)], (uint32_t)(((k - 2) / kS) & 1));
     mbar_wait(&bars[B_IFULL + i], (uint32_t)((k / L::kI) & 1));
     const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
-    if (p.exp & 2) {  // exp: no gathers (timing only)
+    if (ws_exp(p) & 2) {  // exp: no gathers (timing only)
       if (lane == 0) mbar_arrive(&bars[B_FULL + s]);
       continue;
     }
@@ -350,7 +368,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
                    sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
                    sdesc(bt + n * 8192 + ks * 32, 16, 1024, 128), idc, ks > 0);
         mma_commit(&bars[B_CFULL + b]);
-        if constexpr (kAtomic) mma_commit(&bars[B_EMPTY + s]);  // the only read of the A slot
+        // the only read of the A slot (window: held until the write-back)
+        if (kAtomic && !p.window) mma_commit(&bars[B_EMPTY + s]);
         if (k >= 1) issue_u(k - 1);
       }
       if (nk >= 1) issue_u(nk - 1);
@@ -431,12 +450,14 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
     };
     auto epi2 = [&](int64_t k, const Tile& t) {
-      // the row indices of the 8-row RED groups, shuffled before the wait
+      // the row indices of the 4-row RED groups, shuffled before the wait:
+      // this warp sends rows 16 h + 4 i + lane / 8 of its lane quarter
       int32_t gq[kN][4];
 #pragma unroll
       for (int n = 0; n < kN; ++n)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], i * 8 + (lane >> 2));
+        for (int i = 0; i < 4; ++i)
+          gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], h * 16 + i * 4 + (lane >> 3));
       mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
       tc_after();
       uint32_t u[kN][16];
@@ -448,11 +469,14 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
       if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
       const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
-      // Per mode: the warp writes its column half of its 32 step rows into a
-      // private 2 KB staging tile (64-B rows, 16-B chunks XOR (row/2) % 4:
-      // conflict-free both ways), then sends them as 64-B row segments, 8
-      // rows per RED (or STG) instruction -- no cross-warp barrier.
-      uint8_t* stage = sm + L::o_stage + ew * 2048;
+      // Per mode: the lane quarter's two warps write their column halves of
+      // the quarter's 32 step rows into a shared 4 KB staging tile (128-B
+      // rows, SWIZZLE_128B chunks: conflict-free both ways), then each sends
+      // 16 whole rows, 4 rows of 128 B per RED (or STG) instruction: half the
+      // L1 wavefronts / L2 requests of 64-B segments for the same bytes
+      // (scripts/microtests/red_segments.cu: 6.3 vs 5.3 TB/s).  Two 64-thread
+      // named barriers per mode (halves written / tile read).
+      uint8_t* stage = sm + L::o_stage + q * 4096;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
 #pragma unroll
@@ -469,26 +493,26 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
             st.z = a.z + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
             st.w = a.w + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
           }
-          *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
+          *reinterpret_cast<float4*>(stage + swz(lane, h * 64 + q4 * 16, 128)) = st;
         }
-        __syncwarp();
+        named_bar(5 + q, 64);  // both halves of the quarter's rows staged
         float* dst = p.a[n];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int rl = i * 8 + (lane >> 2), ch = lane & 3;
+          const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
           const int32_t g = gq[n][i];
-          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
-          if (g >= 0 && !(p.exp & 16)) {  // exp 16: no write-back (timing only)
-            float* gp = dst + (size_t)g * kW + h * 16 + ch * 4;
+          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
+          if (g >= 0 && !(ws_exp(p) & 16)) {  // exp 16: no write-back (timing only)
+            float* gp = dst + (size_t)g * kW + ch * 4;
             if constexpr (kAtomic)
               red_add_v4(gp, v);
             else
               *reinterpret_cast<float4*>(gp) = v;
           }
         }
-        __syncwarp();
+        named_bar(5 + q, 64);  // the sibling is done reading before the next mode's stores
       }
-      if constexpr (!kAtomic) {
+      if (!kAtomic || p.window) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);
       }
@@ -673,11 +697,12 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor3_kernel(const __grid_
       if (lane == 0) mbar_arrive(&bars[B_DFULL + b]);
     };
     auto epi2 = [&](int64_t k, const Tile& t) {
-      int32_t gq[kN][4];
+      int32_t gq[kN][4];  // rows 16 h + 4 i + lane / 8 of the quarter (as ws_factor_kernel)
 #pragma unroll
       for (int n = 0; n < kN; ++n)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], i * 8 + (lane >> 2));
+        for (int i = 0; i < 4; ++i)
+          gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], h * 16 + i * 4 + (lane >> 3));
       mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
       tc_after();
       uint32_t u[kN][16];
@@ -689,7 +714,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor3_kernel(const __grid_
       if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
       const float r = t.resid, lr = p.lr, reg = p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
-      uint8_t* stage = sm + L::o_stage + ew * 2048;
+      uint8_t* stage = sm + L::o_stage + q * 4096;  // the quarter's whole 128-B rows
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
 #pragma unroll
@@ -701,18 +726,18 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor3_kernel(const __grid_
           st.y = lr * (r * __uint_as_float(u[n][q4 * 4 + 1]) - reg * a.y);
           st.z = lr * (r * __uint_as_float(u[n][q4 * 4 + 2]) - reg * a.z);
           st.w = lr * (r * __uint_as_float(u[n][q4 * 4 + 3]) - reg * a.w);
-          *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = st;
+          *reinterpret_cast<float4*>(stage + swz(lane, h * 64 + q4 * 16, 128)) = st;
         }
-        __syncwarp();
+        named_bar(5 + q, 64);
         float* dst = p.a[n];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int rl = i * 8 + (lane >> 2), ch = lane & 3;
+          const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
           const int32_t g = gq[n][i];
-          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
-          if (g >= 0) red_add_v4(dst + (size_t)g * kW + h * 16 + ch * 4, v);
+          const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
+          if (g >= 0) red_add_v4(dst + (size_t)g * kW + ch * 4, v);
         }
-        __syncwarp();
+        named_bar(5 + q, 64);
       }
       if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);  // a read: the slot is free
     };
@@ -763,13 +788,13 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
         const uint64_t da = sdesc_l(a0, kModeTile, 512, 1);
         const uint64_t dd = sdesc_l(d0, kModeTile, 512, 1);
-        if (!(p.exp & 4))  // exp 4: no G GEMM (timing only)
+        if (!(ws_exp(p) & 4))  // exp 4: no G GEMM (timing only)
 #pragma unroll 4
           for (int ks = 0; ks < kRows / 8; ++ks)
             mma_ss(tmem + kG, da + (uint64_t)(ks * 64), dd + (uint64_t)(ks * 64), idg,
                    (k > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&bars[B_DEMPTY]);
-        if (!(p.exp & 1)) mma_commit(&bars[B_EMPTY + s]);
+        if (!(ws_exp(p) & 1)) mma_commit(&bars[B_EMPTY + s]);
       };
       for (int64_t k = 0; k < nk; ++k) {
         const int b = (int)(k & 1);
@@ -788,7 +813,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
             }
           }
         mma_commit(&bars[B_CFULL + b]);
-        if (p.exp & 1) mma_commit(&bars[B_EMPTY + (int)(k % kS)]);  // exp: slot freed after C
+        if (ws_exp(p) & 1) mma_commit(&bars[B_EMPTY + (int)(k % kS)]);  // exp: slot freed after C
         if (k >= 1) issue_g(k - 1);
       }
       if (nk >= 1) issue_g(nk - 1);
@@ -806,7 +831,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_kernel(const __grid_con
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
         uint32_t v[16];
-        if (p.exp & 8) {  // exp 8: no smem reads of the rows (timing only)
+        if (ws_exp(p) & 8) {  // exp 8: no smem reads of the rows (timing only)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0x3f800000u;
         } else
@@ -1158,7 +1183,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       mbar_wait(&bars[H_IFULL + i], (uint32_t)((k / L::kI) & 1));
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
       uint8_t* slot = sm + L::o_a + s * L::kSlot;
-      if (p.exp & 2) {  // exp 2: no gathers (timing only)
+      if (ws_exp(p) & 2) {  // exp 2: no gathers (timing only)
         if (lane == 0) {
           mbar_arrive(&bars[H_IEMPTY + i]);
           mbar_arrive(&bars[H_FULL + s]);
@@ -1195,7 +1220,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         // G[j'][n R + r] += sum_t A[t][j'] (r D_n)[t][r]: M = 3 stacked modes
         // (+ one garbage block), N = 96, K = 16 nonzeros per instruction
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot), dd = d0 + db * L::kSlot;
-        if (!(p.exp & 4))  // exp 4: no G GEMM (timing only)
+        if (!(ws_exp(p) & 4))  // exp 4: no G GEMM (timing only)
 #pragma unroll
           for (int ks = 0; ks < kRows / 16; ++ks)
             mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
@@ -1235,7 +1260,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       {  // the three modes' columns in flight before one wait
         uint32_t v[kN][16];
 #pragma unroll
-        if (!(p.exp & 128)) {  // exp 128: no TMEM loads (timing only)
+        if (!(ws_exp(p) & 128)) {  // exp 128: no TMEM loads (timing only)
           for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 96 + n * kW + h * 16, v[n]);
           tmem_wait_ld();
         } else {
@@ -1252,10 +1277,19 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[H_CEMPTY + b]);  // C(k + 2) may land
-      // x_hat halves exchanged with the sibling warp of this lane quarter
-      float part = 0.0f;
+      // column pairs in packed fp32 (FMUL2 / FFMA2): C_1 C_2 (shared by
+      // x_hat and D'_0), x_hat as an even / odd pair of partial sums
+      f2 c0[8], c1[8], c2[8], p12[8], acc = {0.0f, 0.0f};
 #pragma unroll
-      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
+      for (int i = 0; i < 8; ++i) {
+        c0[i] = f2{c[0][2 * i], c[0][2 * i + 1]};
+        c1[i] = f2{c[1][2 * i], c[1][2 * i + 1]};
+        c2[i] = f2{c[2][2 * i], c[2][2 * i + 1]};
+        p12[i] = mul2(c1[i], c2[i]);
+        acc = fma2(c0[i], p12[i], acc);
+      }
+      // x_hat halves exchanged with the sibling warp of this lane quarter
+      const float part = acc.x + acc.y;
       float* xp = reinterpret_cast<float*>(sm + L::o_xp);
       xp[(b * 2 + h) * kRows + row] = part;
       named_bar(1 + q + 4 * eg, 64);
@@ -1266,15 +1300,17 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       if (lane == 0) mbar_arrive(&bars[H_IEMPTY + ii]);
       mbar_wait(&bars[H_DEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));  // G(k - 2) done with D[b]
       uint8_t* dt = sm + L::o_d + b * L::kSlot;
-      if (p.exp & 32) {  // exp 32: no r D tile (timing only)
+      if (ws_exp(p) & 32) {  // exp 32: no r D tile (timing only)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[H_DFULL + b]);
         continue;
       }
-      // r D'_n: r (C_1 C_2), (r C_0) C_2, (r C_0) C_1 -- five products per column
-      float rc0[16];
+      // r D'_n: r (C_1 C_2), (r C_0) C_2, (r C_0) C_1 -- four packed products
+      // per column pair after x_hat's two
+      const f2 rr = {resid, resid};
+      f2 rc0[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) rc0[i] = resid * c[0][i];
+      for (int i = 0; i < 8; ++i) rc0[i] = mul2(rr, c0[i]);
 #pragma unroll
       for (int n = 0; n < kN; ++n)
 #pragma unroll
@@ -1282,10 +1318,9 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int i0 = q2 * 8 + e * 2;
-#define FTK_D(ii) (n == 0 ? resid * (c[1][ii] * c[2][ii]) : (n == 1 ? rc0[ii] * c[2][ii] : rc0[ii] * c[1][ii]))
-            w[e] = f16x2_sat(FTK_D(i0), FTK_D(i0 + 1));
-#undef FTK_D
+            const int i = q2 * 4 + e;
+            w[e] = f16x2_sat(n == 0 ? mul2(rr, p12[i])
+                                    : (n == 1 ? mul2(rc0[i], c2[i]) : mul2(rc0[i], c1[i])));
           }
           *reinterpret_cast<uint4*>(dt + n * kModeTile16 + swz(row, (h * 16 + q2 * 8) * 2, 64)) =
               make_uint4(w[0], w[1], w[2], w[3]);
@@ -1312,18 +1347,18 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
 //
 // The factor sweep's write-back alone, for the roofline that binds at
 // L2-resident shapes: same tile stream, thread -> (row, column half) map,
-// 2 KB per-warp staging tiles and 8-row RED.v4 groups as epi2 of
+// per-quarter 4 KB staging tiles and 4-row x 128-B RED.v4 groups as epi2 of
 // ws_factor_kernel<true> -- no gathers, no MMA, no TMEM -- at full occupancy
 // (8 CTAs per SM, so index-load latency is hidden), adding 1.0f to
 // every element of each nonzero's three rows of `dst` (a scratch copy of the
 // factor shapes).  Its time is the floor the full sweep's RED stream sets.
 __global__ void __launch_bounds__(kEpiWarps * 32, 8)
     ws_writeback_kernel(const __grid_constant__ WsParams p, float* const* dst) {
-  __shared__ __align__(16) uint8_t stage_all[kEpiWarps * 2048];
+  __shared__ __align__(1024) uint8_t stage_all[4 * 4096];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = (warp + 2) & 3, h = warp >> 2;  // the epilogue warps' map (warp 2 + w)
   const int row = q * 32 + lane;
-  uint8_t* stage = stage_all + warp * 2048;
+  uint8_t* stage = stage_all + q * 4096;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   for (int64_t k = 0; k < nk; ++k) {
     const int64_t tile = ws_tile(p, k);
@@ -1335,21 +1370,23 @@ __global__ void __launch_bounds__(kEpiWarps * 32, 8)
 #pragma unroll
     for (int n = 0; n < kN; ++n)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) gq[n][i] = __shfl_sync(0xffffffffu, g[n], i * 8 + (lane >> 2));
+      for (int i = 0; i < 4; ++i)
+        gq[n][i] = __shfl_sync(0xffffffffu, g[n], h * 16 + i * 4 + (lane >> 3));
 #pragma unroll
     for (int n = 0; n < kN; ++n) {
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
-        *reinterpret_cast<float4*>(stage + swz(lane, q4 * 16, 64)) = make_float4(1.f, 1.f, 1.f, 1.f);
-      __syncwarp();
+        *reinterpret_cast<float4*>(stage + swz(lane, h * 64 + q4 * 16, 128)) =
+            make_float4(1.f, 1.f, 1.f, 1.f);
+      named_bar(1 + q, 64);
       float* d = dst[n];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int rl = i * 8 + (lane >> 2), ch = lane & 3;
-        const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 64));
-        if (gq[n][i] >= 0) red_add_v4(d + (size_t)gq[n][i] * kW + h * 16 + ch * 4, v);
+        const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
+        const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
+        if (gq[n][i] >= 0) red_add_v4(d + (size_t)gq[n][i] * kW + ch * 4, v);
       }
-      __syncwarp();
+      named_bar(1 + q, 64);
     }
   }
 }
@@ -1463,6 +1500,7 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   p.exp = ws_exp_bits();
   if (p.ntiles == 0) return cudaSuccess;
   const bool k3 = p.prec3 && atomic_update;
+  p.window = (atomic_update && !k3) ? v.window : 0;
   const int bytes = (int)(k3 ? WsLayout<false, true>::bytes : WsLayout<false>::bytes);
   auto kern = k3 ? ws_factor3_kernel
                  : (atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>);
