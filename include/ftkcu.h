@@ -264,6 +264,47 @@ int ftkcu_comm_bcast_rows(ftkcu_session* s, int mode, const int64_t* row_off,
 int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t* row_off2,
                             const int64_t* row_off3, const uint64_t* cell_seeds, float lr_a,
                             float reg_a, double* ms);
+/* DSGD ring epochs (dsgd.py ring schedule; no reference counterpart: the
+ * reference is single-host).  Mode 3 is cut into 2*parts blocks that
+ * circulate as tokens (rank g starts an epoch holding blocks 2g, 2g+1 and
+ * mode-2 block g); cell s*2*parts+i of rank g holds its nonzeros of mode-2
+ * block (g+s)%parts and mode-3 block (2g+i)%(2*parts).  One persistent
+ * factor sweep (ws_factor_kernel) walks all cells: after the last CTA
+ * finishes a cell it copies the cell's mode-3 block (and at a round's end
+ * the mode-2 block) into the left neighbour's (rank g-1) factor matrices
+ * over peer memory and raises the neighbour's arrival flag; a cell's gathers
+ * wait only for its own flags.  No stratum barrier, no host sync.
+ *
+ * ftkcu_ring_export writes this session's peer descriptor (factor matrices
+ * and flag array: device pointers + CUDA IPC handles) into blob
+ * (FTKCU_RING_BLOB_BYTES); ftkcu_ring_connect maps the LEFT neighbour's
+ * (same process: its pointers; another process: cudaIpcOpenMemHandle) and
+ * clears this rank's flags -- every rank connects before any ring epoch.
+ * ftkcu_ring_emulate instead points the posts at local scratch and skips the
+ * waits (one GPU timing one rank's share).  Both take the training slot
+ * (uploaded, cells set) and allocate everything an epoch uses, so no
+ * allocation falls between two ranks' launches; model and tensor must stay
+ * as uploaded between connect and the epochs.  N = 3, J = R = 32, tf32. */
+#define FTKCU_RING_BLOB_BYTES 512
+int ftkcu_ring_export(ftkcu_session* s, uint8_t* blob, int cap);
+int ftkcu_ring_connect(ftkcu_session* s, int slot, const uint8_t* left_blob, int len);
+int ftkcu_ring_emulate(ftkcu_session* s, int slot);
+/* One ring factor phase of rank `rank` over `parts` ranks: row_off2 has
+ * parts+1 offsets, row_off3 2*parts+1, cell_seeds 2*parts*parts tile
+ * permutation seeds.  With a communicator of size parts the epoch ends with
+ * the all-gather of the mode-2/3 blocks (as ftkcu_dsgd_factor_epoch). */
+int ftkcu_ring_factor_epoch(ftkcu_session* s, int slot, int parts, int rank,
+                            const int64_t* row_off2, const int64_t* row_off3,
+                            const uint64_t* cell_seeds, float lr_a, float reg_a, double* ms);
+/* Synchronises the session stream; *timed_out != 0 if a ring wait gave up
+ * (a neighbour never posted: the epoch's result is invalid): 0x10000 | the
+ * flag id of the first block wait that gave up, 0x20000 | the round of a
+ * round-end copy that did.  Option "ring_timeout_ms" sets the limit. */
+int ftkcu_ring_status(ftkcu_session* s, int* timed_out);
+/* Test introspection: the first n arrival flags and cell counters
+ * (flag ids: mode-3 block x in round r = r*2P + x; mode-2 block y in round
+ * r = (P+1)*2P + r*P + y; rounds 0..P). */
+int ftkcu_ring_debug(ftkcu_session* s, uint32_t* flags, uint32_t* done, int n);
 /* Sum all-reduce of host fp64 values (metrics partials). */
 int ftkcu_comm_allreduce_f64(ftkcu_session* s, double* host_inout, int n);
 /* Waits for all work queued on the session stream. */

@@ -45,6 +45,8 @@ EXPORTS = (
     "ftkcu_stream_sync", "ftkcu_dsgd_factor_epoch", "ftkcu_fasttucker_factor",
     "ftkcu_fasttucker_core", "ftkcu_ccache_upload", "ftkcu_ccache_download",
     "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core", "ftkcu_writeback_ceiling",
+    "ftkcu_ring_export", "ftkcu_ring_connect", "ftkcu_ring_emulate", "ftkcu_ring_factor_epoch",
+    "ftkcu_ring_status", "ftkcu_ring_debug",
 )
 
 
@@ -116,6 +118,14 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_writeback_ceiling.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _f64p]
     L.ftkcu_dsgd_factor_epoch.argtypes = [C.c_void_p, C.c_int, C.c_int, _i64p, _i64p,
                                           C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
+    L.ftkcu_ring_export.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+    L.ftkcu_ring_connect.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int]
+    L.ftkcu_ring_emulate.argtypes = [C.c_void_p, C.c_int]
+    L.ftkcu_ring_factor_epoch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _i64p, _i64p,
+                                          C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
+    L.ftkcu_ring_status.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+    L.ftkcu_ring_debug.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                   C.c_int]
     _lib = L
     return L
 
@@ -364,6 +374,51 @@ class Session:
             self.h, slot, parts, _p(o2, _i64p), _p(o3, _i64p), _p(sd, C.POINTER(C.c_uint64)),
             lr_a, reg_a, C.byref(ms) if timed else None))
         return ms.value
+
+    # -- DSGD ring epochs (token-passing mode-3 blocks; dsgd.RingTrainer)
+    RING_BLOB_BYTES = 512
+
+    def ring_export(self) -> bytes:
+        """This session's peer descriptor (factor matrices + arrival flags)."""
+        buf = C.create_string_buffer(self.RING_BLOB_BYTES)
+        self._ck(self.lib.ftkcu_ring_export(self.h, buf, self.RING_BLOB_BYTES))
+        return buf.raw
+
+    def ring_connect(self, slot, left_blob: bytes):
+        """Maps the left neighbour's (rank - 1) descriptor, clears this rank's
+        flags and prepares `slot` (uploaded, cells set) for ring epochs."""
+        self._ck(self.lib.ftkcu_ring_connect(self.h, slot, left_blob, len(left_blob)))
+
+    def ring_emulate(self, slot):
+        """No peers: posts go to local scratch and waits are skipped (timing)."""
+        self._ck(self.lib.ftkcu_ring_emulate(self.h, slot))
+
+    def ring_factor_epoch(self, slot, parts, rank, row_off2, row_off3, cell_seeds, lr_a=1e-3,
+                          reg_a=1e-4, timed=False):
+        o2 = np.ascontiguousarray(row_off2, np.int64)
+        o3 = np.ascontiguousarray(row_off3, np.int64)
+        sd = np.ascontiguousarray(np.asarray(cell_seeds, np.uint64))
+        ms = C.c_double(0.0)
+        self._ck(self.lib.ftkcu_ring_factor_epoch(
+            self.h, slot, parts, rank, _p(o2, _i64p), _p(o3, _i64p),
+            _p(sd, C.POINTER(C.c_uint64)), lr_a, reg_a, C.byref(ms) if timed else None))
+        return ms.value
+
+    def ring_status(self) -> int:
+        """Synchronises; nonzero if a ring wait timed out (the epoch is
+        invalid): 0x10000 | flag id of the first stuck block wait, or
+        0x20000 | round of a stuck round-end copy."""
+        v = C.c_int(0)
+        self._ck(self.lib.ftkcu_ring_status(self.h, C.byref(v)))
+        return int(v.value)
+
+    def ring_debug(self, n):
+        """(arrival flags, cell counters), first n entries each (tests)."""
+        f = np.zeros(n, np.uint32)
+        d = np.zeros(n, np.uint32)
+        self._ck(self.lib.ftkcu_ring_debug(self.h, f.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                           d.ctypes.data_as(C.POINTER(C.c_uint32)), n))
+        return f, d
 
     def sync(self):
         self._ck(self.lib.ftkcu_stream_sync(self.h))

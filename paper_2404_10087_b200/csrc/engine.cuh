@@ -244,6 +244,35 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
                            float* grad, int precision, int core16, float* scratch,
                            size_t scratch_bytes, cudaStream_t st);
 
+// DSGD ring epoch (dsgd.py, ring schedule): one persistent factor sweep over
+// all of this rank's cells in order.  Mode-3 blocks circulate as tokens (2P
+// blocks, each rank holds two): the epilogue warp that completes a cell's
+// count copies the cell's mode-3 block into the left neighbour's factor
+// matrices and raises the neighbour's arrival flag; at a round's end every
+// CTA copies a slice of the round's mode-2 block the same way.  A cell's
+// gathers start once its own arrival flags carry this epoch.
+struct RingDev {
+  int ncell = 0;             // 0: not a ring epoch
+  int parts = 0;             // P (cells per round: 2P)
+  int emulate = 0;           // no peers: posts go to local scratch, no waits
+  unsigned epoch = 0;        // flag generation of this epoch (>= 1)
+  const int64_t* cell_tile = nullptr;  // [ncell + 1] physical tile offsets
+  const int64_t* cell_perm = nullptr;  // [ncell][2] affine tile permutation
+  const int4* cell_io = nullptr;       // [ncell] {wait flag, wait flag, post, post}, -1 = none
+  const int4* posts = nullptr;         // {mode, row0, nrows, peer flag}
+  const int* final_waits = nullptr;    // flags CTA 0 waits for before it exits
+  int nfinal = 0;
+  unsigned* done = nullptr;            // [ncell] warp completion counts (zeroed per epoch)
+  unsigned* copied = nullptr;          // [P] round-end mode-2 copy counts (zeroed per epoch)
+  unsigned* flags = nullptr;           // this rank's arrival flags
+  unsigned* peer_flags = nullptr;      // the left neighbour's
+  float* peer_a[kMaxOrder] = {};       // the left neighbour's factor matrices
+  unsigned* err = nullptr;             // the first wait that timed out (0: none)
+  long long timeout_cycles = 4ll << 30;  // ~2 s
+};
+cudaError_t launch_ws_factor_ring(const KView& v, const int32_t* dims, const RingDev& ring,
+                                  float lr, float reg, cudaStream_t st);
+
 // Measurement: the headline factor sweep's RED write-back alone (roofline
 // ceiling at L2-resident shapes); dst_dev: device array of order pointers.
 cudaError_t launch_ws_writeback(const KView& v, const int32_t* dims, int64_t mul, int64_t add,

@@ -45,6 +45,7 @@ struct ftkcu_session {
   int rank = 0, world = 1;
   int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
   int64_t opt_max_ctas = 0;  // sweep grid cap (0 = one CTA per SM)
+  int64_t opt_ring_timeout_ms = 0;  // ring waits give up after this (0: ~2 s)
   int64_t opt_window = 0;  // headline factor sweep read-to-write window in tiles (0 = ring depth)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
@@ -60,6 +61,21 @@ struct ftkcu_session {
   cudaGraphExec_t dsgd_exec = nullptr;
   std::vector<int64_t> dsgd_key;
   int64_t dsgd_launches = 0;
+  // DSGD ring (ftkcu_ring_*): arrival flags, cell counters, the left
+  // neighbour's buffers (or local scratch when emulating), per-epoch tables
+  unsigned* ring_flags = nullptr;  // [kRingFlags]
+  unsigned* ring_done = nullptr;   // [kRingFlags] cell counters, then [kRingFlags] copy counts
+  unsigned* ring_err = nullptr;
+  float* ring_peer_a[3] = {};
+  unsigned* ring_peer_flags = nullptr;
+  void* ring_ipc[4] = {};          // peers opened through CUDA IPC (closed on destroy)
+  float* ring_emu_a[3] = {};
+  unsigned* ring_emu_flags = nullptr;
+  bool ring_ready = false, ring_emulate = false;
+  float* ring_model_a[3] = {};     // factor matrices when connected (must not move)
+  unsigned ring_epoch = 0;
+  uint8_t* ring_tab = nullptr;     // device tables of the current epoch (kRingTabBytes)
+  uint8_t* ring_tab_h = nullptr;   // pinned staging of the tables
   int64_t launches = 0;  // kernels launched by this session (for benches)
   // Which sweep kernel the last factor / core phase ran (FTKCU_K_*), so that
   // tests can assert the dispatch they mean to cover.
@@ -373,6 +389,16 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   if (s->d_boff) cudaFree(s->d_boff);
   if (s->d_cellperm) cudaFree(s->d_cellperm);
   if (s->dsgd_exec) cudaGraphExecDestroy(s->dsgd_exec);
+  for (void* p : s->ring_ipc)
+    if (p) cudaIpcCloseMemHandle(p);
+  for (float* p : s->ring_emu_a)
+    if (p) cudaFree(p);
+  if (s->ring_emu_flags) cudaFree(s->ring_emu_flags);
+  if (s->ring_flags) cudaFree(s->ring_flags);
+  if (s->ring_done) cudaFree(s->ring_done);
+  if (s->ring_err) cudaFree(s->ring_err);
+  if (s->ring_tab) cudaFree(s->ring_tab);
+  if (s->ring_tab_h) cudaFreeHost(s->ring_tab_h);
   if (s->comm) ncclCommDestroy(s->comm);
   cudaEventDestroy(s->ev0);
   cudaEventDestroy(s->ev1);
@@ -422,6 +448,9 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "max_ctas") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "max_ctas must be >= 0");
     s->opt_max_ctas = value;
+  } else if (k == "ring_timeout_ms") {
+    if (value < 0) return fail(s, FTKCU_ERR_ARG, "ring_timeout_ms must be >= 0");
+    s->opt_ring_timeout_ms = value;
   } else if (k == "window") {
     if (value != 0 && value != 2 && value != 3)
       return fail(s, FTKCU_ERR_ARG, "window must be 0, 2 or 3");
@@ -1418,3 +1447,280 @@ int ftkcu_comm_allreduce_grad(ftkcu_session* s) {
 }
 
 }  // extern "C"
+
+// ---- DSGD ring epochs ----------------------------------------------------------
+
+namespace {
+constexpr int kRingFlags = 4096;
+// one epoch's tables at the largest ring (kRingFlags cells): tile offsets,
+// permutations, cell io, posts (<= 2 per cell), final waits
+constexpr size_t kRingTabBytes = 8 * (kRingFlags + 1) + 16 * kRingFlags + 16 * kRingFlags +
+                                 32 * kRingFlags + 64;
+constexpr uint32_t kRingMagic = 0x52494e47u;  // "RING"
+struct RingBlob {
+  uint32_t magic;
+  int32_t pid;
+  int32_t device;
+  int32_t pad;
+  uint64_t a[3];
+  uint64_t flags;
+  cudaIpcMemHandle_t ha[3];
+  cudaIpcMemHandle_t hf;
+};
+static_assert(sizeof(RingBlob) <= FTKCU_RING_BLOB_BYTES, "ring blob size");
+}  // namespace
+
+#include <unistd.h>
+
+// Everything a ring epoch touches is allocated here, before any rank's
+// kernel runs: a device allocation between two ranks' launches would
+// serialise virtual ranks sharing one GPU (implicit synchronisation) and
+// deadlock their flag waits.
+static int ring_buffers(ftkcu_session* s) {
+  if (!s->ring_tab) {
+    CK(cudaMalloc(&s->ring_tab, kRingTabBytes));
+    CK(cudaMallocHost(&s->ring_tab_h, kRingTabBytes));
+  }
+  if (!s->ring_flags) {
+    CK(cudaMalloc(&s->ring_flags, sizeof(unsigned) * kRingFlags));
+    CK(cudaMalloc(&s->ring_done, sizeof(unsigned) * 2 * kRingFlags));
+    CK(cudaMalloc(&s->ring_err, sizeof(unsigned)));
+    CK(cudaMemset(s->ring_flags, 0, sizeof(unsigned) * kRingFlags));
+    CK(cudaMemset(s->ring_done, 0, sizeof(unsigned) * 2 * kRingFlags));
+    CK(cudaMemset(s->ring_err, 0, sizeof(unsigned)));
+  }
+  return FTKCU_OK;
+}
+
+static int ring_model_ok(ftkcu_session* s) {
+  if (!s->have_model || s->model.order != 3)
+    return fail(s, FTKCU_ERR_STATE, "ring epochs need an uploaded order-3 model");
+  return FTKCU_OK;
+}
+
+int ftkcu_ring_export(ftkcu_session* s, uint8_t* blob, int cap) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!blob || cap < (int)sizeof(RingBlob)) return fail(s, FTKCU_ERR_ARG, "blob too small");
+  if ((rc = ring_model_ok(s)) || (rc = ring_buffers(s))) return rc;
+  RingBlob b{};
+  b.magic = kRingMagic;
+  b.pid = (int32_t)getpid();
+  b.device = s->device;
+  for (int n = 0; n < 3; ++n) {
+    b.a[n] = (uint64_t)(uintptr_t)s->model.a[n];
+    CK(cudaIpcGetMemHandle(&b.ha[n], s->model.a[n]));
+  }
+  b.flags = (uint64_t)(uintptr_t)s->ring_flags;
+  CK(cudaIpcGetMemHandle(&b.hf, s->ring_flags));
+  std::memset(blob, 0, cap);
+  std::memcpy(blob, &b, sizeof(b));
+  return FTKCU_OK;
+}
+
+// The slot's Hogwild tile stream is built here too (its first build allocates).
+static int ring_prepare(ftkcu_session* s, int slot) {
+  int rc;
+  if ((rc = check_ready(s, slot)) || (rc = ring_model_ok(s)) || (rc = ring_buffers(s))) return rc;
+  return prepare_stream(s, s->slots[slot], nullptr);
+}
+
+int ftkcu_ring_connect(ftkcu_session* s, int slot, const uint8_t* left_blob, int len) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!left_blob || len < (int)sizeof(RingBlob)) return fail(s, FTKCU_ERR_ARG, "bad ring blob");
+  if ((rc = ring_prepare(s, slot))) return rc;
+  RingBlob b;
+  std::memcpy(&b, left_blob, sizeof(b));
+  if (b.magic != kRingMagic) return fail(s, FTKCU_ERR_ARG, "not a ring blob");
+  for (void*& p : s->ring_ipc)
+    if (p) {
+      CK(cudaIpcCloseMemHandle(p));
+      p = nullptr;
+    }
+  if (b.pid == (int32_t)getpid()) {  // same process (virtual ranks): plain pointers
+    for (int n = 0; n < 3; ++n) s->ring_peer_a[n] = (float*)(uintptr_t)b.a[n];
+    s->ring_peer_flags = (unsigned*)(uintptr_t)b.flags;
+  } else {
+    for (int n = 0; n < 3; ++n) {
+      CK(cudaIpcOpenMemHandle(&s->ring_ipc[n], b.ha[n], cudaIpcMemLazyEnablePeerAccess));
+      s->ring_peer_a[n] = static_cast<float*>(s->ring_ipc[n]);
+    }
+    CK(cudaIpcOpenMemHandle(&s->ring_ipc[3], b.hf, cudaIpcMemLazyEnablePeerAccess));
+    s->ring_peer_flags = static_cast<unsigned*>(s->ring_ipc[3]);
+  }
+  CK(cudaMemsetAsync(s->ring_flags, 0, sizeof(unsigned) * kRingFlags, s->stream));
+  CK(cudaMemsetAsync(s->ring_err, 0, sizeof(unsigned), s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  for (int n = 0; n < 3; ++n) s->ring_model_a[n] = s->model.a[n];
+  s->ring_epoch = 0;
+  s->ring_emulate = false;
+  s->ring_ready = true;
+  return FTKCU_OK;
+}
+
+int ftkcu_ring_emulate(ftkcu_session* s, int slot) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = ring_prepare(s, slot))) return rc;
+  for (int n = 0; n < 3; ++n) {
+    if (s->ring_emu_a[n]) CK(cudaFree(s->ring_emu_a[n]));
+    CK(cudaMalloc(&s->ring_emu_a[n], sizeof(float) * (size_t)s->model.dims[n] * s->model.ranks[n]));
+    s->ring_peer_a[n] = s->ring_emu_a[n];
+  }
+  if (!s->ring_emu_flags) CK(cudaMalloc(&s->ring_emu_flags, sizeof(unsigned) * kRingFlags));
+  CK(cudaMemset(s->ring_emu_flags, 0, sizeof(unsigned) * kRingFlags));
+  CK(cudaStreamSynchronize(s->stream));
+  s->ring_peer_flags = s->ring_emu_flags;
+  for (int n = 0; n < 3; ++n) s->ring_model_a[n] = s->model.a[n];
+  s->ring_epoch = 0;
+  s->ring_emulate = true;
+  s->ring_ready = true;
+  return FTKCU_OK;
+}
+
+int ftkcu_ring_status(ftkcu_session* s, int* timed_out) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!timed_out) return fail(s, FTKCU_ERR_ARG, "null argument");
+  *timed_out = 0;
+  unsigned* e = nullptr;
+  if (s->ring_err && s->ring_tab_h) {
+    e = reinterpret_cast<unsigned*>(s->ring_tab_h + kRingTabBytes - 16);
+    CK(cudaMemcpyAsync(e, s->ring_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
+  }
+  // poll with a sleep instead of a spinning synchronise: ranks sharing one
+  // host (virtual ranks, or few cores) must not starve a rank whose kernel
+  // the others are waiting for of the CPU it needs to launch
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) CK(q);
+    usleep(50);
+  }
+  if (e) *timed_out = (int)*e;
+  return FTKCU_OK;
+}
+
+int ftkcu_ring_debug(ftkcu_session* s, uint32_t* flags, uint32_t* done, int n) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->ring_flags || n < 0 || n > kRingFlags) return fail(s, FTKCU_ERR_ARG, "no ring state");
+  CK(cudaStreamSynchronize(s->stream));
+  if (flags) CK(cudaMemcpy(flags, s->ring_flags, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+  if (done) CK(cudaMemcpy(done, s->ring_done, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+  return FTKCU_OK;
+}
+
+int ftkcu_ring_factor_epoch(ftkcu_session* s, int slot, int parts, int rank,
+                            const int64_t* row_off2, const int64_t* row_off3,
+                            const uint64_t* cell_seeds, float lr_a, float reg_a, double* ms) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if ((rc = check_ready(s, slot))) return rc;
+  if (!s->ring_ready) return fail(s, FTKCU_ERR_STATE, "ring not connected (ftkcu_ring_connect / _emulate)");
+  for (int n = 0; n < 3; ++n)
+    if (s->model.a[n] != s->ring_model_a[n])
+      return fail(s, FTKCU_ERR_STATE, "model reallocated since the ring was connected");
+  DevTensor& t = s->slots[slot];
+  const int P = parts;
+  if (P < 2 || rank < 0 || rank >= P || !row_off2 || !row_off3 || !cell_seeds)
+    return fail(s, FTKCU_ERR_ARG, "bad ring arguments (parts >= 2, 0 <= rank < parts)");
+  // tokens K = mode-3 blocks per rank: the tensor has P * (K P) cells
+  const int ncell = (int)t.cell_off.size() - 1, K = ncell / (P * P), Q = K * P;
+  if (K < 1 || K > 4 || ncell != P * Q)
+    return fail(s, FTKCU_ERR_ARG, "tensor has %d cells, a ring over %d parts needs K*%d (K = 1..4)",
+                ncell, P, P * P);
+  if ((P + 1) * (Q + P) > kRingFlags || ncell > kRingFlags)
+    return fail(s, FTKCU_ERR_ARG, "too many ring parts");
+  if (s->world > 1 && (P != s->world || rank != s->rank))
+    return fail(s, FTKCU_ERR_ARG, "parts/rank disagree with the communicator");
+  const int64_t* offs[2] = {row_off2, row_off3};
+  const int nb[2] = {P, Q};
+  for (int m = 0; m < 2; ++m) {
+    if (offs[m][0] != 0 || offs[m][nb[m]] != s->model.dims[m + 1])
+      return fail(s, FTKCU_ERR_ARG, "mode-%d block offsets must span [0, %d]", m + 2,
+                  s->model.dims[m + 1]);
+    for (int p = 0; p < nb[m]; ++p)
+      if (offs[m][p + 1] < offs[m][p]) return fail(s, FTKCU_ERR_ARG, "block offsets not sorted");
+  }
+  if (s->opt_precision != FTKCU_PREC_TF32 || !s->opt_hog_update)
+    return fail(s, FTKCU_ERR_ARG, "ring epochs run the tf32 accumulate sweep");
+  if (!t.shuffled) return fail(s, FTKCU_ERR_STATE, "tensor changed since the ring was connected");
+  KView v = make_view(s, t, true);
+  v.max_ctas = (int)s->opt_max_ctas;
+  if (!ws_supported(v)) return fail(s, FTKCU_ERR_ARG, "ring epochs need N = 3, J = R = 32");
+  // tables: flag ids F3(round, block) / F2(round, block), rounds 0..P
+  auto F3 = [&](int r, int x) { return r * Q + x; };
+  auto F2 = [&](int r, int y) { return (P + 1) * Q + r * P + y; };
+  std::vector<int64_t> perm(2 * (size_t)ncell);
+  std::vector<int4> io(ncell), posts;
+  for (int c = 0; c < ncell; ++c)
+    tile_perm(cell_seeds[c], t.cell_tile[c + 1] - t.cell_tile[c], &perm[2 * c], &perm[2 * c + 1]);
+  const int g = rank;
+  for (int sr = 0; sr < P; ++sr)
+    for (int i = 0; i < Q; ++i) {
+      const int c = sr * Q + i, x = (K * g + i) % Q, y = (g + sr) % P;
+      int4 e = make_int4(-1, -1, -1, -1);
+      if (sr > 0 || i >= K) e.x = F3(sr, x);  // blocks Kg .. Kg+K-1 are held at the start
+      if (i == 0 && sr > 0) e.y = F2(sr, y);
+      // the mode-3 block goes to rank g-1, which sweeps it K steps later
+      e.z = (int)posts.size();
+      posts.push_back(make_int4(2, (int)row_off3[x], (int)(row_off3[x + 1] - row_off3[x]),
+                                F3(sr + (i + K >= Q ? 1 : 0), x)));
+      if (i == Q - 1) {  // round end: the mode-2 block follows for round sr+1
+        e.w = (int)posts.size();
+        posts.push_back(make_int4(1, (int)row_off2[y], (int)(row_off2[y + 1] - row_off2[y]),
+                                  F2(sr + 1, y)));
+      }
+      io[c] = e;
+    }
+  int finals[5] = {F2(P, g), -1, -1, -1, -1};
+  for (int q = 0; q < K; ++q) finals[1 + q] = F3(P, (K * g + q) % Q);
+  const size_t b_tile = sizeof(int64_t) * (ncell + 1), b_perm = sizeof(int64_t) * perm.size();
+  const size_t b_io = sizeof(int4) * ncell, b_post = sizeof(int4) * posts.size();
+  const size_t o_perm = (b_tile + 15) / 16 * 16, o_io = o_perm + (b_perm + 15) / 16 * 16;
+  const size_t o_post = o_io + b_io, o_fin = o_post + b_post, total = o_fin + sizeof(finals);
+  if (total + 16 > kRingTabBytes) return fail(s, FTKCU_ERR_ARG, "ring tables too large");
+  // the pinned staging is reused: the previous epoch's copy must have run
+  CK(cudaStreamSynchronize(s->stream));
+  uint8_t* h = s->ring_tab_h;
+  std::memcpy(h, t.cell_tile.data(), b_tile);
+  std::memcpy(h + o_perm, perm.data(), b_perm);
+  std::memcpy(h + o_io, io.data(), b_io);
+  std::memcpy(h + o_post, posts.data(), b_post);
+  std::memcpy(h + o_fin, finals, sizeof(finals));
+  CK(cudaEventRecord(s->ev0, s->stream));
+  CK(cudaMemcpyAsync(s->ring_tab, h, total, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemsetAsync(s->ring_done, 0, sizeof(unsigned) * ncell, s->stream));
+  CK(cudaMemsetAsync(s->ring_done + kRingFlags, 0, sizeof(unsigned) * P, s->stream));
+  CK(cudaMemsetAsync(s->ring_err, 0, sizeof(unsigned), s->stream));
+  RingDev r;
+  r.ncell = ncell;
+  r.parts = P;
+  r.copied = s->ring_done + kRingFlags;
+  r.emulate = s->ring_emulate ? 1 : 0;
+  r.epoch = ++s->ring_epoch;
+  r.cell_tile = reinterpret_cast<const int64_t*>(s->ring_tab);
+  r.cell_perm = reinterpret_cast<const int64_t*>(s->ring_tab + o_perm);
+  r.cell_io = reinterpret_cast<const int4*>(s->ring_tab + o_io);
+  r.posts = reinterpret_cast<const int4*>(s->ring_tab + o_post);
+  r.final_waits = reinterpret_cast<const int*>(s->ring_tab + o_fin);
+  r.nfinal = 1 + K;
+  r.done = s->ring_done;
+  r.flags = s->ring_flags;
+  r.peer_flags = s->ring_peer_flags;
+  for (int n = 0; n < 3; ++n) r.peer_a[n] = s->ring_peer_a[n];
+  r.err = s->ring_err;
+  if (s->opt_ring_timeout_ms > 0) r.timeout_cycles = (long long)s->opt_ring_timeout_ms * 2000000ll;
+  CK(launch_ws_factor_ring(v, s->model.dims, r, lr_a, reg_a, s->stream));
+  s->launches += 1;
+  s->last_factor_kernel = FTKCU_K_WS;
+  if (s->world > 1 && s->comm) {
+    std::vector<int64_t> held3(P + 1);
+    for (int p = 0; p <= P; ++p) held3[p] = row_off3[K * p];
+    if ((rc = bcast_blocks(s, 1, row_off2))) return rc;
+    if ((rc = bcast_blocks(s, 2, held3.data()))) return rc;
+  }
+  return finish_timing(s, ms);
+}

@@ -42,6 +42,9 @@ constexpr int kEpiWarps = 8;
 // warps (one elected lane each) -- a single issuing thread serialises them.
 constexpr int kGW = 2;
 constexpr int kThreadsWs = (2 + kEpiWarps + kGW) * 32;
+// ring epochs: one more warp, the round-end mode-2 block copier (ring_agent)
+constexpr int kRingWarp = 2 + kEpiWarps + kGW;
+constexpr int kThreadsRing = kThreadsWs + 32;
 constexpr int kGatherWarp = 2 + kEpiWarps;  // first of the kGW gather warps
 constexpr uint32_t kModeTile = kRows * 128;  // 128 rows x 32 fp32 = 16 KB
 
@@ -60,6 +63,7 @@ struct __align__(64) WsParams {
   const float* cc[kN];  // core sweep, storage scheme: C-row cache (KView::cc)
   int exp;  // timing experiments (FTKCU_WS_EXP), never set in production
   int window;  // ws_factor_kernel<true>: KView::window (0, 2 or 3)
+  RingDev ring;  // ws_factor_kernel<true>: DSGD ring epoch (ring.ncell > 0)
 };
 
 // Timing-experiment bits: a compile-time 0 in the production build, so the
@@ -154,6 +158,61 @@ __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   return p.tile_base + (t * mul + add) % p.ntiles;
 }
 
+// ---- DSGD ring epoch (RingDev, engine.cuh) -----------------------------------
+// A CTA takes tiles b, b + G, ... of every cell in order; each role keeps its
+// own cursor over (cell, tile of the cell).
+__device__ __forceinline__ int64_t ring_cell_nk(const RingDev& r, int c) {
+  const uint32_t T = (uint32_t)(__ldg(r.cell_tile + c + 1) - __ldg(r.cell_tile + c));
+  return T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // 32-bit: < 2^32 tiles
+}
+struct RingCursor {
+  int c = 0;
+  int64_t j = 0, nk = 0;
+  __device__ void enter(const RingDev& r, int c0) {
+    j = 0;
+    nk = 0;
+    for (c = c0; c < r.ncell; ++c)
+      if ((nk = ring_cell_nk(r, c)) > 0) break;
+  }
+  __device__ int64_t tile(const RingDev& r) const {
+    const int64_t base = __ldg(r.cell_tile + c), T = __ldg(r.cell_tile + c + 1) - base;
+    const int64_t t = (int64_t)blockIdx.x + j * gridDim.x;
+    return base + (t * __ldg(r.cell_perm + 2 * c) + __ldg(r.cell_perm + 2 * c + 1)) % T;
+  }
+  __device__ void next(const RingDev& r) {
+    if (++j == nk) enter(r, c + 1);
+  }
+};
+__device__ __forceinline__ int64_t ring_tiles(const RingDev& r) {
+  int64_t n = 0;
+  for (int c = 0; c < r.ncell; ++c) n += ring_cell_nk(r, c);
+  return n;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Waits until arrival flag f carries this epoch (the block it stands for has
+// landed in this rank's factor matrices), then orders the TMA reads behind
+// it.  A wait that outlives ~2 s raises r.err and gives up instead of
+// hanging the device (the host reports the error after the epoch).
+__device__ void ring_wait(const RingDev& r, int f) {
+  if (f < 0 || r.emulate) return;
+  const long long t0 = clock64();
+  while (ld_acquire_sys(r.flags + f) < r.epoch) {
+    if (clock64() - t0 > r.timeout_cycles) {
+      atomicCAS(r.err, 0u, 0x10000u | (unsigned)f);  // the first wait that gave up
+      break;
+    }
+    __nanosleep(128);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <bool kCore, bool k3 = false>
 __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tslot) {
   using L = WsLayout<kCore, k3>;
@@ -233,13 +292,17 @@ __device__ void ws_teardown(uint32_t tmem) {
 
 // Warp 0: the tile's COO columns (N index columns + values, 512 B each) by
 // 1-D bulk copies into a kI-deep ring, running ahead of the gathers.
-template <bool kCore, bool k3 = false>
+template <bool kCore, bool k3 = false, bool kRing = false>
 __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsLayout<kCore, k3>;
   if ((threadIdx.x & 31) != 0) return;
+  constexpr bool ring = kRing;
+  RingCursor cur;
+  if (ring) cur.enter(p.ring, 0);
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
-    const int64_t tile = ws_tile(p, k);
+    const int64_t tile = ring ? cur.tile(p.ring) : ws_tile(p, k);
+    if (ring) cur.next(p.ring);
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
     // valid-row count of the tile rides with its COO slot (published by the
@@ -255,13 +318,22 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
 // Gather warps: as soon as an A slot is free, TMA gather4 of the tile's
 // factor rows (N modes x 32 groups of 4 rows) into it; gather warp w issues
 // groups [w * 96 / kGW, (w + 1) * 96 / kGW) and arrives with its own bytes.
-template <bool kCore, bool k3 = false>
+template <bool kCore, bool k3 = false, bool kRing = false>
 __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsLayout<kCore, k3>;
   const int lane = threadIdx.x & 31, gw = (int)(threadIdx.x >> 5) - kGatherWarp;
   constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
   static_assert(kGroups % (kGW * 8) == 0, "whole batches of 8 groups per gather warp");
+  constexpr bool ring = kRing;
+  RingCursor cur;
+  if (ring) cur.enter(p.ring, 0);
   for (int64_t k = 0; k < nk; ++k) {
+    // ring: the first tile of a cell waits for the cell's blocks to arrive
+    int4 io = make_int4(-1, -1, -1, -1);
+    if (ring) {
+      if (cur.j == 0) io = __ldg(p.ring.cell_io + cur.c);
+      cur.next(p.ring);
+    }
     const int s = (int)(k % kS), i = (int)(k % L::kI);
     mbar_wait(&bars[B_EMPTY + s], (uint32_t)(((k / kS) & 1) ^ 1));
     // window 2: tile k - 2 retired as well (its slot's completion (k - 2) / kS;
@@ -279,6 +351,10 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
     // One elected thread per warp issues: per-lane operands would make the
     // compiler serialise every TMA issue over the 32 lanes (R2UR waterfall).
     if (elect_one()) {
+      if (ring && (io.x >= 0 || io.y >= 0)) {
+        ring_wait(p.ring, io.x);
+        ring_wait(p.ring, io.y);
+      }
       mbar_expect_tx(&bars[B_FULL + s], kPer * 512);
 #pragma unroll 1
       for (int g0 = gw * kPer; g0 < (gw + 1) * kPer; g0 += 8) {
@@ -298,10 +374,81 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
   }
 }
 
+// Ring epoch: this epilogue warp's write-backs of cell c are issued (and,
+// when the count is deferred by a tile, long since performed).  Each warp
+// counts itself in (G x kEpiWarps per cell) after a per-thread fence; the
+// warp that completes the count copies the cell's mode-3 block into the left
+// neighbour's factor matrices and raises its arrival flag.  A round's mode-2
+// block goes by ring_agent.
+__device__ void ring_done(const WsParams& p, int c, int lane) {
+  const RingDev& r = p.ring;
+  __threadfence();  // this thread's REDs of the cell before the count
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) last = atomicAdd(r.done + c, 1u) == gridDim.x * kEpiWarps - 1;
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();  // every warp's REDs of the cell are visible from here on
+  const int post = __ldg(r.cell_io + c).z;
+  if (post < 0) return;
+  const int4 pd = __ldg(r.posts + post);  // {mode, row0, nrows, peer flag}
+  const float4* src = reinterpret_cast<const float4*>(p.a[pd.x] + (size_t)pd.y * kW);
+  float4* dst = reinterpret_cast<float4*>(r.peer_a[pd.x] + (size_t)pd.y * kW);
+  const int n4 = pd.z * (kW / 4);
+#pragma unroll 8
+  for (int i = lane; i < n4; i += 32) dst[i] = __ldcg(src + i);
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) st_release_sys(r.peer_flags + pd.w, r.epoch);
+}
+
+// Ring epoch, warp kRingWarp of every CTA: after round s has been counted in
+// by every epilogue warp of the grid (its last cell's count, signalled
+// without deferral), copy this CTA's slice of the round's mode-2 block into
+// the left neighbour's factor matrix; the CTA that completes the copy count
+// raises the neighbour's flag.  Polls with a sleep, off the sweep's path.
+__device__ void ring_agent(const WsParams& p, int lane) {
+  const RingDev& r = p.ring;
+  const int Q = r.ncell / r.parts;
+  const unsigned want = gridDim.x * kEpiWarps;
+  for (int sr = 0; sr < r.parts; ++sr) {
+    const int c = sr * Q + Q - 1;
+    const int post = __ldg(r.cell_io + c).w;
+    if (post < 0) continue;
+    if (lane == 0) {
+      const long long t0 = clock64();
+      unsigned v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(r.done + c) : "memory");
+        if (v >= want) break;
+        if (clock64() - t0 > r.timeout_cycles) {
+          atomicCAS(r.err, 0u, 0x20000u | (unsigned)sr);
+          break;
+        }
+        __nanosleep(256);
+      }
+    }
+    __syncwarp();
+    const int4 pd = __ldg(r.posts + post);
+    const int64_t n4 = (int64_t)pd.z * (kW / 4);
+    const int64_t lo = n4 * blockIdx.x / gridDim.x, hi = n4 * (blockIdx.x + 1) / gridDim.x;
+    const float4* src = reinterpret_cast<const float4*>(p.a[pd.x] + (size_t)pd.y * kW);
+    float4* dst = reinterpret_cast<float4*>(r.peer_a[pd.x] + (size_t)pd.y * kW);
+#pragma unroll 4
+    for (int64_t i = lo + lane; i < hi; i += 32) dst[i] = __ldcg(src + i);
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0 && atomicAdd(r.copied + sr, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      st_release_sys(r.peer_flags + pd.w, r.epoch);
+    }
+  }
+}
+
 // ---- factor sweep --------------------------------------------------------------
 
-template <bool kAtomic>
-__global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_constant__ WsParams p) {
+template <bool kAtomic, bool kRing = false>
+__global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
+    ws_factor_kernel(const __grid_constant__ WsParams p) {
   using L = WsLayout<false>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
@@ -310,7 +457,10 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   ws_setup<false>(p, sm, bars, tslot);
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr bool ring = kRing;
+  static_assert(!kRing || kAtomic, "ring epochs run the accumulate rule");
+  const int64_t nk = ring ? ring_tiles(p.ring)
+                          : (p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   // TMEM: tile k in buffer b = k & 1 at 192 b; mode n at +64 n holds C_n
   // (overwritten in place by D'_n) and, with atomic rows, a copy of the A
   // rows (+32, from the identity half of the C GEMM's B operand) for the
@@ -319,9 +469,11 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
   constexpr uint32_t kC = 0, kU = 384, kBuf = 192, kMs = 64;
 
   if (warp == 0) {
-    ws_idx_producer<false>(p, sm, bars, nk);
+    ws_idx_producer<false, false, kRing>(p, sm, bars, nk);
+  } else if (kRing && warp == kRingWarp) {
+    ring_agent(p, lane);
   } else if (warp >= kGatherWarp) {
-    ws_gather_producer<false>(p, sm, bars, nk);
+    ws_gather_producer<false, false, kRing>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
@@ -351,13 +503,27 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         }
         mma_commit(&bars[B_UFULL]);
       };
+      // ring: at a cell boundary U(k - 1) goes out BEFORE the wait for tile
+      // k's rows, so a cell's write-back (and the block posts behind it)
+      // never waits for the next cell's blocks to arrive
+      RingCursor mc;
+      if constexpr (kRing) mc.enter(p.ring, 0);
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kS), b = (int)(k & 1);
+        bool early_u = false;
+        if constexpr (kRing) {
+          early_u = k >= 1 && mc.j == 0;
+          mc.next(p.ring);
+          if (early_u) {
+            if (k >= 2) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
+            issue_u(k - 1);
+          }
+        }
         mbar_wait(&bars[B_FULL + s], (uint32_t)((k / kS) & 1));
         // C(k) overwrites buffer b, whose D'(k - 2) is U(k - 2)'s A operand:
         // issue it once U(k - 2) has completed (PTX orders MMAs only per
         // accumulator; U(k - 1) is not issued yet, so the phase is exact)
-        if (k >= 2) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
+        if (k >= 2 && !early_u) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
@@ -370,7 +536,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         mma_commit(&bars[B_CFULL + b]);
         // the only read of the A slot (window: held until the write-back)
         if (kAtomic && !p.window) mma_commit(&bars[B_EMPTY + s]);
-        if (k >= 1) issue_u(k - 1);
+        if (k >= 1 && !early_u) issue_u(k - 1);
       }
       if (nk >= 1) issue_u(nk - 1);
     }
@@ -517,13 +683,53 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_factor_kernel(const __grid_c
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);
       }
     };
+    // ring: cell-completion counts (cells without a tile here count at once)
+    // ring: a cell's count goes in one tile late (its REDs have landed by
+    // then, so the fence is cheap) when the next tile is in the next cell and
+    // the neighbour needs the block only K >= 2 cells later; otherwise (a
+    // round's end, skipped cells, K = 1) right away -- a deferred count that
+    // waited on a block the neighbour posts from the same cell index would
+    // close a cycle around the ring
+    RingCursor rc;
+    int pending = -1;
+    const int rq = p.ring.parts > 0 ? p.ring.ncell / p.ring.parts : 1;
+    const bool can_defer = rq >= 2 * p.ring.parts;
+    if constexpr (ring) {
+      rc.enter(p.ring, 0);
+      for (int c = 0; c < rc.c; ++c) ring_done(p, c, lane);  // no tiles here
+    }
     if (nk > 0) epi1(0, cur);
     for (int64_t k = 0; k < nk; ++k) {
-      if (k + 1 < nk) epi1(k + 1, nxt);
-      epi2(k, cur);
+      if constexpr (ring) {
+        // the last tile of a cell: write-back first, the next cell's epilogue
+        // after (its rows may still be on their way)
+        const int c0 = rc.c;
+        rc.next(p.ring);
+        if (rc.c != c0) {
+          epi2(k, cur);
+          if (pending >= 0) ring_done(p, pending, lane);
+          pending = -1;
+          const bool round_end = rc.c >= p.ring.ncell || rc.c / rq != c0 / rq;
+          if (round_end || !can_defer || rc.c != c0 + 1) ring_done(p, c0, lane);
+          else pending = c0;
+          for (int c = c0 + 1; c < rc.c; ++c) ring_done(p, c, lane);  // no tiles here
+          if (k + 1 < nk) epi1(k + 1, nxt);
+        } else {
+          if (k + 1 < nk) epi1(k + 1, nxt);
+          epi2(k, cur);
+          if (pending >= 0) ring_done(p, pending, lane);
+          pending = -1;
+        }
+      } else {
+        if (k + 1 < nk) epi1(k + 1, nxt);
+        epi2(k, cur);
+      }
       cur = nxt;
     }
   }
+  // ring: the blocks this rank holds at the epoch's end have landed
+  if (kRing && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int f = 0; f < p.ring.nfinal; ++f) ring_wait(p.ring, __ldg(p.ring.final_waits + f));
   ws_teardown(tmem);
 }
 
@@ -1508,6 +1714,26 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   if (e != cudaSuccess) return e;
   const int grid = (int)sweep_grid(v);
   kern<<<grid, kThreadsWs, bytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ws_factor_ring(const KView& v, const int32_t* dims, const RingDev& ring,
+                                  float lr, float reg, cudaStream_t st) {
+  WsParams p{};
+  if (!make_params(p, v, dims, 1, 0, false)) return cudaErrorNotSupported;
+  p.lr = lr;
+  p.reg = reg;
+  p.atomic_update = 1;
+  p.exp = ws_exp_bits();
+  p.ring = ring;
+  const int bytes = (int)WsLayout<false>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(ws_factor_kernel<true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  // every CTA must be resident at once (cells end in cross-CTA counts)
+  int grid = num_sms();
+  if (v.max_ctas > 0 && v.max_ctas < grid) grid = v.max_ctas;
+  ws_factor_kernel<true, true><<<grid, kThreadsRing, bytes, st>>>(p);
   return cudaGetLastError();
 }
 

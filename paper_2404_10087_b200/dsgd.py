@@ -113,6 +113,89 @@ def local_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
     return (np.ascontiguousarray(idx[pos]), np.ascontiguousarray(vals[pos]), off, pos)
 
 
+# ---- ring schedule (token-passing mode-3 blocks) ----------------------------------
+#
+# The stratum loop above pays a device-wide stop at each of its P*P stratum
+# boundaries (every rank must finish a stratum before the mode-3 blocks move).
+# The ring schedule removes them: mode 3 is cut into Q = K*P blocks that
+# circulate as tokens, K per rank.  In round s (mode-2 block (g+s) % P,
+# exchanged once per round as before) rank g sweeps cells i = 0..Q-1 with
+# mode-3 block (K*g + i) % Q and passes each block to rank g-1 as soon as its
+# cell is done; rank g-1 needs that block K cells later (K = 2: one cell of
+# slack hides the transfer; K = 1: the strata's blocks, point-to-point waits
+# instead of device-wide stops).  At any moment every block has one owner, so
+# the sweeps never conflict, and a cell waits only for its own blocks
+# (ftkcu_ring_factor_epoch runs a whole phase as one persistent kernel).
+# After Q steps every block has visited every rank once and the tokens are
+# back at their start (rank g holds K*g .. K*g+K-1).
+
+
+def make_ring_layout(dims, idx: np.ndarray, parts: int, tokens: int = 2) -> Layout:
+    """Blocks of the ring schedule: P for modes 1 and 2, K*P for mode 3."""
+    dims = tuple(int(d) for d in dims)
+    if len(dims) != 3:
+        raise ValueError("DSGD stratification is defined for order-3 tensors (SURVEY.md §8e)")
+    if parts < 2 or tokens < 1:
+        raise ValueError("the ring schedule needs at least 2 parts and 1 token per rank")
+    offs = (balanced_blocks(idx[:, 0], dims[0], parts), balanced_blocks(idx[:, 1], dims[1], parts),
+            balanced_blocks(idx[:, 2], dims[2], tokens * parts))
+    return Layout(parts, dims, offs)
+
+
+def ring_tokens(layout: Layout) -> int:
+    return (len(layout.row_off[2]) - 1) // layout.parts
+
+
+def ring_cell_blocks(parts: int, rank: int, s: int, i: int, tokens: int = 2) -> tuple[int, int, int]:
+    """(mode-1, mode-2, mode-3) blocks of rank ``rank``'s cell (s, i)."""
+    return rank, (rank + s) % parts, (tokens * rank + i) % (tokens * parts)
+
+
+def ring_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
+    """This rank's nonzeros ordered by ring cell ``s*K*P + i``; returns (idx,
+    vals, cell_offsets[K*P*P + 1], global_positions)."""
+    P = layout.parts
+    K = ring_tokens(layout)
+    Q = K * P
+    b1 = layout.block_of(0, idx[:, 0])
+    pos = np.nonzero(b1 == rank)[0]
+    li = idx[pos]
+    s = (layout.block_of(1, li[:, 1]) - rank) % P
+    i = (layout.block_of(2, li[:, 2]) - K * rank) % Q
+    key = (s * Q + i).astype(np.int64)
+    order = np.argsort(key, kind="stable")
+    counts = np.bincount(key, minlength=P * Q)
+    off = np.zeros(P * Q + 1, np.int64)
+    np.cumsum(counts, out=off[1:])
+    pos = pos[order]
+    return (np.ascontiguousarray(idx[pos]), np.ascontiguousarray(vals[pos]), off, pos)
+
+
+def ring_events(parts: int, rank: int, tokens: int = 2):
+    """The protocol of one rank per epoch, in order: ("wait", mode, round,
+    block) before a cell that needs a block from rank+1, ("cell", s, i),
+    ("post", mode, round, block) handing a block to rank-1 (round = the one
+    in which rank-1 sweeps it; round P = the epoch's end), and the final
+    ("wait", ...) for the blocks held at the end.  ftkcu_ring_factor_epoch
+    builds the same tables (flag ids F3(round, block), F2(round, block))."""
+    P, K, g = parts, tokens, rank
+    Q = K * P
+    ev = []
+    for s in range(P):
+        for i in range(Q):
+            x, y = (K * g + i) % Q, (g + s) % P
+            if i == 0 and s > 0:
+                ev.append(("wait", 1, s, y))
+            if s > 0 or i >= K:
+                ev.append(("wait", 2, s, x))
+            ev.append(("cell", s, i))
+            ev.append(("post", 2, s + (1 if i + K >= Q else 0), x))
+            if i == Q - 1:
+                ev.append(("post", 1, s + 1, y))
+    ev += [("wait", 2, P, (K * g + q) % Q) for q in range(K)] + [("wait", 1, P, g)]
+    return ev
+
+
 IN_FLIGHT_TILES_PER_CTA = 3  # A-row slots a factor-sweep CTA keeps in flight
 TILE_NNZ = 128
 
@@ -152,11 +235,16 @@ class DsgdTrainer:
     """
 
     def __init__(self, backend, layout: Layout, rank: int, lr_a=1e-3, lr_b=1e-3, reg_a=1e-4,
-                 reg_b=1e-4, staleness: float | None = None):
+                 reg_b=1e-4, staleness: float | None = None, schedule: str = "strata"):
         self.be = backend
         self.layout = layout
         self.rank = rank
         self.P = layout.parts
+        if schedule not in ("strata", "ring"):
+            raise ValueError(schedule)
+        if schedule == "ring" and (len(layout.row_off[2]) - 1) % layout.parts:
+            raise ValueError("the ring schedule needs make_ring_layout (K*P mode-3 blocks)")
+        self.schedule = schedule
         self.lr_a, self.lr_b, self.reg_a, self.reg_b = lr_a, lr_b, reg_a, reg_b
         if staleness and hasattr(backend, "set_grid_cap"):
             min_rows = min(int(np.min(np.diff(o))) for o in layout.row_off)
@@ -172,13 +260,17 @@ class DsgdTrainer:
 
     def cell_seeds(self, epoch_seed: int) -> np.ndarray:
         P = self.P
-        return np.array([stratum_seed(epoch_seed, s, t) for s in range(P) for t in range(P)],
+        Q = len(self.layout.row_off[2]) - 1 if self.schedule == "ring" else P
+        return np.array([stratum_seed(epoch_seed, s, t) for s in range(P) for t in range(Q)],
                         np.uint64)
 
     def factor_phase(self, epoch_seed: int):
         """One factor phase.  A backend with ``factor_epoch`` runs the whole
         stratum loop natively (one call, CUDA-graph replay); otherwise the
         loop below drives ``factor_cell``/``shift``/``allgather``."""
+        if self.schedule == "ring":
+            self.be.ring_epoch(self.layout, self.cell_seeds(epoch_seed))
+            return
         fused = getattr(self.be, "factor_epoch", None)
         if fused is not None:
             fused(self.layout, self.cell_seeds(epoch_seed))
@@ -249,6 +341,12 @@ class EngineBackend:
 
     def set_grid_cap(self, ctas: int):
         self.s.set_option("max_ctas", int(ctas))
+
+    def ring_epoch(self, layout: Layout, cell_seeds):
+        """A ring factor phase (ftkcu_ring_factor_epoch): one persistent sweep;
+        with a communicator it ends with the all-gather of the held blocks."""
+        self.s.ring_factor_epoch(self.slot, layout.parts, self.rank, layout.row_off[1],
+                                 layout.row_off[2], cell_seeds, self.lr_a, self.reg_a)
 
     def factor_cell(self, cell, seed):
         self.s.factor_phase_cell(self.slot, cell, self.lr_a, self.reg_a, seed)

@@ -4,7 +4,7 @@
 // 8 rows / instr, the production scheme) and 8 (whole 128-B rows, 4 rows /
 // instr).  Same bytes, different numbers of L1 wavefronts / L2 requests per
 // instruction.  Rows of 32 fp32 (J = 32) drawn uniformly from tables of the
-// three Netflix mode sizes; 99,072,000 row updates per launch, every element
+// three Netflix mode sizes and two DSGD block sizes; 99,072,000 row updates per launch, every element
 // += 1 (checked against the per-row counts).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 red_segments.cu -o red_segments
 #include <cuda_runtime.h>
@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(256) red_kernel(float* a, const int* rows, int
 
 int main() {
   const int64_t n = 99072000;
-  const int dims[3] = {480189, 17770, 2182};
+  // the three Netflix mode sizes, then DSGD mode-3 blocks at P = 8
+  // (strata: 2182 / 8 rows; ring: 2182 / 16)
+  const int dims[5] = {480189, 17770, 2182, 273, 136};
   std::vector<int> h(n);
   int *rows;
   float* a;
@@ -54,7 +56,7 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < 5; ++m) {
     std::mt19937_64 rng(m + 1);
     std::vector<int64_t> cnt(dims[m], 0);
     for (auto& x : h) {

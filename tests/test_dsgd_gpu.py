@@ -185,3 +185,112 @@ def test_fused_stratum_loop_matches_python_loop(graphs):
             assert launches == 3 * 9 * 1  # one sweep kernel per cell per epoch
     for n in range(3):
         np.testing.assert_allclose(outs[1][n], outs[0][n], rtol=2e-3, atol=2e-5)
+
+
+# ---- ring schedule (token-passing mode-3 blocks) --------------------------------
+
+
+def _ring_backend_cls():
+    base = engine_host_backend_cls()
+
+    class RingHostBackend(base):
+        """Ring factor phase on the device (ftkcu_ring_factor_epoch: the
+        virtual ranks' persistent kernels pass blocks to each other through
+        peer pointers and flags, concurrently on one GPU); the epoch-end
+        all-gather of the held blocks over the host group."""
+
+        def ring_epoch(self, layout, cell_seeds):
+            self.g.barrier.wait()  # every rank's previous uploads are done
+            super().ring_epoch(layout, cell_seeds)
+            self.g.barrier.wait()  # every rank's kernel is launched before anyone waits
+            assert not self.s.ring_status(), "a ring wait timed out"
+            self.allgather(1, layout.row_off[1])
+            self.allgather(2, layout.row_off[2][0::dsgd.ring_tokens(layout)])
+
+    return RingHostBackend
+
+
+def _run_ring(P, epochs, dims, tr, te, a0, b0, j, K=2):
+    tri, trv = tr
+    tei, tev = te
+    lay = dsgd.make_ring_layout(dims, tri, P, K)
+    grp = HostGroup(P)
+    cls = _ring_backend_cls()
+    hist = [None] * epochs
+    finals = [None] * P
+
+    def rank(g):
+        s = eng.Session(0)
+        try:
+            s.set_option("precision", eng.PREC_TF32)
+            s.set_option("max_ctas", 148 // P)  # all virtual ranks resident at once
+            s.upload_model(dims, [j] * 3, j, [x.copy() for x in a0], [x.copy() for x in b0])
+            idx, vals, off, _ = dsgd.ring_cells(lay, tri, trv, g)
+            be = cls(grp, s, 0, idx, vals, off, dims, trv.size, rank=g, world=P)
+            sel = np.nonzero(lay.block_of(0, tei[:, 0]) == g)[0]
+            be.add_eval(np.ascontiguousarray(tei[sel]), np.ascontiguousarray(tev[sel]), dims)
+            blobs = grp.publish_all(g, s.ring_export())
+            s.ring_connect(0, blobs[(g - 1) % P])
+            grp.barrier.wait()  # every rank's flags are cleared before any post
+            tr_ = dsgd.DsgdTrainer(be, lay, g, schedule="ring")
+            for e in range(epochs):
+                tr_.epoch(host.derive_seed(1, [e + 1]))
+                r = tr_.rmse_mae(1)
+                if g == 0:
+                    hist[e] = r
+            tr_.finalize()
+            finals[g] = s.download_model()
+        finally:
+            s.close()
+
+    grp.run(rank)
+    return np.array(hist), finals
+
+
+@pytest.mark.parametrize("P,K", [(2, 2), (4, 2), (4, 1), (8, 2)])
+def test_ring_rmse_trajectory_vs_reference(P, K):
+    """P virtual ranks run the ring schedule concurrently on one GPU (their
+    kernels wait on each other's flags): the J = R = 32 planted test-RMSE
+    trajectory stays within 1e-3 of the reference's workers = 1 run, and
+    after finalize every rank holds the same replicated model."""
+    from test_accuracy_gpu import c1p32_problem
+
+    z = load("c1p32_trajectory")
+    dims, tr, te, a0, b0, _ = c1p32_problem()
+    epochs = 8
+    hist, finals = _run_ring(P, epochs, dims, tr, te, a0, b0, 32, K)
+    dev = np.abs(hist[:, 0] - z["w1_rmse"][:epochs])
+    assert np.max(dev) < 1e-3, (P, dev)
+    for g in range(1, P):
+        for n in range(3):
+            assert np.array_equal(finals[g][0][n], finals[0][0][n])
+            assert np.array_equal(finals[g][1][n], finals[0][1][n])
+
+
+def test_ring_emulated_epoch_and_errors():
+    """One rank emulating P = 3 (posts to local scratch, no waits) changes
+    only rows of its own cells' blocks; bad arguments raise."""
+    t = O.random_tensor([600, 300, 120], 60_000, 6, 0.0, 2.0)
+    m = O.random_model(t.dims, [32] * 3, 32, 5, 0.2)
+    lay = dsgd.make_ring_layout(t.dims, t.idx, 3)
+    idx, vals, off, _ = dsgd.ring_cells(lay, t.idx, t.vals, 1)
+    with eng.Session(0) as s:
+        s.set_option("precision", eng.PREC_TF32)
+        s.upload_model(t.dims, m.ranks, m.r, [x.copy() for x in m.a], [x.copy() for x in m.b])
+        s.upload_tensor(0, t.dims, idx, vals)
+        s.set_cells(0, off)
+        seeds = dsgd.DsgdTrainer(None, lay, 1, schedule="ring").cell_seeds(7)
+        with pytest.raises(eng.FtkError):  # not connected
+            s.ring_factor_epoch(0, 3, 1, lay.row_off[1], lay.row_off[2], seeds, 0.01, 0.01)
+        s.ring_emulate(0)
+        with pytest.raises(eng.FtkError):  # the tensor's cells are not a 3-part ring's
+            s.ring_factor_epoch(0, 2, 1, lay.row_off[1], lay.row_off[2][:5], seeds[:8], 0.01,
+                                0.01)
+        s.ring_factor_epoch(0, 3, 1, lay.row_off[1], lay.row_off[2], seeds, 0.01, 0.01)
+        assert not s.ring_status()
+        a1, _ = s.download_model()
+        for n in range(3):
+            changed = np.nonzero(np.any(a1[n] != m.a[n], axis=1))[0]
+            touched = np.unique(idx[:, n])
+            assert np.all(np.isin(changed, touched)) and changed.size > 0.5 * touched.size
+        assert np.all(np.isfinite(a1[0]))
