@@ -153,6 +153,8 @@ __device__ __forceinline__ float xhat_full(uint32_t tcol_other, const float (&c)
 
 __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
   const int64_t t = (int64_t)blockIdx.x + k * gridDim.x;
+  // tperm (a captured graph's per-epoch permutation) is read through the
+  // read-only path once per warp and cached in L1 after the first tile
   const int64_t mul = p.tperm ? __ldg(p.tperm) : p.tmul;
   const int64_t add = p.tperm ? __ldg(p.tperm + 1) : p.tadd;
   return p.tile_base + (t * mul + add) % p.ntiles;
@@ -168,16 +170,22 @@ __device__ __forceinline__ int64_t ring_cell_nk(const RingDev& r, int c) {
 struct RingCursor {
   int c = 0;
   int64_t j = 0, nk = 0;
+  int64_t base = 0, T = 1, mul = 1, add = 0;  // the current cell's tiles and permutation
   __device__ void enter(const RingDev& r, int c0) {
     j = 0;
     nk = 0;
     for (c = c0; c < r.ncell; ++c)
       if ((nk = ring_cell_nk(r, c)) > 0) break;
+    if (c < r.ncell) {
+      base = __ldg(r.cell_tile + c);
+      T = __ldg(r.cell_tile + c + 1) - base;
+      mul = __ldg(r.cell_perm + 2 * c);
+      add = __ldg(r.cell_perm + 2 * c + 1);
+    }
   }
-  __device__ int64_t tile(const RingDev& r) const {
-    const int64_t base = __ldg(r.cell_tile + c), T = __ldg(r.cell_tile + c + 1) - base;
+  __device__ int64_t tile(const RingDev&) const {
     const int64_t t = (int64_t)blockIdx.x + j * gridDim.x;
-    return base + (t * __ldg(r.cell_perm + 2 * c) + __ldg(r.cell_perm + 2 * c + 1)) % T;
+    return base + (t * mul + add) % T;
   }
   __device__ void next(const RingDev& r) {
     if (++j == nk) enter(r, c + 1);
@@ -299,15 +307,32 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
   constexpr bool ring = kRing;
   RingCursor cur;
   if (ring) cur.enter(p.ring, 0);
+  // tile ids and valid-row counts one tile ahead: the dependent global loads
+  // (tile permutation -> tile_rows) overlap the wait for the COO slot
+  auto tile_of = [&](int64_t k) -> int64_t {
+    if constexpr (ring) {
+      const int64_t t = cur.tile(p.ring);
+      cur.next(p.ring);
+      return t;
+    } else {
+      return ws_tile(p, k);
+    }
+  };
+  int64_t tile_n = nk > 0 ? tile_of(0) : 0;
+  int32_t rows_n = nk > 0 ? __ldg(p.tile_rows + tile_n) : 0;
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
-    const int64_t tile = ring ? cur.tile(p.ring) : ws_tile(p, k);
-    if (ring) cur.next(p.ring);
+    const int64_t tile = tile_n;
+    const int32_t rows = rows_n;
+    if (k + 1 < nk) {
+      tile_n = tile_of(k + 1);
+      rows_n = __ldg(p.tile_rows + tile_n);
+    }
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
     // valid-row count of the tile rides with its COO slot (published by the
     // arrive below), keeping the global load off the epilogue's critical path
-    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = rows;
     mbar_expect_tx(&bars[B_IFULL + i], L::kIdxSlot);
     for (int n = 0; n < kN; ++n)
       bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[B_IFULL + i]);
@@ -382,7 +407,7 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
 // block goes by ring_agent.
 __device__ void ring_done(const WsParams& p, int c, int lane) {
   const RingDev& r = p.ring;
-  __threadfence();  // this thread's REDs of the cell before the count
+  if (!(ws_exp(p) & 64)) __threadfence();  // this thread's REDs of the cell before the count (exp 64: timing only)
   __syncwarp();
   unsigned last = 0;
   if (lane == 0) last = atomicAdd(r.done + c, 1u) == gridDim.x * kEpiWarps - 1;
