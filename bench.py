@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--tc-ws", type=int, default=1, help="warp-specialized tcgen05 sweeps")
     ap.add_argument("--factor-warps", type=int, default=8, choices=[8, 16],
                     help="epilogue warps of the N=3 J=R=32 factor sweep")
-    ap.add_argument("--core16", type=int, default=1,
+    ap.add_argument("--core16", type=int, default=2,
                     help="tf32 core sweep on an fp16 copy of A (kind::f16, 10-bit mantissa)")
     ap.add_argument("--store-c", type=int, default=0,
                     help="core sweep storage scheme: C rows from a C cache rebuilt every core "

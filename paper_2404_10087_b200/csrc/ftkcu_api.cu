@@ -37,7 +37,7 @@ struct ftkcu_session {
   int64_t opt_hog_update = 1;  // 1: atomic accumulate, 0: overwrite (reference rule)
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
-  int64_t opt_core16 = 1;   // WS core sweep (tf32 precision): gather an fp16 copy of A (2: two epilogue groups)
+  int64_t opt_core16 = 2;   // WS core sweep (tf32 precision): fp16 copy of A; 2 = two epilogue groups (default), 1 = one, 0 = tf32 rows
   int64_t opt_factor_warps = 8;  // N=3 J=R=32 factor sweep: 8 or 16 epilogue warps
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;

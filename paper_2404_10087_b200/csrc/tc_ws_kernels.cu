@@ -307,8 +307,8 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
   constexpr bool ring = kRing;
   RingCursor cur;
   if (ring) cur.enter(p.ring, 0);
-  // tile ids and valid-row counts one tile ahead: the dependent global loads
-  // (tile permutation -> tile_rows) overlap the wait for the COO slot
+  // tile ids and valid-row counts kPf tiles ahead: the dependent global
+  // loads (tile permutation -> tile_rows) overlap the waits for COO slots
   auto tile_of = [&](int64_t k) -> int64_t {
     if constexpr (ring) {
       const int64_t t = cur.tile(p.ring);
@@ -318,15 +318,26 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
       return ws_tile(p, k);
     }
   };
-  int64_t tile_n = nk > 0 ? tile_of(0) : 0;
-  int32_t rows_n = nk > 0 ? __ldg(p.tile_rows + tile_n) : 0;
+  constexpr int kPf = 4;
+  int64_t tq[kPf];
+  int32_t rq[kPf];
+#pragma unroll
+  for (int d = 0; d < kPf; ++d) {
+    tq[d] = d < nk ? tile_of(d) : 0;
+    rq[d] = d < nk ? __ldg(p.tile_rows + tq[d]) : 0;
+  }
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
-    const int64_t tile = tile_n;
-    const int32_t rows = rows_n;
-    if (k + 1 < nk) {
-      tile_n = tile_of(k + 1);
-      rows_n = __ldg(p.tile_rows + tile_n);
+    const int64_t tile = tq[0];
+    const int32_t rows = rq[0];
+#pragma unroll
+    for (int d = 0; d + 1 < kPf; ++d) {
+      tq[d] = tq[d + 1];
+      rq[d] = rq[d + 1];
+    }
+    if (k + kPf < nk) {
+      tq[kPf - 1] = tile_of(k + kPf);
+      rq[kPf - 1] = __ldg(p.tile_rows + tq[kPf - 1]);
     }
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
@@ -1298,6 +1309,9 @@ __global__ void __launch_bounds__(kThreadsWs, 1) ws_core_cc_kernel(const __grid_
 //   warp 1     MMA: C(k), then G(k - 1)       warps 2-9    epilogue: C -> r D (fp16)
 
 constexpr uint32_t kModeTile16 = kRows * 64;  // 128 rows x 32 fp16
+// C accumulators in TMEM (96 columns each): the C GEMM -> epilogue hand-off
+// is latency-bound, so four tiles are in flight (two: 4.9 ms at C2)
+constexpr int kCB = 4;
 
 struct Ws16Layout {
   static constexpr uint32_t kSlot = kN * kModeTile16;  // 24 KB
@@ -1313,7 +1327,7 @@ struct Ws16Layout {
   static constexpr uint32_t o_rows = o_idx + kI * kIdxSlot;
   static constexpr uint32_t o_xp = o_rows + 64;  // x_hat halves [2 tiles][2 halves][128]
   static constexpr uint32_t o_bar = o_xp + 2 * 2 * kRows * 4;
-  static constexpr uint32_t o_tmem = o_bar + 32 * 8;
+  static constexpr uint32_t o_tmem = o_bar + 40 * 8;
   static constexpr uint32_t bytes = o_tmem + 16;
   static_assert(bytes <= 227 * 1024, "shared-memory budget");
 };
@@ -1323,10 +1337,10 @@ enum : int {
   H_EMPTY = 6,    // [6] slot read by the G GEMM
   H_IFULL = 12,   // [6] COO columns landed
   H_IEMPTY = 18,  // [6] COO columns consumed (8 epilogue warps + 2 gather warps)
-  H_CFULL = 24,   // [2] C accumulator ready
-  H_CEMPTY = 26,  // [2] C accumulator read
-  H_DFULL = 28,   // [2] r D tile written
-  H_DEMPTY = 30,  // [2] G GEMM done with the r D tile
+  H_CFULL = 24,   // [kCB] C accumulator ready
+  H_CEMPTY = 28,  // [kCB] C accumulator read
+  H_DFULL = 32,   // [2] r D tile written
+  H_DEMPTY = 34,  // [2] G GEMM done with the r D tile
 };
 
 
@@ -1368,9 +1382,11 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       mbar_init(&bars[H_IFULL + i], 1);
       mbar_init(&bars[H_IEMPTY + i], kEpiWarps + kGW);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kCB; ++b) {
       mbar_init(&bars[H_CFULL + b], 1);
       mbar_init(&bars[H_CEMPTY + b], kEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[H_DFULL + b], kEpiWarps);
       mbar_init(&bars[H_DEMPTY + b], 1);
     }
@@ -1390,21 +1406,43 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kG = 192;  // TMEM: C[b] at 96 b, G at 192
+  constexpr uint32_t kG = 96 * kCB;  // TMEM: C[b] at 96 b, G after them
 
   if (warp == 0) {
-    if (lane == 0)
+    if (lane == 0) {
+      // tile ids and valid-row counts kPf tiles ahead: the dependent global
+      // load is off the per-tile path (in line it capped the sweep near
+      // 0.8 us per tile)
+      constexpr int kPf = 4;
+      int64_t tq[kPf];
+      int32_t rq[kPf];
+#pragma unroll
+      for (int d = 0; d < kPf; ++d) {
+        tq[d] = d < nk ? ws_tile(p, d) : 0;
+        rq[d] = d < nk ? __ldg(p.tile_rows + tq[d]) : 0;
+      }
       for (int64_t k = 0; k < nk; ++k) {
         const int i = (int)(k % L::kI);
-        const int64_t tile = ws_tile(p, k);
+        const int64_t tile = tq[0];
+        const int32_t rows = rq[0];
+#pragma unroll
+        for (int d = 0; d + 1 < kPf; ++d) {
+          tq[d] = tq[d + 1];
+          rq[d] = rq[d + 1];
+        }
+        if (k + kPf < nk) {
+          tq[kPf - 1] = ws_tile(p, k + kPf);
+          rq[kPf - 1] = __ldg(p.tile_rows + tq[kPf - 1]);
+        }
         mbar_wait(&bars[H_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
         int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
-        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = rows;
         mbar_expect_tx(&bars[H_IFULL + i], L::kIdxSlot);
         for (int n = 0; n < kN; ++n)
           bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
         bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[H_IFULL + i]);
       }
+    }
   } else if (warp >= kGather16) {
     const int gw = warp - kGather16;
     constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
@@ -1460,9 +1498,9 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         mma_commit(&bars[H_EMPTY + s]);
       };
       for (int64_t k = 0; k < nk; ++k) {
-        const int s = (int)(k % L::kS), b = (int)(k & 1);
+        const int s = (int)(k % L::kS), b = (int)(k % kCB);
         mbar_wait(&bars[H_FULL + s], (uint32_t)((k / L::kS) & 1));
-        mbar_wait(&bars[H_CEMPTY + b], (uint32_t)(((k >> 1) & 1) ^ 1));
+        mbar_wait(&bars[H_CEMPTY + b], (uint32_t)(((k / kCB) & 1) ^ 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
 #pragma unroll
@@ -1481,25 +1519,18 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     for (int64_t k = eg; k < nk; k += kEG) {
-      const int b = (int)(k & 1), ii = (int)(k % L::kI);
+      const int b = (int)(k & 1), cb = (int)(k % kCB), ii = (int)(k % L::kI);
       const int32_t* s_idx = reinterpret_cast<const int32_t*>(sm + L::o_idx + ii * L::kIdxSlot);
       const float* s_val = reinterpret_cast<const float*>(s_idx + kN * kRows);
       mbar_wait(&bars[H_IFULL + ii], (uint32_t)((k / L::kI) & 1));
-      mbar_wait(&bars[H_CFULL + b], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&bars[H_CFULL + cb], (uint32_t)((k / kCB) & 1));
       tc_after();
       float c[kN][16];
       {  // the three modes' columns in flight before one wait
         uint32_t v[kN][16];
 #pragma unroll
-        if (!(ws_exp(p) & 128)) {  // exp 128: no TMEM loads (timing only)
-          for (int n = 0; n < kN; ++n) tmem_ld16(tl + b * 96 + n * kW + h * 16, v[n]);
-          tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int n = 0; n < kN; ++n)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[n][i] = __float_as_uint((float)(row + i));
-        }
+        for (int n = 0; n < kN; ++n) tmem_ld16(tl + cb * 96 + n * kW + h * 16, v[n]);
+        tmem_wait_ld();
 #pragma unroll
         for (int n = 0; n < kN; ++n)
 #pragma unroll
@@ -1507,7 +1538,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       }
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[H_CEMPTY + b]);  // C(k + 2) may land
+      if (lane == 0) mbar_arrive(&bars[H_CEMPTY + cb]);  // C(k + kCB) may land
       // column pairs in packed fp32 (FMUL2 / FFMA2): C_1 C_2 (shared by
       // x_hat and D'_0), x_hat as an even / odd pair of partial sums
       f2 c0[8], c1[8], c2[8], p12[8], acc = {0.0f, 0.0f};

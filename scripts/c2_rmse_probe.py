@@ -64,7 +64,7 @@ def main():
                           "wall": time.time() - t0}), flush=True)
         for k in opts:  # back to defaults
             s.set_option(k, {"precision": 1, "max_ctas": 0, "staleness": 32, "hog_update": 1,
-                             "core16": 1, "tc_ws": 1}.get(k, 0))
+                             "core16": 2, "tc_ws": 1}.get(k, 0))
     s.close()
 
 

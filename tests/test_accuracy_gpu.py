@@ -324,7 +324,7 @@ def core_grad_fp64(t, m):
     return np.concatenate([x.ravel() for x in g]), np.concatenate([x.ravel() for x in scale])
 
 
-@pytest.mark.parametrize("core16,max_ctas", [(1, 0), (1, 1), (1, 3), (2, 0), (2, 1), (0, 0)],
+@pytest.mark.parametrize("core16,max_ctas", [(1, 0), (1, 1), (1, 3), (2, 0), (2, 1), (2, 3), (0, 0)],
                          ids=["ws16", "ws16-1cta", "ws16-3cta", "ws16x2", "ws16x2-1cta", "ws-tf32"])
 def test_core32_gradient_per_element(session, core16, max_ctas):
     """The headline core sweep (ws_core16_kernel: fp16 copy of A, fp32
@@ -346,7 +346,7 @@ def test_core32_gradient_per_element(session, core16, max_ctas):
     finally:
         for k, v in DEFAULTS.items():
             session.set_option(k, v)
-        session.set_option("core16", 1)
+        session.set_option("core16", 2)  # the default
     assert kern == (eng.K_WS16 if core16 else eng.K_WS)
     want, scale = core_grad_fp64(t, m)
     eps = 2.0 ** -10  # fp16 / tf32 operands (10-bit mantissa), rounded to nearest

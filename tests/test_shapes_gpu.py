@@ -95,7 +95,7 @@ def test_factor_distinct_rows_all_shapes(session, shape, prec):
         np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
 
 
-@pytest.mark.parametrize("core16", [0, 1])
+@pytest.mark.parametrize("core16", [0, 1, 2])
 def test_core_gradient_tf32_and_f16_operand_paths(session, core16):
     """N = 3, J = R = 32 (the headline shape) has two single-pass core sweeps:
     tf32 rows copied into TMEM (core16 = 0) and one fp16 row tile read by both
@@ -109,7 +109,7 @@ def test_core_gradient_tf32_and_f16_operand_paths(session, core16):
         session.upload_model(m.dims, m.ranks, m.r, m.a, m.b)
         _, g = session.core_phase(0, None, 16, 1e-3, 1e-4, HOG, seed=5, want_grad=True)
     finally:
-        session.set_option("core16", 1)
+        session.set_option("core16", 2)  # the default
         session.set_option("precision", eng.PREC_FP32)
     want = O.COracle.core_phase(t, m.copy(), host.global_plan(t.nnz, 16, 1), 16, 1e-3, 1e-4)
     tol = GRAD_TOL[eng.PREC_TF32]
