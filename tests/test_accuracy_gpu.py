@@ -325,7 +325,7 @@ def core_grad_fp64(t, m):
 
 
 @pytest.mark.parametrize("core16,max_ctas", [(1, 0), (1, 1), (1, 3), (2, 0), (2, 1), (2, 3), (0, 0)],
-                         ids=["ws16", "ws16-1cta", "ws16-3cta", "ws16x2", "ws16x2-1cta", "ws-tf32"])
+                         ids=["ws16", "ws16-1cta", "ws16-3cta", "ws16x2", "ws16x2-1cta", "ws16x2-3cta", "ws-tf32"])
 def test_core32_gradient_per_element(session, core16, max_ctas):
     """The headline core sweep (ws_core16_kernel: fp16 copy of A, fp32
     accumulate) with one (core16 = 1) or two (core16 = 2) epilogue warp
