@@ -968,18 +968,22 @@ __global__ void __launch_bounds__(b16::kThreads, 1) big16_core_kernel(const __gr
   const int64_t nk = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (warp == 0) {
-    if (lane == 0)
+    if (lane == 0) {
+      auto ahead = tile_ahead<4>([&](int64_t kk) { return big_tile(p, kk); }, p.tile_rows, nk);
       for (int64_t k = 0; k < nk; ++k) {
         const int i = (int)(k % kI);
-        const int64_t tile = big_tile(p, k);
+        int64_t tile;
+        int32_t valid;
+        ahead.pop(k, tile, valid);
         mbar_wait(&bars[IEMPTY + i], (uint32_t)(((k / kI) & 1) ^ 1));
         int32_t* s_idx = reinterpret_cast<int32_t*>(sm + o_idx + i * kIdxSlot);
-        reinterpret_cast<int32_t*>(sm + o_rows)[i] = __ldg(p.tile_rows + tile);
+        reinterpret_cast<int32_t*>(sm + o_rows)[i] = valid;
         mbar_expect_tx(&bars[IFULL + i], kIdxSlot);
         for (int n = 0; n < kN; ++n)
           bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[IFULL + i]);
         bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[IFULL + i]);
       }
+    }
   } else if (warp >= kGWarp) {
     const int gw = warp - kGWarp;
     constexpr int kPer = kN * kRows / 4 / kGW;  // 48 groups of 4 rows
@@ -1209,18 +1213,22 @@ __global__ void __launch_bounds__(b16p::kThreads, 1) big16p_core_kernel(const __
   auto mode_of = [&](int j) { return j == 0 ? m0 : (j == 1 ? m1 : pm); };
 
   if (warp == 0) {
-    if (lane == 0)
+    if (lane == 0) {
+      auto ahead = tile_ahead<4>([&](int64_t kk) { return big_tile(p, kk); }, p.tile_rows, nk);
       for (int64_t k = 0; k < nk; ++k) {
         const int i = (int)(k % kI);
-        const int64_t tile = big_tile(p, k);
+        int64_t tile;
+        int32_t valid;
+        ahead.pop(k, tile, valid);
         mbar_wait(&bars[IEMPTY + i], (uint32_t)(((k / kI) & 1) ^ 1));
         int32_t* s_idx = reinterpret_cast<int32_t*>(sm + o_idx + i * kIdxSlot);
-        reinterpret_cast<int32_t*>(sm + o_rows)[i] = __ldg(p.tile_rows + tile);
+        reinterpret_cast<int32_t*>(sm + o_rows)[i] = valid;
         mbar_expect_tx(&bars[IFULL + i], kIdxSlot);
         for (int n = 0; n < kN; ++n)
           bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[IFULL + i]);
         bulk_g2s(s_idx + kN * kRows, p.vals + tile * kRows, kRows * 4, &bars[IFULL + i]);
       }
+    }
   } else if (warp >= kGWarp) {
     const int gw = warp - kGWarp;
     constexpr int kPer = kRows / 4 / kGW;  // 16 groups of 4 rows per warp per mode

@@ -318,27 +318,12 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
       return ws_tile(p, k);
     }
   };
-  constexpr int kPf = 4;
-  int64_t tq[kPf];
-  int32_t rq[kPf];
-#pragma unroll
-  for (int d = 0; d < kPf; ++d) {
-    tq[d] = d < nk ? tile_of(d) : 0;
-    rq[d] = d < nk ? __ldg(p.tile_rows + tq[d]) : 0;
-  }
+  auto ahead = tile_ahead<4>(tile_of, p.tile_rows, nk);
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
-    const int64_t tile = tq[0];
-    const int32_t rows = rq[0];
-#pragma unroll
-    for (int d = 0; d + 1 < kPf; ++d) {
-      tq[d] = tq[d + 1];
-      rq[d] = rq[d + 1];
-    }
-    if (k + kPf < nk) {
-      tq[kPf - 1] = tile_of(k + kPf);
-      rq[kPf - 1] = __ldg(p.tile_rows + tq[kPf - 1]);
-    }
+    int64_t tile;
+    int32_t rows;
+    ahead.pop(k, tile, rows);
     mbar_wait(&bars[B_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
     // valid-row count of the tile rides with its COO slot (published by the
@@ -1341,6 +1326,7 @@ enum : int {
   H_CEMPTY = 28,  // [kCB] C accumulator read
   H_DFULL = 32,   // [2] r D tile written
   H_DEMPTY = 34,  // [2] G GEMM done with the r D tile
+  H_GDONE = 36,   // [1] the CTA's last G GEMM completed (G may be read)
 };
 
 
@@ -1390,6 +1376,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       mbar_init(&bars[H_DFULL + b], kEpiWarps);
       mbar_init(&bars[H_DEMPTY + b], 1);
     }
+    mbar_init(&bars[H_GDONE], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int n = 0; n < kN; ++n) prefetch_tmap(&p.tmap[n]);
   }
@@ -1410,30 +1397,12 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // tile ids and valid-row counts kPf tiles ahead: the dependent global
-      // load is off the per-tile path (in line it capped the sweep near
-      // 0.8 us per tile)
-      constexpr int kPf = 4;
-      int64_t tq[kPf];
-      int32_t rq[kPf];
-#pragma unroll
-      for (int d = 0; d < kPf; ++d) {
-        tq[d] = d < nk ? ws_tile(p, d) : 0;
-        rq[d] = d < nk ? __ldg(p.tile_rows + tq[d]) : 0;
-      }
+      auto ahead = tile_ahead<4>([&](int64_t kk) { return ws_tile(p, kk); }, p.tile_rows, nk);
       for (int64_t k = 0; k < nk; ++k) {
         const int i = (int)(k % L::kI);
-        const int64_t tile = tq[0];
-        const int32_t rows = rq[0];
-#pragma unroll
-        for (int d = 0; d + 1 < kPf; ++d) {
-          tq[d] = tq[d + 1];
-          rq[d] = rq[d + 1];
-        }
-        if (k + kPf < nk) {
-          tq[kPf - 1] = ws_tile(p, k + kPf);
-          rq[kPf - 1] = __ldg(p.tile_rows + tq[kPf - 1]);
-        }
+        int64_t tile;
+        int32_t rows;
+        ahead.pop(k, tile, rows);
         mbar_wait(&bars[H_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
         int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
         reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = rows;
@@ -1513,6 +1482,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         if (k >= 1) issue_g(k - 1);
       }
       if (nk >= 1) issue_g(nk - 1);
+      mma_commit(&bars[H_GDONE]);  // after every G GEMM (tcgen05.commit tracks all prior MMAs)
     }
   } else {
     const int ew = warp - 2, q = warp & 3, eg = ew / kEpiWarps, h = (ew >> 2) & 1;
@@ -1591,7 +1561,10 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[H_DFULL + b]);
     }
-    if (nk > 0) mbar_wait(&bars[H_DEMPTY + (int)((nk - 1) & 1)], (uint32_t)(((nk - 1) >> 1) & 1));
+    // the last G GEMM: a dedicated barrier -- with two epilogue groups one
+    // group can finish while the other's D barrier is still two phases
+    // behind, which a parity wait on it would mistake for done
+    mbar_wait(&bars[H_GDONE], 0u);
     tc_after();
     if (eg == 0 && q < kN) {
       uint32_t v[16];

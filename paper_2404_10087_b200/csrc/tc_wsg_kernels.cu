@@ -200,12 +200,15 @@ template <int N, bool kCore>
 __device__ void wsg_idx_producer(const WsgParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsgLayout<N, kCore>;
   if ((threadIdx.x & 31) != 0) return;
+  auto ahead = tile_ahead<4>([&](int64_t kk) { return wsg_tile(p, kk); }, p.tile_rows, nk);
   for (int64_t k = 0; k < nk; ++k) {
     const int i = (int)(k % L::kI);
-    const int64_t tile = wsg_tile(p, k);
+    int64_t tile;
+    int32_t valid;
+    ahead.pop(k, tile, valid);
     mbar_wait(&bars[G_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
     int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
-    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+    reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = valid;
     mbar_expect_tx(&bars[G_IFULL + i], L::kIdxSlot);
     for (int n = 0; n < N; ++n)
       bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[G_IFULL + i]);
@@ -379,18 +382,22 @@ __global__ void __launch_bounds__(FW<W>::Threads, 1)
   constexpr int kH = W / 8;  // epilogue warps per lane quarter
 
   if (warp == 0) {
-    if (lane == 0)
+    if (lane == 0) {
+      auto ahead = tile_ahead<4>([&](int64_t kk) { return wsg_tile(p, kk); }, p.tile_rows, nk);
       for (int64_t k = 0; k < nk; ++k) {
         const int i = (int)(k % L::kI);
-        const int64_t tile = wsg_tile(p, k);
+        int64_t tile;
+        int32_t valid;
+        ahead.pop(k, tile, valid);
         mbar_wait(&bars[G_IEMPTY + i], (uint32_t)(((k / L::kI) & 1) ^ 1));
         int32_t* s_idx = reinterpret_cast<int32_t*>(sm + L::o_idx + i * L::kIdxSlot);
-        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = __ldg(p.tile_rows + tile);
+        reinterpret_cast<int32_t*>(sm + L::o_rows)[i] = valid;
         mbar_expect_tx(&bars[G_IFULL + i], L::kIdxSlot);
         for (int n = 0; n < N; ++n)
           bulk_g2s(s_idx + n * kRows, p.idx[n] + tile * kRows, kRows * 4, &bars[G_IFULL + i]);
         bulk_g2s(s_idx + N * kRows, p.vals + tile * kRows, kRows * 4, &bars[G_IFULL + i]);
       }
+    }
   } else if (warp >= F::GWarp) {
     const int gw = warp - F::GWarp;
     constexpr int kGroups = N * kRows / 4, kPer = kGroups / kGW;
