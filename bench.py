@@ -673,6 +673,25 @@ def roofline_of(dom, dom_ms, dom_bytes, achieved, peak, peak_kind, traffic, wb, 
 TRAJ_PATH = os.path.join(ROOT, "tests", "golden", "c2_trajectory.json")
 
 
+def reference_worker_spread():
+    """How far the reference's own uniform-data trajectory moves between
+    workers = 1 and workers = 16 (tests/golden/c2_workers_spread.json,
+    oracle/ref_workers_spread.py: ftkref::train on a statistically equivalent
+    C2 tensor) -- the scale against which an asynchronous engine's uniform
+    RMSE delta reads."""
+    path = os.path.join(ROOT, "tests", "golden", "c2_workers_spread.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        sp = json.load(f)
+    if "1" not in sp or "16" not in sp:
+        return None
+    w1, w16 = sp["1"]["rmse"], sp["16"]["rmse"]
+    return {"workers_1": w1, "workers_16": w16,
+            "max_abs_delta": max(abs(a - b) for a, b in zip(w1, w16)),
+            "tensor": "datagen cpu stream (statistically equivalent, not the bench bytes)"}
+
+
 def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
     """North-star accuracy at the benchmarked configuration: from the
     reference CLI's initial model, E Hogwild epochs of the engine (the same
@@ -720,12 +739,14 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
             s.upload_model(tr.dims, [j] * order, j, a, b)
             ev = s.eval(5, 1, 0.0, 0.0)
             rm = [float(np.sqrt(ev[0] / te.nnz))]
+            ep_ms = []
             for e in range(len(ref["rmse"])):
                 es = host.derive_seed(1, [e + 1])
-                s.factor_phase(4, None, 16, ref["lr_a"], ref["reg_a"], eng.MODE_HOGWILD,
-                               seed=host.derive_seed(es, [1]), timed=False)
-                s.core_phase(4, None, 16, ref["lr_b"], ref["reg_b"], eng.MODE_HOGWILD,
-                             seed=host.derive_seed(es, [2]), timed=False)
+                f_ms = s.factor_phase(4, None, 16, ref["lr_a"], ref["reg_a"], eng.MODE_HOGWILD,
+                                      seed=host.derive_seed(es, [1]), timed=True)
+                c_ms = s.core_phase(4, None, 16, ref["lr_b"], ref["reg_b"], eng.MODE_HOGWILD,
+                                    seed=host.derive_seed(es, [2]), timed=True)
+                ep_ms.append(float(f_ms) + float(c_ms if np.isscalar(c_ms) else c_ms[0]))
                 ev = s.eval(5, 1, 0.0, 0.0)
                 rm.append(float(np.sqrt(ev[0] / te.nnz)))
             for k in opts:
@@ -733,9 +754,16 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
             dev = [abs(x - y) for x, y in zip(rm, want)]
             res[name] = {"engine": rm, "max_abs_delta": max(dev),
                          "within_1e-3": bool(max(dev) <= 1e-3), "options": opts,
-                         "kernels": kernel_names(s)}
+                         "kernels": kernel_names(s),
+                         # device ms per epoch of these (untimed-region) epochs and the
+                         # throughput they imply: the price of the variant
+                         "epoch_ms": float(np.median(ep_ms)),
+                         "nnz_per_s": tr.nnz / (float(np.median(ep_ms)) * 1e-3)}
         out[kind] = dict(res["default"], reference=want, same_tensor=fp == ref["fingerprint_train"],
                          reference_workers=ref["workers"])
+        spread = reference_worker_spread() if kind == "uniform" else None
+        if spread:
+            out[kind]["reference_worker_spread"] = spread
         if len(res) > 1:
             out[kind]["variants"] = {k: v for k, v in res.items() if k != "default"}
         s.release_tensor(4)
