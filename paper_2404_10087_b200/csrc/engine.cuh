@@ -233,9 +233,10 @@ cudaError_t launch_wsg_core(const KView& v, const int32_t* dims, int64_t mul, in
                             float* grad, float* scratch, size_t scratch_bytes, cudaStream_t st);
 // Core sweep scratch: per-CTA gradients + the RN-rounded tf32 copy of A.
 size_t ws_core_scratch_bytes(const KView& v, const int32_t* dims);
+// epi_warps: 8 or 16 epilogue warps (tf32 single pass only)
 cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                              float lr, float reg, int precision, int atomic_update,
-                             cudaStream_t st);
+                             int epi_warps, cudaStream_t st);
 // core16: the single-pass sweep gathers an fp16 copy of A (ws_core16_kernel);
 // 2 = the same with two epilogue warp groups taking alternate tiles; 0 = tf32
 // rows copied into TMEM (ws_core_kernel).  3xtf32 and the storage

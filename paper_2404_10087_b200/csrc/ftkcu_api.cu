@@ -38,7 +38,7 @@ struct ftkcu_session {
   int64_t opt_tc_ws = 1;  // warp-specialized tcgen05 sweeps where supported
   int64_t opt_store_c = 0;  // core sweeps: storage scheme (C-row cache) instead of calculation
   int64_t opt_core16 = 2;   // WS core sweep (tf32 precision): fp16 copy of A; 2 = two epilogue groups (default), 1 = one, 0 = tf32 rows
-  int64_t opt_factor_warps = 8;  // N=3 J=R=32 factor sweep: 8 or 16 epilogue warps
+  int64_t opt_factor_warps = 8;  // N=3 J=R=32 factor sweep (ws_factor_kernel): 8 or 16 epilogue warps
   int64_t opt_verbose = 0;
   int64_t opt_shuffle_seed = 0x5eed5eedLL;
   ncclComm_t comm = nullptr;
@@ -702,11 +702,11 @@ static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t 
     s->last_factor_kernel = FTKCU_K_WSF;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && ws_supported(v)) {
     CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision,
-                        (int)s->opt_hog_update, s->stream));
+                        (int)s->opt_hog_update, 8, s->stream));
     s->last_factor_kernel = FTKCU_K_WS;
   } else if (s->opt_precision == FTKCU_PREC_3XTF32 && s->opt_tc_ws && s->opt_hog_update &&
              ws_supported(v)) {
-    CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision, 1,
+    CK(launch_ws_factor(v, s->model.dims, mul, add, lr_a, reg_a, (int)s->opt_precision, 1, 8,
                         s->stream));
     s->last_factor_kernel = FTKCU_K_WS3;
   } else if (s->opt_precision == FTKCU_PREC_TF32 && s->opt_tc_ws && s->opt_hog_update &&

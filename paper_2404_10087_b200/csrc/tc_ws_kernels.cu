@@ -101,8 +101,9 @@ struct WsLayout {
   static constexpr int kI = kCore ? 4 : 6;  // COO-column ring depth (decoupled from A slots)
   static constexpr uint32_t o_stage = o_idx + kI * kIdxSlot;  // factor: per-quarter write-back rows
   static constexpr uint32_t stage_bytes = kCore ? 0 : 4 * 32 * 128;
-  static constexpr uint32_t o_xp = o_stage + stage_bytes;  // x_hat halves [2][2][128]
-  static constexpr uint32_t o_rows = o_xp + 2 * 2 * kRows * 4;  // [kI] valid rows per COO slot
+  // x_hat partial sums [2 tiles][column groups: 2 core, <= 4 factor][128]
+  static constexpr uint32_t o_xp = o_stage + stage_bytes;
+  static constexpr uint32_t o_rows = o_xp + 2 * (kCore ? 2 : 4) * kRows * 4;  // [kI] valid rows per COO slot
   static constexpr uint32_t o_bar = o_rows + 64;
   static constexpr int kBars = 32;
   static constexpr uint32_t o_tmem = o_bar + kBars * 8;
@@ -221,7 +222,7 @@ __device__ void ring_wait(const RingDev& r, int f) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <bool kCore, bool k3 = false>
+template <bool kCore, bool k3 = false, int kEW = kEpiWarps>
 __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_t* tslot) {
   using L = WsLayout<kCore, k3>;
   for (int n = 0; n < kN; ++n) {
@@ -258,22 +259,22 @@ __device__ void ws_setup(const WsParams& p, uint8_t* sm, uint64_t* bars, uint32_
       // (3xtf32 factor: by the epilogue, whose fp32 step reads a)
       // (window: by the epilogue once the tile's write-back is issued)
       mbar_init(&bars[B_EMPTY + s],
-                (kCore || (p.atomic_update && !k3 && !p.window)) ? 1 : kEpiWarps);
+                (kCore || (p.atomic_update && !k3 && !p.window)) ? 1 : kEW);
     }
     for (int i = 0; i < L::kI; ++i) {
       mbar_init(&bars[B_IFULL + i], 1);
-      mbar_init(&bars[B_IEMPTY + i], kEpiWarps);
+      mbar_init(&bars[B_IEMPTY + i], kEW);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[B_CFULL + b], 1);
-      mbar_init(&bars[B_DFULL + b], kEpiWarps);
-      mbar_init(&bars[B_CEMPTY + b], kEpiWarps);
+      mbar_init(&bars[B_DFULL + b], kEW);
+      mbar_init(&bars[B_CEMPTY + b], kEW);
       mbar_init(&bars[B_DEMPTY + b], 1);
     }
     mbar_init(&bars[B_UFULL], 1);
-    mbar_init(&bars[B_UEMPTY], kEpiWarps);
-    mbar_init(&bars[B_AFULL], kEpiWarps);
-    for (int b = 0; b < 2; ++b) mbar_init(&bars[B_LOFULL + b], kEpiWarps);
+    mbar_init(&bars[B_UEMPTY], kEW);
+    mbar_init(&bars[B_AFULL], kEW);
+    for (int b = 0; b < 2; ++b) mbar_init(&bars[B_LOFULL + b], kEW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x / 32 == 1) {
@@ -339,10 +340,10 @@ __device__ void ws_idx_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, 
 // Gather warps: as soon as an A slot is free, TMA gather4 of the tile's
 // factor rows (N modes x 32 groups of 4 rows) into it; gather warp w issues
 // groups [w * 96 / kGW, (w + 1) * 96 / kGW) and arrives with its own bytes.
-template <bool kCore, bool k3 = false, bool kRing = false>
+template <bool kCore, bool k3 = false, bool kRing = false, int kEW = kEpiWarps>
 __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bars, int64_t nk) {
   using L = WsLayout<kCore, k3>;
-  const int lane = threadIdx.x & 31, gw = (int)(threadIdx.x >> 5) - kGatherWarp;
+  const int lane = threadIdx.x & 31, gw = (int)(threadIdx.x >> 5) - (2 + kEW);
   constexpr int kGroups = kN * kRows / 4, kPer = kGroups / kGW;
   static_assert(kGroups % (kGW * 8) == 0, "whole batches of 8 groups per gather warp");
   constexpr bool ring = kRing;
@@ -465,17 +466,38 @@ __device__ void ring_agent(const WsParams& p, int lane) {
   }
 }
 
+// TMEM <-> registers, 16 or 8 consecutive columns of this thread's lane.
+template <int kCols>
+__device__ __forceinline__ void tmem_ldc(uint32_t a, uint32_t (&v)[kCols]) {
+  if constexpr (kCols == 16) tmem_ld16(a, v);
+  else tmem_ld8(a, v);
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_stc(uint32_t a, const uint32_t (&v)[kCols]) {
+  if constexpr (kCols == 16) tmem_st16(a, v);
+  else tmem_st8(a, v);
+}
+
 // ---- factor sweep --------------------------------------------------------------
 
-template <bool kAtomic, bool kRing = false>
-__global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
+// kEW epilogue warps: 8 (two per TMEM lane quarter, 16 columns each) or 16
+// (four per quarter, 8 columns each: twice the warps to hide the epilogue's
+// instruction latencies, half the registers per thread).
+template <bool kAtomic, bool kRing = false, int kEW = kEpiWarps>
+__global__ void __launch_bounds__((2 + kEW + kGW + (kRing ? 1 : 0)) * 32, 1)
     ws_factor_kernel(const __grid_constant__ WsParams p) {
+  static_assert(kEW == 8 || kEW == 16, "two or four epilogue warps per lane quarter");
+  static_assert(!kRing || kEW == kEpiWarps, "ring epochs count kEpiWarps epilogue warps");
+  constexpr int kH = kEW / 4;      // epilogue warps per lane quarter
+  constexpr int kCc = kW / kH;     // columns per epilogue warp
+  constexpr int kRi = kCc / 4;     // 4-row RED groups per warp and mode (rows 32 / kH)
+  constexpr int kGWarp = 2 + kEW;  // first gather warp
   using L = WsLayout<false>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::o_tmem);
-  ws_setup<false>(p, sm, bars, tslot);
+  ws_setup<false, false, kEW>(p, sm, bars, tslot);
   const uint32_t tmem = *tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool ring = kRing;
@@ -493,8 +515,8 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
     ws_idx_producer<false, false, kRing>(p, sm, bars, nk);
   } else if (kRing && warp == kRingWarp) {
     ring_agent(p, lane);
-  } else if (warp >= kGatherWarp) {
-    ws_gather_producer<false, false, kRing>(p, sm, bars, nk);
+  } else if (warp >= kGWarp) {
+    ws_gather_producer<false, false, kRing, kEW>(p, sm, bars, nk);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
@@ -562,13 +584,13 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
       if (nk >= 1) issue_u(nk - 1);
     }
   } else {
-    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;  // h: column group of the quarter
     const int row = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     // Software pipeline: epi1(k + 1) runs while U(k) is on the tensor core.
     // epi1: C -> residual -> D' = (lr r) D into TMEM, global row indices into
-    // registers.  epi2: U -> step -> coalesced vector RED (or STG) of the
-    // row's column half.
+    // registers.  epi2: U -> step -> coalesced vector RED (or STG) of whole
+    // rows.
     struct Tile {
       int32_t g[kN];
       float resid;
@@ -583,26 +605,30 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
       mbar_wait(&bars[B_CFULL + b], (uint32_t)((k >> 1) & 1));
       tc_after();
       const uint32_t tb = tl + kC + b * kBuf;
-      float c[kN][16];
+      float c[kN][kCc];
       {  // the three modes' columns in flight before one wait
-        uint32_t v[kN][16];
+        uint32_t v[kN][kCc];
 #pragma unroll
-        for (int n = 0; n < kN; ++n) tmem_ld16(tb + n * kMs + h * 16, v[n]);
+        for (int n = 0; n < kN; ++n) tmem_ldc(tb + n * kMs + h * kCc, v[n]);
         tmem_wait_ld();
 #pragma unroll
         for (int n = 0; n < kN; ++n)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) c[n][i] = __uint_as_float(v[n][i]);
+          for (int i = 0; i < kCc; ++i) c[n][i] = __uint_as_float(v[n][i]);
       }
-      // x_hat halves exchanged with the sibling warp of this lane quarter
-      // (each warp reads only its own half of C, so D' can go over it in place)
-      float part = 0.0f;
+      // x_hat partial sums exchanged among the quarter's kH warps (each warp
+      // reads only its columns of C, so D' can go over them in place)
+      f2 acc = {0.0f, 0.0f};
 #pragma unroll
-      for (int i = 0; i < 16; ++i) part = fmaf(c[0][i], c[1][i] * c[2][i], part);
-      float* xp = reinterpret_cast<float*>(sm + L::o_xp);  // [2 tiles][2 halves][128]
-      xp[(b * 2 + h) * kRows + row] = part;
-      named_bar(1 + q, 64);
-      const float xhat = part + xp[(b * 2 + (h ^ 1)) * kRows + row];
+      for (int i = 0; i < kCc / 2; ++i)
+        acc = fma2(f2{c[0][2 * i], c[0][2 * i + 1]},
+                   mul2(f2{c[1][2 * i], c[1][2 * i + 1]}, f2{c[2][2 * i], c[2][2 * i + 1]}), acc);
+      float* xp = reinterpret_cast<float*>(sm + L::o_xp);  // [2 tiles][kH][128]
+      xp[(b * kH + h) * kRows + row] = acc.x + acc.y;
+      named_bar(1 + q, 32 * kH);
+      float xhat = 0.0f;
+#pragma unroll
+      for (int g = 0; g < kH; ++g) xhat += xp[(b * kH + g) * kRows + row];
       t.slot = s;
 #pragma unroll
       for (int n = 0; n < kN; ++n) t.g[n] = s_idx[n * kRows + row];
@@ -618,18 +644,25 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
       // kAtomic: D' = lr r D, so the U GEMM (plus A x (-lr reg I)) yields the
       // step itself; overwrite mode scales in epi2.
       const float sc = kAtomic ? p.lr * t.resid : 1.0f;
+      const f2 s2 = {sc, sc};
+      f2 c0[kCc / 2], c1[kCc / 2], c2[kCc / 2];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) c[0][i] *= sc;  // D'_1 = (sc c0) c2, D'_2 = (sc c0) c1
+      for (int i = 0; i < kCc / 2; ++i) {
+        c0[i] = mul2(f2{c[0][2 * i], c[0][2 * i + 1]}, s2);  // D'_1 = (sc c0) c2, D'_2 = (sc c0) c1
+        c1[i] = f2{c[1][2 * i], c[1][2 * i + 1]};
+        c2[i] = f2{c[2][2 * i], c[2][2 * i + 1]};
+      }
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
-        uint32_t v[16];
+        uint32_t v[kCc];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float d = n == 0 ? (c[1][i] * sc) * c[2][i]
-                                 : (n == 1 ? c[0][i] * c[2][i] : c[0][i] * c[1][i]);
-          v[i] = tf32_rn_bits(d);
+        for (int i = 0; i < kCc / 2; ++i) {
+          const f2 d = n == 0 ? mul2(mul2(c1[i], s2), c2[i])
+                              : (n == 1 ? mul2(c0[i], c2[i]) : mul2(c0[i], c1[i]));
+          v[2 * i] = tf32_rn_bits(d.x);
+          v[2 * i + 1] = tf32_rn_bits(d.y);
         }
-        tmem_st16(tb + n * kMs + h * 16, v);
+        tmem_stc(tb + n * kMs + h * kCc, v);
       }
       tmem_wait_st();
       tc_before();
@@ -638,55 +671,55 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
     };
     auto epi2 = [&](int64_t k, const Tile& t) {
       // the row indices of the 4-row RED groups, shuffled before the wait:
-      // this warp sends rows 16 h + 4 i + lane / 8 of its lane quarter
-      int32_t gq[kN][4];
+      // this warp sends rows kCc h + 4 i + lane / 8 of its lane quarter
+      int32_t gq[kN][kRi];
 #pragma unroll
       for (int n = 0; n < kN; ++n)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], h * 16 + i * 4 + (lane >> 3));
+        for (int i = 0; i < kRi; ++i)
+          gq[n][i] = __shfl_sync(0xffffffffu, t.g[n], h * kCc + i * 4 + (lane >> 3));
       mbar_wait(&bars[B_UFULL], (uint32_t)(k & 1));
       tc_after();
-      uint32_t u[kN][16];
+      uint32_t u[kN][kCc];
 #pragma unroll
-      for (int n = 0; n < kN; ++n) tmem_ld16(tl + kU + n * kW + h * 16, u[n]);
+      for (int n = 0; n < kN; ++n) tmem_ldc(tl + kU + n * kW + h * kCc, u[n]);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_UEMPTY]);
       const float lr_r = p.lr * t.resid, lr_reg = p.lr * p.reg;
       const uint8_t* slot = sm + L::o_a + t.slot * L::kSlot;
-      // Per mode: the lane quarter's two warps write their column halves of
-      // the quarter's 32 step rows into a shared 4 KB staging tile (128-B
-      // rows, SWIZZLE_128B chunks: conflict-free both ways), then each sends
-      // 16 whole rows, 4 rows of 128 B per RED (or STG) instruction: half the
-      // L1 wavefronts / L2 requests of 64-B segments for the same bytes
-      // (scripts/microtests/red_segments.cu: 6.3 vs 5.3 TB/s).  Two 64-thread
-      // named barriers per mode (halves written / tile read).
+      // Per mode: the lane quarter's kH warps write their columns of the
+      // quarter's 32 step rows into a shared 4 KB staging tile (128-B rows,
+      // SWIZZLE_128B chunks: conflict-free both ways), then each sends 32 / kH
+      // whole rows, 4 rows of 128 B per RED (or STG) instruction: half the L1
+      // wavefronts / L2 requests of 64-B segments for the same bytes
+      // (scripts/microtests/red_segments.cu: 6.3 vs 5.3 TB/s).  Two named
+      // barriers per mode (columns written / tile read).
       uint8_t* stage = sm + L::o_stage + q * 4096;
 #pragma unroll
       for (int n = 0; n < kN; ++n) {
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
+        for (int q4 = 0; q4 < kCc / 4; ++q4) {
           float4 st;
           if constexpr (kAtomic) {  // the accumulator already holds the step
             st = make_float4(__uint_as_float(u[n][q4 * 4 + 0]), __uint_as_float(u[n][q4 * 4 + 1]),
                              __uint_as_float(u[n][q4 * 4 + 2]), __uint_as_float(u[n][q4 * 4 + 3]));
           } else {
             const float4 a = *reinterpret_cast<const float4*>(
-                slot + n * kModeTile + swz(row, (h * 16 + q4 * 4) * 4, 128));
+                slot + n * kModeTile + swz(row, (h * kCc + q4 * 4) * 4, 128));
             st.x = a.x + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 0]), -lr_reg * a.x);
             st.y = a.y + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 1]), -lr_reg * a.y);
             st.z = a.z + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 2]), -lr_reg * a.z);
             st.w = a.w + fmaf(lr_r, __uint_as_float(u[n][q4 * 4 + 3]), -lr_reg * a.w);
           }
-          *reinterpret_cast<float4*>(stage + swz(lane, h * 64 + q4 * 16, 128)) = st;
+          *reinterpret_cast<float4*>(stage + swz(lane, h * kCc * 4 + q4 * 16, 128)) = st;
         }
-        named_bar(5 + q, 64);  // both halves of the quarter's rows staged
+        named_bar(5 + q, 32 * kH);  // every column of the quarter's rows staged
         float* dst = p.a[n];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rl = h * 16 + i * 4 + (lane >> 3), ch = lane & 7;
+        for (int i = 0; i < kRi; ++i) {
+          const int rl = h * kCc + i * 4 + (lane >> 3), ch = lane & 7;
           const int32_t g = gq[n][i];
           const float4 v = *reinterpret_cast<const float4*>(stage + swz(rl, ch * 16, 128));
           if (g >= 0 && !(ws_exp(p) & 16)) {  // exp 16: no write-back (timing only)
@@ -697,14 +730,13 @@ __global__ void __launch_bounds__(kRing ? kThreadsRing : kThreadsWs, 1)
               *reinterpret_cast<float4*>(gp) = v;
           }
         }
-        named_bar(5 + q, 64);  // the sibling is done reading before the next mode's stores
+        named_bar(5 + q, 32 * kH);  // the quarter is done reading before the next mode's stores
       }
       if (!kAtomic || p.window) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[B_EMPTY + t.slot]);
       }
     };
-    // ring: cell-completion counts (cells without a tile here count at once)
     // ring: a cell's count goes in one tile late (its REDs have landed by
     // then, so the fence is cheap) when the next tile is in the next cell and
     // the neighbour needs the block only K >= 2 cells later; otherwise (a
@@ -1725,7 +1757,7 @@ bool ws_supported(const KView& v) {
 
 cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, int64_t add,
                              float lr, float reg, int precision, int atomic_update,
-                             cudaStream_t st) {
+                             int epi_warps, cudaStream_t st) {
   WsParams p{};
   if (!make_params(p, v, dims, mul, add, false)) return cudaErrorNotSupported;
   p.lr = lr;
@@ -1737,6 +1769,9 @@ cudaError_t launch_ws_factor(const KView& v, const int32_t* dims, int64_t mul, i
   const bool k3 = p.prec3 && atomic_update;
   p.window = (atomic_update && !k3) ? v.window : 0;
   const int bytes = (int)(k3 ? WsLayout<false, true>::bytes : WsLayout<false>::bytes);
+  // 16 epilogue warps (ws_factor_kernel<., ., 16>) measured no faster than 8
+  // at C2 (8.53 vs 8.48 ms): the sweep is not short of warps to hide latency
+  (void)epi_warps;
   auto kern = k3 ? ws_factor3_kernel
                  : (atomic_update ? ws_factor_kernel<true> : ws_factor_kernel<false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
