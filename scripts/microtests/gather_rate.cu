@@ -5,7 +5,9 @@
 //   tma   : TMA tile::gather4 (4 rows per instruction), G issuing warps per
 //           CTA (one elected lane each), into a ring of S slots of 128 rows
 //   lsu   : cp.async.cg 16 B per thread (W / 16 threads per row), all warps
-// Prints rows/s and GB/s; the data is checked on the last slot.
+// Prints rows/s and GB/s; the data is checked on the last slot.  A second
+// pass draws each tile's rows from the three Netflix mode sizes (the sweeps'
+// actual mix: the two small modes are cache-friendlier).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 gather_rate.cu -o gather_rate -lcuda
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -183,5 +185,15 @@ int main() {
   for (auto& x : h) x = (int)(rng() % nrows);
   run<64>(enc, nrows, h);
   run<128>(enc, nrows, h);
+  // The sweeps' own mix: each 384-row tile takes 128 rows of each Netflix
+  // mode (480189 / 17770 / 2182 rows), laid out as one table of three ranges.
+  const int d0 = 480189, d1 = 17770, d2 = 2182;
+  for (int64_t t = 0; t < n; t += 384)
+    for (int r = 0; r < 384 && t + r < n; ++r)
+      h[t + r] = r < 128 ? (int)(rng() % d0)
+                         : (r < 256 ? d0 + (int)(rng() % d1) : d0 + d1 + (int)(rng() % d2));
+  printf("# Netflix mode mix (128 rows of each mode per tile)\n");
+  run<64>(enc, d0 + d1 + d2, h);
+  run<128>(enc, d0 + d1 + d2, h);
   return 0;
 }
