@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--dsgd", action="store_true",
                     help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-keys", default="packed", choices=["packed", "int32"],
+                    help="COO index format on the host-to-device link in the e2e loop")
     ap.add_argument("--e2e-sync", action="store_true",
                     help="e2e without the double-buffered asynchronous tensor upload")
     ap.add_argument("--no-cpu", action="store_true")
@@ -330,6 +332,11 @@ class SingleGpu:
 
     def upload_ptr_async(self, slot, idx_ptr, val_ptr):
         self.s.upload_tensor_ptr_async(slot, self.coo.dims, self.coo.nnz, idx_ptr, val_ptr)
+
+    def upload_packed_async(self, slot, keys, val_ptr):
+        lo, hi = keys
+        self.s.upload_tensor_packed_ptr_async(slot, self.coo.dims, self.coo.nnz, lo.data_ptr(),
+                                              None if hi is None else hi.data_ptr(), val_ptr)
 
     def host_arrays(self):
         return self.coo.idx, self.coo.vals
@@ -794,7 +801,29 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     from paper_2404_10087_b200 import host
 
     idx, vals = job.host_arrays()
-    idx_h = torch.from_numpy(np.ascontiguousarray(idx)).pin_memory()
+    pipelined = type(job) is SingleGpu and not args.e2e_sync
+    # packed-key COO on the link (ftkcu_pack_keys, built once like a file
+    # format; 12 instead of 16 bytes per nonzero), where the index widths fit
+    keys = None
+    if pipelined and args.e2e_keys == "packed":
+        try:
+            keys = job.s.pack_keys(job.coo.dims, idx)
+        except Exception:
+            keys = None
+    if keys is not None:
+        lo, hi = keys
+        key_h = (torch.from_numpy(lo.view(np.int32)).pin_memory(),
+                 None if hi is None else torch.from_numpy(hi.view(np.int16 if hi.itemsize == 2
+                                                                  else np.int32)).pin_memory())
+        key_bytes = lo.nbytes + (0 if hi is None else hi.nbytes)
+
+        def upload_async(sl, _idx_ptr, vptr):
+            job.upload_packed_async(sl, key_h, vptr)
+        idx_h = key_h[0]
+    else:
+        idx_h = torch.from_numpy(np.ascontiguousarray(idx)).pin_memory()
+        key_bytes = idx_h.numel() * idx_h.element_size()
+        upload_async = job.upload_ptr_async
     val_h = torch.from_numpy(np.ascontiguousarray(vals)).pin_memory()
     a_h = [torch.from_numpy(x.copy()).pin_memory() for x in a0]
     b_h = [torch.from_numpy(x.copy()).pin_memory() for x in b0]
@@ -802,16 +831,15 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     b_np = [x.numpy() for x in b_h]
     # Single GPU: double-buffered tensor slots 2 / 3, step k + 1's COO copy
     # (ftkcu_tensor_upload_async, copy stream) overlapping step k's epoch.
-    pipelined = type(job) is SingleGpu and not args.e2e_sync
     steps = max(1, args.steps if pipelined else min(args.steps, 3))
-    h2d = idx.nbytes + vals.nbytes + sum(x.nbytes for x in a_np + b_np)
+    h2d = key_bytes + vals.nbytes + sum(x.nbytes for x in a_np + b_np)
     d2h = sum(x.nbytes for x in a_np + b_np)
     s = job.s
     if pipelined:
         # untimed: allocate both slots' device buffers (COO, staging, tile
         # stream) once; every timed step still copies its whole COO again
         for sl in (2, 3):
-            job.upload_ptr_async(sl, idx_h.data_ptr(), val_h.data_ptr())
+            upload_async(sl, idx_h.data_ptr(), val_h.data_ptr())
             job.slot = sl
             job.factor(host.derive_seed(5, [sl]))
     torch.cuda.synchronize()
@@ -831,7 +859,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
             print(f"e2e {(time.perf_counter() - t0) * 1e3:8.2f} ms {what}", file=sys.stderr)
 
     if pipelined:
-        job.upload_ptr_async(2, idx_h.data_ptr(), val_h.data_ptr())
+        upload_async(2, idx_h.data_ptr(), val_h.data_ptr())
     for k in range(steps):
         if not pipelined:
             job.upload_ptr(idx_h.data_ptr(), val_h.data_ptr())
@@ -848,7 +876,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
             # enqueued after this step's epoch (whose launches must not wait
             # behind a 1.6 GB copy on the PCIe link); it waits only for the
             # last epoch that read its slot, so it overlaps this one
-            job.upload_ptr_async(2 + (k + 1) % 2, idx_h.data_ptr(), val_h.data_ptr())
+            upload_async(2 + (k + 1) % 2, idx_h.data_ptr(), val_h.data_ptr())
             mark("next upload enqueued")
         s.download_model(a_np, b_np)
         mark("model downloaded")
@@ -866,7 +894,11 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         dt = float(t.item())
     return {"value": job.job_nnz / dt, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps,
-            "path": ("ftkcu_tensor_upload_async into two alternating slots (step k+1's COO "
+            "keys": (f"packed ({key_bytes / job.coo.nnz:.0f} B/nnz, ftkcu_pack_keys; "
+                     f"{(key_bytes + vals.nbytes) / job.coo.nnz:.0f} B/nnz with the values)")
+                    if keys is not None else "int32 per mode (16 B/nnz with values)",
+            "path": (("ftkcu_tensor_upload_packed_async" if keys is not None else
+                      "ftkcu_tensor_upload_async") + " into two alternating slots (step k+1's COO "
                      "copy overlaps step k's epoch)" if pipelined else "ftkcu_tensor_upload")
                     + " + ftkcu_model_upload + factor/core phases + ftkcu_model_download, "
                       "pinned host buffers (per rank, max over ranks)"}

@@ -122,6 +122,24 @@ int ftkcu_tensor_upload(ftkcu_session* s, int slot, int order,
  * reference counterpart (engine addition for pipelined epochs). */
 int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
                               int64_t nnz, const int32_t* idx_rowmajor, const float* values);
+/* Packed-key COO for host-to-device streaming: nonzero e's mode-n index sits
+ * in bits [off_n, off_n + w_n) of its key, w_n = bit width of dims[n] - 1
+ * (at least 1), off_0 = 0, off_n = off_{n-1} + w_{n-1}; needs sum w_n <= 64.
+ * A key is stored as its low 32 bits (`lo`, uint32 per nonzero) and its high
+ * bits (`hi`: none if sum w_n <= 32, uint16 if <= 48, else uint32; see
+ * ftkcu_key_layout).  Netflix shape: 19 + 15 + 12 = 46 bits, 6 bytes per
+ * nonzero on the link (10 with the value) instead of 16.  ftkcu_pack_keys
+ * builds the keys on the host (once, e.g. when the tensor is loaded) and
+ * returns FTKCU_ERR_ARG if the widths do not fit or an index is out of
+ * range.  ftkcu_tensor_upload_packed_async is ftkcu_tensor_upload_async for
+ * packed keys (unpacked on the copy stream).  No reference counterpart
+ * (engine addition for pipelined epochs). */
+int ftkcu_key_layout(int order, const int32_t* dims, int* hi_bytes);
+int ftkcu_pack_keys(int order, const int32_t* dims, int64_t nnz, const int32_t* idx_rowmajor,
+                    uint32_t* lo, void* hi);
+int ftkcu_tensor_upload_packed_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                                     int64_t nnz, const uint32_t* lo, const void* hi,
+                                     const float* values);
 int ftkcu_tensor_release(ftkcu_session* s, int slot);
 int64_t ftkcu_tensor_nnz(ftkcu_session* s, int slot);
 

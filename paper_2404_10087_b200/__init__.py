@@ -46,7 +46,8 @@ EXPORTS = (
     "ftkcu_fasttucker_core", "ftkcu_ccache_upload", "ftkcu_ccache_download",
     "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core", "ftkcu_writeback_ceiling",
     "ftkcu_ring_export", "ftkcu_ring_connect", "ftkcu_ring_emulate", "ftkcu_ring_factor_epoch",
-    "ftkcu_ring_status", "ftkcu_ring_debug",
+    "ftkcu_ring_status", "ftkcu_ring_debug", "ftkcu_key_layout", "ftkcu_pack_keys",
+    "ftkcu_tensor_upload_packed_async",
 )
 
 
@@ -124,6 +125,12 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_ring_factor_epoch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _i64p, _i64p,
                                           C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
     L.ftkcu_ring_status.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+    L.ftkcu_key_layout.argtypes = [C.c_int, _i32p, C.POINTER(C.c_int)]
+    L.ftkcu_pack_keys.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, C.POINTER(C.c_uint32),
+                                  C.c_void_p]
+    L.ftkcu_tensor_upload_packed_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p,
+                                                   C.c_int64, C.POINTER(C.c_uint32), C.c_void_p,
+                                                   _f32p]
     L.ftkcu_ring_debug.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                    C.c_int]
     _lib = L
@@ -217,6 +224,35 @@ class Session:
         self._ck(self.lib.ftkcu_tensor_upload_async(self.h, slot, dims.shape[0],
                                                     _p(dims, _i32p), nnz, C.cast(idx_ptr, _i32p),
                                                     C.cast(vals_ptr, _f32p)))
+
+    @staticmethod
+    def pack_keys(dims, idx):
+        """Packed-key COO (ftkcu_pack_keys): every mode's index in one bit
+        field per nonzero, as (lo uint32 array, hi uint16/uint32 array or
+        None); 10 bytes per nonzero with the values at the Netflix shape
+        instead of 16 on the host-to-device link."""
+        L = load_library()
+        dims = np.ascontiguousarray(dims, np.int32)
+        idx = np.ascontiguousarray(idx, np.int32)
+        hb = C.c_int(0)
+        if L.ftkcu_key_layout(dims.shape[0], _p(dims, _i32p), C.byref(hb)) != 0:
+            raise FtkError(L.ftkcu_last_error(None).decode())
+        lo = np.empty(idx.shape[0], np.uint32)
+        hi = np.empty(idx.shape[0], {2: np.uint16, 4: np.uint32}[hb.value]) if hb.value else None
+        rc = L.ftkcu_pack_keys(dims.shape[0], _p(dims, _i32p), idx.shape[0], _p(idx, _i32p),
+                               lo.ctypes.data_as(C.POINTER(C.c_uint32)),
+                               None if hi is None else hi.ctypes.data)
+        if rc != 0:
+            raise FtkError(L.ftkcu_last_error(None).decode())
+        return lo, hi
+
+    def upload_tensor_packed_ptr_async(self, slot, dims, nnz, lo_ptr: int, hi_ptr, vals_ptr: int):
+        """ftkcu_tensor_upload_packed_async from pinned host pointers
+        (hi_ptr None when the keys have no high part)."""
+        dims = np.ascontiguousarray(dims, np.int32)
+        self._ck(self.lib.ftkcu_tensor_upload_packed_async(
+            self.h, slot, dims.shape[0], _p(dims, _i32p), nnz,
+            C.cast(lo_ptr, C.POINTER(C.c_uint32)), hi_ptr, C.cast(vals_ptr, _f32p)))
 
     def release_tensor(self, slot):
         self._ck(self.lib.ftkcu_tensor_release(self.h, slot))

@@ -44,6 +44,10 @@ struct DevTensor {
   std::vector<int64_t> cell_tile;
   int64_t stream_tiles = 0;
   int64_t stream_cap = 0;            // allocated tiles
+  // order 3: storage-order records (i0, i1, i2, value) of 16 B, so the
+  // shuffle gathers one aligned record per nonzero instead of four words
+  int4* rec16 = nullptr;
+  int64_t rec16_cap = 0;
   // Asynchronous upload (ftkcu_tensor_upload_async): AoS staging on the
   // copy stream, completion event, index-range flag checked at first use.
   int32_t* staging = nullptr;

@@ -161,6 +161,7 @@ void free_tensor(DevTensor& t) {
   if (t.svals) cudaFree(t.svals);
   if (t.tile_rows) cudaFree(t.tile_rows);
   if (t.staging) cudaFree(t.staging);
+  if (t.rec16) cudaFree(t.rec16);
   if (t.d_bad) cudaFree(t.d_bad);
   if (t.ready) cudaEventDestroy(t.ready);
   if (t.used) cudaEventDestroy(t.used);
@@ -191,6 +192,30 @@ __global__ void aos_to_soa_kernel(const int32_t* __restrict__ aos, int64_t nnz, 
     for (int n = 0; n < v.order; ++n) {
       const int32_t x = aos[e * v.order + n];
       if (x < 0 || x >= v.dims[n]) atomicExch(bad, 1);
+      v.col[n][e] = x;
+    }
+  }
+}
+
+// Packed keys (ftkcu_pack_keys layout) -> SoA columns, with the range check.
+struct KeyLayout {
+  int order;
+  int hi_bytes;  // 0, 2 or 4
+  int off[kMaxOrder];
+  uint64_t mask[kMaxOrder];
+};
+__global__ void keys_to_soa_kernel(const uint32_t* __restrict__ lo, const void* __restrict__ hi,
+                                   int64_t nnz, SoAView v, KeyLayout kl, int* __restrict__ bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = __ldcs(lo + e);
+    if (kl.hi_bytes == 2)
+      k |= (uint64_t)__ldcs(static_cast<const uint16_t*>(hi) + e) << 32;
+    else if (kl.hi_bytes == 4)
+      k |= (uint64_t)__ldcs(static_cast<const uint32_t*>(hi) + e) << 32;
+    for (int n = 0; n < kl.order; ++n) {
+      const int32_t x = (int32_t)((k >> kl.off[n]) & kl.mask[n]);
+      if (x >= v.dims[n]) atomicExch(bad, 1);
       v.col[n][e] = x;
     }
   }
@@ -609,6 +634,124 @@ int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32
   CK(cudaGetLastError());
   // the tile stream is built lazily on the session stream (prepare_stream), so
   // the copy stream is free for the next upload as soon as this one is checked
+  CK(cudaEventRecord(t.ready, s->copy_stream));
+  t.pending = true;
+  return FTKCU_OK;
+}
+
+// Bit layout of packed keys: w_n = bit width of dims[n] - 1 (>= 1).
+static bool key_layout(int order, const int32_t* dims, KeyLayout* kl) {
+  int off = 0;
+  kl->order = order;
+  for (int n = 0; n < order; ++n) {
+    int w = 1;
+    while (w < 31 && (int64_t)(dims[n] - 1) >= ((int64_t)1 << w)) ++w;
+    kl->off[n] = off;
+    kl->mask[n] = (1ull << w) - 1;
+    off += w;
+  }
+  kl->hi_bytes = off <= 32 ? 0 : (off <= 48 ? 2 : 4);
+  return off <= 64;
+}
+
+int ftkcu_key_layout(int order, const int32_t* dims, int* hi_bytes) {
+  if (order < 1 || order > kMaxOrder || !dims || !hi_bytes)
+    return fail(nullptr, FTKCU_ERR_ARG, "bad key_layout arguments");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(nullptr, FTKCU_ERR_ARG, "dims must be positive");
+  KeyLayout kl;
+  if (!key_layout(order, dims, &kl)) return fail(nullptr, FTKCU_ERR_ARG, "index widths exceed 64 bits");
+  *hi_bytes = kl.hi_bytes;
+  return FTKCU_OK;
+}
+
+int ftkcu_pack_keys(int order, const int32_t* dims, int64_t nnz, const int32_t* idx_rowmajor,
+                    uint32_t* lo, void* hi) {
+  if (order < 1 || order > kMaxOrder || nnz < 0 || !dims || (nnz && (!idx_rowmajor || !lo)))
+    return fail(nullptr, FTKCU_ERR_ARG, "bad pack_keys arguments");
+  KeyLayout kl;
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(nullptr, FTKCU_ERR_ARG, "dims must be positive");
+  if (!key_layout(order, dims, &kl))
+    return fail(nullptr, FTKCU_ERR_ARG, "index widths exceed 64 bits");
+  if (kl.hi_bytes && nnz && !hi) return fail(nullptr, FTKCU_ERR_ARG, "keys need a high part");
+  int bad = 0;
+  for (int64_t e = 0; e < nnz; ++e) {
+    uint64_t k = 0;
+    for (int n = 0; n < order; ++n) {
+      const int32_t x = idx_rowmajor[e * order + n];
+      bad |= (x < 0 || x >= dims[n]);
+      k |= (uint64_t)(uint32_t)x << kl.off[n];
+    }
+    lo[e] = (uint32_t)k;
+    if (kl.hi_bytes == 2) static_cast<uint16_t*>(hi)[e] = (uint16_t)(k >> 32);
+    else if (kl.hi_bytes == 4) static_cast<uint32_t*>(hi)[e] = (uint32_t)(k >> 32);
+  }
+  if (bad) return fail(nullptr, FTKCU_ERR_ARG, "index out of range");
+  return FTKCU_OK;
+}
+
+int ftkcu_tensor_upload_packed_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                                     int64_t nnz, const uint32_t* lo, const void* hi,
+                                     const float* values) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (order < 1 || order > kMaxOrder)
+    return fail(s, FTKCU_ERR_ARG, "order %d unsupported (1..%d)", order, kMaxOrder);
+  if (nnz < 1 || !lo || !values)
+    return fail(s, FTKCU_ERR_ARG, "asynchronous upload needs a non-empty tensor");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
+  KeyLayout kl;
+  if (!key_layout(order, dims, &kl)) return fail(s, FTKCU_ERR_ARG, "index widths exceed 64 bits");
+  if (kl.hi_bytes && !hi) return fail(s, FTKCU_ERR_ARG, "keys need a high part");
+  DevTensor& t = s->slots[slot];
+  if ((rc = finish_upload(s, t))) return rc;
+  // ordering against the slot's readers: as ftkcu_tensor_upload_async
+  if (slot == s->last_slot || (t.used_rec && !t.used)) {
+    CK(cudaEventRecord(s->ev1, s->stream));
+    CK(cudaStreamWaitEvent(s->copy_stream, s->ev1, 0));
+  } else if (t.used_rec) {
+    CK(cudaStreamWaitEvent(s->copy_stream, t.used, 0));
+  }
+  if (!(t.vals && t.order == order && t.nnz == nnz)) {
+    CK(cudaStreamSynchronize(s->stream));
+    free_tensor(t);
+    t.order = order;
+    t.nnz = nnz;
+    for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * (size_t)nnz));
+    CK(cudaMalloc(&t.vals, sizeof(float) * (size_t)nnz));
+  }
+  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
+  t.cell_off.clear();
+  t.cell_tile.clear();
+  t.shuffled = false;
+  t.stream_tiles = 0;
+  const size_t lb = sizeof(uint32_t) * (size_t)nnz, hb = (size_t)kl.hi_bytes * nnz;
+  const size_t kb = lb + (hb + 15) / 16 * 16;
+  if (t.staging_cap < kb) {
+    if (t.staging) CK(cudaFree(t.staging));
+    t.staging = nullptr;
+    CK(cudaMalloc(&t.staging, kb));
+    t.staging_cap = kb;
+  }
+  if (!t.d_bad) CK(cudaMalloc(&t.d_bad, sizeof(int)));
+  if (!t.ready) CK(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+  uint8_t* st = reinterpret_cast<uint8_t*>(t.staging);
+  CK(cudaMemcpyAsync(st, lo, lb, cudaMemcpyHostToDevice, s->copy_stream));
+  if (hb) CK(cudaMemcpyAsync(st + lb, hi, hb, cudaMemcpyHostToDevice, s->copy_stream));
+  CK(cudaMemcpyAsync(t.vals, values, sizeof(float) * nnz, cudaMemcpyHostToDevice, s->copy_stream));
+  CK(cudaMemsetAsync(t.d_bad, 0, sizeof(int), s->copy_stream));
+  SoAView v{};
+  v.order = order;
+  for (int n = 0; n < order; ++n) {
+    v.dims[n] = dims[n];
+    v.col[n] = t.idx[n];
+  }
+  keys_to_soa_kernel<<<num_sms() * 8, 256, 0, s->copy_stream>>>(
+      reinterpret_cast<const uint32_t*>(st), st + lb, nnz, v, kl, t.d_bad);
+  CK(cudaGetLastError());
   CK(cudaEventRecord(t.ready, s->copy_stream));
   t.pending = true;
   return FTKCU_OK;

@@ -72,6 +72,28 @@ __global__ void shuffle_kernel(ShuffleView v, const int64_t* __restrict__ perm,
   }
 }
 
+// Order 3: the storage-order columns as 16-B records, then one random
+// aligned 16-B gather per nonzero (one sector instead of four).
+__global__ void pack16_kernel(const int32_t* __restrict__ i0, const int32_t* __restrict__ i1,
+                              const int32_t* __restrict__ i2, const float* __restrict__ vals,
+                              int4* __restrict__ rec, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    rec[k] = make_int4(__ldcs(i0 + k), __ldcs(i1 + k), __ldcs(i2 + k), __float_as_int(__ldcs(vals + k)));
+}
+__global__ void shuffle16_kernel(const int4* __restrict__ rec, ShuffleView v,
+                                 const int64_t* __restrict__ perm, int bits, uint64_t seed) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < v.nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = perm ? perm[k] : feistel_perm(k, v.nnz, bits, seed);
+    const int4 r = __ldg(rec + p);
+    v.dst_idx[0][k] = r.x;
+    v.dst_idx[1][k] = r.y;
+    v.dst_idx[2][k] = r.z;
+    v.dst_vals[k] = __int_as_float(r.w);
+  }
+}
+
 // ---- shared-memory layout of the sweep kernels --------------------------------
 
 struct HogLayout {
@@ -399,6 +421,13 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     if (e != cudaSuccess) return e;
     t.stream_cap = tiles;
   }
+  if (t.order == 3 && t.rec16_cap < t.nnz) {
+    if (t.rec16) cudaFree(t.rec16);
+    t.rec16 = nullptr;
+    e = cudaMalloc(&t.rec16, sizeof(int4) * (size_t)t.nnz);
+    if (e != cudaSuccess) return e;
+    t.rec16_cap = t.nnz;
+  }
   for (int n = 0; n < t.order; ++n) {
     e = cudaMemsetAsync(t.sidx[n], 0, sizeof(int32_t) * kHogTile * tiles, st);
     if (e != cudaSuccess) return e;
@@ -427,8 +456,16 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     while ((1ll << bits) < n) bits += 2;
     int64_t blocks = (n + 255) / 256;
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    shuffle_kernel<<<(int)blocks, 256, 0, st>>>(v, d_perm, bits,
-                                                 seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1)));
+    const uint64_t cseed = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1));
+    if (t.order == 3) {
+      pack16_kernel<<<(int)blocks, 256, 0, st>>>(v.src_idx[0], v.src_idx[1], v.src_idx[2],
+                                                  v.src_vals, t.rec16 + off[c], n);
+      shuffle16_kernel<<<(int)blocks, 256, 0, st>>>(t.rec16 + off[c], v,
+                                                     d_perm,
+                                                     bits, cseed);
+    } else {
+      shuffle_kernel<<<(int)blocks, 256, 0, st>>>(v, d_perm, bits, cseed);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -87,3 +87,38 @@ def test_async_upload_into_idle_slot_while_other_slot_runs(session):
     for n in range(3):
         assert np.array_equal(out[0][0][n], out[1][0][n])
         assert np.array_equal(out[0][1][n], out[1][1][n])
+
+
+def test_packed_key_upload_epoch_bit_identical(session):
+    """ftkcu_tensor_upload_packed_async (the e2e link format, 12 B per
+    nonzero): the device tensor equals the int32 upload's, so a deterministic
+    epoch is bit-identical; a key whose field exceeds its mode's extent is
+    reported at the slot's first use."""
+    t, ranks, r, a, b = _problem()
+    plan1 = host.global_plan(t.nnz, 16, 3)
+    plan2 = host.global_plan(t.nnz, 16, 4)
+    out = []
+    for packed in (False, True):
+        session.upload_model(t.dims, ranks, r, a, b)
+        if packed:
+            lo, hi = eng.Session.pack_keys(t.dims, t.idx)
+            assert hi is None  # 6 + 6 + 5 bits
+            kh, vh = _pinned(lo.view(np.int32)), _pinned(t.vals)
+            session.upload_tensor_packed_ptr_async(2, t.dims, t.nnz, kh.data_ptr(), None,
+                                                   vh.data_ptr())
+        else:
+            session.upload_tensor(2, t.dims, t.idx, t.vals)
+        session.factor_phase(2, plan1, 16, 1e-3, 1e-4, DET)
+        session.core_phase(2, plan2, 16, 1e-3, 1e-4, DET)
+        out.append(session.download_model())
+        session.release_tensor(2)
+    for n in range(3):
+        assert np.array_equal(out[0][0][n], out[1][0][n])
+        assert np.array_equal(out[0][1][n], out[1][1][n])
+    # mode 1 has 40 rows (6-bit field): 63 fits the field, not the extent
+    lo, _ = eng.Session.pack_keys(t.dims, t.idx)
+    lo[5] |= np.uint32(63) << np.uint32(6)
+    kh, vh = _pinned(lo.view(np.int32)), _pinned(t.vals)
+    session.upload_tensor_packed_ptr_async(3, t.dims, t.nnz, kh.data_ptr(), None, vh.data_ptr())
+    with pytest.raises(eng.FtkError, match="out of range"):
+        session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
