@@ -149,6 +149,11 @@ int ftkcu_model_upload(ftkcu_session* s, int order, const int32_t* dims,
                        const int32_t* ranks, int32_t R,
                        const float* const* A, const float* const* B);
 int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B);
+/* The same copies enqueued on the session stream without a host
+ * synchronisation (to_device = 1: upload into the resident model of the same
+ * shape; 0: download).  Host buffers must be pinned and stay valid until the
+ * stream passes the copy (ftkcu_stream_sync).  No reference counterpart. */
+int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, float* const* B);
 
 /* ---- the hot path ------------------------------------------------------ */
 

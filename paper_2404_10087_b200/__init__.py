@@ -47,7 +47,7 @@ EXPORTS = (
     "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core", "ftkcu_writeback_ceiling",
     "ftkcu_ring_export", "ftkcu_ring_connect", "ftkcu_ring_emulate", "ftkcu_ring_factor_epoch",
     "ftkcu_ring_status", "ftkcu_ring_debug", "ftkcu_key_layout", "ftkcu_pack_keys",
-    "ftkcu_tensor_upload_packed_async",
+    "ftkcu_tensor_upload_packed_async", "ftkcu_model_copy_async",
 )
 
 
@@ -126,6 +126,7 @@ def load_library(path: str = LIB_PATH):
                                           C.POINTER(C.c_uint64), C.c_float, C.c_float, _f64p]
     L.ftkcu_ring_status.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
     L.ftkcu_key_layout.argtypes = [C.c_int, _i32p, C.POINTER(C.c_int)]
+    L.ftkcu_model_copy_async.argtypes = [C.c_void_p, C.c_int, _fpp, _fpp]
     L.ftkcu_pack_keys.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, C.POINTER(C.c_uint32),
                                   C.c_void_p]
     L.ftkcu_tensor_upload_packed_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p,
@@ -253,6 +254,13 @@ class Session:
         self._ck(self.lib.ftkcu_tensor_upload_packed_async(
             self.h, slot, dims.shape[0], _p(dims, _i32p), nnz,
             C.cast(lo_ptr, C.POINTER(C.c_uint32)), hi_ptr, C.cast(vals_ptr, _f32p)))
+
+    def model_copy_async(self, to_device: bool, a, b):
+        """Enqueued model upload (to_device) or download into pinned numpy
+        views a[n], b[n]; completes in stream order (sync() waits)."""
+        ap = (_f32p * len(a))(*[x.ctypes.data_as(_f32p) for x in a])
+        bp = (_f32p * len(b))(*[x.ctypes.data_as(_f32p) for x in b])
+        self._ck(self.lib.ftkcu_model_copy_async(self.h, 1 if to_device else 0, ap, bp))
 
     def release_tensor(self, slot):
         self._ck(self.lib.ftkcu_tensor_release(self.h, slot))

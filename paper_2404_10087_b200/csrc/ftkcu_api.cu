@@ -833,6 +833,28 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
   return FTKCU_OK;
 }
 
+// Enqueued model copies (pinned host buffers; no host synchronisation): the
+// e2e loop's per-step model transfers stay in stream order without a host
+// round trip between epochs.
+int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, float* const* B) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
+  const DevModel& m = s->model;
+  const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  for (int n = 0; n < m.order; ++n) {
+    const size_t an = sizeof(float) * (size_t)m.dims[n] * m.ranks[n];
+    const size_t bn = sizeof(float) * (size_t)m.ranks[n] * m.r;
+    if (A && A[n]) CK(cudaMemcpyAsync(to_device ? (void*)m.a[n] : (void*)A[n],
+                                      to_device ? (const void*)A[n] : (const void*)m.a[n], an,
+                                      kind, s->stream));
+    if (B && B[n]) CK(cudaMemcpyAsync(to_device ? (void*)m.b[n] : (void*)B[n],
+                                      to_device ? (const void*)B[n] : (const void*)m.b[n], bn,
+                                      kind, s->stream));
+  }
+  return FTKCU_OK;
+}
+
 // Hogwild factor sweep over v's tile range: WS tcgen05 -> tcgen05 -> FFMA.
 static int launch_factor(ftkcu_session* s, const KView& v, int64_t mul, int64_t add,
                          float lr_a, float reg_a) {

@@ -428,12 +428,20 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     if (e != cudaSuccess) return e;
     t.rec16_cap = t.nnz;
   }
-  for (int n = 0; n < t.order; ++n) {
-    e = cudaMemsetAsync(t.sidx[n], 0, sizeof(int32_t) * kHogTile * tiles, st);
-    if (e != cudaSuccess) return e;
+  for (int c = 0; c < ncell; ++c) {
+    // the shuffle writes every valid entry: zero only the cell's padding
+    // (index 0, value 0) instead of the whole stream
+    const int64_t used = off[c + 1] - off[c], pad = (ctile[c + 1] - ctile[c]) * kHogTile - used;
+    if (pad > 0) {
+      const size_t p0 = (size_t)ctile[c] * kHogTile + used;
+      for (int n = 0; n < t.order; ++n) {
+        e = cudaMemsetAsync(t.sidx[n] + p0, 0, sizeof(int32_t) * pad, st);
+        if (e != cudaSuccess) return e;
+      }
+      e = cudaMemsetAsync(t.svals + p0, 0, sizeof(float) * pad, st);
+      if (e != cudaSuccess) return e;
+    }
   }
-  e = cudaMemsetAsync(t.svals, 0, sizeof(float) * kHogTile * tiles, st);
-  if (e != cudaSuccess) return e;
   for (int c = 0; c < ncell; ++c) {
     const int64_t n = off[c + 1] - off[c];
     if (n == 0) continue;
