@@ -518,7 +518,11 @@ __global__ void __launch_bounds__((2 + kEW + kGW + (kRing ? 1 : 0)) * 32, 1)
   } else if (warp >= kGWarp) {
     ws_gather_producer<false, false, kRing, kEW>(p, sm, bars, nk);
   } else if (warp == 1) {
-    if (lane == 0) {
+    // The whole warp runs the MMA loop (barrier waits converged) and one
+    // elected lane issues each GEMM: issued from a lane-0-only branch, ptxas
+    // wrapped every tcgen05.mma in its own ELECT / PLOP3 / BRA loop, ~50
+    // dependent cycles per MMA that kept this warp ~93% busy (36 per tile).
+    {
       constexpr uint32_t id = idesc_tf32(128, kW, 0, 0);
       // atomic rows: N = 64, [C | A] = A [B | I]
       constexpr uint32_t idc = idesc_tf32(128, kAtomic ? 2 * kW : kW, 0, 0);
@@ -532,19 +536,23 @@ __global__ void __launch_bounds__((2 + kEW + kGW + (kRing ? 1 : 0)) * 32, 1)
         mbar_wait(&bars[B_UEMPTY], (uint32_t)((j & 1) ^ 1));
         tc_after();
         const uint32_t tb = tmem + kC + b * kBuf;
+        if (elect_one()) {
 #pragma unroll
-        for (int n = 0; n < kN; ++n) {
-#pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ts(tmem + kU + n * kW, tb + n * kMs + ks * 8,
-                   sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
-          if constexpr (kAtomic)
+          for (int n = 0; n < kN; ++n) {
 #pragma unroll
             for (int ks = 0; ks < kW / 8; ++ks)
-              mma_ts(tmem + kU + n * kW, tb + n * kMs + kW + ks * 8,
-                     sdesc(dg + ks * 32, 16, 1024, 128), id, 1);
+              mma_ts(tmem + kU + n * kW, tb + n * kMs + ks * 8,
+                     sdesc(bb + n * 4096 + ks * 32, 16, 1024, 128), id, ks > 0);
+            if constexpr (kAtomic)
+              if (!(ws_exp(p) & 256))  // exp 256: no regulariser GEMM (timing only)
+#pragma unroll
+                for (int ks = 0; ks < kW / 8; ++ks)
+                  mma_ts(tmem + kU + n * kW, tb + n * kMs + kW + ks * 8,
+                         sdesc(dg + ks * 32, 16, 1024, 128), id, 1);
+          }
+          mma_commit(&bars[B_UFULL]);
         }
-        mma_commit(&bars[B_UFULL]);
+        __syncwarp();
       };
       // ring: at a cell boundary U(k - 1) goes out BEFORE the wait for tile
       // k's rows, so a cell's write-back (and the block posts behind it)
@@ -566,19 +574,23 @@ __global__ void __launch_bounds__((2 + kEW + kGW + (kRing ? 1 : 0)) * 32, 1)
         // C(k) overwrites buffer b, whose D'(k - 2) is U(k - 2)'s A operand:
         // issue it once U(k - 2) has completed (PTX orders MMAs only per
         // accumulator; U(k - 1) is not issued yet, so the phase is exact)
-        if (k >= 2 && !early_u) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
+        // (exp 512: no wait -- timing only, corrupts D')
+        if (k >= 2 && !early_u && !(ws_exp(p) & 512)) mbar_wait(&bars[B_UFULL], (uint32_t)((k - 2) & 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+        if (elect_one()) {
 #pragma unroll
-        for (int n = 0; n < kN; ++n)
+          for (int n = 0; n < kN; ++n)
 #pragma unroll
-          for (int ks = 0; ks < kW / 8; ++ks)
-            mma_ss(tmem + kC + b * kBuf + n * kMs,
-                   sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
-                   sdesc(bt + n * 8192 + ks * 32, 16, 1024, 128), idc, ks > 0);
-        mma_commit(&bars[B_CFULL + b]);
-        // the only read of the A slot (window: held until the write-back)
-        if (kAtomic && !p.window) mma_commit(&bars[B_EMPTY + s]);
+            for (int ks = 0; ks < kW / 8; ++ks)
+              mma_ss(tmem + kC + b * kBuf + n * kMs,
+                     sdesc(a0 + n * kModeTile + ks * 32, 16, 1024, 128),
+                     sdesc(bt + n * 8192 + ks * 32, 16, 1024, 128), idc, ks > 0);
+          mma_commit(&bars[B_CFULL + b]);
+          // the only read of the A slot (window: held until the write-back)
+          if (kAtomic && !p.window) mma_commit(&bars[B_EMPTY + s]);
+        }
+        __syncwarp();
         if (k >= 1 && !early_u) issue_u(k - 1);
       }
       if (nk >= 1) issue_u(nk - 1);
@@ -1479,7 +1491,7 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
       __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; one elected lane issues each GEMM (see ws_factor_kernel)
       constexpr uint32_t idc = idesc_f16(128, kW, 0, 0);
       constexpr uint32_t idg = idesc_f16(128, kN * kW, 1, 1);
       const uint32_t bt = smem_u32(sm + L::o_bt), d0 = smem_u32(sm + L::o_d);
@@ -1490,13 +1502,17 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         // G[j'][n R + r] += sum_t A[t][j'] (r D_n)[t][r]: M = 3 stacked modes
         // (+ one garbage block), N = 96, K = 16 nonzeros per instruction
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot), dd = d0 + db * L::kSlot;
-        if (!(ws_exp(p) & 4))  // exp 4: no G GEMM (timing only)
+        if (elect_one()) {
+          if (!(ws_exp(p) & 4))  // exp 4: no G GEMM (timing only)
 #pragma unroll
-          for (int ks = 0; ks < kRows / 16; ++ks)
-            mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
-                    sdesc_l(dd + ks * 1024, kModeTile16, 512, 4), idg, (k > 0 || ks > 0) ? 1u : 0u);
-        mma_commit(&bars[H_DEMPTY + db]);
-        mma_commit(&bars[H_EMPTY + s]);
+            for (int ks = 0; ks < kRows / 16; ++ks)
+              mma_f16(tmem + kG, sdesc_l(a0 + ks * 1024, kModeTile16, 512, 4),
+                      sdesc_l(dd + ks * 1024, kModeTile16, 512, 4), idg,
+                      (k > 0 || ks > 0) ? 1u : 0u);
+          mma_commit(&bars[H_DEMPTY + db]);
+          mma_commit(&bars[H_EMPTY + s]);
+        }
+        __syncwarp();
       };
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % L::kS), b = (int)(k % kCB);
@@ -1504,17 +1520,24 @@ __global__ void __launch_bounds__((2 + kEG * kEpiWarps + kGW) * 32, 1)
         mbar_wait(&bars[H_CEMPTY + b], (uint32_t)(((k / kCB) & 1) ^ 1));
         tc_after();
         const uint32_t a0 = smem_u32(sm + L::o_a + s * L::kSlot);
+        if (elect_one()) {
 #pragma unroll
-        for (int n = 0; n < kN; ++n)
+          for (int n = 0; n < kN; ++n)
 #pragma unroll
-          for (int ks = 0; ks < kW / 16; ++ks)
-            mma_f16(tmem + b * 96 + n * kW, sdesc_l(a0 + n * kModeTile16 + ks * 32, 16, 512, 4),
-                    sdesc_l(bt + n * 2048 + ks * 32, 16, 512, 4), idc, ks > 0);
-        mma_commit(&bars[H_CFULL + b]);
+            for (int ks = 0; ks < kW / 16; ++ks)
+              mma_f16(tmem + b * 96 + n * kW,
+                      sdesc_l(a0 + n * kModeTile16 + ks * 32, 16, 512, 4),
+                      sdesc_l(bt + n * 2048 + ks * 32, 16, 512, 4), idc, ks > 0);
+          mma_commit(&bars[H_CFULL + b]);
+        }
+        __syncwarp();
         if (k >= 1) issue_g(k - 1);
       }
       if (nk >= 1) issue_g(nk - 1);
-      mma_commit(&bars[H_GDONE]);  // after every G GEMM (tcgen05.commit tracks all prior MMAs)
+      // after every G GEMM: tcgen05.commit tracks all prior MMAs of the thread,
+      // and elect.sync picks the same lane every time (the lowest active one)
+      if (elect_one()) mma_commit(&bars[H_GDONE]);
+      __syncwarp();
     }
   } else {
     const int ew = warp - 2, q = warp & 3, eg = ew / kEpiWarps, h = (ew >> 2) & 1;
