@@ -66,6 +66,10 @@ def parse():
     ap.add_argument("--dsgd", action="store_true",
                     help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="strata", choices=["strata", "ring"],
+                    help="DSGD factor schedule (ring: mode-3 blocks passed over peer memory "
+                         "inside one persistent kernel; 1 GPU emulates rank 0)")
+    ap.add_argument("--tokens", type=int, default=1, help="ring: mode-3 blocks per rank")
     ap.add_argument("--e2e-keys", default="packed", choices=["packed", "int32"],
                     help="COO index format on the host-to-device link in the e2e loop")
     ap.add_argument("--e2e-sync", action="store_true",
@@ -370,19 +374,33 @@ class Dsgd(SingleGpu):
 
     scaling = "strong"
 
-    def __init__(self, eng, host, s, coo, ranks, j, a0, b0, world, rank):
+    def __init__(self, eng, host, s, coo, ranks, j, a0, b0, world, rank, schedule="strata",
+                 tokens=1):
         from paper_2404_10087_b200 import dsgd
 
         super().__init__(eng, host, s, coo, ranks, j, a0, b0, world)
-        self.parallelism = f"dsgd {world}x{world} strata" if world > 1 else "dsgd 1 cell"
+        ring = schedule == "ring" and world > 1
+        self.parallelism = (f"dsgd ring {world} ranks x {tokens * world} mode-3 blocks" if ring
+                            else f"dsgd {world}x{world} strata" if world > 1 else "dsgd 1 cell")
         self.rank = rank
-        self.layout = dsgd.make_layout(coo.dims, coo.idx, world)
-        self.idx, self.vals, self.off, _ = dsgd.local_cells(self.layout, coo.idx, coo.vals, rank)
+        self.layout = (dsgd.make_ring_layout(coo.dims, coo.idx, world, tokens) if ring
+                       else dsgd.make_layout(coo.dims, coo.idx, world))
+        self.idx, self.vals, self.off, _ = (dsgd.ring_cells if ring else dsgd.local_cells)(
+            self.layout, coo.idx, coo.vals, rank)
         self.local_nnz = int(self.vals.shape[0])
         self.job_nnz = coo.nnz
         self.be = dsgd.EngineBackend(s, 0, self.idx, self.vals, self.off, coo.dims, coo.nnz,
                                      rank=rank, world=world)
-        self.tr = dsgd.DsgdTrainer(self.be, self.layout, rank)
+        if ring:
+            # peer descriptors around the ring (CUDA IPC handles), left neighbour mapped
+            import torch.distributed as tdist
+
+            blobs = [None] * world
+            tdist.all_gather_object(blobs, s.ring_export())
+            s.ring_connect(0, blobs[(rank - 1) % world])
+            tdist.barrier()
+        self.tr = dsgd.DsgdTrainer(self.be, self.layout, rank,
+                                   schedule="ring" if ring else "strata")
 
     def upload(self):
         self.s.upload_tensor(0, self.coo.dims, self.idx, self.vals)
@@ -456,7 +474,7 @@ def run_engine(args):
                                            dtype=torch.uint8))
             torch.distributed.broadcast(uid, 0)
             s.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
-        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank)
+        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, args.schedule, args.tokens)
     else:
         job = SingleGpu(eng, host, s, coo, ranks, j, a0, b0, world)
         job.upload()

@@ -1811,7 +1811,10 @@ int ftkcu_ring_factor_epoch(ftkcu_session* s, int slot, int parts, int rank,
   }
   if (s->opt_precision != FTKCU_PREC_TF32 || !s->opt_hog_update)
     return fail(s, FTKCU_ERR_ARG, "ring epochs run the tf32 accumulate sweep");
-  if (!t.shuffled) return fail(s, FTKCU_ERR_STATE, "tensor changed since the ring was connected");
+  // (re)build the tile stream if the tensor was re-uploaded since connect; on
+  // a GPU shared by virtual ranks that must happen before any rank's epoch
+  // (its first build allocates, which would serialise their kernels)
+  if ((rc = prepare_stream(s, t, nullptr))) return rc;
   KView v = make_view(s, t, true);
   v.max_ctas = (int)s->opt_max_ctas;
   if (!ws_supported(v)) return fail(s, FTKCU_ERR_ARG, "ring epochs need N = 3, J = R = 32");
