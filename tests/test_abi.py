@@ -2,6 +2,8 @@
 declared entry point, and fails loudly (never silently on the CPU) when no
 sm_100 device is present."""
 import ctypes as C
+
+import numpy as np
 import os
 import re
 import subprocess
@@ -72,3 +74,30 @@ def test_null_session_errors_are_reported():
     h = C.c_void_p()
     rc = lib.ftkcu_session_create(-5, C.byref(h))
     assert rc != 0 and lib.ftkcu_last_error(None)
+
+
+def test_packed_keys_layout_and_errors():
+    """ftkcu_pack_keys is host code (no GPU): every mode's index in its own
+    bit field (widths of dims - 1), split into a uint32 low part and a
+    0/2/4-byte high part; out-of-range indices and over-wide layouts fail."""
+    rng = np.random.default_rng(3)
+    for dims in ([480189, 17770, 2182], [1000990, 624961, 3075], [50, 40, 30], [7, 1, 2**20, 5]):
+        dims = np.array(dims, np.int32)
+        idx = np.stack([rng.integers(0, d, 5000) for d in dims], 1).astype(np.int32)
+        lo, hi = eng.Session.pack_keys(dims, idx)
+        key = lo.astype(np.uint64)
+        if hi is not None:
+            key |= hi.astype(np.uint64) << np.uint64(32)
+        widths = [max(1, int(d - 1).bit_length()) for d in dims]
+        total = sum(widths)
+        assert (hi is None) == (total <= 32) and (hi is None or hi.itemsize == (2 if total <= 48 else 4))
+        off = 0
+        for n, w in enumerate(widths):
+            got = (key >> np.uint64(off)) & np.uint64((1 << w) - 1)
+            assert np.array_equal(got.astype(np.int64), idx[:, n].astype(np.int64)), (dims, n)
+            off += w
+    bad = np.array([[0, 0, 2182]], np.int32)
+    with pytest.raises(eng.FtkError, match="out of range"):
+        eng.Session.pack_keys(np.array([480189, 17770, 2182], np.int32), bad)
+    with pytest.raises(eng.FtkError, match="64 bits"):
+        eng.Session.pack_keys(np.array([2**30] * 3, np.int32), np.zeros((1, 3), np.int32))

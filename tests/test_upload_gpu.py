@@ -122,3 +122,25 @@ def test_packed_key_upload_epoch_bit_identical(session):
     session.upload_tensor_packed_ptr_async(3, t.dims, t.nnz, kh.data_ptr(), None, vh.data_ptr())
     with pytest.raises(eng.FtkError, match="out of range"):
         session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
+
+
+def test_model_copy_async_round_trip(session):
+    """ftkcu_model_copy_async (the e2e loop's per-step read-back): enqueued
+    download equals the synchronous one; an enqueued upload of modified
+    factors is what the next download sees."""
+    t, ranks, r, a, b = _problem()
+    session.upload_model(t.dims, ranks, r, a, b)
+    pa = [_pinned(np.zeros_like(x)) for x in a]
+    pb = [_pinned(np.zeros_like(x)) for x in b]
+    na, nb = [x.numpy() for x in pa], [x.numpy() for x in pb]
+    session.model_copy_async(False, na, nb)
+    session.sync()
+    for n in range(3):
+        assert np.array_equal(na[n], a[n]) and np.array_equal(nb[n], b[n])
+    for n in range(3):
+        na[n] += 1.0
+    session.model_copy_async(True, na, nb)
+    session.sync()
+    ga, gb = session.download_model()
+    for n in range(3):
+        assert np.array_equal(ga[n], a[n] + np.float32(1.0)) and np.array_equal(gb[n], b[n])
