@@ -2,12 +2,11 @@
 declared entry point, and fails loudly (never silently on the CPU) when no
 sm_100 device is present."""
 import ctypes as C
-
-import numpy as np
 import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 import paper_2404_10087_b200 as eng
