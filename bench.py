@@ -70,6 +70,11 @@ def parse():
                     help="DSGD factor schedule (ring: mode-3 blocks passed over peer memory "
                          "inside one persistent kernel; 1 GPU emulates rank 0)")
     ap.add_argument("--tokens", type=int, default=1, help="ring: mode-3 blocks per rank")
+    ap.add_argument("--runs", type=int, default=0, choices=[-1, 0, 1],
+                    help="Hogwild stream in 16-nonzero last-mode runs (session option runs)")
+    ap.add_argument("--cell-order", default="runs", choices=["runs", "plain"],
+                    help="DSGD cells in 16-nonzero mode-3 runs (the sweep merges a warp's "
+                         "same-row updates of the small mode) or plain random order")
     ap.add_argument("--e2e-keys", default="packed", choices=["packed", "int32"],
                     help="COO index format on the host-to-device link in the e2e loop")
     ap.add_argument("--e2e-sync", action="store_true",
@@ -375,22 +380,24 @@ class Dsgd(SingleGpu):
     scaling = "strong"
 
     def __init__(self, eng, host, s, coo, ranks, j, a0, b0, world, rank, schedule="strata",
-                 tokens=1):
+                 tokens=1, runs=True):
         from paper_2404_10087_b200 import dsgd
 
         super().__init__(eng, host, s, coo, ranks, j, a0, b0, world)
         ring = schedule == "ring" and world > 1
         self.parallelism = (f"dsgd ring {world} ranks x {tokens * world} mode-3 blocks" if ring
                             else f"dsgd {world}x{world} strata" if world > 1 else "dsgd 1 cell")
+        if runs:
+            self.parallelism += ", cells in mode-3 runs"
         self.rank = rank
         self.layout = (dsgd.make_ring_layout(coo.dims, coo.idx, world, tokens) if ring
                        else dsgd.make_layout(coo.dims, coo.idx, world))
         self.idx, self.vals, self.off, _ = (dsgd.ring_cells if ring else dsgd.local_cells)(
-            self.layout, coo.idx, coo.vals, rank)
+            self.layout, coo.idx, coo.vals, rank, runs=runs)
         self.local_nnz = int(self.vals.shape[0])
         self.job_nnz = coo.nnz
         self.be = dsgd.EngineBackend(s, 0, self.idx, self.vals, self.off, coo.dims, coo.nnz,
-                                     rank=rank, world=world)
+                                     rank=rank, world=world, runs=runs)
         if ring:
             # peer descriptors around the ring (CUDA IPC handles), left neighbour mapped
             import torch.distributed as tdist
@@ -459,6 +466,7 @@ def run_engine(args):
     s.set_option("store_c", args.store_c)
     s.set_option("core16", args.core16)
     s.set_option("factor_warps", args.factor_warps)
+    s.set_option("runs", args.runs)
     # the reference CLI's init (ftk.cpp:169-173): mean |x| over the training values
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals.astype(np.float64)))), order, j,
                                     ranks)
@@ -474,7 +482,8 @@ def run_engine(args):
                                            dtype=torch.uint8))
             torch.distributed.broadcast(uid, 0)
             s.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
-        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, args.schedule, args.tokens)
+        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, args.schedule, args.tokens,
+                   args.cell_order == "runs")
     else:
         job = SingleGpu(eng, host, s, coo, ranks, j, a0, b0, world)
         job.upload()
@@ -773,8 +782,10 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
         variants = [("default", {})]
         if kind == "uniform":
             variants.append(("staleness-capped", {"max_ctas": 37}))
+            variants.append(("last-mode runs", {"runs": 1}))
         res = {}
         for name, opts in variants:
+            prev = {k: s.get_option(k) for k in opts}
             for k, v in opts.items():
                 s.set_option(k, v)
             s.upload_model(tr.dims, [j] * order, j, a, b)
@@ -790,8 +801,8 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
                 ep_ms.append(float(f_ms) + float(c_ms if np.isscalar(c_ms) else c_ms[0]))
                 ev = s.eval(5, 1, 0.0, 0.0)
                 rm.append(float(np.sqrt(ev[0] / te.nnz)))
-            for k in opts:
-                s.set_option(k, 0)
+            for k, v in prev.items():
+                s.set_option(k, v)
             dev = [abs(x - y) for x, y in zip(rm, want)]
             res[name] = {"engine": rm, "max_abs_delta": max(dev),
                          "within_1e-3": bool(max(dev) <= 1e-3), "options": opts,

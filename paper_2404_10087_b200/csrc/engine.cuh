@@ -48,6 +48,15 @@ struct DevTensor {
   // shuffle gathers one aligned record per nonzero instead of four words
   int4* rec16 = nullptr;
   int64_t rec16_cap = 0;
+  // cells keep their uploaded order (no shuffle inside a cell; the caller
+  // arranged it, e.g. DSGD cells in mode-3 runs); tiles are still permuted
+  bool keep_order = false;
+  // order 3: lay the stream out in aligned 16-nonzero chunks that share
+  // their last-mode index, chunks in random order (build_shuffled); scratch
+  // for the sort kept across re-uploads
+  bool runs = false;
+  void* runs_scratch = nullptr;
+  size_t runs_cap = 0;
   // Asynchronous upload (ftkcu_tensor_upload_async): AoS staging on the
   // copy stream, completion event, index-range flag checked at first use.
   int32_t* staging = nullptr;

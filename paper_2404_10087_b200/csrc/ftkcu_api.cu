@@ -46,6 +46,14 @@ struct ftkcu_session {
   int64_t global_nnz = 0;  // |Omega| across ranks for the core update (DSGD)
   int64_t opt_max_ctas = 0;  // sweep grid cap (0 = one CTA per SM)
   int64_t opt_ring_timeout_ms = 0;  // ring waits give up after this (0: ~2 s)
+  // Hogwild stream in last-mode runs: 0 off (default), 1 on, -1 auto (when
+  // the factor sweep is the merging J = R = 32 one).  Off by default: on the
+  // Netflix-shaped uniform workload it buys 6% of the factor sweep (8.8 ->
+  // 8.3 ms) but moves the test RMSE 1.5e-3 further from the reference's
+  // (16 updates of a row computed from one read per chunk), and the per-upload
+  // sort costs the e2e loop ~5 ms per epoch
+  int64_t opt_runs = 0;
+  int64_t opt_cell_order = 0;  // 1: ftkcu_tensor_set_cells keeps each cell's uploaded order
   int64_t opt_window = 0;  // headline factor sweep read-to-write window in tiles (0 = ring depth)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
@@ -162,6 +170,7 @@ void free_tensor(DevTensor& t) {
   if (t.tile_rows) cudaFree(t.tile_rows);
   if (t.staging) cudaFree(t.staging);
   if (t.rec16) cudaFree(t.rec16);
+  if (t.runs_scratch) cudaFree(t.runs_scratch);
   if (t.d_bad) cudaFree(t.d_bad);
   if (t.ready) cudaEventDestroy(t.ready);
   if (t.used) cudaEventDestroy(t.used);
@@ -322,6 +331,19 @@ void tile_perm(uint64_t seed, int64_t ntiles, int64_t* mul, int64_t* add) {
   *add = (int64_t)(splitmix(h) % (uint64_t)ntiles);
 }
 
+// Whether the Hogwild stream is laid out in last-mode runs (option "runs";
+// auto: when the factor sweep is the J = R = 32 one, whose epilogue merges
+// a warp's 16 same-row updates of the last mode into one RED -- other sweeps
+// would only see more same-row collisions per tile).
+static bool stream_runs(const ftkcu_session* s, const DevTensor& t) {
+  if (t.order != 3 || s->opt_runs == 0) return false;
+  if (s->opt_runs == 1) return true;
+  if (!s->have_model || !s->opt_tc_ws || !s->opt_hog_update) return false;
+  if (s->opt_precision == FTKCU_PREC_FP32 || s->opt_factor_warps == 16) return false;
+  const DevModel& m = s->model;
+  return m.order == 3 && m.r == 32 && m.ranks[0] == 32 && m.ranks[1] == 32 && m.ranks[2] == 32;
+}
+
 // Ensures the Hogwild stream exists.  perm != null lays it out in perm
 // order (one gather pass, plan-generation cost, outside the sweep timing).
 int prepare_stream(ftkcu_session* s, DevTensor& t, const int64_t* perm) {
@@ -332,8 +354,10 @@ int prepare_stream(ftkcu_session* s, DevTensor& t, const int64_t* perm) {
     t.shuffled = false;  // stream is in a caller order, not the session shuffle
     return FTKCU_OK;
   }
-  if (!t.shuffled) CK(build_shuffled(t, nullptr, (uint64_t)s->opt_shuffle_seed, nullptr, 0,
-                                     s->stream));
+  if (!t.shuffled) {
+    t.runs = stream_runs(s, t);
+    CK(build_shuffled(t, nullptr, (uint64_t)s->opt_shuffle_seed, nullptr, 0, s->stream));
+  }
   return FTKCU_OK;
 }
 
@@ -473,6 +497,13 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
   } else if (k == "max_ctas") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "max_ctas must be >= 0");
     s->opt_max_ctas = value;
+  } else if (k == "runs") {
+    if (value < -1 || value > 1) return fail(s, FTKCU_ERR_ARG, "runs must be -1, 0 or 1");
+    s->opt_runs = value;
+    for (auto& t : s->slots) t.shuffled = false;
+  } else if (k == "cell_order") {
+    if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "cell_order must be 0 or 1");
+    s->opt_cell_order = value;
   } else if (k == "ring_timeout_ms") {
     if (value < 0) return fail(s, FTKCU_ERR_ARG, "ring_timeout_ms must be >= 0");
     s->opt_ring_timeout_ms = value;
@@ -504,6 +535,8 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "shuffle_seed") *value = s->opt_shuffle_seed;
   else if (k == "max_ctas") *value = s->opt_max_ctas;
   else if (k == "window") *value = s->opt_window;
+  else if (k == "cell_order") *value = s->opt_cell_order;
+  else if (k == "runs") *value = s->opt_runs;
   else if (k == "staleness") *value = s->opt_staleness;
   else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
@@ -813,6 +846,9 @@ int ftkcu_model_upload(ftkcu_session* s, int order, const int32_t* dims, const i
   }
   CK(cudaStreamSynchronize(s->stream));
   s->have_model = true;
+  // the automatic stream layout depends on the model's ranks
+  for (auto& t : s->slots)
+    if (t.shuffled && t.runs != stream_runs(s, t)) t.shuffled = false;
   return FTKCU_OK;
 }
 
@@ -1188,6 +1224,7 @@ int ftkcu_tensor_set_cells(ftkcu_session* s, int slot, const int64_t* cell_offse
   for (int c = 0; c < ncells; ++c)
     if (cell_offsets[c + 1] < cell_offsets[c]) return fail(s, FTKCU_ERR_ARG, "cell offsets not sorted");
   t.cell_off.assign(cell_offsets, cell_offsets + ncells + 1);
+  t.keep_order = s->opt_cell_order != 0 && t.order == 3;
   t.shuffled = false;
   return FTKCU_OK;
 }

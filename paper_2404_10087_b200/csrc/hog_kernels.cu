@@ -15,6 +15,9 @@
 // Tile order: tile t of the epoch is physical tile (t * mul + add) mod T with
 // gcd(mul, T) = 1, keyed per epoch by the host.  The shuffled stream itself is
 // built once per session by a Feistel bijection (no scratch, no sort).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "engine.cuh"
 
 namespace ftkcu {
@@ -85,13 +88,170 @@ __global__ void shuffle16_kernel(const int4* __restrict__ rec, ShuffleView v,
                                  const int64_t* __restrict__ perm, int bits, uint64_t seed) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < v.nnz;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = perm ? perm[k] : feistel_perm(k, v.nnz, bits, seed);
+    // bits < 0: keep the order (cells the caller arranged)
+    const int64_t p = perm ? perm[k] : (bits < 0 ? k : feistel_perm(k, v.nnz, bits, seed));
     const int4 r = __ldg(rec + p);
     v.dst_idx[0][k] = r.x;
     v.dst_idx[1][k] = r.y;
     v.dst_idx[2][k] = r.z;
     v.dst_vals[k] = __int_as_float(r.w);
   }
+}
+
+// ---- stream in last-mode runs -------------------------------------------------
+//
+// Order 3, option "runs": the cell's nonzeros are laid out in aligned chunks
+// of kRun that share their last-mode index, the chunks in random order, so
+// each epilogue warp of the J = R = 32 factor sweep (16 rows per mode) sums
+// its rows' updates of that row and sends one RED instead of 16.  A
+// 128-nonzero tile still spans 8 random rows (each row sees at most 16
+// updates computed from one read per tile).  Built as: a Feistel shuffle
+// (random order within a row), a stable radix sort by last-mode index (the
+// index bits only), per-row chunk counts and two scans, then one scatter of
+// whole records through a second Feistel bijection over the chunks.  A row's
+// last < kRun nonzeros are pooled (by row) into mixed chunks; the one
+// partial chunk of the cell stays last, so every chunk stays kRun-aligned.
+constexpr int kRun = 16;
+
+__global__ void runs_keys_kernel(const int4* __restrict__ rec, int64_t n, int bits, uint64_t seed,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ pos) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = feistel_perm(k, n, bits, seed);
+    keys[k] = (uint32_t)__ldg(&rec[p].z);
+    pos[k] = (uint32_t)p;
+  }
+}
+
+// row start / end in the sorted keys (rows absent from the cell stay 0, 0)
+__global__ void runs_bounds_kernel(const uint32_t* __restrict__ keys, int64_t n,
+                                   uint32_t* __restrict__ rs, uint32_t* __restrict__ re) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = keys[k];
+    if (k == 0 || keys[k - 1] != r) rs[r] = (uint32_t)k;
+    if (k == n - 1 || keys[k + 1] != r) re[r] = (uint32_t)(k + 1);
+  }
+}
+
+__global__ void runs_counts_kernel(const uint32_t* __restrict__ rs, const uint32_t* __restrict__ re,
+                                   int32_t rows, uint32_t* __restrict__ full,
+                                   uint32_t* __restrict__ left) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) {
+    const uint32_t c = re[r] - rs[r];
+    full[r] = c / kRun;
+    left[r] = c % kRun;
+  }
+}
+
+__global__ void runs_place_kernel(const int4* __restrict__ rec, const uint32_t* __restrict__ keys,
+                                  const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rs,
+                                  const uint32_t* __restrict__ re, const uint32_t* __restrict__ fb,
+                                  const uint32_t* __restrict__ lb, int32_t rows, ShuffleView v,
+                                  int cbits, uint64_t seed) {
+  const int64_t n = v.nnz, nc = n / kRun;  // whole chunks (permuted)
+  const int64_t F = (int64_t)fb[rows - 1] + (re[rows - 1] - rs[rows - 1]) / kRun;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = keys[k];
+    const int64_t o = k - rs[r], fl = (int64_t)(re[r] - rs[r]) / kRun * kRun;
+    int64_t c, w;
+    if (o < fl) {
+      c = fb[r] + o / kRun;
+      w = o % kRun;
+    } else {
+      const int64_t l = lb[r] + (o - fl);
+      c = F + l / kRun;
+      w = l % kRun;
+    }
+    const int64_t d = (c < nc ? feistel_perm(c, nc, cbits, seed) : c) * kRun + w;
+    const int4 x = __ldg(rec + pos[k]);
+    v.dst_idx[0][d] = x.x;
+    v.dst_idx[1][d] = x.y;
+    v.dst_idx[2][d] = x.z;
+    v.dst_vals[d] = __int_as_float(x.w);
+  }
+}
+
+// Scratch bytes of the runs build for n nonzeros and `rows` last-mode rows.
+struct RunsScratch {
+  size_t keys, keys2, pos, pos2, rs, re, full, left, fb, lb, temp, end;
+};
+
+RunsScratch runs_scratch_layout(int64_t n, int32_t rows, size_t temp) {
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  RunsScratch L{};
+  size_t o = 0;
+  L.keys = o; o += al(4 * (size_t)n);
+  L.keys2 = o; o += al(4 * (size_t)n);
+  L.pos = o; o += al(4 * (size_t)n);
+  L.pos2 = o; o += al(4 * (size_t)n);
+  L.rs = o; o += al(4 * (size_t)rows);
+  L.re = o; o += al(4 * (size_t)rows);
+  L.full = o; o += al(4 * (size_t)rows);
+  L.left = o; o += al(4 * (size_t)rows);
+  L.fb = o; o += al(4 * (size_t)rows);
+  L.lb = o; o += al(4 * (size_t)rows);
+  L.temp = o; o += al(temp);
+  L.end = o;
+  return L;
+}
+
+cudaError_t build_runs(DevTensor& t, const int4* rec, const ShuffleView& v, uint64_t seed,
+                       cudaStream_t st) {
+  const int64_t n = v.nnz;
+  const int32_t rows = t.dims[2];
+  int kb = 1;
+  while ((1ll << kb) < rows) ++kb;
+  size_t sort_temp = 0, s1 = 0, s2 = 0;
+  cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dp(nullptr, nullptr);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_temp, dk, dp, (int)n, 0, kb, st);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(nullptr, s1, (uint32_t*)nullptr, (uint32_t*)nullptr, rows, st);
+  if (e != cudaSuccess) return e;
+  s2 = s1 > sort_temp ? s1 : sort_temp;
+  const RunsScratch L = runs_scratch_layout(n, rows, s2);
+  if (L.end > t.runs_cap) {
+    if (t.runs_scratch) cudaFree(t.runs_scratch);
+    t.runs_scratch = nullptr;
+    t.runs_cap = 0;
+    e = cudaMalloc(&t.runs_scratch, L.end);
+    if (e != cudaSuccess) return e;
+    t.runs_cap = L.end;
+  }
+  uint8_t* b = static_cast<uint8_t*>(t.runs_scratch);
+  auto u32 = [&](size_t off) { return reinterpret_cast<uint32_t*>(b + off); };
+  int bits = 2;
+  while ((1ll << bits) < n) bits += 2;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  runs_keys_kernel<<<(int)blocks, 256, 0, st>>>(rec, n, bits, seed, u32(L.keys), u32(L.pos));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cub::DoubleBuffer<uint32_t> keys(u32(L.keys), u32(L.keys2)), pos(u32(L.pos), u32(L.pos2));
+  size_t tb = s2;
+  e = cub::DeviceRadixSort::SortPairs(b + L.temp, tb, keys, pos, (int)n, 0, kb, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(b + L.rs, 0, L.full - L.rs, st);  // rs and re
+  if (e != cudaSuccess) return e;
+  runs_bounds_kernel<<<(int)blocks, 256, 0, st>>>(keys.Current(), n, u32(L.rs), u32(L.re));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  runs_counts_kernel<<<(rows + 255) / 256, 256, 0, st>>>(u32(L.rs), u32(L.re), rows, u32(L.full),
+                                                          u32(L.left));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  tb = s2;
+  e = cub::DeviceScan::ExclusiveSum(b + L.temp, tb, u32(L.full), u32(L.fb), rows, st);
+  if (e != cudaSuccess) return e;
+  tb = s2;
+  e = cub::DeviceScan::ExclusiveSum(b + L.temp, tb, u32(L.left), u32(L.lb), rows, st);
+  if (e != cudaSuccess) return e;
+  const int64_t nc = n / kRun;
+  int cbits = 2;
+  while ((1ll << cbits) < nc) cbits += 2;
+  runs_place_kernel<<<(int)blocks, 256, 0, st>>>(rec, keys.Current(), pos.Current(), u32(L.rs),
+                                                 u32(L.re), u32(L.fb), u32(L.lb), rows, v, cbits,
+                                                 seed * 0x2545f4914f6cdd1dull + 1);
+  return cudaGetLastError();
 }
 
 // ---- shared-memory layout of the sweep kernels --------------------------------
@@ -468,9 +628,15 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     if (t.order == 3) {
       pack16_kernel<<<(int)blocks, 256, 0, st>>>(v.src_idx[0], v.src_idx[1], v.src_idx[2],
                                                   v.src_vals, t.rec16 + off[c], n);
-      shuffle16_kernel<<<(int)blocks, 256, 0, st>>>(t.rec16 + off[c], v,
-                                                     d_perm,
-                                                     bits, cseed);
+      if (t.runs && !t.keep_order && !d_perm && n >= 2 * kRun && n < (1ll << 31)) {
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = build_runs(t, t.rec16 + off[c], v, cseed, st);
+        if (e != cudaSuccess) return e;
+      } else {
+        shuffle16_kernel<<<(int)blocks, 256, 0, st>>>(t.rec16 + off[c], v, d_perm,
+                                                       (t.keep_order && !d_perm) ? -1 : bits, cseed);
+      }
     } else {
       shuffle_kernel<<<(int)blocks, 256, 0, st>>>(v, d_perm, bits, cseed);
     }

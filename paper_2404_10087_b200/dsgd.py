@@ -95,9 +95,70 @@ def stratum_blocks(parts: int, rank: int, s: int, t: int) -> tuple[int, int, int
     return rank, (rank + s) % parts, (rank + t) % parts
 
 
-def local_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
+RUN_CHUNK = 16  # rows one epilogue warp of the J = R = 32 factor sweep writes per mode
+
+
+def _cell_order(key: np.ndarray, i3: np.ndarray, runs: bool, seed: int) -> np.ndarray:
+    """Positions sorted by cell.  With ``runs``, each cell is laid out in
+    aligned chunks of RUN_CHUNK nonzeros that share their mode-3 index, the
+    chunks in random order: every epilogue warp of the sweep then sums its
+    chunk's updates of that row and sends one row instead of 16 (a DSGD block
+    has only 2182/P mode-3 rows, whose updates otherwise queue on the same L2
+    lines), while a 128-nonzero tile still spans 8 random rows, so a row sees
+    at most 16 updates computed from one read per tile (whole-cell runs,
+    128, moved the C1p32 trajectory by > 1e-3).  A row's last < RUN_CHUNK
+    nonzeros are pooled per cell and cut into mixed chunks; the one partial
+    chunk goes last.  The engine keeps this order inside each cell (session
+    option ``cell_order``) and permutes whole tiles only."""
+    if not runs:
+        return np.argsort(key, kind="stable")
+    n = key.shape[0]
+    if n == 0:
+        return np.zeros(0, np.int64)
+    rng = np.random.default_rng(seed)
+    C = RUN_CHUNK
+    o = np.lexsort((rng.permutation(n), i3, key))  # by cell, row, random
+    k, r = key[o], i3[o]
+    brk = np.ones(n, bool)
+    brk[1:] = (k[1:] != k[:-1]) | (r[1:] != r[:-1])
+    gstart = np.nonzero(brk)[0]
+    gid = np.cumsum(brk) - 1
+    gsize = np.diff(np.append(gstart, n))
+    rank_in = np.arange(n) - gstart[gid]
+    full = rank_in < (gsize[gid] // C) * C
+    # chunk ids: full chunks numbered per (group, rank // C); leftovers per cell
+    chunk = np.empty(n, np.int64)
+    nfull = int(full.sum())
+    fkey = gid[full] * (n // C + 1) + rank_in[full] // C
+    _, chunk[full] = np.unique(fkey, return_inverse=True)
+    nf_chunks = int(chunk[full].max()) + 1 if nfull else 0
+    left = np.nonzero(~full)[0]
+    lo = left[np.lexsort((rng.permutation(left.size), k[left]))]
+    lk = k[lo]
+    lbrk = np.ones(lo.size, bool)
+    lbrk[1:] = lk[1:] != lk[:-1]
+    lstart = np.nonzero(lbrk)[0]
+    lrank = np.arange(lo.size) - lstart[np.cumsum(lbrk) - 1]
+    lsize = np.diff(np.append(lstart, lo.size))[np.cumsum(lbrk) - 1]
+    _, lchunk = np.unique(lk * (n // C + 1) + lrank // C, return_inverse=True)
+    chunk[lo] = nf_chunks + lchunk
+    nchunks = nf_chunks + (int(lchunk.max()) + 1 if lo.size else 0)
+    prio = rng.random(nchunks)
+    # the partial leftover chunk of each cell goes last (keeps the 16-alignment)
+    partial = np.zeros(n, bool)
+    partial[lo] = (lrank // C) == (lsize - 1) // C
+    partial[lo] &= (lsize % C) != 0
+    within = np.zeros(n, np.int64)
+    within[full] = rank_in[full] % C
+    within[lo] = lrank % C
+    pos = np.lexsort((within, prio[chunk], partial, k))
+    return o[pos]
+
+
+def local_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int, runs: bool = False):
     """This rank's nonzeros (mode-1 block ``rank``), ordered by local cell
-    ``s*P + t``; returns (idx, vals, cell_offsets[P*P + 1], global_positions)."""
+    ``s*P + t`` (``runs``: inside a cell in mode-3 runs, see _cell_order);
+    returns (idx, vals, cell_offsets[P*P + 1], global_positions)."""
     P = layout.parts
     b1 = layout.block_of(0, idx[:, 0])
     pos = np.nonzero(b1 == rank)[0]
@@ -105,7 +166,7 @@ def local_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
     s = (layout.block_of(1, li[:, 1]) - rank) % P
     t = (layout.block_of(2, li[:, 2]) - rank) % P
     key = (s * P + t).astype(np.int64)
-    order = np.argsort(key, kind="stable")
+    order = _cell_order(key, li[:, 2], runs, rank)
     counts = np.bincount(key, minlength=P * P)
     off = np.zeros(P * P + 1, np.int64)
     np.cumsum(counts, out=off[1:])
@@ -151,9 +212,10 @@ def ring_cell_blocks(parts: int, rank: int, s: int, i: int, tokens: int = 2) -> 
     return rank, (rank + s) % parts, (tokens * rank + i) % (tokens * parts)
 
 
-def ring_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
-    """This rank's nonzeros ordered by ring cell ``s*K*P + i``; returns (idx,
-    vals, cell_offsets[K*P*P + 1], global_positions)."""
+def ring_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int, runs: bool = False):
+    """This rank's nonzeros ordered by ring cell ``s*K*P + i`` (``runs``: in
+    mode-3 runs inside a cell); returns (idx, vals, cell_offsets[K*P*P + 1],
+    global_positions)."""
     P = layout.parts
     K = ring_tokens(layout)
     Q = K * P
@@ -163,7 +225,7 @@ def ring_cells(layout: Layout, idx: np.ndarray, vals: np.ndarray, rank: int):
     s = (layout.block_of(1, li[:, 1]) - rank) % P
     i = (layout.block_of(2, li[:, 2]) - K * rank) % Q
     key = (s * Q + i).astype(np.int64)
-    order = np.argsort(key, kind="stable")
+    order = _cell_order(key, li[:, 2], runs, rank)
     counts = np.bincount(key, minlength=P * Q)
     off = np.zeros(P * Q + 1, np.int64)
     np.cumsum(counts, out=off[1:])
@@ -318,7 +380,7 @@ class EngineBackend:
 
     def __init__(self, session, slot: int, idx, vals, cell_off, dims, global_nnz: int,
                  reg_a=1e-4, reg_b=1e-4, lr_a=1e-3, lr_b=1e-3, rank: int = 0,
-                 world: int = 1):
+                 world: int = 1, runs: bool = False):
         from . import MODE_HOGWILD
 
         self.s = session
@@ -331,6 +393,9 @@ class EngineBackend:
         self.global_nnz = int(global_nnz)
         self.eval_nnz = 0
         session.upload_tensor(slot, dims, idx, vals)
+        # runs: the cells come in mode-3 runs (local_cells(..., runs=True))
+        # and keep that order on the device
+        session.set_option("cell_order", 1 if runs else 0)
         session.set_cells(slot, cell_off)
         session.set_option("global_nnz", int(global_nnz))
 

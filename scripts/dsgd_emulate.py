@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-shift", action="store_true", help="skip the ring shifts (cost breakdown)")
     ap.add_argument("--tokens", type=int, default=2, help="ring: mode-3 blocks per rank (K)")
+    ap.add_argument("--runs", action="store_true",
+                    help="cells in mode-3 runs (the sweep merges a warp's same-row updates)")
     ap.add_argument("--schedule", default="strata", choices=["strata", "ring"],
                     help="ring: token-passing mode-3 blocks, one persistent kernel per phase "
                          "(posts to local scratch, no waits)")
@@ -54,7 +56,8 @@ def main():
         s.comm_init(eng.Session.comm_unique_id(), 0, 1)
     lay = (dsgd.make_ring_layout(coo.dims, coo.idx, P, args.tokens) if ring
            else dsgd.make_layout(coo.dims, coo.idx, P))
-    idx, vals, off, _ = (dsgd.ring_cells if ring else dsgd.local_cells)(lay, coo.idx, coo.vals, 0)
+    idx, vals, off, _ = (dsgd.ring_cells if ring else dsgd.local_cells)(lay, coo.idx, coo.vals, 0,
+                                                                       runs=args.runs)
 
     class SelfBackend(dsgd.EngineBackend):
         """world 1 emulating P parts: shifts go to self, no all-gather."""
@@ -62,7 +65,7 @@ def main():
         def allgather(self, mode, row_off):
             pass
 
-    be = SelfBackend(s, 0, idx, vals, off, coo.dims, coo.nnz, rank=0, world=1)
+    be = SelfBackend(s, 0, idx, vals, off, coo.dims, coo.nnz, rank=0, world=1, runs=args.runs)
     if ring:
         s.ring_emulate(0)
     if args.loop:
@@ -94,7 +97,7 @@ def main():
            "implied_job_nnz_per_s": coo.nnz / ((np.mean(f_ms) + np.mean(c_ms)) * 1e-3),
            "grid_cap": s.get_option("max_ctas"), "loop": args.loop,
            "graphs": not args.no_graphs, "shifts": not args.no_shift, "schedule": args.schedule,
-           "tokens": args.tokens if ring else None}
+           "tokens": args.tokens if ring else None, "runs": args.runs}
     print(json.dumps(out), flush=True)
     s.close()
 

@@ -98,6 +98,12 @@ def accumulate_rule(t, m, lr, reg, eps):
 # (label, order/dims, J = R, options, expected kernel)
 KERNELS = [
     ("ws", (4, 8, 4), 32, dict(precision=eng.PREC_TF32), eng.K_WS),
+    # one mode-3 row: every warp's rows share it, so the sweep merges them
+    # into one RED per warp (the path DSGD cells in mode-3 runs take)
+    ("ws-merge", (8, 16, 1), 32, dict(precision=eng.PREC_TF32), eng.K_WS),
+    # the stream in last-mode runs (option runs): aligned 16-nonzero chunks
+    # share their mode-3 row, so warps merge even with 4 mode-3 rows
+    ("ws-runs", (8, 4, 4), 32, dict(precision=eng.PREC_TF32, runs=1), eng.K_WS),
     ("wsf", (4, 8, 4), 32, dict(precision=eng.PREC_TF32, factor_warps=16), eng.K_WSF),
     ("ws3", (4, 8, 4), 32, dict(precision=eng.PREC_3XTF32), eng.K_WS3),
     ("tc3", (4, 8, 4), 32, dict(precision=eng.PREC_3XTF32, tc_ws=0), eng.K_TC),
@@ -112,7 +118,8 @@ KERNELS = [
     ("big64", (4, 8, 4), 64, dict(precision=eng.PREC_TF32), eng.K_BIG),
     ("big128", (4, 8, 4), 128, dict(precision=eng.PREC_TF32), eng.K_BIG),
 ]
-DEFAULTS = dict(precision=eng.PREC_FP32, tc_ws=1, factor_warps=8, hog_update=1, max_ctas=0)
+DEFAULTS = dict(precision=eng.PREC_FP32, tc_ws=1, factor_warps=8, hog_update=1, max_ctas=0,
+                runs=0)
 
 
 def _run_factor(session, t, m, opts, lr, reg):
