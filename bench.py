@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--cell-order", default="runs", choices=["runs", "plain"],
                     help="DSGD cells in 16-nonzero mode-3 runs (the sweep merges a warp's "
                          "same-row updates of the small mode) or plain random order")
-    ap.add_argument("--e2e-keys", default="packed", choices=["packed", "int32"],
+    ap.add_argument("--e2e-keys", default="delta", choices=["delta", "packed", "int32"],
                     help="COO index format on the host-to-device link in the e2e loop")
     ap.add_argument("--e2e-sync", action="store_true",
                     help="e2e without the double-buffered asynchronous tensor upload")
@@ -834,12 +834,32 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     # packed-key COO on the link (ftkcu_pack_keys, built once like a file
     # format; 12 instead of 16 bytes per nonzero), where the index widths fit
     keys = None
+    delta = None
+    if pipelined and args.e2e_keys == "delta":
+        # delta-coded COO (ftkcu_pack_delta: sorted mixed-radix keys, chunked
+        # deltas; built once like a file format, untimed): the values travel
+        # in the sorted order
+        try:
+            de, rs, vo, w = job.s.pack_delta(job.coo.dims, idx, vals)
+            delta = (torch.from_numpy(de).pin_memory(), torch.from_numpy(rs.view(np.int64))
+                     .pin_memory(), w)
+            vals = vo
+        except Exception:
+            delta = None
     if pipelined and args.e2e_keys == "packed":
         try:
             keys = job.s.pack_keys(job.coo.dims, idx)
         except Exception:
             keys = None
-    if keys is not None:
+    if delta is not None:
+        de_h, rs_h, width = delta
+        key_bytes = de_h.numel() + rs_h.numel() * 8
+
+        def upload_async(sl, _idx_ptr, vptr):
+            job.s.upload_tensor_delta_ptr_async(sl, job.coo.dims, job.coo.nnz, de_h.data_ptr(),
+                                                width, rs_h.data_ptr(), vptr)
+        idx_h = de_h
+    elif keys is not None:
         lo, hi = keys
         key_h = (torch.from_numpy(lo.view(np.int32)).pin_memory(),
                  None if hi is None else torch.from_numpy(hi.view(np.int16 if hi.itemsize == 2
@@ -871,6 +891,8 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
             upload_async(sl, idx_h.data_ptr(), val_h.data_ptr())
             job.slot = sl
             job.factor(host.derive_seed(5, [sl]))
+        s.model_copy_async(False, a_np, b_np)  # read-back snapshot buffer
+        s.sync()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -887,8 +909,21 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
             tev.append((what, ev))
             print(f"e2e {(time.perf_counter() - t0) * 1e3:8.2f} ms {what}", file=sys.stderr)
 
+    cps = torch.cuda.ExternalStream(s.get_option("copy_stream"), device=dev) if trace else None
+
+    dcs = torch.cuda.ExternalStream(s.get_option("dec_stream"), device=dev) if trace else None
+
+    def mark_copy(what):
+        if trace:
+            for st, w in ((cps, what), (dcs, what.replace("copied", "decoded"))):
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                tev.append((w, ev))
+
+    mark("start")
     if pipelined:
         upload_async(2, idx_h.data_ptr(), val_h.data_ptr())
+        mark_copy("[copy] upload 0 copied")
     for k in range(steps):
         if not pipelined:
             job.upload_ptr(idx_h.data_ptr(), val_h.data_ptr())
@@ -896,6 +931,14 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         # pipelined: the model stays resident across steps (it is the
         # training state, not an input); each step's result is read back
         mark(f"step {k} model uploaded")
+        if pipelined and k + 1 < steps:
+            # step k+1's COO, enqueued before this step's epoch: the copy
+            # engine streams it right behind step k's copy (it waits only for
+            # step k-1, the last epoch that read its slot), so the link stays
+            # busy while step k computes
+            upload_async(2 + (k + 1) % 2, idx_h.data_ptr(), val_h.data_ptr())
+            mark("next upload enqueued")
+            mark_copy(f"[copy] upload {k + 1} copied")
         if pipelined:
             job.slot = 2 + k % 2
         es = host.derive_seed(7, [k + 1])
@@ -903,12 +946,6 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         mark("factor enqueued")
         job.core(es)
         mark("core enqueued")
-        if pipelined and k + 1 < steps:
-            # enqueued after this step's epoch (whose launches must not wait
-            # behind a 1.6 GB copy on the PCIe link); it waits only for the
-            # last epoch that read its slot, so it overlaps this one
-            upload_async(2 + (k + 1) % 2, idx_h.data_ptr(), val_h.data_ptr())
-            mark("next upload enqueued")
         if pipelined:
             s.model_copy_async(False, a_np, b_np)
         else:
@@ -916,7 +953,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         mark("model downloaded")
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    for what, ev in tev:
+    for what, ev in sorted(tev, key=lambda x: tev[0][1].elapsed_time(x[1])):
         print(f"e2e gpu {tev[0][1].elapsed_time(ev):8.2f} ms {what}", file=sys.stderr)
     if pipelined:
         job.slot = 0
@@ -928,10 +965,15 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         dt = float(t.item())
     return {"value": job.job_nnz / dt, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps,
-            "keys": (f"packed ({key_bytes / job.coo.nnz:.0f} B/nnz, ftkcu_pack_keys; "
+            "keys": (f"delta-coded ({key_bytes / job.coo.nnz:.2f} B/nnz: {width}-byte deltas of "
+                     f"sorted mixed-radix keys + a restart key per 4096, ftkcu_pack_delta, built "
+                     f"once like a file format; {(key_bytes + vals.nbytes) / job.coo.nnz:.2f} "
+                     f"B/nnz with the values)") if delta is not None else
+                    (f"packed ({key_bytes / job.coo.nnz:.0f} B/nnz, ftkcu_pack_keys; "
                      f"{(key_bytes + vals.nbytes) / job.coo.nnz:.0f} B/nnz with the values)")
                     if keys is not None else "int32 per mode (16 B/nnz with values)",
-            "path": (("ftkcu_tensor_upload_packed_async" if keys is not None else
+            "path": (("ftkcu_tensor_upload_delta_async" if delta is not None else
+                      "ftkcu_tensor_upload_packed_async" if keys is not None else
                       "ftkcu_tensor_upload_async") + " into two alternating slots (step k+1's COO "
                      "copy overlaps step k's epoch)" if pipelined else "ftkcu_tensor_upload")
                     + (" + factor/core phases + the model read back every step "

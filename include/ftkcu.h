@@ -140,6 +140,24 @@ int ftkcu_pack_keys(int order, const int32_t* dims, int64_t nnz, const int32_t* 
 int ftkcu_tensor_upload_packed_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
                                      int64_t nnz, const uint32_t* lo, const void* hi,
                                      const float* values);
+/* Delta-coded COO for host-to-device streaming: nonzeros sorted by their
+ * mixed-radix key ((i0 d1 + i1) d2 + i2 ...), in chunks of 4096; chunk c
+ * stores its first key in restarts[c] and every later entry the difference
+ * to its predecessor in `width` little-endian bytes (the chunk's first delta
+ * slot holds 0).  Netflix shape: 3 bytes per nonzero (7 with the value)
+ * instead of 6 for packed keys.  ftkcu_pack_delta sorts and encodes on the
+ * host (once per tensor, like a file format): values_out receives the values
+ * in the sorted order, *width the byte width; it fails with FTKCU_ERR_ARG if
+ * deltas_cap < width * nnz (call again with a larger buffer), an index is
+ * out of range or prod(dims) > 2^53.  ftkcu_tensor_upload_delta_async is
+ * ftkcu_tensor_upload_async for this format (one block scan per chunk on the
+ * copy stream).  No reference counterpart (engine addition). */
+int ftkcu_pack_delta(int order, const int32_t* dims, int64_t nnz, const int32_t* idx_rowmajor,
+                     const float* values, uint8_t* deltas, int64_t deltas_cap,
+                     uint64_t* restarts, float* values_out, int* width);
+int ftkcu_tensor_upload_delta_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                                    int64_t nnz, const uint8_t* deltas, int width,
+                                    const uint64_t* restarts, const float* values);
 int ftkcu_tensor_release(ftkcu_session* s, int slot);
 int64_t ftkcu_tensor_nnz(ftkcu_session* s, int slot);
 
@@ -149,10 +167,12 @@ int ftkcu_model_upload(ftkcu_session* s, int order, const int32_t* dims,
                        const int32_t* ranks, int32_t R,
                        const float* const* A, const float* const* B);
 int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B);
-/* The same copies enqueued on the session stream without a host
- * synchronisation (to_device = 1: upload into the resident model of the same
- * shape; 0: download).  Host buffers must be pinned and stay valid until the
- * stream passes the copy (ftkcu_stream_sync).  No reference counterpart. */
+/* The same copies enqueued without a host synchronisation (to_device = 1:
+ * upload into the resident model of the same shape, on the session stream;
+ * 0: download -- a device snapshot on the session stream, then the
+ * device-to-host copy on a read-back stream, so later epochs do not wait for
+ * the PCIe transfer).  Host buffers must be pinned and stay valid until
+ * ftkcu_stream_sync returns.  No reference counterpart. */
 int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, float* const* B);
 
 /* ---- the hot path ------------------------------------------------------ */

@@ -47,7 +47,8 @@ EXPORTS = (
     "ftkcu_fastertucker_factor", "ftkcu_fastertucker_core", "ftkcu_writeback_ceiling",
     "ftkcu_ring_export", "ftkcu_ring_connect", "ftkcu_ring_emulate", "ftkcu_ring_factor_epoch",
     "ftkcu_ring_status", "ftkcu_ring_debug", "ftkcu_key_layout", "ftkcu_pack_keys",
-    "ftkcu_tensor_upload_packed_async", "ftkcu_model_copy_async",
+    "ftkcu_tensor_upload_packed_async", "ftkcu_model_copy_async", "ftkcu_pack_delta",
+    "ftkcu_tensor_upload_delta_async",
 )
 
 
@@ -132,6 +133,11 @@ def load_library(path: str = LIB_PATH):
     L.ftkcu_tensor_upload_packed_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p,
                                                    C.c_int64, C.POINTER(C.c_uint32), C.c_void_p,
                                                    _f32p]
+    L.ftkcu_pack_delta.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, _f32p, C.c_void_p,
+                                   C.c_int64, C.POINTER(C.c_uint64), _f32p, C.POINTER(C.c_int)]
+    L.ftkcu_tensor_upload_delta_async.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, C.c_int64,
+                                                  C.c_void_p, C.c_int, C.POINTER(C.c_uint64),
+                                                  _f32p]
     L.ftkcu_ring_debug.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                    C.c_int]
     _lib = L
@@ -246,6 +252,39 @@ class Session:
         if rc != 0:
             raise FtkError(L.ftkcu_last_error(None).decode())
         return lo, hi
+
+    @staticmethod
+    def pack_delta(dims, idx, vals):
+        """Delta-coded COO (ftkcu_pack_delta): the nonzeros sorted by their
+        mixed-radix key, as (deltas uint8 [width * nnz], restarts uint64
+        [ceil(nnz / 4096)], values float32 in the sorted order, width)."""
+        L = load_library()
+        dims = np.ascontiguousarray(dims, np.int32)
+        idx = np.ascontiguousarray(idx, np.int32)
+        vals = np.ascontiguousarray(vals, np.float32)
+        nnz = idx.shape[0]
+        restarts = np.empty((nnz + 4095) // 4096, np.uint64)
+        vout = np.empty(nnz, np.float32)
+        w = C.c_int(0)
+        for cap in (4, 8):
+            deltas = np.empty(cap * nnz, np.uint8)
+            rc = L.ftkcu_pack_delta(dims.shape[0], _p(dims, _i32p), nnz, _p(idx, _i32p),
+                                    _p(vals, _f32p), deltas.ctypes.data, deltas.size,
+                                    restarts.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    _p(vout, _f32p), C.byref(w))
+            if rc == 0:
+                return deltas[:w.value * nnz], restarts, vout, w.value
+            if w.value <= cap:
+                break
+        raise FtkError(L.ftkcu_last_error(None).decode())
+
+    def upload_tensor_delta_ptr_async(self, slot, dims, nnz, deltas_ptr: int, width: int,
+                                      restarts_ptr: int, vals_ptr: int):
+        """ftkcu_tensor_upload_delta_async from pinned host pointers."""
+        dims = np.ascontiguousarray(dims, np.int32)
+        self._ck(self.lib.ftkcu_tensor_upload_delta_async(
+            self.h, slot, dims.shape[0], _p(dims, _i32p), nnz, deltas_ptr, width,
+            C.cast(restarts_ptr, C.POINTER(C.c_uint64)), C.cast(vals_ptr, _f32p)))
 
     def upload_tensor_packed_ptr_async(self, slot, dims, nnz, lo_ptr: int, hi_ptr, vals_ptr: int):
         """ftkcu_tensor_upload_packed_async from pinned host pointers

@@ -213,6 +213,16 @@ cudaError_t launch_hog_core(const KView& v, int64_t tile_mul, int64_t tile_add,
                             size_t scratch_bytes, cudaStream_t st);
 // Builds the shuffled SoA copy (the tiler).  perm == nullptr: random order
 // from `seed`; otherwise entries are laid out in perm order.
+// Delta-coded uploads (ftkcu_tensor_upload_delta_async): chunks [c0, c1) of
+// kDeltaChunk entries decoded into the SoA columns; with `scatter` (order 3)
+// each record also goes straight to its single-cell tile-stream position
+// (the build_shuffled(seed) layout), finished by finish_scatter_stream.
+constexpr int kDeltaChunk = 4096;
+cudaError_t prepare_scatter_stream(DevTensor& t);
+cudaError_t launch_delta_decode(DevTensor& t, const uint8_t* deltas, const uint64_t* restarts,
+                                int width, int64_t c0, int64_t c1, bool scatter, uint64_t seed,
+                                int* bad, cudaStream_t st);
+cudaError_t finish_scatter_stream(DevTensor& t, cudaStream_t st);
 cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
                            void* scratch, size_t scratch_bytes,
                            cudaStream_t st);

@@ -17,6 +17,15 @@ struct ftkcu_session {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // asynchronous tensor uploads
+  cudaStream_t dec_stream = nullptr;   // delta-coded uploads: decode + stream scatter
+  cudaEvent_t dec_ev[8] = {};
+  // enqueued model read-back (ftkcu_model_copy_async to host): a device
+  // snapshot on the session stream, the device-to-host copy on its own stream
+  cudaStream_t rb_stream = nullptr;
+  cudaEvent_t rb_snap = nullptr, rb_done = nullptr;
+  bool rb_pending = false;
+  std::vector<float*> rb_buf;
+  size_t rb_floats = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
   DevTensor slots[8];
@@ -53,7 +62,8 @@ struct ftkcu_session {
   // (16 updates of a row computed from one read per chunk), and the per-upload
   // sort costs the e2e loop ~5 ms per epoch
   int64_t opt_runs = 0;
-  int64_t opt_cell_order = 0;  // 1: ftkcu_tensor_set_cells keeps each cell's uploaded order
+  int64_t opt_cell_order = 0;
+  int64_t opt_eager_stream = 1;  // delta-coded uploads scatter the tile stream while decoding  // 1: ftkcu_tensor_set_cells keeps each cell's uploaded order
   int64_t opt_window = 0;  // headline factor sweep read-to-write window in tiles (0 = ring depth)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
@@ -344,6 +354,16 @@ static bool stream_runs(const ftkcu_session* s, const DevTensor& t) {
   return m.order == 3 && m.r == 32 && m.ranks[0] == 32 && m.ranks[1] == 32 && m.ranks[2] == 32;
 }
 
+// Ends an asynchronous upload on the copy stream.  The tile stream is built
+// lazily on the session stream (prepare_stream): built here, behind the
+// transfer, it would serialise with it (measured: packed-key e2e 4.8e9 ->
+// 4.0e9 nnz/s).  Delta-coded uploads scatter it chunk by chunk instead.
+int enqueue_ready(ftkcu_session* s, DevTensor& t) {
+  CK(cudaEventRecord(t.ready, s->copy_stream));
+  t.pending = true;
+  return FTKCU_OK;
+}
+
 // Ensures the Hogwild stream exists.  perm != null lays it out in perm
 // order (one gather pass, plan-generation cost, outside the sweep timing).
 int prepare_stream(ftkcu_session* s, DevTensor& t, const int64_t* perm) {
@@ -417,10 +437,17 @@ int ftkcu_session_create(int device, ftkcu_session** out) {
   }
   if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s->rb_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s->dec_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->rb_snap, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->rb_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
     delete s;
     return fail(nullptr, FTKCU_ERR_CUDA, "stream/event creation failed");
   }
+  for (auto& e : s->dec_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return fail(nullptr, FTKCU_ERR_CUDA, "event creation failed");
   *out = s;
   return FTKCU_OK;
 }
@@ -430,7 +457,10 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
   cudaStreamSynchronize(s->copy_stream);
+  cudaStreamSynchronize(s->rb_stream);
+  cudaStreamSynchronize(s->dec_stream);
   for (auto& t : s->slots) free_tensor(t);
+  if (!s->rb_buf.empty() && s->rb_buf[0]) cudaFree(s->rb_buf[0]);
   free_model(s->model);
   if (s->grad) cudaFree(s->grad);
   if (s->scratch) cudaFree(s->scratch);
@@ -453,6 +483,12 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   cudaEventDestroy(s->ev1);
   cudaStreamDestroy(s->stream);
   cudaStreamDestroy(s->copy_stream);
+  cudaStreamDestroy(s->rb_stream);
+  cudaStreamDestroy(s->dec_stream);
+  for (auto e : s->dec_ev)
+    if (e) cudaEventDestroy(e);
+  cudaEventDestroy(s->rb_snap);
+  cudaEventDestroy(s->rb_done);
   delete s;
 }
 
@@ -501,6 +537,8 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     if (value < -1 || value > 1) return fail(s, FTKCU_ERR_ARG, "runs must be -1, 0 or 1");
     s->opt_runs = value;
     for (auto& t : s->slots) t.shuffled = false;
+  } else if (k == "eager_stream") {
+    s->opt_eager_stream = value != 0;
   } else if (k == "cell_order") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "cell_order must be 0 or 1");
     s->opt_cell_order = value;
@@ -537,6 +575,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "window") *value = s->opt_window;
   else if (k == "cell_order") *value = s->opt_cell_order;
   else if (k == "runs") *value = s->opt_runs;
+  else if (k == "eager_stream") *value = s->opt_eager_stream;
   else if (k == "staleness") *value = s->opt_staleness;
   else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
@@ -544,6 +583,8 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "last_factor_kernel") *value = s->last_factor_kernel;
   else if (k == "last_core_kernel") *value = s->last_core_kernel;
   else if (k == "stream") *value = (int64_t)(intptr_t)s->stream;
+  else if (k == "copy_stream") *value = (int64_t)(intptr_t)s->copy_stream;
+  else if (k == "dec_stream") *value = (int64_t)(intptr_t)s->dec_stream;
   else if (k == "num_sms") *value = num_sms();
   else return fail(s, FTKCU_ERR_ARG, "unknown option '%s'", key);
   return FTKCU_OK;
@@ -667,9 +708,7 @@ int ftkcu_tensor_upload_async(ftkcu_session* s, int slot, int order, const int32
   CK(cudaGetLastError());
   // the tile stream is built lazily on the session stream (prepare_stream), so
   // the copy stream is free for the next upload as soon as this one is checked
-  CK(cudaEventRecord(t.ready, s->copy_stream));
-  t.pending = true;
-  return FTKCU_OK;
+  return enqueue_ready(s, t);
 }
 
 // Bit layout of packed keys: w_n = bit width of dims[n] - 1 (>= 1).
@@ -785,9 +824,161 @@ int ftkcu_tensor_upload_packed_async(ftkcu_session* s, int slot, int order, cons
   keys_to_soa_kernel<<<num_sms() * 8, 256, 0, s->copy_stream>>>(
       reinterpret_cast<const uint32_t*>(st), st + lb, nnz, v, kl, t.d_bad);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(t.ready, s->copy_stream));
-  t.pending = true;
+  return enqueue_ready(s, t);
+}
+
+// ---- delta-coded COO --------------------------------------------------------
+
+// Mixed-radix key of every nonzero, sorted ascending (LSD radix sort, 16-bit
+// digits, stable), then chunked deltas.  Host code, run once per tensor
+// (like writing a file format); no reference counterpart.
+constexpr int kDeltaParts = 8;  // H2D / decode pipeline depth of a delta-coded upload
+
+int ftkcu_pack_delta(int order, const int32_t* dims, int64_t nnz, const int32_t* idx_rowmajor,
+                     const float* values, uint8_t* deltas, int64_t deltas_cap,
+                     uint64_t* restarts, float* values_out, int* width) {
+  if (order < 1 || order > kMaxOrder || nnz < 1 || !dims || !idx_rowmajor || !values ||
+      !restarts || !values_out || !width)
+    return fail(nullptr, FTKCU_ERR_ARG, "bad pack_delta arguments");
+  double cells = 1.0;
+  for (int n = 0; n < order; ++n) {
+    if (dims[n] < 1) return fail(nullptr, FTKCU_ERR_ARG, "dims must be positive");
+    cells *= (double)dims[n];
+  }
+  if (cells > 9007199254740992.0)  // 2^53: the decoder divides in double precision
+    return fail(nullptr, FTKCU_ERR_ARG, "delta keys need prod(dims) <= 2^53");
+  std::vector<uint64_t> key((size_t)nnz), key2((size_t)nnz);
+  std::vector<uint32_t> pos((size_t)nnz), pos2((size_t)nnz);
+  if (nnz >= ((int64_t)1 << 32)) return fail(nullptr, FTKCU_ERR_ARG, "pack_delta: nnz >= 2^32");
+  uint64_t kmax = 0;
+  for (int64_t e = 0; e < nnz; ++e) {
+    uint64_t k = 0;
+    for (int n = 0; n < order; ++n) {
+      const int32_t x = idx_rowmajor[e * order + n];
+      if (x < 0 || x >= dims[n]) return fail(nullptr, FTKCU_ERR_ARG, "index out of range");
+      k = k * (uint64_t)dims[n] + (uint64_t)x;
+    }
+    key[e] = k;
+    pos[e] = (uint32_t)e;
+    kmax = std::max(kmax, k);
+  }
+  std::vector<int64_t> cnt(1 << 16);
+  for (int sh = 0; sh < 64 && (kmax >> sh); sh += 16) {
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (int64_t e = 0; e < nnz; ++e) ++cnt[(key[e] >> sh) & 0xffff];
+    int64_t run = 0;
+    for (auto& x : cnt) {
+      const int64_t t = x;
+      x = run;
+      run += t;
+    }
+    for (int64_t e = 0; e < nnz; ++e) {
+      const int64_t d = cnt[(key[e] >> sh) & 0xffff]++;
+      key2[d] = key[e];
+      pos2[d] = pos[e];
+    }
+    key.swap(key2);
+    pos.swap(pos2);
+  }
+  uint64_t dmax = 0;
+  for (int64_t e = 1; e < nnz; ++e)
+    if (e % kDeltaChunk) dmax = std::max(dmax, key[e] - key[e - 1]);
+  int w = 1;
+  while (w < 8 && (dmax >> (8 * w))) ++w;
+  *width = w;
+  if (!deltas || deltas_cap < (int64_t)w * nnz)
+    return fail(nullptr, FTKCU_ERR_ARG, "pack_delta: deltas need %d bytes per nonzero", w);
+  for (int64_t e = 0; e < nnz; ++e) {
+    const uint64_t d = e % kDeltaChunk ? key[e] - key[e - 1] : 0;
+    if (e % kDeltaChunk == 0) restarts[e / kDeltaChunk] = key[e];
+    for (int b = 0; b < w; ++b) deltas[e * w + b] = (uint8_t)(d >> (8 * b));
+    values_out[e] = values[pos[e]];
+  }
   return FTKCU_OK;
+}
+
+int ftkcu_tensor_upload_delta_async(ftkcu_session* s, int slot, int order, const int32_t* dims,
+                                    int64_t nnz, const uint8_t* deltas, int width,
+                                    const uint64_t* restarts, const float* values) {
+  int rc = bind(s);
+  if (rc) return rc;
+  if (slot < 0 || slot >= 8) return fail(s, FTKCU_ERR_ARG, "tensor slot %d out of range", slot);
+  if (order < 1 || order > kMaxOrder)
+    return fail(s, FTKCU_ERR_ARG, "order %d unsupported (1..%d)", order, kMaxOrder);
+  if (nnz < 1 || !deltas || !restarts || !values || width < 1 || width > 8)
+    return fail(s, FTKCU_ERR_ARG, "asynchronous upload needs a non-empty tensor");
+  double cells = 1.0;
+  for (int n = 0; n < order; ++n) {
+    if (dims[n] < 1) return fail(s, FTKCU_ERR_ARG, "dims must be positive");
+    cells *= (double)dims[n];
+  }
+  if (cells > 9007199254740992.0) return fail(s, FTKCU_ERR_ARG, "delta keys need prod(dims) <= 2^53");
+  DevTensor& t = s->slots[slot];
+  if ((rc = finish_upload(s, t))) return rc;
+  // ordering against the slot's readers: as ftkcu_tensor_upload_async
+  if (slot == s->last_slot || (t.used_rec && !t.used)) {
+    CK(cudaEventRecord(s->ev1, s->stream));
+    CK(cudaStreamWaitEvent(s->copy_stream, s->ev1, 0));
+  } else if (t.used_rec) {
+    CK(cudaStreamWaitEvent(s->copy_stream, t.used, 0));
+  }
+  if (!(t.vals && t.order == order && t.nnz == nnz)) {
+    CK(cudaStreamSynchronize(s->stream));
+    free_tensor(t);
+    t.order = order;
+    t.nnz = nnz;
+    for (int n = 0; n < order; ++n) CK(cudaMalloc(&t.idx[n], sizeof(int32_t) * (size_t)nnz));
+    CK(cudaMalloc(&t.vals, sizeof(float) * (size_t)nnz));
+  }
+  for (int n = 0; n < order; ++n) t.dims[n] = dims[n];
+  t.cell_off.clear();
+  t.cell_tile.clear();
+  t.shuffled = false;
+  t.stream_tiles = 0;
+  const int64_t chunks = (nnz + kDeltaChunk - 1) / kDeltaChunk;
+  const size_t db = (size_t)width * nnz, rb = sizeof(uint64_t) * (size_t)chunks;
+  const size_t dpad = (db + 15) / 16 * 16;
+  if (t.staging_cap < dpad + rb) {
+    if (t.staging) CK(cudaFree(t.staging));
+    t.staging = nullptr;
+    CK(cudaMalloc(&t.staging, dpad + rb));
+    t.staging_cap = dpad + rb;
+  }
+  if (!t.d_bad) CK(cudaMalloc(&t.d_bad, sizeof(int)));
+  if (!t.ready) CK(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+  // Order 3 single cell (no runs layout): every decoded chunk scatters its
+  // records straight into the tile stream, so decoding and the stream build
+  // overlap the rest of the transfer (copy stream: the parts' H2D copies;
+  // decode stream: each part's kernel once its bytes have landed).
+  const bool scatter = s->opt_eager_stream && order == 3 && !stream_runs(s, t);
+  if (scatter) CK(prepare_scatter_stream(t));
+  uint8_t* st = reinterpret_cast<uint8_t*>(t.staging);
+  const uint64_t* rs_dev = reinterpret_cast<const uint64_t*>(st + dpad);
+  CK(cudaMemsetAsync(t.d_bad, 0, sizeof(int), s->copy_stream));
+  CK(cudaMemcpyAsync(st + dpad, restarts, rb, cudaMemcpyHostToDevice, s->copy_stream));
+  const int64_t per = (chunks + kDeltaParts - 1) / kDeltaParts;
+  for (int part = 0; part < kDeltaParts; ++part) {
+    const int64_t c0 = std::min<int64_t>(chunks, part * per), c1 = std::min<int64_t>(chunks, c0 + per);
+    if (c1 <= c0) break;
+    const int64_t e0 = c0 * kDeltaChunk, e1 = std::min<int64_t>(nnz, c1 * kDeltaChunk);
+    CK(cudaMemcpyAsync(st + e0 * width, deltas + e0 * width, (size_t)(e1 - e0) * width,
+                       cudaMemcpyHostToDevice, s->copy_stream));
+    CK(cudaMemcpyAsync(t.vals + e0, values + e0, sizeof(float) * (e1 - e0), cudaMemcpyHostToDevice,
+                       s->copy_stream));
+    CK(cudaEventRecord(s->dec_ev[part], s->copy_stream));
+    CK(cudaStreamWaitEvent(s->dec_stream, s->dec_ev[part], 0));
+    CK(launch_delta_decode(t, st, rs_dev, width, c0, c1, scatter, (uint64_t)s->opt_shuffle_seed,
+                           t.d_bad, s->dec_stream));
+  }
+  if (scatter) {
+    CK(finish_scatter_stream(t, s->dec_stream));
+    CK(cudaEventRecord(t.ready, s->dec_stream));
+    t.pending = true;
+    return FTKCU_OK;
+  }
+  CK(cudaEventRecord(s->dec_ev[0], s->dec_stream));
+  CK(cudaStreamWaitEvent(s->copy_stream, s->dec_ev[0], 0));
+  return enqueue_ready(s, t);
 }
 
 int ftkcu_tensor_release(ftkcu_session* s, int slot) {
@@ -877,6 +1068,54 @@ int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, flo
   if (rc) return rc;
   if (!s->have_model) return fail(s, FTKCU_ERR_STATE, "no model uploaded");
   const DevModel& m = s->model;
+  if (!to_device) {
+    // Read-back: snapshot the model on the session stream (a device copy at
+    // HBM speed), then copy the snapshot to the host on rb_stream, so the
+    // next epoch does not wait for the PCIe transfer.  The next snapshot
+    // waits for this transfer (it overwrites the buffer).
+    size_t total = 0;
+    for (int n = 0; n < m.order; ++n)
+      total += (size_t)m.dims[n] * m.ranks[n] + (size_t)m.ranks[n] * m.r;
+    if (s->rb_floats < total) {
+      CK(cudaStreamSynchronize(s->rb_stream));
+      if (!s->rb_buf.empty() && s->rb_buf[0]) CK(cudaFree(s->rb_buf[0]));
+      s->rb_buf.assign(1, nullptr);
+      CK(cudaMalloc(&s->rb_buf[0], sizeof(float) * total));
+      s->rb_floats = total;
+      s->rb_pending = false;
+    }
+    if (s->rb_pending) CK(cudaStreamWaitEvent(s->stream, s->rb_done, 0));
+    float* snap = s->rb_buf[0];
+    std::vector<std::pair<float*, const float*>> parts;  // (host, snapshot)
+    for (int n = 0; n < m.order; ++n) {
+      const size_t an = (size_t)m.dims[n] * m.ranks[n], bn = (size_t)m.ranks[n] * m.r;
+      if (A && A[n]) {
+        CK(cudaMemcpyAsync(snap, m.a[n], sizeof(float) * an, cudaMemcpyDeviceToDevice, s->stream));
+        parts.push_back({A[n], snap});
+      }
+      snap += an;
+      if (B && B[n]) {
+        CK(cudaMemcpyAsync(snap, m.b[n], sizeof(float) * bn, cudaMemcpyDeviceToDevice, s->stream));
+        parts.push_back({B[n], snap});
+      }
+      snap += bn;
+    }
+    CK(cudaEventRecord(s->rb_snap, s->stream));
+    CK(cudaStreamWaitEvent(s->rb_stream, s->rb_snap, 0));
+    snap = s->rb_buf[0];
+    for (int n = 0; n < m.order; ++n) {
+      const size_t an = (size_t)m.dims[n] * m.ranks[n], bn = (size_t)m.ranks[n] * m.r;
+      if (A && A[n])
+        CK(cudaMemcpyAsync(A[n], snap, sizeof(float) * an, cudaMemcpyDeviceToHost, s->rb_stream));
+      snap += an;
+      if (B && B[n])
+        CK(cudaMemcpyAsync(B[n], snap, sizeof(float) * bn, cudaMemcpyDeviceToHost, s->rb_stream));
+      snap += bn;
+    }
+    CK(cudaEventRecord(s->rb_done, s->rb_stream));
+    s->rb_pending = true;
+    return FTKCU_OK;
+  }
   const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   for (int n = 0; n < m.order; ++n) {
     const size_t an = sizeof(float) * (size_t)m.dims[n] * m.ranks[n];
@@ -1544,6 +1783,7 @@ int ftkcu_stream_sync(ftkcu_session* s) {
   int rc = bind(s);
   if (rc) return rc;
   CK(cudaStreamSynchronize(s->stream));
+  CK(cudaStreamSynchronize(s->rb_stream));
   return FTKCU_OK;
 }
 

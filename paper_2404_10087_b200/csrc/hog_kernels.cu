@@ -15,6 +15,7 @@
 // Tile order: tile t of the epoch is physical tile (t * mul + add) mod T with
 // gcd(mul, T) = 1, keyed per epoch by the host.  The shuffled stream itself is
 // built once per session by a Feistel bijection (no scratch, no sort).
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -56,6 +57,23 @@ __device__ int64_t feistel_perm(int64_t i, int64_t n, int bits, uint64_t seed) {
   return (int64_t)x;
 }
 
+// Inverse of feistel_perm (the rounds backwards; cycle walking inverts too).
+__device__ int64_t feistel_inv(int64_t i, int64_t n, int bits, uint64_t seed) {
+  const int hb = bits / 2;
+  const uint64_t mask = (1ull << hb) - 1;
+  uint64_t x = (uint64_t)i;
+  do {
+    uint64_t lo = x & mask, hi = x >> hb;
+    for (int r = 3; r >= 0; --r) {
+      const uint64_t plo = hi;
+      hi = lo ^ (mix32((uint32_t)plo, (uint32_t)(seed >> (r * 8)) ^ (uint32_t)(seed >> 32) * (r + 1)) & mask);
+      lo = plo;
+    }
+    x = (hi << hb) | lo;
+  } while ((int64_t)x >= n);
+  return (int64_t)x;
+}
+
 struct ShuffleView {
   int order;
   const int32_t* src_idx[kMaxOrder];
@@ -90,12 +108,87 @@ __global__ void shuffle16_kernel(const int4* __restrict__ rec, ShuffleView v,
        k += (int64_t)gridDim.x * blockDim.x) {
     // bits < 0: keep the order (cells the caller arranged)
     const int64_t p = perm ? perm[k] : (bits < 0 ? k : feistel_perm(k, v.nnz, bits, seed));
-    const int4 r = __ldg(rec + p);
-    v.dst_idx[0][k] = r.x;
-    v.dst_idx[1][k] = r.y;
-    v.dst_idx[2][k] = r.z;
-    v.dst_vals[k] = __int_as_float(r.w);
+    const int4 r = __ldcs(rec + p);
+    __stcs(v.dst_idx[0] + k, r.x);
+    __stcs(v.dst_idx[1] + k, r.y);
+    __stcs(v.dst_idx[2] + k, r.z);
+    __stcs(v.dst_vals + k, __int_as_float(r.w));
   }
+}
+
+// ---- delta-coded uploads (ftkcu_tensor_upload_delta_async) -------------------
+//
+// One block per chunk of kDeltaChunk entries, 16 consecutive entries per
+// thread, one block scan: entry e = restart[chunk] + the chunk's deltas up to
+// e.  Writes the storage-order SoA columns and, for order 3 with `rec` set,
+// scatters the 16-B record to its tile-stream position feistel_inv(e) -- the
+// position build_shuffled's gather would give it -- so the stream is built
+// chunk by chunk while the rest of the upload is still on the PCIe link.
+constexpr int kDeltaThreads = 256;
+constexpr int kDeltaPer = kDeltaChunk / kDeltaThreads;
+
+struct DeltaDecode {
+  const uint8_t* deltas;
+  const uint64_t* restarts;
+  const float* vals;
+  int32_t* col[kMaxOrder];
+  int32_t dims[kMaxOrder];
+  double inv[kMaxOrder];
+  int order, width, bits;
+  uint64_t seed;
+  int64_t nnz;
+  int4* rec;
+  int* bad;
+};
+
+__global__ void __launch_bounds__(kDeltaThreads) delta_decode_kernel(DeltaDecode d, int64_t c0) {
+  using Scan = cub::BlockScan<uint64_t, kDeltaThreads>;
+  __shared__ typename Scan::TempStorage scan;
+  const int64_t c = c0 + blockIdx.x;
+  const int64_t e0 = c * kDeltaChunk + (int64_t)threadIdx.x * kDeltaPer;
+  const int w = d.width;
+  uint64_t run[kDeltaPer];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kDeltaPer; ++i) {
+    const int64_t e = e0 + i;
+    uint64_t x = 0;
+    if (e < d.nnz && (threadIdx.x | i)) {  // the chunk's first entry is its restart
+      const uint8_t* q = d.deltas + e * w;
+      for (int b = 0; b < w; ++b) x |= (uint64_t)__ldcs(q + b) << (8 * b);
+    }
+    sum += x;
+    run[i] = sum;
+  }
+  uint64_t before;
+  Scan(scan).ExclusiveSum(sum, before);
+  const uint64_t base = d.restarts[c] + before;
+  int flag = 0;
+#pragma unroll
+  for (int i = 0; i < kDeltaPer; ++i) {
+    const int64_t e = e0 + i;
+    if (e >= d.nnz) break;
+    uint64_t k = base + run[i];
+    int32_t ix[kMaxOrder];
+    for (int n = d.order - 1; n > 0; --n) {
+      // k < 2^53 (checked by the caller): the double quotient is off by at most one
+      const uint64_t dn = (uint64_t)d.dims[n];
+      uint64_t q = (uint64_t)((double)k * d.inv[n]);
+      if (q * dn > k) --q;
+      else if ((q + 1) * dn <= k) ++q;
+      ix[n] = (int32_t)(k - q * dn);
+      k = q;
+    }
+    flag |= k >= (uint64_t)d.dims[0];
+    ix[0] = (int32_t)k;
+    // streaming (evict-first) stores: this runs beside an epoch whose factor
+    // rows live in L2
+    for (int n = 0; n < d.order; ++n) __stcs(d.col[n] + e, ix[n]);
+    if (d.rec)
+      __stcs(d.rec + feistel_inv(e, d.nnz, d.bits, d.seed),
+             make_int4(ix[0], ix[1], ix[2], __float_as_int(__ldcs(d.vals + e))));
+  }
+  if (flag) atomicExch(d.bad, 1);
 }
 
 // ---- stream in last-mode runs -------------------------------------------------
@@ -114,11 +207,12 @@ __global__ void shuffle16_kernel(const int4* __restrict__ rec, ShuffleView v,
 constexpr int kRun = 16;
 
 __global__ void runs_keys_kernel(const int4* __restrict__ rec, int64_t n, int bits, uint64_t seed,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ pos) {
+                                 int32_t rows, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ pos) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = feistel_perm(k, n, bits, seed);
-    keys[k] = (uint32_t)__ldg(&rec[p].z);
+    keys[k] = min((uint32_t)__ldg(&rec[p].z), (uint32_t)(rows - 1));  // range-checked later
     pos[k] = (uint32_t)p;
   }
 }
@@ -226,7 +320,8 @@ cudaError_t build_runs(DevTensor& t, const int4* rec, const ShuffleView& v, uint
   while ((1ll << bits) < n) bits += 2;
   int64_t blocks = (n + 255) / 256;
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-  runs_keys_kernel<<<(int)blocks, 256, 0, st>>>(rec, n, bits, seed, u32(L.keys), u32(L.pos));
+  runs_keys_kernel<<<(int)blocks, 256, 0, st>>>(rec, n, bits, seed, rows, u32(L.keys),
+                                                u32(L.pos));
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cub::DoubleBuffer<uint32_t> keys(u32(L.keys), u32(L.keys2)), pos(u32(L.pos), u32(L.pos2));
   size_t tb = s2;
@@ -546,6 +641,14 @@ size_t hog_core_scratch_bytes(const KView& v, int blocks_per_sm) {
 }
 
 // Rows of each tile of a cell of n nonzeros: kHogTile, the last one the rest.
+// Feistel parameters of a cell of n entries (as build_shuffled draws them).
+static void cell_shuffle_params(int64_t n, uint64_t seed, int c, int* bits, uint64_t* cseed) {
+  int b = 2;
+  while ((1ll << b) < n) b += 2;
+  *bits = b;
+  *cseed = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1));
+}
+
 __global__ void tile_rows_kernel(int32_t* __restrict__ rows, int64_t nt, int64_t n) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k < nt) {
@@ -620,11 +723,11 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
     v.src_vals = t.vals + off[c];
     v.dst_vals = t.svals + ctile[c] * kHogTile;
     v.nnz = n;
-    int bits = 2;
-    while ((1ll << bits) < n) bits += 2;
+    int bits;
+    uint64_t cseed;
+    cell_shuffle_params(n, seed, c, &bits, &cseed);
     int64_t blocks = (n + 255) / 256;
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    const uint64_t cseed = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(c + 1));
     if (t.order == 3) {
       pack16_kernel<<<(int)blocks, 256, 0, st>>>(v.src_idx[0], v.src_idx[1], v.src_idx[2],
                                                   v.src_vals, t.rec16 + off[c], n);
@@ -645,6 +748,89 @@ cudaError_t build_shuffled(DevTensor& t, const int64_t* d_perm, uint64_t seed,
   }
   t.cell_tile = ctile;
   t.stream_tiles = tiles;
+  t.shuffled = true;
+  return cudaSuccess;
+}
+
+cudaError_t prepare_scatter_stream(DevTensor& t) {
+  const int64_t tiles = (t.nnz + kHogTile - 1) / kHogTile;
+  cudaError_t e;
+  if (tiles > t.stream_cap || !t.svals) {
+    for (int n = 0; n < t.order; ++n) {
+      if (t.sidx[n]) cudaFree(t.sidx[n]);
+      e = cudaMalloc(&t.sidx[n], sizeof(int32_t) * kHogTile * tiles);
+      if (e != cudaSuccess) return e;
+    }
+    if (t.svals) cudaFree(t.svals);
+    if (t.tile_rows) cudaFree(t.tile_rows);
+    e = cudaMalloc(&t.svals, sizeof(float) * kHogTile * tiles);
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&t.tile_rows, sizeof(int32_t) * tiles);
+    if (e != cudaSuccess) return e;
+    t.stream_cap = tiles;
+  }
+  if (t.rec16_cap < t.nnz) {
+    if (t.rec16) cudaFree(t.rec16);
+    t.rec16 = nullptr;
+    e = cudaMalloc(&t.rec16, sizeof(int4) * (size_t)t.nnz);
+    if (e != cudaSuccess) return e;
+    t.rec16_cap = t.nnz;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_delta_decode(DevTensor& t, const uint8_t* deltas, const uint64_t* restarts,
+                                int width, int64_t c0, int64_t c1, bool scatter, uint64_t seed,
+                                int* bad, cudaStream_t st) {
+  if (c1 <= c0) return cudaSuccess;
+  DeltaDecode d{};
+  d.deltas = deltas;
+  d.restarts = restarts;
+  d.vals = t.vals;
+  d.order = t.order;
+  d.width = width;
+  d.nnz = t.nnz;
+  d.bad = bad;
+  for (int n = 0; n < t.order; ++n) {
+    d.col[n] = t.idx[n];
+    d.dims[n] = t.dims[n];
+    d.inv[n] = 1.0 / (double)t.dims[n];
+  }
+  if (scatter && t.order == 3) {
+    d.rec = t.rec16;
+    cell_shuffle_params(t.nnz, seed, 0, &d.bits, &d.seed);
+  }
+  delta_decode_kernel<<<(unsigned)(c1 - c0), kDeltaThreads, 0, st>>>(d, c0);
+  return cudaGetLastError();
+}
+
+// The scattered records (prepare_scatter_stream, launch_delta_decode with
+// scatter) -> the single-cell tile stream build_shuffled(seed) would build.
+cudaError_t finish_scatter_stream(DevTensor& t, cudaStream_t st) {
+  const int64_t n = t.nnz, tiles = (n + kHogTile - 1) / kHogTile, pad = tiles * kHogTile - n;
+  cudaError_t e;
+  if (pad > 0) {
+    for (int i = 0; i < t.order; ++i) {
+      e = cudaMemsetAsync(t.sidx[i] + n, 0, sizeof(int32_t) * pad, st);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaMemsetAsync(t.svals + n, 0, sizeof(float) * pad, st);
+    if (e != cudaSuccess) return e;
+  }
+  tile_rows_kernel<<<(int)((tiles + 255) / 256), 256, 0, st>>>(t.tile_rows, tiles, n);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ShuffleView v{};
+  v.order = t.order;
+  for (int i = 0; i < t.order; ++i) v.dst_idx[i] = t.sidx[i];
+  v.dst_vals = t.svals;
+  v.nnz = n;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  shuffle16_kernel<<<(int)blocks, 256, 0, st>>>(t.rec16, v, nullptr, -1, 0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  t.cell_tile = {0, tiles};
+  t.stream_tiles = tiles;
+  t.runs = false;
   t.shuffled = true;
   return cudaSuccess;
 }

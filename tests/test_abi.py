@@ -100,3 +100,51 @@ def test_packed_keys_layout_and_errors():
         eng.Session.pack_keys(np.array([480189, 17770, 2182], np.int32), bad)
     with pytest.raises(eng.FtkError, match="64 bits"):
         eng.Session.pack_keys(np.array([2**30] * 3, np.int32), np.zeros((1, 3), np.int32))
+
+
+def _delta_decode(dims, deltas, restarts, w, nnz):
+    """numpy restatement of delta_to_soa_kernel (ftkcu_api.cu)."""
+    d = np.zeros(nnz, np.uint64)
+    for b in range(w):
+        d |= deltas.reshape(nnz, w)[:, b].astype(np.uint64) << np.uint64(8 * b)
+    d[::4096] = 0
+    c = np.arange(nnz) // 4096
+    first = np.cumsum(d)
+    # per-chunk prefix: subtract the running sum before each chunk's start
+    start_sum = first[np.arange(restarts.size) * 4096]
+    keys = restarts[c] + (first - start_sum[c])
+    idx = np.empty((nnz, len(dims)), np.int64)
+    for n in range(len(dims) - 1, -1, -1):
+        idx[:, n] = (keys % np.uint64(dims[n])).astype(np.int64)
+        keys //= np.uint64(dims[n])
+    return idx
+
+
+def test_pack_delta_round_trip():
+    """ftkcu_pack_delta is host code: the nonzeros sorted by mixed-radix key
+    (stable), chunked deltas of the minimal byte width plus a restart key per
+    4096; decoding gives the sorted tensor back, values follow their keys;
+    duplicates, ragged chunks and out-of-range indices."""
+    rng = np.random.default_rng(5)
+    for dims, nnz in (([480189, 17770, 2182], 20000), ([50, 40, 30], 9000),
+                      ([7, 1, 2**20, 5], 5000), ([3, 3, 3], 4097)):
+        dims = np.array(dims, np.int32)
+        idx = np.stack([rng.integers(0, d, nnz) for d in dims], 1).astype(np.int32)
+        vals = rng.random(nnz).astype(np.float32)
+        de, rs, vo, w = eng.Session.pack_delta(dims, idx, vals)
+        key = np.zeros(nnz, np.int64)
+        for n in range(len(dims)):
+            key = key * int(dims[n]) + idx[:, n]
+        o = np.argsort(key, kind="stable")
+        assert de.size == w * nnz and rs.size == (nnz + 4095) // 4096
+        gaps = np.diff(key[o])
+        gaps[np.arange(1, nnz) % 4096 == 0] = 0
+        assert w == max(1, (int(gaps.max()).bit_length() + 7) // 8)
+        assert np.array_equal(_delta_decode(dims, de, rs, w, nnz), idx[o])
+        assert np.array_equal(vo, vals[o])
+    with pytest.raises(eng.FtkError, match="out of range"):
+        eng.Session.pack_delta(np.array([5, 5, 5], np.int32), np.array([[0, 5, 0]], np.int32),
+                               np.ones(1, np.float32))
+    with pytest.raises(eng.FtkError, match="2\\^53"):
+        eng.Session.pack_delta(np.array([2**30] * 2, np.int32), np.zeros((1, 2), np.int32),
+                               np.ones(1, np.float32))

@@ -124,6 +124,91 @@ def test_packed_key_upload_epoch_bit_identical(session):
         session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
 
 
+@pytest.mark.parametrize("nnz", [20000, 4096, 37])
+def test_delta_upload_matches_int32_upload(session, nnz):
+    """ftkcu_tensor_upload_delta_async (the e2e link format, 3 B of key per
+    nonzero at the Netflix shape): the device tensor equals the int32 upload
+    of the same sorted tensor, so a deterministic epoch is bit-identical;
+    whole and ragged chunks."""
+    rng = np.random.default_rng(nnz)
+    dims = np.array([480189, 17770, 2182], np.int32)
+    idx = np.stack([rng.integers(0, d, nnz) for d in dims], 1).astype(np.int32)
+    vals = rng.uniform(1, 5, nnz).astype(np.float32)
+    de, rs, vo, w = eng.Session.pack_delta(dims, idx, vals)
+    key = (idx[:, 0].astype(np.int64) * dims[1] + idx[:, 1]) * dims[2] + idx[:, 2]
+    o = np.argsort(key, kind="stable")
+    ranks, r = [8, 8, 8], 8
+    scale = host.default_init_scale(float(np.mean(vals)), 3, r, ranks)
+    a, b = host.init_model(dims, ranks, r, 3, scale)
+    plan1 = host.global_plan(nnz, 16, 3)
+    plan2 = host.global_plan(nnz, 16, 4)
+    out = []
+    for delta in (False, True):
+        session.upload_model(dims, ranks, r, a, b)
+        if delta:
+            dh, rh, vh = _pinned(de), _pinned(rs.view(np.int64)), _pinned(vo)
+            session.upload_tensor_delta_ptr_async(2, dims, nnz, dh.data_ptr(), w, rh.data_ptr(),
+                                                  vh.data_ptr())
+        else:
+            session.upload_tensor(2, dims, idx[o], vals[o])
+        session.factor_phase(2, plan1, 16, 1e-3, 1e-4, DET)
+        session.core_phase(2, plan2, 16, 1e-3, 1e-4, DET)
+        out.append(session.download_model())
+        session.release_tensor(2)
+    for n in range(3):
+        assert np.array_equal(out[0][0][n], out[1][0][n])
+        assert np.array_equal(out[0][1][n], out[1][1][n])
+    # a restart key past the last cell is reported at the slot's first use
+    rs_bad = rs.copy()
+    rs_bad[-1] = np.uint64(int(dims[0]) * int(dims[1]) * int(dims[2]))
+    dh, rh, vh = _pinned(de), _pinned(rs_bad.view(np.int64)), _pinned(vo)
+    session.upload_tensor_delta_ptr_async(3, dims, nnz, dh.data_ptr(), w, rh.data_ptr(),
+                                          vh.data_ptr())
+    with pytest.raises(eng.FtkError, match="out of range"):
+        session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
+
+
+@pytest.mark.parametrize("nnz", [300000, 5000])
+def test_delta_upload_scattered_stream_equals_gather_build(nnz):
+    """The delta-coded upload builds the Hogwild tile stream by scattering
+    each decoded chunk to feistel_inv(e) (overlapping the transfer); it must
+    equal build_shuffled's gather (the int32 upload of the same sorted tensor,
+    stream built lazily): the Hogwild core gradient, a per-CTA fixed-order
+    sum over the tile stream (deterministic per seed and stream), is
+    bit-identical."""
+    rng = np.random.default_rng(nnz + 1)
+    dims = np.array([4000, 300, 50], np.int32)
+    idx = np.stack([rng.integers(0, d, nnz) for d in dims], 1).astype(np.int32)
+    vals = rng.uniform(1, 5, nnz).astype(np.float32)
+    de, rs, vo, w = eng.Session.pack_delta(dims, idx, vals)
+    key = (idx[:, 0].astype(np.int64) * dims[1] + idx[:, 1]) * dims[2] + idx[:, 2]
+    o = np.argsort(key, kind="stable")
+    scale = host.default_init_scale(float(np.mean(vals)), 3, 32, [32] * 3)
+    a, b = host.init_model(dims, [32] * 3, 32, 3, scale)
+    out = []
+    s = eng.Session(0)
+    try:
+        s.set_option("precision", eng.PREC_TF32)
+        for how in ("int32", "delta", "delta-lazy"):
+            s.set_option("eager_stream", 0 if how == "delta-lazy" else 1)
+            s.upload_model(dims, [32] * 3, 32, a, b)
+            if how == "int32":
+                s.upload_tensor(2, dims, idx[o], vals[o])
+            else:
+                dh, rh, vh = _pinned(de), _pinned(rs.view(np.int64)), _pinned(vo)
+                s.upload_tensor_delta_ptr_async(2, dims, nnz, dh.data_ptr(), w, rh.data_ptr(),
+                                                vh.data_ptr())
+            _, g = s.core_phase(2, None, 16, 0.0, 0.0, eng.MODE_HOGWILD, seed=5, want_grad=True)
+            assert s.get_option("last_core_kernel") in (eng.K_WS, eng.K_WS16)
+            out.append(g)
+            s.release_tensor(2)
+    finally:
+        s.close()
+    assert np.any(out[0] != 0)
+    for g in out[1:]:
+        assert np.array_equal(g, out[0])
+
+
 def test_model_copy_async_round_trip(session):
     """ftkcu_model_copy_async (the e2e loop's per-step read-back): enqueued
     download equals the synchronous one; an enqueued upload of modified
