@@ -66,9 +66,10 @@ def parse():
     ap.add_argument("--dsgd", action="store_true",
                     help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--schedule", default="strata", choices=["strata", "ring"],
-                    help="DSGD factor schedule (ring: mode-3 blocks passed over peer memory "
-                         "inside one persistent kernel; 1 GPU emulates rank 0)")
+    ap.add_argument("--schedule", default="ring", choices=["strata", "ring"],
+                    help="DSGD factor schedule at N > 1 (ring: mode-3 blocks passed over CUDA-IPC "
+                         "peer memory inside one persistent kernel, falling back to the strata "
+                         "if a wait times out; strata: P*P cell launches + NCCL shifts)")
     ap.add_argument("--tokens", type=int, default=1, help="ring: mode-3 blocks per rank")
     ap.add_argument("--runs", type=int, default=0, choices=[-1, 0, 1],
                     help="Hogwild stream in 16-nonzero last-mode runs (session option runs)")
@@ -406,8 +407,20 @@ class Dsgd(SingleGpu):
             tdist.all_gather_object(blobs, s.ring_export())
             s.ring_connect(0, blobs[(rank - 1) % world])
             tdist.barrier()
+        self.ring = ring
         self.tr = dsgd.DsgdTrainer(self.be, self.layout, rank,
                                    schedule="ring" if ring else "strata")
+
+    def ring_ok(self):
+        """One untimed ring factor phase; False on every rank if any rank's
+        wait timed out (the caller then falls back to the strata)."""
+        import torch
+        import torch.distributed as tdist
+
+        self.factor(self.host.derive_seed(3, [0]))
+        bad = torch.tensor([1.0 if self.s.ring_status() else 0.0])
+        tdist.all_reduce(bad, op=tdist.ReduceOp.MAX)
+        return bad.item() == 0.0
 
     def upload(self):
         self.s.upload_tensor(0, self.coo.dims, self.idx, self.vals)
@@ -484,6 +497,12 @@ def run_engine(args):
             s.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
         job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, args.schedule, args.tokens,
                    args.cell_order == "runs")
+        if job.ring and not job.ring_ok():
+            print("bench: a DSGD ring wait timed out; falling back to the strata schedule",
+                  file=sys.stderr)
+            s.upload_model(coo.dims, ranks, j, a0, b0)
+            job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, "strata", args.tokens,
+                       args.cell_order == "runs")
     else:
         job = SingleGpu(eng, host, s, coo, ranks, j, a0, b0, world)
         job.upload()

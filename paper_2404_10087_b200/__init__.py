@@ -490,7 +490,7 @@ class Session:
     def ring_status(self) -> int:
         """Synchronises; nonzero if a ring wait timed out (the epoch is
         invalid): 0x10000 | flag id of the first stuck block wait, or
-        0x20000 | round of a stuck round-end copy."""
+        0x20000 | round of a stuck post (a block copy waiting for its cell)."""
         v = C.c_int(0)
         self._ck(self.lib.ftkcu_ring_status(self.h, C.byref(v)))
         return int(v.value)

@@ -2138,7 +2138,7 @@ int ftkcu_ring_factor_epoch(ftkcu_session* s, int slot, int parts, int rank,
   CK(cudaEventRecord(s->ev0, s->stream));
   CK(cudaMemcpyAsync(s->ring_tab, h, total, cudaMemcpyHostToDevice, s->stream));
   CK(cudaMemsetAsync(s->ring_done, 0, sizeof(unsigned) * ncell, s->stream));
-  CK(cudaMemsetAsync(s->ring_done + kRingFlags, 0, sizeof(unsigned) * P, s->stream));
+  CK(cudaMemsetAsync(s->ring_done + kRingFlags, 0, sizeof(unsigned) * (P + ncell), s->stream));
   CK(cudaMemsetAsync(s->ring_err, 0, sizeof(unsigned), s->stream));
   RingDev r;
   r.ncell = ncell;

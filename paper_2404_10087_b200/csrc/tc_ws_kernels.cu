@@ -162,16 +162,25 @@ __device__ __forceinline__ int64_t ws_tile(const WsParams& p, int64_t k) {
 }
 
 // ---- DSGD ring epoch (RingDev, engine.cuh) -----------------------------------
-// A CTA takes tiles b, b + G, ... of every cell in order; each role keeps its
-// own cursor over (cell, tile of the cell).
+// The cells' tiles, concatenated in cell order, are dealt round-robin over
+// the CTAs (CTA b takes tiles b, b + G, ... of the concatenation), so each
+// CTA's total is balanced to one tile even when every cell leaves a
+// remainder (a fixed start per cell gave CTAs 0..35 an extra tile in all 64
+// cells at P = 8); each role keeps its own cursor over (cell, tile of the cell).
+__device__ __forceinline__ uint32_t ring_cell_cta(const RingDev& r, int c) {
+  // this CTA's position in cell c's deal
+  const uint32_t off = (uint32_t)((__ldg(r.cell_tile + c) - __ldg(r.cell_tile)) % gridDim.x);
+  return (blockIdx.x + gridDim.x - off) % gridDim.x;
+}
 __device__ __forceinline__ int64_t ring_cell_nk(const RingDev& r, int c) {
   const uint32_t T = (uint32_t)(__ldg(r.cell_tile + c + 1) - __ldg(r.cell_tile + c));
-  return T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // 32-bit: < 2^32 tiles
+  const uint32_t b = ring_cell_cta(r, c);
+  return T > b ? (T - 1 - b) / gridDim.x + 1 : 0;  // 32-bit: < 2^32 tiles
 }
 struct RingCursor {
   int c = 0;
   int64_t j = 0, nk = 0;
-  int64_t base = 0, T = 1, mul = 1, add = 0;  // the current cell's tiles and permutation
+  int64_t base = 0, T = 1, mul = 1, add = 0, b = 0;  // the current cell's tiles, permutation, deal
   __device__ void enter(const RingDev& r, int c0) {
     j = 0;
     nk = 0;
@@ -182,10 +191,11 @@ struct RingCursor {
       T = __ldg(r.cell_tile + c + 1) - base;
       mul = __ldg(r.cell_perm + 2 * c);
       add = __ldg(r.cell_perm + 2 * c + 1);
+      b = ring_cell_cta(r, c);
     }
   }
   __device__ int64_t tile(const RingDev&) const {
-    const int64_t t = (int64_t)blockIdx.x + j * gridDim.x;
+    const int64_t t = b + j * gridDim.x;
     return base + (t * mul + add) % T;
   }
   __device__ void next(const RingDev& r) {
@@ -399,43 +409,48 @@ __device__ void ws_gather_producer(const WsParams& p, uint8_t* sm, uint64_t* bar
 // Ring epoch: this epilogue warp's write-backs of cell c are issued (and,
 // when the count is deferred by a tile, long since performed).  Each warp
 // counts itself in (G x kEpiWarps per cell) after a per-thread fence; the
-// warp that completes the count copies the cell's mode-3 block into the left
-// neighbour's factor matrices and raises its arrival flag.  A round's mode-2
-// block goes by ring_agent.
+// block copies to the left neighbour are ring_agent's.
 __device__ void ring_done(const WsParams& p, int c, int lane) {
   const RingDev& r = p.ring;
   if (!(ws_exp(p) & 64)) __threadfence();  // this thread's REDs of the cell before the count (exp 64: timing only)
   __syncwarp();
-  unsigned last = 0;
-  if (lane == 0) last = atomicAdd(r.done + c, 1u) == gridDim.x * kEpiWarps - 1;
-  if (!__shfl_sync(0xffffffffu, last, 0)) return;
-  __threadfence();  // every warp's REDs of the cell are visible from here on
-  const int post = __ldg(r.cell_io + c).z;
-  if (post < 0) return;
-  const int4 pd = __ldg(r.posts + post);  // {mode, row0, nrows, peer flag}
-  const float4* src = reinterpret_cast<const float4*>(p.a[pd.x] + (size_t)pd.y * kW);
-  float4* dst = reinterpret_cast<float4*>(r.peer_a[pd.x] + (size_t)pd.y * kW);
-  const int n4 = pd.z * (kW / 4);
-#pragma unroll 8
-  for (int i = lane; i < n4; i += 32) dst[i] = __ldcg(src + i);
-  __threadfence_system();
-  __syncwarp();
-  if (lane == 0) st_release_sys(r.peer_flags + pd.w, r.epoch);
+  if (lane == 0) atomicAdd(r.done + c, 1u);
 }
 
-// Ring epoch, warp kRingWarp of every CTA: after round s has been counted in
-// by every epilogue warp of the grid (its last cell's count, signalled
-// without deferral), copy this CTA's slice of the round's mode-2 block into
-// the left neighbour's factor matrix; the CTA that completes the copy count
-// raises the neighbour's flag.  Polls with a sleep, off the sweep's path.
+// One post, spread over the grid: this CTA's slice of the block's rows goes
+// to the left neighbour's factor matrix; the CTA that completes the copy
+// count raises the neighbour's flag.
+__device__ void ring_post_slice(const RingDev& r, const WsParams& p, int post, unsigned* count,
+                                int lane) {
+  const int4 pd = __ldg(r.posts + post);  // {mode, row0, nrows, peer flag}
+  const int64_t n4 = (int64_t)pd.z * (kW / 4);
+  const int64_t lo = n4 * blockIdx.x / gridDim.x, hi = n4 * (blockIdx.x + 1) / gridDim.x;
+  const float4* src = reinterpret_cast<const float4*>(p.a[pd.x] + (size_t)pd.y * kW);
+  float4* dst = reinterpret_cast<float4*>(r.peer_a[pd.x] + (size_t)pd.y * kW);
+#pragma unroll 4
+  for (int64_t i = lo + lane; i < hi; i += 32) dst[i] = __ldcg(src + i);
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0 && atomicAdd(count, 1u) == gridDim.x - 1) {
+    __threadfence_system();
+    st_release_sys(r.peer_flags + pd.w, r.epoch);
+  }
+}
+
+// Ring epoch, warp kRingWarp of every CTA: walks the cells in order; once a
+// cell with a post has been counted in by every epilogue warp of the grid,
+// copies this CTA's slice of the cell's mode-3 block (and, at a round's end,
+// of the round's mode-2 block) to the left neighbour (ring_post_slice).
+// Spreading a post over all CTAs keeps it off the epilogue warps: copied by
+// the one warp that completed the count, a 273-row block took ~10 us and
+// stalled that CTA's sweep at every cell.  Polls with a short sleep.
 __device__ void ring_agent(const WsParams& p, int lane) {
   const RingDev& r = p.ring;
   const int Q = r.ncell / r.parts;
   const unsigned want = gridDim.x * kEpiWarps;
-  for (int sr = 0; sr < r.parts; ++sr) {
-    const int c = sr * Q + Q - 1;
-    const int post = __ldg(r.cell_io + c).w;
-    if (post < 0) continue;
+  for (int c = 0; c < r.ncell; ++c) {
+    const int4 io = __ldg(r.cell_io + c);
+    if (io.z < 0 && io.w < 0) continue;
     if (lane == 0) {
       const long long t0 = clock64();
       unsigned v;
@@ -443,26 +458,15 @@ __device__ void ring_agent(const WsParams& p, int lane) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(r.done + c) : "memory");
         if (v >= want) break;
         if (clock64() - t0 > r.timeout_cycles) {
-          atomicCAS(r.err, 0u, 0x20000u | (unsigned)sr);
+          atomicCAS(r.err, 0u, 0x20000u | (unsigned)(c / Q));
           break;
         }
-        __nanosleep(256);
+        __nanosleep(64);
       }
     }
     __syncwarp();
-    const int4 pd = __ldg(r.posts + post);
-    const int64_t n4 = (int64_t)pd.z * (kW / 4);
-    const int64_t lo = n4 * blockIdx.x / gridDim.x, hi = n4 * (blockIdx.x + 1) / gridDim.x;
-    const float4* src = reinterpret_cast<const float4*>(p.a[pd.x] + (size_t)pd.y * kW);
-    float4* dst = reinterpret_cast<float4*>(r.peer_a[pd.x] + (size_t)pd.y * kW);
-#pragma unroll 4
-    for (int64_t i = lo + lane; i < hi; i += 32) dst[i] = __ldcg(src + i);
-    __threadfence_system();
-    __syncwarp();
-    if (lane == 0 && atomicAdd(r.copied + sr, 1u) == gridDim.x - 1) {
-      __threadfence_system();
-      st_release_sys(r.peer_flags + pd.w, r.epoch);
-    }
+    if (io.z >= 0) ring_post_slice(r, p, io.z, r.copied + r.parts + c, lane);
+    if (io.w >= 0) ring_post_slice(r, p, io.w, r.copied + c / Q, lane);
   }
 }
 
