@@ -66,10 +66,12 @@ def parse():
     ap.add_argument("--dsgd", action="store_true",
                     help="DSGD cell path even at 1 GPU (always used for order 3 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--schedule", default="ring", choices=["strata", "ring"],
+    ap.add_argument("--schedule", default="auto", choices=["auto", "strata", "ring"],
                     help="DSGD factor schedule at N > 1 (ring: mode-3 blocks passed over CUDA-IPC "
                          "peer memory inside one persistent kernel, falling back to the strata "
-                         "if a wait times out; strata: P*P cell launches + NCCL shifts)")
+                         "if a wait times out; strata: P*P cell launches + NCCL shifts; auto: "
+                         "the strata at N = 2, where a cell is 12M nonzeros and the stops are "
+                         "cheap, the ring above)")
     ap.add_argument("--tokens", type=int, default=1, help="ring: mode-3 blocks per rank")
     ap.add_argument("--runs", type=int, default=0, choices=[-1, 0, 1],
                     help="Hogwild stream in 16-nonzero last-mode runs (session option runs)")
@@ -495,7 +497,8 @@ def run_engine(args):
                                            dtype=torch.uint8))
             torch.distributed.broadcast(uid, 0)
             s.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
-        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, args.schedule, args.tokens,
+        sched = args.schedule if args.schedule != "auto" else ("strata" if world <= 2 else "ring")
+        job = Dsgd(eng, host, s, coo, ranks, j, a0, b0, world, rank, sched, args.tokens,
                    args.cell_order == "runs")
         if job.ring and not job.ring_ok():
             print("bench: a DSGD ring wait timed out; falling back to the strata schedule",
@@ -624,7 +627,9 @@ def run_engine(args):
                                     "accumulate": "f32"},
                        "parallelism": job.parallelism, "nnz_per_rank": job.local_nnz,
                        "test_frac": cfg.get("test_frac", 0.014),
-                       "l2": "inputs larger than L2 (COO stream 16 B/nnz per sweep)"},
+                       "l2": "no flush between steps: the COO tile stream (16 B/nnz per sweep) "
+                             "is larger than L2; the factor rows stay L2-resident when they fit "
+                             "(C2: 64 MB of the 126 MB L2; C3: 208 MB do not)"},
             "phases_ms": {"factor": f_avg, "core": c_avg},
             "train_loss_before_after": [loss0, loss1],
             "test_rmse_before_after": [test0[0], test1[0]],
@@ -638,7 +643,8 @@ def run_engine(args):
                                     wb, datagen.algorithmic_bytes_per_nnz(order, ranks),
                                     {"factor": f_avg, "core": c_avg},
                                     {"factor": f_bytes, "core": c_bytes,
-                                     "core_rows": job.local_nnz * order}),
+                                     "core_rows": job.local_nnz * order},
+                                    sum(int(d) * r * 4 for d, r in zip(coo.dims, ranks))),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -699,16 +705,31 @@ def time_variant(job, s, eng, host, ext, torch, args, a0, b0, opts, barrier):
             if opts.get("precision") == eng.PREC_3XTF32 else None}
 
 
-def roofline_of(dom, dom_ms, dom_bytes, achieved, peak, peak_kind, traffic, wb, bpn, ms, nbytes):
+L2_RESIDENT_MAX = 96e6  # factor rows up to here stay in the 126 MB L2 (C2: 64 MB; C3: 208 MB)
+
+
+def roofline_of(dom, dom_ms, dom_bytes, achieved, peak, peak_kind, traffic, wb, bpn, ms, nbytes,
+                a_bytes=0):
     """The dominant kernel against the ceiling that binds it.  At the
     Netflix shape the factor rows are L2-resident (ncu: DRAM ~4 % busy), so
     algorithmic bytes over HBM peak exceeds 1 and says nothing; the binding
     ceiling is the L2 atomic (RED) rate of the sweep's own write-back,
-    measured live on the same tile stream.  The HBM view stays alongside."""
+    measured live on the same tile stream.  When the rows do not fit L2
+    (Yahoo: 208 MB) the sweep is HBM-bound: its fraction is the ncu DRAM
+    bytes per launch (`traffic`) over the live kernel time against the
+    measured HBM peak (algorithmic bytes would count the L2 hits of the
+    small modes).  The algorithmic HBM view stays alongside."""
     hbm = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
            "peak_source": peak_kind, "algorithmic_bytes_per_launch": dom_bytes,
            "bytes_per_nnz_epoch": bpn,
            "per_kernel_frac": {k: nbytes[k] / (ms[k] * 1e-3) / 1e9 / peak for k in ms}}
+    if a_bytes > L2_RESIDENT_MAX and dom_ms > 0 and traffic:
+        dram = traffic / (dom_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "kernel": dom, "achieved": dram, "peak": peak, "unit": "GB/s",
+                "frac": dram / peak, "peak_source": peak_kind,
+                "achieved_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                   "(profiles/ncu_traffic.json) / live kernel time",
+                "factor_rows_bytes": a_bytes, "traffic": traffic, "algorithmic": hbm}
     if wb is None or dom_ms <= 0:
         out = {"bound": "hbm", "kernel": dom}
         out.update(hbm)

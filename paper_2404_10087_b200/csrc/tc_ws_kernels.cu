@@ -443,7 +443,9 @@ __device__ void ring_post_slice(const RingDev& r, const WsParams& p, int post, u
 // of the round's mode-2 block) to the left neighbour (ring_post_slice).
 // Spreading a post over all CTAs keeps it off the epilogue warps: copied by
 // the one warp that completed the count, a 273-row block took ~10 us and
-// stalled that CTA's sweep at every cell.  Polls with a short sleep.
+// stalled that CTA's sweep at every cell.  Polls with an exponential
+// back-off (32 ns .. 1 us): 148 agents polling one counter every 64 ns put
+// a hot line in L2 beside the sweep's REDs for the whole of a long cell.
 __device__ void ring_agent(const WsParams& p, int lane) {
   const RingDev& r = p.ring;
   const int Q = r.ncell / r.parts;
@@ -453,7 +455,7 @@ __device__ void ring_agent(const WsParams& p, int lane) {
     if (io.z < 0 && io.w < 0) continue;
     if (lane == 0) {
       const long long t0 = clock64();
-      unsigned v;
+      unsigned v, ns = 32;
       while (true) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(r.done + c) : "memory");
         if (v >= want) break;
@@ -461,7 +463,8 @@ __device__ void ring_agent(const WsParams& p, int lane) {
           atomicCAS(r.err, 0u, 0x20000u | (unsigned)(c / Q));
           break;
         }
-        __nanosleep(64);
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
       }
     }
     __syncwarp();

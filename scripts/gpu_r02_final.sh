@@ -11,9 +11,5 @@ timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_
 timeout 900 python bench.py --impl reference > gpurun_out/${tag}_bench_ref.json 2> gpurun_out/${tag}_bench_ref.err
 bash scripts/gpu_evidence.sh ${tag}_final > /dev/null 2>&1
 rm -f gpurun_out/sweep_${tag}.jsonl; bash scripts/config_sweep.sh ${tag} > /dev/null 2>&1
-rm -f gpurun_out/ring_emu.jsonl
-for P in 2 4 8; do
-  timeout 300 python scripts/dsgd_emulate.py --parts $P --schedule strata >> gpurun_out/${tag}_dsgd_emu.jsonl 2>/dev/null
-  timeout 300 python scripts/dsgd_emulate.py --parts $P --schedule ring --tokens 1 >> gpurun_out/${tag}_dsgd_emu.jsonl 2>/dev/null
-done
+bash scripts/dsgd_table.sh > /dev/null 2>&1; cp gpurun_out/dsgd_table.jsonl gpurun_out/${tag}_dsgd_emu.jsonl
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
