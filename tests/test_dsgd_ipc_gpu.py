@@ -18,6 +18,7 @@ import tempfile
 
 import numpy as np
 import pytest
+import torch  # noqa: F401  (before libftkcu: torch must bind its own NCCL first)
 
 pytestmark = pytest.mark.gpu
 
