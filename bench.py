@@ -421,10 +421,11 @@ class Dsgd(SingleGpu):
 
         try:
             self.factor(self.host.derive_seed(3, [0]))
-            bad = torch.tensor([1.0 if self.s.ring_status() else 0.0])
+            bad = 1.0 if self.s.ring_status() else 0.0
         except Exception as e:  # noqa: BLE001
             print(f"bench: ring probe failed: {e}", file=sys.stderr)
-            bad = torch.tensor([1.0])
+            bad = 1.0
+        bad = torch.tensor([bad], device=torch.device("cuda", torch.cuda.current_device()))
         tdist.all_reduce(bad, op=tdist.ReduceOp.MAX)
         return bad.item() == 0.0
 
