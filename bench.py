@@ -80,6 +80,9 @@ def parse():
                          "same-row updates of the small mode) or plain random order")
     ap.add_argument("--e2e-keys", default="delta", choices=["delta", "packed", "int32"],
                     help="COO index format on the host-to-device link in the e2e loop")
+    ap.add_argument("--delta-decode", type=int, default=0, choices=[0, 1],
+                    help="delta-coded e2e uploads: 0 decode beside the running epochs, 1 at "
+                         "first use on the session stream (session option delta_decode)")
     ap.add_argument("--e2e-sync", action="store_true",
                     help="e2e without the double-buffered asynchronous tensor upload")
     ap.add_argument("--no-cpu", action="store_true")
@@ -487,6 +490,7 @@ def run_engine(args):
     s.set_option("core16", args.core16)
     s.set_option("factor_warps", args.factor_warps)
     s.set_option("runs", args.runs)
+    s.set_option("delta_decode", args.delta_decode)
     # the reference CLI's init (ftk.cpp:169-173): mean |x| over the training values
     scale = host.default_init_scale(float(np.mean(np.abs(coo.vals.astype(np.float64)))), order, j,
                                     ranks)

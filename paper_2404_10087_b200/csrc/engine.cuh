@@ -64,6 +64,12 @@ struct DevTensor {
   int* d_bad = nullptr;
   cudaEvent_t ready = nullptr;
   bool pending = false;
+  // delta-coded upload decoded at first use on the session stream (option
+  // delta_decode = 1): the staging holds the deltas, then the restarts
+  bool delta_pending = false, delta_scatter = false;
+  int delta_width = 0;
+  size_t delta_roff = 0;
+  uint64_t delta_seed = 0;
   // Recorded on the session stream when another slot's work begins: every
   // kernel that read this slot precedes it, so an asynchronous re-upload
   // waits for exactly that (and not for work on other slots).

@@ -63,7 +63,12 @@ struct ftkcu_session {
   // sort costs the e2e loop ~5 ms per epoch
   int64_t opt_runs = 0;
   int64_t opt_cell_order = 0;
-  int64_t opt_eager_stream = 1;  // delta-coded uploads scatter the tile stream while decoding  // 1: ftkcu_tensor_set_cells keeps each cell's uploaded order
+  int64_t opt_eager_stream = 1;  // delta-coded uploads scatter the tile stream while decoding
+  // delta-coded uploads: 0 decode beside the running epochs (decode stream,
+  // part by part as the bytes land), 1 decode at first use on the session
+  // stream (serial with the epochs; measured slower in the e2e loop, 4.4e9 vs
+  // 5.1e9 nnz/s)
+  int64_t opt_delta_decode = 0;  // 1: ftkcu_tensor_set_cells keeps each cell's uploaded order
   int64_t opt_window = 0;  // headline factor sweep read-to-write window in tiles (0 = ring depth)
   // Whole-tensor factor sweeps: cap the grid so that at most this many
   // nonzeros per row of the smallest mode are in flight (0 = off).  See
@@ -240,6 +245,15 @@ __global__ void keys_to_soa_kernel(const uint32_t* __restrict__ lo, const void* 
   }
 }
 
+// Device-to-device copy on the SMs (the read-back snapshot): a copy-engine
+// memcpy of the 64 MB model takes ~0.8 ms beside a concurrent upload on the
+// copy engines, this ~0.05 ms.
+__global__ void copy16_kernel(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcs(src + i);
+}
+
 // A rows of the probe batch after the update (ftkcu_batch_probe A_new).
 __global__ void gather_rows_kernel(KView v, const int64_t* __restrict__ rows, int m_eff,
                                    int cap, int jmax, float* __restrict__ out) {
@@ -278,6 +292,19 @@ int finish_upload(ftkcu_session* s, DevTensor& t) {
   if (!t.pending) return FTKCU_OK;
   t.pending = false;
   CK(cudaStreamWaitEvent(s->stream, t.ready, 0));
+  if (t.delta_pending) {
+    // the decode (and the tile-stream scatter) of a delta-coded upload, on
+    // the session stream behind the epochs already enqueued: serial with
+    // them instead of contending for L2 and HBM beside them
+    t.delta_pending = false;
+    const int64_t chunks = (t.nnz + kDeltaChunk - 1) / kDeltaChunk;
+    const uint8_t* st = reinterpret_cast<const uint8_t*>(t.staging);
+    CK(launch_delta_decode(t, st, reinterpret_cast<const uint64_t*>(st + t.delta_roff),
+                           t.delta_width, 0, chunks, t.delta_scatter, t.delta_seed, t.d_bad,
+                           s->stream));
+    if (t.delta_scatter) CK(finish_scatter_stream(t, s->stream));
+    CK(cudaEventRecord(t.ready, s->stream));
+  }
   CK(cudaEventSynchronize(t.ready));
   int h_bad = 0;
   CK(cudaMemcpy(&h_bad, t.d_bad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -539,6 +566,9 @@ int ftkcu_set_option(ftkcu_session* s, const char* key, int64_t value) {
     for (auto& t : s->slots) t.shuffled = false;
   } else if (k == "eager_stream") {
     s->opt_eager_stream = value != 0;
+  } else if (k == "delta_decode") {
+    if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "delta_decode must be 0 or 1");
+    s->opt_delta_decode = value;
   } else if (k == "cell_order") {
     if (value != 0 && value != 1) return fail(s, FTKCU_ERR_ARG, "cell_order must be 0 or 1");
     s->opt_cell_order = value;
@@ -576,6 +606,7 @@ int ftkcu_get_option(ftkcu_session* s, const char* key, int64_t* value) {
   else if (k == "cell_order") *value = s->opt_cell_order;
   else if (k == "runs") *value = s->opt_runs;
   else if (k == "eager_stream") *value = s->opt_eager_stream;
+  else if (k == "delta_decode") *value = s->opt_delta_decode;
   else if (k == "staleness") *value = s->opt_staleness;
   else if (k == "graphs") *value = s->opt_graphs;
   else if (k == "global_nnz") *value = s->global_nnz;
@@ -956,6 +987,24 @@ int ftkcu_tensor_upload_delta_async(ftkcu_session* s, int slot, int order, const
   const uint64_t* rs_dev = reinterpret_cast<const uint64_t*>(st + dpad);
   CK(cudaMemsetAsync(t.d_bad, 0, sizeof(int), s->copy_stream));
   CK(cudaMemcpyAsync(st + dpad, restarts, rb, cudaMemcpyHostToDevice, s->copy_stream));
+  if (s->opt_delta_decode == 1) {
+    // copies only; decoded at the slot's first use (finish_upload)
+    CK(cudaMemcpyAsync(st, deltas, db, cudaMemcpyHostToDevice, s->copy_stream));
+    CK(cudaMemcpyAsync(t.vals, values, sizeof(float) * nnz, cudaMemcpyHostToDevice,
+                       s->copy_stream));
+    CK(cudaEventRecord(t.ready, s->copy_stream));
+    t.delta_pending = true;
+    t.delta_scatter = scatter;
+    t.delta_width = width;
+    t.delta_roff = dpad;
+    t.delta_seed = (uint64_t)s->opt_shuffle_seed;
+    if (scatter) {
+      t.shuffled = true;  // the stream is built with the decode
+      t.runs = false;
+    }
+    t.pending = true;
+    return FTKCU_OK;
+  }
   const int64_t per = (chunks + kDeltaParts - 1) / kDeltaParts;
   for (int part = 0; part < kDeltaParts; ++part) {
     const int64_t c0 = std::min<int64_t>(chunks, part * per), c1 = std::min<int64_t>(chunks, c0 + per);
@@ -1089,13 +1138,24 @@ int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, flo
     std::vector<std::pair<float*, const float*>> parts;  // (host, snapshot)
     for (int n = 0; n < m.order; ++n) {
       const size_t an = (size_t)m.dims[n] * m.ranks[n], bn = (size_t)m.ranks[n] * m.r;
+      auto dcopy = [&](float* dst, const float* src, size_t nf) -> cudaError_t {
+        if (nf % 4 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+          return cudaMemcpyAsync(dst, src, sizeof(float) * nf, cudaMemcpyDeviceToDevice, s->stream);
+        const int64_t n4 = (int64_t)(nf / 4);
+        int64_t blocks = (n4 + 255) / 256;
+        if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+        if (blocks < 1) return cudaSuccess;
+        copy16_kernel<<<(int)blocks, 256, 0, s->stream>>>(reinterpret_cast<const float4*>(src),
+                                                          reinterpret_cast<float4*>(dst), n4);
+        return cudaGetLastError();
+      };
       if (A && A[n]) {
-        CK(cudaMemcpyAsync(snap, m.a[n], sizeof(float) * an, cudaMemcpyDeviceToDevice, s->stream));
+        CK(dcopy(snap, m.a[n], an));
         parts.push_back({A[n], snap});
       }
       snap += an;
       if (B && B[n]) {
-        CK(cudaMemcpyAsync(snap, m.b[n], sizeof(float) * bn, cudaMemcpyDeviceToDevice, s->stream));
+        CK(dcopy(snap, m.b[n], bn));
         parts.push_back({B[n], snap});
       }
       snap += bn;

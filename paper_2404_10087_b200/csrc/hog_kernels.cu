@@ -141,10 +141,15 @@ struct DeltaDecode {
   int* bad;
 };
 
-__global__ void __launch_bounds__(kDeltaThreads) delta_decode_kernel(DeltaDecode d, int64_t c0) {
+// <= 85 registers (3 blocks per SM): a block must fit beside the factor
+// sweep's persistent CTA (384 threads x 112 registers), or the decode of the
+// next upload waits for the epoch to end
+__global__ void __launch_bounds__(kDeltaThreads, 3)
+    delta_decode_kernel(DeltaDecode d, int64_t c0, int64_t c1) {
   using Scan = cub::BlockScan<uint64_t, kDeltaThreads>;
   __shared__ typename Scan::TempStorage scan;
-  const int64_t c = c0 + blockIdx.x;
+  for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
+  __syncthreads();  // the scan storage of the previous chunk
   const int64_t e0 = c * kDeltaChunk + (int64_t)threadIdx.x * kDeltaPer;
   const int w = d.width;
   uint64_t run[kDeltaPer];
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(kDeltaThreads) delta_decode_kernel(DeltaDecode
              make_int4(ix[0], ix[1], ix[2], __float_as_int(__ldcs(d.vals + e))));
   }
   if (flag) atomicExch(d.bad, 1);
+  }
 }
 
 // ---- stream in last-mode runs -------------------------------------------------
@@ -800,7 +806,15 @@ cudaError_t launch_delta_decode(DevTensor& t, const uint8_t* deltas, const uint6
     d.rec = t.rec16;
     cell_shuffle_params(t.nnz, seed, 0, &d.bits, &d.seed);
   }
-  delta_decode_kernel<<<(unsigned)(c1 - c0), kDeltaThreads, 0, st>>>(d, c0);
+  // a capped grid (a few blocks per SM) when the decode runs beside an
+  // epoch: fewer resident blocks take fewer issue slots from its sweeps
+  static const int64_t cap = [] {
+    const char* e = getenv("FTKCU_DECODE_GRID");
+    return e ? atoll(e) : 0ll;
+  }();
+  int64_t grid = c1 - c0;
+  if (cap > 0 && grid > cap) grid = cap;
+  delta_decode_kernel<<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1);
   return cudaGetLastError();
 }
 

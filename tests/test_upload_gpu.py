@@ -124,8 +124,9 @@ def test_packed_key_upload_epoch_bit_identical(session):
         session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
 
 
+@pytest.mark.parametrize("decode", [0, 1], ids=["concurrent", "at-first-use"])
 @pytest.mark.parametrize("nnz", [20000, 4096, 37])
-def test_delta_upload_matches_int32_upload(session, nnz):
+def test_delta_upload_matches_int32_upload(session, nnz, decode):
     """ftkcu_tensor_upload_delta_async (the e2e link format, 3 B of key per
     nonzero at the Netflix shape): the device tensor equals the int32 upload
     of the same sorted tensor, so a deterministic epoch is bit-identical;
@@ -143,6 +144,7 @@ def test_delta_upload_matches_int32_upload(session, nnz):
     plan1 = host.global_plan(nnz, 16, 3)
     plan2 = host.global_plan(nnz, 16, 4)
     out = []
+    session.set_option("delta_decode", decode)
     for delta in (False, True):
         session.upload_model(dims, ranks, r, a, b)
         if delta:
@@ -166,6 +168,7 @@ def test_delta_upload_matches_int32_upload(session, nnz):
                                           vh.data_ptr())
     with pytest.raises(eng.FtkError, match="out of range"):
         session.factor_phase(3, None, 16, 1e-3, 1e-4, eng.MODE_HOGWILD, seed=1)
+    session.set_option("delta_decode", 0)
 
 
 @pytest.mark.parametrize("nnz", [300000, 5000])
@@ -189,8 +192,9 @@ def test_delta_upload_scattered_stream_equals_gather_build(nnz):
     s = eng.Session(0)
     try:
         s.set_option("precision", eng.PREC_TF32)
-        for how in ("int32", "delta", "delta-lazy"):
+        for how in ("int32", "delta", "delta-concurrent", "delta-lazy"):
             s.set_option("eager_stream", 0 if how == "delta-lazy" else 1)
+            s.set_option("delta_decode", 0 if how == "delta-concurrent" else 1)
             s.upload_model(dims, [32] * 3, 32, a, b)
             if how == "int32":
                 s.upload_tensor(2, dims, idx[o], vals[o])
