@@ -125,6 +125,12 @@ struct DeviceOptions {
   // bit-exact fp32 whatever this says.
   DevicePrecision precision = DevicePrecision::kTf32;
   bool exact_eval = true;          // reference slab order in loss/evaluate
+  // Hogwild at the reference's asynchrony noise floor: at most 3 tiles per
+  // CTA between reading a row and writing it back (session option window =
+  // 3) on half the SMs (max_ctas) -- on unlearnable (uniform) values the
+  // full grid's ~57K nonzeros in flight raise the test RMSE by 3-4e-3, this
+  // by < 1e-3, at about 2x the epoch time (bench.py's `parity` variant).
+  bool parity = false;
 };
 
 void set_device_options(const DeviceOptions& o);

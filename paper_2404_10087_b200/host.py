@@ -77,7 +77,7 @@ def lib():
     L.ftkh_load_coo_binary.argtypes = [C.c_char_p]
     L.ftkh_tensor_order.argtypes = [C.c_void_p]
     L.ftkh_save_coo_binary.argtypes = [C.c_int, _i32p, C.c_int64, _i32p, _f32p, C.c_char_p]
-    L.ftkh_set_device_options.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    L.ftkh_set_device_options.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
     L.ftkh_epoch_plus.argtypes = [C.c_int, _i32p, _i32p, C.c_int32, C.c_int64, _i32p, _f32p,
                                   _fpp, _fpp, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
                                   C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p, _i64p]
@@ -227,10 +227,11 @@ def save_coo(dims, idx, vals, path):
                             _p(vals, _f32p), path.encode()))
 
 
-def set_device_options(device=-1, mode=0, precision=1, exact_eval=True):
+def set_device_options(device=-1, mode=0, precision=1, exact_eval=True, parity=False):
     """mode 0 auto / 1 deterministic / 2 hogwild; precision 0 fp32 / 1 tf32
-    (the C++ default) / 2 3xtf32."""
-    _ck(lib().ftkh_set_device_options(device, mode, precision, int(exact_eval)))
+    (the C++ default) / 2 3xtf32; parity: Hogwild at the reference's
+    asynchrony noise floor (ftk::DeviceOptions::parity)."""
+    _ck(lib().ftkh_set_device_options(device, mode, precision, int(exact_eval), int(parity)))
 
 
 def last_kernels():

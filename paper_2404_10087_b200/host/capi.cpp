@@ -178,13 +178,14 @@ int ftkh_save_coo(int order, const int32_t* dims, int64_t nnz, const int32_t* id
   return guarded([&] { save_coo(make_tensor(order, dims, nnz, idx, vals), path); });
 }
 
-int ftkh_set_device_options(int device, int mode, int precision, int exact_eval) {
+int ftkh_set_device_options(int device, int mode, int precision, int exact_eval, int parity) {
   return guarded([&] {
     DeviceOptions o;
     o.device = device;
     o.mode = static_cast<DeviceMode>(mode);
     o.precision = static_cast<DevicePrecision>(precision);
     o.exact_eval = exact_eval != 0;
+    o.parity = parity != 0;
     set_device_options(o);
   });
 }

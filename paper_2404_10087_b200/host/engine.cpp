@@ -70,6 +70,10 @@ void apply_options(ftkcu_session* s) {
                                                                 : FTKCU_PREC_3XTF32;
   check(ftkcu_set_option(s, "precision", prec));
   check(ftkcu_set_option(s, "eval", g_opts.exact_eval ? FTKCU_EVAL_EXACT : FTKCU_EVAL_FAST));
+  int64_t sms = 0;
+  check(ftkcu_get_option(s, "num_sms", &sms));
+  check(ftkcu_set_option(s, "window", g_opts.parity ? 3 : 0));
+  check(ftkcu_set_option(s, "max_ctas", g_opts.parity ? std::max<int64_t>(1, sms / 2) : 0));
 }
 
 // Content hash of every index and value byte (a sampled

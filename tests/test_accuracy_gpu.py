@@ -259,17 +259,20 @@ def c1p32_problem():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("prec", [eng.PREC_TF32, eng.PREC_3XTF32], ids=["tf32", "3xtf32"])
-def test_c1p32_rmse_trajectory_vs_reference(prec):
+@pytest.mark.parametrize("prec,parity", [(eng.PREC_TF32, False), (eng.PREC_3XTF32, False),
+                                         (eng.PREC_TF32, True)],
+                         ids=["tf32", "3xtf32", "tf32-parity"])
+def test_c1p32_rmse_trajectory_vs_reference(prec, parity):
     """ftk::train, Hogwild, through the J = R = 32 kernels the headline runs:
-    test RMSE within 1e-3 of the reference's workers = 1 run at EVERY epoch."""
+    test RMSE within 1e-3 of the reference's workers = 1 run at EVERY epoch
+    (also with ftk::DeviceOptions::parity: window 3 on half the SMs)."""
     z = load("c1p32_trajectory")
     dims, (tri, trv), (tei, tev), a0, b0, scale = c1p32_problem()
     assert trv.size == int(z["ntrain"]) and tev.size == int(z["ntest"])
     assert np.float32(scale) == z["scale"]
     ref = z["w1_rmse"]
     epochs = ref.size
-    host.set_device_options(mode=2, precision=prec, exact_eval=True)
+    host.set_device_options(mode=2, precision=prec, exact_eval=True, parity=parity)
     try:
         a, b = [x.copy() for x in a0], [x.copy() for x in b0]
         h = host.train(dims, [32] * 3, 32, tri, trv, tei, tev, a, b, epochs=epochs, seed=1,
