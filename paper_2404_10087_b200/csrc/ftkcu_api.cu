@@ -1135,7 +1135,6 @@ int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, flo
     }
     if (s->rb_pending) CK(cudaStreamWaitEvent(s->stream, s->rb_done, 0));
     float* snap = s->rb_buf[0];
-    std::vector<std::pair<float*, const float*>> parts;  // (host, snapshot)
     for (int n = 0; n < m.order; ++n) {
       const size_t an = (size_t)m.dims[n] * m.ranks[n], bn = (size_t)m.ranks[n] * m.r;
       auto dcopy = [&](float* dst, const float* src, size_t nf) -> cudaError_t {
@@ -1149,15 +1148,9 @@ int ftkcu_model_copy_async(ftkcu_session* s, int to_device, float* const* A, flo
                                                           reinterpret_cast<float4*>(dst), n4);
         return cudaGetLastError();
       };
-      if (A && A[n]) {
-        CK(dcopy(snap, m.a[n], an));
-        parts.push_back({A[n], snap});
-      }
+      if (A && A[n]) CK(dcopy(snap, m.a[n], an));
       snap += an;
-      if (B && B[n]) {
-        CK(dcopy(snap, m.b[n], bn));
-        parts.push_back({B[n], snap});
-      }
+      if (B && B[n]) CK(dcopy(snap, m.b[n], bn));
       snap += bn;
     }
     CK(cudaEventRecord(s->rb_snap, s->stream));
