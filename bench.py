@@ -874,6 +874,10 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
     return out or None
 
 
+# e2e tensor slots (slot 0: the device-timed tensor; 4 / 5: the RMSE check)
+E2E_SLOTS = (2, 3, 6)
+
+
 def time_e2e(job, a0, b0, args, torch, world, dev):
     """Same epochs through the C-ABI from pinned host buffers, host<->device
     copies of every step's inputs (this rank's COO share + model) and result
@@ -929,8 +933,14 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     b_h = [torch.from_numpy(x.copy()).pin_memory() for x in b0]
     a_np = [x.numpy() for x in a_h]
     b_np = [x.numpy() for x in b_h]
-    # Single GPU: double-buffered tensor slots 2 / 3, step k + 1's COO copy
-    # (ftkcu_tensor_upload_async, copy stream) overlapping step k's epoch.
+    # Single GPU: tensor slots E2E_SLOTS in rotation, step k + 1's COO copy
+    # (ftkcu_tensor_upload_*_async, copy stream) overlapping step k's epoch.
+    # Three slots, not two: with two, step k+1's copy had to wait for epoch
+    # k-1 (the last reader of its slot), so the link idled between the end of
+    # copy k and the end of epoch k-1 (5.8 ms of an 18.5 ms step in the
+    # FTK_E2E_TRACE timeline) and the last parts of the upload were decoded
+    # after the core sweep instead of beside the factor sweep.
+    nsl = len(E2E_SLOTS)
     steps = max(1, args.steps if pipelined else min(args.steps, 3))
     h2d = key_bytes + vals.nbytes + (0 if pipelined else sum(x.nbytes for x in a_np + b_np))
     d2h = sum(x.nbytes for x in a_np + b_np)
@@ -938,7 +948,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
     if pipelined:
         # untimed: allocate both slots' device buffers (COO, staging, tile
         # stream) once; every timed step still copies its whole COO again
-        for sl in (2, 3):
+        for sl in E2E_SLOTS:
             upload_async(sl, idx_h.data_ptr(), val_h.data_ptr())
             job.slot = sl
             job.factor(host.derive_seed(5, [sl]))
@@ -973,7 +983,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
 
     mark("start")
     if pipelined:
-        upload_async(2, idx_h.data_ptr(), val_h.data_ptr())
+        upload_async(E2E_SLOTS[0], idx_h.data_ptr(), val_h.data_ptr())
         mark_copy("[copy] upload 0 copied")
     for k in range(steps):
         if not pipelined:
@@ -985,13 +995,13 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         if pipelined and k + 1 < steps:
             # step k+1's COO, enqueued before this step's epoch: the copy
             # engine streams it right behind step k's copy (it waits only for
-            # step k-1, the last epoch that read its slot), so the link stays
-            # busy while step k computes
-            upload_async(2 + (k + 1) % 2, idx_h.data_ptr(), val_h.data_ptr())
+            # step k+1-nsl, the last epoch that read its slot), so the link
+            # stays busy while step k computes
+            upload_async(E2E_SLOTS[(k + 1) % nsl], idx_h.data_ptr(), val_h.data_ptr())
             mark("next upload enqueued")
             mark_copy(f"[copy] upload {k + 1} copied")
         if pipelined:
-            job.slot = 2 + k % 2
+            job.slot = E2E_SLOTS[k % nsl]
         es = host.derive_seed(7, [k + 1])
         job.factor(es)
         mark("factor enqueued")
@@ -1008,8 +1018,8 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
         print(f"e2e gpu {tev[0][1].elapsed_time(ev):8.2f} ms {what}", file=sys.stderr)
     if pipelined:
         job.slot = 0
-        s.release_tensor(2)
-        s.release_tensor(3)
+        for sl in E2E_SLOTS:
+            s.release_tensor(sl)
     if world > 1:
         t = torch.tensor([dt], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -1025,7 +1035,7 @@ def time_e2e(job, a0, b0, args, torch, world, dev):
                     if keys is not None else "int32 per mode (16 B/nnz with values)",
             "path": (("ftkcu_tensor_upload_delta_async" if delta is not None else
                       "ftkcu_tensor_upload_packed_async" if keys is not None else
-                      "ftkcu_tensor_upload_async") + " into two alternating slots (step k+1's COO "
+                      "ftkcu_tensor_upload_async") + f" into {nsl} rotating slots (step k+1's COO "
                      "copy overlaps step k's epoch)" if pipelined else "ftkcu_tensor_upload")
                     + (" + factor/core phases + the model read back every step "
                        "(ftkcu_model_copy_async; the model stays resident)" if pipelined else
