@@ -144,6 +144,13 @@ struct DeltaDecode {
 // <= 85 registers (3 blocks per SM): a block must fit beside the factor
 // sweep's persistent CTA (384 threads x 112 registers), or the decode of the
 // next upload waits for the epoch to end
+//
+// kW > 0: the delta width at compile time.  A thread's kDeltaPer deltas are
+// kDeltaPer * kW contiguous, 16-B aligned bytes (chunk and thread offsets are
+// multiples of 16 entries), read as kW 16-B loads instead of kDeltaPer * kW
+// byte loads; the bytes are then picked out of registers.  kW = 0: any width,
+// byte loads (also the ragged last thread of a tensor).
+template <int kW>
 __global__ void __launch_bounds__(kDeltaThreads, 3)
     delta_decode_kernel(DeltaDecode d, int64_t c0, int64_t c1) {
   using Scan = cub::BlockScan<uint64_t, kDeltaThreads>;
@@ -151,19 +158,44 @@ __global__ void __launch_bounds__(kDeltaThreads, 3)
   for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
   __syncthreads();  // the scan storage of the previous chunk
   const int64_t e0 = c * kDeltaChunk + (int64_t)threadIdx.x * kDeltaPer;
-  const int w = d.width;
+  const int w = kW > 0 ? kW : d.width;
   uint64_t run[kDeltaPer];
   uint64_t sum = 0;
+  if (kW > 0 && e0 + kDeltaPer <= d.nnz) {
+    uint32_t wd[4 * (kW > 0 ? kW : 1)];
+    const uint4* q = reinterpret_cast<const uint4*>(d.deltas + e0 * kW);
 #pragma unroll
-  for (int i = 0; i < kDeltaPer; ++i) {
-    const int64_t e = e0 + i;
-    uint64_t x = 0;
-    if (e < d.nnz && (threadIdx.x | i)) {  // the chunk's first entry is its restart
-      const uint8_t* q = d.deltas + e * w;
-      for (int b = 0; b < w; ++b) x |= (uint64_t)__ldcs(q + b) << (8 * b);
+    for (int v = 0; v < (kW > 0 ? kW : 1); ++v) {
+      const uint4 x = __ldcs(q + v);
+      wd[4 * v] = x.x;
+      wd[4 * v + 1] = x.y;
+      wd[4 * v + 2] = x.z;
+      wd[4 * v + 3] = x.w;
     }
-    sum += x;
-    run[i] = sum;
+#pragma unroll
+    for (int i = 0; i < kDeltaPer; ++i) {
+      uint64_t x = 0;
+#pragma unroll
+      for (int b = 0; b < (kW > 0 ? kW : 1); ++b) {
+        const int at = i * kW + b;
+        x |= (uint64_t)((wd[at >> 2] >> (8 * (at & 3))) & 0xffu) << (8 * b);
+      }
+      if (!(threadIdx.x | i)) x = 0;  // the chunk's first entry is its restart
+      sum += x;
+      run[i] = sum;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kDeltaPer; ++i) {
+      const int64_t e = e0 + i;
+      uint64_t x = 0;
+      if (e < d.nnz && (threadIdx.x | i)) {  // the chunk's first entry is its restart
+        const uint8_t* q = d.deltas + e * w;
+        for (int b = 0; b < w; ++b) x |= (uint64_t)__ldcs(q + b) << (8 * b);
+      }
+      sum += x;
+      run[i] = sum;
+    }
   }
   uint64_t before;
   Scan(scan).ExclusiveSum(sum, before);
@@ -814,7 +846,12 @@ cudaError_t launch_delta_decode(DevTensor& t, const uint8_t* deltas, const uint6
   }();
   int64_t grid = c1 - c0;
   if (cap > 0 && grid > cap) grid = cap;
-  delta_decode_kernel<<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1);
+  switch (width) {
+    case 3: delta_decode_kernel<3><<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1); break;
+    case 4: delta_decode_kernel<4><<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1); break;
+    case 2: delta_decode_kernel<2><<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1); break;
+    default: delta_decode_kernel<0><<<(unsigned)grid, kDeltaThreads, 0, st>>>(d, c0, c1); break;
+  }
   return cudaGetLastError();
 }
 
