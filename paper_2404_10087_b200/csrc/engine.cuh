@@ -129,6 +129,10 @@ struct KView {
   // computed (stage_c_rows_from_cache, decomposition.cpp:299-314); null =
   // calculation scheme.
   const float* cc[kMaxOrder];
+  // fp16 operand copies of A (core16 sweeps): set to 1 when an entry is
+  // outside the fp16 range (|a| > 65504 or not finite) and was clamped by
+  // the satfinite conversion; mapped host memory, reported by the session
+  int* f16_range;
 };
 
 int num_sms();

@@ -27,6 +27,10 @@ struct ftkcu_session {
   std::vector<float*> rb_buf;
   size_t rb_floats = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // fp16 range flag of the core16 operand copies (KView::f16_range): mapped
+  // pinned memory, so the host reads it without a synchronisation
+  volatile int* f16_range_h = nullptr;
+  int* f16_range_d = nullptr;
   std::string err;
   DevTensor slots[8];
   int last_slot = -1;  // slot of the most recent phase / evaluation
@@ -143,6 +147,19 @@ int bind(ftkcu_session* s) {
   if (!s) return fail(nullptr, FTKCU_ERR_ARG, "null session");
   CK(cudaSetDevice(s->device));
   return FTKCU_OK;
+}
+
+// An fp16 operand copy of A clamped an entry in an earlier core phase
+// (core16 sweeps convert A with cvt.rn.satfinite): that phase's core gradient
+// is wrong, so the next core phase, evaluation, stream sync or model download
+// fails loudly instead of training on.  Cleared once reported; core16 = 0 runs
+// the core sweep on tf32 rows, which have the fp32 range.
+int check_f16_range(ftkcu_session* s) {
+  if (!s->f16_range_h || !*s->f16_range_h) return FTKCU_OK;
+  *s->f16_range_h = 0;
+  return fail(s, FTKCU_ERR_ARG,
+              "a factor entry exceeded the fp16 range (|a| > 65504 or not finite) in a core16 "
+              "sweep's operand copy and was clamped; set option core16 = 0 (tf32 rows)");
 }
 
 int ensure_scratch(ftkcu_session* s, size_t bytes) {
@@ -278,6 +295,7 @@ KView make_view(const ftkcu_session* s, const DevTensor& t, bool shuffled) {
     v.b[n] = m.b[n];
     v.idx[n] = shuffled ? t.sidx[n] : t.idx[n];
   }
+  v.f16_range = s->f16_range_d;
   v.vals = shuffled ? t.svals : t.vals;
   v.nnz = t.nnz;
   v.tile_rows = shuffled ? t.tile_rows : nullptr;
@@ -475,6 +493,14 @@ int ftkcu_session_create(int device, ftkcu_session** out) {
   for (auto& e : s->dec_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
       return fail(nullptr, FTKCU_ERR_CUDA, "event creation failed");
+  {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->f16_range_d), h, 0) != cudaSuccess)
+      return fail(nullptr, FTKCU_ERR_CUDA, "mapped flag allocation failed");
+    s->f16_range_h = static_cast<volatile int*>(h);
+    *s->f16_range_h = 0;
+  }
   *out = s;
   return FTKCU_OK;
 }
@@ -512,6 +538,7 @@ void ftkcu_session_destroy(ftkcu_session* s) {
   cudaStreamDestroy(s->copy_stream);
   cudaStreamDestroy(s->rb_stream);
   cudaStreamDestroy(s->dec_stream);
+  if (s->f16_range_h) cudaFreeHost(const_cast<int*>(s->f16_range_h));
   for (auto e : s->dec_ev)
     if (e) cudaEventDestroy(e);
   cudaEventDestroy(s->rb_snap);
@@ -1106,7 +1133,7 @@ int ftkcu_model_download(ftkcu_session* s, float* const* A, float* const* B) {
                          cudaMemcpyDeviceToHost, s->stream));
   }
   CK(cudaStreamSynchronize(s->stream));
-  return FTKCU_OK;
+  return check_f16_range(s);
 }
 
 // Enqueued model copies (pinned host buffers; no host synchronisation): the
@@ -1538,6 +1565,7 @@ int ftkcu_core_phase(ftkcu_session* s, int slot, const int64_t* perm, int32_t M,
                      float reg_b, int mode, uint64_t seed, float* grad_out, double* ms) {
   int rc = bind(s);
   if (rc) return rc;
+  if ((rc = check_f16_range(s))) return rc;
   if ((rc = check_ready(s, slot))) return rc;
   if (M < 1) return fail(s, FTKCU_ERR_ARG, "batch size must be positive");
   DevTensor& t = s->slots[slot];
@@ -1622,6 +1650,7 @@ int ftkcu_eval(ftkcu_session* s, int slot, int workers, double reg_a, double reg
                double* out3) {
   int rc = bind(s);
   if (rc) return rc;
+  if ((rc = check_f16_range(s))) return rc;
   if ((rc = check_ready(s, slot))) return rc;
   if (!out3) return fail(s, FTKCU_ERR_ARG, "null output");
   const DevTensor& t = s->slots[slot];
@@ -1837,7 +1866,7 @@ int ftkcu_stream_sync(ftkcu_session* s) {
   if (rc) return rc;
   CK(cudaStreamSynchronize(s->stream));
   CK(cudaStreamSynchronize(s->rb_stream));
-  return FTKCU_OK;
+  return check_f16_range(s);
 }
 
 int ftkcu_dsgd_factor_epoch(ftkcu_session* s, int slot, int parts, const int64_t* row_off2,

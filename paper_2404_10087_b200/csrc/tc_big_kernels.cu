@@ -1384,12 +1384,16 @@ __global__ void __launch_bounds__(b16p::kThreads, 1) big16p_core_kernel(const __
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-__global__ void big_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n2) {
+__global__ void big_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n2,
+                                int* __restrict__ range) {
+  bool out = false;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
        e += (int64_t)gridDim.x * blockDim.x) {
     const float2 x = reinterpret_cast<const float2*>(src)[e];
+    out |= !(fabsf(x.x) <= 65504.f) || !(fabsf(x.y) <= 65504.f);  // NaN too
     reinterpret_cast<uint32_t*>(dst)[e] = f16x2_sat(x.x, x.y);
   }
+  if (out && range) atomicExch(range, 1);  // clamped: reported by the session (KView::f16_range)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 big_encode_fn() {
@@ -1443,7 +1447,7 @@ cudaError_t run_core16(const KView& v, const int32_t* dims, int64_t mul, int64_t
     const int64_t n2 = (int64_t)dims[n] * W / 2;
     int64_t blocks = (n2 + 255) / 256;
     if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2);
+    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2, v.f16_range);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!big_row_map16(&p.tmap[n], a16, dims[n])) return cudaErrorNotSupported;
@@ -1482,7 +1486,7 @@ cudaError_t run_core16p(const KView& v, const int32_t* dims, int64_t mul, int64_
     const int64_t n2 = (int64_t)dims[n] * W / 2;
     int64_t blocks = (n2 + 255) / 256;
     if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2);
+    big_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, n2, v.f16_range);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!big_row_map16(&p.tmap[n], a16, dims[n], W)) return cudaErrorNotSupported;

@@ -1419,13 +1419,17 @@ enum : int {
 
 
 
-__global__ void ws_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+__global__ void ws_half_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n,
+                               int* __restrict__ range) {
   const int64_t n2 = n / 2;  // n = rows x 32: even
+  bool out = false;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
        e += (int64_t)gridDim.x * blockDim.x) {
     const float2 x = reinterpret_cast<const float2*>(src)[e];
+    out |= !(fabsf(x.x) <= 65504.f) || !(fabsf(x.y) <= 65504.f);  // NaN too
     reinterpret_cast<uint32_t*>(dst)[e] = f16x2_sat(x.x, x.y);
   }
+  if (out && range) atomicExch(range, 1);
 }
 
 // kEG epilogue groups of 8 warps: group g takes the tiles k = g (mod kEG), so
@@ -1890,7 +1894,7 @@ cudaError_t launch_ws_core(const KView& v, const int32_t* dims, int64_t mul, int
       const int64_t cnt = (int64_t)dims[n] * kW;
       int64_t blocks = (cnt + 255) / 256;
       if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-      ws_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, cnt);
+      ws_half_kernel<<<(int)blocks, 256, 0, st>>>(v.a[n], a16, cnt, v.f16_range);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (!make_row_map16(&p.tmap[n], a16, dims[n])) return cudaErrorNotSupported;
