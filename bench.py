@@ -834,10 +834,20 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
         if kind == "uniform":
             variants.append(("parity (window 3, 74 CTAs)", {"window": 3, "max_ctas": 74}))
             variants.append(("last-mode runs", {"runs": 1}))
+            # the reference's sampler redraws every nonzero's position each
+            # epoch (sparse_tensor.cpp:271-282); the engine shuffles once per
+            # upload and permutes whole tiles per epoch.  This variant rebuilds
+            # the stream with a fresh seed before every epoch (the rebuild is
+            # not in its epoch_ms, which times the sweep kernels)
+            variants.append(("reshuffled every epoch", {"reshuffle": 1}))
         res = {}
         for name, opts in variants:
-            prev = {k: s.get_option(k) for k in opts}
-            for k, v in opts.items():
+            reshuffle = bool(opts.get("reshuffle"))
+            opts_set = {k: v for k, v in opts.items() if k != "reshuffle"}
+            if reshuffle:
+                opts_set["shuffle_seed"] = s.get_option("shuffle_seed")
+            prev = {k: s.get_option(k) for k in opts_set}
+            for k, v in opts_set.items():
                 s.set_option(k, v)
             s.upload_model(tr.dims, [j] * order, j, a, b)
             ev = s.eval(5, 1, 0.0, 0.0)
@@ -845,6 +855,8 @@ def rmse_vs_reference(args, cfg, j, coo, test, s, eng, host):
             ep_ms = []
             for e in range(len(ref["rmse"])):
                 es = host.derive_seed(1, [e + 1])
+                if reshuffle:
+                    s.set_option("shuffle_seed", int(host.derive_seed(es, [3]) & 0x7fffffffffffffff))
                 f_ms = s.factor_phase(4, None, 16, ref["lr_a"], ref["reg_a"], eng.MODE_HOGWILD,
                                       seed=host.derive_seed(es, [1]), timed=True)
                 c_ms = s.core_phase(4, None, 16, ref["lr_b"], ref["reg_b"], eng.MODE_HOGWILD,
